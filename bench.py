@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""SI-MLSDC sweep-path benchmark (BASELINE.json metric).
+
+Workload: BASELINE configs[1] (1-D viscous Burgers, 512 elements, P 8/4,
+M 5/3, nu=5e-3, CFL 1) -- the config the metric is quoted on that fits one
+GPU.  A "step" is one SI-MLSDC time slab (FMG start, 5 V-cycles, closing fine
+sweep: 6 fine sweeps + 12 coarse passes), replayed from a CUDA graph with the
+state resident in HBM.  value = DOF-sweep updates/s summed over ranks.
+
+  python bench.py [--gpus N --steps K --warmup W]      # our CUDA path
+  python bench.py --impl reference                       # reference algorithm on CPU
+
+Multi-GPU (torchrun): each rank advances an independent seeded replica of the
+workload (weak scaling); the 1-D configs are latency bound, so they are not
+element-partitioned ("Multi-GPU").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "fp64 DOF-sweep updates/sec per SI-MLSDC step"
+UNIT = "DOF-sweep updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2"])
+    ap.add_argument("--cpu-sample-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cluster-ctas", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.gpu)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_hbm_peak():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------- CPU (oracle)
+def cpu_port_rate(w, n_steps, threads_limit=1):
+    """Time the oracle's restatement of the reference algorithm (SuperLU +
+    defect iteration, dgsem.py:503-533) on the host: the reference port."""
+    from threadpoolctl import threadpool_limits
+    from oracle import sweeper as osw, workloads
+    from paper_2504_18526_b200.dgsem import Mesh1D, compute_delta
+    u0 = w.initial_state(Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes)
+    dt, _ = w.time_step(u0, compute_delta(w.p_fine))
+    with threadpool_limits(limits=threads_limit):
+        h, _ = workloads.build_hierarchy(w, solver="lu")
+        u = u0
+        osw.run_mlsdc(h, u, 0.0, dt, w.n_cycles, "fmg")   # warm caches (LU factorisation)
+        t0 = time.perf_counter()
+        for s in range(n_steps):
+            u = osw.run_mlsdc(h, u, s * dt, dt, w.n_cycles, "fmg").u[-1].copy()
+        el = time.perf_counter() - t0
+    U = w.dof_sweeps_per_step()[0]
+    return U * n_steps / el, el / n_steps
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2504_18526_b200.configs import WORKLOADS
+    w = WORKLOADS[args.workload]
+    cores = os.cpu_count() or 1
+    from threadpoolctl import threadpool_limits
+    from oracle import sweeper as osw, workloads
+    from paper_2504_18526_b200.dgsem import Mesh1D, compute_delta
+    u0 = w.initial_state(Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes)
+    dt, _ = w.time_step(u0, compute_delta(w.p_fine))
+    with threadpool_limits(limits=cores):
+        h, _ = workloads.build_hierarchy(w, solver="lu")
+        u = u0
+        for s in range(args.warmup):
+            u = osw.run_mlsdc(h, u, s * dt, dt, w.n_cycles, "fmg").u[-1].copy()
+        t0 = time.perf_counter()
+        for s in range(args.steps):
+            u = osw.run_mlsdc(h, u, (args.warmup + s) * dt, dt, w.n_cycles, "fmg").u[-1].copy()
+        el = time.perf_counter() - t0
+    U = w.dof_sweeps_per_step()[0]
+    val = U * args.steps / el
+    out = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name + " (BASELINE configs[1])", "dof_sweeps_per_step": U,
+                   "fine_sweeps_per_step": w.n_cycles + 1, "schedule": "fmg + 5 V-cycles + closing sweep"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} SI-MLSDC steps of {w.name} after {args.warmup} warm-up steps; "
+                                   "oracle restatement of the reference (SuperLU + defect iteration), "
+                                   "Python/numpy/scipy (the reference itself is not on the GPU box)"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- our path
+def cg_roofline(hier, rt, torch, dt, reps=64):
+    """Average duration of the dominant kernel (the cluster PCG) measured live
+    with CUDA events on its stream, over a CUDA graph of ``reps`` fine-level
+    solves on a state from the run; algorithmic bytes per SURVEY 8(d)."""
+    from paper_2504_18526_b200.dgsem import SICoefficient
+    fine = hier.fine
+    op = fine.ctx
+    u_prev = fine.sol.u[1].clone()
+    rhs = fine.sol.u[2].clone()
+    dtm = dt * float(fine.rule.tau[2] - fine.rule.tau[1])   # a real fine substep
+    coef = SICoefficient(u_prev, dtm)
+    x = rt.empty(op.ndof)
+    op.eager_checks = False
+    n0 = rt.status()[2]
+    stream = torch.cuda.Stream(device=rt.device)
+    stream.wait_stream(torch.cuda.current_stream(rt.device))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(reps):
+            op.implicit_solve(coef, dtm, rhs, out=x)
+    rt.bind_stream()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3 / reps
+    its, _ = rt.cg_log()
+    k = float(np.mean(its[n0:n0 + reps])) if len(its) > n0 else float("nan")
+    N, V = op.ndof, 1.0
+    bytes_per = 8.0 * N * ((3 + V) + k * (10 + V))
+    op.eager_checks = True
+    return t, k, bytes_per
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2504_18526_b200 import dgsem, mlsdc, problems
+    from paper_2504_18526_b200.configs import WORKLOADS
+    from paper_2504_18526_b200.runtime import get_runtime
+    w = WORKLOADS[args.workload]
+    rt = get_runtime(local)
+    rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=args.cluster_ctas)
+
+    def make_op(P):
+        prob = problems.Burgers(w.params["nu"]) if w.problem == "burgers" else \
+            problems.ConvectionDiffusion(w.params["speed"], w.params["nu"])
+        return dgsem.DGOperator(dgsem.Mesh1D(w.x_left, w.x_right, w.n_elem, P), prob, device=local)
+
+    hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+    nodes = dgsem.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes
+    u0 = w.initial_state(nodes)
+    if rank > 0:   # independent replica per rank
+        rng = np.random.default_rng(1000 + rank)
+        u0 = u0 + 1e-3 * np.sin(np.arange(u0.size) * 0.01 + rng.random())
+    dt, n_total = w.time_step(u0, dgsem.compute_delta(w.p_fine))
+    g = mlsdc.SlabGraph(hier, u0, 0.0, dt, w.n_cycles, "fmg")
+    U, U_fine = w.dof_sweeps_per_step()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=rt.device)   # > 126 MB L2
+    rt.reset_status()
+    for _ in range(args.warmup):
+        g.step()
+    torch.cuda.synchronize()
+    n_log0 = rt.status()[2]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for e0, e1 in evs:
+            flush.fill_(1.0)          # L2 flush between timed steps (outside the events)
+            e0.record()
+            g.step()
+            e1.record()
+        torch.cuda.synchronize()
+    t_steps = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
+    rt.raise_on_failure()
+    its, margins = rt.cg_log()
+    step_its = its[n_log0:]
+    solves_per_step = len(step_its) / max(1, args.steps) if len(step_its) else float("nan")
+    t_max = t_steps
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_steps], device=rt.device, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+        dist.barrier()
+    value = U * args.steps * world / t_max
+    # e2e through the public slab API with pinned host buffers
+    h_in = torch.empty(hier.fine.ctx.ndof, dtype=torch.float64, pin_memory=True)
+    h_out = torch.empty_like(h_in)
+    h_in.copy_(torch.as_tensor(u0))
+    ke = max(5, min(args.steps, 50))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(ke):
+        g.u.copy_(h_in, non_blocking=True)
+        g.step()
+        h_out.copy_(g.u, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    t_e2e = e0.elapsed_time(e1) * 1e-3
+    e2e_val = U * ke * world / t_e2e
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=rt.device, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_val = U * ke * world / float(tt.item())
+    # dominant kernel roofline (measured live)
+    t_cg, k_cg, bytes_cg = cg_roofline(hier, rt, torch, dt)
+    peak, peak_kind = measured_hbm_peak()
+    achieved = bytes_cg / t_cg / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, tstep = cpu_port_rate(w, args.cpu_sample_steps, threads_limit=1)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_sample_steps} SI-MLSDC steps of {w.name} from the seeded IC, "
+                         f"{tstep * 1e3:.1f} ms/step: oracle restatement of the reference algorithm "
+                         "(SuperLU + defect iteration), numpy/scipy, 1 thread"}
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic seeded IC (SURVEY 8d); periodic Burgers, no dataset",
+            "config": {
+                "workload": w.name + " (BASELINE configs[1])",
+                "n_elem": w.n_elem, "degrees": [w.p_coarse, w.p_fine], "nodes": [w.m_coarse, w.m_fine],
+                "dt": dt, "steps_to_t_end": n_total,
+                "schedule": "SI(2) incremental, radau_right, fmg start, 5 V-cycles + closing fine sweep",
+                "fine_sweeps_per_step": w.n_cycles + 1, "coarse_passes_per_step": 2 + 2 * w.n_cycles,
+                "dof_sweeps_per_step": U, "fine_dof_sweeps_per_s": U_fine * args.steps * world / t_max,
+                "cg_solves_per_step": solves_per_step, "cg_mean_iterations": float(np.mean(step_its)) if len(step_its) else None,
+                "cg_rtol": 1e-14, "l2": "256 MiB buffer written between timed steps, outside the CUDA events",
+                "parallelism": "replicas" if world > 1 else "single GPU",
+                "timing": "CUDA events around each CUDA-graph slab replay, summed; max over ranks",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "k_cg1d (cluster-resident Jacobi-PCG, one launch per implicit solve)",
+                         "kernel_us": t_cg * 1e6, "kernel_mean_iterations": k_cg,
+                         "algorithmic_bytes_per_launch": bytes_cg,
+                         "note": "8N[(3+V)+k(10+V)] bytes per solve, V=1; the level fits in shared memory, "
+                                 "so the kernel is latency bound, not HBM bound"},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * hier.fine.ctx.ndof,
+                    "d2h_bytes_per_step": 8 * hier.fine.ctx.ndof},
+            "gpu_launches": int(g.kernels_per_step * args.steps),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,195 @@
+"""Generate golden vectors by running the REFERENCE itself in-process.
+
+Usage (in the build container, where /root/reference exists):
+    python oracle/make_golden.py
+Writes tests/golden/*.npz.  The reference package is imported read-only from
+/root/reference/pkg/src; nothing from it is copied into the repo -- only its
+numerical outputs on seeded inputs.  The CG-trajectory goldens run the
+reference's own sdc/mlsdc code with ``DGOperator.implicit_solve`` replaced by
+the pinned PCG of ``oracle/cg.py`` (the north star's CG formulation).
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from sisdc import collocation as rc, dgsem as rd, mlsdc as rm, problems as rp, sdc as rs, transfer as rt  # noqa: E402
+
+from oracle.cg import pcg  # noqa: E402
+from paper_2504_18526_b200.configs import CFG1, CFG2  # noqa: E402
+
+OUT = os.path.join(REPO, "tests", "golden")
+
+
+def ref_problem(w):
+    if w.problem == "convdiff":
+        return rp.ConvectionDiffusion(w.params["speed"], w.params["nu"])
+    return rp.Burgers(w.params["nu"])
+
+
+def build_ref_hier(w):
+    ops = [rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, w.n_elem, P), ref_problem(w))
+           for P in (w.p_coarse, w.p_fine)]
+    rules = [rc.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
+    wts = [rc.make_weights(r) for r in rules]
+    levels = [rm.Level(o, r, ww, "si2") for o, r, ww in zip(ops, rules, wts)]
+    pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_only")
+    spat = rt.build_spatial_p_transfer(w.p_coarse, w.p_fine, w.n_elem, 1, "embedded")
+    return rm.Hierarchy(levels, [rt.SpaceTimeTransfer(pair, spat)], n_coarse=2, n_sweep=1,
+                        form="incremental", post_sweep_on_finest=True), ops
+
+
+class PcgPatch:
+    """Swap DGOperator.implicit_solve for the pinned PCG; log iterations."""
+
+    def __init__(self, rtol=1e-14):
+        self.rtol = rtol
+        self.log = []
+        self._orig = rd.DGOperator.implicit_solve
+
+    def __enter__(self):
+        patch = self
+
+        def solve(op, coeff, a, rhs, t=0.0):
+            if a == 0.0:
+                return rhs
+            rhs = np.asarray(rhs)
+            m = op._mass_flat
+            b = m * rhs.reshape(-1)
+            if not b.any():
+                return np.zeros_like(rhs)
+            Amat = op.assemble_implicit(coeff, a)
+            diag = np.asarray(Amat.diagonal())
+            A = lambda x: m * x - a * m * op.apply_diffusion(coeff, x, t)
+            x, it, margin = pcg(A, diag, b, rhs.reshape(-1).copy(), patch.rtol, 1000)
+            assert it >= 0
+            patch.log.append((it, margin))
+            return x.reshape(rhs.shape)
+
+        rd.DGOperator.implicit_solve = solve
+        return self
+
+    def __exit__(self, *exc):
+        rd.DGOperator.implicit_solve = self._orig
+
+
+def gen_tables():
+    out = {}
+    for M in (1, 2, 3, 4, 5, 7):
+        r = rc.make_nodes("radau_right", M)
+        ww = rc.make_weights(r)
+        out[f"radau_tau_{M}"] = r.tau
+        out[f"radau_wnn_{M}"] = ww.w_nn
+        out[f"radau_w0n_{M}"] = ww.w_0n
+    for M in (2, 3, 5):
+        out[f"lobatto_tau_{M}"] = rc.make_nodes("lobatto", M).tau
+    for P in (3, 4, 7, 8):
+        x, wt = rc.gauss_lobatto(P + 1)
+        out[f"gll_x_{P}"], out[f"gll_w_{P}"] = x, wt
+        out[f"D_{P}"] = rd._diff_matrix(x)
+        out[f"delta_{P}"] = np.array(rd.compute_delta(P))
+    for pc, pf in ((4, 8), (3, 7)):
+        s = rt.build_spatial_p_transfer(pc, pf, 1)
+        out[f"psp_interp_{pc}_{pf}"] = s.blocks["interp"]
+        out[f"psp_project_{pc}_{pf}"] = s.blocks["project"]
+    for mc, mf in ((2, 4), (3, 5), (2, 5)):
+        pr_ = rt.build_temporal_transfer(rc.make_nodes("radau_right", mc), rc.make_nodes("radau_right", mf))
+        out[f"t_interp_{mc}_{mf}"], out[f"t_project_{mc}_{mf}"] = pr_.interp, pr_.project
+    np.savez_compressed(os.path.join(OUT, "tables.npz"), **out)
+
+
+def gen_operators():
+    """Operator outputs on seeded fields at the cfg-1/cfg-2 meshes and a
+    small 1-D CNS mesh (matrix coefficients)."""
+    rng = np.random.default_rng(1234)
+    out = {}
+    for tag, w, ne in (("cfg1", CFG1, CFG1.n_elem), ("cfg2", CFG2, 64)):
+        for P in (w.p_fine, w.p_coarse):
+            op = rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, ne, P), ref_problem(w))
+            k = f"{tag}_P{P}"
+            u = 1.0 + 0.3 * rng.standard_normal(op.ndof)
+            fld = 0.01 + 0.02 * rng.random((ne, P + 1))
+            out[k + "_u"] = u
+            out[k + "_fld"] = fld
+            out[k + "_conv"] = op.apply_convection(u)
+            out[k + "_diff_const"] = op.apply_diffusion(0.0137, u)
+            out[k + "_diff_field"] = op.apply_diffusion(fld, u)
+            out[k + "_rhs"] = op.eval_rhs(u, 0.0)
+            c = op.modified_diffusion_matrix(u, 0.0123, "si2")
+            out[k + "_modc"] = np.asarray(c)
+            out[k + "_diagA_field"] = op.assemble_implicit(fld, 0.0123).diagonal()
+            out[k + "_diagA_const"] = op.assemble_implicit(0.0137, 0.0123).diagonal()
+            rhs = u * 0.5 + 0.1 * np.sin(np.arange(op.ndof))
+            out[k + "_solve_rhs"] = rhs
+            out[k + "_solve_const"] = op.implicit_solve(0.0137, 0.0123, rhs)
+            op2 = rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, ne, P), ref_problem(w))
+            out[k + "_solve_field"] = op2.implicit_solve(fld, 0.0123, rhs)
+    cf = rp.CompressibleFlow(eta=1e-3)
+    op = rd.DGOperator(rd.Mesh1D(0.0, 1.0, 8, 5), cf)
+    u3 = np.stack([1.0 + 0.1 * rng.random((8, 6)), 0.3 * rng.random((8, 6)), 3.0 + 0.3 * rng.random((8, 6))])
+    u = u3.reshape(-1)
+    out["cns_u"] = u
+    out["cns_conv"] = op.apply_convection(u)
+    out["cns_rhs"] = op.eval_rhs(u, 0.0)
+    out["cns_coeff"] = cf.diffusion_coeff(u3)
+    out["cns_diff"] = op.apply_diffusion(cf.diffusion_coeff(u3), u)
+    out["cns_modc"] = op.modified_diffusion_matrix(u, 0.01, "si2")
+    np.savez_compressed(os.path.join(OUT, "operators.npz"), **out)
+
+
+def gen_trajectories():
+    """Reference MLSDC steps for cfg1/cfg2: LU (the reference as shipped) and
+    with the pinned PCG swapped in (iteration counts logged)."""
+    out = {}
+    for tag, w, nsteps in (("cfg1", CFG1, 3), ("cfg2", CFG2, 2)):
+        hier, ops = build_ref_hier(w)
+        fine = ops[1]
+        u0 = w.initial_state(fine.mesh.ref_nodes)
+        dt, n = w.time_step(u0, rd.compute_delta(w.p_fine))
+        out[f"{tag}_u0"] = u0
+        out[f"{tag}_dt"] = np.array(dt)
+        out[f"{tag}_nsteps_total"] = np.array(n)
+        # LU trajectory (reference unmodified)
+        u = u0
+        for s in range(nsteps):
+            sol = rm.run_mlsdc(hier, u, s * dt, dt, w.n_cycles, strategy="fmg")
+            if s == 0:
+                out[f"{tag}_lu_step1_nodes"] = sol.u.copy()
+            u = sol.end_value.copy()
+            out[f"{tag}_lu_u{s + 1}"] = u
+        # PCG trajectory (reference sweeps/cycles, pinned PCG solve)
+        for rtol, rk in ((1e-14, "pcg"), (1e-13, "pcg13")):
+            hier, ops = build_ref_hier(w)
+            with PcgPatch(rtol) as pp:
+                u = u0
+                for s in range(nsteps):
+                    n0 = len(pp.log)
+                    sol = rm.run_mlsdc(hier, u, s * dt, dt, w.n_cycles, strategy="fmg")
+                    u = sol.end_value.copy()
+                    out[f"{tag}_{rk}_u{s + 1}"] = u
+                    out[f"{tag}_{rk}_iters{s + 1}"] = np.array([it for it, _ in pp.log[n0:]])
+                    out[f"{tag}_{rk}_margin{s + 1}"] = np.array([mg for _, mg in pp.log[n0:]])
+        # single-level SDC: predictor + 2 sweeps on the fine level (LU)
+        opf = rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine), ref_problem(w))
+        rule = rc.make_nodes("radau_right", w.m_fine)
+        wts = rc.make_weights(rule)
+        sol = rs.run_sdc(opf, rule, wts, dt, "si2", u0, 0.0, 2)
+        out[f"{tag}_sdc2_u"], out[f"{tag}_sdc2_f"] = sol.u, sol.f
+        out[f"{tag}_sdc2_h1"], out[f"{tag}_sdc2_h2"] = sol.h1, sol.h2
+    np.savez_compressed(os.path.join(OUT, "trajectories.npz"), **out)
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    gen_tables()
+    gen_operators()
+    gen_trajectories()
+    for f in sorted(os.listdir(OUT)):
+        print(f, os.path.getsize(os.path.join(OUT, f)))

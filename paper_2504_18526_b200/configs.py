@@ -1,0 +1,94 @@
+"""BASELINE.json workloads: seeded synthetic initial data and pinned schedules.
+
+These are *inputs*, shared by the CUDA path, the tests and the CPU oracle.
+The generators and the open parameters BASELINE.json leaves (seeds, dt for
+config 2, the MLSDC schedule) are pinned here and recorded in DESIGN.md:
+
+* schedule: SI(2), incremental, Radau-right, FMG start (== cascade for two
+  levels), N_c = 2, N_s = 1, 5 V-cycles + closing fine sweep -- the
+  reference CLI defaults (``cli.py:273-295``).  6 fine sweeps per step.
+* cfg1: conv-diff, 64 el, P 8/4, M 4/2, a=1, nu=1e-2, CFL 1 on |a|.
+* cfg2: Burgers, 512 el, P 8/4, M 5/3, nu=5e-3, CFL 1 on max|u0|, run to
+  t = 1.5 with the reference's step rule n = ceil(t_end/dt0), dt = t_end/n
+  (``cli.py:825-836``).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+TWO_PI = 2.0 * math.pi
+
+
+@dataclass(frozen=True)
+class Workload1D:
+    name: str
+    problem: str          # "convdiff" | "burgers"
+    n_elem: int
+    p_fine: int
+    p_coarse: int
+    m_fine: int
+    m_coarse: int
+    params: dict
+    seed: int
+    cfl: float = 1.0
+    t_end: float = None
+    n_steps: int = None
+    n_cycles: int = 5
+    x_left: float = 0.0
+    x_right: float = TWO_PI
+
+    @property
+    def dx(self):
+        return (self.x_right - self.x_left) / self.n_elem
+
+    def nodes_x(self, degree, gll_nodes):
+        e = self.x_left + self.dx * np.arange(self.n_elem)
+        return e[:, None] + 0.5 * self.dx * (np.asarray(gll_nodes) + 1.0)[None, :]
+
+    def initial_state(self, gll_nodes):
+        """Seeded IC on the fine GLL nodes, flat (1, ne, P+1)."""
+        x = self.nodes_x(self.p_fine, gll_nodes)
+        rng = np.random.default_rng(self.seed)
+        if self.problem == "convdiff":
+            ks = np.sort(rng.choice(np.arange(2, 9), 4, replace=False))
+            amps = rng.normal(0.0, 0.1, 4)
+            u = np.sin(x) + sum(a * np.sin(k * x) for k, a in zip(ks, amps))
+        elif self.problem == "burgers":
+            amps = rng.normal(0.0, 0.01, 15)
+            u = 1.0 + 0.5 * np.sin(x) + sum(a * np.sin(k * x) for k, a in zip(range(2, 17), amps))
+        else:
+            raise ValueError(self.problem)
+        return np.ascontiguousarray(u.reshape(-1), dtype=np.float64)
+
+    def time_step(self, u0, delta_p):
+        """(dt, n_steps) -- ``cli.py:825-836`` semantics with CFL on the
+        convective wave speed; delta_p = compute_delta(p_fine)."""
+        lam = abs(self.params["speed"]) if self.problem == "convdiff" else float(np.max(np.abs(u0)))
+        dt0 = self.cfl * self.dx / (2.0 * delta_p * lam)
+        if self.n_steps is not None:
+            return dt0, self.n_steps
+        n = max(1, math.ceil(self.t_end / dt0 - 1e-12))
+        return self.t_end / n, n
+
+    def dof(self):
+        return self.n_elem * (self.p_fine + 1), self.n_elem * (self.p_coarse + 1)
+
+    def dof_sweeps_per_step(self):
+        """U = sum_l N_l M_l passes_l: 6 fine sweeps, 12 coarse
+        passes (1 predictor + 1 FMG sweep + 2 per cycle)."""
+        nf, nc = self.dof()
+        fine_passes = self.n_cycles + 1
+        coarse_passes = 2 + 2 * self.n_cycles
+        return nf * self.m_fine * fine_passes + nc * self.m_coarse * coarse_passes, \
+            nf * self.m_fine * fine_passes
+
+
+CFG1 = Workload1D("cfg1_convdiff_64el_P8", "convdiff", 64, 8, 4, 4, 2,
+                  {"speed": 1.0, "nu": 1e-2}, seed=1, n_steps=100)
+CFG2 = Workload1D("cfg2_burgers_512el_P8", "burgers", 512, 8, 4, 5, 3,
+                  {"nu": 5e-3}, seed=2, t_end=1.5)
+
+WORKLOADS = {"cfg1": CFG1, "cfg2": CFG2}

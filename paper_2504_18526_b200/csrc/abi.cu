@@ -1,0 +1,416 @@
+// C ABI of libsisdc_b200.so: contexts, operators, transfers and the exported
+// OperatorContext / sweep-stage entry points (include/sisdc_b200.h).
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+#include "sisdc_dev.cuh"
+#include "sisdc_host.h"
+
+using namespace sisdc;
+
+struct sisdc_ctx {
+  Ctx c;
+};
+
+struct sisdc_op1d {
+  sisdc_ctx* ctx;
+  sisdc_op1d_desc desc;
+  Op1DDev dev;
+  double* d_tab = nullptr;
+  std::vector<double> nodes, weights, D;
+};
+
+struct sisdc_xfer {
+  sisdc_ctx* ctx;
+  XferDev dev;
+  double* d_tab = nullptr;
+};
+
+namespace {
+
+// ---------------------------------------------- host element tables
+void legendre(int n, double x, double& p, double& dp) {
+  double p0 = 1.0, p1 = x, d0 = 0.0, d1 = 1.0;
+  if (n == 0) { p = 1.0; dp = 0.0; return; }
+  for (int k = 1; k < n; ++k) {
+    double p2 = ((2 * k + 1) * x * p1 - k * p0) / (k + 1);
+    double d2 = d0 + (2 * k + 1) * p1;
+    p0 = p1; p1 = p2; d0 = d1; d1 = d2;
+  }
+  p = p1; dp = d1;
+}
+
+// GLL nodes (roots of (1-x^2) P'_P) by Newton from Chebyshev-Lobatto guesses,
+// weights 2/(P(P+1) P_P(x)^2)  (collocation.py:163-167)
+void gll(int p1, std::vector<double>& x, std::vector<double>& w) {
+  const int P = p1 - 1;
+  x.assign(p1, 0.0); w.assign(p1, 0.0);
+  x[0] = -1.0; x[P] = 1.0;
+  for (int j = 1; j < P; ++j) {
+    double z = -std::cos(M_PI * j / P);
+    for (int it = 0; it < 100; ++it) {
+      double p, dp;
+      legendre(P, z, p, dp);
+      double d2 = (2.0 * z * dp - P * (P + 1) * p) / (1.0 - z * z);
+      double step = dp / d2;
+      z -= step;
+      if (std::fabs(step) < 1e-16) break;
+    }
+    x[j] = z;
+  }
+  for (int j = 0; j < p1; ++j) {
+    double p, dp;
+    legendre(P, x[j], p, dp);
+    w[j] = 2.0 / (P * (P + 1) * p * p);
+  }
+}
+
+// barycentric D (dgsem.py:33-43)
+std::vector<double> diff_matrix(const std::vector<double>& x) {
+  int n = (int)x.size();
+  std::vector<double> lam(n), D(n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double pr = 1.0;
+    for (int k = 0; k < n; ++k) if (k != j) pr *= (x[j] - x[k]);
+    lam[j] = 1.0 / pr;
+  }
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) {
+      if (i == j) continue;
+      D[i * n + j] = (lam[j] / lam[i]) / (x[i] - x[j]);
+      s += D[i * n + j];
+    }
+    D[i * n + i] = -s;
+  }
+  return D;
+}
+
+bool invert(std::vector<double> A, int n, std::vector<double>& inv) {
+  inv.assign(n * n, 0.0);
+  for (int i = 0; i < n; ++i) inv[i * n + i] = 1.0;
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r) if (std::fabs(A[r * n + c]) > std::fabs(A[piv * n + c])) piv = r;
+    if (A[piv * n + c] == 0.0) return false;
+    for (int k = 0; k < n; ++k) { std::swap(A[c * n + k], A[piv * n + k]); std::swap(inv[c * n + k], inv[piv * n + k]); }
+    double d = A[c * n + c];
+    for (int k = 0; k < n; ++k) { A[c * n + k] /= d; inv[c * n + k] /= d; }
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      double f = A[r * n + c];
+      if (f == 0.0) continue;
+      for (int k = 0; k < n; ++k) { A[r * n + k] -= f * A[c * n + k]; inv[r * n + k] -= f * inv[c * n + k]; }
+    }
+  }
+  return true;
+}
+
+inline Ctx* C(sisdc_op1d* op) { return &op->ctx->c; }
+inline CoefDev coef(sisdc_coef k) { return CoefDev{k.kind, k.value, k.ptr}; }
+
+int check_coef(Ctx* c, sisdc_coef k) {
+  if (k.kind < SISDC_COEF_NONE || k.kind > SISDC_COEF_PHYS) return c->fail(SISDC_ERR_ARG, "unknown coefficient kind");
+  if ((k.kind == SISDC_COEF_FIELD || k.kind == SISDC_COEF_SI) && !k.ptr)
+    return c->fail(SISDC_ERR_ARG, "coefficient needs a device pointer");
+  return SISDC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sisdc_abi_version(void) { return SISDC_ABI_VERSION; }
+
+int sisdc_ctx_create(int device, sisdc_ctx** out) {
+  if (!out) return SISDC_ERR_ARG;
+  *out = nullptr;
+  sisdc_ctx* x = new (std::nothrow) sisdc_ctx();
+  if (!x) return SISDC_ERR_ARG;
+  Ctx& c = x->c;
+  c.device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(&c.d_status, 4 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&c.d_log_it, c.log_cap * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&c.d_log_margin, c.log_cap * sizeof(double));
+  if (e != cudaSuccess) {
+    delete x;
+    return SISDC_ERR_CUDA;
+  }
+  int init[4] = {INT_MAX, 0, 0, 0};
+  cudaMemcpy(c.d_status, init, sizeof(init), cudaMemcpyHostToDevice);
+  *out = x;
+  return SISDC_OK;
+}
+
+void sisdc_ctx_destroy(sisdc_ctx* x) {
+  if (!x) return;
+  cudaFree(x->c.d_status);
+  cudaFree(x->c.d_log_it);
+  cudaFree(x->c.d_log_margin);
+  delete x;
+}
+
+const char* sisdc_ctx_last_error(const sisdc_ctx* x) { return x ? x->c.err.c_str() : "null context"; }
+
+int sisdc_ctx_set_stream(sisdc_ctx* x, void* stream) {
+  if (!x) return SISDC_ERR_ARG;
+  x->c.stream = (cudaStream_t)stream;
+  return SISDC_OK;
+}
+
+int sisdc_ctx_synchronize(sisdc_ctx* x) {
+  if (!x) return SISDC_ERR_ARG;
+  return x->c.cuda(cudaStreamSynchronize(x->c.stream), "synchronize");
+}
+
+int sisdc_ctx_set_cg(sisdc_ctx* x, double rtol, int maxit, int cluster_ctas) {
+  if (!x || !(rtol > 0.0) || maxit < 1 || cluster_ctas < 0 || cluster_ctas > 16) return SISDC_ERR_ARG;
+  x->c.rtol = rtol;
+  x->c.maxit = maxit;
+  x->c.cluster_ctas = cluster_ctas;
+  return SISDC_OK;
+}
+
+int sisdc_ctx_status(sisdc_ctx* x, int* nonfinite_elem, int* cg_failures, int* n_solves) {
+  if (!x) return SISDC_ERR_ARG;
+  int h[4];
+  int rc = x->c.cuda(cudaStreamSynchronize(x->c.stream), "status sync");
+  if (rc) return rc;
+  rc = x->c.cuda(cudaMemcpy(h, x->c.d_status, sizeof(h), cudaMemcpyDeviceToHost), "status read");
+  if (rc) return rc;
+  if (nonfinite_elem) *nonfinite_elem = h[0] == INT_MAX ? -1 : h[0];
+  if (cg_failures) *cg_failures = h[1];
+  if (n_solves) *n_solves = h[2];
+  return SISDC_OK;
+}
+
+int sisdc_ctx_reset_status(sisdc_ctx* x) {
+  if (!x) return SISDC_ERR_ARG;
+  k_reset_status<<<1, 32, 0, x->c.stream>>>(x->c.d_status);   // kernel, so it is graph-capturable
+  return x->c.after_launch("reset_status");
+}
+
+int sisdc_ctx_cg_log(sisdc_ctx* x, int cap, int* iters, double* margins, int* n_out) {
+  if (!x || cap < 0) return SISDC_ERR_ARG;
+  int n = 0;
+  int rc = sisdc_ctx_status(x, nullptr, nullptr, &n);
+  if (rc) return rc;
+  if (n > x->c.log_cap) n = x->c.log_cap;
+  int m = n < cap ? n : cap;
+  if (m > 0 && iters) rc = x->c.cuda(cudaMemcpy(iters, x->c.d_log_it, m * sizeof(int), cudaMemcpyDeviceToHost), "log");
+  if (!rc && m > 0 && margins)
+    rc = x->c.cuda(cudaMemcpy(margins, x->c.d_log_margin, m * sizeof(double), cudaMemcpyDeviceToHost), "log");
+  if (n_out) *n_out = n;
+  return rc;
+}
+
+int64_t sisdc_ctx_launch_count(const sisdc_ctx* x) { return x ? x->c.launches : -1; }
+
+int sisdc_copy(sisdc_ctx* x, double* dst, const double* src, int64_t n) {
+  if (!x || n < 0 || (n > 0 && (!dst || !src))) return SISDC_ERR_ARG;
+  if (n == 0) return SISDC_OK;
+  return x->c.cuda(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, x->c.stream), "copy");
+}
+
+// ------------------------------------------------------------ operators
+int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) {
+  if (!x || !d || !out) return SISDC_ERR_ARG;
+  *out = nullptr;
+  Ctx& c = x->c;
+  if (!(d->x_right > d->x_left)) return c.fail(SISDC_ERR_ARG, "empty domain");
+  if (d->n_elem < 1 || d->degree < 1) return c.fail(SISDC_ERR_ARG, "need at least one element and degree >= 1");
+  if (d->degree + 1 > MAXP1) return c.fail(SISDC_ERR_UNSUPPORTED, "degree above 15");
+  if (d->ncomp != 1) return c.fail(SISDC_ERR_UNSUPPORTED, "only scalar problems (ncomp == 1) are built");
+  if (d->bc != SISDC_PERIODIC) return c.fail(SISDC_ERR_UNSUPPORTED, "only periodic meshes are built");
+  if (d->problem != SISDC_CONVDIFF && d->problem != SISDC_BURGERS) return c.fail(SISDC_ERR_ARG, "unknown problem");
+  if (d->nu < 0) return c.fail(SISDC_ERR_ARG, "diffusion coefficient must be nonnegative");
+  sisdc_op1d* op = new (std::nothrow) sisdc_op1d();
+  if (!op) return SISDC_ERR_ARG;
+  op->ctx = x;
+  op->desc = *d;
+  const int p1 = d->degree + 1;
+  gll(p1, op->nodes, op->weights);
+  op->D = diff_matrix(op->nodes);
+  const double dx = (d->x_right - d->x_left) / d->n_elem;
+  std::vector<double> tab(TabOff::size(p1), 0.0);
+  for (int i = 0; i < p1; ++i)
+    for (int k = 0; k < p1; ++k) {
+      tab[TabOff::D(p1) + i * p1 + k] = op->D[i * p1 + k];
+      tab[TabOff::DTW(p1) + i * p1 + k] = op->D[k * p1 + i] * op->weights[k];
+      tab[TabOff::D2W(p1) + i * p1 + k] = op->D[k * p1 + i] * op->D[k * p1 + i] * op->weights[k];
+    }
+  for (int i = 0; i < p1; ++i) {
+    double m = 0.5 * dx * op->weights[i];
+    tab[TabOff::w(p1) + i] = op->weights[i];
+    tab[TabOff::m(p1) + i] = m;
+    tab[TabOff::minv(p1) + i] = 1.0 / m;
+  }
+  std::vector<double> V(p1 * p1), Vi;
+  for (int i = 0; i < p1; ++i)
+    for (int k = 0; k < p1; ++k) { double p, dp; legendre(k, op->nodes[i], p, dp); V[i * p1 + k] = p; }
+  invert(V, p1, Vi);
+  for (int i = 0; i < p1 * p1; ++i) tab[TabOff::Vinv(p1) + i] = Vi[i];
+  cudaError_t e = cudaMalloc(&op->d_tab, tab.size() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(op->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    int rc = c.cuda(e, "op1d tables");
+    delete op;
+    return rc;
+  }
+  Op1DDev& v = op->dev;
+  v.ne = d->n_elem; v.p1 = p1; v.n = d->n_elem * p1; v.problem = d->problem;
+  v.dx = dx; v.s = 2.0 / dx; v.mu0 = d->penalty * p1 * p1 / dx;   // dgsem.py:137
+  v.speed = d->speed; v.nu = d->nu; v.tab = op->d_tab; v.nu_art = nullptr;
+  *out = op;
+  return SISDC_OK;
+}
+
+void sisdc_op1d_destroy(sisdc_op1d* op) {
+  if (!op) return;
+  cudaFree(op->d_tab);
+  delete op;
+}
+
+int sisdc_op1d_tables(const sisdc_op1d* op, double* nodes, double* weights, double* D) {
+  if (!op) return SISDC_ERR_ARG;
+  int p1 = op->dev.p1;
+  if (nodes) std::memcpy(nodes, op->nodes.data(), p1 * sizeof(double));
+  if (weights) std::memcpy(weights, op->weights.data(), p1 * sizeof(double));
+  if (D) std::memcpy(D, op->D.data(), p1 * p1 * sizeof(double));
+  return SISDC_OK;
+}
+
+int sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art) {
+  if (!op) return SISDC_ERR_ARG;
+  op->dev.nu_art = nu_art;
+  return SISDC_OK;
+}
+
+int sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, double c_s, double* nu_art) {
+  if (!op || !u || !nu_art || !(kappa_s > 0)) return SISDC_ERR_ARG;
+  return launch_persson(C(op), op->dev, u, kappa_s, c_s, nu_art);
+}
+
+int sisdc_apply_convection(sisdc_op1d* op, const double* u, double, double* out) {
+  if (!op || !u || !out) return SISDC_ERR_ARG;
+  return launch_apply_convection(C(op), op->dev, u, out);
+}
+
+int sisdc_apply_diffusion(sisdc_op1d* op, sisdc_coef k, const double* u, double, double* out) {
+  if (!op || !u || !out) return SISDC_ERR_ARG;
+  if (int rc = check_coef(C(op), k)) return rc;
+  if (k.kind == SISDC_COEF_NONE || (k.kind == SISDC_COEF_CONST && k.value == 0.0))
+    return C(op)->cuda(cudaMemsetAsync(out, 0, op->dev.n * sizeof(double), C(op)->stream), "zero");
+  return launch_apply_diffusion(C(op), op->dev, coef(k), u, out);
+}
+
+int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double, double* out) {
+  if (!op || !u || !out) return SISDC_ERR_ARG;
+  return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
+}
+
+int sisdc_coef_field(sisdc_op1d* op, sisdc_coef k, double* out) {
+  if (!op || !out) return SISDC_ERR_ARG;
+  if (int rc = check_coef(C(op), k)) return rc;
+  return launch_coef_field(C(op), op->dev, coef(k), out);
+}
+
+int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* rhs, double, double* x) {
+  if (!op || !rhs || !x) return SISDC_ERR_ARG;
+  if (int rc = check_coef(C(op), k)) return rc;
+  if (a == 0.0) {   // dgsem.py:505-506
+    if (x == rhs) return SISDC_OK;
+    return sisdc_copy(op->ctx, x, rhs, op->dev.n);
+  }
+  if (k.kind == SISDC_COEF_NONE) return C(op)->fail(SISDC_ERR_ARG, "cannot assemble a zero coefficient");
+  return launch_cg1d(C(op), op->dev, coef(k), a, rhs, x);
+}
+
+int sisdc_stage_rhs(sisdc_op1d* op, const double* base, const double* conv_in, double dt_m, const double* f_old,
+                    int M, const double* w_row, double dt, const double* g_m, const double* h_old, double,
+                    double* rhs, double* conv_out) {
+  if (!op || !base || !conv_in || !rhs || M < 0 || M > MAXM || (f_old && !w_row)) return SISDC_ERR_ARG;
+  return launch_stage_rhs(C(op), op->dev, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
+}
+
+int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_count, const double* u0,
+                      const double* u, const double* conv_prev, const double* dts, double, const double*,
+                      double* f, double* h1, double* h2) {
+  if (!op || !u0 || !u || !dts || !f || !h1) return SISDC_ERR_ARG;
+  if (scheme < SISDC_EULER || scheme > SISDC_SI2) return C(op)->fail(SISDC_ERR_ARG, "unknown scheme");
+  if (conv_prev && m_count != 1) return C(op)->fail(SISDC_ERR_ARG, "conv_prev needs m_count == 1");
+  return launch_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
+}
+
+int sisdc_eval_rhs_nodes(sisdc_op1d* op, int M, const double* u, const double*, double* f) {
+  if (!op || !u || !f || M < 1 || M > MAXM) return SISDC_ERR_ARG;
+  return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
+}
+
+int sisdc_collocation_defect(sisdc_op1d* op, int M, const double* W, double dt, int incremental, const double* u0,
+                             const double* u, const double* f, double sign, const double* add, double* out) {
+  if (!op || !W || !u0 || !u || !f || !out || M < 1 || M > MAXM) return SISDC_ERR_ARG;
+  return launch_defect(C(op), op->dev.n, M, W, dt, incremental, u0, u, f, sign, add, out);
+}
+
+// ------------------------------------------------------------ transfers
+int sisdc_xfer_create(sisdc_ctx* x, int n_elem, int pc1, int pf1, int Mc, int Mf,
+                      const double* It, const double* Pt, const double* Isp, const double* Psp, sisdc_xfer** out) {
+  if (!x || !It || !Pt || !Isp || !Psp || !out) return SISDC_ERR_ARG;
+  *out = nullptr;
+  if (n_elem < 1 || pc1 < 1 || pf1 < pc1 || pf1 > MAXP1) return x->c.fail(SISDC_ERR_ARG, "bad element sizes");
+  if (Mc < 1 || Mf < Mc || Mf > MAXM) return x->c.fail(SISDC_ERR_ARG, "bad node counts");
+  sisdc_xfer* t = new (std::nothrow) sisdc_xfer();
+  if (!t) return SISDC_ERR_ARG;
+  t->ctx = x;
+  XferDev& d = t->dev;
+  d.ne = n_elem; d.pc = pc1; d.pf = pf1; d.Mc = Mc; d.Mf = Mf;
+  std::vector<double> tab(xo_size(d));
+  std::memcpy(tab.data() + xo_It(d), It, Mf * Mc * sizeof(double));
+  std::memcpy(tab.data() + xo_Pt(d), Pt, Mf * Mc * sizeof(double));
+  std::memcpy(tab.data() + xo_Isp(d), Isp, d.pf * d.pc * sizeof(double));
+  std::memcpy(tab.data() + xo_Psp(d), Psp, d.pf * d.pc * sizeof(double));
+  cudaError_t e = cudaMalloc(&t->d_tab, tab.size() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(t->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    int rc = x->c.cuda(e, "xfer tables");
+    delete t;
+    return rc;
+  }
+  d.tab = t->d_tab;
+  *out = t;
+  return SISDC_OK;
+}
+
+void sisdc_xfer_destroy(sisdc_xfer* t) {
+  if (!t) return;
+  cudaFree(t->d_tab);
+  delete t;
+}
+
+int sisdc_xfer_spatial(sisdc_xfer* t, int dir, const double* in, double* out) {
+  if (!t || !in || !out || dir < 0 || dir > 2) return SISDC_ERR_ARG;
+  return launch_xfer_spatial(&t->ctx->c, t->dev, dir, in, out);
+}
+
+int sisdc_xfer_down(sisdc_xfer* t, int spatial_dir, int temporal_dir, const double* in, double* out) {
+  if (!t || !in || !out || spatial_dir < 1 || spatial_dir > 2 || temporal_dir < 1 || temporal_dir > 2)
+    return SISDC_ERR_ARG;
+  return launch_xfer_down(&t->ctx->c, t->dev, spatial_dir, temporal_dir, in, out);
+}
+
+int sisdc_xfer_fas_restrict(sisdc_xfer* t, const double* Wf, double dt, int incremental, const double* u0f,
+                            const double* uf, const double* ff, const double* gf, double* v, double* rr) {
+  if (!t || !Wf || !u0f || !uf || !ff || !v || !rr) return SISDC_ERR_ARG;
+  return launch_fas_restrict(&t->ctx->c, t->dev, Wf, dt, incremental, u0f, uf, ff, gf, v, rr);
+}
+
+int sisdc_xfer_interp(sisdc_xfer* t, int accumulate, const double* uc, const double* vc, double* uf) {
+  if (!t || !uc || !uf) return SISDC_ERR_ARG;
+  return launch_xfer_interp(&t->ctx->c, t->dev, accumulate, uc, vc, uf);
+}
+
+}  // extern "C"

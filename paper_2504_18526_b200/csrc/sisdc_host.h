@@ -1,0 +1,66 @@
+// Host-side internals shared by the ABI and the kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include "../../include/sisdc_b200.h"
+
+namespace sisdc {
+
+struct Op1DDev;
+struct CoefDev;
+struct XferDev;
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int* d_status = nullptr;        // [0] first non-finite element (INT_MAX: none), [1] CG failures, [2] log count
+  int* d_log_it = nullptr;        // per-solve CG iterations
+  double* d_log_margin = nullptr; // per-solve ||r||/(rtol ||b||)
+  int log_cap = 1 << 16;
+  double rtol = 1e-14;
+  int maxit = 1000;
+  int cluster_ctas = 0;
+  int64_t launches = 0;
+  std::string err;
+
+  int fail(int code, const std::string& msg) {
+    err = msg;
+    return code;
+  }
+  int cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return SISDC_OK;
+    err = std::string(what) + ": " + cudaGetErrorString(e);
+    return SISDC_ERR_CUDA;
+  }
+  int after_launch(const char* name) {
+    ++launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      err = std::string("launch ") + name + ": " + cudaGetErrorString(e);
+      return SISDC_ERR_CUDA;
+    }
+    return SISDC_OK;
+  }
+};
+
+int launch_apply_convection(Ctx* c, const Op1DDev& op, const double* u, double* out);
+int launch_apply_diffusion(Ctx* c, const Op1DDev& op, CoefDev k, const double* u, double* out);
+int launch_coef_field(Ctx* c, const Op1DDev& op, CoefDev k, double* out);
+int launch_node_eval(Ctx* c, const Op1DDev& op, int mode, int scheme, int M, int m_first, int m_count,
+                     const double* u0, const double* u, const double* conv_prev, const double* dts,
+                     double* f, double* h1, double* h2);
+int launch_stage_rhs(Ctx* c, const Op1DDev& op, const double* base, const double* conv_in, double dt_m,
+                     const double* f_old, int M, const double* w_row, double dt, const double* g,
+                     const double* h, double* rhs, double* conv_out);
+int launch_defect(Ctx* c, int N, int M, const double* W, double dt, int incremental, const double* u0,
+                  const double* u, const double* f, double sign, const double* add, double* out);
+int launch_xfer_spatial(Ctx* c, const XferDev& x, int dir, const double* in, double* out);
+int launch_fas_restrict(Ctx* c, const XferDev& x, const double* Wf, double dt, int incremental, const double* u0f,
+                        const double* uf, const double* ff, const double* gf, double* v, double* rr);
+int launch_xfer_down(Ctx* c, const XferDev& x, int sdir, int tdir, const double* in, double* out);
+int launch_xfer_interp(Ctx* c, const XferDev& x, int accumulate, const double* uc, const double* vc, double* uf);
+int launch_persson(Ctx* c, const Op1DDev& op, const double* u, double kappa, double cs, double* nu_art);
+int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x);
+
+}  // namespace sisdc

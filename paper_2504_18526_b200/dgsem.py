@@ -1,0 +1,314 @@
+"""GPU nodal DG-SEM operator: the reference's ``DGOperator`` on sm_100a.
+
+Mirrors ``dgsem.py`` of the reference (``Mesh1D`` ``:72-106``, ``DGOperator``
+``:117-571``, ``compute_delta``/``dt_from_cfl`` ``:46-69``) with the
+``OperatorContext`` methods executed by ``libsisdc_b200.so``:
+
+* ``apply_convection``  -> weak volume term + Rusanov faces   (``:205-225``)
+* ``apply_diffusion``   -> matrix-free SIP                     (``:251-309``)
+* ``eval_rhs``          -> convection + physical diffusion     (``:337-352``)
+* ``implicit_solve``    -> cluster-resident Jacobi-PCG         (replaces ``:503-533``)
+* ``persson_viscosity`` -> modal sensor                        (``:537-559``)
+
+States are torch float64 CUDA tensors (numpy inputs are uploaded); results
+are returned as new CUDA tensors unless ``out=`` is given.  Scope of the
+built path: periodic meshes, scalar problems (ConvectionDiffusion, Burgers).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from functools import cached_property, lru_cache
+from typing import Any, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import Coef, SolverError
+from .collocation import gauss_lobatto
+from .runtime import get_runtime
+
+__all__ = ["Mesh1D", "DGOperator", "SolverError", "ArtificialViscosityParams", "SICoefficient",
+           "compute_delta", "cfl_number", "dt_from_cfl", "max_wave_speed"]
+
+
+def _diff_matrix(x) -> np.ndarray:
+    x = np.asarray(x, dtype=float)
+    n = len(x)
+    lam = np.array([1.0 / np.prod([x[j] - x[k] for k in range(n) if k != j]) for j in range(n)])
+    D = np.zeros((n, n))
+    for i in range(n):
+        for j in range(n):
+            if i != j:
+                D[i, j] = (lam[j] / lam[i]) / (x[i] - x[j])
+        D[i, i] = -D[i].sum()
+    return D
+
+
+@lru_cache(maxsize=None)
+def compute_delta(degree: int) -> float:
+    """delta(P): spectral radius of the inflow-stripped derivative (``dgsem.py:46-59``)."""
+    if degree < 1:
+        raise ValueError("degree must be >= 1")
+    x, _ = gauss_lobatto(degree + 1)
+    return float(np.max(np.abs(np.linalg.eigvals(-_diff_matrix(x)[1:, 1:]))))
+
+
+def cfl_number(dt, dx_elem, lam_max, degree):
+    return dt * lam_max * 2.0 * compute_delta(degree) / dx_elem
+
+
+def dt_from_cfl(cfl, dx_elem, lam_max, degree):
+    return cfl * dx_elem / (2.0 * compute_delta(degree) * lam_max)
+
+
+@dataclass(frozen=True)
+class Mesh1D:
+    """Uniform 1-D mesh of n_elem elements with degree-P GLL nodes."""
+
+    x_left: float
+    x_right: float
+    n_elem: int
+    degree: int
+    bc: str = "periodic"
+
+    def __post_init__(self):
+        if self.x_right <= self.x_left:
+            raise ValueError("empty domain")
+        if self.n_elem < 1 or self.degree < 1:
+            raise ValueError("need at least one element and degree >= 1")
+        if self.bc not in ("periodic", "dirichlet"):
+            raise ValueError(f"unknown bc {self.bc!r}")
+
+    @property
+    def dx(self) -> float:
+        return (self.x_right - self.x_left) / self.n_elem
+
+    @cached_property
+    def ref_nodes(self) -> np.ndarray:
+        return gauss_lobatto(self.degree + 1)[0]
+
+    @cached_property
+    def ref_weights(self) -> np.ndarray:
+        return gauss_lobatto(self.degree + 1)[1]
+
+    @cached_property
+    def nodes_x(self) -> np.ndarray:
+        edges = self.x_left + self.dx * np.arange(self.n_elem)
+        return edges[:, None] + 0.5 * self.dx * (self.ref_nodes + 1.0)[None, :]
+
+
+@dataclass(frozen=True)
+class ArtificialViscosityParams:
+    kappa_s: float
+    c_s: float
+
+
+class SICoefficient:
+    """Opaque semi-implicit coefficient (dt_m/2) A_c(u_b)^2 + A_d (+nu_art)
+    frozen at u_b (``dgsem.py:356-396``); evaluated on the fly in-kernel.
+    ``u_b`` is owned (a snapshot) unless created by the fused sweeper."""
+
+    __slots__ = ("u_b", "dt_m", "kind")
+
+    def __init__(self, u_b, dt_m: float, kind: int = _lib.COEF_SI):
+        self.u_b = u_b
+        self.dt_m = float(dt_m)
+        self.kind = kind
+
+    def c(self) -> Coef:
+        return Coef(self.kind, self.dt_m, self.u_b.data_ptr() if self.u_b is not None else None)
+
+
+class DGOperator:
+    """Spatial operator bundle on one mesh/problem pair, executed on the GPU."""
+
+    def __init__(self, mesh: Mesh1D, problem, av: Optional[ArtificialViscosityParams] = None,
+                 penalty_const: float = 2.0, device: int = 0, eager_checks: bool = True):
+        if mesh.bc != "periodic":
+            raise NotImplementedError("the GPU path is built for periodic meshes (Dirichlet is next, SURVEY 8f)")
+        if getattr(problem, "source", None) is not None:
+            raise NotImplementedError("source terms are not built on the GPU path")
+        self.mesh = mesh
+        self.problem = problem
+        self.av = av
+        self.ncomp = problem.ncomp
+        self.p1 = mesh.degree + 1
+        self.ndof = self.ncomp * mesh.n_elem * self.p1
+        self.rt = get_runtime(device)
+        self.lib = self.rt.lib
+        self.eager_checks = eager_checks
+        kind = {"convdiff": _lib.CONVDIFF, "burgers": _lib.BURGERS}[problem.kind]
+        self._desc = _lib.Op1DDesc(mesh.n_elem, mesh.degree, self.ncomp, _lib.PERIODIC, kind,
+                                   float(mesh.x_left), float(mesh.x_right), float(getattr(problem, "speed", 0.0)),
+                                   float(problem.nu), float(penalty_const))
+        h = C.c_void_p()
+        self.rt.check(self.lib.sisdc_op1d_create(self.rt.h, C.byref(self._desc), C.byref(h)), "op1d_create")
+        self.h = h
+        nodes = np.zeros(self.p1)
+        wts = np.zeros(self.p1)
+        Dm = np.zeros(self.p1 * self.p1)
+        self.lib.sisdc_op1d_tables(h, nodes.ctypes.data_as(_lib.DP), wts.ctypes.data_as(_lib.DP),
+                                   Dm.ctypes.data_as(_lib.DP))
+        self.ref_nodes, self.ref_weights, self.D = nodes, wts, Dm.reshape(self.p1, self.p1)
+        self.mass_node = 0.5 * mesh.dx * wts
+        self.inv_mass = 1.0 / self.mass_node
+        self.mu0 = penalty_const * self.p1 ** 2 / mesh.dx
+        self.nu_art = None            # device tensor (n_elem,) when AV is active
+        self._last_dt = None
+        self._scratch = None
+
+    def __del__(self):
+        try:
+            self.lib.sisdc_op1d_destroy(self.h)
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------- layout
+    def as_nodes(self, u):
+        return self.rt.to_device(u).reshape(self.ncomp, self.mesh.n_elem, self.p1)
+
+    def flat(self, u3):
+        return self.rt.to_device(u3).reshape(-1)
+
+    def nodal_field(self, fn):
+        vals = np.asarray(fn(self.mesh.nodes_x))
+        if vals.shape != (self.ncomp, self.mesh.n_elem, self.p1):
+            raise ValueError("initial data has the wrong shape")
+        return self.rt.to_device(vals.reshape(-1))
+
+    def scratch(self):
+        """Per-operator device scratch used by the fused sweeper."""
+        if self._scratch is None:
+            self._scratch = {k: self.rt.empty(self.ndof) for k in ("rhs", "stage", "conv")}
+        return self._scratch
+
+    # ------------------------------------------------------- coefficients
+    def _coef(self, coeff, keep: list) -> Coef:
+        if coeff is None:
+            return Coef(_lib.COEF_NONE, 0.0, None)
+        if isinstance(coeff, SICoefficient):
+            return coeff.c()
+        if np.isscalar(coeff):
+            return Coef(_lib.COEF_CONST, float(coeff), None)
+        t = self.rt.to_device(coeff)
+        if t.numel() != self.mesh.n_elem * self.p1:
+            raise NotImplementedError("matrix-valued coefficients are not built on the GPU path")
+        keep.append(t)
+        return Coef(_lib.COEF_FIELD, 0.0, t.data_ptr())
+
+    def _phys(self):
+        """Physical coefficient as the reference returns it (``dgsem.py:313-326``)."""
+        nu = self.problem.nu
+        if self.nu_art is None:
+            return nu if nu > 0 else None
+        return SICoefficient(None, 0.0, _lib.COEF_PHYS)
+
+    def modified_diffusion_matrix(self, u_b, dt_m: float, scheme: str) -> Any:
+        if scheme == "euler":
+            return self._phys()
+        if scheme not in ("si1", "si2"):
+            raise ValueError(f"unknown scheme {scheme!r}")
+        if self.problem.is_linear and self.nu_art is None:
+            # constant: exactly the reference's float (dgsem.py:382-393)
+            half = 0.5 * dt_m * float(self.problem.speed) ** 2
+            return half + self.problem.nu if self.problem.nu > 0 else half
+        return SICoefficient(self.rt.to_device(u_b).clone(), dt_m)
+
+    # ---------------------------------------------------------- operators
+    def _out(self, out):
+        self.rt.bind_stream()
+        return self.rt.empty(self.ndof) if out is None else out
+
+    def apply_convection(self, u, t: float = 0.0, out=None):
+        u = self.rt.to_device(u)
+        out = self._out(out)
+        self.rt.check(self.lib.sisdc_apply_convection(self.h, u.data_ptr(), float(t), out.data_ptr()),
+                      "apply_convection")
+        return out
+
+    def apply_diffusion(self, coeff, u, t: float = 0.0, out=None):
+        keep = []
+        c = self._coef(coeff, keep)
+        u = self.rt.to_device(u)
+        out = self._out(out)
+        self.rt.check(self.lib.sisdc_apply_diffusion(self.h, c, u.data_ptr(), float(t), out.data_ptr()),
+                      "apply_diffusion")
+        return out
+
+    def eval_rhs(self, u, t: float = 0.0, out=None):
+        u = self.rt.to_device(u)
+        out = self._out(out)
+        if self.eager_checks:
+            self.rt.reset_status()
+        self.rt.check(self.lib.sisdc_eval_rhs(self.h, u.data_ptr(), float(t), out.data_ptr()), "eval_rhs")
+        if self.eager_checks:
+            self.rt.raise_on_failure()
+        return out
+
+    def apply_source(self, u, t: float):
+        return self.rt.zeros(self.ndof)
+
+    def coefficient_field(self, coeff):
+        """Materialise a coefficient as an (n_elem, P+1) device field."""
+        keep = []
+        c = self._coef(coeff, keep)
+        out = self.rt.empty(self.mesh.n_elem * self.p1)
+        self.rt.bind_stream()
+        self.rt.check(self.lib.sisdc_coef_field(self.h, c, out.data_ptr()), "coef_field")
+        return out.reshape(self.mesh.n_elem, self.p1)
+
+    def implicit_solve(self, coeff, a: float, rhs, t: float = 0.0, out=None):
+        """Solve (M + a B[coeff]) x = M rhs with the pinned Jacobi-PCG."""
+        if a == 0.0:
+            return rhs
+        keep = []
+        c = self._coef(coeff, keep)
+        rhs = self.rt.to_device(rhs)
+        out = self._out(out)
+        if self.eager_checks:
+            self.rt.reset_status()
+        self.rt.check(self.lib.sisdc_implicit_solve(self.h, c, float(a), rhs.data_ptr(), float(t), out.data_ptr()),
+                      "implicit_solve")
+        if self.eager_checks:
+            self.rt.raise_on_failure()
+        return out
+
+    # ---------------------------------------------------- shock sensor / slab
+    def persson_viscosity(self, u):
+        out = self.rt.zeros(self.mesh.n_elem)
+        if self.av is None:
+            return out
+        u = self.rt.to_device(u)
+        self.rt.bind_stream()
+        self.rt.check(self.lib.sisdc_persson_viscosity(self.h, u.data_ptr(), float(self.av.kappa_s),
+                                                       float(self.av.c_s), out.data_ptr()), "persson")
+        return out
+
+    def begin_slab(self, u0, t0: float, dt: float) -> None:
+        """Freeze per-slab data (``dgsem.py:563-571``): the AV field."""
+        if self.av is not None:
+            if self.nu_art is None:
+                self.nu_art = self.rt.zeros(self.mesh.n_elem)
+            u0 = self.rt.to_device(u0)
+            self.rt.bind_stream()
+            self.rt.check(self.lib.sisdc_persson_viscosity(self.h, u0.data_ptr(), float(self.av.kappa_s),
+                                                           float(self.av.c_s), self.nu_art.data_ptr()), "persson")
+            self.lib.sisdc_op1d_set_nu_art(self.h, self.nu_art.data_ptr())
+        self._last_dt = dt
+
+    # ------------------------------------------------------------ helpers
+    def total_integral(self, u):
+        u3 = self.as_nodes(u)
+        return (u3 * self.rt.to_device(self.mass_node)).sum(dim=(1, 2))
+
+    def norm_l2(self, u) -> float:
+        u3 = self.as_nodes(u)
+        return float(((u3 ** 2) * self.rt.to_device(self.mass_node)).sum().sqrt())
+
+
+def max_wave_speed(op: DGOperator, u) -> float:
+    if op.problem.kind == "convdiff":
+        return abs(op.problem.speed)
+    return float(op.rt.to_device(u).abs().max())

@@ -1,0 +1,45 @@
+"""Problem descriptors (``problems.py:25-82`` of the reference).
+
+The pointwise physics -- flux, wave speed, convective Jacobian A_c and
+diffusion coefficient A_d -- is evaluated inside the sm_100a kernels
+(``csrc/sisdc_dev.cuh``); these objects carry the parameters and the
+attributes the sweeper and the operator read (``ncomp``, ``is_linear``,
+``source``, ``boundary_state``).
+"""
+from __future__ import annotations
+
+
+class ConvectionDiffusion:
+    """u_t + v u_x = nu u_xx, constant coefficients (``problems.py:25-52``)."""
+
+    ncomp = 1
+    is_linear = True
+    source = None
+    kind = "convdiff"
+
+    def __init__(self, speed: float = 1.0, nu: float = 0.0, boundary=None):
+        if nu < 0:
+            raise ValueError("diffusion coefficient must be nonnegative")
+        self.speed = float(speed)
+        self.nu = float(nu)
+        self.boundary_state = boundary
+
+    def conv_jacobian_const(self):
+        return self.speed
+
+
+class Burgers:
+    """u_t + (u^2/2)_x = nu u_xx (``problems.py:55-82``); sources are not
+    built on the GPU path."""
+
+    ncomp = 1
+    is_linear = False
+    kind = "burgers"
+
+    def __init__(self, nu: float = 0.0, source=None, boundary=None):
+        if nu < 0:
+            raise ValueError("diffusion coefficient must be nonnegative")
+        self.nu = float(nu)
+        self.source = source
+        self.boundary_state = boundary
+        self.speed = 0.0

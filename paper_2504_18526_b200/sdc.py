@@ -1,0 +1,251 @@
+"""Deferred-correction sweeps on one time slab, on the GPU (reference ``sdc.py``).
+
+Same functions and semantics as the reference sweeper; every per-node
+substep is a short fixed sequence of fused kernels on the context's stream:
+
+    stage_rhs  rhs = u_{m-1} + Q_m (+g_m) + dt_m conv(u_{m-1}) - h1_old[m]   (sdc.py:218,228-235)
+    cg         stage = S_m(rhs)                                             (dgsem.py:503-533 -> PCG)
+    stage_rhs  rhs = u_{m-1} + Q_m (+g_m) + dt_m conv(stage) - h2_old[m]     (sdc.py:237)
+    cg         u_m = S_m(rhs)
+    caches     f_m, h1_m, h2_m                                              (sdc.py:77-98)
+
+The semi-implicit coefficient (dt_m/2) A_c(u_{m-1})^2 + A_d is never stored:
+the kernels evaluate it from u_{m-1} on the fly.  No host synchronisation
+happens inside a sweep, so whole slabs can be captured in a CUDA graph.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import Coef
+from .collocation import CollocationRule, QuadratureWeights
+
+Form = str
+
+
+@dataclass
+class NodalSolution:
+    """Slab iterate (``sdc.py:24-52``): device tensors u0 (N), u/f/h1/h2 (M, N)."""
+    u0: object
+    u: object
+    f: object
+    h1: object
+    h2: Optional[object]
+    t0: float
+
+    def copy(self) -> "NodalSolution":
+        return NodalSolution(self.u0.clone(), self.u.clone(), self.f.clone(), self.h1.clone(),
+                             None if self.h2 is None else self.h2.clone(), self.t0)
+
+    @property
+    def end_value(self):
+        return self.u[-1]
+
+
+def _rt(ctx):
+    return ctx.rt
+
+
+def _node_times(rule, dt, t0):
+    return t0 + dt * rule.tau
+
+
+def _dts(rule, dt):
+    return dt * np.diff(np.concatenate(([0.0], rule.tau)))
+
+
+def _alloc(ctx, u0, M: int, scheme: str, t0: float) -> NodalSolution:
+    rt = _rt(ctx)
+    u0 = rt.to_device(u0)
+    n = u0.numel()
+    h2 = rt.empty(M, n) if scheme == "si2" else None
+    return NodalSolution(u0.clone(), rt.empty(M, n), rt.empty(M, n), rt.empty(M, n), h2, t0)
+
+
+def _scheme_id(scheme):
+    try:
+        return _lib.SCHEMES[scheme]
+    except KeyError:
+        raise ValueError(f"unknown scheme {scheme!r}") from None
+
+
+def _coef(ctx, scheme, u_prev, dt_m) -> Coef:
+    """C_m frozen at u_{m-1}: SI for si1/si2, physical for euler (dgsem.py:356-396)."""
+    if scheme == "euler":
+        return Coef(_lib.COEF_PHYS, 0.0, None)
+    return Coef(_lib.COEF_SI, float(dt_m), u_prev.data_ptr())
+
+
+def _caches(ctx, scheme, sol, M, m_first, m_count, dts, conv_prev=None):
+    rt = _rt(ctx)
+    arr, p = _lib.darr(dts)
+    rt.check(rt.lib.sisdc_node_caches(
+        ctx.h, _scheme_id(scheme), M, m_first, m_count, sol.u0.data_ptr(), sol.u.data_ptr(),
+        None if conv_prev is None else conv_prev.data_ptr(), p, float(sol.t0), None,
+        sol.f.data_ptr(), sol.h1.data_ptr(), None if sol.h2 is None else sol.h2.data_ptr()), "node_caches")
+
+
+def refresh_caches(ctx, rule: CollocationRule, dt: float, scheme: str, sol: NodalSolution) -> None:
+    """Rebuild all caches after node values changed outside a sweep
+    (``sdc.py:101-119``): one kernel over all M nodes."""
+    _rt(ctx).bind_stream()
+    _caches(ctx, scheme, sol, rule.M, 0, rule.M, _dts(rule, dt))
+
+
+def _stage(ctx, base, conv_in, dt_m, f_old, w_row, dt, g_m, h_old, rhs, conv_out):
+    rt = _rt(ctx)
+    M = 0 if f_old is None else f_old.shape[0]
+    wa, wp = _lib.darr(w_row if w_row is not None else np.zeros(1))
+    rt.check(rt.lib.sisdc_stage_rhs(
+        ctx.h, base.data_ptr(), conv_in.data_ptr(), float(dt_m),
+        None if f_old is None else f_old.data_ptr(), M, wp if f_old is not None else None, float(dt),
+        None if g_m is None else g_m.data_ptr(), None if h_old is None else h_old.data_ptr(), 0.0,
+        rhs.data_ptr(), None if conv_out is None else conv_out.data_ptr()), "stage_rhs")
+
+
+def _solve(ctx, coef: Coef, a, rhs, out):
+    rt = _rt(ctx)
+    rt.check(rt.lib.sisdc_implicit_solve(ctx.h, coef, float(a), rhs.data_ptr(), 0.0, out.data_ptr()),
+             "implicit_solve")
+
+
+def _substep(ctx, scheme, up, dtm, f_old, w_row, dt, g_m, h1_old, h2_old, out):
+    """One SI substep into ``out`` (predictor when f_old/h are None)."""
+    s = ctx.scratch()
+    c = _coef(ctx, scheme, up, dtm)
+    _stage(ctx, up, up, dtm, f_old, w_row, dt, g_m, h1_old, s["rhs"], s["conv"])
+    if scheme in ("euler", "si1"):
+        _solve(ctx, c, dtm, s["rhs"], out)
+    elif scheme == "si2":
+        _solve(ctx, c, dtm, s["rhs"], s["stage"])
+        _stage(ctx, up, s["stage"], dtm, f_old, w_row, dt, g_m, h2_old, s["rhs"], None)
+        _solve(ctx, c, dtm, s["rhs"], out)
+    else:
+        raise ValueError(f"unknown scheme {scheme!r}")
+    return s["conv"]
+
+
+def predict(ctx, rule, dt, scheme, u0, t0, out: Optional[NodalSolution] = None) -> NodalSolution:
+    """0-th iterate by marching the substepper (``sdc.py:122-156``)."""
+    _rt(ctx).bind_stream()
+    sol = out if out is not None else _alloc(ctx, u0, rule.M, scheme, t0)
+    if out is not None:
+        _rt(ctx).copy(sol.u0, _rt(ctx).to_device(u0))
+        sol.t0 = t0
+    dts = _dts(rule, dt)
+    for m in range(rule.M):
+        up = sol.u0 if m == 0 else sol.u[m - 1]
+        if dts[m] == 0.0:
+            _rt(ctx).copy(sol.u[m], up)
+            _caches(ctx, scheme, sol, rule.M, m, 1, dts)
+            continue
+        conv = _substep(ctx, scheme, up, dts[m], None, None, 0.0, None, None, None, sol.u[m])
+        _caches(ctx, scheme, sol, rule.M, m, 1, dts, conv)
+    return sol
+
+
+def constant_start(ctx, rule, dt, scheme, u0, t0) -> NodalSolution:
+    sol = _alloc(ctx, u0, rule.M, scheme, t0)
+    sol.u[:] = sol.u0
+    refresh_caches(ctx, rule, dt, scheme, sol)
+    return sol
+
+
+def from_nodes(ctx, rule, dt, scheme, u0, t0, u_nodes, out: Optional[NodalSolution] = None) -> NodalSolution:
+    sol = out if out is not None else _alloc(ctx, u0, rule.M, scheme, t0)
+    if u_nodes is not sol.u:
+        sol.u.copy_(_rt(ctx).to_device(u_nodes))
+    refresh_caches(ctx, rule, dt, scheme, sol)
+    return sol
+
+
+def sweep(ctx, rule: CollocationRule, weights: QuadratureWeights, dt: float, scheme: str,
+          sol: NodalSolution, g=None, form: Form = "incremental",
+          out: Optional[NodalSolution] = None) -> NodalSolution:
+    """One correction sweep (``sdc.py:190-242``); returns the next iterate."""
+    if form == "nonincremental":
+        return _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g)
+    if form != "incremental":
+        raise ValueError(f"unknown sweep form {form!r}")
+    rt = _rt(ctx)
+    rt.bind_stream()
+    new = out if out is not None else _alloc(ctx, sol.u0, rule.M, scheme, sol.t0)
+    if out is not None:
+        rt.copy(new.u0, sol.u0)
+        new.t0 = sol.t0
+    dts = _dts(rule, dt)
+    for m in range(rule.M):
+        up = new.u0 if m == 0 else new.u[m - 1]
+        gm = None if g is None else g[m]
+        if dts[m] == 0.0:
+            _stage(ctx, up, up, 0.0, sol.f, weights.w_nn[m], dt, gm, None, new.u[m], None)
+            _caches(ctx, scheme, new, rule.M, m, 1, dts)
+            continue
+        conv = _substep(ctx, scheme, up, dts[m], sol.f, weights.w_nn[m], dt, gm, sol.h1[m],
+                        None if sol.h2 is None else sol.h2[m], new.u[m])
+        _caches(ctx, scheme, new, rule.M, m, 1, dts, conv)
+    return new
+
+
+def _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g):
+    raise NotImplementedError("the non-incremental sweep form is next-tier on the GPU path (SURVEY 8f)")
+
+
+def collocation_defect(rule, weights, dt, sol: NodalSolution, form: Form = "incremental", ctx=None,
+                       sign: float = 1.0, add=None, out=None):
+    """F(u) with the cached rhs (``sdc.py:304-319``)."""
+    if ctx is None:
+        raise ValueError("the GPU defect needs the level's operator context (ctx=)")
+    rt = _rt(ctx)
+    rt.bind_stream()
+    inc = 1 if form == "incremental" else 0
+    W = weights.w_nn if inc else weights.w_0n
+    wa, wp = _lib.darr(W)
+    if out is None:
+        out = rt.empty(*sol.u.shape)
+    rt.check(rt.lib.sisdc_collocation_defect(ctx.h, rule.M, wp, float(dt), inc, sol.u0.data_ptr(), sol.u.data_ptr(),
+                                             sol.f.data_ptr(), float(sign),
+                                             None if add is None else add.data_ptr(), out.data_ptr()),
+             "collocation_defect")
+    return out
+
+
+def residual(rule, weights, dt, sol, g=None, form: Form = "incremental", ctx=None):
+    """g - F(u) (``sdc.py:287-301``)."""
+    return collocation_defect(rule, weights, dt, sol, form, ctx=ctx, sign=-1.0, add=g)
+
+
+def run_sdc(ctx, rule, weights, dt, scheme, u0, t0, n_sweeps, form: Form = "incremental",
+            start: str = "predictor", observer: Optional[Callable] = None) -> NodalSolution:
+    """Predictor (or constant start) plus n_sweeps corrections (``sdc.py:322-354``)."""
+    if hasattr(ctx, "begin_slab"):
+        ctx.begin_slab(u0, t0, dt)
+    if start == "predictor":
+        sol = predict(ctx, rule, dt, scheme, u0, t0)
+    elif start == "constant":
+        sol = constant_start(ctx, rule, dt, scheme, u0, t0)
+    else:
+        raise ValueError(f"unknown start {start!r}")
+    if observer is not None:
+        observer(0, sol)
+    for k in range(1, n_sweeps + 1):
+        sol = sweep(ctx, rule, weights, dt, scheme, sol, form=form)
+        if observer is not None:
+            observer(k, sol)
+    return sol
+
+
+def integrate_sdc(ctx, rule, weights, scheme, u0, t0, dt, n_steps, n_sweeps, form: Form = "incremental"):
+    """March n_steps slabs (``sdc.py:357-376``)."""
+    u = ctx.rt.to_device(u0)
+    t = t0
+    for _ in range(n_steps):
+        sol = run_sdc(ctx, rule, weights, dt, scheme, u, t, n_sweeps, form=form)
+        u = sol.end_value.clone()
+        t += dt
+    ctx.rt.raise_on_failure()
+    return u

@@ -1,0 +1,200 @@
+"""Inter-level transfers in time and space (reference ``transfer.py``).
+
+The dense operator matrices are host-side setup (``build_temporal_transfer``
+``:61-96``, ``build_spatial_p_transfer`` ``:213-245``); applying them to
+device states runs in the library's element-local transfer kernels, with the
+composition order of ``SpaceTimeTransfer`` (``:324-352``): fine->coarse
+spatial first, coarse->fine temporal first.  Built: embedded projection,
+nodes_only convention, p-coarsening on a fixed mesh (every BASELINE config).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .collocation import CollocationRule, gauss_legendre, lagrange_matrix, make_nodes
+from .runtime import get_runtime
+
+Direction = str
+
+
+@dataclass(frozen=True)
+class TransferPair:
+    """Dense operator triple for one axis (``transfer.py:27-45``)."""
+    interp: np.ndarray
+    project: np.ndarray
+    restrict: np.ndarray
+    axis: str
+    projection_kind: str
+    meta: dict
+
+    def matrix(self, direction: Direction) -> np.ndarray:
+        if direction not in ("interp", "project", "restrict"):
+            raise ValueError(f"unknown direction {direction!r}")
+        return getattr(self, direction)
+
+
+def _l2_project_matrix(src, dst, domain=(0.0, 1.0)) -> np.ndarray:
+    a, b = domain
+    gx, gw = gauss_legendre(len(src) + 3)
+    pts = 0.5 * (b - a) * gx + 0.5 * (a + b)
+    wts = 0.5 * (b - a) * gw
+    Ld, Ls = lagrange_matrix(dst, pts), lagrange_matrix(src, pts)
+    return np.linalg.solve(Ld.T @ (wts[:, None] * Ld), Ld.T @ (wts[:, None] * Ls))
+
+
+def build_temporal_transfer(coarse_rule: CollocationRule, fine_rule: CollocationRule,
+                            projection_kind: str = "embedded", node_convention: str = "nodes_only") -> TransferPair:
+    if coarse_rule.M > fine_rule.M:
+        raise ValueError("coarse rule must not have more nodes than the fine one")
+    if node_convention != "nodes_only":
+        raise NotImplementedError("the GPU path builds the nodes_only convention (the reference default)")
+    src, dst = coarse_rule.tau, fine_rule.tau
+    interp = lagrange_matrix(src, dst)
+    if projection_kind == "embedded":
+        project = lagrange_matrix(dst, src)
+    elif projection_kind == "l2":
+        project = _l2_project_matrix(dst, src)
+    else:
+        raise ValueError(f"unknown projection kind {projection_kind!r}")
+    return TransferPair(interp, project, interp.T.copy(), "temporal", projection_kind,
+                        {"node_convention": node_convention, "M": (coarse_rule.M, fine_rule.M)})
+
+
+def _gll_reference(n: int) -> np.ndarray:
+    return 2.0 * make_nodes("lobatto", n).tau - 1.0
+
+
+@dataclass
+class SpatialTransfer:
+    """Per-element p-transfer blocks (``transfer.py:129-203``); GPU apply."""
+    kind: str
+    ncomp: int
+    ne_coarse: int
+    ne_fine: int
+    np_coarse: int
+    np_fine: int
+    blocks: dict
+    projection_kind: str
+    jump_policy: Optional[str] = None
+
+    def apply(self, direction: Direction, u_flat):
+        """Apply to one device state (``transfer.py:149-163``)."""
+        rt = get_runtime()
+        u = rt.to_device(u_flat)
+        if self.kind == "identity":
+            return u.clone()
+        h = _xfer_handle(self, None)
+        dirn = {"interp": 0, "project": 1, "restrict": 2}[direction]
+        out = rt.empty(self.ncomp * self.ne_coarse * (self.np_fine if dirn == 0 else self.np_coarse))
+        rt.bind_stream()
+        rt.check(rt.lib.sisdc_xfer_spatial(h.h, dirn, u.data_ptr(), out.data_ptr()), "xfer_spatial")
+        return out
+
+
+def build_spatial_p_transfer(p_coarse: int, p_fine: int, n_elem: int, ncomp: int = 1,
+                             projection_kind: str = "embedded") -> SpatialTransfer:
+    if p_coarse > p_fine:
+        raise ValueError("coarse degree must not exceed fine degree")
+    if p_coarse == p_fine:
+        return SpatialTransfer("identity", ncomp, n_elem, n_elem, p_coarse + 1, p_fine + 1, {}, "embedded")
+    xc, xf = _gll_reference(p_coarse + 1), _gll_reference(p_fine + 1)
+    interp = lagrange_matrix(xc, xf)
+    if projection_kind == "embedded":
+        project = lagrange_matrix(xf, xc)
+    elif projection_kind == "l2":
+        project = _l2_project_matrix(xf, xc, domain=(-1.0, 1.0))
+    else:
+        raise ValueError(f"unknown projection kind {projection_kind!r}")
+    return SpatialTransfer("p", ncomp, n_elem, n_elem, p_coarse + 1, p_fine + 1,
+                           {"interp": interp, "project": project, "restrict": interp.T.copy()}, projection_kind)
+
+
+class _XferHandle:
+    def __init__(self, spatial: SpatialTransfer, temporal: Optional[TransferPair]):
+        rt = get_runtime()
+        self.rt = rt
+        if temporal is None:
+            It = Pt = np.ones((1, 1))
+            Mc = Mf = 1
+        else:
+            It, Pt = temporal.interp, temporal.project
+            Mf, Mc = It.shape
+        Isp, Psp = spatial.blocks["interp"], spatial.blocks["project"]
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (It, Pt, Isp, Psp)]
+        h = C.c_void_p()
+        ptrs = [a.ctypes.data_as(_lib.DP) for a in self._keep]
+        rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_fine, spatial.np_coarse, spatial.np_fine, Mc, Mf,
+                                          *ptrs, C.byref(h)), "xfer_create")
+        self.h = h
+        self.Mc, self.Mf = Mc, Mf
+
+    def __del__(self):
+        try:
+            self.rt.lib.sisdc_xfer_destroy(self.h)
+        except Exception:
+            pass
+
+
+def _xfer_handle(spatial: SpatialTransfer, temporal: Optional[TransferPair]) -> _XferHandle:
+    key = "_xh_t" if temporal is not None else "_xh_s"
+    owner = temporal if temporal is not None else spatial
+    h = getattr(spatial, key, None)
+    if h is None or getattr(h, "_temporal", None) is not temporal:
+        h = _XferHandle(spatial, temporal)
+        h._temporal = temporal
+        setattr(spatial, key, h)
+    return h
+
+
+def build_identity_spatial(ndof: int) -> SpatialTransfer:
+    return SpatialTransfer("identity", 1, 1, 1, ndof, ndof, {}, "embedded")
+
+
+@dataclass(frozen=True)
+class SpaceTimeTransfer:
+    """Tensor composition of a temporal and a spatial pair (``transfer.py:324-352``)."""
+    temporal: TransferPair
+    spatial: SpatialTransfer
+
+    @property
+    def handle(self) -> _XferHandle:
+        if self.spatial.kind != "p":
+            raise NotImplementedError("the GPU path builds spatial p-transfers")
+        return _xfer_handle(self.spatial, self.temporal)
+
+    def _down(self, sdir, tdir, nodes):
+        h = self.handle
+        rt = h.rt
+        x = rt.to_device(nodes)
+        out = rt.empty(h.Mc, self.spatial.ncomp * self.spatial.ne_coarse * self.spatial.np_coarse)
+        rt.bind_stream()
+        rt.check(rt.lib.sisdc_xfer_down(h.h, sdir, tdir, x.data_ptr(), out.data_ptr()), "xfer_down")
+        return out
+
+    def project_solution(self, u_nodes_f, u0_f=None):
+        return self._down(1, 1, u_nodes_f)
+
+    def restrict_residual(self, r_nodes_f):
+        return self._down(2, 2, r_nodes_f)
+
+    def _up(self, nodes_c, sub=None, out=None, accumulate=False):
+        h = self.handle
+        rt = h.rt
+        uc = rt.to_device(nodes_c)
+        if out is None:
+            out = rt.empty(h.Mf, self.spatial.ncomp * self.spatial.ne_fine * self.spatial.np_fine)
+        rt.bind_stream()
+        rt.check(rt.lib.sisdc_xfer_interp(h.h, int(accumulate), uc.data_ptr(),
+                                          None if sub is None else sub.data_ptr(), out.data_ptr()), "xfer_interp")
+        return out
+
+    def interp_correction(self, d_nodes_c):
+        return self._up(d_nodes_c)
+
+    def interp_solution(self, u_nodes_c, u0_c=None):
+        return self._up(u_nodes_c)

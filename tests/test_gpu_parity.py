@@ -1,0 +1,218 @@
+"""CUDA path vs the CPU oracle and the reference goldens (needs a B200).
+
+Tolerances: the north star's per-step bound is 1e-11 relative L2 with
+identical CG iteration counts.  Operator outputs are compared at 1e-12
+relative to max(1, |ref|); quantities that apply the diffusion operator to a
+state (f = eval_rhs) amplify state roundoff by ||D[nu]|| and get 1e-10.
+"""
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+from oracle import dg1d, sweeper as osw, workloads  # noqa: E402
+from paper_2504_18526_b200.configs import CFG1, CFG2  # noqa: E402
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
+
+
+def l2rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def gpu_problem(w):
+    from paper_2504_18526_b200 import problems
+    if w.problem == "convdiff":
+        return problems.ConvectionDiffusion(w.params["speed"], w.params["nu"])
+    return problems.Burgers(w.params["nu"])
+
+
+def gpu_op(w, P, ne=None):
+    from paper_2504_18526_b200 import dgsem
+    return dgsem.DGOperator(dgsem.Mesh1D(w.x_left, w.x_right, ne or w.n_elem, P), gpu_problem(w))
+
+
+def gpu_hier(w):
+    from paper_2504_18526_b200 import mlsdc
+    return mlsdc.build_p_hierarchy(lambda P: gpu_op(w, P), [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+
+
+@pytest.fixture(scope="module")
+def rt():
+    from paper_2504_18526_b200.runtime import get_runtime
+    r = get_runtime()
+    r.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=0)
+    return r
+
+
+def new_log_slice(rt, n0):
+    it, mg = rt.cg_log()
+    return it[n0:].tolist(), mg[n0:]
+
+
+# ------------------------------------------------------------- operators
+@pytest.mark.parametrize("tag,w,ne", [("cfg1", CFG1, CFG1.n_elem), ("cfg2", CFG2, 64)])
+def test_operators_vs_reference_goldens(rt, golden, tag, w, ne):
+    from paper_2504_18526_b200.dgsem import SICoefficient
+    G = golden["operators"]
+    for P in (w.p_fine, w.p_coarse):
+        k = f"{tag}_P{P}"
+        op = gpu_op(w, P, ne)
+        u, fld = G[k + "_u"], G[k + "_fld"]
+        assert rel(op.apply_convection(u), G[k + "_conv"]) < 1e-13
+        assert rel(op.apply_diffusion(0.0137, u), G[k + "_diff_const"]) < 1e-12
+        assert rel(op.apply_diffusion(fld, u), G[k + "_diff_field"]) < 1e-12
+        assert rel(op.eval_rhs(u), G[k + "_rhs"]) < 1e-12
+        c = op.modified_diffusion_matrix(u, 0.0123, "si2")
+        if isinstance(c, SICoefficient):
+            assert rel(op.coefficient_field(c), G[k + "_modc"]) < 1e-14
+        else:
+            assert abs(c - float(G[k + "_modc"])) < 1e-16
+        rhs = G[k + "_solve_rhs"]
+        assert rel(op.implicit_solve(0.0137, 0.0123, rhs), G[k + "_solve_const"]) < 1e-11
+        assert rel(op.implicit_solve(fld, 0.0123, rhs), G[k + "_solve_field"]) < 1e-11
+
+
+@pytest.mark.parametrize("cluster", [0, 1, 2, 3, 4, 8, 16])
+def test_cg_matches_oracle_iterations(rt, golden, cluster):
+    """Every cluster partition reproduces the oracle PCG's iteration count and
+    solution (cfg-2 mesh, field coefficient)."""
+    w = CFG2
+    G = golden["operators"]
+    k = f"cfg2_P{w.p_fine}"
+    u, fld, rhs = G[k + "_u"], G[k + "_fld"], G[k + "_solve_rhs"]
+    rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=cluster)
+    try:
+        op = gpu_op(w, w.p_fine, 64)
+        orc = dg1d.Op1D(w.x_left, w.x_right, 64, w.p_fine, workloads.make_problem(w), solver="pcg")
+        for coeff in (fld, 0.0137):
+            n0 = rt.status()[2]
+            x = op.implicit_solve(coeff, 0.0123, rhs)
+            xo = orc.implicit_solve(coeff, 0.0123, rhs)
+            its, mg = new_log_slice(rt, n0)
+            assert its == [orc.cg_log[-1][0]]
+            assert rel(x, xo) < 1e-13
+    finally:
+        rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=0)
+
+
+def test_implicit_solve_edge_cases(rt):
+    w = CFG1
+    op = gpu_op(w, 4, 8)
+    rhs = np.random.default_rng(0).standard_normal(op.ndof)
+    assert op.implicit_solve(0.01, 0.0, rhs) is rhs                      # a == 0 -> rhs (dgsem.py:505)
+    x = op.implicit_solve(0.01, 0.1, np.zeros(op.ndof))                   # b == 0 -> zeros (dgsem.py:510)
+    assert float(x.abs().max()) == 0.0
+    # residual contract (test_dgsem.py:304-309): x - a D[C] x = rhs
+    x = op.implicit_solve(0.02, 0.05, rhs)
+    r = x - 0.05 * op.apply_diffusion(0.02, x) - op.rt.to_device(rhs)
+    assert float(r.abs().max()) < 1e-11 * np.abs(rhs).max()
+
+
+def test_nonfinite_rhs_reports_element(rt):
+    from paper_2504_18526_b200.dgsem import SolverError
+    op = gpu_op(CFG1, 3, 8)
+    u = np.zeros(op.ndof)
+    u[5 * 4 + 1] = np.nan
+    with pytest.raises(SolverError, match="element 5"):
+        op.eval_rhs(u, 0.0)
+    rt.reset_status()
+
+
+def test_level_too_large_is_an_error(rt):
+    from paper_2504_18526_b200 import dgsem, problems
+    op = dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, 20000, 8), problems.Burgers(1e-3))
+    with pytest.raises(Exception, match="too large"):
+        op.implicit_solve(0.01, 0.1, np.ones(op.ndof))
+
+
+# ---------------------------------------------------- sweeps and slabs
+@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2)])
+def test_predict_and_sweeps_vs_oracle(rt, golden, tag, w):
+    from paper_2504_18526_b200 import collocation, sdc
+    G = golden["trajectories"]
+    dt, u0 = float(G[f"{tag}_dt"]), G[f"{tag}_u0"]
+    op = gpu_op(w, w.p_fine)
+    rule = collocation.make_nodes("radau_right", w.m_fine)
+    wts = collocation.make_weights(rule)
+    log = []
+    orc = dg1d.Op1D(w.x_left, w.x_right, w.n_elem, w.p_fine, workloads.make_problem(w), solver="pcg", cg_log=log)
+    orule = osw.Rule("radau_right", w.m_fine)
+    n0 = rt.status()[2]
+    s = sdc.predict(op, rule, dt, "si2", u0, 0.0)
+    so = osw.predict(orc, orule, dt, "si2", u0, 0.0)
+    for _ in range(2):
+        s = sdc.sweep(op, rule, wts, dt, "si2", s)
+        so = osw.sweep(orc, orule, dt, "si2", so)
+    its, _ = new_log_slice(rt, n0)
+    assert its == [it for it, _ in log]
+    assert l2rel(s.u, so.u) < 1e-12
+    assert rel(s.f, so.f) < 1e-10
+    assert rel(s.h1, so.h1) < 1e-12 and rel(s.h2, so.h2) < 1e-12
+    F = sdc.collocation_defect(rule, wts, dt, s, ctx=op)
+    assert rel(F, osw.defect(orule, dt, so)) < 1e-11
+
+
+@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2)])
+def test_mlsdc_step_parity(rt, golden, tag, w):
+    """One SI-MLSDC step from the golden input: <= 1e-11 rel L2 against the
+    reference (LU as shipped, and with the pinned PCG), identical CG
+    iteration sequence, 6 fine sweeps / 12 coarse passes."""
+    from paper_2504_18526_b200 import mlsdc
+    G = golden["trajectories"]
+    dt = float(G[f"{tag}_dt"])
+    h = gpu_hier(w)
+    for step in (1, 2):
+        uin = G[f"{tag}_u0"] if step == 1 else G[f"{tag}_pcg_u1"]
+        n0 = rt.status()[2]
+        sol = mlsdc.run_mlsdc(h, uin, (step - 1) * dt, dt, w.n_cycles, strategy="fmg")
+        its, margins = new_log_slice(rt, n0)
+        assert its == G[f"{tag}_pcg_iters{step}"].tolist()
+        assert l2rel(sol.u[-1], G[f"{tag}_pcg_u{step}"]) < 1e-11
+        if step == 1:
+            assert l2rel(sol.u[-1], G[f"{tag}_lu_u1"]) < 1e-11
+    assert h.fine_sweeps == 12 and h.coarse_passes == 24
+    rt.raise_on_failure()
+
+
+def test_graph_replay_equals_eager(rt, golden):
+    from paper_2504_18526_b200 import mlsdc
+    w = CFG2
+    G = golden["trajectories"]
+    dt, u0 = float(G["cfg2_dt"]), G["cfg2_u0"]
+    h1 = gpu_hier(w)
+    u_eager = mlsdc.integrate_mlsdc(h1, u0, 0.0, dt, 2, w.n_cycles, strategy="fmg")
+    h2 = gpu_hier(w)
+    g = mlsdc.SlabGraph(h2, u0, 0.0, dt, w.n_cycles, "fmg")
+    assert g.kernels_per_step > 100
+    g.step()
+    g.step()
+    rt.synchronize()
+    assert float((g.u - u_eager).abs().max()) == 0.0       # deterministic kernels, bitwise
+    assert l2rel(g.u, G["cfg2_pcg_u2"]) < 1e-11
+
+
+# ------------------------------------------- full-size properties (cfg 2)
+def test_full_size_properties(rt):
+    """Size-independent identities at the cfg-2 fine level: conservation of
+    convection and diffusion, SIP symmetry in the mass inner product."""
+    w = CFG2
+    op = gpu_op(w, w.p_fine)
+    rng = np.random.default_rng(7)
+    m = np.tile(op.mass_node, w.n_elem)
+    u = 1.0 + 0.2 * rng.standard_normal(op.ndof)
+    c = op.apply_convection(u).cpu().numpy()
+    assert abs(np.dot(m, c)) < 1e-10
+    fld = 0.01 + 0.01 * rng.random((w.n_elem, w.p_fine + 1))
+    x, y = rng.standard_normal(op.ndof), rng.standard_normal(op.ndof)
+    dx, dy = op.apply_diffusion(fld, x).cpu().numpy(), op.apply_diffusion(fld, y).cpu().numpy()
+    assert abs(np.dot(m, dx)) < 1e-9
+    assert abs(np.dot(m * y, dx) - np.dot(m * x, dy)) < 1e-9 * max(1.0, abs(np.dot(m * y, dx)))
+    assert np.dot(m * x, dx) < 0.0

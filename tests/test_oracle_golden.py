@@ -1,0 +1,95 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself
+(oracle/make_golden.py runs /root/reference in-process)."""
+import numpy as np
+import pytest
+
+from oracle import dg1d, quad, sweeper, workloads
+from paper_2504_18526_b200.configs import CFG1, CFG2
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(1.0, np.abs(np.asarray(b)).max()))
+
+
+def test_tables(golden):
+    G = golden["tables"]
+    for M in (1, 2, 3, 4, 5, 7):
+        tau = quad.radau_right(M)
+        assert np.abs(tau - G[f"radau_tau_{M}"]).max() < 1e-15
+        assert np.abs(quad.weights_nn(tau) - G[f"radau_wnn_{M}"]).max() < 1e-14
+        assert np.abs(quad.weights_0n(quad.weights_nn(tau)) - G[f"radau_w0n_{M}"]).max() < 1e-14
+    for M in (2, 3, 5):
+        assert np.abs(quad.lobatto(M) - G[f"lobatto_tau_{M}"]).max() < 1e-15
+    for P in (3, 4, 7, 8):
+        x, w = quad.gll(P + 1)
+        assert np.abs(x - G[f"gll_x_{P}"]).max() < 1e-15
+        assert np.abs(w - G[f"gll_w_{P}"]).max() < 1e-15
+        assert rel(quad.diff_matrix(x), G[f"D_{P}"]) < 1e-14
+        assert abs(quad.delta_of_degree(P) - float(G[f"delta_{P}"])) < 1e-12
+    for pc, pf in ((4, 8), (3, 7)):
+        assert rel(quad.lagrange(quad.gll(pc + 1)[0], quad.gll(pf + 1)[0]), G[f"psp_interp_{pc}_{pf}"]) < 1e-14
+        assert rel(quad.lagrange(quad.gll(pf + 1)[0], quad.gll(pc + 1)[0]), G[f"psp_project_{pc}_{pf}"]) < 1e-14
+
+
+@pytest.mark.parametrize("tag,w,ne", [("cfg1", CFG1, CFG1.n_elem), ("cfg2", CFG2, 64)])
+def test_operators(golden, tag, w, ne):
+    G = golden["operators"]
+    for P in (w.p_fine, w.p_coarse):
+        k = f"{tag}_P{P}"
+        op = dg1d.Op1D(w.x_left, w.x_right, ne, P, workloads.make_problem(w), solver="lu")
+        u, fld = G[k + "_u"], G[k + "_fld"]
+        assert rel(op.apply_convection(u), G[k + "_conv"]) < 1e-13
+        assert rel(op.apply_diffusion(0.0137, u), G[k + "_diff_const"]) < 1e-13
+        assert rel(op.apply_diffusion(fld, u), G[k + "_diff_field"]) < 1e-13
+        assert rel(op.eval_rhs(u), G[k + "_rhs"]) < 1e-13
+        assert rel(np.asarray(op.modified_coeff(u, 0.0123, "si2")), G[k + "_modc"]) < 1e-14
+        assert rel(op.mflat + 0.0123 * op.stiffness_diag(fld), G[k + "_diagA_field"]) < 1e-14
+        assert rel(op.mflat + 0.0123 * op.stiffness_diag(0.0137), G[k + "_diagA_const"]) < 1e-14
+        rhs = G[k + "_solve_rhs"]
+        assert rel(op.implicit_solve(0.0137, 0.0123, rhs), G[k + "_solve_const"]) < 1e-12
+        op2 = dg1d.Op1D(w.x_left, w.x_right, ne, P, workloads.make_problem(w), solver="lu")
+        assert rel(op2.implicit_solve(fld, 0.0123, rhs), G[k + "_solve_field"]) < 1e-11
+        op3 = dg1d.Op1D(w.x_left, w.x_right, ne, P, workloads.make_problem(w), solver="pcg")
+        assert rel(op3.implicit_solve(fld, 0.0123, rhs), G[k + "_solve_field"]) < 1e-11
+
+
+def test_cns_matrix_coefficient(golden):
+    G = golden["operators"]
+    op = dg1d.Op1D(0.0, 1.0, 8, 5, dg1d.CNS1D(eta=1e-3))
+    u = G["cns_u"]
+    assert rel(op.apply_convection(u), G["cns_conv"]) < 1e-13
+    assert rel(op.eval_rhs(u), G["cns_rhs"]) < 1e-13
+    assert rel(op.apply_diffusion(G["cns_coeff"], u), G["cns_diff"]) < 1e-13
+    assert rel(op.modified_coeff(u, 0.01, "si2"), G["cns_modc"]) < 1e-13
+
+
+@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2)])
+def test_mlsdc_step_lu_and_pcg(golden, tag, w):
+    """One SI-MLSDC step from the shared golden input: LU restatement vs the
+    reference as shipped; PCG vs the reference with the pinned PCG swapped in
+    (identical CG iteration sequence)."""
+    G = golden["trajectories"]
+    dt = float(G[f"{tag}_dt"])
+    u0 = G[f"{tag}_u0"]
+    assert np.abs(u0 - w.initial_state(workloads.fine_nodes(w))).max() < 1e-14
+    for solver, key, tol in (("lu", "lu", 1e-12), ("pcg", "pcg", 1e-12)):
+        h, log = workloads.build_hierarchy(w, solver=solver)
+        sol = sweeper.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, "fmg")
+        ref = G[f"{tag}_{key}_u1"]
+        assert np.linalg.norm(sol.u[-1] - ref) / np.linalg.norm(ref) < tol
+        assert h.fine_sweeps == 6 and h.coarse_passes == 12
+        if solver == "pcg":
+            assert [it for it, _ in log] == G[f"{tag}_pcg_iters1"].tolist()
+    if tag == "cfg1":
+        assert np.abs(sol.u - G["cfg1_lu_step1_nodes"]).max() < 1e-12
+
+
+def test_single_level_sdc(golden):
+    G = golden["trajectories"]
+    w = CFG1
+    op = dg1d.Op1D(w.x_left, w.x_right, w.n_elem, w.p_fine, workloads.make_problem(w), solver="lu")
+    rule = sweeper.Rule("radau_right", w.m_fine)
+    s = sweeper.run_sdc(op, rule, float(G["cfg1_dt"]), "si2", G["cfg1_u0"], 0.0, 2)
+    # f = eval_rhs(u) amplifies state roundoff by ||D[nu]|| ~ 1e4: looser bound
+    for k, tol in (("u", 1e-13), ("f", 1e-10), ("h1", 1e-12), ("h2", 1e-12)):
+        assert rel(getattr(s, k), G[f"cfg1_sdc2_{k}"]) < tol
