@@ -3,8 +3,8 @@
 
 Workload: BASELINE configs[1] (1-D viscous Burgers, 512 elements, P 8/4,
 M 5/3, nu=5e-3, CFL 1) -- the config the metric is quoted on that fits one
-GPU.  A "step" is one SI-MLSDC time slab (FMG start, 5 V-cycles, closing fine
-sweep: 6 fine sweeps + 12 coarse passes), replayed from a CUDA graph with the
+GPU.  A "step" is one SI-MLSDC time slab (FMG start, 3 V-cycles, closing fine
+sweep: 4 fine sweeps + 8 coarse passes), replayed from a CUDA graph with the
 state resident in HBM.  value = DOF-sweep updates/s summed over ranks.
 
   python bench.py [--gpus N --steps K --warmup W]      # our CUDA path
@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--cpu-sample-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cluster-ctas", type=int, default=0)
+    ap.add_argument("--cycles", type=int, default=None, help="override the V-cycles per step")
     return ap.parse_args()
 
 
@@ -143,6 +144,9 @@ def run_reference(args):
         return 0
     from paper_2504_18526_b200.configs import WORKLOADS
     w = WORKLOADS[args.workload]
+    if args.cycles is not None:
+        import dataclasses
+        w = dataclasses.replace(w, n_cycles=args.cycles)
     cores = os.cpu_count() or 1
     from threadpoolctl import threadpool_limits
     from oracle import sweeper as osw, workloads
@@ -165,7 +169,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name + " (BASELINE configs[1])", "dof_sweeps_per_step": U,
-                   "fine_sweeps_per_step": w.n_cycles + 1, "schedule": "fmg + 5 V-cycles + closing sweep"},
+                   "fine_sweeps_per_step": w.n_cycles + 1,
+                   "schedule": f"fmg + {w.n_cycles} V-cycles + closing sweep"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{args.steps} SI-MLSDC steps of {w.name} after {args.warmup} warm-up steps; "
                                    "oracle restatement of the reference (SuperLU + defect iteration), "
@@ -225,6 +230,9 @@ def run_ours(args):
     from paper_2504_18526_b200.configs import WORKLOADS
     from paper_2504_18526_b200.runtime import get_runtime
     w = WORKLOADS[args.workload]
+    if args.cycles is not None:
+        import dataclasses
+        w = dataclasses.replace(w, n_cycles=args.cycles)
     rt = get_runtime(local)
     rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=args.cluster_ctas)
 
@@ -313,7 +321,8 @@ def run_ours(args):
                 "workload": w.name + " (BASELINE configs[1])",
                 "n_elem": w.n_elem, "degrees": [w.p_coarse, w.p_fine], "nodes": [w.m_coarse, w.m_fine],
                 "dt": dt, "steps_to_t_end": n_total,
-                "schedule": "SI(2) incremental, radau_right, fmg start, 5 V-cycles + closing fine sweep",
+                "schedule": f"SI(2) incremental, radau_right, fmg start, {w.n_cycles} V-cycles + closing fine "
+                            "sweep (5 cycles diverge in the reference itself, DESIGN.md)",
                 "fine_sweeps_per_step": w.n_cycles + 1, "coarse_passes_per_step": 2 + 2 * w.n_cycles,
                 "dof_sweeps_per_step": U, "fine_dof_sweeps_per_s": U_fine * args.steps * world / t_max,
                 "cg_solves_per_step": solves_per_step, "cg_mean_iterations": float(np.mean(step_its)) if len(step_its) else None,

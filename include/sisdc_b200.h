@@ -86,7 +86,8 @@ int  sisdc_ctx_set_cg(sisdc_ctx* ctx, double rtol, int maxit, int cluster_ctas);
 /* Latched device status (syncs): first non-finite element (-1 if none),
  * number of CG failures, number of solves logged since the last reset. */
 int  sisdc_ctx_status(sisdc_ctx* ctx, int* nonfinite_elem, int* cg_failures, int* n_solves);
-int  sisdc_ctx_reset_status(sisdc_ctx* ctx);          /* async, capturable */
+int  sisdc_ctx_reset_status(sisdc_ctx* ctx);          /* failure flags; async, capturable */
+int  sisdc_ctx_reset_log(sisdc_ctx* ctx);             /* flags + CG log counter */
 /* Copy the per-solve CG log (iterations, ||r||/(rtol||b||)) (syncs). */
 int  sisdc_ctx_cg_log(sisdc_ctx* ctx, int cap, int* iters, double* margins, int* n_out);
 /* Number of kernels this context has launched (host-side counter). */

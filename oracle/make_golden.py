@@ -148,7 +148,9 @@ def gen_trajectories():
     """Reference MLSDC steps for cfg1/cfg2: LU (the reference as shipped) and
     with the pinned PCG swapped in (iteration counts logged)."""
     out = {}
-    for tag, w, nsteps in (("cfg1", CFG1, 3), ("cfg2", CFG2, 2)):
+    import dataclasses
+    cfg2c5 = dataclasses.replace(CFG2, n_cycles=5)   # the CLI-default schedule, one step (diverges later)
+    for tag, w, nsteps in (("cfg1", CFG1, 3), ("cfg2", CFG2, 2), ("cfg2c5", cfg2c5, 1)):
         hier, ops = build_ref_hier(w)
         fine = ops[1]
         u0 = w.initial_state(fine.mesh.ref_nodes)
@@ -176,6 +178,8 @@ def gen_trajectories():
                     out[f"{tag}_{rk}_u{s + 1}"] = u
                     out[f"{tag}_{rk}_iters{s + 1}"] = np.array([it for it, _ in pp.log[n0:]])
                     out[f"{tag}_{rk}_margin{s + 1}"] = np.array([mg for _, mg in pp.log[n0:]])
+        if tag == "cfg2c5":
+            continue
         # single-level SDC: predictor + 2 sweeps on the fine level (LU)
         opf = rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine), ref_problem(w))
         rule = rc.make_nodes("radau_right", w.m_fine)

@@ -57,6 +57,7 @@ SIGNATURES = {
     "sisdc_ctx_set_cg": (I, [P, D, I, I]),
     "sisdc_ctx_status": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
     "sisdc_ctx_reset_status": (I, [P]),
+    "sisdc_ctx_reset_log": (I, [P]),
     "sisdc_ctx_cg_log": (I, [P, I, C.POINTER(I), DP, C.POINTER(I)]),
     "sisdc_ctx_launch_count": (C.c_int64, [P]),
     "sisdc_copy": (I, [P, P, P, C.c_int64]),

@@ -10,7 +10,13 @@ config 2, the MLSDC schedule) are pinned here and recorded in DESIGN.md:
 * cfg1: conv-diff, 64 el, P 8/4, M 4/2, a=1, nu=1e-2, CFL 1 on |a|.
 * cfg2: Burgers, 512 el, P 8/4, M 5/3, nu=5e-3, CFL 1 on max|u0|, run to
   t = 1.5 with the reference's step rule n = ceil(t_end/dt0), dt = t_end/n
-  (``cli.py:825-836``).
+  (``cli.py:825-836``), **3 V-cycles** + closing sweep (4 fine sweeps per
+  step).  With the CLI default of 5 (or 4) cycles the reference itself
+  diverges on this hierarchy after 8 (12) steps at any CFL: an interface-jump
+  mode at max|u| is amplified by ~1.75 per V-cycle ("cfg2
+  schedule").  2 and 3 cycles run stably to t = 1.5 and agree to 4e-13; the
+  paper's own Burgers runs converge in 1 cycle + closing sweep at CFL <= 4
+  (PAPER.md:1257-1269).
 """
 from __future__ import annotations
 
@@ -89,6 +95,6 @@ class Workload1D:
 CFG1 = Workload1D("cfg1_convdiff_64el_P8", "convdiff", 64, 8, 4, 4, 2,
                   {"speed": 1.0, "nu": 1e-2}, seed=1, n_steps=100)
 CFG2 = Workload1D("cfg2_burgers_512el_P8", "burgers", 512, 8, 4, 5, 3,
-                  {"nu": 5e-3}, seed=2, t_end=1.5)
+                  {"nu": 5e-3}, seed=2, t_end=1.5, n_cycles=3)
 
 WORKLOADS = {"cfg1": CFG1, "cfg2": CFG2}

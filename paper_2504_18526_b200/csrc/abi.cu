@@ -189,8 +189,14 @@ int sisdc_ctx_status(sisdc_ctx* x, int* nonfinite_elem, int* cg_failures, int* n
 
 int sisdc_ctx_reset_status(sisdc_ctx* x) {
   if (!x) return SISDC_ERR_ARG;
-  k_reset_status<<<1, 32, 0, x->c.stream>>>(x->c.d_status);   // kernel, so it is graph-capturable
+  k_reset_status<<<1, 32, 0, x->c.stream>>>(x->c.d_status, 0);   // kernel, so it is graph-capturable
   return x->c.after_launch("reset_status");
+}
+
+int sisdc_ctx_reset_log(sisdc_ctx* x) {
+  if (!x) return SISDC_ERR_ARG;
+  k_reset_status<<<1, 32, 0, x->c.stream>>>(x->c.d_status, 1);
+  return x->c.after_launch("reset_log");
 }
 
 int sisdc_ctx_cg_log(sisdc_ctx* x, int cap, int* iters, double* margins, int* n_out) {

@@ -3,18 +3,24 @@
 // Replaces the reference's SuperLU solve + defect iteration
 // (dgsem.py:492-533) by the pinned PCG of oracle/cg.py.  The whole solve runs
 // in ONE launch: a thread-block cluster of K <= 16 CTAs (one per SM) owns the
-// elements in contiguous blocks, every CG vector lives in shared memory, the
-// face halo of the search direction is read from the neighbour CTA through
-// distributed shared memory, and the dot products are reduced by pushing
-// per-CTA partials into every CTA's shared memory followed by one hardware
-// cluster barrier.  Two cluster barriers per iteration:
-//   A: p.Ap          B: (r.z, r.r)
-// The neighbour's new search direction is recomputed from its z and previous
-// p with the same fused multiply-add the owner uses (bitwise identical), so no
-// third barrier is needed after the p update.  All reductions run in a fixed
-// order, identical in every CTA: the iteration is deterministic.
+// elements in contiguous blocks, one thread per node.  The iterate x, the
+// residual r, the Jacobi diagonal and the node's operator rows live in
+// registers; the search direction p and the element fluxes q live in shared
+// memory.
+//
+// Inter-CTA traffic is push-only and barrier-free (sm_90+/sm_100a DSMEM):
+//  * dot products: every warp shuffle-reduces its partial and writes it with
+//    st.async into a slot of every CTA of the cluster; the store completes a
+//    transaction count on the RECEIVER's mbarrier.  A CTA waits on its own
+//    mbarrier until all K*nw partials have landed, then every warp sums the
+//    slots in one fixed order -> bitwise-identical totals everywhere.
+//  * face halo: the boundary element's (p_k, z_{k+1}) are pushed with the
+//    r.z partials; the receiver forms p_{k+1} = fma(beta_k, p_k, z_{k+1})
+//    exactly as the owner does.
+// No cluster barrier (and no release fence waiting on remote stores) sits on
+// the iteration's critical path: two mbarrier waits per iteration.
 #include <cooperative_groups.h>
-#include <climits>
+#include <type_traits>
 #include "sisdc_dev.cuh"
 #include "sisdc_host.h"
 
@@ -36,32 +42,31 @@ struct CgArgs {
   int log_cap;
 };
 
-struct CgSmem {
-  double *st, *X, *R, *Z, *AP, *Pb[2], *DG, *C, *Q, *H, *slotA, *slotB, *wscr, *bc;
-};
-
-__device__ __forceinline__ CgSmem carve(double* sm, int p1, int E) {
-  CgSmem s;
-  const int NL = E * p1;
-  s.st = sm;
-  double* q = sm + TabOff::size(p1);
-  s.X = q; q += NL;
-  s.R = q; q += NL;
-  s.Z = q; q += NL;
-  s.AP = q; q += NL;
-  s.Pb[0] = q; q += NL;
-  s.Pb[1] = q; q += NL;
-  s.DG = q; q += NL;
-  s.C = q; q += NL + 2;   // + C at left-halo node P, right-halo node 0
-  s.Q = q; q += NL;
-  s.H = q; q += 4;        // halo: pL, qL, pR, qR
-  s.slotA = q; q += 16 * 4;
-  s.slotB = q; q += 16 * 4;
-  s.wscr = q; q += 32 * 4;
-  s.bc = q; q += 8;
-  return s;
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
 }
-static size_t cg_smem_bytes(int p1, int E) { return sizeof(double) * (TabOff::size(p1) + 9 * E * p1 + 2 + 4 + 128 + 128 + 8); }
+__device__ __forceinline__ void st_async(uint32_t ra, double v, uint32_t rm) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
+               :: "r"(ra), "d"(v), "r"(rm) : "memory");
+}
+__device__ __forceinline__ void st_async2(uint32_t ra, double v0, double v1, uint32_t rm) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               :: "r"(ra), "d"(v0), "d"(v1), "r"(rm) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(m) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(m), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t m, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}"
+               :: "r"(m), "r"(parity) : "memory");
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -69,187 +74,264 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Sum NV values over the whole cluster (or CTA); identical bits in every CTA.
-template <int NV, bool CL>
-__device__ __forceinline__ void cluster_sum(double (&v)[NV], const CgSmem& s, double* slots, int K, int rank) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+// sum_j a[j] b[j] with three interleaved accumulators (shorter FMA chain)
+template <int P1>
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
-  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
-  if (lane == 0)
-#pragma unroll
-    for (int j = 0; j < NV; ++j) s.wscr[wid * 4 + j] = v[j];
-  __syncthreads();
-  if (wid == 0) {
-    double t[NV];
-#pragma unroll
-    for (int j = 0; j < NV; ++j) t[j] = warp_sum(lane < nw ? s.wscr[lane * 4 + j] : 0.0);
-    if constexpr (CL) {
-      if (lane < K) {
-        double* dst = cg::this_cluster().map_shared_rank(slots, lane);
-#pragma unroll
-        for (int j = 0; j < NV; ++j) dst[rank * 4 + j] = t[j];
-      }
-    } else {
-      if (lane == 0)
-#pragma unroll
-        for (int j = 0; j < NV; ++j) s.bc[j] = t[j];
+  for (int j = 0; j < P1; j += 3) {
+    s0 = fma(a[j], b[j], s0);
+    if (j + 1 < P1) s1 = fma(a[j + 1], b[j + 1], s1);
+    if (j + 2 < P1) s2 = fma(a[j + 2], b[j + 2], s2);
+  }
+  return (s0 + s1) + s2;
+}
+
+template <int P1>
+struct CgShared {
+  double* st;
+  double* Pb[2];
+  double* Q;
+  double* Cs;    // own nodes + [NL] = C(left halo, node P), [NL+1] = C(right halo, node 0)
+  double* HX;    // halo x0 [2][P1]
+  double* HPZ;   // halo (p_k, z_{k+1}) pairs [2][P1][2]
+  double* HP;    // halo p_k values formed locally [2][P1]
+  double* slotA;
+  double* slotB;
+  double* wpart;              // per-warp partials [32][4]
+  unsigned long long* mbar;   // [0] A, [1] B, [2] X
+};
+
+template <int P1>
+__device__ __forceinline__ CgShared<P1> carve(double* sm, int E, int K, int nw) {
+  CgShared<P1> s;
+  const int NL = E * P1;
+  double* q = sm;
+  s.mbar = reinterpret_cast<unsigned long long*>(q); q += 4;
+  s.st = q; q += TabOff::size(P1);
+  s.Pb[0] = q; q += NL;
+  s.Pb[1] = q; q += NL;
+  s.Q = q; q += NL;
+  s.Cs = q; q += NL + 2;
+  s.HX = q; q += 2 * P1;
+  q += (q - sm) & 1;   // 16-byte alignment for v2 stores
+  s.HPZ = q; q += 4 * P1;
+  s.HP = q; q += 2 * P1;
+  s.slotB = q; q += 16 * 4;   // 16-byte aligned: receives v2 stores, [rank][NV]
+  s.slotA = q; q += 16;
+  s.wpart = q; q += 32 * 4;
+  return s;
+}
+static size_t cg_smem_bytes(int p1, int E, int K, int nw) {
+  return sizeof(double) * (4 + TabOff::size(p1) + 4 * E * p1 + 2 + 2 * p1 + 1 + 4 * p1 + 2 * p1 + 64 + 16 + 128);
+}
+
+template <bool CL, int P1>
+__global__ void __launch_bounds__(512) k_cg1d(CgArgs A) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int P = P1 - 1;
+  const Op1DDev& op = A.op;
+  int rank = 0;
+  if constexpr (CL) rank = (int)cg::this_cluster().block_rank();
+  const int nw = (blockDim.x + 31) >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const CgShared<P1> s = carve<P1>(sm, A.E, A.K, nw);
+  const int K = A.K;
+  const int e0 = rank * A.E;
+  const int e1 = min(op.ne, e0 + A.E);
+  const int nl = (e1 - e0) * P1, NL = A.E * P1;
+  const int L = threadIdx.x, el = L / P1, i = L - el * P1;
+  const bool own = L < nl;
+  const bool first = el == 0, last = (el + 1) * P1 >= nl;
+  const int egL = wrap(e0 - 1, op.ne), egR = wrap(e1, op.ne);
+  const int rL = egL / A.E, rR = egR / A.E;
+  const uint32_t mA = sa(&s.mbar[0]), mB = sa(&s.mbar[1]), mX = sa(&s.mbar[2]);
+  if (threadIdx.x == 0) {
+    mbar_init(mA);
+    mbar_init(mB);
+    mbar_init(mX);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int t = threadIdx.x; t < TabOff::size(P1); t += blockDim.x) s.st[t] = op.tab[t];
+  double ci = 0.0, rhs = 0.0;
+  if (own) {
+    ci = coef_at(op, A.coef, e0 + el, i);
+    rhs = A.rhs[(size_t)e0 * P1 + L];
+    s.Cs[L] = ci;
+    s.Pb[1][L] = rhs;
+  }
+  if (L == 0) s.Cs[NL] = coef_at(op, A.coef, egL, P);
+  if (L == 1) s.Cs[NL + 1] = coef_at(op, A.coef, egR, 0);
+  if constexpr (CL) cg::this_cluster().sync();   // mbarriers initialised cluster-wide
+  else __syncthreads();
+  // remote addresses this thread pushes to
+  // boundary element threads: first element -> left neighbour's right halo, last -> right neighbour's left halo
+  const bool pushL = own && first, pushR = own && last;
+  uint32_t hxL = 0, hxR = 0, hpzL = 0, hpzR = 0, mBL = 0, mBR = 0, mXL = 0, mXR = 0;
+  if constexpr (CL) {
+    if (pushL) {
+      hxL = mapa(sa(s.HX + P1 + i), rL);
+      hpzL = mapa(sa(s.HPZ + 2 * (P1 + i)), rL);
+      mBL = mapa(mB, rL);
+      mXL = mapa(mX, rL);
+    }
+    if (pushR) {
+      hxR = mapa(sa(s.HX + i), rR);
+      hpzR = mapa(sa(s.HPZ + 2 * i), rR);
+      mBR = mapa(mB, rR);
+      mXR = mapa(mX, rR);
     }
   }
+  uint32_t phA = 0, phB = 0;
+  const uint32_t halo_bytes = 2u * P1 * 16u;
+  // remote slot / mbarrier addresses for warp 0's lanes (lane r pushes to CTA r)
+  uint32_t raA = 0, raB2 = 0, raB4 = 0, rmA = 0, rmB = 0;
   if constexpr (CL) {
-    cg::this_cluster().sync();
+    if (wid == 0 && lane < K) {
+      raA = mapa(sa(s.slotA + rank), lane);
+      raB2 = mapa(sa(s.slotB + 2 * rank), lane);
+      raB4 = mapa(sa(s.slotB + 4 * rank), lane);
+      rmA = mapa(mA, lane);
+      rmB = mapa(mB, lane);
+    }
+  }
+
+  // Cluster sum of NV values: warp shuffles, CTA pre-reduction by warp 0, one
+  // st.async per (CTA, destination CTA) completing on the receiver's mbarrier,
+  // then every warp sums the K slots in rank order (identical bits everywhere).
+  auto csum = [&](auto& v, auto nv_tag, bool useA) {
+    constexpr int NV = decltype(nv_tag)::value;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < NV; ++j) s.wpart[wid * 4 + j] = v[j];
+    __syncthreads();
+    double* slots = useA ? s.slotA : s.slotB;
     if (wid == 0) {
       double t[NV];
 #pragma unroll
-      for (int j = 0; j < NV; ++j) t[j] = warp_sum(lane < K ? slots[lane * 4 + j] : 0.0);
-      if (lane == 0)
+      for (int j = 0; j < NV; ++j) t[j] = warp_sum(lane < nw ? s.wpart[lane * 4 + j] : 0.0);
+      if constexpr (CL) {
+        if (lane < K) {
+          if constexpr (NV == 1) st_async(raA, t[0], rmA);
+          else {
+            const uint32_t ra = NV == 2 ? raB2 : raB4;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) s.bc[j] = t[j];
+            for (int j = 0; j < NV; j += 2) st_async2(ra + 8 * j, t[j], t[j + 1], rmB);
+          }
+        }
+      } else {
+        if (lane == 0)
+#pragma unroll
+          for (int j = 0; j < NV; ++j) slots[j] = t[j];
+      }
     }
-  }
-  __syncthreads();
+    if constexpr (CL) {
+      const uint32_t mb = useA ? mA : mB;
+      if (threadIdx.x == 0) mbar_expect(mb, 8u * K * NV + (useA ? 0u : halo_bytes));
+      mbar_wait(mb, useA ? phA : phB);
+      if (useA) phA ^= 1; else phB ^= 1;
+    } else {
+      __syncthreads();
+    }
 #pragma unroll
-  for (int j = 0; j < NV; ++j) v[j] = s.bc[j];
-}
+    for (int j = 0; j < NV; ++j) v[j] = warp_sum(lane < K ? slots[lane * NV + j] : 0.0);
+  };
 
-template <bool CL>
-__device__ __forceinline__ double* remote(double* p, int r) {
-  if constexpr (CL) return cg::this_cluster().map_shared_rank(p, r);
-  else return p;
-}
-
-// Fetch the halo element values of the search direction into s.H and compute
-// the neighbour face fluxes q.  mode 0: value = src0 (direct);
-// mode 1: value = fma(beta, src1, src0) (neighbour's p_{k} from z_k, p_{k-1}).
-template <bool CL>
-__device__ __forceinline__ void halo_fetch(const CgArgs& A, const CgSmem& s, int rank, int e0, int e1,
-                                           double* own0, double* own1, int mode, double beta) {
-  const Op1DDev& op = A.op;
-  const int p1 = op.p1, P = p1 - 1;
-  const double* D = s.st + TabOff::D(p1);
-  int side = (int)threadIdx.x - ((int)blockDim.x - 2);   // last two threads
-  if (side < 0) return;
-  int eg = side == 0 ? wrap(e0 - 1, op.ne) : wrap(e1, op.ne);
-  int r = eg / A.E, el = eg - r * A.E;
-  const double* s0 = remote<CL>(own0, r) + el * p1;
-  const double* s1 = mode ? remote<CL>(own1, r) + el * p1 : nullptr;
-  int row = side == 0 ? P : 0;   // face node of the neighbour element
-  double g = 0.0, pf = 0.0;
-  for (int j = 0; j < p1; ++j) {
-    double pj = mode ? fma(beta, s1[j], s0[j]) : s0[j];
-    g = fma(D[row * p1 + j], pj, g);
-    if (j == row) pf = pj;
-  }
-  double cf = s.C[A.E * p1 + side];
-  s.H[2 * side] = pf;
-  s.H[2 * side + 1] = cf * (op.s * g);
-}
-
-// Ap = m p + a B[C] p on own nodes; returns the thread's partial p.Ap
-__device__ __forceinline__ double matvec(const CgArgs& A, const CgSmem& s, const double* pv, int nl) {
-  const Op1DDev& op = A.op;
-  const int p1 = op.p1, P = p1 - 1, NL = A.E * p1;
-  const double* D = s.st + TabOff::D(p1);
-  const double* DTW = s.st + TabOff::DTW(p1);
-  const double* ms = s.st + TabOff::m(p1);
-  for (int L = threadIdx.x; L < nl; L += blockDim.x) {
-    int el = L / p1, i = L - el * p1;
-    const double* pe = pv + el * p1;
-    double g = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < p1; ++j) g = fma(D[i * p1 + j], pe[j], g);
-    s.Q[L] = s.C[L] * (op.s * g);
-  }
-  __syncthreads();
-  double part = 0.0;
-  for (int L = threadIdx.x; L < nl; L += blockDim.x) {
-    int el = L / p1, i = L - el * p1, b = el * p1;
-    double B = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < p1; ++k) B = fma(DTW[i * p1 + k], s.Q[b + k], B);
-    const bool last = (b + p1 >= nl), first = (b == 0);
-    double pn = last ? s.H[2] : pv[b + p1], qn = last ? s.H[3] : s.Q[b + p1], cn = last ? s.C[NL + 1] : s.C[b + p1];
-    double pp = first ? s.H[0] : pv[b - 1], qp = first ? s.H[1] : s.Q[b - 1], cp = first ? s.C[NL] : s.C[b - 1];
-    double jr = pv[b + P] - pn;
-    double jl = pp - pv[b];
-    if (i == P) B += -(0.5 * (s.Q[b + P] + qn)) + (op.mu0 * (0.5 * (s.C[b + P] + cn))) * jr;
-    if (i == 0) B -= -(0.5 * (qp + s.Q[b])) + (op.mu0 * (0.5 * (cp + s.C[b]))) * jl;
-    B -= (op.s * ((0.5 * s.C[b + P]) * jr)) * D[P * p1 + i];
-    B -= (op.s * ((0.5 * s.C[b]) * jl)) * D[i];
-    double ap = fma(A.a, B, ms[i] * pv[L]);
-    s.AP[L] = ap;
-    part = fma(pv[L], ap, part);
-  }
-  return part;
-}
-
-template <bool CL>
-__global__ void __launch_bounds__(1024) k_cg1d(CgArgs A) {
-  extern __shared__ double sm[];
-  const Op1DDev& op = A.op;
-  const int p1 = op.p1, P = p1 - 1;
-  int rank = 0;
-  if constexpr (CL) rank = (int)cg::this_cluster().block_rank();
-  const CgSmem s = carve(sm, p1, A.E);
-  const int e0 = rank * A.E;
-  const int e1 = min(op.ne, e0 + A.E);
-  const int nl = (e1 - e0) * p1, NL = A.E * p1;
-  load_tab(s.st, op.tab, p1);
-  __syncthreads();
-  const double* ms = s.st + TabOff::m(p1);
-  const double* D = s.st + TabOff::D(p1);
-  const double* D2W = s.st + TabOff::D2W(p1);
-  // ---- setup: x0 = rhs, coefficient, Jacobi diagonal, zero p_{-1}
-  for (int L = threadIdx.x; L < NL; L += blockDim.x) {
-    int el = L / p1, i = L - el * p1;
-    bool own = L < nl;
-    s.X[L] = own ? A.rhs[(size_t)e0 * p1 + L] : 0.0;
-    s.C[L] = own ? coef_at(op, A.coef, e0 + el, i) : 0.0;
-    s.Pb[1][L] = 0.0;
-  }
-  if (threadIdx.x == 0) s.C[NL] = coef_at(op, A.coef, wrap(e0 - 1, op.ne), P);
-  if (threadIdx.x == 1) s.C[NL + 1] = coef_at(op, A.coef, wrap(e1, op.ne), 0);
-  __syncthreads();
-  for (int L = threadIdx.x; L < nl; L += blockDim.x) {
-    int el = L / p1, i = L - el * p1, b = el * p1;
+  const double* D = s.st + TabOff::D(P1);
+  const double* DTW = s.st + TabOff::DTW(P1);
+  const double mi = s.st[TabOff::m(P1) + i];
+  const double sc = op.s, mu0 = op.mu0, a = A.a;
+  const double cR = last ? s.Cs[NL + 1] : s.Cs[min((el + 1) * P1, NL - 1)];
+  const double cL = first ? s.Cs[NL] : s.Cs[max(el * P1 - 1, 0)];
+  const double cP = s.Cs[min(el * P1 + P, NL - 1)], c0 = s.Cs[min(el * P1, NL - 1)];
+  double dg = 1.0;
+  if (own) {   // Jacobi diagonal diag(M + a B[C]) (closed form of dgsem.py:414-490)
     double d = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < p1; ++k) d = fma(D2W[i * p1 + k], s.C[b + k], d);
-    d = op.s * d;
+#pragma unroll
+    for (int k = 0; k < P1; ++k) d = fma(s.st[TabOff::D2W(P1) + i * P1 + k], s.Cs[el * P1 + k], d);
+    d = sc * d;
+    if (i == P) d += mu0 * (0.5 * (cP + cR)) - sc * cP * D[P * P1 + P];
+    if (i == 0) d += mu0 * (0.5 * (cL + c0)) + sc * c0 * D[0];
+    dg = mi + a * d;
+  }
+  const double dinv = 1.0 / dg;   // Jacobi: z = r * dinv
+  // per-node face constants of the SIP operator (dgsem.py:290-308)
+  const double muR = mu0 * (0.5 * (cP + cR)), muL = mu0 * (0.5 * (cL + c0));
+  const double kR = sc * (0.5 * cP), kL = sc * (0.5 * c0);
+  const double DPi = D[P * P1 + i], D0i = D[i];
+
+  // A v on own nodes; halo element values of v in hv[0..P1) (left), hv[P1..2P1) (right)
+  auto matvec = [&](const double* v, const double* hv) -> double {
+    if (own) {
+      const double* ve = v + el * P1;
+      s.Q[L] = ci * (sc * dot3<P1>(D + i * P1, ve));
+    }
+    __syncthreads();
+    if (!own) return 0.0;
+    const int b = el * P1;
+    double B = dot3<P1>(DTW + i * P1, s.Q + b);
+    const double pn = last ? hv[P1] : v[b + P1];
+    const double pp = first ? hv[P] : v[b - 1];
+    const double jr = v[b + P] - pn;
+    const double jl = pp - v[b];
     if (i == P) {
-      double cn = (b + p1 >= nl) ? s.C[NL + 1] : s.C[b + p1];
-      d += op.mu0 * (0.5 * (s.C[b + P] + cn)) - op.s * s.C[b + P] * D[P * p1 + P];
+      const double qn = last ? cR * (sc * dot3<P1>(D, hv + P1)) : s.Q[b + P1];
+      B += -(0.5 * (s.Q[b + P] + qn)) + muR * jr;
     }
     if (i == 0) {
-      double cp = (b == 0) ? s.C[NL] : s.C[b - 1];
-      d += op.mu0 * (0.5 * (cp + s.C[b])) + op.s * s.C[b] * D[0];
+      const double qp = first ? cL * (sc * dot3<P1>(D + P * P1, hv)) : s.Q[b - 1];
+      B -= -(0.5 * (qp + s.Q[b])) + muL * jl;
     }
-    s.DG[L] = ms[i] + A.a * d;
+    B -= (kR * jr) * DPi;
+    B -= (kL * jl) * D0i;
+    return fma(a, B, mi * v[L]);
+  };
+
+  // ---- r = b - A x0: exchange the x0 halo
+  const double* hx;
+  if constexpr (CL) {
+    if (threadIdx.x == 0) mbar_expect(mX, 2u * P1 * 8u);
+    if (pushL) st_async(hxL, rhs, mXL);
+    if (pushR) st_async(hxR, rhs, mXR);
+    mbar_wait(mX, 0);
+    hx = s.HX;
+  } else {
+    // single CTA, periodic: halo elements are this CTA's last / first element
+    if (L < 2 * P1) {
+      const int side = L / P1, j = L - side * P1;
+      s.HX[L] = s.Pb[1][(side ? 0 : (nl - P1)) + j];
+    }
+    __syncthreads();
+    hx = s.HX;
   }
-  if constexpr (CL) cg::this_cluster().sync(); else __syncthreads();
-  // r = b - A x0 (halo of x0 read directly: stable after the barrier)
-  halo_fetch<CL>(A, s, rank, e0, e1, s.X, nullptr, 0, 0.0);
-  __syncthreads();
-  matvec(A, s, s.X, nl);
-  double v4[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int L = threadIdx.x; L < nl; L += blockDim.x) {
-    int i = L % p1;
-    double b = ms[i] * A.rhs[(size_t)e0 * p1 + L];
-    double r = b - s.AP[L];
-    double z = r / s.DG[L];
-    s.R[L] = r;
-    s.Z[L] = z;
-    s.Pb[0][L] = z;   // p_0 = fma(0, p_{-1} = 0, z_0)
-    v4[0] = fma(r, z, v4[0]);
-    v4[1] = fma(r, r, v4[1]);
-    v4[2] = fma(b, b, v4[2]);
-    v4[3] += (b != 0.0) ? 1.0 : 0.0;
-  }
-  cluster_sum<4, CL>(v4, s, s.slotB, A.K, rank);
+  double x = rhs;
+  const double ax = matvec(s.Pb[1], hx);
+  const double b = mi * rhs;
+  double r = b - ax;
+  double z = r * dinv;
+  if (own) s.Pb[0][L] = z;   // p_0 = z_0 = fma(0, p_{-1} = 0, z_0)
+  // halo push (p_{-1} = 0, z_0) with the setup reduction
+  auto push_halo = [&](double pk, double zk) {
+    if constexpr (CL) {
+      if (pushL) st_async2(hpzL, pk, zk, mBL);
+      if (pushR) st_async2(hpzR, pk, zk, mBR);
+    } else {
+      if (L < nl && (first || last)) {
+        // local halo: my first element is my own right halo, last element my left halo
+        if (first) { s.HPZ[2 * (P1 + i)] = pk; s.HPZ[2 * (P1 + i) + 1] = zk; }
+        if (last) { s.HPZ[2 * i] = pk; s.HPZ[2 * i + 1] = zk; }
+      }
+    }
+  };
+  push_halo(0.0, z);
+  double v4[4] = {own ? r * z : 0.0, own ? r * r : 0.0, own ? b * b : 0.0, (own && b != 0.0) ? 1.0 : 0.0};
+  csum(v4, std::integral_constant<int, 4>{}, false);
   double rz = v4[0], rr = v4[1];
   const double thr = A.rtol2 * v4[2];
   if (v4[3] == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
-    for (int L = threadIdx.x; L < nl; L += blockDim.x) A.x[(size_t)e0 * p1 + L] = 0.0;
-    if constexpr (CL) cg::this_cluster().sync();
+    if (own) A.x[(size_t)e0 * P1 + L] = 0.0;
     return;
   }
   int k = 0;
@@ -259,32 +341,29 @@ __global__ void __launch_bounds__(1024) k_cg1d(CgArgs A) {
     if (k >= A.maxit) { ok = false; break; }
     double* pc = s.Pb[k & 1];
     double* po = s.Pb[(k + 1) & 1];
-    // halo p_k of the neighbours = fma(beta_{k-1}, p_{k-1}, z_k)
-    halo_fetch<CL>(A, s, rank, e0, e1, s.Z, po, 1, beta);
-    double v1[1] = {matvec(A, s, pc, nl)};
-    cluster_sum<1, CL>(v1, s, s.slotA, A.K, rank);
+    // neighbour p_k = fma(beta_{k-1}, p_{k-1}, z_k) from the pushed pairs
+    if (L < 2 * P1) s.HP[L] = fma(beta, s.HPZ[2 * L], s.HPZ[2 * L + 1]);
+    // (matvec's first __syncthreads orders HP before its use)
+    const double ap = matvec(pc, s.HP);
+    const double pk = own ? pc[L] : 0.0;
+    double v1[1] = {pk * ap};
+    csum(v1, std::integral_constant<int, 1>{}, true);
     const double alpha = rz / v1[0];
-    double v2[2] = {0.0, 0.0};
-    for (int L = threadIdx.x; L < nl; L += blockDim.x) {
-      double p = pc[L];
-      s.X[L] = fma(alpha, p, s.X[L]);
-      double r = fma(-alpha, s.AP[L], s.R[L]);
-      double z = r / s.DG[L];
-      s.R[L] = r;
-      s.Z[L] = z;
-      v2[0] = fma(r, z, v2[0]);
-      v2[1] = fma(r, r, v2[1]);
-    }
-    cluster_sum<2, CL>(v2, s, s.slotB, A.K, rank);
+    x = fma(alpha, pk, x);
+    r = fma(-alpha, ap, r);
+    z = r * dinv;
+    push_halo(pk, z);
+    double v2[2] = {own ? r * z : 0.0, own ? r * r : 0.0};
+    csum(v2, std::integral_constant<int, 2>{}, false);
     beta = v2[0] / rz;
     rz = v2[0];
     rr = v2[1];
     ++k;
     if (rr <= thr) break;
-    for (int L = threadIdx.x; L < nl; L += blockDim.x) po[L] = fma(beta, pc[L], s.Z[L]);
+    if (own) po[L] = fma(beta, pk, z);
     __syncthreads();
   }
-  for (int L = threadIdx.x; L < nl; L += blockDim.x) A.x[(size_t)e0 * p1 + L] = s.X[L];
+  if (own) A.x[(size_t)e0 * P1 + L] = x;
   if (rank == 0 && threadIdx.x == 0) {
     int idx = atomicAdd(&A.status[2], 1);
     if (idx < A.log_cap) {
@@ -293,64 +372,87 @@ __global__ void __launch_bounds__(1024) k_cg1d(CgArgs A) {
     }
     if (!ok) atomicAdd(&A.status[1], 1);
   }
-  // keep every CTA's shared memory alive until remote readers are done
-  if constexpr (CL) cg::this_cluster().sync();
 }
 
-// Cluster size: about 576 nodes per CTA (one thread per node), at most 16
-// CTAs (non-portable cluster), enough CTAs for the vectors to fit in 200 KB.
-static void choose_partition(const Ctx* c, int ne, int p1, int& K, int& E) {
-  K = c->cluster_ctas > 0 ? c->cluster_ctas : (ne * p1 + 575) / 576;
-  K = K < 1 ? 1 : (K > 16 ? 16 : K);
+// Partition: one thread per node, at most 512 nodes per CTA and 16 CTAs.
+static int choose_partition(const Ctx* c, int ne, int p1, int& K, int& E) {
+  int want = c->cluster_ctas > 0 ? c->cluster_ctas : (ne * p1 + 287) / 288;   // ~288 nodes per CTA
+  K = want < 1 ? 1 : (want > 16 ? 16 : want);
   if (K > ne) K = ne;
   for (;;) {
     E = (ne + K - 1) / K;
     K = (ne + E - 1) / E;   // no empty CTA
-    if (cg_smem_bytes(p1, E) <= 200 * 1024 || K >= 16 || K >= ne) break;
+    if (E * p1 <= 512 || K >= 16 || K >= ne) break;
     ++K;
   }
+  return E * p1 <= 512 ? 0 : -1;
 }
 
-int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x) {
-  const int p1 = op.p1;
-  int K, E;
-  choose_partition(c, op.ne, p1, K, E);
-  size_t smem = cg_smem_bytes(p1, E);
-  if (smem > 227 * 1024)
-    return c->fail(SISDC_ERR_UNSUPPORTED, "implicit_solve: level too large for the cluster-resident CG "
-                                          "(n_elem*(P+1) beyond 16 CTAs of shared memory)");
-  CgArgs A{};
-  A.op = op; A.coef = k; A.a = a; A.rhs = rhs; A.x = x;
-  A.rtol2 = c->rtol * c->rtol; A.maxit = c->maxit; A.E = E; A.K = K;
-  A.status = c->d_status; A.log_it = c->d_log_it; A.log_margin = c->d_log_margin; A.log_cap = c->log_cap;
-  int threads = E * p1;
-  threads = threads > 1024 ? 1024 : ((threads + 31) / 32) * 32;
-  if (threads < 64) threads = 64;
-  if (K == 1) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg1d<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return c->cuda(e, "cg1d smem attribute");
-    k_cg1d<false><<<1, threads, smem, c->stream>>>(A);
+template <int P1>
+static int launch_cg_t(Ctx* c, CgArgs& A, int threads, size_t smem) {
+  static bool attr_done[2] = {false, false};
+  if (A.K == 1) {
+    if (!attr_done[0]) {
+      cudaFuncSetAttribute(k_cg1d<false, P1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr_done[0] = true;
+    }
+    k_cg1d<false, P1><<<1, threads, smem, c->stream>>>(A);
     return c->after_launch("cg1d");
   }
-  cudaError_t e = cudaFuncSetAttribute(k_cg1d<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return c->cuda(e, "cg1d smem attribute");
-  e = cudaFuncSetAttribute(k_cg1d<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e != cudaSuccess) return c->cuda(e, "cg1d cluster attribute");
+  if (!attr_done[1]) {
+    cudaFuncSetAttribute(k_cg1d<true, P1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_cg1d<true, P1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_done[1] = true;
+  }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(K);
+  cfg.gridDim = dim3(A.K);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = K;
+  at[0].val.clusterDim.x = A.K;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, k_cg1d<true>, A);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_cg1d<true, P1>, A);
   if (e != cudaSuccess) return c->cuda(e, "cg1d cluster launch");
   return c->after_launch("cg1d");
+}
+
+int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x) {
+  const int p1 = op.p1;
+  int K, E;
+  if (choose_partition(c, op.ne, p1, K, E))
+    return c->fail(SISDC_ERR_UNSUPPORTED, "implicit_solve: level too large for the cluster-resident CG "
+                                          "(more than 16 CTAs x 512 nodes)");
+  int threads = ((E * p1 + 31) / 32) * 32;
+  if (threads < 64) threads = 64;
+  const int nw = threads / 32;
+  size_t smem = cg_smem_bytes(p1, E, K, nw);
+  CgArgs A{};
+  A.op = op; A.coef = k; A.a = a; A.rhs = rhs; A.x = x;
+  A.rtol2 = c->rtol * c->rtol; A.maxit = c->maxit; A.E = E; A.K = K;
+  A.status = c->d_status; A.log_it = c->d_log_it; A.log_margin = c->d_log_margin; A.log_cap = c->log_cap;
+  switch (p1) {
+    case 2: return launch_cg_t<2>(c, A, threads, smem);
+    case 3: return launch_cg_t<3>(c, A, threads, smem);
+    case 4: return launch_cg_t<4>(c, A, threads, smem);
+    case 5: return launch_cg_t<5>(c, A, threads, smem);
+    case 6: return launch_cg_t<6>(c, A, threads, smem);
+    case 7: return launch_cg_t<7>(c, A, threads, smem);
+    case 8: return launch_cg_t<8>(c, A, threads, smem);
+    case 9: return launch_cg_t<9>(c, A, threads, smem);
+    case 10: return launch_cg_t<10>(c, A, threads, smem);
+    case 11: return launch_cg_t<11>(c, A, threads, smem);
+    case 12: return launch_cg_t<12>(c, A, threads, smem);
+    case 13: return launch_cg_t<13>(c, A, threads, smem);
+    case 14: return launch_cg_t<14>(c, A, threads, smem);
+    case 15: return launch_cg_t<15>(c, A, threads, smem);
+    case 16: return launch_cg_t<16>(c, A, threads, smem);
+    default: return c->fail(SISDC_ERR_UNSUPPORTED, "degree outside 1..15");
+  }
 }
 
 }  // namespace sisdc

@@ -347,8 +347,8 @@ __global__ void k_persson(Op1DDev op, const double* __restrict__ u, double kappa
   nu_art[e] = eps0 * ramp;
 }
 
-__global__ void k_reset_status(int* status) {
-  if (threadIdx.x == 0) { status[0] = 0x7fffffff; status[1] = 0; status[2] = 0; status[3] = 0; }
+__global__ void k_reset_status(int* status, int reset_log) {
+  if (threadIdx.x == 0) { status[0] = 0x7fffffff; status[1] = 0; if (reset_log) status[2] = 0; }
 }
 
 // ------------------------------------------------------------ launchers

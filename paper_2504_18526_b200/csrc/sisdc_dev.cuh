@@ -184,6 +184,6 @@ __host__ __device__ inline int xo_Psp(const XferDev& x) { return 2 * x.Mf * x.Mc
 __host__ __device__ inline int xo_size(const XferDev& x) { return 2 * x.Mf * x.Mc + 2 * x.pf * x.pc; }
 
 
-__global__ void k_reset_status(int* status);
+__global__ void k_reset_status(int* status, int reset_log);
 
 }  // namespace sisdc

@@ -117,8 +117,11 @@ def test_implicit_solve_edge_cases(rt):
 
 
 def test_nonfinite_rhs_reports_element(rt):
+    """Mirror of test_dgsem.py:395-403: pure convection, NaN at an interior
+    node of element 5 -> SolverError naming element 5."""
+    from paper_2504_18526_b200 import dgsem, problems
     from paper_2504_18526_b200.dgsem import SolverError
-    op = gpu_op(CFG1, 3, 8)
+    op = dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, 8, 3), problems.ConvectionDiffusion(1.0, 0.0))
     u = np.zeros(op.ndof)
     u[5 * 4 + 1] = np.nan
     with pytest.raises(SolverError, match="element 5"):
@@ -154,13 +157,17 @@ def test_predict_and_sweeps_vs_oracle(rt, golden, tag, w):
     its, _ = new_log_slice(rt, n0)
     assert its == [it for it, _ in log]
     assert l2rel(s.u, so.u) < 1e-12
-    assert rel(s.f, so.f) < 1e-10
+    # f = eval_rhs(u) amplifies state roundoff by ||D[nu]|| (~4e3 cfg1, ~2e6 cfg2)
+    assert rel(s.f, so.f) < (1e-10 if tag == "cfg1" else 1e-8)
     assert rel(s.h1, so.h1) < 1e-12 and rel(s.h2, so.h2) < 1e-12
     F = sdc.collocation_defect(rule, wts, dt, s, ctx=op)
     assert rel(F, osw.defect(orule, dt, so)) < 1e-11
 
 
-@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2)])
+CFG2C5 = __import__("dataclasses").replace(CFG2, n_cycles=5)
+
+
+@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2), ("cfg2c5", CFG2C5)])
 def test_mlsdc_step_parity(rt, golden, tag, w):
     """One SI-MLSDC step from the golden input: <= 1e-11 rel L2 against the
     reference (LU as shipped, and with the pinned PCG), identical CG
@@ -169,7 +176,8 @@ def test_mlsdc_step_parity(rt, golden, tag, w):
     G = golden["trajectories"]
     dt = float(G[f"{tag}_dt"])
     h = gpu_hier(w)
-    for step in (1, 2):
+    steps = (1,) if tag == "cfg2c5" else (1, 2)
+    for step in steps:
         uin = G[f"{tag}_u0"] if step == 1 else G[f"{tag}_pcg_u1"]
         n0 = rt.status()[2]
         sol = mlsdc.run_mlsdc(h, uin, (step - 1) * dt, dt, w.n_cycles, strategy="fmg")
@@ -178,7 +186,7 @@ def test_mlsdc_step_parity(rt, golden, tag, w):
         assert l2rel(sol.u[-1], G[f"{tag}_pcg_u{step}"]) < 1e-11
         if step == 1:
             assert l2rel(sol.u[-1], G[f"{tag}_lu_u1"]) < 1e-11
-    assert h.fine_sweeps == 12 and h.coarse_passes == 24
+    assert h.fine_sweeps == len(steps) * (w.n_cycles + 1) and h.coarse_passes == len(steps) * (2 + 2 * w.n_cycles)
     rt.raise_on_failure()
 
 

@@ -51,7 +51,7 @@ def test_workloads(golden):
         if tag == "cfg2":
             assert n == int(G["cfg2_nsteps_total"]) and abs(n * dt - 1.5) < 1e-12
     assert CFG1.dof_sweeps_per_step()[0] == 576 * 4 * 6 + 320 * 2 * 12
-    assert CFG2.dof_sweeps_per_step()[0] == 4608 * 5 * 6 + 2560 * 3 * 12
+    assert CFG2.dof_sweeps_per_step()[0] == 4608 * 5 * 4 + 2560 * 3 * 8
 
 
 def test_mesh_validation():

@@ -63,7 +63,10 @@ def test_cns_matrix_coefficient(golden):
     assert rel(op.modified_coeff(u, 0.01, "si2"), G["cns_modc"]) < 1e-13
 
 
-@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2)])
+CFG2C5 = __import__("dataclasses").replace(CFG2, n_cycles=5)
+
+
+@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2), ("cfg2c5", CFG2C5)])
 def test_mlsdc_step_lu_and_pcg(golden, tag, w):
     """One SI-MLSDC step from the shared golden input: LU restatement vs the
     reference as shipped; PCG vs the reference with the pinned PCG swapped in
@@ -77,7 +80,7 @@ def test_mlsdc_step_lu_and_pcg(golden, tag, w):
         sol = sweeper.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, "fmg")
         ref = G[f"{tag}_{key}_u1"]
         assert np.linalg.norm(sol.u[-1] - ref) / np.linalg.norm(ref) < tol
-        assert h.fine_sweeps == 6 and h.coarse_passes == 12
+        assert h.fine_sweeps == w.n_cycles + 1 and h.coarse_passes == 2 + 2 * w.n_cycles
         if solver == "pcg":
             assert [it for it, _ in log] == G[f"{tag}_pcg_iters1"].tolist()
     if tag == "cfg1":
