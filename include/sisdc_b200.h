@@ -90,6 +90,10 @@ int  sisdc_ctx_reset_status(sisdc_ctx* ctx);          /* failure flags; async, c
 int  sisdc_ctx_reset_log(sisdc_ctx* ctx);             /* flags + CG log counter */
 /* Copy the per-solve CG log (iterations, ||r||/(rtol||b||)) (syncs). */
 int  sisdc_ctx_cg_log(sisdc_ctx* ctx, int cap, int* iters, double* margins, int* n_out);
+/* Diagnostics: clock64 stamps of the last implicit solve's CTA 0 (setup
+ * milestones [0..3], end of iteration k at [4+k], end [64], iterations [65]);
+ * needs SISDC_CG_TIMING=1 in the environment when the context is created. */
+int  sisdc_ctx_debug_timing(sisdc_ctx* ctx, long long* out, int cap);
 /* Number of kernels this context has launched (host-side counter). */
 int64_t sisdc_ctx_launch_count(const sisdc_ctx* ctx);
 int  sisdc_copy(sisdc_ctx* ctx, double* dst, const double* src, int64_t n);  /* D2D, async */

@@ -6,7 +6,8 @@ Writes tests/golden/*.npz.  The reference package is imported read-only from
 /root/reference/pkg/src; nothing from it is copied into the repo -- only its
 numerical outputs on seeded inputs.  The CG-trajectory goldens run the
 reference's own sdc/mlsdc code with ``DGOperator.implicit_solve`` replaced by
-the pinned PCG of ``oracle/cg.py`` (the north star's CG formulation).
+the pinned PCG of ``oracle/cg.py`` (the north star's CG formulation); the
+two-reduction Hestenes-Stiefel form is recorded too (``*_hs_iters*``).
 """
 from __future__ import annotations
 
@@ -22,7 +23,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from sisdc import collocation as rc, dgsem as rd, mlsdc as rm, problems as rp, sdc as rs, transfer as rt  # noqa: E402
 
-from oracle.cg import pcg  # noqa: E402
+from oracle.cg import pcg, pcg_hs  # noqa: E402
 from paper_2504_18526_b200.configs import CFG1, CFG2  # noqa: E402
 
 OUT = os.path.join(REPO, "tests", "golden")
@@ -49,8 +50,9 @@ def build_ref_hier(w):
 class PcgPatch:
     """Swap DGOperator.implicit_solve for the pinned PCG; log iterations."""
 
-    def __init__(self, rtol=1e-14):
+    def __init__(self, rtol=1e-14, solver=pcg):
         self.rtol = rtol
+        self.solver = solver
         self.log = []
         self._orig = rd.DGOperator.implicit_solve
 
@@ -68,7 +70,7 @@ class PcgPatch:
             Amat = op.assemble_implicit(coeff, a)
             diag = np.asarray(Amat.diagonal())
             A = lambda x: m * x - a * m * op.apply_diffusion(coeff, x, t)
-            x, it, margin = pcg(A, diag, b, rhs.reshape(-1).copy(), patch.rtol, 1000)
+            x, it, margin = patch.solver(A, diag, b, rhs.reshape(-1).copy(), patch.rtol, 1000)
             assert it >= 0
             patch.log.append((it, margin))
             return x.reshape(rhs.shape)
@@ -167,9 +169,9 @@ def gen_trajectories():
             u = sol.end_value.copy()
             out[f"{tag}_lu_u{s + 1}"] = u
         # PCG trajectory (reference sweeps/cycles, pinned PCG solve)
-        for rtol, rk in ((1e-14, "pcg"), (1e-13, "pcg13")):
+        for rtol, rk, solver in ((1e-14, "pcg", pcg), (1e-13, "pcg13", pcg), (1e-14, "hs", pcg_hs)):
             hier, ops = build_ref_hier(w)
-            with PcgPatch(rtol) as pp:
+            with PcgPatch(rtol, solver) as pp:
                 u = u0
                 for s in range(nsteps):
                     n0 = len(pp.log)

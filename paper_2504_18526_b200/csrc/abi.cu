@@ -1,6 +1,7 @@
 // C ABI of libsisdc_b200.so: contexts, operators, transfers and the exported
 // OperatorContext / sweep-stage entry points (include/sisdc_b200.h).
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -139,6 +140,8 @@ int sisdc_ctx_create(int device, sisdc_ctx** out) {
     delete x;
     return SISDC_ERR_CUDA;
   }
+  const char* tm = getenv("SISDC_CG_TIMING");
+  if (e == cudaSuccess && tm && tm[0] == '1') e = cudaMalloc(&c.d_timing, 80 * sizeof(long long));
   int init[4] = {INT_MAX, 0, 0, 0};
   cudaMemcpy(c.d_status, init, sizeof(init), cudaMemcpyHostToDevice);
   *out = x;
@@ -150,6 +153,7 @@ void sisdc_ctx_destroy(sisdc_ctx* x) {
   cudaFree(x->c.d_status);
   cudaFree(x->c.d_log_it);
   cudaFree(x->c.d_log_margin);
+  cudaFree(x->c.d_timing);
   delete x;
 }
 
@@ -210,6 +214,15 @@ int sisdc_ctx_cg_log(sisdc_ctx* x, int cap, int* iters, double* margins, int* n_
   if (!rc && m > 0 && margins)
     rc = x->c.cuda(cudaMemcpy(margins, x->c.d_log_margin, m * sizeof(double), cudaMemcpyDeviceToHost), "log");
   if (n_out) *n_out = n;
+  return rc;
+}
+
+int sisdc_ctx_debug_timing(sisdc_ctx* x, long long* out, int cap) {
+  if (!x || !out || cap < 0) return SISDC_ERR_ARG;
+  if (!x->c.d_timing) return x->c.fail(SISDC_ERR_UNSUPPORTED, "set SISDC_CG_TIMING=1 before creating the context");
+  int n = cap < 80 ? cap : 80;
+  int rc = x->c.cuda(cudaStreamSynchronize(x->c.stream), "timing sync");
+  if (!rc) rc = x->c.cuda(cudaMemcpy(out, x->c.d_timing, n * sizeof(long long), cudaMemcpyDeviceToHost), "timing");
   return rc;
 }
 

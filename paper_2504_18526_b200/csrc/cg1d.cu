@@ -1,24 +1,25 @@
 // Cluster-resident Jacobi-PCG for the implicit substep (M + a B[C]) x = M rhs.
 //
 // Replaces the reference's SuperLU solve + defect iteration
-// (dgsem.py:492-533) by the pinned PCG of oracle/cg.py.  The whole solve runs
-// in ONE launch: a thread-block cluster of K <= 16 CTAs (one per SM) owns the
-// elements in contiguous blocks, one thread per node.  The iterate x, the
-// residual r, the Jacobi diagonal and the node's operator rows live in
-// registers; the search direction p and the element fluxes q live in shared
-// memory.
+// (dgsem.py:492-533) by the pinned PCG of oracle/cg.py (Chronopoulos-Gear
+// form: the Hestenes-Stiefel iterates with ONE fused reduction per iteration,
+// (gamma, delta, rho) = ((r,u), (w,u), (r,r)) with u = D^-1 r, w = A u).
 //
-// Inter-CTA traffic is push-only and barrier-free (sm_90+/sm_100a DSMEM):
-//  * dot products: every warp shuffle-reduces its partial and writes it with
-//    st.async into a slot of every CTA of the cluster; the store completes a
-//    transaction count on the RECEIVER's mbarrier.  A CTA waits on its own
-//    mbarrier until all K*nw partials have landed, then every warp sums the
-//    slots in one fixed order -> bitwise-identical totals everywhere.
-//  * face halo: the boundary element's (p_k, z_{k+1}) are pushed with the
-//    r.z partials; the receiver forms p_{k+1} = fma(beta_k, p_k, z_{k+1})
-//    exactly as the owner does.
-// No cluster barrier (and no release fence waiting on remote stores) sits on
-// the iteration's critical path: two mbarrier waits per iteration.
+// The whole solve runs in ONE launch: a thread-block cluster of K <= 16 CTAs
+// (one per SM) owns the elements in contiguous blocks, one thread per node.
+// x, r, u, w, p, s and the Jacobi reciprocal live in registers; u (read by
+// the element contraction) and the element fluxes q live in shared memory.
+//
+// Inter-CTA traffic is push-only (sm_90+/sm_100a DSMEM):
+//  * the reduction: warps shuffle-reduce, warp 0 pre-reduces the CTA and
+//    writes it with st.async into a slot of every CTA of the cluster; each
+//    store completes a transaction count on the RECEIVER's mbarrier.  After
+//    its own mbarrier phase completes a CTA sums the K slots in rank order
+//    -> bitwise-identical scalars everywhere, no cluster barrier.
+//  * the face halo: boundary nodes push (r, w, s) with the partials; the
+//    receiver forms s' = fma(beta, s, w), r' = fma(-alpha, s', r), u' = r' dinv
+//    with exactly the owner's operations, so u's halo needs no extra exchange.
+// One mbarrier wait per iteration; slot/halo buffers alternate by parity.
 #include <cooperative_groups.h>
 #include <type_traits>
 #include "sisdc_dev.cuh"
@@ -40,6 +41,7 @@ struct CgArgs {
   int* log_it;
   double* log_margin;
   int log_cap;
+  long long* timing;   // diagnostics: clock64 stamps of CTA 0 (nullable)
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -87,47 +89,62 @@ __device__ __forceinline__ double dot3(const double* a, const double* b) {
   return (s0 + s1) + s2;
 }
 
-template <int P1>
-struct CgShared {
-  double* st;
-  double* Pb[2];
-  double* Q;
-  double* Cs;    // own nodes + [NL] = C(left halo, node P), [NL+1] = C(right halo, node 0)
-  double* HX;    // halo x0 [2][P1]
-  double* HPZ;   // halo (p_k, z_{k+1}) pairs [2][P1][2]
-  double* HP;    // halo p_k values formed locally [2][P1]
-  double* slotA;
-  double* slotB;
-  double* wpart;              // per-warp partials [32][4]
-  unsigned long long* mbar;   // [0] A, [1] B, [2] X
-};
+constexpr int NVS = 6;   // setup reduction: gamma, delta, rho, (b,b), #nonzero b, pad
+constexpr int NVL = 4;   // loop reduction:  gamma, delta, rho, pad
 
 template <int P1>
-__device__ __forceinline__ CgShared<P1> carve(double* sm, int E, int K, int nw) {
+struct CgShared {
+  unsigned long long* mbar;   // [0],[1] reduction parity 0/1, [2] x0 halo, [3] u0 halo
+  double* st;
+  double* Xs;     // x0 (setup only)
+  double* Ub;     // u, read by the element contraction
+  double* Q;      // element fluxes
+  double* Cs;     // coefficient: own nodes + [NL] left halo node P, [NL+1] right halo node 0
+  double* HXD;    // halo (x0, dinv) pairs [2 sides][P1][2]
+  double* HX;     // halo x0 [2][P1]
+  double* HD;     // halo dinv [2][P1]
+  double* HU0;    // halo u0 [2][P1]
+  double* HU;     // halo u formed locally [2][P1]
+  double* HRWS;   // pushed halo (r, w, s, pad) [2 parity][2 sides][P1][4]
+  double* slots;  // reduction slots [2 parity][16 ranks][NVS]
+  double* wbuf;   // per-thread partials [NVS][blockDim] (structure of arrays)
+  double* bcast;  // reduced scalars [NVS]
+  double* HQ;     // halo face fluxes q: [0] left element node P, [1] right element node 0
+};
+
+// nodes per element padded to an even count: elements start 16-byte aligned
+__host__ __device__ constexpr int padded(int p1) { return p1 + (p1 & 1); }
+
+template <int P1>
+__device__ __forceinline__ CgShared<P1> carve(double* sm, int E, int nt) {
   CgShared<P1> s;
-  const int NL = E * P1;
+  const int NL = E * P1, NLP = E * padded(P1);
   double* q = sm;
   s.mbar = reinterpret_cast<unsigned long long*>(q); q += 4;
+  s.HXD = q; q += 4 * P1;          // 16-byte aligned (v2 stores)
+  s.HRWS = q; q += 16 * P1;        // 16-byte aligned
+  s.slots = q; q += 2 * 16 * NVS;  // 16-byte aligned (NVS even)
+  s.Xs = q; q += NLP;              // padded element layout, 16-byte aligned
+  s.Ub = q; q += NLP;
+  s.Q = q; q += NLP;
+  s.wbuf = q; q += NVS * nt;
+  s.bcast = q; q += 8;
   s.st = q; q += TabOff::size(P1);
-  s.Pb[0] = q; q += NL;
-  s.Pb[1] = q; q += NL;
-  s.Q = q; q += NL;
   s.Cs = q; q += NL + 2;
   s.HX = q; q += 2 * P1;
-  q += (q - sm) & 1;   // 16-byte alignment for v2 stores
-  s.HPZ = q; q += 4 * P1;
-  s.HP = q; q += 2 * P1;
-  s.slotB = q; q += 16 * 4;   // 16-byte aligned: receives v2 stores, [rank][NV]
-  s.slotA = q; q += 16;
-  s.wpart = q; q += 32 * 4;
+  s.HD = q; q += 2 * P1;
+  s.HU0 = q; q += 2 * P1;
+  s.HU = q; q += 2 * P1;
+  s.HQ = q; q += 2;
   return s;
 }
-static size_t cg_smem_bytes(int p1, int E, int K, int nw) {
-  return sizeof(double) * (4 + TabOff::size(p1) + 4 * E * p1 + 2 + 2 * p1 + 1 + 4 * p1 + 2 * p1 + 64 + 16 + 128);
+static size_t cg_smem_bytes(int p1, int E, int nt) {
+  return sizeof(double) * (4 + 4 * p1 + 16 * p1 + 2 * 16 * NVS + 3 * E * padded(p1) + NVS * nt + 8 +
+                           TabOff::size(p1) + E * p1 + 2 + 8 * p1 + 2);
 }
 
 template <bool CL, int P1>
-__global__ void __launch_bounds__(512) k_cg1d(CgArgs A) {
+__global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   extern __shared__ __align__(16) double sm[];
   constexpr int P = P1 - 1;
   const Op1DDev& op = A.op;
@@ -135,7 +152,8 @@ __global__ void __launch_bounds__(512) k_cg1d(CgArgs A) {
   if constexpr (CL) rank = (int)cg::this_cluster().block_rank();
   const int nw = (blockDim.x + 31) >> 5;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const CgShared<P1> s = carve<P1>(sm, A.E, A.K, nw);
+  constexpr int P1P = padded(P1);
+  const CgShared<P1> s = carve<P1>(sm, A.E, blockDim.x);
   const int K = A.K;
   const int e0 = rank * A.E;
   const int e1 = min(op.ne, e0 + A.E);
@@ -143,108 +161,41 @@ __global__ void __launch_bounds__(512) k_cg1d(CgArgs A) {
   const int L = threadIdx.x, el = L / P1, i = L - el * P1;
   const bool own = L < nl;
   const bool first = el == 0, last = (el + 1) * P1 >= nl;
+  const int ob = el * P1P, oL = ob + i;   // element base / node slot in the padded layout
+  const bool helper = wid == 0;            // warp 0 rebuilds the halo element values
   const int egL = wrap(e0 - 1, op.ne), egR = wrap(e1, op.ne);
   const int rL = egL / A.E, rR = egR / A.E;
-  const uint32_t mA = sa(&s.mbar[0]), mB = sa(&s.mbar[1]), mX = sa(&s.mbar[2]);
-  if (threadIdx.x == 0) {
-    mbar_init(mA);
-    mbar_init(mB);
-    mbar_init(mX);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint32_t mb[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) mb[j] = sa(&s.mbar[j]);
+  if constexpr (CL) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mbar_init(mb[j]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
   }
+  const bool stamp = A.timing != nullptr && rank == 0 && threadIdx.x == 0;
+  if (stamp) A.timing[0] = clock64();
   for (int t = threadIdx.x; t < TabOff::size(P1); t += blockDim.x) s.st[t] = op.tab[t];
-  double ci = 0.0, rhs = 0.0;
+  double ci = 0.0, x = 0.0;
   if (own) {
     ci = coef_at(op, A.coef, e0 + el, i);
-    rhs = A.rhs[(size_t)e0 * P1 + L];
+    x = A.rhs[(size_t)e0 * P1 + L];   // x0 = rhs
     s.Cs[L] = ci;
-    s.Pb[1][L] = rhs;
+    s.Xs[oL] = x;
   }
   if (L == 0) s.Cs[NL] = coef_at(op, A.coef, egL, P);
   if (L == 1) s.Cs[NL + 1] = coef_at(op, A.coef, egR, 0);
   if constexpr (CL) cg::this_cluster().sync();   // mbarriers initialised cluster-wide
   else __syncthreads();
-  // remote addresses this thread pushes to
-  // boundary element threads: first element -> left neighbour's right halo, last -> right neighbour's left halo
-  const bool pushL = own && first, pushR = own && last;
-  uint32_t hxL = 0, hxR = 0, hpzL = 0, hpzR = 0, mBL = 0, mBR = 0, mXL = 0, mXR = 0;
-  if constexpr (CL) {
-    if (pushL) {
-      hxL = mapa(sa(s.HX + P1 + i), rL);
-      hpzL = mapa(sa(s.HPZ + 2 * (P1 + i)), rL);
-      mBL = mapa(mB, rL);
-      mXL = mapa(mX, rL);
-    }
-    if (pushR) {
-      hxR = mapa(sa(s.HX + i), rR);
-      hpzR = mapa(sa(s.HPZ + 2 * i), rR);
-      mBR = mapa(mB, rR);
-      mXR = mapa(mX, rR);
-    }
-  }
-  uint32_t phA = 0, phB = 0;
-  const uint32_t halo_bytes = 2u * P1 * 16u;
-  // remote slot / mbarrier addresses for warp 0's lanes (lane r pushes to CTA r)
-  uint32_t raA = 0, raB2 = 0, raB4 = 0, rmA = 0, rmB = 0;
-  if constexpr (CL) {
-    if (wid == 0 && lane < K) {
-      raA = mapa(sa(s.slotA + rank), lane);
-      raB2 = mapa(sa(s.slotB + 2 * rank), lane);
-      raB4 = mapa(sa(s.slotB + 4 * rank), lane);
-      rmA = mapa(mA, lane);
-      rmB = mapa(mB, lane);
-    }
-  }
-
-  // Cluster sum of NV values: warp shuffles, CTA pre-reduction by warp 0, one
-  // st.async per (CTA, destination CTA) completing on the receiver's mbarrier,
-  // then every warp sums the K slots in rank order (identical bits everywhere).
-  auto csum = [&](auto& v, auto nv_tag, bool useA) {
-    constexpr int NV = decltype(nv_tag)::value;
-#pragma unroll
-    for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
-    if (lane == 0)
-#pragma unroll
-      for (int j = 0; j < NV; ++j) s.wpart[wid * 4 + j] = v[j];
-    __syncthreads();
-    double* slots = useA ? s.slotA : s.slotB;
-    if (wid == 0) {
-      double t[NV];
-#pragma unroll
-      for (int j = 0; j < NV; ++j) t[j] = warp_sum(lane < nw ? s.wpart[lane * 4 + j] : 0.0);
-      if constexpr (CL) {
-        if (lane < K) {
-          if constexpr (NV == 1) st_async(raA, t[0], rmA);
-          else {
-            const uint32_t ra = NV == 2 ? raB2 : raB4;
-#pragma unroll
-            for (int j = 0; j < NV; j += 2) st_async2(ra + 8 * j, t[j], t[j + 1], rmB);
-          }
-        }
-      } else {
-        if (lane == 0)
-#pragma unroll
-          for (int j = 0; j < NV; ++j) slots[j] = t[j];
-      }
-    }
-    if constexpr (CL) {
-      const uint32_t mb = useA ? mA : mB;
-      if (threadIdx.x == 0) mbar_expect(mb, 8u * K * NV + (useA ? 0u : halo_bytes));
-      mbar_wait(mb, useA ? phA : phB);
-      if (useA) phA ^= 1; else phB ^= 1;
-    } else {
-      __syncthreads();
-    }
-#pragma unroll
-    for (int j = 0; j < NV; ++j) v[j] = warp_sum(lane < K ? slots[lane * NV + j] : 0.0);
-  };
 
   const double* D = s.st + TabOff::D(P1);
   const double* DTW = s.st + TabOff::DTW(P1);
   const double mi = s.st[TabOff::m(P1) + i];
   const double sc = op.s, mu0 = op.mu0, a = A.a;
   const double cR = last ? s.Cs[NL + 1] : s.Cs[min((el + 1) * P1, NL - 1)];
-  const double cL = first ? s.Cs[NL] : s.Cs[max(el * P1 - 1, 0)];
+  const double cL = first ? s.Cs[NL] : s.Cs[min(max(el * P1 - 1, 0), NL - 1)];
   const double cP = s.Cs[min(el * P1 + P, NL - 1)], c0 = s.Cs[min(el * P1, NL - 1)];
   double dg = 1.0;
   if (own) {   // Jacobi diagonal diag(M + a B[C]) (closed form of dgsem.py:414-490)
@@ -256,125 +207,253 @@ __global__ void __launch_bounds__(512) k_cg1d(CgArgs A) {
     if (i == 0) d += mu0 * (0.5 * (cL + c0)) + sc * c0 * D[0];
     dg = mi + a * d;
   }
-  const double dinv = 1.0 / dg;   // Jacobi: z = r * dinv
+  const double dinv = 1.0 / dg;
   // per-node face constants of the SIP operator (dgsem.py:290-308)
   const double muR = mu0 * (0.5 * (cP + cR)), muL = mu0 * (0.5 * (cL + c0));
   const double kR = sc * (0.5 * cP), kL = sc * (0.5 * c0);
   const double DPi = D[P * P1 + i], D0i = D[i];
 
-  // A v on own nodes; halo element values of v in hv[0..P1) (left), hv[P1..2P1) (right)
-  auto matvec = [&](const double* v, const double* hv) -> double {
-    if (own) {
-      const double* ve = v + el * P1;
-      s.Q[L] = ci * (sc * dot3<P1>(D + i * P1, ve));
+  // ---- push targets (boundary nodes) and reduction targets (warp 0 lanes)
+  const bool pushL = own && first, pushR = own && last;   // first elem -> left nb's right side, last -> right nb's left
+  uint32_t tL[4] = {0, 0, 0, 0}, tR[4] = {0, 0, 0, 0};    // remote: HXD, HU0, HRWS parity 0, HRWS parity 1
+  uint32_t mL[4] = {0, 0, 0, 0}, mR[4] = {0, 0, 0, 0};
+  uint32_t rslot[2] = {0, 0}, rmb[2] = {0, 0};
+  if constexpr (CL) {
+    if (pushL) {
+      tL[0] = mapa(sa(s.HXD + 2 * (P1 + i)), rL);
+      tL[1] = mapa(sa(s.HU0 + P1 + i), rL);
+      tL[2] = mapa(sa(s.HRWS + 4 * (P1 + i)), rL);
+      tL[3] = mapa(sa(s.HRWS + 8 * P1 + 4 * (P1 + i)), rL);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mL[j] = mapa(mb[j], rL);
     }
+    if (pushR) {
+      tR[0] = mapa(sa(s.HXD + 2 * i), rR);
+      tR[1] = mapa(sa(s.HU0 + i), rR);
+      tR[2] = mapa(sa(s.HRWS + 4 * i), rR);
+      tR[3] = mapa(sa(s.HRWS + 8 * P1 + 4 * i), rR);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mR[j] = mapa(mb[j], rR);
+    }
+    if (wid == 0 && lane < K) {
+      rslot[0] = mapa(sa(s.slots + rank * NVS), lane);
+      rslot[1] = mapa(sa(s.slots + (16 + rank) * NVS), lane);
+      rmb[0] = mapa(mb[0], lane);
+      rmb[1] = mapa(mb[1], lane);
+    }
+  }
+  const uint32_t halo_rws_bytes = 2u * P1 * 32u;
+
+  // Cluster sum of NV values into buffer `par` (with the (r,w,s) halo pushed
+  // by the caller on the same mbarrier); identical bits in every CTA.
+  // Only warp 0 shuffles: every thread parks its NR partials in shared memory
+  // (structure of arrays), warp 0 reduces them in a fixed order, pushes the
+  // CTA total to every CTA (NV slots, NR <= NV real values), waits for the K
+  // totals, reduces them in rank order and broadcasts through shared memory.
+  auto csum = [&](auto& v, auto nr_tag, auto nv_tag, int par, uint32_t& phase) {
+    constexpr int NR = decltype(nr_tag)::value;
+    constexpr int NV = decltype(nv_tag)::value;
+    constexpr int MAXW = 12;   // <= 384 threads
+    const int nt = blockDim.x;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) s.wbuf[j * nt + threadIdx.x] = v[j];
+    __syncthreads();
+    if (wid == 0) {
+      double t[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) t[j] = 0.0;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {   // pairwise tree over the <= 12 values of this lane
+        double e[MAXW];
+#pragma unroll
+        for (int m = 0; m < MAXW; ++m) e[m] = (lane + 32 * m < nt) ? s.wbuf[j * nt + lane + 32 * m] : 0.0;
+#pragma unroll
+        for (int w2 = 1; w2 < MAXW; w2 *= 2)
+#pragma unroll
+          for (int m = 0; m + w2 < MAXW; m += 2 * w2) e[m] += e[m + w2];
+        t[j] = warp_sum(e[0]);
+      }
+      double* slots = s.slots + par * 16 * NVS;
+      if constexpr (CL) {
+        if (lane < K)
+#pragma unroll
+          for (int j = 0; j < NV; j += 2) st_async2(rslot[par] + 8 * j, t[j], t[j + 1], rmb[par]);
+        if (lane == 0) mbar_expect(mb[par], 8u * K * NV + halo_rws_bytes);
+        mbar_wait(mb[par], phase);
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {   // K <= 16 slots: 4 butterfly levels
+          double q = lane < K ? slots[lane * NVS + j] : 0.0;
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+          t[j] = q;
+        }
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) s.bcast[j] = t[j];
+    }
+    if constexpr (CL) phase ^= 1;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NR; ++j) v[j] = s.bcast[j];
+  };
+
+  // w = A v on own nodes: v = own shared vector, hv = halo values [left P1][right P1]
+  // element rows of D and D^T W for this node, in registers
+  double Dr[P1], DTr[P1];
+#pragma unroll
+  for (int j = 0; j < P1; ++j) {
+    Dr[j] = D[i * P1 + j];
+    DTr[j] = DTW[i * P1 + j];
+  }
+  // sum_j row[j] e[j] over a padded (16-byte aligned) element with double2 loads
+  auto erow = [&](const double (&row)[P1], const double* e) -> double {
+    const double2* e2 = reinterpret_cast<const double2*>(e);
+    double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+    for (int j2 = 0; j2 < P1P / 2; ++j2) {
+      const double2 t = e2[j2];
+      g0 = fma(row[2 * j2], t.x, g0);
+      if (2 * j2 + 1 < P1) g1 = fma(row[2 * j2 + 1], t.y, g1);
+    }
+    return g0 + g1;
+  };
+  auto matvec = [&](const double* v, const double* hv) -> double {
+    if (own) s.Q[oL] = ci * (sc * erow(Dr, v + ob));
     __syncthreads();
     if (!own) return 0.0;
-    const int b = el * P1;
-    double B = dot3<P1>(DTW + i * P1, s.Q + b);
-    const double pn = last ? hv[P1] : v[b + P1];
-    const double pp = first ? hv[P] : v[b - 1];
-    const double jr = v[b + P] - pn;
-    const double jl = pp - v[b];
+    double B = erow(DTr, s.Q + ob);
+    const double pn = last ? hv[P1] : v[ob + P1P];
+    const double pp = first ? hv[P] : v[ob - P1P + P];
+    const double jr = v[ob + P] - pn;
+    const double jl = pp - v[ob];
     if (i == P) {
-      const double qn = last ? cR * (sc * dot3<P1>(D, hv + P1)) : s.Q[b + P1];
-      B += -(0.5 * (s.Q[b + P] + qn)) + muR * jr;
+      const double qn = last ? cR * (sc * dot3<P1>(D, hv + P1)) : s.Q[ob + P1P];
+      B += -(0.5 * (s.Q[ob + P] + qn)) + muR * jr;
     }
     if (i == 0) {
-      const double qp = first ? cL * (sc * dot3<P1>(D + P * P1, hv)) : s.Q[b - 1];
-      B -= -(0.5 * (qp + s.Q[b])) + muL * jl;
+      const double qp = first ? cL * (sc * dot3<P1>(D + P * P1, hv)) : s.Q[ob - P1P + P];
+      B -= -(0.5 * (qp + s.Q[ob])) + muL * jl;
     }
     B -= (kR * jr) * DPi;
     B -= (kL * jl) * D0i;
-    return fma(a, B, mi * v[L]);
+    return fma(a, B, mi * v[oL]);
   };
 
-  // ---- r = b - A x0: exchange the x0 halo
-  const double* hx;
+  // ---- setup 1: halo (x0, dinv) -> r0 = b - A x0, u0 = D^-1 r0
   if constexpr (CL) {
-    if (threadIdx.x == 0) mbar_expect(mX, 2u * P1 * 8u);
-    if (pushL) st_async(hxL, rhs, mXL);
-    if (pushR) st_async(hxR, rhs, mXR);
-    mbar_wait(mX, 0);
-    hx = s.HX;
+    if (threadIdx.x == 0) mbar_expect(mb[2], 2u * P1 * 16u);
+    if (pushL) st_async2(tL[0], x, dinv, mL[2]);
+    if (pushR) st_async2(tR[0], x, dinv, mR[2]);
+    mbar_wait(mb[2], 0);
   } else {
-    // single CTA, periodic: halo elements are this CTA's last / first element
-    if (L < 2 * P1) {
-      const int side = L / P1, j = L - side * P1;
-      s.HX[L] = s.Pb[1][(side ? 0 : (nl - P1)) + j];
-    }
+    if (own && last) { s.HXD[2 * i] = x; s.HXD[2 * i + 1] = dinv; }
+    if (own && first) { s.HXD[2 * (P1 + i)] = x; s.HXD[2 * (P1 + i) + 1] = dinv; }
     __syncthreads();
-    hx = s.HX;
   }
-  double x = rhs;
-  const double ax = matvec(s.Pb[1], hx);
-  const double b = mi * rhs;
-  double r = b - ax;
-  double z = r * dinv;
-  if (own) s.Pb[0][L] = z;   // p_0 = z_0 = fma(0, p_{-1} = 0, z_0)
-  // halo push (p_{-1} = 0, z_0) with the setup reduction
-  auto push_halo = [&](double pk, double zk) {
+  if (helper && lane < 2 * P1) {
+    s.HX[lane] = s.HXD[2 * lane];
+    s.HD[lane] = s.HXD[2 * lane + 1];
+  }
+  const double bi = mi * x;   // b = M rhs
+  double r = bi - matvec(s.Xs, s.HX);
+  double u = r * dinv;
+  // ---- setup 2: halo u0 -> w0 = A u0
+  if (own) s.Ub[oL] = u;
+  if constexpr (CL) {
+    if (threadIdx.x == 0) mbar_expect(mb[3], 2u * P1 * 8u);
+    if (pushL) st_async(tL[1], u, mL[3]);
+    if (pushR) st_async(tR[1], u, mR[3]);
+    mbar_wait(mb[3], 0);
+  } else {
+    if (own && last) s.HU0[i] = u;
+    if (own && first) s.HU0[P1 + i] = u;
+  }
+  __syncthreads();
+  if (stamp) A.timing[1] = clock64();
+  double w = matvec(s.Ub, s.HU0);
+  double p = 0.0, sv = 0.0;   // p_{-1} = s_{-1} = 0
+  // push (r0, w0, s_{-1} = 0) with the setup reduction (parity 0)
+  auto push_rws = [&](int par) {
     if constexpr (CL) {
-      if (pushL) st_async2(hpzL, pk, zk, mBL);
-      if (pushR) st_async2(hpzR, pk, zk, mBR);
+      if (pushL) { st_async2(tL[2 + par], r, w, mL[par]); st_async2(tL[2 + par] + 16, sv, 0.0, mL[par]); }
+      if (pushR) { st_async2(tR[2 + par], r, w, mR[par]); st_async2(tR[2 + par] + 16, sv, 0.0, mR[par]); }
     } else {
-      if (L < nl && (first || last)) {
-        // local halo: my first element is my own right halo, last element my left halo
-        if (first) { s.HPZ[2 * (P1 + i)] = pk; s.HPZ[2 * (P1 + i) + 1] = zk; }
-        if (last) { s.HPZ[2 * i] = pk; s.HPZ[2 * i + 1] = zk; }
-      }
+      double* h = s.HRWS + par * 8 * P1;
+      if (own && last) { h[4 * i] = r; h[4 * i + 1] = w; h[4 * i + 2] = sv; }
+      if (own && first) { h[4 * (P1 + i)] = r; h[4 * (P1 + i) + 1] = w; h[4 * (P1 + i) + 2] = sv; }
     }
   };
-  push_halo(0.0, z);
-  double v4[4] = {own ? r * z : 0.0, own ? r * r : 0.0, own ? b * b : 0.0, (own && b != 0.0) ? 1.0 : 0.0};
-  csum(v4, std::integral_constant<int, 4>{}, false);
-  double rz = v4[0], rr = v4[1];
-  const double thr = A.rtol2 * v4[2];
-  if (v4[3] == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
+  push_rws(0);
+  uint32_t ph[2] = {0, 0};
+  double v6[NVS] = {own ? r * u : 0.0, own ? w * u : 0.0, own ? r * r : 0.0, own ? bi * bi : 0.0,
+                    (own && bi != 0.0) ? 1.0 : 0.0, 0.0};
+  if (stamp) A.timing[2] = clock64();
+  csum(v6, std::integral_constant<int, 5>{}, std::integral_constant<int, NVS>{}, 0, ph[0]);
+  if (stamp) A.timing[3] = clock64();
+  double gamma = v6[0], rho = v6[2];
+  const double thr = A.rtol2 * v6[3];
+  if (v6[4] == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
     if (own) A.x[(size_t)e0 * P1 + L] = 0.0;
     return;
   }
+  double alpha = gamma / v6[1], beta = 0.0;
+  double rgamma = 1.0 / gamma, ralpha = 1.0 / alpha;   // reciprocals off the critical path
   int k = 0;
-  double beta = 0.0;
   bool ok = true;
-  while (rr > thr) {
+  while (rho > thr) {
     if (k >= A.maxit) { ok = false; break; }
-    double* pc = s.Pb[k & 1];
-    double* po = s.Pb[(k + 1) & 1];
-    // neighbour p_k = fma(beta_{k-1}, p_{k-1}, z_k) from the pushed pairs
-    if (L < 2 * P1) s.HP[L] = fma(beta, s.HPZ[2 * L], s.HPZ[2 * L + 1]);
-    // (matvec's first __syncthreads orders HP before its use)
-    const double ap = matvec(pc, s.HP);
-    const double pk = own ? pc[L] : 0.0;
-    double v1[1] = {pk * ap};
-    csum(v1, std::integral_constant<int, 1>{}, true);
-    const double alpha = rz / v1[0];
-    x = fma(alpha, pk, x);
-    r = fma(-alpha, ap, r);
-    z = r * dinv;
-    push_halo(pk, z);
-    double v2[2] = {own ? r * z : 0.0, own ? r * r : 0.0};
-    csum(v2, std::integral_constant<int, 2>{}, false);
-    beta = v2[0] / rz;
-    rz = v2[0];
-    rr = v2[1];
-    ++k;
-    if (rr <= thr) break;
-    if (own) po[L] = fma(beta, pk, z);
+    const int par = k & 1;          // halo data from the previous reduction
+    // neighbour u_{k+1} from its pushed (r, w, s): the owner's exact operations
+    if (helper) {   // warp 0 rebuilds the neighbours' u from their pushed (r, w, s)
+      if (lane < 2 * P1) {
+        const double* h = s.HRWS + par * 8 * P1 + 4 * lane;
+        const double sh = fma(beta, h[2], h[1]);
+        const double rh = fma(-alpha, sh, h[0]);
+        s.HU[lane] = rh * s.HD[lane];
+      }
+    }
+    p = fma(beta, p, u);
+    sv = fma(beta, sv, w);
+    x = fma(alpha, p, x);
+    r = fma(-alpha, sv, r);
+    u = r * dinv;
+    if (own) s.Ub[oL] = u;
+    const bool sub = stamp && k == 5;
+    if (sub) A.timing[70] = clock64();
     __syncthreads();
+    if (sub) A.timing[71] = clock64();
+    w = matvec(s.Ub, s.HU);
+    if (sub) A.timing[72] = clock64();
+    push_rws(par ^ 1);
+    double v4[NVL] = {own ? r * u : 0.0, own ? w * u : 0.0, own ? r * r : 0.0, 0.0};
+    csum(v4, std::integral_constant<int, 3>{}, std::integral_constant<int, NVL>{}, par ^ 1, ph[par ^ 1]);
+    if (sub) A.timing[73] = clock64();
+    ++k;
+    if (stamp && k < 60) A.timing[4 + k] = clock64();
+    rho = v4[2];
+    if (rho <= thr) break;
+    const double gn = v4[0];
+    beta = __dmul_rn(gn, rgamma);   // one division on the critical path
+    alpha = gn / __dsub_rn(v4[1], __dmul_rn(beta, __dmul_rn(gn, ralpha)));
+    ralpha = 1.0 / alpha;
+    gamma = gn;
+    rgamma = 1.0 / gamma;
+    if (sub) A.timing[74] = clock64();
   }
   if (own) A.x[(size_t)e0 * P1 + L] = x;
+  if (stamp) { A.timing[64] = clock64(); A.timing[65] = k; }
   if (rank == 0 && threadIdx.x == 0) {
     int idx = atomicAdd(&A.status[2], 1);
     if (idx < A.log_cap) {
       A.log_it[idx] = ok ? k : -1;
-      A.log_margin[idx] = thr > 0.0 ? sqrt(rr / thr) : 0.0;
+      A.log_margin[idx] = thr > 0.0 ? sqrt(rho / thr) : 0.0;
     }
     if (!ok) atomicAdd(&A.status[1], 1);
   }
 }
 
-// Partition: one thread per node, at most 512 nodes per CTA and 16 CTAs.
+// Partition: one thread per node, at most 384 nodes per CTA and 16 CTAs.
 static int choose_partition(const Ctx* c, int ne, int p1, int& K, int& E) {
   int want = c->cluster_ctas > 0 ? c->cluster_ctas : (ne * p1 + 287) / 288;   // ~288 nodes per CTA
   K = want < 1 ? 1 : (want > 16 ? 16 : want);
@@ -382,10 +461,10 @@ static int choose_partition(const Ctx* c, int ne, int p1, int& K, int& E) {
   for (;;) {
     E = (ne + K - 1) / K;
     K = (ne + E - 1) / E;   // no empty CTA
-    if (E * p1 <= 512 || K >= 16 || K >= ne) break;
+    if (E * p1 <= 384 || K >= 16 || K >= ne) break;
     ++K;
   }
-  return E * p1 <= 512 ? 0 : -1;
+  return E * p1 <= 384 ? 0 : -1;
 }
 
 template <int P1>
@@ -426,15 +505,15 @@ int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rh
   int K, E;
   if (choose_partition(c, op.ne, p1, K, E))
     return c->fail(SISDC_ERR_UNSUPPORTED, "implicit_solve: level too large for the cluster-resident CG "
-                                          "(more than 16 CTAs x 512 nodes)");
+                                          "(more than 16 CTAs x 384 nodes)");
   int threads = ((E * p1 + 31) / 32) * 32;
   if (threads < 64) threads = 64;
-  const int nw = threads / 32;
-  size_t smem = cg_smem_bytes(p1, E, K, nw);
+  size_t smem = cg_smem_bytes(p1, E, threads);
   CgArgs A{};
   A.op = op; A.coef = k; A.a = a; A.rhs = rhs; A.x = x;
   A.rtol2 = c->rtol * c->rtol; A.maxit = c->maxit; A.E = E; A.K = K;
   A.status = c->d_status; A.log_it = c->d_log_it; A.log_margin = c->d_log_margin; A.log_cap = c->log_cap;
+  A.timing = c->d_timing;
   switch (p1) {
     case 2: return launch_cg_t<2>(c, A, threads, smem);
     case 3: return launch_cg_t<3>(c, A, threads, smem);

@@ -80,7 +80,11 @@ __device__ __forceinline__ double coef_at(const Op1DDev& op, const CoefDev& k, i
 }
 
 // ----------------------------------------------------------- tiles
-__device__ __forceinline__ int wrap(int e, int ne) { return e < 0 ? e + ne : (e >= ne ? e - ne : e); }
+// periodic element index; tiles may be wider than the whole mesh, so fold fully
+__device__ __forceinline__ int wrap(int e, int ne) {
+  e %= ne;
+  return e < 0 ? e + ne : e;
+}
 
 // tile[(el+1)*p1 + i] = u[(ebase+el) wrapped, i] for el = -1..EB
 __device__ __forceinline__ void load_tile(double* tile, const double* __restrict__ u, int ebase, int EB,

@@ -18,6 +18,7 @@ struct Ctx {
   int* d_log_it = nullptr;        // per-solve CG iterations
   double* d_log_margin = nullptr; // per-solve ||r||/(rtol ||b||)
   int log_cap = 1 << 16;
+  long long* d_timing = nullptr;  // SISDC_CG_TIMING=1: CG clock64 stamps [66]
   double rtol = 1e-14;
   int maxit = 1000;
   int cluster_ctas = 0;

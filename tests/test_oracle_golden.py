@@ -83,6 +83,8 @@ def test_mlsdc_step_lu_and_pcg(golden, tag, w):
         assert h.fine_sweeps == w.n_cycles + 1 and h.coarse_passes == 2 + 2 * w.n_cycles
         if solver == "pcg":
             assert [it for it, _ in log] == G[f"{tag}_pcg_iters1"].tolist()
+            # the two-reduction textbook form takes the same iterations
+            assert G[f"{tag}_pcg_iters1"].tolist() == G[f"{tag}_hs_iters1"].tolist()
     if tag == "cfg1":
         assert np.abs(sol.u - G["cfg1_lu_step1_nodes"]).max() < 1e-12
 
