@@ -108,6 +108,15 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(HERE, "profiles", "r01_cg_traffic.json")) as f:
+            return float(json.load(f)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def measured_hbm_peak():
     p = os.path.join(HERE, "MEASURED_PEAKS.json")
     try:
@@ -331,7 +340,7 @@ def run_ours(args):
                 "timing": "CUDA events around each CUDA-graph slab replay, summed; max over ranks",
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": measured_traffic(), "peak_kind": peak_kind,
                          "kernel": "k_cg1d (cluster-resident Jacobi-PCG, one launch per implicit solve)",
                          "kernel_us": t_cg * 1e6, "kernel_mean_iterations": k_cg,
                          "algorithmic_bytes_per_launch": bytes_cg,

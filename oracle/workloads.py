@@ -23,3 +23,19 @@ def build_hierarchy(w, solver="pcg", rtol=1e-14, log=None):
 
 def fine_nodes(w):
     return quad.gll(w.p_fine + 1)[0]
+
+
+def build_hierarchy_2d(make_problem2d, x0, x1, y0, y1, nex, ney, p_coarse, p_fine, m_coarse, m_fine,
+                       rtol=1e-14, log=None, n_coarse=2):
+    """Two-level 2-D p-hierarchy (oracle) sharing one CG log in call order."""
+    from . import dg2d
+    log = [] if log is None else log
+
+    def mk(lvl):
+        P = p_coarse if lvl == "coarse" else p_fine
+        return dg2d.Op2D(x0, x1, y0, y1, nex, ney, P, make_problem2d(), rtol=rtol, cg_log=log)
+
+    cc, cf = mk("coarse"), mk("fine")
+    rc, rf = sweeper.Rule("radau_right", m_coarse), sweeper.Rule("radau_right", m_fine)
+    levels = [sweeper.Lev(cc, rc), sweeper.Lev(cf, rf)]
+    return sweeper.Hier(levels, [dg2d.PTransfer2D(cc, cf, rc, rf)], n_coarse, 1, "incremental", True), log
