@@ -40,7 +40,11 @@ enum sisdc_status {
   SISDC_ERR_UNSUPPORTED = 5   /* configuration outside the built path            */
 };
 
-enum sisdc_problem { SISDC_CONVDIFF = 0, SISDC_BURGERS = 1 };   /* problems.py:25-82 */
+enum sisdc_problem {
+  SISDC_CONVDIFF = 0, SISDC_BURGERS = 1,        /* 1-D, problems.py:25-82               */
+  SISDC_EULER2D = 2,                            /* 2-D Euler / NS (isotropic viscosity)  */
+  SISDC_ADVECTION2D = 3, SISDC_BURGERS2D = 4    /* 2-D scalar (cross-dimension checks)   */
+};
 enum sisdc_bc { SISDC_PERIODIC = 0 };                            /* Mesh1D.bc         */
 enum sisdc_scheme { SISDC_EULER = 0, SISDC_SI1 = 1, SISDC_SI2 = 2 }; /* integrators.py:26 */
 
@@ -73,6 +77,23 @@ typedef struct {
   double penalty;    /* DGOperator penalty_const (2.0)    */
 } sisdc_op1d_desc;
 
+/* 2-D tensor-product DG-SEM on a uniform periodic nex x ney mesh of
+ * [x_left,x_right] x [y_bottom,y_top] (BASELINE configs 3-5; the reference is
+ * 1-D only).  State layout (ncomp, ney, nex, P+1 [y], P+1 [x]).  Every
+ * operator entry point below accepts a 2-D handle; the SI coefficient is the
+ * isotropic (dt_m/2) lambda(u_b)^2 + nu, lambda = |v| + c. */
+typedef struct {
+  int nex, ney;
+  int degree;        /* P, 1..8                                   */
+  int ncomp;         /* 4 for Euler/NS, 1 for the scalar problems  */
+  int problem;       /* SISDC_EULER2D / SISDC_ADVECTION2D / SISDC_BURGERS2D */
+  double x_left, x_right, y_bottom, y_top;
+  double gamma;      /* ideal gas                                  */
+  double nu;         /* isotropic kinematic viscosity (0 => Euler) */
+  double ax, ay;     /* advection velocity (SISDC_ADVECTION2D)     */
+  double penalty;    /* SIP penalty constant (2.0)                 */
+} sisdc_op2d_desc;
+
 /* ----------------------------------------------------------- context */
 int  sisdc_abi_version(void);
 int  sisdc_ctx_create(int device, sisdc_ctx** out);
@@ -100,6 +121,8 @@ int  sisdc_copy(sisdc_ctx* ctx, double* dst, const double* src, int64_t n);  /* 
 
 /* ------------------------------------------------------ DG operator */
 int  sisdc_op1d_create(sisdc_ctx* ctx, const sisdc_op1d_desc* desc, sisdc_op1d** out);
+/* 2-D operator: returns the same opaque handle type (dimension-tagged). */
+int  sisdc_op2d_create(sisdc_ctx* ctx, const sisdc_op2d_desc* desc, sisdc_op1d** out);
 void sisdc_op1d_destroy(sisdc_op1d* op);
 /* Host copies of the element tables: GLL nodes/weights (P+1), D ((P+1)^2). */
 int  sisdc_op1d_tables(const sisdc_op1d* op, double* nodes, double* weights, double* D);
@@ -148,6 +171,10 @@ int  sisdc_collocation_defect(sisdc_op1d* op, int M, const double* W, double dt,
 /* ------------------------------------- space-time p-transfers (transfer.py) */
 /* It (Mf x Mc) = Lagrange(tau_c -> tau_f), Pt (Mc x Mf); Isp ((Pf+1) x (Pc+1)),
  * Psp ((Pc+1) x (Pf+1)); restrictions are the transposes (transfer.py:61-96,213-245). */
+/* 2-D: n_elem = nex*ney*ncomp element slabs, spatial matrices applied in x and y. */
+int  sisdc_xfer2d_create(sisdc_ctx* ctx, int n_elem, int pc1, int pf1, int Mc, int Mf,
+                         const double* It, const double* Pt, const double* Isp, const double* Psp,
+                         sisdc_xfer** out);
 int  sisdc_xfer_create(sisdc_ctx* ctx, int n_elem, int pc1, int pf1,
                        int Mc, int Mf, const double* It, const double* Pt,
                        const double* Isp, const double* Psp, sisdc_xfer** out);

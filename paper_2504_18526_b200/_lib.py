@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsisdc_b200.so")
 
 OK, ERR_ARG, ERR_CUDA, ERR_NONFINITE, ERR_NOCONV, ERR_UNSUPPORTED = range(6)
-CONVDIFF, BURGERS = 0, 1
+CONVDIFF, BURGERS, EULER2D, ADVECTION2D, BURGERS2D = 0, 1, 2, 3, 4
 PERIODIC = 0
 SCHEMES = {"euler": 0, "si1": 1, "si2": 2}
 COEF_NONE, COEF_CONST, COEF_FIELD, COEF_SI, COEF_PHYS = range(5)
@@ -32,6 +32,13 @@ class LibraryError(RuntimeError):
 
 class Coef(C.Structure):
     _fields_ = [("kind", C.c_int), ("value", C.c_double), ("ptr", C.c_void_p)]
+
+
+class Op2DDesc(C.Structure):
+    _fields_ = [("nex", C.c_int), ("ney", C.c_int), ("degree", C.c_int), ("ncomp", C.c_int), ("problem", C.c_int),
+                ("x_left", C.c_double), ("x_right", C.c_double), ("y_bottom", C.c_double), ("y_top", C.c_double),
+                ("gamma", C.c_double), ("nu", C.c_double), ("ax", C.c_double), ("ay", C.c_double),
+                ("penalty", C.c_double)]
 
 
 class Op1DDesc(C.Structure):
@@ -63,6 +70,7 @@ SIGNATURES = {
     "sisdc_ctx_debug_timing": (I, [P, C.POINTER(C.c_longlong), I]),
     "sisdc_copy": (I, [P, P, P, C.c_int64]),
     "sisdc_op1d_create": (I, [P, C.POINTER(Op1DDesc), C.POINTER(P)]),
+    "sisdc_op2d_create": (I, [P, C.POINTER(Op2DDesc), C.POINTER(P)]),
     "sisdc_op1d_destroy": (None, [P]),
     "sisdc_op1d_tables": (I, [P, DP, DP, DP]),
     "sisdc_op1d_set_nu_art": (I, [P, P]),
@@ -77,6 +85,7 @@ SIGNATURES = {
     "sisdc_eval_rhs_nodes": (I, [P, I, P, DP, P]),
     "sisdc_collocation_defect": (I, [P, I, DP, D, I, P, P, P, D, P, P]),
     "sisdc_xfer_create": (I, [P, I, I, I, I, I, DP, DP, DP, DP, C.POINTER(P)]),
+    "sisdc_xfer2d_create": (I, [P, I, I, I, I, I, DP, DP, DP, DP, C.POINTER(P)]),
     "sisdc_xfer_destroy": (None, [P]),
     "sisdc_xfer_spatial": (I, [P, I, P, P]),
     "sisdc_xfer_down": (I, [P, I, I, P, P]),

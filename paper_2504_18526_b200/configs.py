@@ -98,3 +98,79 @@ CFG2 = Workload1D("cfg2_burgers_512el_P8", "burgers", 512, 8, 4, 5, 3,
                   {"nu": 5e-3}, seed=2, t_end=1.5, n_cycles=3)
 
 WORKLOADS = {"cfg1": CFG1, "cfg2": CFG2}
+
+
+# ---------------------------------------------------------------- 2-D (cfgs 3-5)
+@dataclass(frozen=True)
+class Workload2D:
+    """2-D compressible Euler / NS workloads (BASELINE configs 3-5; no
+    reference implementation).  Seeded synthetic ICs:
+    isentropic vortex (cfg3) and the double shear layer (cfgs 4-5)."""
+    name: str
+    kind: str            # "vortex" | "shear"
+    nex: int
+    ney: int
+    p_fine: int
+    p_coarse: int
+    m_fine: int
+    m_coarse: int
+    length: float
+    seed: int
+    gamma: float = 1.4
+    nu: float = 0.0
+    mach: float = 0.1
+    cfl: float = 1.0
+    n_cycles: int = 3
+    n_steps: int = 20
+
+    @property
+    def ncomp(self):
+        return 4
+
+    def dof(self):
+        nf = 4 * self.nex * self.ney * (self.p_fine + 1) ** 2
+        nc = 4 * self.nex * self.ney * (self.p_coarse + 1) ** 2
+        return nf, nc
+
+    def dof_sweeps_per_step(self):
+        nf, nc = self.dof()
+        return nf * self.m_fine * (self.n_cycles + 1) + nc * self.m_coarse * (2 + 2 * self.n_cycles), \
+            nf * self.m_fine * (self.n_cycles + 1)
+
+    def initial_state(self, X, Y):
+        """Conservative (rho, rho u, rho v, rho E) on node arrays X, Y (ney, nex, p1, p1)."""
+        g = self.gamma
+        rng = np.random.default_rng(self.seed)
+        if self.kind == "vortex":
+            x0, y0 = rng.uniform(0.25 * self.length, 0.75 * self.length, 2)
+            beta = 5.0
+            r2 = (X - x0) ** 2 + (Y - y0) ** 2
+            e = np.exp(0.5 * (1.0 - r2))
+            u = 1.0 - beta / (2.0 * math.pi) * (Y - y0) * e
+            v = 1.0 + beta / (2.0 * math.pi) * (X - x0) * e
+            T = 1.0 - (g - 1.0) * beta ** 2 / (8.0 * g * math.pi ** 2) * np.exp(1.0 - r2)
+            rho = T ** (1.0 / (g - 1.0))
+            p = rho ** g
+        else:
+            delta = 0.05
+            u = np.where(Y <= math.pi, np.tanh((Y - math.pi / 2) / delta), np.tanh((3 * math.pi / 2 - Y) / delta))
+            v = 0.05 * np.sin(X) + 1e-3 * rng.standard_normal(X.shape)
+            rho = np.ones_like(X)
+            p = np.full_like(X, 1.0 / (g * self.mach ** 2))
+        E = p / (g - 1.0) + 0.5 * rho * (u * u + v * v)
+        return np.ascontiguousarray(np.stack([rho, rho * u, rho * v, E]).reshape(-1), dtype=np.float64)
+
+    def time_step(self, u0, delta_p):
+        """dt from the acoustic CFL on max(|v| + c) (builder choice)."""
+        q = u0.reshape(4, -1)
+        rho, mx, my, E = q
+        p = (self.gamma - 1.0) * (E - 0.5 * (mx * mx + my * my) / rho)
+        lam = float(np.max(np.sqrt(mx * mx + my * my) / rho + np.sqrt(self.gamma * p / rho)))
+        h = self.length / self.nex
+        return self.cfl * h / (2.0 * delta_p * lam)
+
+
+CFG3 = Workload2D("cfg3_euler_vortex_128x128_P7", "vortex", 128, 128, 7, 3, 4, 2, 10.0, seed=3)
+CFG4 = Workload2D("cfg4_ns_shear_256x256_P7", "shear", 256, 256, 7, 3, 5, 3, TWO_PI, seed=4, nu=1e-4)
+CFG5 = Workload2D("cfg5_ns_shear_1024x1024_P7", "shear", 1024, 1024, 7, 3, 5, 3, TWO_PI, seed=5, nu=1e-4)
+WORKLOADS.update({"cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5})

@@ -7,6 +7,7 @@
 #include <new>
 #include <vector>
 #include "sisdc_dev.cuh"
+#include "sisdc_dev2d.cuh"
 #include "sisdc_host.h"
 
 using namespace sisdc;
@@ -15,17 +16,24 @@ struct sisdc_ctx {
   Ctx c;
 };
 
-struct sisdc_op1d {
+struct sisdc_op1d {   // dimension-tagged operator handle (1-D or 2-D)
   sisdc_ctx* ctx;
+  int dim = 1;
   sisdc_op1d_desc desc;
   Op1DDev dev;
+  Op2DDev dev2;
   double* d_tab = nullptr;
+  double* d_cgws = nullptr;   // 2-D CG workspace (allocated at creation: graph-safe)
+  int cg_blocks = 0;
   std::vector<double> nodes, weights, D;
+  long long n() const { return dim == 1 ? dev.n : dev2.n; }
 };
 
 struct sisdc_xfer {
   sisdc_ctx* ctx;
+  int dim = 1;
   XferDev dev;
+  Xfer2Dev dev2;
   double* d_tab = nullptr;
 };
 
@@ -287,9 +295,74 @@ int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) 
   return SISDC_OK;
 }
 
+// 2-D operator: shared 1-D element tables + tensor-product kernels
+int sisdc_op2d_create(sisdc_ctx* x, const sisdc_op2d_desc* d, sisdc_op1d** out) {
+  if (!x || !d || !out) return SISDC_ERR_ARG;
+  *out = nullptr;
+  Ctx& c = x->c;
+  if (!(d->x_right > d->x_left) || !(d->y_top > d->y_bottom)) return c.fail(SISDC_ERR_ARG, "empty domain");
+  if (d->nex < 1 || d->ney < 1 || d->degree < 1) return c.fail(SISDC_ERR_ARG, "need elements and degree >= 1");
+  if (d->degree + 1 > 9) return c.fail(SISDC_ERR_UNSUPPORTED, "2-D degree above 8");
+  const bool euler = d->problem == SISDC_EULER2D;
+  if (!euler && d->problem != SISDC_ADVECTION2D && d->problem != SISDC_BURGERS2D)
+    return c.fail(SISDC_ERR_ARG, "unknown 2-D problem");
+  if ((euler && d->ncomp != 4) || (!euler && d->ncomp != 1)) return c.fail(SISDC_ERR_ARG, "ncomp does not match the problem");
+  if (d->nu < 0) return c.fail(SISDC_ERR_ARG, "viscosity must be nonnegative");
+  sisdc_op1d* op = new (std::nothrow) sisdc_op1d();
+  if (!op) return SISDC_ERR_ARG;
+  op->ctx = x;
+  op->dim = 2;
+  const int p1 = d->degree + 1;
+  gll(p1, op->nodes, op->weights);
+  op->D = diff_matrix(op->nodes);
+  const double dx = (d->x_right - d->x_left) / d->nex, dy = (d->y_top - d->y_bottom) / d->ney;
+  std::vector<double> tab(TabOff::size(p1), 0.0);
+  for (int i = 0; i < p1; ++i)
+    for (int k = 0; k < p1; ++k) {
+      tab[TabOff::D(p1) + i * p1 + k] = op->D[i * p1 + k];
+      tab[TabOff::DTW(p1) + i * p1 + k] = op->D[k * p1 + i] * op->weights[k];
+      tab[TabOff::D2W(p1) + i * p1 + k] = op->D[k * p1 + i] * op->D[k * p1 + i] * op->weights[k];
+    }
+  for (int i = 0; i < p1; ++i) {
+    tab[TabOff::w(p1) + i] = op->weights[i];
+    tab[TabOff::m(p1) + i] = op->weights[i];
+    tab[TabOff::minv(p1) + i] = 1.0 / op->weights[i];
+  }
+  Op2DDev& v = op->dev2;
+  v.nex = d->nex; v.ney = d->ney; v.p1 = p1; v.nc = d->ncomp;
+  v.nn = (long long)d->nex * d->ney * p1 * p1;
+  v.n = v.nn * d->ncomp;
+  v.problem = d->problem;
+  v.dx = dx; v.dy = dy; v.sx = 2.0 / dx; v.sy = 2.0 / dy;
+  v.mux = d->penalty * p1 * p1 / dx; v.muy = d->penalty * p1 * p1 / dy;
+  v.gamma = d->gamma; v.nu = d->nu; v.ax = d->ax; v.ay = d->ay;
+  v.nu_art = nullptr;
+  cudaError_t e = cudaMalloc(&op->d_tab, tab.size() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(op->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    int rc = c.cuda(e, "op2d tables");
+    delete op;
+    return rc;
+  }
+  v.tab = op->d_tab;
+  int rc = cg2_blocks(&c, v, &op->cg_blocks);
+  if (rc) { cudaFree(op->d_tab); delete op; return rc; }
+  const size_t ws = 4 * (size_t)v.n + 2 * (size_t)v.nn + 16 + 4 * (size_t)op->cg_blocks;
+  e = cudaMalloc(&op->d_cgws, ws * sizeof(double));
+  if (e != cudaSuccess) {
+    rc = c.cuda(e, "op2d CG workspace");
+    cudaFree(op->d_tab);
+    delete op;
+    return rc;
+  }
+  *out = op;
+  return SISDC_OK;
+}
+
 void sisdc_op1d_destroy(sisdc_op1d* op) {
   if (!op) return;
   cudaFree(op->d_tab);
+  cudaFree(op->d_cgws);
   delete op;
 }
 
@@ -305,16 +378,19 @@ int sisdc_op1d_tables(const sisdc_op1d* op, double* nodes, double* weights, doub
 int sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art) {
   if (!op) return SISDC_ERR_ARG;
   op->dev.nu_art = nu_art;
+  op->dev2.nu_art = nu_art;
   return SISDC_OK;
 }
 
 int sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, double c_s, double* nu_art) {
   if (!op || !u || !nu_art || !(kappa_s > 0)) return SISDC_ERR_ARG;
+  if (op->dim == 2) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "the modal sensor is built for 1-D meshes");
   return launch_persson(C(op), op->dev, u, kappa_s, c_s, nu_art);
 }
 
 int sisdc_apply_convection(sisdc_op1d* op, const double* u, double, double* out) {
   if (!op || !u || !out) return SISDC_ERR_ARG;
+  if (op->dim == 2) return launch2_conv(C(op), op->dev2, u, out);
   return launch_apply_convection(C(op), op->dev, u, out);
 }
 
@@ -322,18 +398,22 @@ int sisdc_apply_diffusion(sisdc_op1d* op, sisdc_coef k, const double* u, double,
   if (!op || !u || !out) return SISDC_ERR_ARG;
   if (int rc = check_coef(C(op), k)) return rc;
   if (k.kind == SISDC_COEF_NONE || (k.kind == SISDC_COEF_CONST && k.value == 0.0))
-    return C(op)->cuda(cudaMemsetAsync(out, 0, op->dev.n * sizeof(double), C(op)->stream), "zero");
+    return C(op)->cuda(cudaMemsetAsync(out, 0, op->n() * sizeof(double), C(op)->stream), "zero");
+  if (op->dim == 2) return launch2_sip(C(op), op->dev2, coef(k), u, out);
   return launch_apply_diffusion(C(op), op->dev, coef(k), u, out);
 }
 
 int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double, double* out) {
   if (!op || !u || !out) return SISDC_ERR_ARG;
+  if (op->dim == 2)
+    return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
   return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
 }
 
 int sisdc_coef_field(sisdc_op1d* op, sisdc_coef k, double* out) {
   if (!op || !out) return SISDC_ERR_ARG;
   if (int rc = check_coef(C(op), k)) return rc;
+  if (op->dim == 2) return launch2_coef(C(op), op->dev2, coef(k), out);
   return launch_coef_field(C(op), op->dev, coef(k), out);
 }
 
@@ -342,9 +422,10 @@ int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* r
   if (int rc = check_coef(C(op), k)) return rc;
   if (a == 0.0) {   // dgsem.py:505-506
     if (x == rhs) return SISDC_OK;
-    return sisdc_copy(op->ctx, x, rhs, op->dev.n);
+    return sisdc_copy(op->ctx, x, rhs, op->n());
   }
   if (k.kind == SISDC_COEF_NONE) return C(op)->fail(SISDC_ERR_ARG, "cannot assemble a zero coefficient");
+  if (op->dim == 2) return launch2_cg(C(op), op->dev2, coef(k), a, rhs, x, op->d_cgws, op->cg_blocks);
   return launch_cg1d(C(op), op->dev, coef(k), a, rhs, x);
 }
 
@@ -352,6 +433,7 @@ int sisdc_stage_rhs(sisdc_op1d* op, const double* base, const double* conv_in, d
                     int M, const double* w_row, double dt, const double* g_m, const double* h_old, double,
                     double* rhs, double* conv_out) {
   if (!op || !base || !conv_in || !rhs || M < 0 || M > MAXM || (f_old && !w_row)) return SISDC_ERR_ARG;
+  if (op->dim == 2) return launch2_stage(C(op), op->dev2, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
   return launch_stage_rhs(C(op), op->dev, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
 }
 
@@ -361,18 +443,21 @@ int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_coun
   if (!op || !u0 || !u || !dts || !f || !h1) return SISDC_ERR_ARG;
   if (scheme < SISDC_EULER || scheme > SISDC_SI2) return C(op)->fail(SISDC_ERR_ARG, "unknown scheme");
   if (conv_prev && m_count != 1) return C(op)->fail(SISDC_ERR_ARG, "conv_prev needs m_count == 1");
+  if (op->dim == 2)
+    return launch2_node_eval(C(op), op->dev2, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
   return launch_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
 }
 
 int sisdc_eval_rhs_nodes(sisdc_op1d* op, int M, const double* u, const double*, double* f) {
   if (!op || !u || !f || M < 1 || M > MAXM) return SISDC_ERR_ARG;
+  if (op->dim == 2) return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
   return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
 }
 
 int sisdc_collocation_defect(sisdc_op1d* op, int M, const double* W, double dt, int incremental, const double* u0,
                              const double* u, const double* f, double sign, const double* add, double* out) {
   if (!op || !W || !u0 || !u || !f || !out || M < 1 || M > MAXM) return SISDC_ERR_ARG;
-  return launch_defect(C(op), op->dev.n, M, W, dt, incremental, u0, u, f, sign, add, out);
+  return launch_defect(C(op), (int)op->n(), M, W, dt, incremental, u0, u, f, sign, add, out);
 }
 
 // ------------------------------------------------------------ transfers
@@ -404,6 +489,17 @@ int sisdc_xfer_create(sisdc_ctx* x, int n_elem, int pc1, int pf1, int Mc, int Mf
   return SISDC_OK;
 }
 
+int sisdc_xfer2d_create(sisdc_ctx* x, int n_elem, int pc1, int pf1, int Mc, int Mf, const double* It,
+                        const double* Pt, const double* Isp, const double* Psp, sisdc_xfer** out) {
+  int rc = sisdc_xfer_create(x, n_elem, pc1, pf1, Mc, Mf, It, Pt, Isp, Psp, out);
+  if (rc) return rc;
+  sisdc_xfer* t = *out;
+  t->dim = 2;
+  t->dev2.nslab = n_elem; t->dev2.pc = pc1; t->dev2.pf = pf1; t->dev2.Mc = Mc; t->dev2.Mf = Mf;
+  t->dev2.tab = t->d_tab;
+  return SISDC_OK;
+}
+
 void sisdc_xfer_destroy(sisdc_xfer* t) {
   if (!t) return;
   cudaFree(t->d_tab);
@@ -412,23 +508,27 @@ void sisdc_xfer_destroy(sisdc_xfer* t) {
 
 int sisdc_xfer_spatial(sisdc_xfer* t, int dir, const double* in, double* out) {
   if (!t || !in || !out || dir < 0 || dir > 2) return SISDC_ERR_ARG;
+  if (t->dim == 2) return launch2x_spatial(&t->ctx->c, t->dev2, dir, in, out);
   return launch_xfer_spatial(&t->ctx->c, t->dev, dir, in, out);
 }
 
 int sisdc_xfer_down(sisdc_xfer* t, int spatial_dir, int temporal_dir, const double* in, double* out) {
   if (!t || !in || !out || spatial_dir < 1 || spatial_dir > 2 || temporal_dir < 1 || temporal_dir > 2)
     return SISDC_ERR_ARG;
+  if (t->dim == 2) return launch2x_down(&t->ctx->c, t->dev2, spatial_dir, temporal_dir, in, out);
   return launch_xfer_down(&t->ctx->c, t->dev, spatial_dir, temporal_dir, in, out);
 }
 
 int sisdc_xfer_fas_restrict(sisdc_xfer* t, const double* Wf, double dt, int incremental, const double* u0f,
                             const double* uf, const double* ff, const double* gf, double* v, double* rr) {
   if (!t || !Wf || !u0f || !uf || !ff || !v || !rr) return SISDC_ERR_ARG;
+  if (t->dim == 2) return launch2x_fas(&t->ctx->c, t->dev2, Wf, dt, incremental, u0f, uf, ff, gf, v, rr);
   return launch_fas_restrict(&t->ctx->c, t->dev, Wf, dt, incremental, u0f, uf, ff, gf, v, rr);
 }
 
 int sisdc_xfer_interp(sisdc_xfer* t, int accumulate, const double* uc, const double* vc, double* uf) {
   if (!t || !uc || !uf) return SISDC_ERR_ARG;
+  if (t->dim == 2) return launch2x_interp(&t->ctx->c, t->dev2, accumulate, uc, vc, uf);
   return launch_xfer_interp(&t->ctx->c, t->dev, accumulate, uc, vc, uf);
 }
 

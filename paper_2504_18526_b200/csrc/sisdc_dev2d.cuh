@@ -1,0 +1,115 @@
+// 2-D tensor-product DG-SEM building blocks (sm_100a, fp64).
+//
+// Uniform periodic Cartesian mesh, GLL collocation: the weak convection and
+// the scalar-coefficient SIP operator are sums of the reference's 1-D
+// operators (dgsem.py:205-225, 251-309) applied along x-lines and y-lines.
+// State layout (ncomp, ney, nex, P+1 [y], P+1 [x]); one thread per node.
+#pragma once
+#include "sisdc_dev.cuh"
+
+namespace sisdc {
+
+struct Op2DDev {
+  int nex, ney, p1, nc;
+  long long nn;          // nodes per field = ney*nex*p1*p1
+  long long n;           // nc * nn
+  int problem;
+  double dx, dy, sx, sy, mux, muy;
+  double gamma, nu, ax, ay;
+  const double* tab;     // 1-D element tables (TabOff layout)
+  const double* nu_art;  // per element (ney*nex) or nullptr
+};
+
+constexpr int NC_MAX = 4;
+
+// element / node addressing -------------------------------------------------
+__device__ __forceinline__ long long nidx(const Op2DDev& op, int c, int ey, int ex, int j, int i) {
+  return (((long long)c * op.ney + ey) * op.nex + ex) * (op.p1 * op.p1) + j * op.p1 + i;
+}
+__device__ __forceinline__ int wrapi(int a, int n) {
+  a %= n;
+  return a < 0 ? a + n : a;
+}
+
+// physics (Euler / NS isotropic, scalar advection, scalar Burgers along x) --
+__device__ __forceinline__ void flux2d(const Op2DDev& op, const double* s, int axis, double* f) {
+  if (op.problem == SISDC_EULER2D) {
+    const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
+    const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
+    const double vn = axis == 0 ? vx : vy;
+    f[0] = s[1 + axis];
+    f[1] = s[1] * vn + (axis == 0 ? p : 0.0);
+    f[2] = s[2] * vn + (axis == 1 ? p : 0.0);
+    f[3] = vn * (s[3] + p);
+  } else if (op.problem == SISDC_ADVECTION2D) {
+    f[0] = (axis == 0 ? op.ax : op.ay) * s[0];
+  } else {   // Burgers2D: x-flux only
+    f[0] = axis == 0 ? 0.5 * s[0] * s[0] : 0.0;
+  }
+}
+__device__ __forceinline__ double speed2d(const Op2DDev& op, const double* s, int axis) {
+  if (op.problem == SISDC_EULER2D) {
+    const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
+    const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
+    return fabs(axis == 0 ? vx : vy) + sqrt(op.gamma * p / rho);
+  }
+  if (op.problem == SISDC_ADVECTION2D) return fabs(axis == 0 ? op.ax : op.ay);
+  return axis == 0 ? fabs(s[0]) : 0.0;
+}
+__device__ __forceinline__ double lam_max2d(const Op2DDev& op, const double* s) {
+  if (op.problem == SISDC_EULER2D) {
+    const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
+    const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
+    return sqrt(vx * vx + vy * vy) + sqrt(op.gamma * p / rho);
+  }
+  if (op.problem == SISDC_ADVECTION2D) return hypot(op.ax, op.ay);
+  return fabs(s[0]);
+}
+
+// coefficient at a node (element eg = ey*nex+ex, in-field node index) --------
+__device__ __forceinline__ bool phys2d(const Op2DDev& op, int eg, double& c) {
+  if (op.nu_art) {
+    c = (op.nu > 0.0 ? op.nu : 0.0) + op.nu_art[eg];
+    return true;
+  }
+  c = op.nu;
+  return op.nu > 0.0;
+}
+__device__ __forceinline__ double coef2d(const Op2DDev& op, const CoefDev& k, int ey, int ex, int j, int i) {
+  const int eg = ey * op.nex + ex;
+  switch (k.kind) {
+    case SISDC_COEF_CONST: return k.value;
+    case SISDC_COEF_FIELD: return k.ptr[(long long)eg * op.p1 * op.p1 + j * op.p1 + i];
+    case SISDC_COEF_SI: {
+      double s[NC_MAX];
+      for (int c = 0; c < op.nc; ++c) s[c] = k.ptr[nidx(op, c, ey, ex, j, i)];
+      const double lam = lam_max2d(op, s);
+      const double half = 0.5 * k.value * (lam * lam);
+      double ph;
+      return phys2d(op, eg, ph) ? half + ph : half;
+    }
+    case SISDC_COEF_PHYS: {
+      double ph;
+      return phys2d(op, eg, ph) ? ph : 0.0;
+    }
+    default: return 0.0;
+  }
+}
+
+// tensor-product transfer tables (same table layout as XferDev)
+struct Xfer2Dev {
+  int nslab, pc, pf, Mc, Mf;
+  const double* tab;   // It (Mf*Mc) | Pt (Mc*Mf) | Isp (pf*pc) | Psp (pc*pf)
+};
+
+// ---------------------------------------------------------------- Rusanov
+__device__ __forceinline__ void rusanov2d(const Op2DDev& op, const double* um, const double* up, int axis,
+                                          double* fh) {
+  double fm[NC_MAX], fp[NC_MAX];
+  flux2d(op, um, axis, fm);
+  flux2d(op, up, axis, fp);
+  const double lam = fmax(speed2d(op, um, axis), speed2d(op, up, axis));
+  for (int c = 0; c < op.nc; ++c) fh[c] = 0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[c] - um[c]);
+}
+
+}  // namespace sisdc

@@ -10,6 +10,8 @@ namespace sisdc {
 struct Op1DDev;
 struct CoefDev;
 struct XferDev;
+struct Op2DDev;
+struct Xfer2Dev;
 
 struct Ctx {
   int device = 0;
@@ -63,5 +65,22 @@ int launch_xfer_down(Ctx* c, const XferDev& x, int sdir, int tdir, const double*
 int launch_xfer_interp(Ctx* c, const XferDev& x, int accumulate, const double* uc, const double* vc, double* uf);
 int launch_persson(Ctx* c, const Op1DDev& op, const double* u, double kappa, double cs, double* nu_art);
 int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x);
+// 2-D (ops2d.cu)
+int launch2_conv(Ctx* c, const Op2DDev& op, const double* u, double* out);
+int launch2_sip(Ctx* c, const Op2DDev& op, CoefDev k, const double* u, double* out);
+int launch2_coef(Ctx* c, const Op2DDev& op, CoefDev k, double* out);
+int launch2_node_eval(Ctx* c, const Op2DDev& op, int mode, int scheme, int M, int m_first, int m_count,
+                      const double* u0, const double* u, const double* conv_prev, const double* dts,
+                      double* f, double* h1, double* h2);
+int launch2_stage(Ctx* c, const Op2DDev& op, const double* base, const double* conv_in, double dt_m,
+                  const double* f_old, int M, const double* w_row, double dt, const double* g,
+                  const double* h, double* rhs, double* conv_out);
+int launch2x_spatial(Ctx* c, const Xfer2Dev& x, int dir, const double* in, double* out);
+int launch2x_down(Ctx* c, const Xfer2Dev& x, int sdir, int tdir, const double* in, double* out);
+int launch2x_fas(Ctx* c, const Xfer2Dev& x, const double* Wf, double dt, int incremental, const double* u0f,
+                 const double* uf, const double* ff, const double* gf, double* v, double* rr);
+int launch2x_interp(Ctx* c, const Xfer2Dev& x, int accumulate, const double* uc, const double* vc, double* uf);
+int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int nblocks);
+int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks);
 
 }  // namespace sisdc

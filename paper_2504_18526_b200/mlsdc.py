@@ -307,14 +307,18 @@ def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes:
                       n_coarse: int = 2, n_sweep: int = 1, post_sweep_on_finest: bool = True) -> Hierarchy:
     """Hierarchy of p-levels on one mesh as the reference CLI builds it
     (``cli.py:776-815``); ``make_op(degree)`` returns a DGOperator."""
-    from .transfer import build_spatial_p_transfer
+    from .transfer import build_spatial_p_transfer, build_spatial_p_transfer_2d
     ops = [make_op(p) for p in degrees]
     rules = [make_nodes(nodes, M) for M in node_counts]
     levels = [Level(o, r, make_weights(r), scheme) for o, r in zip(ops, rules)]
     transfers = []
     for lo, hi in zip(range(len(ops) - 1), range(1, len(ops))):
         pair = build_temporal_transfer(rules[lo], rules[hi])
-        spatial = build_spatial_p_transfer(degrees[lo], degrees[hi], ops[lo].mesh.n_elem, ops[lo].ncomp)
+        if getattr(ops[lo], "is2d", False):
+            spatial = build_spatial_p_transfer_2d(degrees[lo], degrees[hi], ops[lo].mesh.nex, ops[lo].mesh.ney,
+                                                  ops[lo].ncomp)
+        else:
+            spatial = build_spatial_p_transfer(degrees[lo], degrees[hi], ops[lo].mesh.n_elem, ops[lo].ncomp)
         transfers.append(SpaceTimeTransfer(pair, spatial))
     return Hierarchy(levels, transfers, n_coarse=n_coarse, n_sweep=n_sweep, form="incremental",
                      post_sweep_on_finest=post_sweep_on_finest)

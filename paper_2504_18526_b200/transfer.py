@@ -90,7 +90,8 @@ class SpatialTransfer:
             return u.clone()
         h = _xfer_handle(self, None)
         dirn = {"interp": 0, "project": 1, "restrict": 2}[direction]
-        out = rt.empty(self.ncomp * self.ne_coarse * (self.np_fine if dirn == 0 else self.np_coarse))
+        npn = self.np_fine if dirn == 0 else self.np_coarse
+        out = rt.empty(self.ncomp * self.ne_coarse * (npn * npn if self.kind == "p2d" else npn))
         rt.bind_stream()
         rt.check(rt.lib.sisdc_xfer_spatial(h.h, dirn, u.data_ptr(), out.data_ptr()), "xfer_spatial")
         return out
@@ -128,8 +129,12 @@ class _XferHandle:
         self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (It, Pt, Isp, Psp)]
         h = C.c_void_p()
         ptrs = [a.ctypes.data_as(_lib.DP) for a in self._keep]
-        rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_fine, spatial.np_coarse, spatial.np_fine, Mc, Mf,
-                                          *ptrs, C.byref(h)), "xfer_create")
+        if spatial.kind == "p2d":   # element slabs of (P+1)^2 nodes, matrices applied in x and y
+            rt.check(rt.lib.sisdc_xfer2d_create(rt.h, spatial.ne_fine * spatial.ncomp, spatial.np_coarse,
+                                                spatial.np_fine, Mc, Mf, *ptrs, C.byref(h)), "xfer2d_create")
+        else:
+            rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_fine, spatial.np_coarse, spatial.np_fine, Mc, Mf,
+                                              *ptrs, C.byref(h)), "xfer_create")
         self.h = h
         self.Mc, self.Mf = Mc, Mf
 
@@ -151,6 +156,15 @@ def _xfer_handle(spatial: SpatialTransfer, temporal: Optional[TransferPair]) -> 
     return h
 
 
+def build_spatial_p_transfer_2d(p_coarse: int, p_fine: int, nex: int, ney: int, ncomp: int = 1) -> SpatialTransfer:
+    """Tensor-product p-transfer on a fixed 2-D mesh: the 1-D GLL Lagrange
+    blocks of ``transfer.py:213-245`` applied along x and along y."""
+    one = build_spatial_p_transfer(p_coarse, p_fine, 1)
+    if one.kind == "identity":
+        return SpatialTransfer("identity", ncomp, nex * ney, nex * ney, p_coarse + 1, p_fine + 1, {}, "embedded")
+    return SpatialTransfer("p2d", ncomp, nex * ney, nex * ney, p_coarse + 1, p_fine + 1, one.blocks, "embedded")
+
+
 def build_identity_spatial(ndof: int) -> SpatialTransfer:
     return SpatialTransfer("identity", 1, 1, 1, ndof, ndof, {}, "embedded")
 
@@ -163,7 +177,7 @@ class SpaceTimeTransfer:
 
     @property
     def handle(self) -> _XferHandle:
-        if self.spatial.kind != "p":
+        if self.spatial.kind not in ("p", "p2d"):
             raise NotImplementedError("the GPU path builds spatial p-transfers")
         return _xfer_handle(self.spatial, self.temporal)
 
@@ -171,10 +185,13 @@ class SpaceTimeTransfer:
         h = self.handle
         rt = h.rt
         x = rt.to_device(nodes)
-        out = rt.empty(h.Mc, self.spatial.ncomp * self.spatial.ne_coarse * self.spatial.np_coarse)
+        out = rt.empty(h.Mc, self.spatial.ncomp * self.spatial.ne_coarse * self._nodes(self.spatial.np_coarse))
         rt.bind_stream()
         rt.check(rt.lib.sisdc_xfer_down(h.h, sdir, tdir, x.data_ptr(), out.data_ptr()), "xfer_down")
         return out
+
+    def _nodes(self, npe):
+        return npe * npe if self.spatial.kind == "p2d" else npe
 
     def project_solution(self, u_nodes_f, u0_f=None):
         return self._down(1, 1, u_nodes_f)
@@ -187,7 +204,7 @@ class SpaceTimeTransfer:
         rt = h.rt
         uc = rt.to_device(nodes_c)
         if out is None:
-            out = rt.empty(h.Mf, self.spatial.ncomp * self.spatial.ne_fine * self.spatial.np_fine)
+            out = rt.empty(h.Mf, self.spatial.ncomp * self.spatial.ne_fine * self._nodes(self.spatial.np_fine))
         rt.bind_stream()
         rt.check(rt.lib.sisdc_xfer_interp(h.h, int(accumulate), uc.data_ptr(),
                                           None if sub is None else sub.data_ptr(), out.data_ptr()), "xfer_interp")
