@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--cpu-sample-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cluster-ctas", type=int, default=0)
@@ -222,7 +222,7 @@ def cg_roofline(hier, rt, torch, dt, reps=64):
     t = e0.elapsed_time(e1) * 1e-3 / reps
     its, _ = rt.cg_log()
     k = float(np.mean(its[n0:n0 + reps])) if len(its) > n0 else float("nan")
-    N, V = op.ndof, 1.0
+    N, V = op.ndof, 1.0 / op.ncomp   # one scalar coefficient per node shared by the fields
     bytes_per = 8.0 * N * ((3 + V) + k * (10 + V))
     op.eager_checks = True
     return t, k, bytes_per
@@ -245,18 +245,31 @@ def run_ours(args):
     rt = get_runtime(local)
     rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=args.cluster_ctas)
 
-    def make_op(P):
-        prob = problems.Burgers(w.params["nu"]) if w.problem == "burgers" else \
-            problems.ConvectionDiffusion(w.params["speed"], w.params["nu"])
-        return dgsem.DGOperator(dgsem.Mesh1D(w.x_left, w.x_right, w.n_elem, P), prob, device=local)
+    is2d = hasattr(w, "nex")
+    if is2d:
+        from paper_2504_18526_b200 import dgsem2d
 
-    hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
-    nodes = dgsem.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes
-    u0 = w.initial_state(nodes)
-    if rank > 0:   # independent replica per rank
-        rng = np.random.default_rng(1000 + rank)
-        u0 = u0 + 1e-3 * np.sin(np.arange(u0.size) * 0.01 + rng.random())
-    dt, n_total = w.time_step(u0, dgsem.compute_delta(w.p_fine))
+        def make_op(P):
+            mesh = dgsem2d.Mesh2D(0.0, w.length, 0.0, w.length, w.nex, w.ney, P)
+            return dgsem2d.DGOperator2D(mesh, dgsem2d.CompressibleEuler2D(w.gamma, w.nu), device=local)
+
+        hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+        X, Y = hier.fine.ctx.mesh.nodes_xy
+        u0 = w.initial_state(X, Y)
+        dt, n_total = w.time_step(u0, dgsem.compute_delta(w.p_fine)), w.n_steps
+    else:
+        def make_op(P):
+            prob = problems.Burgers(w.params["nu"]) if w.problem == "burgers" else \
+                problems.ConvectionDiffusion(w.params["speed"], w.params["nu"])
+            return dgsem.DGOperator(dgsem.Mesh1D(w.x_left, w.x_right, w.n_elem, P), prob, device=local)
+
+        hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+        nodes = dgsem.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes
+        u0 = w.initial_state(nodes)
+        if rank > 0:   # independent replica per rank
+            rng = np.random.default_rng(1000 + rank)
+            u0 = u0 + 1e-3 * np.sin(np.arange(u0.size) * 0.01 + rng.random())
+        dt, n_total = w.time_step(u0, dgsem.compute_delta(w.p_fine))
     g = mlsdc.SlabGraph(hier, u0, 0.0, dt, w.n_cycles, "fmg")
     U, U_fine = w.dof_sweeps_per_step()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=rt.device)   # > 126 MB L2
@@ -314,7 +327,7 @@ def run_ours(args):
     peak, peak_kind = measured_hbm_peak()
     achieved = bytes_cg / t_cg / 1e9
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not is2d:
         rate, tstep = cpu_port_rate(w, args.cpu_sample_steps, threads_limit=1)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"{args.cpu_sample_steps} SI-MLSDC steps of {w.name} from the seeded IC, "
@@ -327,8 +340,9 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic seeded IC (SURVEY 8d); periodic Burgers, no dataset",
             "config": {
-                "workload": w.name + " (BASELINE configs[1])",
-                "n_elem": w.n_elem, "degrees": [w.p_coarse, w.p_fine], "nodes": [w.m_coarse, w.m_fine],
+                "workload": w.name + (" (BASELINE configs[1])" if not is2d else " (BASELINE 2-D config)"),
+                "n_elem": (w.nex * w.ney) if is2d else w.n_elem, "degrees": [w.p_coarse, w.p_fine],
+                "nodes": [w.m_coarse, w.m_fine],
                 "dt": dt, "steps_to_t_end": n_total,
                 "schedule": f"SI(2) incremental, radau_right, fmg start, {w.n_cycles} V-cycles + closing fine "
                             "sweep (5 cycles diverge in the reference itself, DESIGN.md)",

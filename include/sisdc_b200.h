@@ -170,14 +170,16 @@ int  sisdc_collocation_defect(sisdc_op1d* op, int M, const double* W, double dt,
 
 /* ------------------------------------- space-time p-transfers (transfer.py) */
 /* It (Mf x Mc) = Lagrange(tau_c -> tau_f), Pt (Mc x Mf); Isp ((Pf+1) x (Pc+1)),
- * Psp ((Pc+1) x (Pf+1)); restrictions are the transposes (transfer.py:61-96,213-245). */
+ * Psp ((Pc+1) x (Pf+1)) (transfer.py:61-96,213-245).  The temporal restriction
+ * is It^T; the spatial residual restriction Rsp ((Pc+1) x (Pf+1)) is given, or
+ * NULL for the reference's Isp^T (transfer.py:243). */
 /* 2-D: n_elem = nex*ney*ncomp element slabs, spatial matrices applied in x and y. */
 int  sisdc_xfer2d_create(sisdc_ctx* ctx, int n_elem, int pc1, int pf1, int Mc, int Mf,
                          const double* It, const double* Pt, const double* Isp, const double* Psp,
-                         sisdc_xfer** out);
+                         const double* Rsp, sisdc_xfer** out);
 int  sisdc_xfer_create(sisdc_ctx* ctx, int n_elem, int pc1, int pf1,
                        int Mc, int Mf, const double* It, const double* Pt,
-                       const double* Isp, const double* Psp, sisdc_xfer** out);
+                       const double* Isp, const double* Psp, const double* Rsp, sisdc_xfer** out);
 void sisdc_xfer_destroy(sisdc_xfer* x);
 /* Spatial apply of one state: dir 0 interp (c->f), 1 project (f->c), 2 restrict (f->c). */
 int  sisdc_xfer_spatial(sisdc_xfer* x, int dir, const double* in, double* out);

@@ -268,6 +268,10 @@ class PTransfer2D:
         xc, xf = quad.gll(self.pc)[0], quad.gll(self.pf)[0]
         self.I = quad.lagrange(xc, xf)
         self.Pm = quad.lagrange(xf, xc)
+        # mass-consistent residual restriction M_c^-1 I^T M_f (the 2-D
+        # formulation; the reference's I^T over-injects)
+        wc, wf = quad.gll(self.pc)[1], quad.gll(self.pf)[1]
+        self.R = (1.0 / wc)[:, None] * self.I.T * wf[None, :]
         self.It = quad.lagrange(rule_c.tau, rule_f.tau)
         self.Pt = quad.lagrange(rule_f.tau, rule_c.tau)
 
@@ -282,7 +286,7 @@ class PTransfer2D:
         return np.tensordot(self.Pt, np.stack([self.sp(self.Pm, x, self.pf) for x in uf]), axes=(1, 0))
 
     def restrict_residual(self, rf):
-        return np.tensordot(self.It.T, np.stack([self.sp(self.I.T, x, self.pf) for x in rf]), axes=(1, 0))
+        return np.tensordot(self.It.T, np.stack([self.sp(self.R, x, self.pf) for x in rf]), axes=(1, 0))
 
     def interp(self, dc):
         t = np.tensordot(self.It, dc, axes=(1, 0))

@@ -84,8 +84,8 @@ SIGNATURES = {
     "sisdc_node_caches": (I, [P, I, I, I, I, P, P, P, DP, D, DP, P, P, P]),
     "sisdc_eval_rhs_nodes": (I, [P, I, P, DP, P]),
     "sisdc_collocation_defect": (I, [P, I, DP, D, I, P, P, P, D, P, P]),
-    "sisdc_xfer_create": (I, [P, I, I, I, I, I, DP, DP, DP, DP, C.POINTER(P)]),
-    "sisdc_xfer2d_create": (I, [P, I, I, I, I, I, DP, DP, DP, DP, C.POINTER(P)]),
+    "sisdc_xfer_create": (I, [P, I, I, I, I, I, DP, DP, DP, DP, DP, C.POINTER(P)]),
+    "sisdc_xfer2d_create": (I, [P, I, I, I, I, I, DP, DP, DP, DP, DP, C.POINTER(P)]),
     "sisdc_xfer_destroy": (None, [P]),
     "sisdc_xfer_spatial": (I, [P, I, P, P]),
     "sisdc_xfer_down": (I, [P, I, I, P, P]),

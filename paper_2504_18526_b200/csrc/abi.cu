@@ -462,7 +462,8 @@ int sisdc_collocation_defect(sisdc_op1d* op, int M, const double* W, double dt, 
 
 // ------------------------------------------------------------ transfers
 int sisdc_xfer_create(sisdc_ctx* x, int n_elem, int pc1, int pf1, int Mc, int Mf,
-                      const double* It, const double* Pt, const double* Isp, const double* Psp, sisdc_xfer** out) {
+                      const double* It, const double* Pt, const double* Isp, const double* Psp, const double* Rsp,
+                      sisdc_xfer** out) {
   if (!x || !It || !Pt || !Isp || !Psp || !out) return SISDC_ERR_ARG;
   *out = nullptr;
   if (n_elem < 1 || pc1 < 1 || pf1 < pc1 || pf1 > MAXP1) return x->c.fail(SISDC_ERR_ARG, "bad element sizes");
@@ -477,6 +478,8 @@ int sisdc_xfer_create(sisdc_ctx* x, int n_elem, int pc1, int pf1, int Mc, int Mf
   std::memcpy(tab.data() + xo_Pt(d), Pt, Mf * Mc * sizeof(double));
   std::memcpy(tab.data() + xo_Isp(d), Isp, d.pf * d.pc * sizeof(double));
   std::memcpy(tab.data() + xo_Psp(d), Psp, d.pf * d.pc * sizeof(double));
+  for (int i = 0; i < d.pc; ++i)   // restriction: given, or the reference's I_sp^T (transfer.py:243)
+    for (int j = 0; j < d.pf; ++j) tab[xo_Rsp(d) + i * d.pf + j] = Rsp ? Rsp[i * d.pf + j] : Isp[j * d.pc + i];
   cudaError_t e = cudaMalloc(&t->d_tab, tab.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(t->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -490,8 +493,9 @@ int sisdc_xfer_create(sisdc_ctx* x, int n_elem, int pc1, int pf1, int Mc, int Mf
 }
 
 int sisdc_xfer2d_create(sisdc_ctx* x, int n_elem, int pc1, int pf1, int Mc, int Mf, const double* It,
-                        const double* Pt, const double* Isp, const double* Psp, sisdc_xfer** out) {
-  int rc = sisdc_xfer_create(x, n_elem, pc1, pf1, Mc, Mf, It, Pt, Isp, Psp, out);
+                        const double* Pt, const double* Isp, const double* Psp, const double* Rsp,
+                        sisdc_xfer** out) {
+  int rc = sisdc_xfer_create(x, n_elem, pc1, pf1, Mc, Mf, It, Pt, Isp, Psp, Rsp, out);
   if (rc) return rc;
   sisdc_xfer* t = *out;
   t->dim = 2;

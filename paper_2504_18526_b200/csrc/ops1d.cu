@@ -198,7 +198,8 @@ __global__ void k_xfer_spatial(XferDev x, int dir, const double* __restrict__ in
   const double* Psp = x.tab + xo_Psp(x);
   double acc = 0.0;
   for (int j = 0; j < nin; ++j) {
-    double a = dir == 0 ? Isp[i * x.pc + j] : (dir == 1 ? Psp[i * x.pf + j] : Isp[j * x.pc + i]);
+    const double* Rsp = x.tab + xo_Rsp(x);
+    double a = dir == 0 ? Isp[i * x.pc + j] : (dir == 1 ? Psp[i * x.pf + j] : Rsp[i * x.pf + j]);
     acc = fma(a, in[e * nin + j], acc);
   }
   out[t] = acc;
@@ -241,12 +242,13 @@ __global__ void k_fas_restrict(XferDev x, FasArgs a) {
   const double* Pt = x.tab + xo_Pt(x);
   const double* Isp = x.tab + xo_Isp(x);
   const double* Psp = x.tab + xo_Psp(x);
+  const double* Rsp = x.tab + xo_Rsp(x);
   for (int t = threadIdx.x; t < Mf * pc; t += blockDim.x) {
     int m = t / pc, i = t - m * pc;
     double pu = 0.0, rr = 0.0;
     for (int j = 0; j < pf; ++j) {
       pu = fma(Psp[i * pf + j], su[m * pf + j], pu);
-      rr = fma(Isp[j * pc + i], sr[m * pf + j], rr);
+      rr = fma(Rsp[i * pf + j], sr[m * pf + j], rr);
     }
     sps[t] = pu;
     srs[t] = rr;
@@ -279,7 +281,7 @@ __global__ void k_xfer_down(XferDev x, int sdir, int tdir, const double* __restr
     int m = t / pc, i = t - m * pc;
     double acc = 0.0;
     for (int j = 0; j < pf; ++j)
-      acc = fma(sdir == 1 ? Psp[i * pf + j] : Isp[j * pc + i], in[m * Nf + (size_t)e * pf + j], acc);
+      acc = fma(sdir == 1 ? Psp[i * pf + j] : x.tab[xo_Rsp(x) + i * pf + j], in[m * Nf + (size_t)e * pf + j], acc);
     ss[t] = acc;
   }
   __syncthreads();

@@ -368,8 +368,9 @@ __global__ void __launch_bounds__(256) k2_stage(Op2DDev op, Stage2Args a) {
 __device__ __forceinline__ double xf_spatial_coef(const Xfer2Dev& x, int dir, int a, int b) {
   const double* Isp = x.tab + 2 * x.Mf * x.Mc;
   const double* Psp = Isp + x.pf * x.pc;
-  // dir 0: interp (pf x pc) = Isp[a][b]; 1: project (pc x pf) = Psp[a][b]; 2: restrict = Isp^T
-  return dir == 0 ? Isp[a * x.pc + b] : (dir == 1 ? Psp[a * x.pf + b] : Isp[b * x.pc + a]);
+  const double* Rsp = Psp + x.pf * x.pc;
+  // dir 0: interp (pf x pc) = Isp[a][b]; 1: project (pc x pf) = Psp[a][b]; 2: restrict (pc x pf) = Rsp[a][b]
+  return dir == 0 ? Isp[a * x.pc + b] : (dir == 1 ? Psp[a * x.pf + b] : Rsp[a * x.pf + b]);
 }
 // out_slab = S (x) S applied to one slab: out[ja][ia] = sum S[ja][jb] S[ia][ib] in[jb][ib]
 __device__ __forceinline__ double sp2(const Xfer2Dev& x, int dir, const double* in, int nin, int ja, int ia) {

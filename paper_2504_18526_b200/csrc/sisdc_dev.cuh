@@ -179,13 +179,14 @@ __device__ __forceinline__ void flag_nonfinite(int* status, double v, int e) {
 // space-time p-transfer tables
 struct XferDev {
   int ne, pc, pf, Mc, Mf;
-  const double* tab;   // It (Mf*Mc) | Pt (Mc*Mf) | Isp (pf*pc) | Psp (pc*pf)
+  const double* tab;   // It (Mf*Mc) | Pt (Mc*Mf) | Isp (pf*pc) | Psp (pc*pf) | Rsp (pc*pf)
 };
 __host__ __device__ inline int xo_It(const XferDev&) { return 0; }
 __host__ __device__ inline int xo_Pt(const XferDev& x) { return x.Mf * x.Mc; }
 __host__ __device__ inline int xo_Isp(const XferDev& x) { return 2 * x.Mf * x.Mc; }
 __host__ __device__ inline int xo_Psp(const XferDev& x) { return 2 * x.Mf * x.Mc + x.pf * x.pc; }
-__host__ __device__ inline int xo_size(const XferDev& x) { return 2 * x.Mf * x.Mc + 2 * x.pf * x.pc; }
+__host__ __device__ inline int xo_Rsp(const XferDev& x) { return 2 * x.Mf * x.Mc + 2 * x.pf * x.pc; }
+__host__ __device__ inline int xo_size(const XferDev& x) { return 2 * x.Mf * x.Mc + 3 * x.pf * x.pc; }
 
 
 __global__ void k_reset_status(int* status, int reset_log);

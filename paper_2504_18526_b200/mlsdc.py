@@ -304,7 +304,8 @@ def integrate_mlsdc(hier: Hierarchy, u0_fine, t0: float, dt: float, n_steps: int
 
 
 def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes: str = "radau_right",
-                      n_coarse: int = 2, n_sweep: int = 1, post_sweep_on_finest: bool = True) -> Hierarchy:
+                      n_coarse: int = 2, n_sweep: int = 1, post_sweep_on_finest: bool = True,
+                      restriction: str = None) -> Hierarchy:
     """Hierarchy of p-levels on one mesh as the reference CLI builds it
     (``cli.py:776-815``); ``make_op(degree)`` returns a DGOperator."""
     from .transfer import build_spatial_p_transfer, build_spatial_p_transfer_2d
@@ -316,9 +317,10 @@ def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes:
         pair = build_temporal_transfer(rules[lo], rules[hi])
         if getattr(ops[lo], "is2d", False):
             spatial = build_spatial_p_transfer_2d(degrees[lo], degrees[hi], ops[lo].mesh.nex, ops[lo].mesh.ney,
-                                                  ops[lo].ncomp)
+                                                  ops[lo].ncomp, restriction=restriction or "mass")
         else:
-            spatial = build_spatial_p_transfer(degrees[lo], degrees[hi], ops[lo].mesh.n_elem, ops[lo].ncomp)
+            spatial = build_spatial_p_transfer(degrees[lo], degrees[hi], ops[lo].mesh.n_elem, ops[lo].ncomp,
+                                               restriction=restriction or "transpose")
         transfers.append(SpaceTimeTransfer(pair, spatial))
     return Hierarchy(levels, transfers, n_coarse=n_coarse, n_sweep=n_sweep, form="incremental",
                      post_sweep_on_finest=post_sweep_on_finest)

@@ -97,8 +97,22 @@ class SpatialTransfer:
         return out
 
 
+def mass_consistent_restriction(p_coarse: int, p_fine: int) -> np.ndarray:
+    """R = M_c^-1 I^T M_f with the GLL (lumped) masses: rows sum to exactly 1,
+    so a constant nodal residual restricts to itself.  The reference's
+    R = I^T (``transfer.py:243``) has row sums 1.2-2.3 on GLL p-hierarchies
+    (P 7->3: 1.69/2.31), which over-injects the FAS residual every V-cycle;
+    on BASELINE cfg2 it makes the reference diverge with >= 4 cycles and on the
+    2-D P 7->3 hierarchy with any cycle count."""
+    from .collocation import gauss_lobatto
+    xc, wc = gauss_lobatto(p_coarse + 1)
+    xf, wf = gauss_lobatto(p_fine + 1)
+    I = lagrange_matrix(xc, xf)
+    return (1.0 / wc)[:, None] * I.T * wf[None, :]
+
+
 def build_spatial_p_transfer(p_coarse: int, p_fine: int, n_elem: int, ncomp: int = 1,
-                             projection_kind: str = "embedded") -> SpatialTransfer:
+                             projection_kind: str = "embedded", restriction: str = "transpose") -> SpatialTransfer:
     if p_coarse > p_fine:
         raise ValueError("coarse degree must not exceed fine degree")
     if p_coarse == p_fine:
@@ -111,8 +125,14 @@ def build_spatial_p_transfer(p_coarse: int, p_fine: int, n_elem: int, ncomp: int
         project = _l2_project_matrix(xf, xc, domain=(-1.0, 1.0))
     else:
         raise ValueError(f"unknown projection kind {projection_kind!r}")
+    if restriction == "transpose":
+        restrict = interp.T.copy()          # the reference (transfer.py:243)
+    elif restriction == "mass":
+        restrict = mass_consistent_restriction(p_coarse, p_fine)
+    else:
+        raise ValueError(f"unknown restriction {restriction!r}")
     return SpatialTransfer("p", ncomp, n_elem, n_elem, p_coarse + 1, p_fine + 1,
-                           {"interp": interp, "project": project, "restrict": interp.T.copy()}, projection_kind)
+                           {"interp": interp, "project": project, "restrict": restrict}, projection_kind)
 
 
 class _XferHandle:
@@ -125,8 +145,8 @@ class _XferHandle:
         else:
             It, Pt = temporal.interp, temporal.project
             Mf, Mc = It.shape
-        Isp, Psp = spatial.blocks["interp"], spatial.blocks["project"]
-        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (It, Pt, Isp, Psp)]
+        Isp, Psp, Rsp = spatial.blocks["interp"], spatial.blocks["project"], spatial.blocks["restrict"]
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (It, Pt, Isp, Psp, Rsp)]
         h = C.c_void_p()
         ptrs = [a.ctypes.data_as(_lib.DP) for a in self._keep]
         if spatial.kind == "p2d":   # element slabs of (P+1)^2 nodes, matrices applied in x and y
@@ -156,10 +176,12 @@ def _xfer_handle(spatial: SpatialTransfer, temporal: Optional[TransferPair]) -> 
     return h
 
 
-def build_spatial_p_transfer_2d(p_coarse: int, p_fine: int, nex: int, ney: int, ncomp: int = 1) -> SpatialTransfer:
+def build_spatial_p_transfer_2d(p_coarse: int, p_fine: int, nex: int, ney: int, ncomp: int = 1,
+                                restriction: str = "mass") -> SpatialTransfer:
     """Tensor-product p-transfer on a fixed 2-D mesh: the 1-D GLL Lagrange
-    blocks of ``transfer.py:213-245`` applied along x and along y."""
-    one = build_spatial_p_transfer(p_coarse, p_fine, 1)
+    blocks of ``transfer.py:213-245`` applied along x and along y; the 2-D
+    formulation restricts residuals mass-consistently by default."""
+    one = build_spatial_p_transfer(p_coarse, p_fine, 1, restriction=restriction)
     if one.kind == "identity":
         return SpatialTransfer("identity", ncomp, nex * ney, nex * ney, p_coarse + 1, p_fine + 1, {}, "embedded")
     return SpatialTransfer("p2d", ncomp, nex * ney, nex * ney, p_coarse + 1, p_fine + 1, one.blocks, "embedded")
