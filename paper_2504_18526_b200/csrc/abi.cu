@@ -345,9 +345,10 @@ int sisdc_op2d_create(sisdc_ctx* x, const sisdc_op2d_desc* d, sisdc_op1d** out) 
     return rc;
   }
   v.tab = op->d_tab;
-  int rc = cg2_blocks(&c, v, &op->cg_blocks);
+  int rc = set_cg2_tables(&c, p1, tab.data());
+  if (!rc) rc = cg2_blocks(&c, v, &op->cg_blocks);
   if (rc) { cudaFree(op->d_tab); delete op; return rc; }
-  const size_t ws = 4 * (size_t)v.n + 2 * (size_t)v.nn + 16 + 4 * (size_t)op->cg_blocks;
+  const size_t ws = 4 * (size_t)v.n + 2 * (size_t)v.nn + 16 + 8 * (size_t)op->cg_blocks;
   e = cudaMalloc(&op->d_cgws, ws * sizeof(double));
   if (e != cudaSuccess) {
     rc = c.cuda(e, "op2d CG workspace");

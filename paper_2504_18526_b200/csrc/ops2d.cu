@@ -2,6 +2,7 @@
 // stages, tensor-product space-time transfers and the grid-persistent
 // Chronopoulos-Gear PCG over HBM-resident vectors.
 #include <cooperative_groups.h>
+#include <vector>
 #include "sisdc_dev2d.cuh"
 #include "sisdc_host.h"
 
@@ -484,10 +485,19 @@ __global__ void k2x_interp(Xfer2Dev x, int accumulate, const double* __restrict_
 
 // ------------------------------------------------- grid-persistent 2-D PCG
 // Chronopoulos-Gear Jacobi-PCG (oracle/cg.py) on HBM-resident vectors.  u is
-// never stored: u = r * dinv on the fly.  Per iteration three grid-wide
-// phases: A (stream p, s, x, r; partial (r,u), (r,r)), B (w = A u element
-// matvec; partial (w,u)), R (block 0 reduces the partials in a fixed order ->
-// alpha, beta, convergence), each followed by a grid barrier.
+// never stored: u = r * dinv on the fly.  Each iteration is two grid-wide
+// phases, each closed by one grid barrier:
+//   A  streaming update of p, s, x, r over (in-field node, field) with
+//      16-byte accesses, partials (r,u) and (r,r);
+//   B  w = A u over strip tiles (EB consecutive elements of one row) staged in
+//      shared memory with their x/y neighbours by coalesced loads.  The
+//      element contractions run per grid LINE (one thread = one x-row or
+//      y-column of one element and field) with the reference-element
+//      matrices in the constant bank, so the only shared-memory traffic is
+//      the line itself (padded rows: conflict-free); partial (w,u).
+// After the barrier every block reduces the per-block partials itself in one
+// fixed order, so all blocks hold bitwise-identical alpha/beta and there is no
+// separate reduction phase; partial slots alternate between iterations.
 struct Cg2Args {
   Op2DDev op;
   CoefDev coef;
@@ -502,7 +512,7 @@ struct Cg2Args {
   double* S;
   double* DINV;   // per in-field node
   double* Cf;     // per in-field node
-  double* part;   // [gridDim][4]
+  double* part;   // [2][gridDim][4]
   double* scal;   // [16]
   int* status;
   int* log_it;
@@ -510,48 +520,300 @@ struct Cg2Args {
   int log_cap;
 };
 
+// reference-element matrices per P1 in the constant bank: D | DTW | D2W | w
+__host__ __device__ constexpr int ctab_off(int p1) {
+  int o = 0;
+  for (int p = 2; p < p1; ++p) o += 3 * p * p + p;
+  return o;
+}
+__constant__ double c_tab2[ctab_off(10)];
 template <int P1>
-__global__ void __launch_bounds__(256) k2_cg(Cg2Args A) {
+struct CT {
+  static constexpr int D = ctab_off(P1), DTW = D + P1 * P1, D2W = DTW + P1 * P1, W = D2W + P1 * P1;
+};
+
+// shared-memory carve (doubles) of the CG strip tiles; element rows padded to
+// P1+1 so line accesses are bank-conflict free
+template <int P1>
+struct CgSm {
+  static constexpr int NN = P1 * P1, EB = Blk<P1>::EB, RP = P1 + 1, NP = P1 * RP;
+  static constexpr int NS = 3 * EB + 2;   // slots: 0 left, 1..cnt own, cnt+1 right, EB+2.. above, 2EB+2.. below
+  static constexpr int U = 0;                                   // [NC_MAX][NS][NP]
+  static constexpr int C = U + NC_MAX * NS * NP;                // [NS][NP] coefficient
+  static constexpr int QX = C + NS * NP, QY = QX + NC_MAX * EB * NP;   // [NC_MAX][EB][NP]
+  static constexpr int BX = QY + NC_MAX * EB * NP, BY = BX + NC_MAX * EB * NP;
+  static constexpr int FQ = BY + NC_MAX * EB * NP;              // [NC_MAX][EB][4][P1] neighbour face fluxes
+  static constexpr int RED = FQ + NC_MAX * EB * 4 * P1;         // [32][4]
+  static constexpr int SIZE = RED + 128;
+  static_assert(Sm2<P1>::FU <= C, "setup scratch exceeds the U region");
+};
+
+// One strip tile of w = (M + a B2) v (B2 as in sip_block MODE 1, same operation
+// order), v = src * scale (scale per in-field node, or null).  epi(g, w, v) per
+// own node and field, g the global index.
+template <int P1, typename Epi>
+__device__ __forceinline__ void cg_tile(const Op2DDev& op, double* sm, int tile, int tpr, const double* src,
+                                        const double* scale, const double* Cf, double a, Epi&& epi) {
+  using L = CgSm<P1>;
+  using T = CT<P1>;
+  constexpr int NN = P1 * P1, EB = Blk<P1>::EB, P = P1 - 1, RP = L::RP, NP = L::NP, NS = L::NS;
+  const int nc = op.nc;
+  const long long fld = op.nn;
+  const int ey = tile / tpr, ex0 = (tile - ey * tpr) * EB;
+  const int cnt = min(EB, op.nex - ex0);
+  // tile-variant zero (tile < 2^30): keeps the constant-bank matrix loads inside the
+  // tile loop (uniform-register operands) instead of hoisted into the register file
+  const double* ct = c_tab2 + (tile >> 30);
+  const long long rowm = (long long)ey * op.nex;
+  const long long rowt = (long long)wrapi(ey + 1, op.ney) * op.nex;
+  const long long rowb = (long long)wrapi(ey - 1, op.ney) * op.nex;
+  const int exl = wrapi(ex0 - 1, op.nex), exr = wrapi(ex0 + cnt, op.nex);
+  __syncthreads();   // the previous tile's readers are done with the buffers
+  // ---- stage: strip + x-halo (slots 0..cnt+1), rows above / below (contiguous runs)
+  {
+    const int n1 = (cnt + 2) * NN, ntot = n1 + 2 * cnt * NN;
+    for (int t = threadIdx.x; t < ntot; t += blockDim.x) {
+      long long f;
+      int slot, nd;
+      if (t < n1) {
+        const int s = t / NN;
+        nd = t - s * NN;
+        slot = s;
+        f = (rowm + (s == 0 ? exl : (s == cnt + 1 ? exr : ex0 + s - 1))) * NN + nd;
+      } else {
+        const int tt = t - n1;
+        const bool up = tt < cnt * NN;
+        const int t2 = up ? tt : tt - cnt * NN;
+        const int el = t2 / NN;
+        nd = t2 - el * NN;
+        slot = (up ? EB + 2 : 2 * EB + 2) + el;
+        f = ((up ? rowt : rowb) + ex0) * NN + t2;
+      }
+      const int jj = nd / P1, o = slot * NP + jj * RP + (nd - jj * P1);
+      const double sc = scale ? scale[f] : 1.0;
+      sm[L::C + o] = Cf[f];
+#pragma unroll
+      for (int c = 0; c < NC_MAX; ++c)
+        if (c < nc) {
+          const double v = src[c * fld + f];
+          sm[L::U + c * NS * NP + o] = scale ? v * sc : v;
+        }
+    }
+  }
+  __syncthreads();
+  const int nl = nc * cnt * P1;   // element lines per direction
+  // ---- fluxes q = C s D v along every own x-row / y-column; neighbour face fluxes
+  for (int it = threadIdx.x; it < 2 * nl; it += blockDim.x) {
+    const bool yd = it >= nl;
+    const int r = yd ? it - nl : it;
+    const int c = r / (cnt * P1), rem = r - c * cnt * P1, el = rem / P1, l = rem - el * P1;
+    const int base = yd ? l : l * RP, stride = yd ? RP : 1;
+    const double* U = sm + L::U + (c * NS + el + 1) * NP + base;
+    const double* Cc = sm + L::C + (el + 1) * NP + base;
+    double* Q = sm + (yd ? L::QY : L::QX) + (c * EB + el) * NP + base;
+    const double s = yd ? op.sy : op.sx;
+    double u[P1];
+#pragma unroll
+    for (int q = 0; q < P1; ++q) u[q] = U[q * stride];
+#pragma unroll
+    for (int i = 0; i < P1; ++i) {
+      double g = 0.0;
+#pragma unroll
+      for (int q = 0; q < P1; ++q) g = fma(ct[T::D + i * P1 + q], u[q], g);
+      Q[i * stride] = Cc[i * stride] * (s * g);
+    }
+  }
+  for (int it = threadIdx.x; it < 4 * nl; it += blockDim.x) {
+    const int c = it / (cnt * 4 * P1), rem = it - c * cnt * 4 * P1, el = rem / (4 * P1), r2 = rem - el * 4 * P1;
+    const int face = r2 / P1, k = r2 - face * P1;
+    const double* Un = sm + L::U + c * NS * NP;
+    double g = 0.0, cf, s;
+    if (face == FR) {          // right neighbour, row k, derivative at its node (k,0)
+      const double* row = Un + (el + 2) * NP + k * RP;
+#pragma unroll
+      for (int q = 0; q < P1; ++q) g = fma(ct[T::D + q], row[q], g);
+      cf = sm[L::C + (el + 2) * NP + k * RP];
+      s = op.sx;
+    } else if (face == FL) {   // left neighbour, row k, at its node (k,P)
+      const double* row = Un + el * NP + k * RP;
+#pragma unroll
+      for (int q = 0; q < P1; ++q) g = fma(ct[T::D + P * P1 + q], row[q], g);
+      cf = sm[L::C + el * NP + k * RP + P];
+      s = op.sx;
+    } else if (face == FT) {   // element above, column k, at its node (0,k)
+      const double* col = Un + (EB + 2 + el) * NP + k;
+#pragma unroll
+      for (int q = 0; q < P1; ++q) g = fma(ct[T::D + q], col[q * RP], g);
+      cf = sm[L::C + (EB + 2 + el) * NP + k];
+      s = op.sy;
+    } else {                   // element below, column k, at its node (P,k)
+      const double* col = Un + (2 * EB + 2 + el) * NP + k;
+#pragma unroll
+      for (int q = 0; q < P1; ++q) g = fma(ct[T::D + P * P1 + q], col[q * RP], g);
+      cf = sm[L::C + (2 * EB + 2 + el) * NP + P * RP + k];
+      s = op.sy;
+    }
+    sm[L::FQ + ((c * EB + el) * 4 + face) * P1 + k] = cf * (s * g);
+  }
+  __syncthreads();
+  // ---- SIP accumulators per line: volume DTW q, face terms, adjoint lifting
+  for (int it = threadIdx.x; it < 2 * nl; it += blockDim.x) {
+    const bool yd = it >= nl;
+    const int r = yd ? it - nl : it;
+    const int c = r / (cnt * P1), rem = r - c * cnt * P1, el = rem / P1, l = rem - el * P1;
+    const int base = yd ? l : l * RP, stride = yd ? RP : 1;
+    const double* Q = sm + (yd ? L::QY : L::QX) + (c * EB + el) * NP + base;
+    const double* U = sm + L::U + (c * NS + el + 1) * NP + base;
+    const double* Cc = sm + L::C + (el + 1) * NP + base;
+    const double* fq = sm + L::FQ + (c * EB + el) * 4 * P1;
+    double q[P1];
+#pragma unroll
+    for (int k = 0; k < P1; ++k) q[k] = Q[k * stride];
+    const double cP = Cc[P * stride], c0 = Cc[0];
+    double jp, jm, fcp, fcm, qp, qm, mu, s;
+    if (!yd) {   // row l: right face at (l,P), left face at (l,0)
+      const int ub = (c * NS) * NP + l * RP;
+      jp = U[P] - sm[L::U + ub + (el + 2) * NP];
+      jm = sm[L::U + ub + el * NP + P] - U[0];
+      fcp = sm[L::C + (el + 2) * NP + l * RP];
+      fcm = sm[L::C + el * NP + l * RP + P];
+      qp = fq[FR * P1 + l];
+      qm = fq[FL * P1 + l];
+      mu = op.mux;
+      s = op.sx;
+    } else {     // column l: top face at (P,l), bottom face at (0,l)
+      const int ub = (c * NS) * NP + l;
+      jp = U[P * RP] - sm[L::U + ub + (EB + 2 + el) * NP];
+      jm = sm[L::U + ub + (2 * EB + 2 + el) * NP + P * RP] - U[0];
+      fcp = sm[L::C + (EB + 2 + el) * NP + l];
+      fcm = sm[L::C + (2 * EB + 2 + el) * NP + P * RP + l];
+      qp = fq[FT * P1 + l];
+      qm = fq[FB * P1 + l];
+      mu = op.muy;
+      s = op.sy;
+    }
+    const double fp = -(0.5 * (q[P] + qp)) + (mu * (0.5 * (cP + fcp))) * jp;
+    const double fm = -(0.5 * (qm + q[0])) + (mu * (0.5 * (fcm + c0))) * jm;
+    const double lp = s * ((0.5 * cP) * jp), lm = s * ((0.5 * c0) * jm);
+    double* Bo = sm + (yd ? L::BY : L::BX) + (c * EB + el) * NP + base;
+#pragma unroll
+    for (int i = 0; i < P1; ++i) {
+      double b = 0.0;
+#pragma unroll
+      for (int k = 0; k < P1; ++k) b = fma(ct[T::DTW + i * P1 + k], q[k], b);
+      if (i == P) b += fp;
+      if (i == 0) b -= fm;
+      b -= lp * ct[T::D + P * P1 + i];
+      Bo[i * stride] = b - lm * ct[T::D + i];
+    }
+  }
+  __syncthreads();
+  // ---- combine per node: w = a (hwy Bx + hwx By) + hwx hwy v
+  const int el = threadIdx.x / NN;
+  if (el >= cnt) return;
+  const int nd = threadIdx.x - el * NN, j = nd / P1, i = nd - j * P1, o = el * NP + j * RP + i;
+  const double hwx = 0.5 * op.dx * ct[T::W + i], hwy = 0.5 * op.dy * ct[T::W + j];
+  const long long g0 = (rowm + ex0 + el) * NN + nd;
+  for (int c = 0; c < nc; ++c) {
+    const double Bx = sm[L::BX + c * EB * NP + o], By = sm[L::BY + c * EB * NP + o];
+    const double v = sm[L::U + (c * NS + 1) * NP + o];
+    epi(c * fld + g0, fma(a, fma(hwy, Bx, hwx * By), (hwx * hwy) * v), v);
+  }
+}
+
+// phase A over in-field nodes [f, f+2) of all fields; returns partials via ru, rr
+__device__ __forceinline__ void cg_update2(const Cg2Args& A, long long h, long long nh, int nc, double alpha,
+                                           double beta, double& ru, double& rr) {
+  const double2 di = reinterpret_cast<const double2*>(A.DINV)[h];
+#pragma unroll
+  for (int c = 0; c < NC_MAX; ++c)
+    if (c < nc) {
+      const long long t = c * nh + h;
+      double2 r = reinterpret_cast<const double2*>(A.R)[t];
+      const double2 pv = reinterpret_cast<const double2*>(A.Pv)[t];
+      const double2 sv = reinterpret_cast<const double2*>(A.S)[t];
+      const double2 wv = reinterpret_cast<const double2*>(A.W)[t];
+      const double2 xv = reinterpret_cast<const double2*>(A.x)[t];
+      double2 p, s, x;
+      p.x = fma(beta, pv.x, r.x * di.x);
+      p.y = fma(beta, pv.y, r.y * di.y);
+      s.x = fma(beta, sv.x, wv.x);
+      s.y = fma(beta, sv.y, wv.y);
+      x.x = fma(alpha, p.x, xv.x);
+      x.y = fma(alpha, p.y, xv.y);
+      r.x = fma(-alpha, s.x, r.x);
+      r.y = fma(-alpha, s.y, r.y);
+      reinterpret_cast<double2*>(A.Pv)[t] = p;
+      reinterpret_cast<double2*>(A.S)[t] = s;
+      reinterpret_cast<double2*>(A.x)[t] = x;
+      reinterpret_cast<double2*>(A.R)[t] = r;
+      ru = fma(r.x, r.x * di.x, ru);
+      rr = fma(r.x, r.x, rr);
+      ru = fma(r.y, r.y * di.y, ru);
+      rr = fma(r.y, r.y, rr);
+    }
+}
+
+template <int P1>
+__global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   extern __shared__ double sm[];
+  using L = CgSm<P1>;
+  using T = CT<P1>;
   cg::grid_group grid = cg::this_grid();
   const Op2DDev& op = A.op;
-  constexpr int NN = P1 * P1, P = P1 - 1;
-  load_tab2<P1>(sm + Sm2<P1>::ST, op.tab);
-  __syncthreads();
-  const double* st = sm + Sm2<P1>::ST;
-  const double* D2W = st + TabOff::D2W(P1);
-  const double* D = st + TabOff::D(P1);
-  const double* w = st + TabOff::w(P1);
-  const int ntiles = (op.nex * op.ney + Blk<P1>::EB - 1) / Blk<P1>::EB;
-  const long long nthr = (long long)gridDim.x * blockDim.x;
+  constexpr int NN = P1 * P1, P = P1 - 1, EB = Blk<P1>::EB;
+  const int nc = op.nc;
+  const long long nn = op.nn;
+  const int G = gridDim.x;
+  const int tpr = (op.nex + EB - 1) / EB, ntiles = tpr * op.ney;
+  const long long nthr = (long long)G * blockDim.x;
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  double* red = sm;   // block reduction scratch (aliases FX, unused here) [32][4]
-  auto block_sum = [&](double (&v)[3]) {
+  const bool vec = (nn & 1) == 0 && ((reinterpret_cast<uintptr_t>(A.x) & 15) == 0);
+  double* red = sm + L::RED;
+  // per-block partials of three sums -> slot[blockIdx]
+  auto block_part = [&](double v0, double v1, double v2, double* slot) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int q = 0; q < 3; ++q)
-      for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
-    if (lane == 0)
-      for (int q = 0; q < 3; ++q) red[wid * 4 + q] = v[q];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t[3] = {0.0, 0.0, 0.0};
-      for (int ww = 0; ww < nw; ++ww)
-        for (int q = 0; q < 3; ++q) t[q] += red[ww * 4 + q];
-      for (int q = 0; q < 3; ++q) A.part[blockIdx.x * 4 + q] = t[q];
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+      v2 += __shfl_xor_sync(0xffffffffu, v2, o);
     }
     __syncthreads();
+    if (lane == 0) { red[wid * 4] = v0; red[wid * 4 + 1] = v1; red[wid * 4 + 2] = v2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+      for (int ww = 0; ww < nw; ++ww) { t0 += red[ww * 4]; t1 += red[ww * 4 + 1]; t2 += red[ww * 4 + 2]; }
+      slot[blockIdx.x * 4] = t0; slot[blockIdx.x * 4 + 1] = t1; slot[blockIdx.x * 4 + 2] = t2;
+    }
   };
-  auto mass = [&](long long f) -> double {   // lumped mass of in-field node f
-    const int nd = (int)(f % NN);
-    return (0.5 * op.dx * w[nd % P1]) * (0.5 * op.dy * w[nd / P1]);
+  // after a grid barrier: every block sums all slots in the same fixed order
+  auto grid_total = [&](const double* slot, double (&t)[3]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int b = threadIdx.x; b < G; b += blockDim.x) { v0 += slot[b * 4]; v1 += slot[b * 4 + 1]; v2 += slot[b * 4 + 2]; }
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+      v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+    }
+    __syncthreads();
+    if (lane == 0) { red[wid * 4] = v0; red[wid * 4 + 1] = v1; red[wid * 4 + 2] = v2; }
+    __syncthreads();
+    t[0] = t[1] = t[2] = 0.0;
+    for (int ww = 0; ww < nw; ++ww) { t[0] += red[ww * 4]; t[1] += red[ww * 4 + 1]; t[2] += red[ww * 4 + 2]; }
   };
+  double* slot0 = A.part;
+  double* slot1 = A.part + 4 * G;
   // ---- setup 1: C, dinv per in-field node (closed-form diag of M + a B2), x0 = rhs, p = s = 0
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int ntiles_el = (op.nex * op.ney + EB - 1) / EB;
+  for (int tile = blockIdx.x; tile < ntiles_el; tile += G) {
     const Node2 n = node2<P1>(op, tile);
     double* CS = sm + Sm2<P1>::CS + n.el * NN;
     double* FCo = sm + Sm2<P1>::FC + n.el * 4 * P1;
     const int exr = wrapi(n.ex + 1, op.nex), exl = wrapi(n.ex - 1, op.nex);
     const int eyt = wrapi(n.ey + 1, op.ney), eyb = wrapi(n.ey - 1, op.ney);
+    __syncthreads();
     if (n.valid) {
       CS[n.nd] = coef2d(op, A.coef, n.ey, n.ex, n.j, n.i);
       if (n.i == P) FCo[FR * P1 + n.j] = coef2d(op, A.coef, n.ey, exr, n.j, 0);
@@ -563,22 +825,23 @@ __global__ void __launch_bounds__(256) k2_cg(Cg2Args A) {
     if (n.valid) {
       const int i = n.i, j = n.j;
       double dx_ = 0.0, dy_ = 0.0;
+#pragma unroll
       for (int q = 0; q < P1; ++q) {
-        dx_ = fma(D2W[i * P1 + q], CS[j * P1 + q], dx_);
-        dy_ = fma(D2W[j * P1 + q], CS[q * P1 + i], dy_);
+        dx_ = fma(c_tab2[T::D2W + i * P1 + q], CS[j * P1 + q], dx_);
+        dy_ = fma(c_tab2[T::D2W + j * P1 + q], CS[q * P1 + i], dy_);
       }
+      const double DPP = c_tab2[T::D + P * P1 + P], D00 = c_tab2[T::D];
       dx_ *= op.sx;
       dy_ *= op.sy;
-      if (i == P) dx_ += op.mux * (0.5 * (CS[j * P1 + P] + FCo[FR * P1 + j])) - op.sx * CS[j * P1 + P] * D[P * P1 + P];
-      if (i == 0) dx_ += op.mux * (0.5 * (FCo[FL * P1 + j] + CS[j * P1])) + op.sx * CS[j * P1] * D[0];
-      if (j == P) dy_ += op.muy * (0.5 * (CS[P * P1 + i] + FCo[FT * P1 + i])) - op.sy * CS[P * P1 + i] * D[P * P1 + P];
-      if (j == 0) dy_ += op.muy * (0.5 * (FCo[FB * P1 + i] + CS[i])) + op.sy * CS[i] * D[0];
-      const double hwx = 0.5 * op.dx * w[i], hwy = 0.5 * op.dy * w[j];
+      if (i == P) dx_ += op.mux * (0.5 * (CS[j * P1 + P] + FCo[FR * P1 + j])) - op.sx * CS[j * P1 + P] * DPP;
+      if (i == 0) dx_ += op.mux * (0.5 * (FCo[FL * P1 + j] + CS[j * P1])) + op.sx * CS[j * P1] * D00;
+      if (j == P) dy_ += op.muy * (0.5 * (CS[P * P1 + i] + FCo[FT * P1 + i])) - op.sy * CS[P * P1 + i] * DPP;
+      if (j == 0) dy_ += op.muy * (0.5 * (FCo[FB * P1 + i] + CS[i])) + op.sy * CS[i] * D00;
+      const double hwx = 0.5 * op.dx * c_tab2[T::W + i], hwy = 0.5 * op.dy * c_tab2[T::W + j];
       const long long f = (long long)n.eg * NN + n.nd;
       A.Cf[f] = CS[n.nd];
       A.DINV[f] = 1.0 / (hwx * hwy + A.a * (hwy * dx_ + hwx * dy_));
     }
-    __syncthreads();
   }
   for (long long t = gtid; t < op.n; t += nthr) {
     A.x[t] = A.rhs[t];
@@ -586,127 +849,107 @@ __global__ void __launch_bounds__(256) k2_cg(Cg2Args A) {
     A.S[t] = 0.0;
   }
   grid.sync();
-  const CoefDev cfield{SISDC_COEF_FIELD, 0.0, A.Cf};
-  // ---- setup 2: r0 = b - A x0 (b = M rhs), partial (b,b), #nonzero
+  // ---- setup 2: r0 = b - A x0 (b = M rhs); partials (b,b), #nonzero -> slot 0
   {
-    double v[3] = {0.0, 0.0, 0.0};
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const Node2 n = node2<P1>(op, tile);
-      double ax[NC_MAX];
-      sip_block<P1, 1>(op, sm, cfield, A.x, nullptr, op.nc, A.a, n, ax);
-      if (n.valid) {
-        const double mi = (0.5 * op.dx * w[n.i]) * (0.5 * op.dy * w[n.j]);
-        for (int c = 0; c < op.nc; ++c) {
-          const long long g = nidx(op, c, n.ey, n.ex, n.j, n.i);
-          const double b = mi * A.rhs[g];
-          A.R[g] = b - ax[c];
-          v[0] = fma(b, b, v[0]);
-          v[1] += b != 0.0 ? 1.0 : 0.0;
-        }
-      }
-    }
-    block_sum(v);
+    double bb = 0.0, nz = 0.0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += G)
+      cg_tile<P1>(op, sm, tile, tpr, A.x, nullptr, A.Cf, A.a, [&](long long g, double ax, double) {
+        const int nd = (int)(g % NN);
+        const double mi = (0.5 * op.dx * c_tab2[T::W + nd % P1]) * (0.5 * op.dy * c_tab2[T::W + nd / P1]);
+        const double b = mi * A.rhs[g];
+        A.R[g] = b - ax;
+        bb = fma(b, b, bb);
+        nz += b != 0.0 ? 1.0 : 0.0;
+      });
+    block_part(bb, nz, 0.0, slot0);
   }
   grid.sync();
-  // ---- setup 3: w0 = A u0, u0 = r0 dinv; partials gamma, delta, rho
-  double bb = 0.0, nnz = 0.0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double t0 = 0.0, t1 = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) { t0 += A.part[b * 4]; t1 += A.part[b * 4 + 1]; }
-    A.scal[8] = t0;
-    A.scal[9] = t1;
-  }
-  grid.sync();   // the partial slots are reused below
-  auto phase_B = [&]() {   // w = A u, u = r dinv; partial (w,u) into slot 1 (slots 0, 2 from phase A)
-    double v[3] = {0.0, 0.0, 0.0};
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const Node2 n = node2<P1>(op, tile);
-      double wv[NC_MAX];
-      sip_block<P1, 1>(op, sm, cfield, A.R, A.DINV, op.nc, A.a, n, wv);
-      if (n.valid) {
-        const long long f = (long long)n.eg * NN + n.nd;
-        const double di = A.DINV[f];
-        for (int c = 0; c < op.nc; ++c) {
-          const long long g = nidx(op, c, n.ey, n.ex, n.j, n.i);
-          A.W[g] = wv[c];
-          v[1] = fma(wv[c], A.R[g] * di, v[1]);
-        }
-      }
-    }
-    return v[1];
-  };
-  double v3[3] = {0.0, 0.0, 0.0};
-  v3[1] = phase_B();
-  for (long long t = gtid; t < op.n; t += nthr) {
-    const double r = A.R[t], u = r * A.DINV[t % op.nn];
-    v3[0] = fma(r, u, v3[0]);
-    v3[2] = fma(r, r, v3[2]);
-  }
-  block_sum(v3);
-  grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double t[3] = {0.0, 0.0, 0.0};
-    for (int b = 0; b < (int)gridDim.x; ++b)
-      for (int q = 0; q < 3; ++q) t[q] += A.part[b * 4 + q];
-    A.scal[0] = t[0];              // gamma
-    A.scal[1] = t[1];              // delta
-    A.scal[2] = t[2];              // rho
-    A.scal[3] = t[0] / t[1];       // alpha
-    A.scal[4] = 0.0;               // beta
-    A.scal[5] = 1.0 / t[0];        // 1/gamma
-    A.scal[6] = 1.0 / A.scal[3];   // 1/alpha
-  }
-  grid.sync();
-  bb = A.scal[8];
-  nnz = A.scal[9];
-  const double thr = A.rtol2 * bb;
-  if (nnz == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
+  double tot[3];
+  grid_total(slot0, tot);
+  const double thr = A.rtol2 * tot[0];
+  if (tot[1] == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
     for (long long t = gtid; t < op.n; t += nthr) A.x[t] = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      int idx = atomicAdd(&A.status[2], 1);
+      if (idx < A.log_cap) { A.log_it[idx] = 0; A.log_margin[idx] = 0.0; }
+    }
     return;
   }
+  // phase B body: w = A u, u = r dinv; partial (w,u)
+  auto phase_B = [&]() {
+    double wu = 0.0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += G)
+      cg_tile<P1>(op, sm, tile, tpr, A.R, A.DINV, A.Cf, A.a, [&](long long g, double wv, double u) {
+        A.W[g] = wv;
+        wu = fma(wv, u, wu);
+      });
+    return wu;
+  };
+  // ---- setup 3: w0 = A u0; gamma, delta, rho -> slot 1
+  {
+    const double wu = phase_B();
+    double ru = 0.0, rr = 0.0;
+    for (long long f = gtid; f < nn; f += nthr) {
+      const double di = A.DINV[f];
+#pragma unroll
+      for (int c = 0; c < NC_MAX; ++c)
+        if (c < nc) {
+          const double r = A.R[c * nn + f], u = r * di;
+          ru = fma(r, u, ru);
+          rr = fma(r, r, rr);
+        }
+    }
+    block_part(ru, wu, rr, slot1);
+  }
+  grid.sync();
+  grid_total(slot1, tot);
+  double rho = tot[2];
+  double alpha = tot[0] / tot[1], beta = 0.0;
+  double rgam = 1.0 / tot[0], ralpha = 1.0 / alpha;
   int k = 0;
   bool ok = true;
-  double rho = A.scal[2];
   while (rho > thr) {
     if (k >= A.maxit) { ok = false; break; }
-    const double alpha = A.scal[3], beta = A.scal[4];
     // phase A: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s
-    double v[3] = {0.0, 0.0, 0.0};
-    for (long long t = gtid; t < op.n; t += nthr) {
-      const double di = A.DINV[t % op.nn];
-      double r = A.R[t];
-      const double p = fma(beta, A.Pv[t], r * di);
-      const double s = fma(beta, A.S[t], A.W[t]);
-      A.Pv[t] = p;
-      A.S[t] = s;
-      A.x[t] = fma(alpha, p, A.x[t]);
-      r = fma(-alpha, s, r);
-      A.R[t] = r;
-      v[0] = fma(r, r * di, v[0]);
-      v[2] = fma(r, r, v[2]);
+    double ru = 0.0, rr = 0.0;
+    if (vec) {
+      const long long nh = nn >> 1;
+      for (long long h = gtid; h < nh; h += nthr) cg_update2(A, h, nh, nc, alpha, beta, ru, rr);
+    } else {
+      for (long long f = gtid; f < nn; f += nthr) {
+        const double di = A.DINV[f];
+#pragma unroll
+        for (int c = 0; c < NC_MAX; ++c)
+          if (c < nc) {
+            const long long t = c * nn + f;
+            double r = A.R[t];
+            const double p = fma(beta, A.Pv[t], r * di);
+            const double s = fma(beta, A.S[t], A.W[t]);
+            A.Pv[t] = p;
+            A.S[t] = s;
+            A.x[t] = fma(alpha, p, A.x[t]);
+            r = fma(-alpha, s, r);
+            A.R[t] = r;
+            ru = fma(r, r * di, ru);
+            rr = fma(r, r, rr);
+          }
+      }
     }
     grid.sync();
-    v[1] = phase_B();
-    block_sum(v);
+    const double wu = phase_B();
+    double* slot = (k & 1) ? slot1 : slot0;
+    block_part(ru, wu, rr, slot);
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      double t[3] = {0.0, 0.0, 0.0};
-      for (int b = 0; b < (int)gridDim.x; ++b)
-        for (int q = 0; q < 3; ++q) t[q] += A.part[b * 4 + q];
-      const double gn = t[0];
-      const double be = gn * A.scal[5];
-      const double al = gn / (t[1] - be * (gn * A.scal[6]));
-      A.scal[0] = gn;
-      A.scal[1] = t[1];
-      A.scal[2] = t[2];
-      A.scal[3] = al;
-      A.scal[4] = be;
-      A.scal[5] = 1.0 / gn;
-      A.scal[6] = 1.0 / al;
-    }
-    grid.sync();
+    grid_total(slot, tot);
+    const double gn = tot[0];
+    const double be = gn * rgam;
+    const double al = gn / (tot[1] - be * (gn * ralpha));
+    rho = tot[2];
+    alpha = al;
+    beta = be;
+    rgam = 1.0 / gn;
+    ralpha = 1.0 / al;
     ++k;
-    rho = A.scal[2];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     int idx = atomicAdd(&A.status[2], 1);
@@ -718,9 +961,27 @@ __global__ void __launch_bounds__(256) k2_cg(Cg2Args A) {
   }
 }
 
+// constant-bank copy of the reference-element matrices for one P1 (idempotent:
+// they depend on P1 only); called at operator creation, outside any capture
+int set_cg2_tables(Ctx* c, int p1, const double* tab) {
+  if (p1 < 2 || p1 > 9) return c->fail(SISDC_ERR_UNSUPPORTED, "2-D degree outside 1..8");
+  std::vector<double> h(3 * p1 * p1 + p1);
+  for (int t = 0; t < p1 * p1; ++t) {
+    h[t] = tab[TabOff::D(p1) + t];
+    h[p1 * p1 + t] = tab[TabOff::DTW(p1) + t];
+    h[2 * p1 * p1 + t] = tab[TabOff::D2W(p1) + t];
+  }
+  for (int t = 0; t < p1; ++t) h[3 * p1 * p1 + t] = tab[TabOff::w(p1) + t];
+  cudaError_t e = cudaMemcpyToSymbol(c_tab2, h.data(), h.size() * sizeof(double), ctab_off(p1) * sizeof(double));
+  if (e != cudaSuccess) return c->cuda(e, "2-D constant tables");
+  return SISDC_OK;
+}
+
 // ------------------------------------------------------------- launchers
 template <int P1>
 static size_t smem2() { return sizeof(double) * Sm2<P1>::SIZE; }
+template <int P1>
+static size_t smem_cg() { return sizeof(double) * CgSm<P1>::SIZE; }
 
 #define SISDC_P1_SWITCH(p1, ...)                                 \
   switch (p1) {                                                  \
@@ -842,8 +1103,8 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
   void* args[] = {&A};
   cudaError_t e = cudaSuccess;
   SISDC_P1_SWITCH(op.p1, {
-    set_smem<P1>(k2_cg<P1>);
-    e = cudaLaunchCooperativeKernel((void*)k2_cg<P1>, dim3(nblocks), dim3(Blk<P1>::NT), args, smem2<P1>(), c->stream);
+    cudaFuncSetAttribute(k2_cg<P1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cg<P1>());
+    e = cudaLaunchCooperativeKernel((void*)k2_cg<P1>, dim3(nblocks), dim3(Blk<P1>::NT), args, smem_cg<P1>(), c->stream);
   });
   if (e != cudaSuccess) return c->cuda(e, "k2_cg cooperative launch");
   return c->after_launch("k2_cg");
@@ -853,9 +1114,9 @@ int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks) {
   int per_sm = 0, sms = 0;
   cudaError_t e = cudaSuccess;
   SISDC_P1_SWITCH(op.p1, {
-    set_smem<P1>(k2_cg<P1>);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_cg<P1>, Blk<P1>::NT, smem2<P1>());
-    const int ntiles = (op.nex * op.ney + Blk<P1>::EB - 1) / Blk<P1>::EB;
+    cudaFuncSetAttribute(k2_cg<P1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cg<P1>());
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_cg<P1>, Blk<P1>::NT, smem_cg<P1>());
+    const int ntiles = (op.nex + Blk<P1>::EB - 1) / Blk<P1>::EB * op.ney;   // strip tiles
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     long long nb = (long long)per_sm * sms;
     if (nb > ntiles) nb = ntiles;

@@ -82,7 +82,8 @@ __device__ __forceinline__ double coef2d(const Op2DDev& op, const CoefDev& k, in
     case SISDC_COEF_FIELD: return k.ptr[(long long)eg * op.p1 * op.p1 + j * op.p1 + i];
     case SISDC_COEF_SI: {
       double s[NC_MAX];
-      for (int c = 0; c < op.nc; ++c) s[c] = k.ptr[nidx(op, c, ey, ex, j, i)];
+#pragma unroll
+      for (int c = 0; c < NC_MAX; ++c) s[c] = c < op.nc ? k.ptr[nidx(op, c, ey, ex, j, i)] : 1.0;
       const double lam = lam_max2d(op, s);
       const double half = 0.5 * k.value * (lam * lam);
       double ph;

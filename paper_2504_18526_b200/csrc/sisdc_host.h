@@ -82,5 +82,6 @@ int launch2x_fas(Ctx* c, const Xfer2Dev& x, const double* Wf, double dt, int inc
 int launch2x_interp(Ctx* c, const Xfer2Dev& x, int accumulate, const double* uc, const double* vc, double* uf);
 int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int nblocks);
 int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks);
+int set_cg2_tables(Ctx* c, int p1, const double* tab);
 
 }  // namespace sisdc

@@ -1,0 +1,42 @@
+"""Time one 2-D implicit solve (k2_cg) on a BASELINE 2-D level; ncu target.
+
+usage: python tools/cg2_one.py [cfg3|cfg4|cfg5] [P] [reps]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2504_18526_b200 import dgsem, dgsem2d
+from paper_2504_18526_b200.configs import WORKLOADS
+from paper_2504_18526_b200.runtime import get_runtime
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
+w = WORKLOADS[name]
+P = int(sys.argv[2]) if len(sys.argv) > 2 else w.p_fine
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+rt = get_runtime()
+rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=0)
+op = dgsem2d.DGOperator2D(dgsem2d.Mesh2D(0.0, w.length, 0.0, w.length, w.nex, w.ney, P),
+                          dgsem2d.CompressibleEuler2D(w.gamma, w.nu))
+X, Y = op.mesh.nodes_xy
+u = rt.to_device(w.initial_state(X, Y))
+dt = w.time_step(u.cpu().numpy(), dgsem.compute_delta(w.p_fine))
+a = 0.5 * dt
+c = op.modified_diffusion_matrix(u, a, "si2")
+out = torch.empty_like(u)
+op.eager_checks = False
+ts = []
+for r in range(reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    op.implicit_solve(c, a, u, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1) * 1e3)
+its = rt.cg_log()[0][-reps:].tolist()
+n = u.numel()
+print(f"{name} P={P} n={n} iterations={its} us/solve={[round(t) for t in ts]} "
+      f"us/iter={ts[-1] / max(its[-1], 1):.1f} ideal_us/iter(94B/DOF)={94 * n / 6553.6e3:.1f}")
