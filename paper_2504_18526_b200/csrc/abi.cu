@@ -149,7 +149,10 @@ int sisdc_ctx_create(int device, sisdc_ctx** out) {
     return SISDC_ERR_CUDA;
   }
   const char* tm = getenv("SISDC_CG_TIMING");
-  if (e == cudaSuccess && tm && tm[0] == '1') e = cudaMalloc(&c.d_timing, 80 * sizeof(long long));
+  if (e == cudaSuccess && tm && tm[0] == '1') {
+    e = cudaMalloc(&c.d_timing, 80 * sizeof(long long));
+    if (e == cudaSuccess) e = cudaMemset(c.d_timing, 0, 80 * sizeof(long long));
+  }
   int init[4] = {INT_MAX, 0, 0, 0};
   cudaMemcpy(c.d_status, init, sizeof(init), cudaMemcpyHostToDevice);
   *out = x;
@@ -348,7 +351,7 @@ int sisdc_op2d_create(sisdc_ctx* x, const sisdc_op2d_desc* d, sisdc_op1d** out) 
   int rc = set_cg2_tables(&c, p1, tab.data());
   if (!rc) rc = cg2_blocks(&c, v, &op->cg_blocks);
   if (rc) { cudaFree(op->d_tab); delete op; return rc; }
-  const size_t ws = 4 * (size_t)v.n + 2 * (size_t)v.nn + 16 + 8 * (size_t)op->cg_blocks;
+  const size_t ws = 5 * (size_t)v.n + 2 * (size_t)v.nn + 16 + 8 * (size_t)op->cg_blocks;
   e = cudaMalloc(&op->d_cgws, ws * sizeof(double));
   if (e != cudaSuccess) {
     rc = c.cuda(e, "op2d CG workspace");

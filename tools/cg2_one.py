@@ -40,3 +40,17 @@ its = rt.cg_log()[0][-reps:].tolist()
 n = u.numel()
 print(f"{name} P={P} n={n} iterations={its} us/solve={[round(t) for t in ts]} "
       f"us/iter={ts[-1] / max(its[-1], 1):.1f} ideal_us/iter(94B/DOF)={94 * n / 6553.6e3:.1f}")
+if os.environ.get("SISDC_CG_TIMING") == "1":
+    import ctypes as C
+    import numpy as np
+    buf = (C.c_longlong * 80)()
+    rt.check(rt.lib.sisdc_ctx_debug_timing(rt.h, buf, 80))
+    t = np.array(buf[:20], dtype=np.float64)
+    for b, o in (("block 0", 0), ("block G-1", 10)):
+        d = np.diff(t[o:o + 7]) / 1e3
+        print(f"  {b} iteration 2 (us): phaseA {d[0]:.1f} sync {d[1]:.1f} phaseB {d[2]:.1f} part {d[3]:.1f} "
+              f"sync {d[4]:.1f} total {d[5]:.1f}")
+    t2 = np.array(buf[20:23], dtype=np.float64)
+    if t2[2] > 0:
+        print(f"  block0/warp0 phase B per element: wait {t2[0]/t2[2]:.0f} cycles, compute {t2[1]/t2[2]:.0f} cycles "
+              f"({int(t2[2])} elements over all solves)")
