@@ -899,10 +899,14 @@ __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const M
   // neighbour face fluxes: lane = face*8 + k
   {
     const int f = lane >> 3, k = lane & 7;
-    const double* ln = Nb + f * NC * 64;
+    const double* ln = Nb + f * NC * 64 + k * 8;
     double gd = 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) gd = fma(K.drow[q], ln[f < FT ? nsw(k, q) : nsw(q, k)], gd);
+    for (int j = 0; j < 4; ++j) {
+      const double2 v = *reinterpret_cast<const double2*>(ln + 2 * (j ^ (k >> 1)));
+      gd = fma(K.drow[2 * j], v.x, gd);
+      gd = fma(K.drow[2 * j + 1], v.y, gd);
+    }
     DT[lane] = K.cfn * ((f < FT ? op.sx : op.sy) * gd);
   }
   __syncwarp();
@@ -917,8 +921,8 @@ __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const M
     const bool yd = lane >= 8;
     const int r = lane & 7;
     const int up = yd ? P * RP + r : r * RP + P, u0 = yd ? r : r * RP;
-    const double jp = Ue[up] - Nb[(yd ? FT : FR) * NC * 64 + (yd ? nsw(0, r) : nsw(r, 0))];
-    const double jm = Nb[(yd ? FB : FL) * NC * 64 + (yd ? nsw(P, r) : nsw(r, P))] - Ue[u0];
+    const double jp = Ue[up] - Nb[(yd ? FT : FR) * NC * 64 + nsw(r, 0)];
+    const double jm = Nb[(yd ? FB : FL) * NC * 64 + nsw(r, P)] - Ue[u0];
     const double cP = Ce[up], c0 = Ce[u0];
     const double fcp = ws[W::CFN + (yd ? 16 : 0) + r], fcm = ws[W::CFN + (yd ? 24 : 8) + r];
     const double qP = (yd ? QY : QX)[up], q0 = (yd ? QY : QX)[u0];
@@ -967,28 +971,39 @@ __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const d
   const int r = lane >> 2, cc = (lane & 3) * 2;
   const int f = lane >> 3, k = lane & 7;
   const int fnode = f == FR ? k * 8 : f == FL ? k * 8 + 7 : f == FT ? k : 56 + k;   // neighbour's face node
+  const double* srcc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) srcc[c] = src + c * nn;
+  const int swz = r * 8 + 2 * ((lane & 3) ^ (r >> 1));            // row r, chunk lane&3 (swizzled)
+  const int tr0 = nsw(lane & 7, lane >> 3), tr1 = nsw(lane & 7, 4 + (lane >> 3));   // transposed: node v -> line v%8, pos v/8
   for (int e = blockIdx.x * nwb + warp; e < ne; e += gridDim.x * nwb) {
     const int ey = e / op.nex, ex = e - ey * op.nex;
     const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
     const int eyt = ey + 1 == op.ney ? 0 : ey + 1, eyb = ey == 0 ? op.ney - 1 : ey - 1;
-    const long long eo = (long long)e * 64;
-    const long long nb[4] = {((long long)ey * op.nex + exr) * 64, ((long long)ey * op.nex + exl) * 64,
-                             ((long long)eyt * op.nex + ex) * 64, ((long long)eyb * op.nex + ex) * 64};
+    const unsigned eo = (unsigned)e * 64u;
+    const unsigned nb[4] = {((unsigned)ey * op.nex + exr) * 64u, ((unsigned)ey * op.nex + exl) * 64u,
+                            ((unsigned)eyt * op.nex + ex) * 64u, ((unsigned)eyb * op.nex + ex) * 64u};
 #pragma unroll
-    for (int c = 0; c < NC; ++c) cp_async16(ws + W::OWN + c * W::NP + r * W::RP + cc, src + c * nn + eo + 2 * lane);
+    for (int c = 0; c < NC; ++c) cp_async16(ws + W::OWN + c * W::NP + r * W::RP + cc, srcc[c] + eo + 2 * lane);
     cp_async16(ws + W::COEF + r * W::RP + cc, Cf + eo + 2 * lane);
-    const int swz = r * 8 + 2 * ((lane & 3) ^ (r >> 1));   // neighbour rows: 16-byte chunks XOR-swizzled
+    // face lines in swizzled rows: R/L neighbours row-wise (16-byte copies), T/B
+    // neighbours transposed (8-byte copies) so every face line is a row
 #pragma unroll
-    for (int ff = 0; ff < 4; ++ff)
-#pragma unroll
-      for (int c = 0; c < NC; ++c) cp_async16(ws + W::NBR + (ff * NC + c) * 64 + swz, src + c * nn + nb[ff] + 2 * lane);
+    for (int c = 0; c < NC; ++c) {
+      cp_async16(ws + W::NBR + (FR * NC + c) * 64 + swz, srcc[c] + nb[FR] + 2 * lane);
+      cp_async16(ws + W::NBR + (FL * NC + c) * 64 + swz, srcc[c] + nb[FL] + 2 * lane);
+      cp_async8(ws + W::NBR + (FT * NC + c) * 64 + tr0, srcc[c] + nb[FT] + lane);
+      cp_async8(ws + W::NBR + (FT * NC + c) * 64 + tr1, srcc[c] + nb[FT] + 32 + lane);
+      cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr0, srcc[c] + nb[FB] + lane);
+      cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr1, srcc[c] + nb[FB] + 32 + lane);
+    }
     K.cfn = Cf[nb[f] + fnode];
     ws[W::CFN + lane] = K.cfn;
     const long long c0 = clock64();
     cp_async_wait_all();
     const int g = lane >> 2, n0 = 2 * (lane & 3);
     __syncwarp();
-    const long long gi = eo + g * 8 + n0;
+    const long long gi = (long long)eo + g * 8 + n0;
     const long long c1 = clock64();
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) wpe_field<NC>(op, ws, K, c, a, gi, epi);
@@ -1091,6 +1106,10 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     A.Pv[t] = 0.0;
     A.S[t] = 0.0;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // phase-A chunk counters
+    reinterpret_cast<unsigned*>(A.scal)[0] = 0u;
+    reinterpret_cast<unsigned*>(A.scal)[1] = 0u;
+  }
   grid.sync();
   // ---- setup 2: r0 = b - A x0 (b = M rhs); partials (b,b), #nonzero -> slot 0
   {
@@ -1179,9 +1198,25 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     if (stamp) tm[0] = gtimer();
     // phase A: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = r dinv
     double ru = 0.0, rr = 0.0;
-    if (vec) {
+    if (vec) {   // blocks claim 1024-pair chunks dynamically (balance + DRAM page locality)
       const long long nh = nn >> 1;
-      for (long long h = gtid; h < nh; h += nthr) cg_update2<NC>(A, h, nh, alpha, beta, ru, rr);
+      const unsigned nchunk = (unsigned)((nh + 1023) >> 10);
+      unsigned* ctr = reinterpret_cast<unsigned*>(A.scal) + (k & 1);
+      __shared__ unsigned chs[2];
+      if (threadIdx.x == 0) chs[0] = atomicAdd(ctr, 1u);
+      __syncthreads();
+      for (int it = 0;; ++it) {
+        const unsigned ch = chs[it & 1];
+        if (ch >= nchunk) break;
+        if (threadIdx.x == 0) chs[(it + 1) & 1] = atomicAdd(ctr, 1u);
+        const long long h0 = (long long)ch << 10;
+#pragma unroll 1
+        for (int i = 0; i < 4; ++i) {
+          const long long h = h0 + i * 256 + threadIdx.x;
+          if (h < nh) cg_update2<NC>(A, h, nh, alpha, beta, ru, rr);
+        }
+        __syncthreads();
+      }
     } else {
       for (long long f = gtid; f < nn; f += nthr) {
         const double di = A.DINV[f];
@@ -1206,6 +1241,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     }
     if (stamp) tm[1] = gtimer();
     grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) reinterpret_cast<unsigned*>(A.scal)[k & 1] = 0u;   // next use: k+2
     if (stamp) tm[2] = gtimer();
     const double wu = phase_B();
     if (stamp) tm[3] = gtimer();
