@@ -71,16 +71,20 @@ __device__ __forceinline__ void conv_block(const Op2DDev& op, double* sm, const 
   double* FYs = sm + Sm2<P1>::FY + n.el * NC_MAX * NN;
   double s[NC_MAX], f[NC_MAX];
   if (n.valid) {
-    for (int c = 0; c < op.nc; ++c) s[c] = u[nidx(op, c, n.ey, n.ex, n.j, n.i)];
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) s[c] = u[nidx(op, c, n.ey, n.ex, n.j, n.i)];
     flux2d(op, s, 0, f);
-    for (int c = 0; c < op.nc; ++c) FXs[c * NN + n.nd] = f[c];
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) FXs[c * NN + n.nd] = f[c];
     flux2d(op, s, 1, f);
-    for (int c = 0; c < op.nc; ++c) FYs[c * NN + n.nd] = f[c];
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) FYs[c * NN + n.nd] = f[c];
   }
   __syncthreads();
   if (n.valid) {
     double vx[NC_MAX], vy[NC_MAX];
-    for (int c = 0; c < op.nc; ++c) {
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) {
       double ax = 0.0, ay = 0.0;
 #pragma unroll
       for (int k = 0; k < P1; ++k) {
@@ -93,29 +97,38 @@ __device__ __forceinline__ void conv_block(const Op2DDev& op, double* sm, const 
     double nb[NC_MAX], fh[NC_MAX];
     if (n.i == P) {   // right x-face: own (P,j) | right neighbour (0,j)
       const int exr = wrapi(n.ex + 1, op.nex);
-      for (int c = 0; c < op.nc; ++c) nb[c] = u[nidx(op, c, n.ey, exr, n.j, 0)];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) nb[c] = u[nidx(op, c, n.ey, exr, n.j, 0)];
       rusanov2d(op, s, nb, 0, fh);
-      for (int c = 0; c < op.nc; ++c) vx[c] -= fh[c];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) vx[c] -= fh[c];
     }
     if (n.i == 0) {   // left x-face: left neighbour (P,j) | own (0,j)
       const int exl = wrapi(n.ex - 1, op.nex);
-      for (int c = 0; c < op.nc; ++c) nb[c] = u[nidx(op, c, n.ey, exl, n.j, P)];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) nb[c] = u[nidx(op, c, n.ey, exl, n.j, P)];
       rusanov2d(op, nb, s, 0, fh);
-      for (int c = 0; c < op.nc; ++c) vx[c] += fh[c];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) vx[c] += fh[c];
     }
     if (n.j == P) {   // top y-face
       const int eyt = wrapi(n.ey + 1, op.ney);
-      for (int c = 0; c < op.nc; ++c) nb[c] = u[nidx(op, c, eyt, n.ex, 0, n.i)];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) nb[c] = u[nidx(op, c, eyt, n.ex, 0, n.i)];
       rusanov2d(op, s, nb, 1, fh);
-      for (int c = 0; c < op.nc; ++c) vy[c] -= fh[c];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) vy[c] -= fh[c];
     }
     if (n.j == 0) {   // bottom y-face
       const int eyb = wrapi(n.ey - 1, op.ney);
-      for (int c = 0; c < op.nc; ++c) nb[c] = u[nidx(op, c, eyb, n.ex, P, n.i)];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) nb[c] = u[nidx(op, c, eyb, n.ex, P, n.i)];
       rusanov2d(op, nb, s, 1, fh);
-      for (int c = 0; c < op.nc; ++c) vy[c] += fh[c];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) vy[c] += fh[c];
     }
-    for (int c = 0; c < op.nc; ++c) r[c] = vx[c] * op.sx / w[n.i] + vy[c] * op.sy / w[n.j];
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) r[c] = vx[c] * op.sx / w[n.i] + vy[c] * op.sy / w[n.j];
   }
   __syncthreads();
 }
@@ -241,7 +254,8 @@ __global__ void __launch_bounds__(256) k2_conv(Op2DDev op, const double* __restr
   double r[NC_MAX];
   conv_block<P1>(op, sm, u, n, r);
   if (n.valid)
-    for (int c = 0; c < op.nc; ++c) out[nidx(op, c, n.ey, n.ex, n.j, n.i)] = r[c];
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) out[nidx(op, c, n.ey, n.ex, n.j, n.i)] = r[c];
 }
 
 template <int P1>
@@ -253,7 +267,8 @@ __global__ void __launch_bounds__(256) k2_sip(Op2DDev op, CoefDev k, const doubl
   double r[NC_MAX];
   sip_block<P1, 0>(op, sm, k, u, nullptr, op.nc, 0.0, n, r);
   if (n.valid)
-    for (int c = 0; c < op.nc; ++c) out[nidx(op, c, n.ey, n.ex, n.j, n.i)] = r[c];
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) out[nidx(op, c, n.ey, n.ex, n.j, n.i)] = r[c];
 }
 
 template <int P1>
@@ -294,16 +309,21 @@ __global__ void __launch_bounds__(256) k2_node_eval(Op2DDev op, Cache2Args a) {
   const CoefDev phys{SISDC_COEF_PHYS, 0.0, nullptr};
   if (has_phys) sip_block<P1, 0>(op, sm, phys, um, nullptr, op.nc, 0.0, n, d);
   if (n.valid)
-    for (int c = 0; c < op.nc; ++c) {
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) {
       const double f = has_phys ? cm[c] + d[c] : cm[c];
       if (!isfinite(f)) atomicMin(a.status, n.eg);
       a.f[(size_t)m * op.n + nidx(op, c, n.ey, n.ex, n.j, n.i)] = f;
     }
   if (a.mode == 0) return;
-  const double dtm = a.dts[m];
+  double dtm = 0.0;   // static-index select (a dynamic index copies the parameter block to local memory)
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j == m) dtm = a.dts[j];
   if (dtm == 0.0) {
     if (n.valid)
-      for (int c = 0; c < op.nc; ++c) {
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) {
         const long long g = (size_t)m * op.n + nidx(op, c, n.ey, n.ex, n.j, n.i);
         a.h1[g] = 0.0;
         if (a.h2) a.h2[g] = 0.0;
@@ -315,12 +335,14 @@ __global__ void __launch_bounds__(256) k2_node_eval(Op2DDev op, Cache2Args a) {
   double cp[NC_MAX];
   if (a.conv_prev) {
     if (n.valid)
-      for (int c = 0; c < op.nc; ++c) cp[c] = a.conv_prev[nidx(op, c, n.ey, n.ex, n.j, n.i)];
+#pragma unroll
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c) cp[c] = a.conv_prev[nidx(op, c, n.ey, n.ex, n.j, n.i)];
   } else {
     conv_block<P1>(op, sm, up, n, cp);
   }
   if (n.valid)
-    for (int c = 0; c < op.nc; ++c) {
+#pragma unroll
+    for (int c = 0; c < NC_MAX && c < op.nc; ++c) {
       const long long g = (size_t)m * op.n + nidx(op, c, n.ey, n.ex, n.j, n.i);
       a.h1[g] = dtm * (cp[c] + d[c]);
       if (a.h2) a.h2[g] = dtm * (cm[c] + d[c]);
@@ -349,7 +371,8 @@ __global__ void __launch_bounds__(256) k2_stage(Op2DDev op, Stage2Args a) {
   double cv[NC_MAX];
   conv_block<P1>(op, sm, a.conv_in, n, cv);
   if (!n.valid) return;
-  for (int c = 0; c < op.nc; ++c) {
+#pragma unroll
+  for (int c = 0; c < NC_MAX && c < op.nc; ++c) {
     const long long gi = nidx(op, c, n.ey, n.ex, n.j, n.i);
     if (a.conv_out) a.conv_out[gi] = cv[c];
     double q = 0.0;
@@ -841,6 +864,7 @@ struct MmaLane {            // per-lane constants, g = lane/4, t = lane%4, n0 = 
   double dPn[2], d0n[2];    // D[P][n0+i], D[0][n0+i]
   double dPg, d0g;          // D[P][g], D[0][g]
   double hwy, hwx[2], hh[2];
+  double wn[2], wg;         // GLL weights w[n0+i], w[g]
   double cfn;               // this lane's neighbour face coefficient (per element)
 };
 // lane-varying constants come from the global operator table (TabOff layout):
@@ -869,22 +893,22 @@ __device__ __forceinline__ void mma_lane_init(const Op2DDev& op, MmaLane& K) {
   K.hwy = 0.5 * op.dy * w[g];
   K.hh[0] = K.hwx[0] * K.hwy;
   K.hh[1] = K.hwx[1] * K.hwy;
+  K.wn[0] = w[n0];
+  K.wn[1] = w[n0 + 1];
+  K.wg = w[g];
 }
 
-// one field of a staged element; epi(g, w0, w1, v0, v1) for the lane's node pair
-template <int NC, typename Epi>
-__device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const MmaLane& K, int c, double a,
-                                          long long gi, Epi&& epi) {
-  using W = Wpe<NC>;
-  constexpr int RP = W::RP, P = 7;
+// SIP accumulators of one field of a staged element for the lane's node pair
+// (row g, columns n0, n0+1): bx = Bx, by = By incl. face and adjoint terms
+// (sip_block).  Ue: own element (padded rows), Nb: neighbour face lines of this
+// field, Ce / cfn: coefficient at the own nodes (padded rows) / at the
+// neighbour face nodes (lane = face*8 + k).  Scratch: QX, QY, DT, FC.
+template <int NC>
+__device__ __forceinline__ void wpe_sip(const Op2DDev& op, const MmaLane& K, const double* Ue, const double* Nb,
+                                        const double* Ce, const double* cfn, double* QX, double* QY, double* DT,
+                                        double* FC, double& bx0, double& bx1, double& by0, double& by1) {
+  constexpr int RP = 10, P = 7;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, n0 = 2 * t;
-  const double* Ue = ws + W::OWN + c * W::NP;
-  const double* Ce = ws + W::COEF;
-  const double* Nb = ws + W::NBR + c * 64;      // face f at Nb + f * NC * 64 (swizzled rows)
-  double* QX = ws + W::QX;
-  double* QY = ws + W::QY;
-  double* DT = ws + W::DOT;
-  double* FC = ws + W::FCON;
   // Q = C s (D u) along x and y
   double qx0 = 0.0, qx1 = 0.0, qy0 = 0.0, qy1 = 0.0;
   dmma(qx0, qx1, Ue[g * RP + t], K.d0);
@@ -896,7 +920,7 @@ __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const M
     *reinterpret_cast<double2*>(QX + g * RP + n0) = make_double2(cg.x * (op.sx * qx0), cg.y * (op.sx * qx1));
     *reinterpret_cast<double2*>(QY + g * RP + n0) = make_double2(cg.x * (op.sy * qy0), cg.y * (op.sy * qy1));
   }
-  // neighbour face fluxes: lane = face*8 + k
+  // neighbour face fluxes: lane = face*8 + k, line k of face f
   {
     const int f = lane >> 3, k = lane & 7;
     const double* ln = Nb + f * NC * 64 + k * 8;
@@ -907,11 +931,10 @@ __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const M
       gd = fma(K.drow[2 * j], v.x, gd);
       gd = fma(K.drow[2 * j + 1], v.y, gd);
     }
-    DT[lane] = K.cfn * ((f < FT ? op.sx : op.sy) * gd);
+    DT[lane] = cfn[lane] * ((f < FT ? op.sx : op.sy) * gd);
   }
   __syncwarp();
-  // second products
-  double bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
+  bx0 = bx1 = by0 = by1 = 0.0;
   dmma(bx0, bx1, QX[g * RP + t], K.w0);
   dmma(bx0, bx1, QX[g * RP + 4 + t], K.w1);
   dmma(by0, by1, K.w0, QY[t * RP + g]);
@@ -924,7 +947,7 @@ __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const M
     const double jp = Ue[up] - Nb[(yd ? FT : FR) * NC * 64 + nsw(r, 0)];
     const double jm = Nb[(yd ? FB : FL) * NC * 64 + nsw(r, P)] - Ue[u0];
     const double cP = Ce[up], c0 = Ce[u0];
-    const double fcp = ws[W::CFN + (yd ? 16 : 0) + r], fcm = ws[W::CFN + (yd ? 24 : 8) + r];
+    const double fcp = cfn[(yd ? 16 : 0) + r], fcm = cfn[(yd ? 24 : 8) + r];
     const double qP = (yd ? QY : QX)[up], q0 = (yd ? QY : QX)[u0];
     const double qnp = DT[(yd ? 16 : 0) + r], qnm = DT[(yd ? 24 : 8) + r];
     const double mu = yd ? op.muy : op.mux, sc = yd ? op.sy : op.sx;
@@ -950,11 +973,23 @@ __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const M
     by0 -= ca.w * K.d0g;
     by1 -= cb.w * K.d0g;
   }
-  // w = a (hwy Bx + hwx By) + hwx hwy v
-  const double2 v = *reinterpret_cast<const double2*>(Ue + g * RP + n0);
+  __syncwarp();   // QX / QY / DT / FC are rewritten by the next call
+}
+
+// one field of a staged element: w = a (hwy Bx + hwx By) + hwx hwy v;
+// epi(g, w0, w1, v0, v1) for the lane's node pair
+template <int NC, typename Epi>
+__device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const MmaLane& K, int c, double a,
+                                          long long gi, Epi&& epi) {
+  using W = Wpe<NC>;
+  const int lane = threadIdx.x & 31, g = lane >> 2, n0 = 2 * (lane & 3);
+  const double* Ue = ws + W::OWN + c * W::NP;
+  double bx0, bx1, by0, by1;
+  wpe_sip<NC>(op, K, Ue, ws + W::NBR + c * 64, ws + W::COEF, ws + W::CFN, ws + W::QX, ws + W::QY, ws + W::DOT,
+              ws + W::FCON, bx0, bx1, by0, by1);
+  const double2 v = *reinterpret_cast<const double2*>(Ue + g * W::RP + n0);
   epi(gi + c * op.nn, fma(a, fma(K.hwy, bx0, K.hwx[0] * by0), K.hh[0] * v.x),
       fma(a, fma(K.hwy, bx1, K.hwx[1] * by1), K.hh[1] * v.y), v.x, v.y);
-  __syncwarp();   // QX / QY / DOT / FC are rewritten by the next field
 }
 
 // the block's share of phase B: warps stride over elements
@@ -997,7 +1032,7 @@ __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const d
       cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr0, srcc[c] + nb[FB] + lane);
       cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr1, srcc[c] + nb[FB] + 32 + lane);
     }
-    K.cfn = Cf[nb[f] + fnode];
+    K.cfn = Cf[(f == FR ? nb[FR] : f == FL ? nb[FL] : f == FT ? nb[FT] : nb[FB]) + fnode];
     ws[W::CFN + lane] = K.cfn;
     const long long c0 = clock64();
     cp_async_wait_all();
@@ -1008,6 +1043,205 @@ __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const d
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) wpe_field<NC>(op, ws, K, c, a, gi, epi);
     if (tacc) { tacc[0] += c1 - c0; tacc[1] += clock64() - c1; tacc[2] += 1; }
+  }
+}
+
+// ------------------------------------------------------------------------
+// P = 7 (P1 = 8) node evaluation / cache refresh (k2_node_eval semantics), one
+// warp per element: u_m and its face neighbours staged as in the CG phase B,
+// the convective volume terms and the SIP operators (physical and SI
+// coefficient) on the fp64 tensor cores, Rusanov face fluxes per face node.
+template <int NC>
+struct Ev {                 // per-warp shared region (doubles)
+  static constexpr int RP = 10, NP = 80;
+  static constexpr int OWN = 0;                     // [NC][NP] u_m
+  static constexpr int NBR = OWN + NC * NP;         // [4][NC][64] u_m face neighbours (lines)
+  static constexpr int UPO = NBR + 4 * NC * 64;     // [NC][NP] u_{m-1}
+  static constexpr int CSI = UPO + NC * NP, CFS = CSI + NP;   // SI coefficient own / face
+  static constexpr int CPH = CFS + 32, CFP = CPH + NP;        // physical coefficient own / face
+  static constexpr int QX = CFP + 32, QY = QX + NP, DOT = QY + NP, FCON = DOT + 32;
+  static constexpr int FX = FCON + 64, FY = FX + NP;
+  static constexpr int FHM = FY + NP, FHP = FHM + 32 * NC;   // Rusanov fluxes [lane][NC]
+  static constexpr int WARP = FHP + 32 * NC;
+};
+constexpr int EV_WARPS = 4;
+__device__ __forceinline__ double pick4(const double* v, int c) {   // register select, no local memory
+  return c == 0 ? v[0] : c == 1 ? v[1] : c == 2 ? v[2] : v[3];
+}
+
+// convective term of field c at the lane's node pair from the staged element
+// (state rows in `own`, padded) and the face fluxes fh[lane*NC + c]
+template <int NC>
+__device__ __forceinline__ void wpe_conv(const Op2DDev& op, const MmaLane& K, const double* own, const double* fh,
+                                         int c, double* FX, double* FY, double& r0, double& r1) {
+  constexpr int RP = 10, P = 7;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, n0 = 2 * t;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    double st[NC_MAX], fl[NC_MAX];
+#pragma unroll
+    for (int q = 0; q < NC_MAX; ++q) st[q] = q < NC ? own[q * 80 + g * RP + n0 + i] : 1.0;
+    flux2d(op, st, 0, fl);
+    FX[g * RP + n0 + i] = pick4(fl, c);
+    flux2d(op, st, 1, fl);
+    FY[g * RP + n0 + i] = pick4(fl, c);
+  }
+  __syncwarp();
+  double vx0 = 0.0, vx1 = 0.0, vy0 = 0.0, vy1 = 0.0;
+  dmma(vx0, vx1, FX[g * RP + t], K.w0);
+  dmma(vx0, vx1, FX[g * RP + 4 + t], K.w1);
+  dmma(vy0, vy1, K.w0, FY[t * RP + g]);
+  dmma(vy0, vy1, K.w1, FY[(4 + t) * RP + g]);
+  if (n0 + 1 == P) vx1 -= fh[(FR * 8 + g) * NC + c];
+  if (n0 == 0) vx0 += fh[(FL * 8 + g) * NC + c];
+  if (g == P) { vy0 -= fh[(FT * 8 + n0) * NC + c]; vy1 -= fh[(FT * 8 + n0 + 1) * NC + c]; }
+  if (g == 0) { vy0 += fh[(FB * 8 + n0) * NC + c]; vy1 += fh[(FB * 8 + n0 + 1) * NC + c]; }
+  r0 = vx0 * op.sx / K.wn[0] + vy0 * op.sy / K.wg;
+  r1 = vx1 * op.sx / K.wn[1] + vy1 * op.sy / K.wg;
+  __syncwarp();   // FX / FY are rewritten by the next call
+}
+
+template <int NC>
+__global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args a) {
+  extern __shared__ double sm[];
+  using W = Ev<NC>;
+  constexpr int RP = 10, P = 7;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ws = sm + warp * W::WARP;
+  const int m = a.m_first + blockIdx.y;
+  const long long nn = op.nn;
+  const double* um = a.u + (size_t)m * op.n;
+  const double* up = m == 0 ? a.u0 : a.u + (size_t)(m - 1) * op.n;
+  double dtm = 0.0;   // static-index select: a dynamic index would copy the parameter block to local memory
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j == m) dtm = a.dts[j];
+  double ph;
+  const bool has_phys = phys2d(op, 0, ph);          // constant nu (no AV on this path)
+  const bool need_si = a.mode != 0 && dtm != 0.0 && a.scheme != SISDC_EULER;
+  const bool need_h = a.mode != 0 && dtm != 0.0;
+  const bool conv_up = need_h && a.conv_prev == nullptr;
+  MmaLane K;
+  mma_lane_init(op, K);
+  const int g = lane >> 2, n0 = 2 * (lane & 3), r = g, cc = n0;
+  const int f = lane >> 3, k = lane & 7;
+  const int fnode = f == FR ? k * 8 : f == FL ? k * 8 + 7 : f == FT ? k : 56 + k;
+  const int ownf = f == FR ? k * RP + P : f == FL ? k * RP : f == FT ? P * RP + k : k;   // own face node (padded)
+  const int npos = nsw(k, (f == FR || f == FT) ? 0 : P);                                // neighbour node on line k
+  const int swz = r * 8 + 2 * ((lane & 3) ^ (r >> 1));
+  const int tr0 = nsw(lane & 7, lane >> 3), tr1 = nsw(lane & 7, 4 + (lane >> 3));
+  if (has_phys) {
+    for (int q = lane; q < W::NP; q += 32) ws[W::CPH + q] = ph;
+    ws[W::CFP + lane] = ph;
+  }
+  const int ne = op.nex * op.ney;
+  for (int e = blockIdx.x * EV_WARPS + warp; e < ne; e += gridDim.x * EV_WARPS) {
+    const int ey = e / op.nex, ex = e - ey * op.nex;
+    const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
+    const int eyt = ey + 1 == op.ney ? 0 : ey + 1, eyb = ey == 0 ? op.ney - 1 : ey - 1;
+    const unsigned eo = (unsigned)e * 64u;
+    const unsigned nb[4] = {((unsigned)ey * op.nex + exr) * 64u, ((unsigned)ey * op.nex + exl) * 64u,
+                            ((unsigned)eyt * op.nex + ex) * 64u, ((unsigned)eyb * op.nex + ex) * 64u};
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double* uc = um + c * nn;
+      cp_async16(ws + W::OWN + c * W::NP + r * RP + cc, uc + eo + 2 * lane);
+      cp_async16(ws + W::NBR + (FR * NC + c) * 64 + swz, uc + nb[FR] + 2 * lane);
+      cp_async16(ws + W::NBR + (FL * NC + c) * 64 + swz, uc + nb[FL] + 2 * lane);
+      cp_async8(ws + W::NBR + (FT * NC + c) * 64 + tr0, uc + nb[FT] + lane);
+      cp_async8(ws + W::NBR + (FT * NC + c) * 64 + tr1, uc + nb[FT] + 32 + lane);
+      cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr0, uc + nb[FB] + lane);
+      cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr1, uc + nb[FB] + 32 + lane);
+      if (need_si || conv_up) cp_async16(ws + W::UPO + c * W::NP + r * RP + cc, up + c * nn + eo + 2 * lane);
+    }
+    double upf[NC_MAX];   // u_{m-1} at this lane's neighbour face node
+    const unsigned nbf = (f == FR ? nb[FR] : f == FL ? nb[FL] : f == FT ? nb[FT] : nb[FB]) + fnode;
+#pragma unroll
+    for (int c = 0; c < NC_MAX; ++c) upf[c] = (c < NC && (need_si || conv_up)) ? up[c * nn + nbf] : 1.0;
+    cp_async_wait_all();
+    __syncwarp();
+    // SI coefficient (dt_m/2) lam(u_{m-1})^2 + phys at the own nodes and the neighbour face nodes
+    if (need_si) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double st[NC_MAX];
+#pragma unroll
+        for (int q = 0; q < NC_MAX; ++q) st[q] = q < NC ? ws[W::UPO + q * W::NP + g * RP + n0 + i] : 1.0;
+        const double lam = lam_max2d(op, st);
+        const double half = 0.5 * dtm * (lam * lam);
+        ws[W::CSI + g * RP + n0 + i] = has_phys ? half + ph : half;
+      }
+      const double lam = lam_max2d(op, upf);
+      const double half = 0.5 * dtm * (lam * lam);
+      ws[W::CFS + lane] = has_phys ? half + ph : half;
+    }
+    // Rusanov fluxes at this lane's face node for u_m (and u_{m-1})
+    {
+      double so[NC_MAX], sn[NC_MAX], fh[NC_MAX];
+#pragma unroll
+      for (int c = 0; c < NC_MAX; ++c) {
+        so[c] = c < NC ? ws[W::OWN + c * W::NP + ownf] : 1.0;
+        sn[c] = c < NC ? ws[W::NBR + (f * NC + c) * 64 + npos] : 1.0;
+      }
+      const int axis = f < FT ? 0 : 1;
+      if (f == FR || f == FT) rusanov2d(op, so, sn, axis, fh); else rusanov2d(op, sn, so, axis, fh);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) ws[W::FHM + lane * NC + c] = fh[c];
+      if (conv_up) {
+#pragma unroll
+        for (int c = 0; c < NC_MAX; ++c) so[c] = c < NC ? ws[W::UPO + c * W::NP + ownf] : 1.0;
+        if (f == FR || f == FT) rusanov2d(op, so, upf, axis, fh); else rusanov2d(op, upf, so, axis, fh);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) ws[W::FHP + lane * NC + c] = fh[c];
+      }
+    }
+    __syncwarp();
+    const long long gi = (long long)eo + g * 8 + n0;
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c) {
+      const double* Ue = ws + W::OWN + c * W::NP;
+      const double* Nb = ws + W::NBR + c * 64;
+      double bx0, bx1, by0, by1;
+      double dp0 = 0.0, dp1 = 0.0, ds0 = 0.0, ds1 = 0.0;
+      if (has_phys) {
+        wpe_sip<NC>(op, K, Ue, Nb, ws + W::CPH, ws + W::CFP, ws + W::QX, ws + W::QY, ws + W::DOT, ws + W::FCON,
+                    bx0, bx1, by0, by1);
+        dp0 = -(bx0 / K.hwx[0]) - by0 / K.hwy;
+        dp1 = -(bx1 / K.hwx[1]) - by1 / K.hwy;
+      }
+      if (need_si) {
+        wpe_sip<NC>(op, K, Ue, Nb, ws + W::CSI, ws + W::CFS, ws + W::QX, ws + W::QY, ws + W::DOT, ws + W::FCON,
+                    bx0, bx1, by0, by1);
+        ds0 = -(bx0 / K.hwx[0]) - by0 / K.hwy;
+        ds1 = -(bx1 / K.hwx[1]) - by1 / K.hwy;
+      } else if (need_h) {   // implicit-Euler scheme: modified coefficient = physical
+        ds0 = dp0;
+        ds1 = dp1;
+      }
+      double cm0, cm1;
+      wpe_conv<NC>(op, K, ws + W::OWN, ws + W::FHM, c, ws + W::FX, ws + W::FY, cm0, cm1);
+      const long long go = (size_t)m * op.n + c * nn + gi;
+      const double f0 = has_phys ? cm0 + dp0 : cm0, f1 = has_phys ? cm1 + dp1 : cm1;
+      if (!isfinite(f0) || !isfinite(f1)) atomicMin(a.status, e);
+      *reinterpret_cast<double2*>(a.f + go) = make_double2(f0, f1);
+      if (a.mode == 0) continue;
+      if (!need_h) {
+        *reinterpret_cast<double2*>(a.h1 + go) = make_double2(0.0, 0.0);
+        if (a.h2) *reinterpret_cast<double2*>(a.h2 + go) = make_double2(0.0, 0.0);
+        continue;
+      }
+      double cp0, cp1;
+      if (a.conv_prev) {
+        const double2 v = *reinterpret_cast<const double2*>(a.conv_prev + c * nn + gi);
+        cp0 = v.x;
+        cp1 = v.y;
+      } else {
+        wpe_conv<NC>(op, K, ws + W::UPO, ws + W::FHP, c, ws + W::FX, ws + W::FY, cp0, cp1);
+      }
+      *reinterpret_cast<double2*>(a.h1 + go) = make_double2(dtm * (cp0 + ds0), dtm * (cp1 + ds1));
+      if (a.h2) *reinterpret_cast<double2*>(a.h2 + go) = make_double2(dtm * (cm0 + ds0), dtm * (cm1 + ds1));
+    }
+    __syncwarp();   // the next element overwrites the staged data
   }
 }
 
@@ -1355,6 +1589,23 @@ int launch2_node_eval(Ctx* c, const Op2DDev& op, int mode, int scheme, int M, in
   a.u0 = u0; a.u = u; a.conv_prev = conv_prev; a.scheme = scheme; a.m_first = m_first; a.mode = mode;
   for (int j = 0; j < M; ++j) a.dts[j] = dts ? dts[j] : 0.0;
   a.f = f; a.h1 = h1; a.h2 = h2; a.status = c->d_status;
+  const bool al16 = ((reinterpret_cast<uintptr_t>(u0) | reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(f) |
+                      reinterpret_cast<uintptr_t>(h1) | reinterpret_cast<uintptr_t>(h2) |
+                      reinterpret_cast<uintptr_t>(conv_prev)) & 15) == 0;
+  if (op.p1 == 8 && op.nu_art == nullptr && op.nc == 4 && al16) {   // tensor-core warp-per-element path
+    const size_t smem = sizeof(double) * EV_WARPS * Ev<4>::WARP;
+    cudaFuncSetAttribute(k2_eval8<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int ne = op.nex * op.ney;
+    int nb = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2_eval8<4>, EV_WARPS * 32, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    long long gx = (long long)(nb > 0 ? nb : 1) * sms * 4 / m_count;
+    if (gx < 1) gx = 1;
+    const long long need = (ne + EV_WARPS - 1) / EV_WARPS;
+    if (gx > need) gx = need;
+    k2_eval8<4><<<dim3((unsigned)gx, m_count), EV_WARPS * 32, smem, c->stream>>>(op, a);
+    return c->after_launch("k2_eval8");
+  }
   SISDC_P1_SWITCH(op.p1, {
     set_smem<P1>(k2_node_eval<P1>);
     k2_node_eval<P1><<<grid2<P1>(op, m_count), Blk<P1>::NT, smem2<P1>(), c->stream>>>(op, a);

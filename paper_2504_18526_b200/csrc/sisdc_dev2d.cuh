@@ -110,7 +110,9 @@ __device__ __forceinline__ void rusanov2d(const Op2DDev& op, const double* um, c
   flux2d(op, um, axis, fm);
   flux2d(op, up, axis, fp);
   const double lam = fmax(speed2d(op, um, axis), speed2d(op, up, axis));
-  for (int c = 0; c < op.nc; ++c) fh[c] = 0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[c] - um[c]);
+#pragma unroll
+  for (int c = 0; c < NC_MAX; ++c)
+    if (c < op.nc) fh[c] = 0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[c] - um[c]);
 }
 
 }  // namespace sisdc
