@@ -1,18 +1,21 @@
 #!/usr/bin/env python
 """SI-MLSDC sweep-path benchmark (BASELINE.json metric).
 
-Workload: BASELINE configs[1] (1-D viscous Burgers, 512 elements, P 8/4,
-M 5/3, nu=5e-3, CFL 1) -- the config the metric is quoted on that fits one
-GPU.  A "step" is one SI-MLSDC time slab (FMG start, 3 V-cycles, closing fine
-sweep: 4 fine sweeps + 8 coarse passes), replayed from a CUDA graph with the
-state resident in HBM.  value = DOF-sweep updates/s summed over ranks.
+Headline workload: BASELINE configs[1] (1-D viscous Burgers, 512 elements,
+P 8/4, M 5/3, nu=5e-3, CFL 1) -- the config the metric is quoted on that fits
+one GPU.  A "step" is one SI-MLSDC time slab (FMG start, 3 V-cycles, closing
+fine sweep: 4 fine sweeps + 8 coarse passes), replayed from a CUDA graph with
+the state resident in HBM.  value = DOF-sweep updates/s summed over ranks.
+At N=1 the line also carries "secondary": the same contract measured on
+BASELINE configs[3] (2-D Navier-Stokes shear layer, 256^2 elements, P 7/3),
+whose fine level is HBM resident (the roofline the north star grades).
 
-  python bench.py [--gpus N --steps K --warmup W]      # our CUDA path
+  python bench.py [--gpus N --steps K --warmup W] [--workload cfgN] [--no-2d]
   python bench.py --impl reference                       # reference algorithm on CPU
 
 Multi-GPU (torchrun): each rank advances an independent seeded replica of the
-workload (weak scaling); the 1-D configs are latency bound, so they are not
-element-partitioned ("Multi-GPU").
+workload (weak scaling, "replicas"): DESIGN.md "Multi-GPU" gives the status
+of the element-partitioned 2-D path.
 """
 from __future__ import annotations
 
@@ -45,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cluster-ctas", type=int, default=0)
     ap.add_argument("--cycles", type=int, default=None, help="override the V-cycles per step")
+    ap.add_argument("--no-2d", dest="also_2d", action="store_false",
+                    help="skip the secondary 2-D (cfg4) line that rides along the 1-D headline")
     return ap.parse_args()
 
 
@@ -108,10 +113,11 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def measured_traffic():
+def measured_traffic(kind="1d"):
     """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    name = "r01_cg_traffic.json" if kind == "1d" else "r01_cg2_traffic.json"
     try:
-        with open(os.path.join(HERE, "profiles", "r01_cg_traffic.json")) as f:
+        with open(os.path.join(HERE, "profiles", name)) as f:
             return float(json.load(f)["dram_bytes_per_launch"])
     except Exception:
         return None
@@ -228,23 +234,11 @@ def cg_roofline(hier, rt, torch, dt, reps=64):
     return t, k, bytes_per
 
 
-def run_ours(args):
-    import torch
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True):
+    """Time `steps` SI-MLSDC slabs of workload `w` (CUDA-graph replays, L2
+    flushed between steps, CUDA events, max over ranks); e2e through the slab
+    API with pinned host buffers; live roofline of the dominant kernel."""
     from paper_2504_18526_b200 import dgsem, mlsdc, problems
-    from paper_2504_18526_b200.configs import WORKLOADS
-    from paper_2504_18526_b200.runtime import get_runtime
-    w = WORKLOADS[args.workload]
-    if args.cycles is not None:
-        import dataclasses
-        w = dataclasses.replace(w, n_cycles=args.cycles)
-    rt = get_runtime(local)
-    rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=args.cluster_ctas)
-
     is2d = hasattr(w, "nex")
     if is2d:
         from paper_2504_18526_b200 import dgsem2d
@@ -266,23 +260,23 @@ def run_ours(args):
         hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
         nodes = dgsem.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes
         u0 = w.initial_state(nodes)
-        if rank > 0:   # independent replica per rank
-            rng = np.random.default_rng(1000 + rank)
-            u0 = u0 + 1e-3 * np.sin(np.arange(u0.size) * 0.01 + rng.random())
         dt, n_total = w.time_step(u0, dgsem.compute_delta(w.p_fine))
+    if rank > 0:   # independent replica per rank
+        rng = np.random.default_rng(1000 + rank)
+        u0 = u0 * (1.0 + 1e-6 * rng.random())
     g = mlsdc.SlabGraph(hier, u0, 0.0, dt, w.n_cycles, "fmg")
     U, U_fine = w.dof_sweeps_per_step()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=rt.device)   # > 126 MB L2
     rt.reset_status()
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         g.step()
     torch.cuda.synchronize()
     n_log0 = rt.status()[2]
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local if clock else -1) as clk:
         for e0, e1 in evs:
             flush.fill_(1.0)          # L2 flush between timed steps (outside the events)
             e0.record()
@@ -293,7 +287,7 @@ def run_ours(args):
     rt.raise_on_failure()
     its, margins = rt.cg_log()
     step_its = its[n_log0:]
-    solves_per_step = len(step_its) / max(1, args.steps) if len(step_its) else float("nan")
+    solves_per_step = len(step_its) / max(1, steps) if len(step_its) else float("nan")
     t_max = t_steps
     if world > 1:
         import torch.distributed as dist
@@ -301,12 +295,12 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
         dist.barrier()
-    value = U * args.steps * world / t_max
+    value = U * steps * world / t_max
     # e2e through the public slab API with pinned host buffers
     h_in = torch.empty(hier.fine.ctx.ndof, dtype=torch.float64, pin_memory=True)
     h_out = torch.empty_like(h_in)
-    h_in.copy_(torch.as_tensor(u0))
-    ke = max(5, min(args.steps, 50))
+    h_in.copy_(torch.as_tensor(np.ascontiguousarray(u0).reshape(-1)))
+    ke = max(3, min(steps, 50))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -317,55 +311,98 @@ def run_ours(args):
     e1.record()
     torch.cuda.synchronize()
     t_e2e = e0.elapsed_time(e1) * 1e-3
-    e2e_val = U * ke * world / t_e2e
     if world > 1:
         tt = torch.tensor([t_e2e], device=rt.device, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e_val = U * ke * world / float(tt.item())
+        t_e2e = float(tt.item())
+    e2e_val = U * ke * world / t_e2e
     # dominant kernel roofline (measured live)
     t_cg, k_cg, bytes_cg = cg_roofline(hier, rt, torch, dt)
     peak, peak_kind = measured_hbm_peak()
     achieved = bytes_cg / t_cg / 1e9
+    if is2d:
+        kern = "k2_cg<8,4> (grid-persistent cooperative Jacobi-PCG; phase B warp-per-element on fp64 mma.m8n8k4)"
+        note = ("8N[(3+V)+k(10+V)] bytes per solve (SURVEY 8d), V=1/4: one scalar coefficient per node shared by "
+                "the 4 fields; fine level 134 MB per vector, HBM resident")
+        data = f"synthetic seeded IC (SURVEY 8d): {w.name}, no dataset"
+    else:
+        kern = "k_cg1d (cluster-resident Jacobi-PCG, one launch per implicit solve)"
+        note = ("8N[(3+V)+k(10+V)] bytes per solve (SURVEY 8d), V=1; the level fits in shared memory, so the "
+                "kernel is latency bound, not HBM bound")
+        data = f"synthetic seeded IC (SURVEY 8d): {w.name}, no dataset"
+    res = {
+        "value": value, "ms_per_step": 1e3 * t_max / steps, "steps": steps, "warmup": warmup, "data": data,
+        "config": {
+            "workload": w.name, "n_elem": (w.nex * w.ney) if is2d else w.n_elem,
+            "degrees": [w.p_coarse, w.p_fine], "nodes": [w.m_coarse, w.m_fine],
+            "dt": dt, "steps_to_t_end": n_total,
+            "schedule": f"SI(2) incremental, radau_right, fmg start, {w.n_cycles} V-cycles + closing fine sweep"
+                        + ("; FAS residual restricted mass-consistently (DESIGN.md)" if is2d else
+                           " (the reference itself diverges with >= 4 cycles on cfg2, DESIGN.md)"),
+            "fine_sweeps_per_step": w.n_cycles + 1, "coarse_passes_per_step": 2 + 2 * w.n_cycles,
+            "dof_sweeps_per_step": U, "fine_dof_sweeps_per_s": U_fine * steps * world / t_max,
+            "cg_solves_per_step": solves_per_step,
+            "cg_mean_iterations": float(np.mean(step_its)) if len(step_its) else None,
+            "cg_rtol": 1e-14, "l2": "256 MiB buffer written between timed steps, outside the CUDA events",
+            "parallelism": "replicas" if world > 1 else "single GPU",
+            "timing": "CUDA events around each CUDA-graph slab replay, summed; max over ranks",
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": measured_traffic("2d" if is2d else "1d"),
+                     "peak_kind": peak_kind, "kernel": kern, "kernel_us": t_cg * 1e6,
+                     "kernel_mean_iterations": k_cg, "algorithmic_bytes_per_launch": bytes_cg, "note": note},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * hier.fine.ctx.ndof,
+                "d2h_bytes_per_step": 8 * hier.fine.ctx.ndof},
+        "gpu_launches": int(g.kernels_per_step * steps),
+    }
+    del g, hier, flush
+    return res
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2504_18526_b200.configs import WORKLOADS
+    from paper_2504_18526_b200.runtime import get_runtime
+    w = WORKLOADS[args.workload]
+    if args.cycles is not None:
+        import dataclasses
+        w = dataclasses.replace(w, n_cycles=args.cycles)
+    rt = get_runtime(local)
+    rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=args.cluster_ctas)
+    r = measure(w, args, torch, rt, rank, world, local, args.steps, args.warmup)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not is2d:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not hasattr(w, "nex"):
         rate, tstep = cpu_port_rate(w, args.cpu_sample_steps, threads_limit=1)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"{args.cpu_sample_steps} SI-MLSDC steps of {w.name} from the seeded IC, "
                          f"{tstep * 1e3:.1f} ms/step: oracle restatement of the reference algorithm "
                          "(SuperLU + defect iteration), numpy/scipy, 1 thread"}
+    secondary = None
+    if world == 1 and args.also_2d and not hasattr(w, "nex"):
+        torch.cuda.empty_cache()
+        w2 = WORKLOADS["cfg4"]
+        r2 = measure(w2, args, torch, rt, rank, world, local, 3, 3)
+        secondary = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64", **r2,
+                     "note": "BASELINE configs[3] (2-D Navier-Stokes shear layer 256^2, P 7/3, M 5/3), same "
+                             "contract as the main line; reported beside it because the headline config is 1-D"}
     if rank == 0:
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic seeded IC (SURVEY 8d); periodic Burgers, no dataset",
-            "config": {
-                "workload": w.name + (" (BASELINE configs[1])" if not is2d else " (BASELINE 2-D config)"),
-                "n_elem": (w.nex * w.ney) if is2d else w.n_elem, "degrees": [w.p_coarse, w.p_fine],
-                "nodes": [w.m_coarse, w.m_fine],
-                "dt": dt, "steps_to_t_end": n_total,
-                "schedule": f"SI(2) incremental, radau_right, fmg start, {w.n_cycles} V-cycles + closing fine "
-                            "sweep (5 cycles diverge in the reference itself, DESIGN.md)",
-                "fine_sweeps_per_step": w.n_cycles + 1, "coarse_passes_per_step": 2 + 2 * w.n_cycles,
-                "dof_sweeps_per_step": U, "fine_dof_sweeps_per_s": U_fine * args.steps * world / t_max,
-                "cg_solves_per_step": solves_per_step, "cg_mean_iterations": float(np.mean(step_its)) if len(step_its) else None,
-                "cg_rtol": 1e-14, "l2": "256 MiB buffer written between timed steps, outside the CUDA events",
-                "parallelism": "replicas" if world > 1 else "single GPU",
-                "timing": "CUDA events around each CUDA-graph slab replay, summed; max over ranks",
-            },
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": measured_traffic(), "peak_kind": peak_kind,
-                         "kernel": "k_cg1d (cluster-resident Jacobi-PCG, one launch per implicit solve)",
-                         "kernel_us": t_cg * 1e6, "kernel_mean_iterations": k_cg,
-                         "algorithmic_bytes_per_launch": bytes_cg,
-                         "note": "8N[(3+V)+k(10+V)] bytes per solve, V=1; the level fits in shared memory, "
-                                 "so the kernel is latency bound, not HBM bound"},
-            "cpu_baseline": cpu,
-            "clocks": clk.summary(),
-            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * hier.fine.ctx.ndof,
-                    "d2h_bytes_per_step": 8 * hier.fine.ctx.ndof},
-            "gpu_launches": int(g.kernels_per_step * args.steps),
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": r["data"],
+            "config": {**r["config"], "workload": r["config"]["workload"]
+                       + (" (BASELINE configs[1])" if args.workload == "cfg2" else "")},
+            "roofline": r["roofline"], "cpu_baseline": cpu, "clocks": r["clocks"], "e2e": r["e2e"],
+            "gpu_launches": r["gpu_launches"],
         }
+        if secondary is not None:
+            out["secondary"] = {"cfg4": secondary}
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
