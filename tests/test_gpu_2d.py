@@ -93,3 +93,103 @@ def test_mlsdc_step_2d(rt):
     assert np.linalg.norm(sol.u[-1].cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-11
     assert its == [i for i, _ in log]
     rt.raise_on_failure()
+
+
+@pytest.mark.parametrize("base,nex,ney", [(CFG4, 5, 3), (CFG3, 7, 5)])
+def test_mlsdc_step_2d_shapes(rt, base, nex, ney):
+    """One SI-MLSDC step on non-square meshes, with (cfg4: NS, nu > 0) and
+    without (cfg3: Euler) the physical diffusion: GPU vs restatement, identical
+    CG iteration sequence."""
+    from paper_2504_18526_b200 import dgsem, dgsem2d, mlsdc
+    w = small(base, nex, ney)
+    L = w.length
+    mk = lambda P: dgsem2d.DGOperator2D(dgsem2d.Mesh2D(0.0, L, 0.0, L, w.nex, w.ney, P),
+                                        dgsem2d.CompressibleEuler2D(w.gamma, w.nu))
+    h = mlsdc.build_p_hierarchy(mk, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+    X, Y = h.fine.ctx.mesh.nodes_xy
+    u0 = w.initial_state(X, Y)
+    dt = w.time_step(u0, dgsem.compute_delta(w.p_fine))
+    n0 = rt.status()[2]
+    sol = mlsdc.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, strategy="fmg")
+    its = rt.cg_log()[0][n0:].tolist()
+    oh, log = workloads.build_hierarchy_2d(lambda: dg2d.Euler2D(w.gamma, w.nu), 0.0, L, 0.0, L, w.nex, w.ney,
+                                           w.p_coarse, w.p_fine, w.m_coarse, w.m_fine)
+    so = osw.run_mlsdc(oh, u0, 0.0, dt, w.n_cycles, "fmg")
+    ref = so.u[-1]
+    assert np.linalg.norm(sol.u[-1].cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-11
+    assert its == [i for i, _ in log]
+    rt.raise_on_failure()
+
+
+@pytest.mark.parametrize("nex,ney,P", [(16, 12, 7), (13, 9, 3), (9, 17, 7)])
+def test_implicit_solve_2d_larger(rt, nex, ney, P):
+    """Implicit solves on meshes with many strip tiles / warps (and strips that
+    do not divide the row): identical iterations and solution vs restatement."""
+    w = small(CFG4, nex, ney)
+    op, orc, u = pair(w, P)
+    for a in (2e-3, 5e-2):
+        c = op.modified_diffusion_matrix(u, a, "si2")
+        n0 = rt.status()[2]
+        x = op.implicit_solve(c, a, u)
+        xo = orc.implicit_solve(orc.modified_coeff(u, a), a, u)
+        assert rt.cg_log()[0][n0:].tolist() == [orc.cg_log[-1][0]]
+        assert rel(x, xo) < 1e-13
+
+
+def test_graph_replay_equals_eager_2d(rt):
+    """A captured 2-D slab replays bitwise like the eager slab."""
+    from paper_2504_18526_b200 import dgsem, dgsem2d, mlsdc
+    w = small(CFG4, 6, 4)
+    L = w.length
+    mk = lambda P: dgsem2d.DGOperator2D(dgsem2d.Mesh2D(0.0, L, 0.0, L, w.nex, w.ney, P),
+                                        dgsem2d.CompressibleEuler2D(w.gamma, w.nu))
+    h = mlsdc.build_p_hierarchy(mk, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+    X, Y = h.fine.ctx.mesh.nodes_xy
+    u0 = w.initial_state(X, Y)
+    dt = w.time_step(u0, dgsem.compute_delta(w.p_fine))
+    eager = mlsdc.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, strategy="fmg").u[-1].clone()
+    g = mlsdc.SlabGraph(h, u0, 0.0, dt, w.n_cycles, "fmg")
+    g.step()
+    assert bool((g.u == eager).all())
+
+
+def test_full_size_properties_cfg4(rt):
+    """BASELINE cfg4 size (256^2 elements, P = 7, 16.8M DOF): the implicit
+    solve conserves the mass-weighted integral of every field (periodic SIP has
+    zero column sums), free stream is a fixed point of the convection, and the
+    solve reproduces its right-hand side when applied back (residual check)."""
+    import torch
+    from paper_2504_18526_b200 import dgsem, dgsem2d
+    w = CFG4
+    mesh = dgsem2d.Mesh2D(0.0, w.length, 0.0, w.length, w.nex, w.ney, w.p_fine)
+    op = dgsem2d.DGOperator2D(mesh, dgsem2d.CompressibleEuler2D(w.gamma, w.nu))
+    X, Y = mesh.nodes_xy
+    u = rt.to_device(w.initial_state(X, Y))
+    dt = w.time_step(u.cpu().numpy(), dgsem.compute_delta(w.p_fine))
+    a = 0.5 * dt
+    c = op.modified_diffusion_matrix(u, a, "si2")
+    n0 = rt.status()[2]
+    x = op.implicit_solve(c, a, u)
+    its = rt.cg_log()[0][n0:]
+    assert len(its) == 1 and 1 <= its[0] < 200
+    wq = mesh.mass_weights if hasattr(mesh, "mass_weights") else None
+    nc = 4
+    xs, us = x.view(nc, -1), u.view(nc, -1)
+    if wq is None:
+        from paper_2504_18526_b200.collocation import gauss_lobatto
+        _, wl = gauss_lobatto(w.p_fine + 1)
+        wl = torch.tensor(wl, dtype=torch.float64, device=u.device)
+        wq = torch.outer(wl, wl).reshape(-1).repeat(w.nex * w.ney)
+    for f in range(nc):
+        ix, iu = float((xs[f] * wq).sum()), float((us[f] * wq).sum())
+        assert abs(ix - iu) <= 1e-11 * max(1.0, float((us[f].abs() * wq).sum()))
+    # (M + a B) x == M rhs: M x - a M apply_diffusion(c, x) against M u
+    r = x - a * op.apply_diffusion(c, x) - u
+    assert float(r.abs().max()) <= 1e-9 * float(u.abs().max())
+    free = torch.zeros_like(u).view(nc, -1)
+    free[0] = 1.0
+    free[1] = 0.3
+    free[2] = -0.2
+    free[3] = 2.5 + 0.5 * (0.3 ** 2 + 0.2 ** 2)
+    conv = op.apply_convection(free.reshape(-1))
+    assert float(conv.abs().max()) < 1e-11
