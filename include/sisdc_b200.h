@@ -197,6 +197,39 @@ int  sisdc_xfer_fas_restrict(sisdc_xfer* x, const double* Wf, double dt, int inc
  * (transfer.py:344-352, mlsdc.py:125-126,134-142). */
 int  sisdc_xfer_interp(sisdc_xfer* x, int accumulate, const double* uc, const double* vc, double* uf);
 
+/* ------------------------------ element-row partitioned 2-D operators
+ * (BASELINE north star: elements partitioned across the GPUs of one
+ * box, NCCL only for the face halo and the CG allreduce).  The reference has no
+ * parallel path; these calls have no reference counterpart.
+ * A partitioned operator owns contiguous element-row blocks of the global
+ * mesh `desc`; rank q of nranks owns rows [q*b + min(q,r), +b + (q<r)) with
+ * b = ney/nranks, r = ney%nranks.  Its state vectors are the concatenation of
+ * its local partitions, each stored (ncomp, rows+2, nex, P+1, P+1) with one
+ * ghost row on either side (the neighbours' boundary rows, refreshed by the
+ * operator itself before every face-coupled kernel).  Every OperatorContext,
+ * sweep-stage and transfer entry point above accepts it unchanged (transfers
+ * with n_elem = the storage element slabs, ghost rows included).
+ *  - comm == NULL: all nranks partitions are local to this process
+ *    (nlocal == nranks, first_rank 0): halo exchange and allreduce are device
+ *    copies / fixed-order sums (one GPU emulating nranks ranks).
+ *  - comm != NULL: one local partition, rank = comm's rank; halo exchange by
+ *    NCCL send/recv, the CG dot products by one NCCL allreduce per iteration.
+ * The partitioned implicit solve polls its convergence flag on the host once
+ * per two iterations and therefore cannot be captured in a CUDA graph. */
+typedef struct sisdc_comm sisdc_comm;
+/* NCCL unique id (128 bytes) made on rank 0 and broadcast by the caller. */
+int  sisdc_nccl_unique_id(unsigned char* id128);
+int  sisdc_comm_create(sisdc_ctx* ctx, const unsigned char* id128, int nranks, int rank, sisdc_comm** out);
+void sisdc_comm_destroy(sisdc_comm* comm);
+int  sisdc_op2d_create_part(sisdc_ctx* ctx, const sisdc_op2d_desc* global_desc, int nranks, int first_rank,
+                            int nlocal, sisdc_comm* comm, sisdc_op1d** out);
+/* Local partitions: first global row, owned rows, offset in a state vector. */
+int  sisdc_op2d_part_layout(const sisdc_op1d* op, int cap, int* row_begin, int* row_count, int64_t* offset,
+                            int* nparts);
+/* Refresh the ghost rows of mcount node vectors (stride mstride) of a state
+ * (scalar_field 0) or of a scalar coefficient field (scalar_field 1). */
+int  sisdc_halo_exchange(sisdc_op1d* op, double* vec, int mcount, int64_t mstride, int scalar_field);
+
 #ifdef __cplusplus
 }
 #endif

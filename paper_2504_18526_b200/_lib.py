@@ -91,6 +91,12 @@ SIGNATURES = {
     "sisdc_xfer_down": (I, [P, I, I, P, P]),
     "sisdc_xfer_fas_restrict": (I, [P, DP, D, I, P, P, P, P, P, P]),
     "sisdc_xfer_interp": (I, [P, I, P, P, P]),
+    "sisdc_nccl_unique_id": (I, [C.c_char_p]),
+    "sisdc_comm_create": (I, [P, C.c_char_p, I, I, C.POINTER(P)]),
+    "sisdc_comm_destroy": (None, [P]),
+    "sisdc_op2d_create_part": (I, [P, C.POINTER(Op2DDesc), I, I, I, P, C.POINTER(P)]),
+    "sisdc_op2d_part_layout": (I, [P, I, C.POINTER(I), C.POINTER(I), C.POINTER(C.c_int64), C.POINTER(I)]),
+    "sisdc_halo_exchange": (I, [P, P, I, C.c_int64, I]),
 }
 
 _lib = None

@@ -12,30 +12,7 @@
 
 using namespace sisdc;
 
-struct sisdc_ctx {
-  Ctx c;
-};
-
-struct sisdc_op1d {   // dimension-tagged operator handle (1-D or 2-D)
-  sisdc_ctx* ctx;
-  int dim = 1;
-  sisdc_op1d_desc desc;
-  Op1DDev dev;
-  Op2DDev dev2;
-  double* d_tab = nullptr;
-  double* d_cgws = nullptr;   // 2-D CG workspace (allocated at creation: graph-safe)
-  int cg_blocks = 0;
-  std::vector<double> nodes, weights, D;
-  long long n() const { return dim == 1 ? dev.n : dev2.n; }
-};
-
-struct sisdc_xfer {
-  sisdc_ctx* ctx;
-  int dim = 1;
-  XferDev dev;
-  Xfer2Dev dev2;
-  double* d_tab = nullptr;
-};
+#include "abi_internal.h"
 
 namespace {
 
@@ -116,9 +93,6 @@ bool invert(std::vector<double> A, int n, std::vector<double>& inv) {
   }
   return true;
 }
-
-inline Ctx* C(sisdc_op1d* op) { return &op->ctx->c; }
-inline CoefDev coef(sisdc_coef k) { return CoefDev{k.kind, k.value, k.ptr}; }
 
 int check_coef(Ctx* c, sisdc_coef k) {
   if (k.kind < SISDC_COEF_NONE || k.kind > SISDC_COEF_PHYS) return c->fail(SISDC_ERR_ARG, "unknown coefficient kind");
@@ -298,8 +272,10 @@ int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) 
   return SISDC_OK;
 }
 
+}  // extern "C"
+
 // 2-D operator: shared 1-D element tables + tensor-product kernels
-int sisdc_op2d_create(sisdc_ctx* x, const sisdc_op2d_desc* d, sisdc_op1d** out) {
+int op2d_create_impl(sisdc_ctx* x, const sisdc_op2d_desc* d, bool alloc_cg, sisdc_op1d** out) {
   if (!x || !d || !out) return SISDC_ERR_ARG;
   *out = nullptr;
   Ctx& c = x->c;
@@ -333,8 +309,10 @@ int sisdc_op2d_create(sisdc_ctx* x, const sisdc_op2d_desc* d, sisdc_op1d** out) 
   }
   Op2DDev& v = op->dev2;
   v.nex = d->nex; v.ney = d->ney; v.p1 = p1; v.nc = d->ncomp;
+  v.nys = d->ney; v.row0 = 0; v.e0 = 0;
   v.nn = (long long)d->nex * d->ney * p1 * p1;
   v.n = v.nn * d->ncomp;
+  v.ns = v.n;
   v.problem = d->problem;
   v.dx = dx; v.dy = dy; v.sx = 2.0 / dx; v.sy = 2.0 / dy;
   v.mux = d->penalty * p1 * p1 / dx; v.muy = d->penalty * p1 * p1 / dy;
@@ -349,8 +327,12 @@ int sisdc_op2d_create(sisdc_ctx* x, const sisdc_op2d_desc* d, sisdc_op1d** out) 
   }
   v.tab = op->d_tab;
   int rc = set_cg2_tables(&c, p1, tab.data());
-  if (!rc) rc = cg2_blocks(&c, v, &op->cg_blocks);
+  if (!rc && alloc_cg) rc = cg2_blocks(&c, v, &op->cg_blocks);
   if (rc) { cudaFree(op->d_tab); delete op; return rc; }
+  if (!alloc_cg) {
+    *out = op;
+    return SISDC_OK;
+  }
   const size_t ws = 5 * (size_t)v.n + 2 * (size_t)v.nn + 16 + 8 * (size_t)op->cg_blocks;
   e = cudaMalloc(&op->d_cgws, ws * sizeof(double));
   if (e != cudaSuccess) {
@@ -363,8 +345,15 @@ int sisdc_op2d_create(sisdc_ctx* x, const sisdc_op2d_desc* d, sisdc_op1d** out) 
   return SISDC_OK;
 }
 
+extern "C" {
+
+int sisdc_op2d_create(sisdc_ctx* x, const sisdc_op2d_desc* d, sisdc_op1d** out) {
+  return op2d_create_impl(x, d, true, out);
+}
+
 void sisdc_op1d_destroy(sisdc_op1d* op) {
   if (!op) return;
+  if (op->parted()) part2_destroy(op);
   cudaFree(op->d_tab);
   cudaFree(op->d_cgws);
   delete op;
@@ -381,6 +370,7 @@ int sisdc_op1d_tables(const sisdc_op1d* op, double* nodes, double* weights, doub
 
 int sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art) {
   if (!op) return SISDC_ERR_ARG;
+  if (op->parted() && nu_art) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "artificial viscosity on a partitioned operator");
   op->dev.nu_art = nu_art;
   op->dev2.nu_art = nu_art;
   return SISDC_OK;
@@ -394,6 +384,7 @@ int sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, dou
 
 int sisdc_apply_convection(sisdc_op1d* op, const double* u, double, double* out) {
   if (!op || !u || !out) return SISDC_ERR_ARG;
+  if (op->parted()) return part2_conv(op, u, out);
   if (op->dim == 2) return launch2_conv(C(op), op->dev2, u, out);
   return launch_apply_convection(C(op), op->dev, u, out);
 }
@@ -403,12 +394,14 @@ int sisdc_apply_diffusion(sisdc_op1d* op, sisdc_coef k, const double* u, double,
   if (int rc = check_coef(C(op), k)) return rc;
   if (k.kind == SISDC_COEF_NONE || (k.kind == SISDC_COEF_CONST && k.value == 0.0))
     return C(op)->cuda(cudaMemsetAsync(out, 0, op->n() * sizeof(double), C(op)->stream), "zero");
+  if (op->parted()) return part2_sip(op, coef(k), u, out);
   if (op->dim == 2) return launch2_sip(C(op), op->dev2, coef(k), u, out);
   return launch_apply_diffusion(C(op), op->dev, coef(k), u, out);
 }
 
 int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double, double* out) {
   if (!op || !u || !out) return SISDC_ERR_ARG;
+  if (op->parted()) return part2_eval_nodes(op, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
   return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
@@ -417,6 +410,7 @@ int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double, double* out) {
 int sisdc_coef_field(sisdc_op1d* op, sisdc_coef k, double* out) {
   if (!op || !out) return SISDC_ERR_ARG;
   if (int rc = check_coef(C(op), k)) return rc;
+  if (op->parted()) return part2_coef_field(op, coef(k), out);
   if (op->dim == 2) return launch2_coef(C(op), op->dev2, coef(k), out);
   return launch_coef_field(C(op), op->dev, coef(k), out);
 }
@@ -429,6 +423,7 @@ int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* r
     return sisdc_copy(op->ctx, x, rhs, op->n());
   }
   if (k.kind == SISDC_COEF_NONE) return C(op)->fail(SISDC_ERR_ARG, "cannot assemble a zero coefficient");
+  if (op->parted()) return part2_solve(op, coef(k), a, rhs, x);
   if (op->dim == 2) return launch2_cg(C(op), op->dev2, coef(k), a, rhs, x, op->d_cgws, op->cg_blocks);
   return launch_cg1d(C(op), op->dev, coef(k), a, rhs, x);
 }
@@ -437,6 +432,7 @@ int sisdc_stage_rhs(sisdc_op1d* op, const double* base, const double* conv_in, d
                     int M, const double* w_row, double dt, const double* g_m, const double* h_old, double,
                     double* rhs, double* conv_out) {
   if (!op || !base || !conv_in || !rhs || M < 0 || M > MAXM || (f_old && !w_row)) return SISDC_ERR_ARG;
+  if (op->parted()) return part2_stage(op, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
   if (op->dim == 2) return launch2_stage(C(op), op->dev2, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
   return launch_stage_rhs(C(op), op->dev, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
 }
@@ -447,6 +443,7 @@ int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_coun
   if (!op || !u0 || !u || !dts || !f || !h1) return SISDC_ERR_ARG;
   if (scheme < SISDC_EULER || scheme > SISDC_SI2) return C(op)->fail(SISDC_ERR_ARG, "unknown scheme");
   if (conv_prev && m_count != 1) return C(op)->fail(SISDC_ERR_ARG, "conv_prev needs m_count == 1");
+  if (op->parted()) return part2_eval_nodes(op, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
   return launch_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
@@ -454,6 +451,7 @@ int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_coun
 
 int sisdc_eval_rhs_nodes(sisdc_op1d* op, int M, const double* u, const double*, double* f) {
   if (!op || !u || !f || M < 1 || M > MAXM) return SISDC_ERR_ARG;
+  if (op->parted()) return part2_eval_nodes(op, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
   if (op->dim == 2) return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
   return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
 }

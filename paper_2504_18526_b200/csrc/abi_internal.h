@@ -1,0 +1,71 @@
+// Internal definitions of the opaque ABI handles, shared by abi.cu and
+// part2d.cu (element-row partitioned 2-D operators).
+#pragma once
+#include <vector>
+#include "sisdc_dev.cuh"
+#include "sisdc_dev2d.cuh"
+#include "sisdc_host.h"
+
+struct sisdc_ctx {
+  sisdc::Ctx c;
+};
+
+struct sisdc_comm;   // NCCL communicator (part2d.cu)
+
+// one element-row partition of a 2-D operator (ghost-row storage)
+struct Part2D {
+  sisdc::Op2DDev dev;
+  long long off = 0;    // offset of the partition in a state vector of the operator
+  long long offc = 0;   // offset in a scalar (coefficient) field
+  int row_begin = 0;    // first owned global element row
+  int rank = 0;         // global rank that owns it
+  double* ws = nullptr; // split-CG workspace (cg2p_ws_doubles)
+  int G = 0;            // blocks of the split-CG kernels
+};
+
+struct sisdc_op1d {   // dimension-tagged operator handle (1-D or 2-D)
+  sisdc_ctx* ctx;
+  int dim = 1;
+  sisdc_op1d_desc desc;
+  sisdc::Op1DDev dev;
+  sisdc::Op2DDev dev2;
+  double* d_tab = nullptr;
+  double* d_cgws = nullptr;   // 2-D CG workspace (allocated at creation: graph-safe)
+  int cg_blocks = 0;
+  std::vector<double> nodes, weights, D;
+  // partitioned 2-D operator (empty parts: single periodic domain)
+  std::vector<Part2D> parts;
+  sisdc_comm* comm = nullptr;  // NULL: every partition is local (in-process)
+  int nranks = 1;
+  long long n_total = 0, nn_total = 0;
+  double* d_red = nullptr;           // [0..3] local partial sums, [4..7] allreduced sums
+  sisdc::CgPScal* d_sc = nullptr;
+  int* h_done = nullptr;             // pinned [2]
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool parted() const { return !parts.empty(); }
+  long long n() const { return dim == 1 ? dev.n : (parted() ? n_total : dev2.n); }
+};
+
+struct sisdc_xfer {
+  sisdc_ctx* ctx;
+  int dim = 1;
+  sisdc::XferDev dev;
+  sisdc::Xfer2Dev dev2;
+  double* d_tab = nullptr;
+};
+
+inline sisdc::Ctx* C(sisdc_op1d* op) { return &op->ctx->c; }
+inline sisdc::CoefDev coef(sisdc_coef k) { return sisdc::CoefDev{k.kind, k.value, k.ptr}; }
+
+// 2-D operator creation (abi.cu); alloc_cg = false skips the cooperative-CG workspace
+int op2d_create_impl(sisdc_ctx* x, const sisdc_op2d_desc* d, bool alloc_cg, sisdc_op1d** out);
+void part2_destroy(sisdc_op1d* op);
+// partitioned OperatorContext entry points (part2d.cu)
+int part2_conv(sisdc_op1d* op, const double* u, double* out);
+int part2_sip(sisdc_op1d* op, sisdc::CoefDev k, const double* u, double* out);
+int part2_coef_field(sisdc_op1d* op, sisdc::CoefDev k, double* out);
+int part2_eval_nodes(sisdc_op1d* op, int mode, int scheme, int M, int m_first, int m_count, const double* u0,
+                     const double* u, const double* conv_prev, const double* dts, double* f, double* h1, double* h2);
+int part2_stage(sisdc_op1d* op, const double* base, const double* conv_in, double dt_m, const double* f_old, int M,
+                const double* w_row, double dt, const double* g, const double* h, double* rhs, double* conv_out);
+int part2_solve(sisdc_op1d* op, sisdc::CoefDev k, double a, const double* rhs, double* x);

@@ -34,7 +34,8 @@ struct Sm2 {
 enum { FR = 0, FL = 1, FT = 2, FB = 3 };   // right, left, top, bottom neighbour faces
 
 struct Node2 {
-  int el, nd, i, j, eg, ey, ex;
+  int el, nd, i, j, eg, ey, ex;   // eg: owned element index; ey: STORAGE row
+  int es;                          // storage element index ey * nex + ex
   bool valid;
 };
 template <int P1>
@@ -48,8 +49,10 @@ __device__ __forceinline__ Node2 node2(const Op2DDev& op, int tile) {
   n.eg = tile * Blk<P1>::EB + n.el;
   n.valid = n.el < Blk<P1>::EB && n.eg < op.nex * op.ney;
   const int eg = n.valid ? n.eg : 0;
-  n.ey = eg / op.nex;
-  n.ex = eg - n.ey * op.nex;
+  const int oy = eg / op.nex;
+  n.ex = eg - oy * op.nex;
+  n.ey = oy + op.row0;
+  n.es = n.ey * op.nex + n.ex;
   return n;
 }
 
@@ -112,7 +115,7 @@ __device__ __forceinline__ void conv_block(const Op2DDev& op, double* sm, const 
       for (int c = 0; c < NC_MAX && c < op.nc; ++c) vx[c] += fh[c];
     }
     if (n.j == P) {   // top y-face
-      const int eyt = wrapi(n.ey + 1, op.ney);
+      const int eyt = ynb(op, n.ey, 1);
 #pragma unroll
       for (int c = 0; c < NC_MAX && c < op.nc; ++c) nb[c] = u[nidx(op, c, eyt, n.ex, 0, n.i)];
       rusanov2d(op, s, nb, 1, fh);
@@ -120,7 +123,7 @@ __device__ __forceinline__ void conv_block(const Op2DDev& op, double* sm, const 
       for (int c = 0; c < NC_MAX && c < op.nc; ++c) vy[c] -= fh[c];
     }
     if (n.j == 0) {   // bottom y-face
-      const int eyb = wrapi(n.ey - 1, op.ney);
+      const int eyb = ynb(op, n.ey, -1);
 #pragma unroll
       for (int c = 0; c < NC_MAX && c < op.nc; ++c) nb[c] = u[nidx(op, c, eyb, n.ex, P, n.i)];
       rusanov2d(op, nb, s, 1, fh);
@@ -156,7 +159,7 @@ __device__ __forceinline__ void sip_block(const Op2DDev& op, double* sm, const C
   double* FUo = sm + Sm2<P1>::FU + n.el * 4 * P1;
   double* FQo = sm + Sm2<P1>::FQ + n.el * 4 * P1;
   const int exr = wrapi(n.ex + 1, op.nex), exl = wrapi(n.ex - 1, op.nex);
-  const int eyt = wrapi(n.ey + 1, op.ney), eyb = wrapi(n.ey - 1, op.ney);
+  const int eyt = ynb(op, n.ey, 1), eyb = ynb(op, n.ey, -1);
   const long long fld = op.nn;
   auto in_field = [&](int ey, int ex, int j, int i) -> long long {
     return ((long long)ey * op.nex + ex) * NN + j * P1 + i;
@@ -300,8 +303,8 @@ __global__ void __launch_bounds__(256) k2_node_eval(Op2DDev op, Cache2Args a) {
   __syncthreads();
   const Node2 n = node2<P1>(op, blockIdx.x);
   const int m = a.m_first + blockIdx.y;
-  const double* um = a.u + (size_t)m * op.n;
-  const double* up = m == 0 ? a.u0 : a.u + (size_t)(m - 1) * op.n;
+  const double* um = a.u + (size_t)m * op.ns;
+  const double* up = m == 0 ? a.u0 : a.u + (size_t)(m - 1) * op.ns;
   double cm[NC_MAX], d[NC_MAX];
   conv_block<P1>(op, sm, um, n, cm);
   double ph;
@@ -312,8 +315,8 @@ __global__ void __launch_bounds__(256) k2_node_eval(Op2DDev op, Cache2Args a) {
 #pragma unroll
     for (int c = 0; c < NC_MAX && c < op.nc; ++c) {
       const double f = has_phys ? cm[c] + d[c] : cm[c];
-      if (!isfinite(f)) atomicMin(a.status, n.eg);
-      a.f[(size_t)m * op.n + nidx(op, c, n.ey, n.ex, n.j, n.i)] = f;
+      if (!isfinite(f)) atomicMin(a.status, (int)(op.e0 + n.eg));
+      a.f[(size_t)m * op.ns + nidx(op, c, n.ey, n.ex, n.j, n.i)] = f;
     }
   if (a.mode == 0) return;
   double dtm = 0.0;   // static-index select (a dynamic index copies the parameter block to local memory)
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(256) k2_node_eval(Op2DDev op, Cache2Args a) {
     if (n.valid)
 #pragma unroll
       for (int c = 0; c < NC_MAX && c < op.nc; ++c) {
-        const long long g = (size_t)m * op.n + nidx(op, c, n.ey, n.ex, n.j, n.i);
+        const long long g = (size_t)m * op.ns + nidx(op, c, n.ey, n.ex, n.j, n.i);
         a.h1[g] = 0.0;
         if (a.h2) a.h2[g] = 0.0;
       }
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(256) k2_node_eval(Op2DDev op, Cache2Args a) {
   if (n.valid)
 #pragma unroll
     for (int c = 0; c < NC_MAX && c < op.nc; ++c) {
-      const long long g = (size_t)m * op.n + nidx(op, c, n.ey, n.ex, n.j, n.i);
+      const long long g = (size_t)m * op.ns + nidx(op, c, n.ey, n.ex, n.j, n.i);
       a.h1[g] = dtm * (cp[c] + d[c]);
       if (a.h2) a.h2[g] = dtm * (cm[c] + d[c]);
     }
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(256) k2_stage(Op2DDev op, Stage2Args a) {
     double q = 0.0;
     if (a.f_old) {
       double acc = 0.0;
-      for (int jj = 0; jj < a.M; ++jj) acc = fma(a.w[jj], a.f_old[(size_t)jj * op.n + gi], acc);
+      for (int jj = 0; jj < a.M; ++jj) acc = fma(a.w[jj], a.f_old[(size_t)jj * op.ns + gi], acc);
       q = a.dt * acc;
     }
     if (a.g) q = q + a.g[gi];
@@ -545,6 +548,9 @@ struct Cg2Args {
   int log_cap;
   long long* timing;   // diagnostics: globaltimer stamps of blocks 0 and G-1 (nullable)
   int dbg;             // diagnostics only (SISDC_CG_DBG): 1 skip staging, 2 skip unit compute
+  // partitioned (split) solve only: phase-B partial slots and the solve scalars
+  double* part2;       // [gridDim][4]
+  const struct CgPScal* sc;
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -602,14 +608,14 @@ __device__ __forceinline__ void cg_tile(const Op2DDev& op, double* sm, int tile,
   constexpr int NN = P1 * P1, EB = Blk<P1>::EB, P = P1 - 1, RP = L::RP, NP = L::NP, NS = L::NS;
   constexpr int nc = NC;
   const long long fld = op.nn;
-  const int ey = tile / tpr, ex0 = (tile - ey * tpr) * EB;
+  const int oy = tile / tpr, ex0 = (tile - oy * tpr) * EB, ey = oy + op.row0;
   const int cnt = min(EB, op.nex - ex0);
   // tile-variant zero (tile < 2^30): keeps the constant-bank matrix loads inside the
   // tile loop (uniform-register operands) instead of hoisted into the register file
   const double* ct = c_tab2 + (tile >> 30);
   const long long rowm = (long long)ey * op.nex;
-  const long long rowt = (long long)wrapi(ey + 1, op.ney) * op.nex;
-  const long long rowb = (long long)wrapi(ey - 1, op.ney) * op.nex;
+  const long long rowt = (long long)ynb(op, ey, 1) * op.nex;
+  const long long rowb = (long long)ynb(op, ey, -1) * op.nex;
   const int exl = wrapi(ex0 - 1, op.nex), exr = wrapi(ex0 + cnt, op.nex);
   __syncthreads();   // the previous tile's readers are done with the buffers
   // ---- stage: strip + x-halo (slots 0..cnt+1), rows above / below (contiguous
@@ -1012,10 +1018,10 @@ __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const d
   const int swz = r * 8 + 2 * ((lane & 3) ^ (r >> 1));            // row r, chunk lane&3 (swizzled)
   const int tr0 = nsw(lane & 7, lane >> 3), tr1 = nsw(lane & 7, 4 + (lane >> 3));   // transposed: node v -> line v%8, pos v/8
   for (int e = blockIdx.x * nwb + warp; e < ne; e += gridDim.x * nwb) {
-    const int ey = e / op.nex, ex = e - ey * op.nex;
+    const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
     const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
-    const int eyt = ey + 1 == op.ney ? 0 : ey + 1, eyb = ey == 0 ? op.ney - 1 : ey - 1;
-    const unsigned eo = (unsigned)e * 64u;
+    const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
+    const unsigned eo = ((unsigned)ey * op.nex + ex) * 64u;
     const unsigned nb[4] = {((unsigned)ey * op.nex + exr) * 64u, ((unsigned)ey * op.nex + exl) * 64u,
                             ((unsigned)eyt * op.nex + ex) * 64u, ((unsigned)eyb * op.nex + ex) * 64u};
 #pragma unroll
@@ -1110,8 +1116,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
   double* ws = sm + warp * W::WARP;
   const int m = a.m_first + blockIdx.y;
   const long long nn = op.nn;
-  const double* um = a.u + (size_t)m * op.n;
-  const double* up = m == 0 ? a.u0 : a.u + (size_t)(m - 1) * op.n;
+  const double* um = a.u + (size_t)m * op.ns;
+  const double* up = m == 0 ? a.u0 : a.u + (size_t)(m - 1) * op.ns;
   double dtm = 0.0;   // static-index select: a dynamic index would copy the parameter block to local memory
 #pragma unroll
   for (int j = 0; j < 16; ++j)
@@ -1136,10 +1142,10 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
   }
   const int ne = op.nex * op.ney;
   for (int e = blockIdx.x * EV_WARPS + warp; e < ne; e += gridDim.x * EV_WARPS) {
-    const int ey = e / op.nex, ex = e - ey * op.nex;
+    const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
     const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
-    const int eyt = ey + 1 == op.ney ? 0 : ey + 1, eyb = ey == 0 ? op.ney - 1 : ey - 1;
-    const unsigned eo = (unsigned)e * 64u;
+    const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
+    const unsigned eo = ((unsigned)ey * op.nex + ex) * 64u;
     const unsigned nb[4] = {((unsigned)ey * op.nex + exr) * 64u, ((unsigned)ey * op.nex + exl) * 64u,
                             ((unsigned)eyt * op.nex + ex) * 64u, ((unsigned)eyb * op.nex + ex) * 64u};
 #pragma unroll
@@ -1220,9 +1226,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
       }
       double cm0, cm1;
       wpe_conv<NC>(op, K, ws + W::OWN, ws + W::FHM, c, ws + W::FX, ws + W::FY, cm0, cm1);
-      const long long go = (size_t)m * op.n + c * nn + gi;
+      const long long go = (size_t)m * op.ns + c * nn + gi;
       const double f0 = has_phys ? cm0 + dp0 : cm0, f1 = has_phys ? cm1 + dp1 : cm1;
-      if (!isfinite(f0) || !isfinite(f1)) atomicMin(a.status, e);
+      if (!isfinite(f0) || !isfinite(f1)) atomicMin(a.status, (int)(op.e0 + e));
       *reinterpret_cast<double2*>(a.f + go) = make_double2(f0, f1);
       if (a.mode == 0) continue;
       if (!need_h) {
@@ -1304,7 +1310,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     double* CS = sm + Sm2<P1>::CS + n.el * NN;
     double* FCo = sm + Sm2<P1>::FC + n.el * 4 * P1;
     const int exr = wrapi(n.ex + 1, op.nex), exl = wrapi(n.ex - 1, op.nex);
-    const int eyt = wrapi(n.ey + 1, op.ney), eyb = wrapi(n.ey - 1, op.ney);
+    const int eyt = ynb(op, n.ey, 1), eyb = ynb(op, n.ey, -1);
     __syncthreads();
     if (n.valid) {
       CS[n.nd] = coef2d(op, A.coef, n.ey, n.ex, n.j, n.i);
@@ -1330,7 +1336,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
       if (j == P) dy_ += op.muy * (0.5 * (CS[P * P1 + i] + FCo[FT * P1 + i])) - op.sy * CS[P * P1 + i] * DPP;
       if (j == 0) dy_ += op.muy * (0.5 * (FCo[FB * P1 + i] + CS[i])) + op.sy * CS[i] * D00;
       const double hwx = 0.5 * op.dx * c_tab2[T::W + i], hwy = 0.5 * op.dy * c_tab2[T::W + j];
-      const long long f = (long long)n.eg * NN + n.nd;
+      const long long f = (long long)n.es * NN + n.nd;
       A.Cf[f] = CS[n.nd];
       A.DINV[f] = 1.0 / (hwx * hwy + A.a * (hwy * dx_ + hwx * dy_));
     }
@@ -1504,6 +1510,345 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     }
     if (!ok) atomicAdd(&A.status[1], 1);
   }
+}
+
+// ------------------------------------------------ partitioned (split) 2-D PCG
+// k2_cg's Chronopoulos-Gear iteration for one element-row partition with ghost
+// rows, one kernel per phase, so that the face halo of u and the allreduce of
+// the three dot products (NCCL across ranks, part2d.cu) sit between launches:
+//   per iteration  update (phase A) -> halo(u) -> matvec (phase B) -> reduce
+//                  -> allreduce -> scalars
+// Per-node arithmetic is k2_cg's; the reductions are fixed-order per block,
+// per partition and then over partitions / ranks, and every rank derives
+// alpha, beta from the same allreduced sums (CgPScal), so the ranks stay in
+// lock step.  Kernels launched after convergence return immediately.
+// Workspace per partition (doubles): R W U P S (n each) | DINV Cf (nn each) |
+// partA partB (4 G each).
+__device__ __forceinline__ void blk_part3(double v0, double v1, double v2, double* red, double* slot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+  }
+  __syncthreads();
+  if (lane == 0) { red[wid * 4] = v0; red[wid * 4 + 1] = v1; red[wid * 4 + 2] = v2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int ww = 0; ww < nw; ++ww) { t0 += red[ww * 4]; t1 += red[ww * 4 + 1]; t2 += red[ww * 4 + 2]; }
+    slot[blockIdx.x * 4] = t0; slot[blockIdx.x * 4 + 1] = t1; slot[blockIdx.x * 4 + 2] = t2;
+  }
+}
+__device__ __forceinline__ long long own0(const Op2DDev& op) { return (long long)op.row0 * op.nex * op.p1 * op.p1; }
+__device__ __forceinline__ long long nown(const Op2DDev& op) { return (long long)op.ney * op.nex * op.p1 * op.p1; }
+
+// Cf at every storage node (the ghost rows' coefficient source was exchanged
+// first), x0 = rhs, p = s = 0
+template <int P1>
+__global__ void k2p_init(Cg2Args A) {
+  const Op2DDev& op = A.op;
+  constexpr int NN = P1 * P1;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < op.n; t += nt) {
+    if (t < op.nn) {
+      const long long es = t / NN;
+      const int nd = (int)(t - es * NN);
+      A.Cf[t] = coef2d(op, A.coef, (int)(es / op.nex), (int)(es % op.nex), nd / P1, nd % P1);
+    }
+    A.x[t] = A.rhs[t];
+    A.Pv[t] = 0.0;
+    A.S[t] = 0.0;
+  }
+}
+
+// closed-form Jacobi diagonal of M + a B2 at the owned nodes (k2_cg setup 1)
+template <int P1>
+__global__ void k2p_dinv(Cg2Args A) {
+  const Op2DDev& op = A.op;
+  using T = CT<P1>;
+  constexpr int NN = P1 * P1, P = P1 - 1;
+  const long long nt = (long long)gridDim.x * blockDim.x, no = nown(op);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < no; t += nt) {
+    const long long eo = t / NN;
+    const int nd = (int)(t - eo * NN), j = nd / P1, i = nd - j * P1;
+    const int oy = (int)(eo / op.nex), ex = (int)(eo - (long long)oy * op.nex), ey = oy + op.row0;
+    const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
+    const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
+    const long long es = (long long)ey * op.nex + ex;
+    const double* CS = A.Cf + es * NN;
+    double dx_ = 0.0, dy_ = 0.0;
+#pragma unroll
+    for (int q = 0; q < P1; ++q) {
+      dx_ = fma(c_tab2[T::D2W + i * P1 + q], CS[j * P1 + q], dx_);
+      dy_ = fma(c_tab2[T::D2W + j * P1 + q], CS[q * P1 + i], dy_);
+    }
+    const double DPP = c_tab2[T::D + P * P1 + P], D00 = c_tab2[T::D];
+    dx_ *= op.sx;
+    dy_ *= op.sy;
+    if (i == P) {
+      const double fr = A.Cf[((long long)ey * op.nex + exr) * NN + j * P1];
+      dx_ += op.mux * (0.5 * (CS[j * P1 + P] + fr)) - op.sx * CS[j * P1 + P] * DPP;
+    }
+    if (i == 0) {
+      const double fl = A.Cf[((long long)ey * op.nex + exl) * NN + j * P1 + P];
+      dx_ += op.mux * (0.5 * (fl + CS[j * P1])) + op.sx * CS[j * P1] * D00;
+    }
+    if (j == P) {
+      const double ft = A.Cf[((long long)eyt * op.nex + ex) * NN + i];
+      dy_ += op.muy * (0.5 * (CS[P * P1 + i] + ft)) - op.sy * CS[P * P1 + i] * DPP;
+    }
+    if (j == 0) {
+      const double fb = A.Cf[((long long)eyb * op.nex + ex) * NN + P * P1 + i];
+      dy_ += op.muy * (0.5 * (fb + CS[i])) + op.sy * CS[i] * D00;
+    }
+    const double hwx = 0.5 * op.dx * c_tab2[T::W + i], hwy = 0.5 * op.dy * c_tab2[T::W + j];
+    A.DINV[es * NN + nd] = 1.0 / (hwx * hwy + A.a * (hwy * dx_ + hwx * dy_));
+  }
+}
+
+// r0 = b - A x0 (b = M rhs); partials (b,b), #nonzero -> part2
+template <int P1, int NC>
+__global__ void __launch_bounds__(256, 2) k2p_resid(Cg2Args A) {
+  extern __shared__ double sm[];
+  using L = CgSm<P1, NC>;
+  using T = CT<P1>;
+  constexpr int NN = P1 * P1, EB = Blk<P1>::EB;
+  const Op2DDev& op = A.op;
+  double bb = 0.0, nz = 0.0;
+  auto epi = [&](long long g, double ax, double) {
+    const int nd = (int)(g % NN);
+    const double mi = (0.5 * op.dx * c_tab2[T::W + nd % P1]) * (0.5 * op.dy * c_tab2[T::W + nd / P1]);
+    const double b = mi * A.rhs[g];
+    A.R[g] = b - ax;
+    bb = fma(b, b, bb);
+    nz += b != 0.0 ? 1.0 : 0.0;
+  };
+  if constexpr (P1 == 8) {
+    wpe_phase<NC>(op, sm, A.x, A.Cf, A.a, [&](long long g, double w0, double w1, double v0, double v1) {
+      epi(g, w0, v0);
+      epi(g + 1, w1, v1);
+    });
+  } else {
+    const int tpr = (op.nex + EB - 1) / EB, ntiles = tpr * op.ney;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) cg_tile<P1, NC>(op, sm, tile, tpr, A.x, nullptr, A.Cf, A.a, epi);
+  }
+  blk_part3(bb, nz, 0.0, sm + L::RED, A.part2);
+}
+
+// u0 = r0 dinv; partials (r,u), (r,r) -> part.  b == 0: x = 0 (dgsem.py:510-511)
+template <int NC>
+__global__ void __launch_bounds__(256) k2p_u0(Cg2Args A) {
+  __shared__ double red[32 * 4];
+  const Op2DDev& op = A.op;
+  const long long nn = op.nn, o0 = own0(op), o1 = o0 + nown(op);
+  const long long nt = (long long)gridDim.x * blockDim.x, g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (A.sc->zero) {
+    for (long long f = o0 + g0; f < o1; f += nt)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) A.x[c * nn + f] = 0.0;
+    return;
+  }
+  double ru = 0.0, rr = 0.0;
+  for (long long f = o0 + g0; f < o1; f += nt) {
+    const double di = A.DINV[f];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double r = A.R[c * nn + f], u = r * di;
+      A.U[c * nn + f] = u;
+      ru = fma(r, u, ru);
+      rr = fma(r, r, rr);
+    }
+  }
+  blk_part3(ru, rr, 0.0, red, A.part);
+}
+
+// phase A: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = r dinv
+template <int NC>
+__global__ void __launch_bounds__(256) k2p_update(Cg2Args A) {
+  __shared__ double red[32 * 4];
+  if (A.sc->done) return;
+  const double alpha = A.sc->alpha, beta = A.sc->beta;
+  const Op2DDev& op = A.op;
+  const long long nn = op.nn, o0 = own0(op), o1 = o0 + nown(op);
+  const long long nt = (long long)gridDim.x * blockDim.x, g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool vec = ((nn | o0 | o1) & 1) == 0 && ((reinterpret_cast<uintptr_t>(A.x) & 15) == 0);
+  double ru = 0.0, rr = 0.0;
+  if (vec) {
+    const long long nh = nn >> 1;
+    for (long long h = (o0 >> 1) + g0; h < (o1 >> 1); h += nt) cg_update2<NC>(A, h, nh, alpha, beta, ru, rr);
+  } else {
+    for (long long f = o0 + g0; f < o1; f += nt) {
+      const double di = A.DINV[f];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const long long t = c * nn + f;
+        double r = A.R[t];
+        const double p = fma(beta, A.Pv[t], r * di);
+        const double s = fma(beta, A.S[t], A.W[t]);
+        A.Pv[t] = p;
+        A.S[t] = s;
+        A.x[t] = fma(alpha, p, A.x[t]);
+        r = fma(-alpha, s, r);
+        A.R[t] = r;
+        const double u = r * di;
+        A.U[t] = u;
+        ru = fma(r, u, ru);
+        rr = fma(r, r, rr);
+      }
+    }
+  }
+  blk_part3(ru, rr, 0.0, red, A.part);
+}
+
+// phase B: w = A u; partial (w,u) -> part2
+template <int P1, int NC>
+__global__ void __launch_bounds__(256, 2) k2p_matvec(Cg2Args A) {
+  extern __shared__ double sm[];
+  using L = CgSm<P1, NC>;
+  constexpr int EB = Blk<P1>::EB;
+  if (A.sc->done) return;
+  const Op2DDev& op = A.op;
+  double wu = 0.0;
+  if constexpr (P1 == 8) {
+    wpe_phase<NC>(op, sm, A.U, A.Cf, A.a, [&](long long g, double w0, double w1, double v0, double v1) {
+      *reinterpret_cast<double2*>(A.W + g) = make_double2(w0, w1);
+      wu = fma(w0, v0, wu);
+      wu = fma(w1, v1, wu);
+    });
+  } else {
+    const int tpr = (op.nex + EB - 1) / EB, ntiles = tpr * op.ney;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      cg_tile<P1, NC>(op, sm, tile, tpr, A.U, nullptr, A.Cf, A.a, [&](long long g, double wv, double u) {
+        A.W[g] = wv;
+        wu = fma(wv, u, wu);
+      });
+  }
+  blk_part3(wu, 0.0, 0.0, sm + L::RED, A.part2);
+}
+
+// fixed-order sum of the block partials of every local partition, then of the
+// partition totals in partition order.  mode 0: (b,b), #nonzero; mode 1:
+// (r,u), (w,u), (r,r).  One block.
+struct RedPArgs {
+  int nparts, G, mode;
+  const double* pa[MAXPART];
+  const double* pb[MAXPART];
+  double* out;
+};
+__global__ void __launch_bounds__(256) k2p_reduce(RedPArgs R) {
+  __shared__ double red[32 * 4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double tot[3] = {0.0, 0.0, 0.0};
+  for (int p = 0; p < R.nparts; ++p) {
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int b = threadIdx.x; b < R.G; b += blockDim.x) {
+      if (R.mode == 0) {
+        v0 += R.pb[p][b * 4];
+        v1 += R.pb[p][b * 4 + 1];
+      } else {
+        v0 += R.pa[p][b * 4];
+        v1 += R.pb[p][b * 4];
+        v2 += R.pa[p][b * 4 + 1];
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+      v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+    }
+    __syncthreads();
+    if (lane == 0) { red[wid * 4] = v0; red[wid * 4 + 1] = v1; red[wid * 4 + 2] = v2; }
+    __syncthreads();
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int ww = 0; ww < nw; ++ww) { t0 += red[ww * 4]; t1 += red[ww * 4 + 1]; t2 += red[ww * 4 + 2]; }
+    tot[0] += t0;
+    tot[1] += t1;
+    tot[2] += t2;
+  }
+  if (threadIdx.x == 0) { R.out[0] = tot[0]; R.out[1] = tot[1]; R.out[2] = tot[2]; }
+}
+
+// solve scalars from the allreduced sums (k2_cg's recurrences and stopping
+// rule); mode 0 after r0, 1 after w0, 2 after every iteration.  One thread.
+struct ScalPArgs {
+  int mode, maxit;
+  double rtol2;
+  const double* tot;
+  CgPScal* sc;
+  int* status;
+  int* log_it;
+  double* log_margin;
+  int log_cap;
+};
+__global__ void k2p_scalar(ScalPArgs S) {
+  CgPScal& s = *S.sc;
+  const double* t = S.tot;
+  auto log = [&](int it, double margin) {
+    const int idx = atomicAdd(&S.status[2], 1);
+    if (idx < S.log_cap) { S.log_it[idx] = it; S.log_margin[idx] = margin; }
+  };
+  if (S.mode == 0) {
+    s.thr = S.rtol2 * t[0];
+    s.zero = t[1] == 0.0 ? 1 : 0;
+    s.done = s.zero;
+    s.ok = 1;
+    s.k = 0;
+    s.rho = 0.0;
+    s.alpha = s.beta = 0.0;
+    if (s.zero) log(0, 0.0);
+    return;
+  }
+  if (s.done) return;
+  if (S.mode == 1) {
+    s.rho = t[2];
+    s.alpha = t[0] / t[1];
+    s.beta = 0.0;
+    s.rgam = 1.0 / t[0];
+    s.ralpha = 1.0 / s.alpha;
+  } else {
+    const double gn = t[0];
+    const double be = gn * s.rgam;
+    const double al = gn / (t[1] - be * (gn * s.ralpha));
+    s.rho = t[2];
+    s.alpha = al;
+    s.beta = be;
+    s.rgam = 1.0 / gn;
+    s.ralpha = 1.0 / al;
+    ++s.k;
+  }
+  if (!(s.rho > s.thr)) {
+    s.done = 1;
+    log(s.k, s.thr > 0.0 ? sqrt(s.rho / s.thr) : 0.0);
+  } else if (s.k >= S.maxit) {
+    s.done = 1;
+    s.ok = 0;
+    log(-1, s.thr > 0.0 ? sqrt(s.rho / s.thr) : 0.0);
+    atomicAdd(&S.status[1], 1);
+  }
+}
+
+// in-process face halo between the local partitions of one operator: ghost
+// row 0 of partition r <- last owned row of r-1, ghost row ney+1 <- first owned
+// row of r+1 (periodic in y), for nc fields and mcount node vectors
+struct HaloPArgs {
+  int nparts, nc, nex, nnod, mcount;
+  long long mstride;
+  double* base[MAXPART];
+  int ney[MAXPART];
+  long long nn[MAXPART];
+};
+__global__ void k2p_halo(HaloPArgs H) {
+  const long long row = (long long)H.nex * H.nnod;
+  const int y = blockIdx.y, side = y & 1, rc = y >> 1, c = rc % H.nc, r = rc / H.nc;
+  const int src = side == 0 ? (r + 1) % H.nparts : (r + H.nparts - 1) % H.nparts;
+  const long long so = side == 0 ? row : (long long)H.ney[src] * row;        // first / last owned row
+  const long long dof = side == 0 ? (long long)(H.ney[r] + 1) * row : 0;    // top / bottom ghost row
+  const long long mo = (long long)blockIdx.z * H.mstride;
+  const double* s = H.base[src] + mo + c * H.nn[src] + so;
+  double* d = H.base[r] + mo + c * H.nn[r] + dof;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < row; t += (long long)gridDim.x * blockDim.x)
+    d[t] = s[t];
 }
 
 // constant-bank copy of the reference-element matrices for one P1 (idempotent:
@@ -1704,6 +2049,125 @@ int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks) {
     *nblocks = (int)nb;
   });
   if (e != cudaSuccess) return c->cuda(e, "k2_cg occupancy");
+  return SISDC_OK;
+}
+
+
+// ------------------------------------------------ partitioned solve launchers
+size_t cg2p_ws_doubles(const Op2DDev& op, int G) { return 5 * (size_t)op.n + 2 * (size_t)op.nn + 8 * (size_t)G; }
+double* cg2p_U(const Op2DDev& op, double* ws) { return ws + 2 * op.n; }
+
+static Cg2Args cg2p_args(const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int G,
+                         const CgPScal* sc) {
+  Cg2Args A{};
+  A.op = op; A.coef = k; A.a = a; A.rhs = rhs; A.x = x;
+  double* p = ws;
+  A.R = p; p += op.n;
+  A.W = p; p += op.n;
+  A.U = p; p += op.n;
+  A.Pv = p; p += op.n;
+  A.S = p; p += op.n;
+  A.DINV = p; p += op.nn;
+  A.Cf = p; p += op.nn;
+  A.part = p; p += 4 * G;
+  A.part2 = p;
+  A.sc = sc;
+  return A;
+}
+
+template <int P1, int NC>
+static cudaError_t p2_phase(int phase, const Cg2Args& A, int G, cudaStream_t st) {
+  const size_t smem = smem_cg<P1, NC>();
+  switch (phase) {
+    case P2_INIT: k2p_init<P1><<<G, 256, 0, st>>>(A); break;
+    case P2_DINV: k2p_dinv<P1><<<G, 256, 0, st>>>(A); break;
+    case P2_RESID:
+      cudaFuncSetAttribute(k2p_resid<P1, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k2p_resid<P1, NC><<<G, Blk<P1>::NT, smem, st>>>(A);
+      break;
+    case P2_U0: k2p_u0<NC><<<G, 256, 0, st>>>(A); break;
+    case P2_UPDATE: k2p_update<NC><<<G, 256, 0, st>>>(A); break;
+    case P2_MATVEC:
+      cudaFuncSetAttribute(k2p_matvec<P1, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k2p_matvec<P1, NC><<<G, Blk<P1>::NT, smem, st>>>(A);
+      break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+int launch2p_phase(Ctx* c, int phase, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x,
+                   double* ws, int G, const CgPScal* sc) {
+  const Cg2Args A = cg2p_args(op, k, a, rhs, x, ws, G, sc);
+  cudaError_t e = cudaSuccess;
+  SISDC_P1_SWITCH(op.p1, {
+    e = op.nc == 4 ? p2_phase<P1, 4>(phase, A, G, c->stream) : p2_phase<P1, 1>(phase, A, G, c->stream);
+  });
+  ++c->launches;
+  if (e != cudaSuccess) return c->cuda(e, "k2p phase launch");
+  return SISDC_OK;
+}
+
+int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out) {
+  if (nparts < 1 || nparts > MAXPART) return c->fail(SISDC_ERR_ARG, "partition count");
+  RedPArgs R{};
+  R.nparts = nparts; R.G = G; R.mode = mode; R.out = out;
+  for (int p = 0; p < nparts; ++p) {
+    const double* base = ws[p] + 5 * ops[p].n + 2 * ops[p].nn;
+    R.pa[p] = base;
+    R.pb[p] = base + 4 * G;
+  }
+  k2p_reduce<<<1, 256, 0, c->stream>>>(R);
+  return c->after_launch("k2p_reduce");
+}
+
+int launch2p_scalar(Ctx* c, int mode, const double* tot, CgPScal* sc) {
+  ScalPArgs S{};
+  S.mode = mode; S.maxit = c->maxit; S.rtol2 = c->rtol * c->rtol; S.tot = tot; S.sc = sc;
+  S.status = c->d_status; S.log_it = c->d_log_it; S.log_margin = c->d_log_margin; S.log_cap = c->log_cap;
+  k2p_scalar<<<1, 1, 0, c->stream>>>(S);
+  return c->after_launch("k2p_scalar");
+}
+
+int launch2p_halo(Ctx* c, int nparts, const Op2DDev* ops, double* const* base, int nc, int mcount, long long mstride) {
+  if (nparts < 1 || nparts > MAXPART || mcount < 1) return c->fail(SISDC_ERR_ARG, "halo arguments");
+  HaloPArgs H{};
+  H.nparts = nparts; H.nc = nc; H.nex = ops[0].nex; H.nnod = ops[0].p1 * ops[0].p1; H.mcount = mcount;
+  H.mstride = mstride;
+  for (int p = 0; p < nparts; ++p) {
+    H.base[p] = base[p];
+    H.ney[p] = ops[p].ney;
+    H.nn[p] = ops[p].nn;
+  }
+  const long long row = (long long)H.nex * H.nnod;
+  const unsigned gx = (unsigned)((row + 255) / 256 < 64 ? (row + 255) / 256 : 64);
+  k2p_halo<<<dim3(gx, 2 * nc * nparts, mcount), 256, 0, c->stream>>>(H);
+  return c->after_launch("k2p_halo");
+}
+
+// blocks of the split-solve kernels: resident blocks of the matvec x SMs,
+// capped by the partition's work units
+int cg2p_blocks(Ctx* c, const Op2DDev& op, int* G) {
+  int per_sm = 0, sms = 0;
+  cudaError_t e = cudaSuccess;
+  SISDC_P1_SWITCH(op.p1, {
+    const size_t smem = smem_cg<P1, 4>() > smem_cg<P1, 1>() ? smem_cg<P1, 4>() : smem_cg<P1, 1>();
+    if (op.nc == 4) {
+      cudaFuncSetAttribute(k2p_matvec<P1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2p_matvec<P1, 4>, Blk<P1>::NT, smem_cg<P1, 4>());
+    } else {
+      cudaFuncSetAttribute(k2p_matvec<P1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2p_matvec<P1, 1>, Blk<P1>::NT, smem_cg<P1, 1>());
+    }
+    const long long units = P1 == 8 ? ((long long)op.nex * op.ney + 7) / 8
+                                    : (long long)((op.nex + Blk<P1>::EB - 1) / Blk<P1>::EB) * op.ney;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    long long nb = (long long)(per_sm > 0 ? per_sm : 1) * sms;
+    if (nb > units) nb = units;
+    if (nb < 1) nb = 1;
+    *G = (int)nb;
+  });
+  if (e != cudaSuccess) return c->cuda(e, "k2p occupancy");
   return SISDC_OK;
 }
 

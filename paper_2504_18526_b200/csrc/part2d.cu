@@ -1,0 +1,431 @@
+// Element-row partitioned 2-D operators (BASELINE configs 4-5 across GPUs).
+//
+// The global nex x ney mesh is cut into contiguous blocks of element rows, one
+// per rank.  A partition stores its rows with one ghost row on
+// each side, (ncomp, rows + 2, nex, P+1, P+1); the 2-D kernels read y-neighbours
+// of their boundary rows from the ghost rows (Op2DDev::row0 / ynb), so every
+// kernel is unchanged except for addressing.  Before a face-coupled operator
+// runs, the ghost rows of its face-coupled inputs are refreshed by the halo
+// exchange:
+//   * ranks on different GPUs: NCCL send/recv of the boundary rows (one
+//     contiguous nex*(P+1)^2 run per field and side) inside one NCCL group on
+//     the operator's stream, so it orders with the kernels and needs no host
+//     synchronisation;
+//   * partitions driven by one process (the single-GPU emulation of R ranks,
+//     and the 1-rank case): one copy kernel over all local partitions.
+// The implicit solve is the split Chronopoulos-Gear PCG (ops2d.cu k2p_*): per
+// iteration phase A, halo(u), phase B, a fixed-order reduction, one NCCL
+// allreduce of three doubles, and the scalar recurrences on the device.  The
+// host polls the convergence flag one batch behind the launches.
+// Elementwise work (defects, transfers, copies) runs over the concatenated
+// storage of the local partitions unchanged.
+#include <cstring>
+#include <dlfcn.h>
+#include <new>
+#include <nccl.h>
+#include "abi_internal.h"
+
+using namespace sisdc;
+
+// ------------------------------------------------------------------ NCCL
+// resolved at run time from the libnccl.so.2 already loaded by the host
+// process (torch), so the library itself links without NCCL
+namespace {
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*);
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*commDestroy)(ncclComm_t);
+  ncclResult_t (*groupStart)();
+  ncclResult_t (*groupEnd)();
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  const char* (*errorString)(ncclResult_t);
+  bool ok = false;
+};
+
+NcclApi* nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api.ok ? &api : nullptr;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return nullptr;
+#define SISDC_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name)); if (!api.field) return nullptr;
+  SISDC_SYM(getUniqueId, "ncclGetUniqueId");
+  SISDC_SYM(commInitRank, "ncclCommInitRank");
+  SISDC_SYM(commDestroy, "ncclCommDestroy");
+  SISDC_SYM(groupStart, "ncclGroupStart");
+  SISDC_SYM(groupEnd, "ncclGroupEnd");
+  SISDC_SYM(send, "ncclSend");
+  SISDC_SYM(recv, "ncclRecv");
+  SISDC_SYM(allReduce, "ncclAllReduce");
+  SISDC_SYM(errorString, "ncclGetErrorString");
+#undef SISDC_SYM
+  api.ok = true;
+  return &api;
+}
+}  // namespace
+
+struct sisdc_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+namespace {
+
+int nccl_fail(Ctx* c, ncclResult_t r, const char* what) {
+  NcclApi* api = nccl();
+  return c->fail(SISDC_ERR_CUDA, std::string(what) + ": " + (api ? api->errorString(r) : "NCCL unavailable"));
+}
+
+// rows of global rank q when ney rows are split over nranks
+void rank_rows(int ney, int nranks, int q, int* begin, int* count) {
+  const int base = ney / nranks, rem = ney % nranks;
+  *count = base + (q < rem ? 1 : 0);
+  *begin = q * base + (q < rem ? q : rem);
+}
+
+// refresh the ghost rows of mcount node vectors (stride mstride) of a state
+// (nc = ncomp, scalar = false) or of a scalar field (nc = 1, scalar = true)
+int halo(sisdc_op1d* op, const double* vec_c, int mcount, long long mstride, bool scalar) {
+  Ctx* c = C(op);
+  double* vec = const_cast<double*>(vec_c);   // ghost rows are scratch of every operator input
+  const int nc = scalar ? 1 : op->dev2.nc;
+  const int np = (int)op->parts.size();
+  if (!op->comm) {
+    Op2DDev ops[MAXPART];
+    double* base[MAXPART];
+    for (int p = 0; p < np; ++p) {
+      ops[p] = op->parts[p].dev;
+      base[p] = vec + (scalar ? op->parts[p].offc : op->parts[p].off);
+    }
+    return launch2p_halo(c, np, ops, base, nc, mcount, mstride);
+  }
+  NcclApi* api = nccl();
+  if (!api) return c->fail(SISDC_ERR_UNSUPPORTED, "NCCL is not available in this process");
+  const Part2D& P = op->parts[0];
+  const int R = op->comm->nranks, q = op->comm->rank;
+  const int prev = (q + R - 1) % R, next = (q + 1) % R;
+  const size_t row = (size_t)P.dev.nex * P.dev.p1 * P.dev.p1;
+  ncclResult_t r = api->groupStart();
+  for (int m = 0; m < mcount && r == ncclSuccess; ++m)
+    for (int f = 0; f < nc && r == ncclSuccess; ++f) {
+      double* b = vec + m * mstride + f * P.dev.nn;
+      // first owned row -> prev's top ghost; last owned row -> next's bottom ghost
+      r = api->send(b + row, row, ncclDouble, prev, op->comm->comm, c->stream);
+      if (r == ncclSuccess) r = api->send(b + (size_t)P.dev.ney * row, row, ncclDouble, next, op->comm->comm, c->stream);
+      if (r == ncclSuccess) r = api->recv(b + (size_t)(P.dev.ney + 1) * row, row, ncclDouble, next, op->comm->comm, c->stream);
+      if (r == ncclSuccess) r = api->recv(b, row, ncclDouble, prev, op->comm->comm, c->stream);
+    }
+  const ncclResult_t r2 = api->groupEnd();
+  if (r != ncclSuccess) return nccl_fail(c, r, "halo send/recv");
+  if (r2 != ncclSuccess) return nccl_fail(c, r2, "halo group");
+  ++c->launches;
+  return SISDC_OK;
+}
+
+int halo_coef(sisdc_op1d* op, const CoefDev& k) {
+  if (k.kind == SISDC_COEF_SI) return halo(op, k.ptr, 1, 0, false);
+  if (k.kind == SISDC_COEF_FIELD) return halo(op, k.ptr, 1, 0, true);
+  return SISDC_OK;
+}
+
+CoefDev coef_part(const CoefDev& k, const Part2D& P) {
+  CoefDev r = k;
+  if (k.kind == SISDC_COEF_SI) r.ptr = k.ptr + P.off;
+  if (k.kind == SISDC_COEF_FIELD) r.ptr = k.ptr + P.offc;
+  return r;
+}
+
+inline const double* at(const double* p, long long o) { return p ? p + o : nullptr; }
+inline double* at(double* p, long long o) { return p ? p + o : nullptr; }
+
+}  // namespace
+
+// ------------------------------------------------------ entry points
+int part2_conv(sisdc_op1d* op, const double* u, double* out) {
+  if (int rc = halo(op, u, 1, 0, false)) return rc;
+  for (const Part2D& P : op->parts)
+    if (int rc = launch2_conv(C(op), P.dev, u + P.off, out + P.off)) return rc;
+  return SISDC_OK;
+}
+
+int part2_sip(sisdc_op1d* op, CoefDev k, const double* u, double* out) {
+  if (int rc = halo(op, u, 1, 0, false)) return rc;
+  if (int rc = halo_coef(op, k)) return rc;
+  for (const Part2D& P : op->parts)
+    if (int rc = launch2_sip(C(op), P.dev, coef_part(k, P), u + P.off, out + P.off)) return rc;
+  return SISDC_OK;
+}
+
+int part2_coef_field(sisdc_op1d* op, CoefDev k, double* out) {
+  if (int rc = halo_coef(op, k)) return rc;
+  for (const Part2D& P : op->parts)
+    if (int rc = launch2_coef(C(op), P.dev, coef_part(k, P), out + P.offc)) return rc;
+  return SISDC_OK;
+}
+
+int part2_eval_nodes(sisdc_op1d* op, int mode, int scheme, int M, int m_first, int m_count, const double* u0,
+                     const double* u, const double* conv_prev, const double* dts, double* f, double* h1, double* h2) {
+  if (M > 16 || m_first < 0 || m_count < 1 || m_first + m_count > M) return C(op)->fail(SISDC_ERR_ARG, "bad node range");
+  const long long ns = op->n_total;
+  // u_m for the evaluated nodes and u_{m-1} (SI coefficient, conv of the previous node)
+  if (mode != 0) {
+    if (m_first == 0) {
+      if (int rc = halo(op, u0, 1, 0, false)) return rc;
+      if (int rc = halo(op, u, m_count, ns, false)) return rc;
+    } else if (int rc = halo(op, u + (m_first - 1) * ns, m_count + 1, ns, false)) {
+      return rc;
+    }
+  } else if (int rc = halo(op, u + m_first * ns, m_count, ns, false)) {
+    return rc;
+  }
+  for (const Part2D& P : op->parts)
+    if (int rc = launch2_node_eval(C(op), P.dev, mode, scheme, M, m_first, m_count, u0 + P.off, u + P.off,
+                                   at(conv_prev, P.off), dts, f + P.off, at(h1, P.off), at(h2, P.off)))
+      return rc;
+  return SISDC_OK;
+}
+
+int part2_stage(sisdc_op1d* op, const double* base, const double* conv_in, double dt_m, const double* f_old, int M,
+                const double* w_row, double dt, const double* g, const double* h, double* rhs, double* conv_out) {
+  if (int rc = halo(op, conv_in, 1, 0, false)) return rc;
+  for (const Part2D& P : op->parts)
+    if (int rc = launch2_stage(C(op), P.dev, base + P.off, conv_in + P.off, dt_m, at(f_old, P.off), M, w_row, dt,
+                               at(g, P.off), at(h, P.off), rhs + P.off, at(conv_out, P.off)))
+      return rc;
+  return SISDC_OK;
+}
+
+namespace {
+// sums of the local partitions (fixed order) -> allreduced sums at d_red + 4
+int reduce_all(sisdc_op1d* op, int mode) {
+  Ctx* c = C(op);
+  const int np = (int)op->parts.size();
+  Op2DDev ops[MAXPART];
+  double* ws[MAXPART];
+  for (int p = 0; p < np; ++p) {
+    ops[p] = op->parts[p].dev;
+    ws[p] = op->parts[p].ws;
+  }
+  if (!op->comm) return launch2p_reduce(c, np, ws, ops, op->parts[0].G, mode, op->d_red + 4);
+  if (int rc = launch2p_reduce(c, np, ws, ops, op->parts[0].G, mode, op->d_red)) return rc;
+  NcclApi* api = nccl();
+  if (!api) return c->fail(SISDC_ERR_UNSUPPORTED, "NCCL is not available in this process");
+  const ncclResult_t r = api->allReduce(op->d_red, op->d_red + 4, 3, ncclDouble, ncclSum, op->comm->comm, c->stream);
+  if (r != ncclSuccess) return nccl_fail(c, r, "CG allreduce");
+  ++c->launches;
+  return SISDC_OK;
+}
+
+int phase_all(sisdc_op1d* op, int phase, const CoefDev& k, double a, const double* rhs, double* x) {
+  for (const Part2D& P : op->parts)
+    if (int rc = launch2p_phase(C(op), phase, P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc))
+      return rc;
+  return SISDC_OK;
+}
+
+int halo_u(sisdc_op1d* op) {
+  Ctx* c = C(op);
+  const int np = (int)op->parts.size();
+  if (!op->comm) {
+    Op2DDev ops[MAXPART];
+    double* base[MAXPART];
+    for (int p = 0; p < np; ++p) {
+      ops[p] = op->parts[p].dev;
+      base[p] = cg2p_U(ops[p], op->parts[p].ws);
+    }
+    return launch2p_halo(c, np, ops, base, ops[0].nc, 1, 0);
+  }
+  // one local partition: its workspace u has the storage layout of a state
+  const Part2D& P = op->parts[0];
+  return halo(op, cg2p_U(P.dev, P.ws) - P.off, 1, 0, false);
+}
+
+int iterate(sisdc_op1d* op, const CoefDev& k, double a, const double* rhs, double* x) {
+  if (int rc = phase_all(op, P2_UPDATE, k, a, rhs, x)) return rc;
+  if (int rc = halo_u(op)) return rc;
+  if (int rc = phase_all(op, P2_MATVEC, k, a, rhs, x)) return rc;
+  if (int rc = reduce_all(op, 1)) return rc;
+  return launch2p_scalar(C(op), 2, op->d_red + 4, op->d_sc);
+}
+}  // namespace
+
+int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* x) {
+  Ctx* c = C(op);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cap);
+  if (cap != cudaStreamCaptureStatusNone)
+    return c->fail(SISDC_ERR_UNSUPPORTED, "a partitioned implicit solve polls its convergence flag and cannot be captured");
+  // coefficient source and rhs (x0 = rhs feeds the first matvec)
+  if (int rc = halo_coef(op, k)) return rc;
+  if (int rc = halo(op, rhs, 1, 0, false)) return rc;
+  if (int rc = phase_all(op, P2_INIT, k, a, rhs, x)) return rc;
+  if (int rc = phase_all(op, P2_DINV, k, a, rhs, x)) return rc;
+  if (int rc = phase_all(op, P2_RESID, k, a, rhs, x)) return rc;
+  if (int rc = reduce_all(op, 0)) return rc;
+  if (int rc = launch2p_scalar(c, 0, op->d_red + 4, op->d_sc)) return rc;
+  if (int rc = phase_all(op, P2_U0, k, a, rhs, x)) return rc;
+  if (int rc = halo_u(op)) return rc;
+  if (int rc = phase_all(op, P2_MATVEC, k, a, rhs, x)) return rc;
+  if (int rc = reduce_all(op, 1)) return rc;
+  if (int rc = launch2p_scalar(c, 1, op->d_red + 4, op->d_sc)) return rc;
+  // iterations in batches of B; the flag of batch j-1 is read while batch j runs
+  constexpr int B = 2;
+  const int max_batches = c->maxit / B + 3;
+  for (int j = 0; j < max_batches; ++j) {
+    for (int i = 0; i < B; ++i)
+      if (int rc = iterate(op, k, a, rhs, x)) return rc;
+    cudaError_t e = cudaMemcpyAsync(op->h_done + (j & 1), &op->d_sc->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(op->ev[j & 1], c->stream);
+    if (e != cudaSuccess) return c->cuda(e, "CG convergence flag");
+    if (j > 0) {
+      e = cudaEventSynchronize(op->ev[(j - 1) & 1]);
+      if (e != cudaSuccess) return c->cuda(e, "CG convergence flag");
+      if (op->h_done[(j - 1) & 1]) return SISDC_OK;
+    }
+  }
+  cudaError_t e = cudaEventSynchronize(op->ev[(max_batches - 1) & 1]);
+  if (e != cudaSuccess) return c->cuda(e, "CG convergence flag");
+  return SISDC_OK;   // the scalar kernel latched the failure (status[1]) at maxit
+}
+
+void part2_destroy(sisdc_op1d* op) {
+  for (Part2D& P : op->parts) cudaFree(P.ws);
+  op->parts.clear();
+  cudaFree(op->d_red);
+  cudaFree(op->d_sc);
+  if (op->h_done) cudaFreeHost(op->h_done);
+  for (cudaEvent_t& e : op->ev)
+    if (e) cudaEventDestroy(e);
+}
+
+// ------------------------------------------------------------------ ABI
+extern "C" {
+
+int sisdc_nccl_unique_id(unsigned char* id) {
+  if (!id) return SISDC_ERR_ARG;
+  NcclApi* api = nccl();
+  if (!api) return SISDC_ERR_UNSUPPORTED;
+  ncclUniqueId u;
+  if (api->getUniqueId(&u) != ncclSuccess) return SISDC_ERR_CUDA;
+  std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  return SISDC_OK;
+}
+
+int sisdc_comm_create(sisdc_ctx* x, const unsigned char* id, int nranks, int rank, sisdc_comm** out) {
+  if (!x || !id || !out || nranks < 1 || rank < 0 || rank >= nranks) return SISDC_ERR_ARG;
+  *out = nullptr;
+  NcclApi* api = nccl();
+  if (!api) return x->c.fail(SISDC_ERR_UNSUPPORTED, "NCCL is not available in this process");
+  sisdc_comm* cm = new (std::nothrow) sisdc_comm();
+  if (!cm) return SISDC_ERR_ARG;
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+  cudaSetDevice(x->c.device);
+  const ncclResult_t r = api->commInitRank(&cm->comm, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete cm;
+    return nccl_fail(&x->c, r, "ncclCommInitRank");
+  }
+  cm->nranks = nranks;
+  cm->rank = rank;
+  *out = cm;
+  return SISDC_OK;
+}
+
+void sisdc_comm_destroy(sisdc_comm* cm) {
+  if (!cm) return;
+  NcclApi* api = nccl();
+  if (api && cm->comm) api->commDestroy(cm->comm);
+  delete cm;
+}
+
+int sisdc_op2d_create_part(sisdc_ctx* x, const sisdc_op2d_desc* d, int nranks, int first_rank, int nlocal,
+                           sisdc_comm* comm, sisdc_op1d** out) {
+  if (!x || !d || !out) return SISDC_ERR_ARG;
+  *out = nullptr;
+  Ctx& c = x->c;
+  if (nranks < 1 || nlocal < 1 || nlocal > MAXPART || first_rank < 0 || first_rank + nlocal > nranks)
+    return c.fail(SISDC_ERR_ARG, "bad partition counts");
+  if (nranks > d->ney) return c.fail(SISDC_ERR_ARG, "more ranks than element rows");
+  if (comm && (comm->nranks != nranks || comm->rank != first_rank || nlocal != 1))
+    return c.fail(SISDC_ERR_ARG, "an NCCL communicator drives exactly one local partition (its own rank)");
+  if (!comm && nlocal != nranks) return c.fail(SISDC_ERR_ARG, "without a communicator every partition must be local");
+  sisdc_op1d* op = nullptr;
+  if (int rc = op2d_create_impl(x, d, false, &op)) return rc;
+  op->comm = comm;
+  op->nranks = nranks;
+  const Op2DDev& g = op->dev2;
+  const long long nnod = (long long)g.p1 * g.p1;
+  long long off = 0, offc = 0;
+  for (int l = 0; l < nlocal; ++l) {
+    Part2D P;
+    P.rank = first_rank + l;
+    int rb = 0, rcnt = 0;
+    rank_rows(d->ney, nranks, P.rank, &rb, &rcnt);
+    P.row_begin = rb;
+    P.dev = g;
+    P.dev.ney = rcnt;
+    P.dev.nys = rcnt + 2;
+    P.dev.row0 = 1;
+    P.dev.e0 = (long long)rb * g.nex;
+    P.dev.nn = (long long)P.dev.nys * g.nex * nnod;
+    P.dev.n = P.dev.nn * g.nc;
+    P.off = off;
+    P.offc = offc;
+    off += P.dev.n;
+    offc += P.dev.nn;
+    op->parts.push_back(P);
+  }
+  op->n_total = off;
+  op->nn_total = offc;
+  cudaError_t e = cudaSuccess;
+  for (Part2D& P : op->parts) {
+    P.dev.ns = off;
+    int rc = cg2p_blocks(&c, P.dev, &P.G);
+    if (rc) { sisdc_op1d_destroy(op); return rc; }
+  }
+  // one block count for all partitions (the reduction walks G slots of each)
+  int G = op->parts[0].G;
+  for (const Part2D& P : op->parts) G = P.G < G ? P.G : G;
+  for (Part2D& P : op->parts) {
+    P.G = G;
+    if (e == cudaSuccess) e = cudaMalloc(&P.ws, cg2p_ws_doubles(P.dev, G) * sizeof(double));
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&op->d_red, 8 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&op->d_sc, sizeof(CgPScal));
+  if (e == cudaSuccess) e = cudaMemset(op->d_sc, 0, sizeof(CgPScal));
+  if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&op->h_done), 2 * sizeof(int), cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&op->ev[0], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&op->ev[1], cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    const int rc = c.cuda(e, "partition workspace");
+    sisdc_op1d_destroy(op);
+    return rc;
+  }
+  *out = op;
+  return SISDC_OK;
+}
+
+int sisdc_op2d_part_layout(const sisdc_op1d* op, int cap, int* row_begin, int* row_count, int64_t* offset,
+                           int* nparts) {
+  if (!op || !nparts) return SISDC_ERR_ARG;
+  *nparts = (int)op->parts.size();
+  for (int p = 0; p < *nparts && p < cap; ++p) {
+    if (row_begin) row_begin[p] = op->parts[p].row_begin;
+    if (row_count) row_count[p] = op->parts[p].dev.ney;
+    if (offset) offset[p] = op->parts[p].off;
+  }
+  return SISDC_OK;
+}
+
+int sisdc_halo_exchange(sisdc_op1d* op, double* vec, int mcount, int64_t mstride, int scalar_field) {
+  if (!op || !vec || mcount < 1) return SISDC_ERR_ARG;
+  if (!op->parted()) return C(op)->fail(SISDC_ERR_ARG, "not a partitioned operator");
+  return halo(op, vec, mcount, mstride, scalar_field != 0);
+}
+
+}  // extern "C"

@@ -10,9 +10,15 @@
 namespace sisdc {
 
 struct Op2DDev {
-  int nex, ney, p1, nc;
-  long long nn;          // nodes per field = ney*nex*p1*p1
-  long long n;           // nc * nn
+  int nex, ney, p1, nc;  // ney: element rows this operator (partition) owns
+  int nys, row0;         // storage rows and the storage row of owned row 0:
+                         // (ney, 0) periodic single domain; (ney + 2, 1) for a
+                         // partition whose ghost rows 0 / ney+1 hold the
+                         // neighbour partitions' boundary rows (halo exchange)
+  long long e0;          // global index of the first owned element (diagnostics)
+  long long nn;          // field stride = nodes per field in storage = nys*nex*p1*p1
+  long long n;           // nc * nn (one state vector of this partition)
+  long long ns;          // node-array stride: u[m] = u + m * ns (n unless partitions are concatenated)
   int problem;
   double dx, dy, sx, sy, mux, muy;
   double gamma, nu, ax, ay;
@@ -22,13 +28,27 @@ struct Op2DDev {
 
 constexpr int NC_MAX = 4;
 
+// scalars of one partitioned (split) CG solve: every rank computes them from
+// the same allreduced sums, so they are bitwise identical across ranks
+struct CgPScal {
+  double alpha, beta, rgam, ralpha, rho, thr;
+  int k, done, ok, zero;
+};
+constexpr int MAXPART = 16;   // partitions one process can drive (in-process emulation)
+
 // element / node addressing -------------------------------------------------
+// ey is always a STORAGE row (owned rows are row0 .. row0+ney-1)
 __device__ __forceinline__ long long nidx(const Op2DDev& op, int c, int ey, int ex, int j, int i) {
-  return (((long long)c * op.ney + ey) * op.nex + ex) * (op.p1 * op.p1) + j * op.p1 + i;
+  return (((long long)c * op.nys + ey) * op.nex + ex) * (op.p1 * op.p1) + j * op.p1 + i;
 }
 __device__ __forceinline__ int wrapi(int a, int n) {
   a %= n;
   return a < 0 ? a + n : a;
+}
+// storage row of the y-neighbour (d = +1 above, -1 below) of storage row sy:
+// periodic wrap on a single domain, the ghost row on a partition
+__device__ __forceinline__ int ynb(const Op2DDev& op, int sy, int d) {
+  return op.row0 ? sy + d : wrapi(sy + d, op.ney);
 }
 
 // physics (Euler / NS isotropic, scalar advection, scalar Burgers along x) --

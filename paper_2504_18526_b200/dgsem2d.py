@@ -106,11 +106,70 @@ class Burgers2D:
 _KIND = {"euler2d": _lib.EULER2D, "advection2d": _lib.ADVECTION2D, "burgers2d": _lib.BURGERS2D}
 
 
+def rank_rows(ney: int, nranks: int, rank: int):
+    """(first row, row count) of ``rank`` when ``ney`` element rows are split
+    into contiguous blocks (the split ``sisdc_op2d_create_part`` uses)."""
+    if not 1 <= nranks <= ney:
+        raise ValueError(f"cannot split {ney} element rows over {nranks} ranks")
+    if not 0 <= rank < nranks:
+        raise ValueError("rank out of range")
+    base, rem = divmod(ney, nranks)
+    return rank * base + min(rank, rem), base + (1 if rank < rem else 0)
+
+
+@dataclass(frozen=True)
+class Partition:
+    """Element-row partition of a 2-D mesh.
+
+    ``comm=None``: all ``nranks`` partitions live in this process on one GPU
+    (halo exchange and CG allreduce are device copies / fixed-order sums).
+    With an :class:`NcclComm` the process owns only partition ``comm.rank``;
+    the halo and the CG dot products go through NCCL."""
+    nranks: int
+    comm: object = None
+
+    @property
+    def first_rank(self):
+        return 0 if self.comm is None else self.comm.rank
+
+    @property
+    def nlocal(self):
+        return self.nranks if self.comm is None else 1
+
+
+class NcclComm:
+    """NCCL communicator of the partition layer, bootstrapped through
+    torch.distributed (rank 0 makes the unique id, every rank receives it)."""
+
+    def __init__(self, rank: int, nranks: int, device: int = 0, group=None):
+        import torch.distributed as dist
+        self.rt = get_runtime(device)
+        self.lib = self.rt.lib
+        self.rank, self.nranks = rank, nranks
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            self.rt.check(self.lib.sisdc_nccl_unique_id(uid), "nccl_unique_id")
+        obj = [bytes(uid.raw)]
+        if nranks > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        h = C.c_void_p()
+        self.rt.check(self.lib.sisdc_comm_create(self.rt.h, obj[0], nranks, rank, C.byref(h)), "comm_create")
+        self.h = h
+
+    def __del__(self):
+        try:
+            self.lib.sisdc_comm_destroy(self.h)
+        except Exception:
+            pass
+
+
 class DGOperator2D:
     is2d = True
 
-    def __init__(self, mesh: Mesh2D, problem, penalty_const: float = 2.0, device: int = 0, eager_checks: bool = True):
+    def __init__(self, mesh: Mesh2D, problem, penalty_const: float = 2.0, device: int = 0, eager_checks: bool = True,
+                 partition: Partition = None):
         self.mesh = mesh
+        self.partition = partition
         self.problem = problem
         self.av = None
         self.ncomp = problem.ncomp
@@ -125,7 +184,21 @@ class DGOperator2D:
                           float(getattr(problem, "ax", 0.0)), float(getattr(problem, "ay", 0.0)), float(penalty_const))
         self._desc = d
         h = C.c_void_p()
-        self.rt.check(self.lib.sisdc_op2d_create(self.rt.h, C.byref(d), C.byref(h)), "op2d_create")
+        self.parts = None
+        if partition is None:
+            self.rt.check(self.lib.sisdc_op2d_create(self.rt.h, C.byref(d), C.byref(h)), "op2d_create")
+            self.slab_rows = mesh.ney
+        else:
+            self._comm = partition.comm   # keeps the communicator alive with the operator
+            self.rt.check(self.lib.sisdc_op2d_create_part(
+                self.rt.h, C.byref(d), partition.nranks, partition.first_rank, partition.nlocal,
+                None if partition.comm is None else partition.comm.h, C.byref(h)), "op2d_create_part")
+            k = partition.nlocal
+            rb, rc, off, npart = (C.c_int * k)(), (C.c_int * k)(), (C.c_int64 * k)(), C.c_int()
+            self.rt.check(self.lib.sisdc_op2d_part_layout(h, k, rb, rc, off, C.byref(npart)), "part_layout")
+            self.parts = [(rb[i], rc[i], off[i]) for i in range(npart.value)]
+            self.slab_rows = sum(r + 2 for _, r, _ in self.parts)
+            self.ndof = self.ncomp * self.slab_rows * mesh.nex * self.p1 * self.p1
         self.h = h
         self._scratch = None
         self.nu_art = None
@@ -137,7 +210,46 @@ class DGOperator2D:
             pass
 
     def as_nodes(self, u):
+        if self.parts is not None:
+            raise ValueError("a partitioned state has ghost rows: use owned_views() / gather()")
         return self.rt.to_device(u).reshape(self.ncomp, self.mesh.ney, self.mesh.nex, self.p1, self.p1)
+
+    # ------------------------------------------------ partitioned layout
+    def _part_view(self, vec, i):
+        _, rows, off = self.parts[i]
+        n = self.ncomp * (rows + 2) * self.mesh.nex * self.p1 * self.p1
+        return vec[off:off + n].view(self.ncomp, rows + 2, self.mesh.nex, self.p1, self.p1)
+
+    def owned_views(self, vec):
+        """[(first global row, (ncomp, rows, nex, P+1, P+1) view of the owned rows)]"""
+        return [(rb, self._part_view(vec, i)[:, 1:-1]) for i, (rb, _, _) in enumerate(self.parts)]
+
+    def scatter(self, u_global):
+        """Global state (ncomp, ney, nex, P+1, P+1) -> this process's storage
+        vector (ghost rows zero; the operators exchange them before use)."""
+        if self.parts is None:
+            return self.rt.to_device(u_global).reshape(-1).clone()
+        g = np.asarray(u_global.cpu() if hasattr(u_global, "cpu") else u_global, dtype=np.float64)
+        g = g.reshape(self.ncomp, self.mesh.ney, self.mesh.nex, self.p1, self.p1)
+        out = self.rt.zeros(self.ndof)
+        for rb, v in self.owned_views(out):
+            v.copy_(self.rt.to_device(np.ascontiguousarray(g[:, rb:rb + v.shape[1]])))
+        return out
+
+    def gather(self, vec):
+        """Owned rows of this process's partitions -> numpy (ncomp, ney, nex,
+        P+1, P+1), rows of other processes' partitions left NaN."""
+        if self.parts is None:
+            return self.as_nodes(vec).cpu().numpy()
+        out = np.full((self.ncomp, self.mesh.ney, self.mesh.nex, self.p1, self.p1), np.nan)
+        for rb, v in self.owned_views(vec):
+            out[:, rb:rb + v.shape[1]] = v.cpu().numpy()
+        return out
+
+    def halo_exchange(self, vec, mcount: int = 1, mstride: int = 0, scalar_field: bool = False):
+        self.rt.bind_stream()
+        self.rt.check(self.lib.sisdc_halo_exchange(self.h, vec.data_ptr(), int(mcount), int(mstride),
+                                                   1 if scalar_field else 0), "halo_exchange")
 
     def scratch(self):
         if self._scratch is None:
@@ -196,7 +308,7 @@ class DGOperator2D:
     def coefficient_field(self, coeff):
         keep = []
         c = self._coef(coeff, keep)
-        out = self.rt.empty(self.mesh.n_elem * self.p1 * self.p1)
+        out = self.rt.empty(self.mesh.nex * self.slab_rows * self.p1 * self.p1)
         self.rt.bind_stream()
         self.rt.check(self.lib.sisdc_coef_field(self.h, c, out.data_ptr()), "coef_field")
         return out

@@ -316,7 +316,9 @@ def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes:
     for lo, hi in zip(range(len(ops) - 1), range(1, len(ops))):
         pair = build_temporal_transfer(rules[lo], rules[hi])
         if getattr(ops[lo], "is2d", False):
-            spatial = build_spatial_p_transfer_2d(degrees[lo], degrees[hi], ops[lo].mesh.nex, ops[lo].mesh.ney,
+            # element slabs in storage order (a partitioned operator's ghost rows included)
+            spatial = build_spatial_p_transfer_2d(degrees[lo], degrees[hi], ops[lo].mesh.nex,
+                                                  getattr(ops[lo], "slab_rows", ops[lo].mesh.ney),
                                                   ops[lo].ncomp, restriction=restriction or "mass")
         else:
             spatial = build_spatial_p_transfer(degrees[lo], degrees[hi], ops[lo].mesh.n_elem, ops[lo].ncomp,
