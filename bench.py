@@ -49,7 +49,12 @@ def parse():
     ap.add_argument("--cluster-ctas", type=int, default=0)
     ap.add_argument("--cycles", type=int, default=None, help="override the V-cycles per step")
     ap.add_argument("--no-2d", dest="also_2d", action="store_false",
-                    help="skip the secondary 2-D (cfg4) line that rides along the 1-D headline")
+                    help="skip the secondary 2-D lines (cfg4, cfg5) that ride along the 1-D headline")
+    ap.add_argument("--no-cfg5", dest="also_cfg5", action="store_false",
+                    help="skip the secondary cfg5 (1024^2, 268M DOF) line")
+    ap.add_argument("--partition", type=int, default=0,
+                    help="2-D workloads on one GPU: run the element-row partitioned path with this many "
+                         "in-process partitions (emulated ranks); --partition -1 = one NCCL rank")
     return ap.parse_args()
 
 
@@ -244,7 +249,7 @@ def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True):
         from paper_2504_18526_b200 import dgsem2d
 
         def make_op(P):
-            mesh = dgsem2d.Mesh2D(0.0, w.length, 0.0, w.length, w.nex, w.ney, P)
+            mesh = dgsem2d.Mesh2D(0.0, w.length, 0.0, w.ly, w.nex, w.ney, P)
             return dgsem2d.DGOperator2D(mesh, dgsem2d.CompressibleEuler2D(w.gamma, w.nu), device=local)
 
         hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
@@ -317,13 +322,13 @@ def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True):
         t_e2e = float(tt.item())
     e2e_val = U * ke * world / t_e2e
     # dominant kernel roofline (measured live)
-    t_cg, k_cg, bytes_cg = cg_roofline(hier, rt, torch, dt)
+    t_cg, k_cg, bytes_cg = cg_roofline(hier, rt, torch, dt, reps=64 if U < 2e9 else 4)
     peak, peak_kind = measured_hbm_peak()
     achieved = bytes_cg / t_cg / 1e9
     if is2d:
         kern = "k2_cg<8,4> (grid-persistent cooperative Jacobi-PCG; phase B warp-per-element on fp64 mma.m8n8k4)"
         note = ("8N[(3+V)+k(10+V)] bytes per solve (SURVEY 8d), V=1/4: one scalar coefficient per node shared by "
-                "the 4 fields; fine level 134 MB per vector, HBM resident")
+                f"the 4 fields; fine level {8 * hier.fine.ctx.ndof / 1e6:.0f} MB per vector, HBM resident")
         data = f"synthetic seeded IC (SURVEY 8d): {w.name}, no dataset"
     else:
         kern = "k_cg1d (cluster-resident Jacobi-PCG, one launch per implicit solve)"
@@ -360,6 +365,143 @@ def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True):
     return res
 
 
+def measure_part(w, args, torch, rt, rank, world, local, steps, warmup, emulate=0):
+    """Element-row partitioned 2-D path: with world > 1 every rank
+    owns one block of element rows (NCCL face halo + one NCCL allreduce per CG
+    iteration); with world == 1, `emulate` in-process partitions on one GPU
+    (emulate == -1: one rank through NCCL).  Strong scaling: value = the whole
+    problem's DOF-sweeps per step x steps / max-over-ranks time.  Eager slabs
+    (the partitioned solve polls its convergence flag, so it is not captured)."""
+    import dataclasses as _dc
+    from paper_2504_18526_b200 import dgsem, dgsem2d, mlsdc
+    if world > 1:
+        part = dgsem2d.Partition(world, dgsem2d.NcclComm(rank, world, local))
+        how = f"element rows block-partitioned over {world} GPUs, NCCL face halo + 1 allreduce per CG iteration"
+    elif emulate == -1:
+        part = dgsem2d.Partition(1, dgsem2d.NcclComm(0, 1, local))
+        how = "one NCCL rank (halo send/recv to itself, allreduce) on one GPU"
+    else:
+        part = dgsem2d.Partition(emulate)
+        how = f"{emulate} element-row partitions emulated in one process on one GPU (device-copy halo)"
+
+    def make_op(P):
+        mesh = dgsem2d.Mesh2D(0.0, w.length, 0.0, w.ly, w.nex, w.ney, P)
+        return dgsem2d.DGOperator2D(mesh, dgsem2d.CompressibleEuler2D(w.gamma, w.nu), device=local, partition=part)
+
+    hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+    fine = hier.fine.ctx
+    X, Y = fine.mesh.nodes_xy
+    u0g = w.initial_state(X, Y)
+    dt = w.time_step(u0g, dgsem.compute_delta(w.p_fine))
+    u = fine.scatter(u0g)
+    del X, Y, u0g
+    U, U_fine = w.dof_sweeps_per_step()
+    for o in (fine, hier.levels[0].ctx):
+        o.eager_checks = False
+
+    def slab():
+        sol = mlsdc.run_mlsdc(hier, u, 0.0, dt, w.n_cycles, strategy="fmg")
+        rt.copy(u, sol.u[-1])
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=rt.device)
+    rt.reset_status()
+    for _ in range(warmup):
+        slab()
+    torch.cuda.synchronize()
+    n_log0 = rt.status()[2]
+    l0 = rt.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for e0, e1 in evs:
+            flush.fill_(1.0)
+            e0.record()
+            slab()
+            e1.record()
+        torch.cuda.synchronize()
+    launches = rt.launch_count() - l0
+    t_steps = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
+    rt.raise_on_failure()
+    its = rt.cg_log()[0][n_log0:]
+
+    def tmax(t):
+        if world == 1:
+            return t
+        tt = torch.tensor([t], device=rt.device, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        return float(tt.item())
+    t_max = tmax(t_steps)
+    # e2e: this rank's storage vector from / to pinned host memory every step
+    h_in = torch.empty(fine.ndof, dtype=torch.float64, pin_memory=True)
+    h_in.copy_(u.cpu())
+    h_out = torch.empty_like(h_in)
+    ke = max(3, min(steps, 5))
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(ke):
+        u.copy_(h_in, non_blocking=True)
+        slab()
+        h_out.copy_(u, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    t_e2e = tmax(e0.elapsed_time(e1) * 1e-3)
+    # the split PCG on the fine level: one solve, CUDA events, bytes of this rank
+    from paper_2504_18526_b200.dgsem import SICoefficient
+    sol = hier.fine.sol
+    dtm = dt * float(hier.fine.rule.tau[2] - hier.fine.rule.tau[1])
+    coef = SICoefficient(sol.u[1].clone(), dtm)
+    rhs, x = sol.u[2].clone(), rt.empty(fine.ndof)
+    fine.implicit_solve(coef, dtm, rhs, out=x)
+    torch.cuda.synchronize()
+    n1 = rt.status()[2]
+    reps = 3
+    e0.record()
+    for _ in range(reps):
+        fine.implicit_solve(coef, dtm, rhs, out=x)
+    e1.record()
+    torch.cuda.synchronize()
+    t_cg = e0.elapsed_time(e1) * 1e-3 / reps
+    k_cg = float(np.mean(rt.cg_log()[0][n1:n1 + reps]))
+    n_own = fine.ncomp * sum(r for _, r, _ in fine.parts) * w.nex * (w.p_fine + 1) ** 2
+    bytes_cg = 8.0 * n_own * ((3 + 0.25) + k_cg * (10 + 0.25))
+    peak, peak_kind = measured_hbm_peak()
+    achieved = bytes_cg / t_cg / 1e9
+    res = {
+        "metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64",
+        "value": U * steps / t_max, "ms_per_step": 1e3 * t_max / steps, "steps": steps, "warmup": warmup,
+        "n_gpus": world, "scaling": "strong",
+        "data": f"synthetic seeded IC (SURVEY 8d): {w.name}, no dataset",
+        "config": {
+            "workload": w.name, "n_elem": w.nex * w.ney, "degrees": [w.p_coarse, w.p_fine],
+            "nodes": [w.m_coarse, w.m_fine], "dt": dt,
+            "schedule": f"SI(2) incremental, radau_right, fmg start, {w.n_cycles} V-cycles + closing fine sweep; "
+                        "FAS residual restricted mass-consistently (DESIGN.md)",
+            "dof_sweeps_per_step": U, "fine_dof_sweeps_per_s": U_fine * steps / t_max,
+            "cg_solves_per_step": len(its) / steps, "cg_mean_iterations": float(np.mean(its)) if len(its) else None,
+            "cg_rtol": 1e-14, "l2": "256 MiB buffer written between timed steps, outside the CUDA events",
+            "parallelism": how, "rows_per_rank": [r for _, r, _ in fine.parts] if world == 1 else None,
+            "timing": "CUDA events around each eager slab, summed; max over ranks",
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "split PCG of one fine solve (k2p_update + halo + k2p_matvec + reduce/allreduce "
+                               "per iteration), this rank's partition",
+                     "kernel_us": t_cg * 1e6, "kernel_mean_iterations": k_cg, "algorithmic_bytes_per_launch": bytes_cg,
+                     "note": "8N[(3+V)+k(10+V)] bytes per solve over this rank's owned DOFs, V=1/4"},
+        "clocks": clk.summary(),
+        "e2e": {"value": U * ke / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * fine.ndof,
+                "d2h_bytes_per_step": 8 * fine.ndof},
+        "gpu_launches": int(launches),
+    }
+    del hier, flush, u, h_in, h_out, sol, coef, rhs, x
+    return res
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -375,6 +517,13 @@ def run_ours(args):
         w = dataclasses.replace(w, n_cycles=args.cycles)
     rt = get_runtime(local)
     rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=args.cluster_ctas)
+    if hasattr(w, "nex") and (world > 1 or args.partition):
+        r = measure_part(w, args, torch, rt, rank, world, local, args.steps, args.warmup, emulate=args.partition)
+        if rank == 0:
+            print(json.dumps({k: v for k, v in r.items()}), flush=True)
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
     r = measure(w, args, torch, rt, rank, world, local, args.steps, args.warmup)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not hasattr(w, "nex"):
@@ -383,14 +532,29 @@ def run_ours(args):
                "sample": f"{args.cpu_sample_steps} SI-MLSDC steps of {w.name} from the seeded IC, "
                          f"{tstep * 1e3:.1f} ms/step: oracle restatement of the reference algorithm "
                          "(SuperLU + defect iteration), numpy/scipy, 1 thread"}
-    secondary = None
+    secondary = {}
     if world == 1 and args.also_2d and not hasattr(w, "nex"):
         torch.cuda.empty_cache()
         w2 = WORKLOADS["cfg4"]
         r2 = measure(w2, args, torch, rt, rank, world, local, 3, 3)
-        secondary = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64", **r2,
-                     "note": "BASELINE configs[3] (2-D Navier-Stokes shear layer 256^2, P 7/3, M 5/3), same "
-                             "contract as the main line; reported beside it because the headline config is 1-D"}
+        secondary["cfg4"] = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64", **r2,
+                             "note": "BASELINE configs[3] (2-D Navier-Stokes shear layer 256^2, P 7/3, M 5/3), "
+                                     "same contract as the main line; reported beside it because the headline "
+                                     "config is 1-D"}
+    if args.also_2d and args.also_cfg5 and not hasattr(w, "nex"):
+        # BASELINE configs[4], the scaling config: single domain on 1 GPU (CUDA graph), element rows
+        # partitioned over the ranks (NCCL halo + CG allreduce) on N GPUs -- strong scaling
+        torch.cuda.empty_cache()
+        w5 = WORKLOADS["cfg5"]
+        if world == 1:
+            r5 = measure(w5, args, torch, rt, rank, world, local, 3, 3)
+            r5 = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64", "n_gpus": 1,
+                  "scaling": "strong", **r5}
+        else:
+            r5 = measure_part(w5, args, torch, rt, rank, world, local, 3, 3)
+        r5["note"] = ("BASELINE configs[4] (1024^2 elements, P 7/3, 268M fine DOF): the multi-GPU scaling config; "
+                      "value is the whole problem's DOF-sweeps/s (strong scaling over n_gpus)")
+        secondary["cfg5"] = r5
     if rank == 0:
         out = {
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -401,8 +565,8 @@ def run_ours(args):
             "roofline": r["roofline"], "cpu_baseline": cpu, "clocks": r["clocks"], "e2e": r["e2e"],
             "gpu_launches": r["gpu_launches"],
         }
-        if secondary is not None:
-            out["secondary"] = {"cfg4": secondary}
+        if secondary:
+            out["secondary"] = secondary
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -122,10 +122,15 @@ class Workload2D:
     cfl: float = 1.0
     n_cycles: int = 3
     n_steps: int = 20
+    length_y: float = None   # None: square domain; set for one rank's share of a mesh (tools/scaling_estimate.py)
 
     @property
     def ncomp(self):
         return 4
+
+    @property
+    def ly(self):
+        return self.length if self.length_y is None else self.length_y
 
     def dof(self):
         nf = 4 * self.nex * self.ney * (self.p_fine + 1) ** 2

@@ -113,7 +113,9 @@ int halo(sisdc_op1d* op, const double* vec_c, int mcount, long long mstride, boo
   for (int m = 0; m < mcount && r == ncclSuccess; ++m)
     for (int f = 0; f < nc && r == ncclSuccess; ++f) {
       double* b = vec + m * mstride + f * P.dev.nn;
-      // first owned row -> prev's top ghost; last owned row -> next's bottom ghost
+      // first owned row -> prev's top ghost; last owned row -> next's bottom ghost.  Issue order =
+      // dgsem2d.halo_schedule (NCCL pairs the k-th send to a peer with its k-th receive from us;
+      // correct for 1 rank (self), 2 ranks (prev == next) and more), tested over gloo on CPU
       r = api->send(b + row, row, ncclDouble, prev, op->comm->comm, c->stream);
       if (r == ncclSuccess) r = api->send(b + (size_t)P.dev.ney * row, row, ncclDouble, next, op->comm->comm, c->stream);
       if (r == ncclSuccess) r = api->recv(b + (size_t)(P.dev.ney + 1) * row, row, ncclDouble, next, op->comm->comm, c->stream);

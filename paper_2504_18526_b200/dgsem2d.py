@@ -117,6 +117,63 @@ def rank_rows(ney: int, nranks: int, rank: int):
     return rank * base + min(rank, rem), base + (1 if rank < rem else 0)
 
 
+def part_layout(ney: int, nex: int, p1: int, ncomp: int, nranks: int, ranks):
+    """[(first row, rows, offset)] of the partitions of ``ranks`` in the
+    concatenated storage vector (ghost row on either side of each partition;
+    mirrors ``sisdc_op2d_create_part``)."""
+    out, off = [], 0
+    for q in ranks:
+        rb, rc = rank_rows(ney, nranks, q)
+        out.append((rb, rc, off))
+        off += ncomp * (rc + 2) * nex * p1 * p1
+    return out
+
+
+def to_storage(g, parts, out):
+    """Owned rows of a global state g (ncomp, ney, nex, p1, p1) into the storage
+    vector ``out`` (numpy or torch, 1-D) of ``parts``; ghost rows untouched."""
+    nc, _, nex, p1, _ = g.shape
+    for rb, rc, off in parts:
+        v = out[off:off + nc * (rc + 2) * nex * p1 * p1].reshape(nc, rc + 2, nex, p1, p1)
+        blk = g[:, rb:rb + rc]
+        if hasattr(v, "copy_"):
+            import torch
+            v[:, 1:-1].copy_(torch.as_tensor(np.ascontiguousarray(blk)))
+        else:
+            v[:, 1:-1] = blk
+    return out
+
+
+def from_storage(vec, parts, shape):
+    """Owned rows of the storage vector ``vec`` (numpy, 1-D) -> global array of
+    ``shape`` (ncomp, ney, nex, p1, p1), rows of other ranks NaN."""
+    nc, _, nex, p1, _ = shape
+    out = np.full(shape, np.nan)
+    for rb, rc, off in parts:
+        out[:, rb:rb + rc] = vec[off:off + nc * (rc + 2) * nex * p1 * p1].reshape(nc, rc + 2, nex, p1, p1)[:, 1:-1]
+    return out
+
+
+def halo_schedule(rank: int, nranks: int):
+    """Issue order of the NCCL halo exchange of one field (part2d.cu ``halo``):
+    ("send", peer, storage row) / ("recv", peer, storage row) with rows counted
+    in the partition's storage (0 and rows+1 are the ghost rows).  NCCL pairs
+    the k-th send to a peer with that peer's k-th receive from us, so this
+    order is correct for 1 (self), 2 (prev == next) and more ranks."""
+    prev, next_ = (rank - 1) % nranks, (rank + 1) % nranks
+    return [("send", prev, "first"), ("send", next_, "last"), ("recv", next_, "top_ghost"),
+            ("recv", prev, "bottom_ghost")]
+
+
+def bootstrap_id(rank: int, nranks: int, make_id, group=None) -> bytes:
+    """Rank 0 makes the 128-byte NCCL unique id, every rank receives it."""
+    obj = [make_id() if rank == 0 else None]
+    if nranks > 1:
+        import torch.distributed as dist
+        dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
 @dataclass(frozen=True)
 class Partition:
     """Element-row partition of a 2-D mesh.
@@ -142,18 +199,17 @@ class NcclComm:
     torch.distributed (rank 0 makes the unique id, every rank receives it)."""
 
     def __init__(self, rank: int, nranks: int, device: int = 0, group=None):
-        import torch.distributed as dist
         self.rt = get_runtime(device)
         self.lib = self.rt.lib
         self.rank, self.nranks = rank, nranks
-        uid = C.create_string_buffer(128)
-        if rank == 0:
+        def make_id():
+            uid = C.create_string_buffer(128)
             self.rt.check(self.lib.sisdc_nccl_unique_id(uid), "nccl_unique_id")
-        obj = [bytes(uid.raw)]
-        if nranks > 1:
-            dist.broadcast_object_list(obj, src=0, group=group)
+            return bytes(uid.raw)
+
+        uid = bootstrap_id(rank, nranks, make_id, group)
         h = C.c_void_p()
-        self.rt.check(self.lib.sisdc_comm_create(self.rt.h, obj[0], nranks, rank, C.byref(h)), "comm_create")
+        self.rt.check(self.lib.sisdc_comm_create(self.rt.h, uid, nranks, rank, C.byref(h)), "comm_create")
         self.h = h
 
     def __del__(self):
@@ -197,6 +253,9 @@ class DGOperator2D:
             rb, rc, off, npart = (C.c_int * k)(), (C.c_int * k)(), (C.c_int64 * k)(), C.c_int()
             self.rt.check(self.lib.sisdc_op2d_part_layout(h, k, rb, rc, off, C.byref(npart)), "part_layout")
             self.parts = [(rb[i], rc[i], off[i]) for i in range(npart.value)]
+            ranks = range(partition.first_rank, partition.first_rank + partition.nlocal)
+            if self.parts != part_layout(mesh.ney, mesh.nex, self.p1, self.ncomp, partition.nranks, ranks):
+                raise RuntimeError("library partition layout disagrees with part_layout()")
             self.slab_rows = sum(r + 2 for _, r, _ in self.parts)
             self.ndof = self.ncomp * self.slab_rows * mesh.nex * self.p1 * self.p1
         self.h = h
@@ -231,20 +290,15 @@ class DGOperator2D:
             return self.rt.to_device(u_global).reshape(-1).clone()
         g = np.asarray(u_global.cpu() if hasattr(u_global, "cpu") else u_global, dtype=np.float64)
         g = g.reshape(self.ncomp, self.mesh.ney, self.mesh.nex, self.p1, self.p1)
-        out = self.rt.zeros(self.ndof)
-        for rb, v in self.owned_views(out):
-            v.copy_(self.rt.to_device(np.ascontiguousarray(g[:, rb:rb + v.shape[1]])))
-        return out
+        return to_storage(g, self.parts, self.rt.zeros(self.ndof))
 
     def gather(self, vec):
         """Owned rows of this process's partitions -> numpy (ncomp, ney, nex,
         P+1, P+1), rows of other processes' partitions left NaN."""
         if self.parts is None:
             return self.as_nodes(vec).cpu().numpy()
-        out = np.full((self.ncomp, self.mesh.ney, self.mesh.nex, self.p1, self.p1), np.nan)
-        for rb, v in self.owned_views(vec):
-            out[:, rb:rb + v.shape[1]] = v.cpu().numpy()
-        return out
+        return from_storage(vec.detach().cpu().numpy(), self.parts,
+                            (self.ncomp, self.mesh.ney, self.mesh.nex, self.p1, self.p1))
 
     def halo_exchange(self, vec, mcount: int = 1, mstride: int = 0, scalar_field: bool = False):
         self.rt.bind_stream()
