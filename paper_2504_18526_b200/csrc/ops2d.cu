@@ -535,7 +535,8 @@ struct Cg2Args {
   int maxit;
   double* R;
   double* W;
-  double* U;      // u = r dinv, written by phase A
+  double* U;      // u = r dinv, written by phase A (split solve: this iteration's u)
+  double* U2;     // the other u buffer (split solve: the previous iteration's u, for p / x)
   double* Pv;
   double* S;
   double* DINV;   // per in-field node
@@ -551,6 +552,7 @@ struct Cg2Args {
   // partitioned (split) solve only: phase-B partial slots and the solve scalars
   double* part2;       // [gridDim][4]
   const struct CgPScal* sc;
+  int px;              // split matvec: also advance p, x (p = u_prev + beta p, x += alpha p)
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -828,6 +830,77 @@ __device__ __forceinline__ void cg_update2(const Cg2Args& A, long long h, long l
   }
 }
 
+// phase A' (p / x deferred to phase B): s = w + beta s, r -= alpha s,
+// u_new = r dinv over in-field pairs; partials (r,u), (r,r).  p and x only feed
+// the final x, so their update p = u_prev + beta p, x += alpha p (the same
+// operations as cg_update2, u_prev = r_old dinv bitwise) rides in the
+// issue-bound phase B, which has HBM bandwidth to spare; u is double-buffered.
+template <int NC>
+__device__ __forceinline__ void cg_update2s(const Cg2Args& A, double* Un, long long h, long long nh, double alpha,
+                                            double beta, double& ru, double& rr) {
+  const double2 di = reinterpret_cast<const double2*>(A.DINV)[h];
+  double2 r[NC], sv[NC], wv[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const long long t = c * nh + h;
+    r[c] = reinterpret_cast<const double2*>(A.R)[t];
+    sv[c] = reinterpret_cast<const double2*>(A.S)[t];
+    wv[c] = reinterpret_cast<const double2*>(A.W)[t];
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const long long t = c * nh + h;
+    double2 s, rn;
+    s.x = fma(beta, sv[c].x, wv[c].x);
+    s.y = fma(beta, sv[c].y, wv[c].y);
+    rn.x = fma(-alpha, s.x, r[c].x);
+    rn.y = fma(-alpha, s.y, r[c].y);
+    reinterpret_cast<double2*>(A.S)[t] = s;
+    reinterpret_cast<double2*>(A.R)[t] = rn;
+    const double2 un = make_double2(rn.x * di.x, rn.y * di.y);
+    reinterpret_cast<double2*>(Un)[t] = un;
+    ru = fma(rn.x, un.x, ru);
+    rr = fma(rn.x, rn.x, rr);
+    ru = fma(rn.y, un.y, ru);
+    rr = fma(rn.y, rn.y, rr);
+  }
+}
+// scalar form (odd sizes / misaligned x)
+template <int NC>
+__device__ __forceinline__ void cg_update1s(const Cg2Args& A, double* Un, long long f, long long nn, double alpha,
+                                            double beta, double& ru, double& rr) {
+  const double di = A.DINV[f];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const long long t = c * nn + f;
+    const double s = fma(beta, A.S[t], A.W[t]);
+    A.S[t] = s;
+    const double r = fma(-alpha, s, A.R[t]);
+    A.R[t] = r;
+    const double u = r * di;
+    Un[t] = u;
+    ru = fma(r, u, ru);
+    rr = fma(r, r, rr);
+  }
+}
+// deferred p / x update at global index g (pair when two)
+__device__ __forceinline__ void cg_px2(const Cg2Args& A, const double* Up, long long g, double alpha, double beta) {
+  const double2 u = *reinterpret_cast<const double2*>(Up + g);
+  double2 p = *reinterpret_cast<const double2*>(A.Pv + g);
+  double2 x = *reinterpret_cast<const double2*>(A.x + g);
+  p.x = fma(beta, p.x, u.x);
+  p.y = fma(beta, p.y, u.y);
+  x.x = fma(alpha, p.x, x.x);
+  x.y = fma(alpha, p.y, x.y);
+  *reinterpret_cast<double2*>(A.Pv + g) = p;
+  *reinterpret_cast<double2*>(A.x + g) = x;
+}
+__device__ __forceinline__ void cg_px1(const Cg2Args& A, const double* Up, long long g, double alpha, double beta) {
+  const double p = fma(beta, A.Pv[g], Up[g]);
+  A.Pv[g] = p;
+  A.x[g] = fma(alpha, p, A.x[g]);
+}
+
 // ------------------------------------------------------------------------
 // P = 7 (P1 = 8) phase B: one warp per element, fp64 tensor cores.
 // A warp owns element e (all fields).  It copies the element and its four face
@@ -982,26 +1055,52 @@ __device__ __forceinline__ void wpe_sip(const Op2DDev& op, const MmaLane& K, con
   __syncwarp();   // QX / QY / DT / FC are rewritten by the next call
 }
 
+// deferred CG p / x update riding in phase B (see cg_update2s); up == nullptr: none
+struct PxArgs {
+  const double* up;
+  double* p;
+  double* x;
+  double al, be;
+};
+
 // one field of a staged element: w = a (hwy Bx + hwx By) + hwx hwy v;
-// epi(g, w0, w1, v0, v1) for the lane's node pair
+// epi(g, w0, w1, v0, v1) for the lane's node pair.  With px.up, the field's
+// p / x operands are loaded before the contractions (their latency hides
+// behind the tensor-core work) and updated after.
 template <int NC, typename Epi>
 __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const MmaLane& K, int c, double a,
-                                          long long gi, Epi&& epi) {
+                                          long long gi, Epi&& epi, const PxArgs& px) {
   using W = Wpe<NC>;
   const int lane = threadIdx.x & 31, g = lane >> 2, n0 = 2 * (lane & 3);
   const double* Ue = ws + W::OWN + c * W::NP;
+  const long long gc = gi + c * op.nn;
+  double2 pu, pp, px_;
+  if (px.up) {
+    pu = __ldcs(reinterpret_cast<const double2*>(px.up + gc));
+    pp = __ldcs(reinterpret_cast<const double2*>(px.p + gc));
+    px_ = __ldcs(reinterpret_cast<const double2*>(px.x + gc));
+  }
   double bx0, bx1, by0, by1;
   wpe_sip<NC>(op, K, Ue, ws + W::NBR + c * 64, ws + W::COEF, ws + W::CFN, ws + W::QX, ws + W::QY, ws + W::DOT,
               ws + W::FCON, bx0, bx1, by0, by1);
   const double2 v = *reinterpret_cast<const double2*>(Ue + g * W::RP + n0);
-  epi(gi + c * op.nn, fma(a, fma(K.hwy, bx0, K.hwx[0] * by0), K.hh[0] * v.x),
+  epi(gc, fma(a, fma(K.hwy, bx0, K.hwx[0] * by0), K.hh[0] * v.x),
       fma(a, fma(K.hwy, bx1, K.hwx[1] * by1), K.hh[1] * v.y), v.x, v.y);
+  if (px.up) {
+    pp.x = fma(px.be, pp.x, pu.x);
+    pp.y = fma(px.be, pp.y, pu.y);
+    px_.x = fma(px.al, pp.x, px_.x);
+    px_.y = fma(px.al, pp.y, px_.y);
+    __stcs(reinterpret_cast<double2*>(px.p + gc), pp);
+    __stcs(reinterpret_cast<double2*>(px.x + gc), px_);
+  }
 }
 
 // the block's share of phase B: warps stride over elements
 template <int NC, typename Epi>
 __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const double* src, const double* Cf,
-                                          double a, Epi&& epi, long long* tacc = nullptr) {
+                                          double a, Epi&& epi, long long* tacc = nullptr,
+                                          const PxArgs& px = PxArgs{nullptr, nullptr, nullptr, 0.0, 0.0}) {
   using W = Wpe<NC>;
   MmaLane K;
   mma_lane_init(op, K);
@@ -1047,7 +1146,7 @@ __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const d
     const long long gi = (long long)eo + g * 8 + n0;
     const long long c1 = clock64();
 #pragma unroll 1
-    for (int c = 0; c < NC; ++c) wpe_field<NC>(op, ws, K, c, a, gi, epi);
+    for (int c = 0; c < NC; ++c) wpe_field<NC>(op, ws, K, c, a, gi, epi, px);
     if (tacc) { tacc[0] += c1 - c0; tacc[1] += clock64() - c1; tacc[2] += 1; }
   }
 }
@@ -1384,23 +1483,25 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     }
     return;
   }
-  // phase B body: w = A u; partial (w,u)
-  auto phase_B = [&]() {
+  // phase B body: w = A un; partial (w,un); with Up, the deferred p / x update
+  // of this iteration (p = Up + beta p, x += alpha p) at the same nodes
+  auto phase_B = [&](const double* Un, const double* Up, double al, double be) {
     double wu = 0.0;
     if constexpr (P1 == 8) {
       long long ta[3] = {0, 0, 0};
       const bool tw = A.timing != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-      wpe_phase<NC>(op, sm, A.U, A.Cf, A.a, [&](long long g, double w0, double w1, double v0, double v1) {
+      wpe_phase<NC>(op, sm, Un, A.Cf, A.a, [&](long long g, double w0, double w1, double v0, double v1) {
         *reinterpret_cast<double2*>(A.W + g) = make_double2(w0, w1);
         wu = fma(w0, v0, wu);
         wu = fma(w1, v1, wu);
-      }, tw ? ta : nullptr);
+      }, tw ? ta : nullptr, PxArgs{Up, A.Pv, A.x, al, be});
       if (tw) { A.timing[20] += ta[0]; A.timing[21] += ta[1]; A.timing[22] += ta[2]; }
     } else {
       for (int tile = blockIdx.x; tile < ntiles; tile += G)
-        cg_tile<P1, NC>(op, sm, tile, tpr, A.U, nullptr, A.Cf, A.a, [&](long long g, double wv, double u) {
+        cg_tile<P1, NC>(op, sm, tile, tpr, Un, nullptr, A.Cf, A.a, [&](long long g, double wv, double u) {
           A.W[g] = wv;
           wu = fma(wv, u, wu);
+          if (Up) cg_px1(A, Up, g, al, be);
         });
     }
     return wu;
@@ -1420,7 +1521,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
         }
     }
     grid.sync();
-    const double wu = phase_B();
+    const double wu = phase_B(A.U, nullptr, 0.0, 0.0);
     block_part(ru, wu, rr, slot1);
   }
   grid.sync();
@@ -1436,7 +1537,9 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     if (k >= (A.dbg ? 10 : A.maxit)) { ok = false; break; }
     const bool stamp = stampb && k == 2;
     if (stamp) tm[0] = gtimer();
-    // phase A: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = r dinv
+    // phase A': s = w + beta s, r -= alpha s, u_new = r dinv (p, x in phase B)
+    double* const Un = (k & 1) ? A.U : A.U2;     // register selects: no local-memory array
+    const double* const Up = (k & 1) ? A.U2 : A.U;
     double ru = 0.0, rr = 0.0;
     if (vec) {   // blocks claim 1024-pair chunks dynamically (balance + DRAM page locality)
       const long long nh = nn >> 1;
@@ -1453,37 +1556,18 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
 #pragma unroll 1
         for (int i = 0; i < 4; ++i) {
           const long long h = h0 + i * 256 + threadIdx.x;
-          if (h < nh) cg_update2<NC>(A, h, nh, alpha, beta, ru, rr);
+          if (h < nh) cg_update2s<NC>(A, Un, h, nh, alpha, beta, ru, rr);
         }
         __syncthreads();
       }
     } else {
-      for (long long f = gtid; f < nn; f += nthr) {
-        const double di = A.DINV[f];
-#pragma unroll
-        for (int c = 0; c < NC_MAX; ++c)
-          if (c < nc) {
-            const long long t = c * nn + f;
-            double r = A.R[t];
-            const double p = fma(beta, A.Pv[t], r * di);
-            const double s = fma(beta, A.S[t], A.W[t]);
-            A.Pv[t] = p;
-            A.S[t] = s;
-            A.x[t] = fma(alpha, p, A.x[t]);
-            r = fma(-alpha, s, r);
-            A.R[t] = r;
-            const double u = r * di;
-            A.U[t] = u;
-            ru = fma(r, u, ru);
-            rr = fma(r, r, rr);
-          }
-      }
+      for (long long f = gtid; f < nn; f += nthr) cg_update1s<NC>(A, Un, f, nn, alpha, beta, ru, rr);
     }
     if (stamp) tm[1] = gtimer();
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) reinterpret_cast<unsigned*>(A.scal)[k & 1] = 0u;   // next use: k+2
     if (stamp) tm[2] = gtimer();
-    const double wu = phase_B();
+    const double wu = phase_B(Un, Up, alpha, beta);
     if (stamp) tm[3] = gtimer();
     double* slot = (k & 1) ? slot1 : slot0;
     block_part(ru, wu, rr, slot);
@@ -1663,7 +1747,7 @@ __global__ void __launch_bounds__(256) k2p_u0(Cg2Args A) {
   blk_part3(ru, rr, 0.0, red, A.part);
 }
 
-// phase A: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = r dinv
+// phase A': s = w + beta s, r -= alpha s, u = r dinv into A.U (p, x in the matvec)
 template <int NC>
 __global__ void __launch_bounds__(256) k2p_update(Cg2Args A) {
   __shared__ double red[32 * 4];
@@ -1672,36 +1756,19 @@ __global__ void __launch_bounds__(256) k2p_update(Cg2Args A) {
   const Op2DDev& op = A.op;
   const long long nn = op.nn, o0 = own0(op), o1 = o0 + nown(op);
   const long long nt = (long long)gridDim.x * blockDim.x, g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool vec = ((nn | o0 | o1) & 1) == 0 && ((reinterpret_cast<uintptr_t>(A.x) & 15) == 0);
+  const bool vec = ((nn | o0 | o1) & 1) == 0;
   double ru = 0.0, rr = 0.0;
   if (vec) {
     const long long nh = nn >> 1;
-    for (long long h = (o0 >> 1) + g0; h < (o1 >> 1); h += nt) cg_update2<NC>(A, h, nh, alpha, beta, ru, rr);
+    for (long long h = (o0 >> 1) + g0; h < (o1 >> 1); h += nt) cg_update2s<NC>(A, A.U, h, nh, alpha, beta, ru, rr);
   } else {
-    for (long long f = o0 + g0; f < o1; f += nt) {
-      const double di = A.DINV[f];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const long long t = c * nn + f;
-        double r = A.R[t];
-        const double p = fma(beta, A.Pv[t], r * di);
-        const double s = fma(beta, A.S[t], A.W[t]);
-        A.Pv[t] = p;
-        A.S[t] = s;
-        A.x[t] = fma(alpha, p, A.x[t]);
-        r = fma(-alpha, s, r);
-        A.R[t] = r;
-        const double u = r * di;
-        A.U[t] = u;
-        ru = fma(r, u, ru);
-        rr = fma(r, r, rr);
-      }
-    }
+    for (long long f = o0 + g0; f < o1; f += nt) cg_update1s<NC>(A, A.U, f, nn, alpha, beta, ru, rr);
   }
   blk_part3(ru, rr, 0.0, red, A.part);
 }
 
-// phase B: w = A u; partial (w,u) -> part2
+// phase B: w = A u; partial (w,u) -> part2; with A.px the deferred p / x
+// update of this iteration from the previous u (A.U2)
 template <int P1, int NC>
 __global__ void __launch_bounds__(256, 2) k2p_matvec(Cg2Args A) {
   extern __shared__ double sm[];
@@ -1709,19 +1776,22 @@ __global__ void __launch_bounds__(256, 2) k2p_matvec(Cg2Args A) {
   constexpr int EB = Blk<P1>::EB;
   if (A.sc->done) return;
   const Op2DDev& op = A.op;
+  const double alpha = A.sc->alpha, beta = A.sc->beta;
+  const double* Up = A.px ? A.U2 : nullptr;
   double wu = 0.0;
   if constexpr (P1 == 8) {
     wpe_phase<NC>(op, sm, A.U, A.Cf, A.a, [&](long long g, double w0, double w1, double v0, double v1) {
       *reinterpret_cast<double2*>(A.W + g) = make_double2(w0, w1);
       wu = fma(w0, v0, wu);
       wu = fma(w1, v1, wu);
-    });
+    }, nullptr, PxArgs{Up, A.Pv, A.x, alpha, beta});
   } else {
     const int tpr = (op.nex + EB - 1) / EB, ntiles = tpr * op.ney;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
       cg_tile<P1, NC>(op, sm, tile, tpr, A.U, nullptr, A.Cf, A.a, [&](long long g, double wv, double u) {
         A.W[g] = wv;
         wu = fma(wv, u, wu);
+        if (Up) cg_px1(A, Up, g, alpha, beta);
       });
   }
   blk_part3(wu, 0.0, 0.0, sm + L::RED, A.part2);
@@ -2016,6 +2086,7 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
   A.U = p; p += op.n;
   A.Pv = p; p += op.n;
   A.S = p; p += op.n;
+  A.U2 = p; p += op.n;
   A.DINV = p; p += op.nn;
   A.Cf = p; p += op.nn;
   A.scal = p; p += 16;
@@ -2054,11 +2125,12 @@ int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks) {
 
 
 // ------------------------------------------------ partitioned solve launchers
-size_t cg2p_ws_doubles(const Op2DDev& op, int G) { return 5 * (size_t)op.n + 2 * (size_t)op.nn + 8 * (size_t)G; }
-double* cg2p_U(const Op2DDev& op, double* ws) { return ws + 2 * op.n; }
+size_t cg2p_ws_doubles(const Op2DDev& op, int G) { return 6 * (size_t)op.n + 2 * (size_t)op.nn + 8 * (size_t)G; }
+// the two u buffers of the split solve: which 0 -> U, 1 -> U2
+double* cg2p_U(const Op2DDev& op, double* ws, int which) { return ws + (which ? 5 : 2) * op.n; }
 
 static Cg2Args cg2p_args(const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int G,
-                         const CgPScal* sc) {
+                         const CgPScal* sc, int ucur) {
   Cg2Args A{};
   A.op = op; A.coef = k; A.a = a; A.rhs = rhs; A.x = x;
   double* p = ws;
@@ -2067,11 +2139,20 @@ static Cg2Args cg2p_args(const Op2DDev& op, CoefDev k, double a, const double* r
   A.U = p; p += op.n;
   A.Pv = p; p += op.n;
   A.S = p; p += op.n;
+  A.U2 = p; p += op.n;
   A.DINV = p; p += op.nn;
   A.Cf = p; p += op.nn;
   A.part = p; p += 4 * G;
   A.part2 = p;
   A.sc = sc;
+  // ucur: 0 / 1 = which buffer holds this iteration's u (the other the previous u);
+  // -1: setup (u0 into buffer 0, no p / x update)
+  if (ucur == 1) {
+    double* t = A.U;
+    A.U = A.U2;
+    A.U2 = t;
+  }
+  A.px = ucur >= 0 ? 1 : 0;
   return A;
 }
 
@@ -2097,8 +2178,8 @@ static cudaError_t p2_phase(int phase, const Cg2Args& A, int G, cudaStream_t st)
 }
 
 int launch2p_phase(Ctx* c, int phase, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x,
-                   double* ws, int G, const CgPScal* sc) {
-  const Cg2Args A = cg2p_args(op, k, a, rhs, x, ws, G, sc);
+                   double* ws, int G, const CgPScal* sc, int ucur) {
+  const Cg2Args A = cg2p_args(op, k, a, rhs, x, ws, G, sc, ucur);
   cudaError_t e = cudaSuccess;
   SISDC_P1_SWITCH(op.p1, {
     e = op.nc == 4 ? p2_phase<P1, 4>(phase, A, G, c->stream) : p2_phase<P1, 1>(phase, A, G, c->stream);
@@ -2113,7 +2194,7 @@ int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, i
   RedPArgs R{};
   R.nparts = nparts; R.G = G; R.mode = mode; R.out = out;
   for (int p = 0; p < nparts; ++p) {
-    const double* base = ws[p] + 5 * ops[p].n + 2 * ops[p].nn;
+    const double* base = ws[p] + 6 * ops[p].n + 2 * ops[p].nn;
     R.pa[p] = base;
     R.pb[p] = base + 4 * G;
   }

@@ -222,14 +222,16 @@ int reduce_all(sisdc_op1d* op, int mode) {
   return SISDC_OK;
 }
 
-int phase_all(sisdc_op1d* op, int phase, const CoefDev& k, double a, const double* rhs, double* x) {
+// ucur: which u buffer holds this iteration's u (the other the previous one); -1 setup
+int phase_all(sisdc_op1d* op, int phase, const CoefDev& k, double a, const double* rhs, double* x, int ucur = -1) {
   for (const Part2D& P : op->parts)
-    if (int rc = launch2p_phase(C(op), phase, P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc))
+    if (int rc = launch2p_phase(C(op), phase, P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc,
+                                ucur))
       return rc;
   return SISDC_OK;
 }
 
-int halo_u(sisdc_op1d* op) {
+int halo_u(sisdc_op1d* op, int which) {
   Ctx* c = C(op);
   const int np = (int)op->parts.size();
   if (!op->comm) {
@@ -237,19 +239,21 @@ int halo_u(sisdc_op1d* op) {
     double* base[MAXPART];
     for (int p = 0; p < np; ++p) {
       ops[p] = op->parts[p].dev;
-      base[p] = cg2p_U(ops[p], op->parts[p].ws);
+      base[p] = cg2p_U(ops[p], op->parts[p].ws, which);
     }
     return launch2p_halo(c, np, ops, base, ops[0].nc, 1, 0);
   }
   // one local partition: its workspace u has the storage layout of a state
   const Part2D& P = op->parts[0];
-  return halo(op, cg2p_U(P.dev, P.ws) - P.off, 1, 0, false);
+  return halo(op, cg2p_U(P.dev, P.ws, which) - P.off, 1, 0, false);
 }
 
-int iterate(sisdc_op1d* op, const CoefDev& k, double a, const double* rhs, double* x) {
-  if (int rc = phase_all(op, P2_UPDATE, k, a, rhs, x)) return rc;
-  if (int rc = halo_u(op)) return rc;
-  if (int rc = phase_all(op, P2_MATVEC, k, a, rhs, x)) return rc;
+// iteration j: u_prev in buffer j & 1 (the setup's u0 in buffer 0), u_new in the other
+int iterate(sisdc_op1d* op, int j, const CoefDev& k, double a, const double* rhs, double* x) {
+  const int ucur = (j + 1) & 1;
+  if (int rc = phase_all(op, P2_UPDATE, k, a, rhs, x, ucur)) return rc;
+  if (int rc = halo_u(op, ucur)) return rc;
+  if (int rc = phase_all(op, P2_MATVEC, k, a, rhs, x, ucur)) return rc;
   if (int rc = reduce_all(op, 1)) return rc;
   return launch2p_scalar(C(op), 2, op->d_red + 4, op->d_sc);
 }
@@ -261,6 +265,8 @@ int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* 
   cudaStreamIsCapturing(c->stream, &cap);
   if (cap != cudaStreamCaptureStatusNone)
     return c->fail(SISDC_ERR_UNSUPPORTED, "a partitioned implicit solve polls its convergence flag and cannot be captured");
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(rhs)) & 15))
+    return c->fail(SISDC_ERR_ARG, "2-D implicit solve: rhs and x must be 16-byte aligned");
   // coefficient source and rhs (x0 = rhs feeds the first matvec)
   if (int rc = halo_coef(op, k)) return rc;
   if (int rc = halo(op, rhs, 1, 0, false)) return rc;
@@ -270,7 +276,7 @@ int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* 
   if (int rc = reduce_all(op, 0)) return rc;
   if (int rc = launch2p_scalar(c, 0, op->d_red + 4, op->d_sc)) return rc;
   if (int rc = phase_all(op, P2_U0, k, a, rhs, x)) return rc;
-  if (int rc = halo_u(op)) return rc;
+  if (int rc = halo_u(op, 0)) return rc;
   if (int rc = phase_all(op, P2_MATVEC, k, a, rhs, x)) return rc;
   if (int rc = reduce_all(op, 1)) return rc;
   if (int rc = launch2p_scalar(c, 1, op->d_red + 4, op->d_sc)) return rc;
@@ -279,7 +285,7 @@ int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* 
   const int max_batches = c->maxit / B + 3;
   for (int j = 0; j < max_batches; ++j) {
     for (int i = 0; i < B; ++i)
-      if (int rc = iterate(op, k, a, rhs, x)) return rc;
+      if (int rc = iterate(op, j * B + i, k, a, rhs, x)) return rc;
     cudaError_t e = cudaMemcpyAsync(op->h_done + (j & 1), &op->d_sc->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaEventRecord(op->ev[j & 1], c->stream);
     if (e != cudaSuccess) return c->cuda(e, "CG convergence flag");

@@ -87,10 +87,10 @@ int set_cg2_tables(Ctx* c, int p1, const double* tab);
 struct CgPScal;
 enum { P2_INIT = 0, P2_DINV, P2_RESID, P2_U0, P2_UPDATE, P2_MATVEC };
 size_t cg2p_ws_doubles(const Op2DDev& op, int G);
-double* cg2p_U(const Op2DDev& op, double* ws);
+double* cg2p_U(const Op2DDev& op, double* ws, int which);
 int cg2p_blocks(Ctx* c, const Op2DDev& op, int* G);
 int launch2p_phase(Ctx* c, int phase, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x,
-                   double* ws, int G, const CgPScal* sc);
+                   double* ws, int G, const CgPScal* sc, int ucur);
 int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out);
 int launch2p_scalar(Ctx* c, int mode, const double* tot, CgPScal* sc);
 int launch2p_halo(Ctx* c, int nparts, const Op2DDev* ops, double* const* base, int nc, int mcount, long long mstride);
