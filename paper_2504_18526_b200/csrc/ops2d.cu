@@ -1137,8 +1137,8 @@ __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const d
       cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr0, srcc[c] + nb[FB] + lane);
       cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr1, srcc[c] + nb[FB] + 32 + lane);
     }
-    K.cfn = Cf[(f == FR ? nb[FR] : f == FL ? nb[FL] : f == FT ? nb[FT] : nb[FB]) + fnode];
-    ws[W::CFN + lane] = K.cfn;
+    // neighbour face coefficient: asynchronous too (a blocking load here stalled the warp)
+    cp_async8(ws + W::CFN + lane, Cf + (f == FR ? nb[FR] : f == FL ? nb[FL] : f == FT ? nb[FT] : nb[FB]) + fnode);
     const long long c0 = clock64();
     cp_async_wait_all();
     const int g = lane >> 2, n0 = 2 * (lane & 3);
