@@ -553,6 +553,7 @@ struct Cg2Args {
   double* part2;       // [gridDim][4]
   const struct CgPScal* sc;
   int px;              // split matvec: also advance p, x (p = u_prev + beta p, x += alpha p)
+  int defer;           // split solve: p / x deferred to the matvec (P = 7), else in the update
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -789,11 +790,112 @@ __device__ __forceinline__ void cg_tile(const Op2DDev& op, double* sm, int tile,
   }
 }
 
+// P = 3 (P1 = 4) CG matvec, register-resident: a half-warp owns an element
+// (lane = node, j = t/4, i = t%4), all fields.  The element, its four face
+// neighbours and the coefficient are read straight from global memory (one
+// coalesced 128-byte run per element and field); every line contraction
+// reaches its operands by warp shuffles, so there is no shared memory and no
+// block barrier (cg_tile staged 3 EB + 2 elements per tile behind
+// __syncthreads and was latency bound).  Same operations in the same order as
+// cg_tile, so the results are bitwise identical.  epi(g, w, v) per own node.
+__device__ __forceinline__ double pick4(const double* v, int c) {   // register select, no local memory
+  return c == 0 ? v[0] : c == 1 ? v[1] : c == 2 ? v[2] : v[3];
+}
+template <int NC, typename Epi>
+__device__ __forceinline__ void wph_phase(const Op2DDev& op, const double* src, const double* Cf, double a, Epi&& epi) {
+  constexpr int P1 = 4, P = 3, NN = 16;
+  using T = CT<P1>;
+  // D | DTW in shared memory (lane-varying rows; registers are the limit here)
+  __shared__ double sT[32];
+  if (threadIdx.x < 32) sT[threadIdx.x] = op.tab[threadIdx.x];   // TabOff: D (16) then DTW (16)
+  __syncthreads();
+  const int lane = threadIdx.x & 31, t = lane & 15, j = t >> 2, i = t & 3, hb = lane & 16;
+  const double hwx = 0.5 * op.dx * op.tab[TabOff::w(P1) + i], hwy = 0.5 * op.dy * op.tab[TabOff::w(P1) + j];
+  auto sh = [&](double v, int src_t) { return __shfl_sync(0xffffffffu, v, hb | src_t); };
+  const int ne = op.nex * op.ney;
+  const int nw = (blockDim.x >> 5) * gridDim.x, w0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nn = op.nn;
+  for (int pr = w0; 2 * pr < ne; pr += nw) {
+    const int e = 2 * pr + (hb ? 1 : 0);
+    const bool valid = e < ne;
+    const int ee = valid ? e : ne - 1;
+    const int oy = ee / op.nex, ex = ee - oy * op.nex, ey = oy + op.row0;
+    const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
+    const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
+    const long long eo = ((long long)ey * op.nex + ex) * NN;
+    const long long oR = ((long long)ey * op.nex + exr) * NN, oL = ((long long)ey * op.nex + exl) * NN;
+    const long long oT = ((long long)eyt * op.nex + ex) * NN, oB = ((long long)eyb * op.nex + ex) * NN;
+    // coefficient: own node, and the neighbours' face nodes of this lane's row / column
+    const double cc = Cf[eo + t];
+    const double fcp_x = Cf[oR + j * P1], fcm_x = Cf[oL + j * P1 + P];
+    const double fcp_y = Cf[oT + i], fcm_y = Cf[oB + P * P1 + i];
+    const double cPx = sh(cc, j * 4 + P), c0x = sh(cc, j * 4), cPy = sh(cc, P * 4 + i), c0y = sh(cc, i);
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c) {
+      const double* sc = src + c * nn;
+      const double v = sc[eo + t], nR = sc[oR + t], nL = sc[oL + t], nT = sc[oT + t], nB = sc[oB + t];
+      // q = C s D u along the row (x) and the column (y) of this node
+      double gx = 0.0, gy = 0.0, row0, rowP, col0, colP;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double r_ = sh(v, j * 4 + q), c_ = sh(v, q * 4 + i);
+        gx = fma(sT[i * P1 + q], r_, gx);
+        gy = fma(sT[j * P1 + q], c_, gy);
+        if (q == 0) { row0 = r_; col0 = c_; }
+        if (q == P) { rowP = r_; colP = c_; }
+      }
+      const double qx = cc * (op.sx * gx), qy = cc * (op.sy * gy);
+      // neighbour face fluxes of this row / column and the neighbour face values
+      double gR = 0.0, gL = 0.0, gT = 0.0, gB = 0.0, uRf = 0.0, uLf = 0.0, uTf = 0.0, uBf = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double r_ = sh(nR, j * 4 + q), l_ = sh(nL, j * 4 + q);
+        const double t_ = sh(nT, q * 4 + i), b_ = sh(nB, q * 4 + i);
+        gR = fma(c_tab2[T::D + q], r_, gR);
+        gL = fma(c_tab2[T::D + P * P1 + q], l_, gL);
+        gT = fma(c_tab2[T::D + q], t_, gT);
+        gB = fma(c_tab2[T::D + P * P1 + q], b_, gB);
+        if (q == 0) { uRf = r_; uTf = t_; }
+        if (q == P) { uLf = l_; uBf = b_; }
+      }
+      const double qp_x = fcp_x * (op.sx * gR), qm_x = fcm_x * (op.sx * gL);
+      const double qp_y = fcp_y * (op.sy * gT), qm_y = fcm_y * (op.sy * gB);
+      double bx = 0.0, by = 0.0, qx0, qxP, qy0, qyP;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double a_ = sh(qx, j * 4 + k), b_ = sh(qy, k * 4 + i);
+        bx = fma(sT[16 + i * P1 + k], a_, bx);
+        by = fma(sT[16 + j * P1 + k], b_, by);
+        if (k == 0) { qx0 = a_; qy0 = b_; }
+        if (k == P) { qxP = a_; qyP = b_; }
+      }
+      // x-line (row j) and y-line (column i) face and adjoint-lift terms
+      const double jpx = rowP - uRf, jmx = uLf - row0;
+      const double fpx = -(0.5 * (qxP + qp_x)) + (op.mux * (0.5 * (cPx + fcp_x))) * jpx;
+      const double fmx = -(0.5 * (qm_x + qx0)) + (op.mux * (0.5 * (fcm_x + c0x))) * jmx;
+      const double lpx = op.sx * ((0.5 * cPx) * jpx), lmx = op.sx * ((0.5 * c0x) * jmx);
+      const double jpy = colP - uTf, jmy = uBf - col0;
+      const double fpy = -(0.5 * (qyP + qp_y)) + (op.muy * (0.5 * (cPy + fcp_y))) * jpy;
+      const double fmy = -(0.5 * (qm_y + qy0)) + (op.muy * (0.5 * (fcm_y + c0y))) * jmy;
+      const double lpy = op.sy * ((0.5 * cPy) * jpy), lmy = op.sy * ((0.5 * c0y) * jmy);
+      if (i == P) bx += fpx;
+      if (i == 0) bx -= fmx;
+      bx -= lpx * c_tab2[T::D + P * P1 + i];
+      bx = bx - lmx * c_tab2[T::D + i];
+      if (j == P) by += fpy;
+      if (j == 0) by -= fmy;
+      by -= lpy * c_tab2[T::D + P * P1 + j];
+      by = by - lmy * c_tab2[T::D + j];
+      if (valid) epi(c * nn + eo + t, fma(a, fma(hwy, bx, hwx * by), (hwx * hwy) * v), v);
+    }
+  }
+}
+
 // phase A over in-field nodes [2h, 2h+2) of all fields: every load first, then
 // the updates and stores; accumulates the partials (r,u), (r,r)
 template <int NC>
-__device__ __forceinline__ void cg_update2(const Cg2Args& A, long long h, long long nh, double alpha, double beta,
-                                           double& ru, double& rr) {
+__device__ __forceinline__ void cg_update2(const Cg2Args& A, double* Un, long long h, long long nh, double alpha,
+                                           double beta, double& ru, double& rr) {
   const double2 di = reinterpret_cast<const double2*>(A.DINV)[h];
   double2 r[NC], pv[NC], sv[NC], wv[NC], xv[NC];
 #pragma unroll
@@ -822,7 +924,7 @@ __device__ __forceinline__ void cg_update2(const Cg2Args& A, long long h, long l
     reinterpret_cast<double2*>(A.x)[t] = x;
     reinterpret_cast<double2*>(A.R)[t] = rn;
     const double2 un = make_double2(rn.x * di.x, rn.y * di.y);
-    reinterpret_cast<double2*>(A.U)[t] = un;
+    reinterpret_cast<double2*>(Un)[t] = un;
     ru = fma(rn.x, un.x, ru);
     rr = fma(rn.x, rn.x, rr);
     ru = fma(rn.y, un.y, ru);
@@ -876,6 +978,28 @@ __device__ __forceinline__ void cg_update1s(const Cg2Args& A, double* Un, long l
     const double s = fma(beta, A.S[t], A.W[t]);
     A.S[t] = s;
     const double r = fma(-alpha, s, A.R[t]);
+    A.R[t] = r;
+    const double u = r * di;
+    Un[t] = u;
+    ru = fma(r, u, ru);
+    rr = fma(r, r, rr);
+  }
+}
+// full scalar update (p, x in phase A: the P != 7 levels, see k2_cg)
+template <int NC>
+__device__ __forceinline__ void cg_update1(const Cg2Args& A, double* Un, long long f, long long nn, double alpha,
+                                           double beta, double& ru, double& rr) {
+  const double di = A.DINV[f];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const long long t = c * nn + f;
+    double r = A.R[t];
+    const double p = fma(beta, A.Pv[t], r * di);
+    const double s = fma(beta, A.S[t], A.W[t]);
+    A.Pv[t] = p;
+    A.S[t] = s;
+    A.x[t] = fma(alpha, p, A.x[t]);
+    r = fma(-alpha, s, r);
     A.R[t] = r;
     const double u = r * di;
     Un[t] = u;
@@ -1170,9 +1294,6 @@ struct Ev {                 // per-warp shared region (doubles)
   static constexpr int WARP = FHP + 32 * NC;
 };
 constexpr int EV_WARPS = 4;
-__device__ __forceinline__ double pick4(const double* v, int c) {   // register select, no local memory
-  return c == 0 ? v[0] : c == 1 ? v[1] : c == 2 ? v[2] : v[3];
-}
 
 // convective term of field c at the lane's node pair from the staged element
 // (state rows in `own`, padded) and the face fluxes fh[lane*NC + c]
@@ -1359,6 +1480,10 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   const Op2DDev& op = A.op;
   constexpr int NN = P1 * P1, P = P1 - 1, EB = Blk<P1>::EB;
   constexpr int nc = NC;
+  // p / x deferred into phase B only where phase B is issue bound (P = 7 tensor-core
+  // path); the register-lean lower-degree matvecs are latency bound, and extra
+  // dependent loads there cost more than the streaming pass saves
+  constexpr bool DEFER = P1 == 8;
   const long long nn = op.nn;
   const int G = gridDim.x;
   const int tpr = (op.nex + EB - 1) / EB, ntiles = tpr * op.ney;
@@ -1466,6 +1591,8 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
         epi(g, w0, v0);
         epi(g + 1, w1, v1);
       });
+    } else if constexpr (P1 == 4) {
+      wph_phase<NC>(op, A.x, A.Cf, A.a, epi);
     } else {
       for (int tile = blockIdx.x; tile < ntiles; tile += G) cg_tile<P1, NC>(op, sm, tile, tpr, A.x, nullptr, A.Cf, A.a, epi);
     }
@@ -1497,12 +1624,16 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
       }, tw ? ta : nullptr, PxArgs{Up, A.Pv, A.x, al, be});
       if (tw) { A.timing[20] += ta[0]; A.timing[21] += ta[1]; A.timing[22] += ta[2]; }
     } else {
-      for (int tile = blockIdx.x; tile < ntiles; tile += G)
-        cg_tile<P1, NC>(op, sm, tile, tpr, Un, nullptr, A.Cf, A.a, [&](long long g, double wv, double u) {
-          A.W[g] = wv;
-          wu = fma(wv, u, wu);
-          if (Up) cg_px1(A, Up, g, al, be);
-        });
+      auto epi = [&](long long g, double wv, double u) {
+        A.W[g] = wv;
+        wu = fma(wv, u, wu);
+        if (Up) cg_px1(A, Up, g, al, be);
+      };
+      if constexpr (P1 == 4) {
+        wph_phase<NC>(op, Un, A.Cf, A.a, epi);
+      } else {
+        for (int tile = blockIdx.x; tile < ntiles; tile += G) cg_tile<P1, NC>(op, sm, tile, tpr, Un, nullptr, A.Cf, A.a, epi);
+      }
     }
     return wu;
   };
@@ -1556,18 +1687,24 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
 #pragma unroll 1
         for (int i = 0; i < 4; ++i) {
           const long long h = h0 + i * 256 + threadIdx.x;
-          if (h < nh) cg_update2s<NC>(A, Un, h, nh, alpha, beta, ru, rr);
+          if (h < nh) {
+            if constexpr (DEFER) cg_update2s<NC>(A, Un, h, nh, alpha, beta, ru, rr);
+            else cg_update2<NC>(A, Un, h, nh, alpha, beta, ru, rr);
+          }
         }
         __syncthreads();
       }
     } else {
-      for (long long f = gtid; f < nn; f += nthr) cg_update1s<NC>(A, Un, f, nn, alpha, beta, ru, rr);
+      for (long long f = gtid; f < nn; f += nthr) {
+        if constexpr (DEFER) cg_update1s<NC>(A, Un, f, nn, alpha, beta, ru, rr);
+        else cg_update1<NC>(A, Un, f, nn, alpha, beta, ru, rr);
+      }
     }
     if (stamp) tm[1] = gtimer();
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) reinterpret_cast<unsigned*>(A.scal)[k & 1] = 0u;   // next use: k+2
     if (stamp) tm[2] = gtimer();
-    const double wu = phase_B(Un, Up, alpha, beta);
+    const double wu = phase_B(Un, DEFER ? Up : nullptr, alpha, beta);
     if (stamp) tm[3] = gtimer();
     double* slot = (k & 1) ? slot1 : slot0;
     block_part(ru, wu, rr, slot);
@@ -1713,6 +1850,8 @@ __global__ void __launch_bounds__(256, 2) k2p_resid(Cg2Args A) {
       epi(g, w0, v0);
       epi(g + 1, w1, v1);
     });
+  } else if constexpr (P1 == 4) {
+    wph_phase<NC>(op, A.x, A.Cf, A.a, epi);
   } else {
     const int tpr = (op.nex + EB - 1) / EB, ntiles = tpr * op.ney;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) cg_tile<P1, NC>(op, sm, tile, tpr, A.x, nullptr, A.Cf, A.a, epi);
@@ -1756,13 +1895,19 @@ __global__ void __launch_bounds__(256) k2p_update(Cg2Args A) {
   const Op2DDev& op = A.op;
   const long long nn = op.nn, o0 = own0(op), o1 = o0 + nown(op);
   const long long nt = (long long)gridDim.x * blockDim.x, g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool vec = ((nn | o0 | o1) & 1) == 0;
+  const bool vec = ((nn | o0 | o1) & 1) == 0 && (A.defer || (reinterpret_cast<uintptr_t>(A.x) & 15) == 0);
   double ru = 0.0, rr = 0.0;
   if (vec) {
     const long long nh = nn >> 1;
-    for (long long h = (o0 >> 1) + g0; h < (o1 >> 1); h += nt) cg_update2s<NC>(A, A.U, h, nh, alpha, beta, ru, rr);
+    for (long long h = (o0 >> 1) + g0; h < (o1 >> 1); h += nt) {
+      if (A.defer) cg_update2s<NC>(A, A.U, h, nh, alpha, beta, ru, rr);
+      else cg_update2<NC>(A, A.U, h, nh, alpha, beta, ru, rr);
+    }
   } else {
-    for (long long f = o0 + g0; f < o1; f += nt) cg_update1s<NC>(A, A.U, f, nn, alpha, beta, ru, rr);
+    for (long long f = o0 + g0; f < o1; f += nt) {
+      if (A.defer) cg_update1s<NC>(A, A.U, f, nn, alpha, beta, ru, rr);
+      else cg_update1<NC>(A, A.U, f, nn, alpha, beta, ru, rr);
+    }
   }
   blk_part3(ru, rr, 0.0, red, A.part);
 }
@@ -1777,7 +1922,7 @@ __global__ void __launch_bounds__(256, 2) k2p_matvec(Cg2Args A) {
   if (A.sc->done) return;
   const Op2DDev& op = A.op;
   const double alpha = A.sc->alpha, beta = A.sc->beta;
-  const double* Up = A.px ? A.U2 : nullptr;
+  const double* Up = A.px && A.defer ? A.U2 : nullptr;
   double wu = 0.0;
   if constexpr (P1 == 8) {
     wpe_phase<NC>(op, sm, A.U, A.Cf, A.a, [&](long long g, double w0, double w1, double v0, double v1) {
@@ -1786,13 +1931,17 @@ __global__ void __launch_bounds__(256, 2) k2p_matvec(Cg2Args A) {
       wu = fma(w1, v1, wu);
     }, nullptr, PxArgs{Up, A.Pv, A.x, alpha, beta});
   } else {
-    const int tpr = (op.nex + EB - 1) / EB, ntiles = tpr * op.ney;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-      cg_tile<P1, NC>(op, sm, tile, tpr, A.U, nullptr, A.Cf, A.a, [&](long long g, double wv, double u) {
-        A.W[g] = wv;
-        wu = fma(wv, u, wu);
-        if (Up) cg_px1(A, Up, g, alpha, beta);
-      });
+    auto epi = [&](long long g, double wv, double u) {
+      A.W[g] = wv;
+      wu = fma(wv, u, wu);
+      if (Up) cg_px1(A, Up, g, alpha, beta);
+    };
+    if constexpr (P1 == 4) {
+      wph_phase<NC>(op, A.U, A.Cf, A.a, epi);
+    } else {
+      const int tpr = (op.nex + EB - 1) / EB, ntiles = tpr * op.ney;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) cg_tile<P1, NC>(op, sm, tile, tpr, A.U, nullptr, A.Cf, A.a, epi);
+    }
   }
   blk_part3(wu, 0.0, 0.0, sm + L::RED, A.part2);
 }
@@ -2153,6 +2302,7 @@ static Cg2Args cg2p_args(const Op2DDev& op, CoefDev k, double a, const double* r
     A.U2 = t;
   }
   A.px = ucur >= 0 ? 1 : 0;
+  A.defer = op.p1 == 8 ? 1 : 0;
   return A;
 }
 

@@ -18,11 +18,13 @@ P = int(sys.argv[2]) if len(sys.argv) > 2 else w.p_fine
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 rt = get_runtime()
 rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=0)
+npart = int(os.environ.get("SISDC_PART", "0"))   # > 0: split CG of an R-partition operator
 op = dgsem2d.DGOperator2D(dgsem2d.Mesh2D(0.0, w.length, 0.0, w.length, w.nex, w.ney, P),
-                          dgsem2d.CompressibleEuler2D(w.gamma, w.nu))
+                          dgsem2d.CompressibleEuler2D(w.gamma, w.nu),
+                          partition=dgsem2d.Partition(npart) if npart > 0 else None)
 X, Y = op.mesh.nodes_xy
-u = rt.to_device(w.initial_state(X, Y))
-dt = w.time_step(u.cpu().numpy(), dgsem.compute_delta(w.p_fine))
+u = op.scatter(w.initial_state(X, Y))
+dt = w.time_step(w.initial_state(X, Y), dgsem.compute_delta(w.p_fine))
 a = 0.5 * dt
 c = op.modified_diffusion_matrix(u, a, "si2")
 out = torch.empty_like(u)
