@@ -118,6 +118,11 @@ int  sisdc_ctx_debug_timing(sisdc_ctx* ctx, long long* out, int cap);
 /* Number of kernels this context has launched (host-side counter). */
 int64_t sisdc_ctx_launch_count(const sisdc_ctx* ctx);
 int  sisdc_copy(sisdc_ctx* ctx, double* dst, const double* src, int64_t n);  /* D2D, async */
+/* out = coef4[0] v0 + coef4[1] v1 + coef4[2] v2 + coef4[3] v3 (NULL terms
+ * skipped; coef4 host), async: the vector updates of the non-incremental
+ * sweep (sdc.py:245-284). */
+int  sisdc_lincomb(sisdc_ctx* ctx, int64_t n, const double* coef4, const double* v0, const double* v1,
+                   const double* v2, const double* v3, double* out);
 
 /* ------------------------------------------------------ DG operator */
 int  sisdc_op1d_create(sisdc_ctx* ctx, const sisdc_op1d_desc* desc, sisdc_op1d** out);

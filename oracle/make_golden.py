@@ -35,7 +35,7 @@ def ref_problem(w):
     return rp.Burgers(w.params["nu"])
 
 
-def build_ref_hier(w):
+def build_ref_hier(w, form="incremental"):
     ops = [rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, w.n_elem, P), ref_problem(w))
            for P in (w.p_coarse, w.p_fine)]
     rules = [rc.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
@@ -44,7 +44,7 @@ def build_ref_hier(w):
     pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_only")
     spat = rt.build_spatial_p_transfer(w.p_coarse, w.p_fine, w.n_elem, 1, "embedded")
     return rm.Hierarchy(levels, [rt.SpaceTimeTransfer(pair, spat)], n_coarse=2, n_sweep=1,
-                        form="incremental", post_sweep_on_finest=True), ops
+                        form=form, post_sweep_on_finest=True), ops
 
 
 class PcgPatch:
@@ -192,10 +192,39 @@ def gen_trajectories():
     np.savez_compressed(os.path.join(OUT, "trajectories.npz"), **out)
 
 
+def gen_nonincremental():
+    """The reference's non-incremental sweep form (sdc.py:245-284): single-level
+    run_sdc (predictor + 2 sweeps, si2 and si1) and one MLSDC step with the
+    non-incremental hierarchy (mlsdc.py:68-101 form branches), SuperLU as
+    shipped and with the pinned PCG (iteration counts)."""
+    out = {}
+    for tag, w in (("cfg1", CFG1), ("cfg2", CFG2)):
+        opf = rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine), ref_problem(w))
+        u0 = w.initial_state(opf.mesh.ref_nodes)
+        dt, _ = w.time_step(u0, rd.compute_delta(w.p_fine))
+        rule = rc.make_nodes("radau_right", w.m_fine)
+        wts = rc.make_weights(rule)
+        for scheme in ("si2", "si1"):
+            sol = rs.run_sdc(opf, rule, wts, dt, scheme, u0, 0.0, 2, form="nonincremental")
+            out[f"{tag}_ni_{scheme}_u"], out[f"{tag}_ni_{scheme}_f"] = sol.u, sol.f
+            out[f"{tag}_ni_{scheme}_h1"] = sol.h1
+        hier, _ = build_ref_hier(w, "nonincremental")
+        out[f"{tag}_ni_mlsdc_lu_u1"] = rm.run_mlsdc(hier, u0, 0.0, dt, w.n_cycles, strategy="fmg").end_value.copy()
+        hier, _ = build_ref_hier(w, "nonincremental")
+        with PcgPatch(1e-14, pcg) as pp:
+            out[f"{tag}_ni_mlsdc_pcg_u1"] = rm.run_mlsdc(hier, u0, 0.0, dt, w.n_cycles, strategy="fmg").end_value.copy()
+            out[f"{tag}_ni_mlsdc_pcg_iters1"] = np.array([it for it, _ in pp.log])
+    np.savez_compressed(os.path.join(OUT, "nonincremental.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "nonincremental":
+        gen_nonincremental()
+        sys.exit(0)
     gen_tables()
     gen_operators()
     gen_trajectories()
+    gen_nonincremental()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -69,6 +69,7 @@ SIGNATURES = {
     "sisdc_ctx_launch_count": (C.c_int64, [P]),
     "sisdc_ctx_debug_timing": (I, [P, C.POINTER(C.c_longlong), I]),
     "sisdc_copy": (I, [P, P, P, C.c_int64]),
+    "sisdc_lincomb": (I, [P, C.c_int64, DP, P, P, P, P, P]),
     "sisdc_op1d_create": (I, [P, C.POINTER(Op1DDesc), C.POINTER(P)]),
     "sisdc_op2d_create": (I, [P, C.POINTER(Op2DDesc), C.POINTER(P)]),
     "sisdc_op1d_destroy": (None, [P]),

@@ -213,6 +213,13 @@ int sisdc_ctx_debug_timing(sisdc_ctx* x, long long* out, int cap) {
 
 int64_t sisdc_ctx_launch_count(const sisdc_ctx* x) { return x ? x->c.launches : -1; }
 
+int sisdc_lincomb(sisdc_ctx* x, int64_t n, const double* coef4, const double* v0, const double* v1,
+                  const double* v2, const double* v3, double* out) {
+  if (!x || !coef4 || !out || n < 0) return SISDC_ERR_ARG;
+  const double* v[4] = {v0, v1, v2, v3};
+  return launch_lincomb(&x->c, n, coef4, v, out);
+}
+
 int sisdc_copy(sisdc_ctx* x, double* dst, const double* src, int64_t n) {
   if (!x || n < 0 || (n > 0 && (!dst || !src))) return SISDC_ERR_ARG;
   if (n == 0) return SISDC_OK;

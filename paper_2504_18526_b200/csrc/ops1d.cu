@@ -187,6 +187,24 @@ __global__ void k_defect(int N, DefectArgs a) {
   a.out[(size_t)m * N + gi] = v;
 }
 
+// out = c0 v0 + c1 v1 + c2 v2 + c3 v3 (null vectors skipped), evaluated left to
+// right as ((c0 v0 + c1 v1) + c2 v2) + c3 v3 -- the vector updates of the
+// non-incremental sweep (sdc.py:245-284: running sum S, g differences)
+struct LinArgs {
+  double c[4];
+  const double* v[4];
+  double* out;
+};
+__global__ void k_lincomb(long long n, LinArgs a) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    double acc = a.v[0] ? a.c[0] * a.v[0][t] : 0.0;
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+      if (a.v[k]) acc = acc + a.c[k] * a.v[k][t];
+    a.out[t] = acc;
+  }
+}
+
 // ---------------------------------------------------------- transfers
 // spatial single state: dir 0 interp c->f, 1 project f->c, 2 restrict f->c  (transfer.py:156-163)
 __global__ void k_xfer_spatial(XferDev x, int dir, const double* __restrict__ in, double* __restrict__ out) {
@@ -403,6 +421,16 @@ int launch_defect(Ctx* c, int N, int M, const double* W, double dt, int incremen
   a.u0 = u0; a.u = u; a.f = f; a.add = add; a.out = out;
   k_defect<<<dim3((N + 255) / 256, M), 256, 0, c->stream>>>(N, a);
   return c->after_launch("collocation_defect");
+}
+int launch_lincomb(Ctx* c, long long n, const double* coef, const double* const* v, double* out) {
+  LinArgs a{};
+  for (int k = 0; k < 4; ++k) { a.c[k] = coef[k]; a.v[k] = v[k]; }
+  a.out = out;
+  long long nb = (n + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  if (nb < 1) nb = 1;
+  k_lincomb<<<(unsigned)nb, 256, 0, c->stream>>>(n, a);
+  return c->after_launch("lincomb");
 }
 int launch_xfer_spatial(Ctx* c, const XferDev& x, int dir, const double* in, double* out) {
   int n = x.ne * (dir == 0 ? x.pf : x.pc);

@@ -70,8 +70,8 @@ class Hierarchy:
     def __post_init__(self):
         if len(self.transfers) != len(self.levels) - 1:
             raise ValueError("need exactly one transfer per adjacent level pair")
-        if self.form != "incremental":
-            raise NotImplementedError("the GPU multilevel engine builds the incremental form (reference default)")
+        if self.form not in ("incremental", "nonincremental"):
+            raise ValueError(f"unknown sweep form {self.form!r}")
         if self.presmooth is not None:
             raise NotImplementedError("presmoothing (smooth_start) is next-tier on the GPU path")
         self.fine_sweeps = 0
@@ -100,17 +100,18 @@ def fas_rhs(hier: Hierarchy, i: int, dt: float):
     rr = lower.work("rr", Mc, n_c)
     fr = lower.work("f_fresh", Mc, n_c)
     g = lower.work("g", Mc, n_c)
-    Wf = upper.weights.w_nn
+    inc = 1 if hier.form == "incremental" else 0
+    Wf = upper.weights.w_nn if inc else upper.weights.w_0n
     wa, wp = _lib.darr(Wf)
     rt.check(rt.lib.sisdc_xfer_fas_restrict(
-        st.handle.h, wp, float(dt), 1, upper.sol.u0.data_ptr(), upper.sol.u.data_ptr(), upper.sol.f.data_ptr(),
+        st.handle.h, wp, float(dt), inc, upper.sol.u0.data_ptr(), upper.sol.u.data_ptr(), upper.sol.f.data_ptr(),
         None if upper.g is None else upper.g.data_ptr(), v.data_ptr(), rr.data_ptr()), "fas_restrict")
     lower.v = v
     # coarse defect of v with fresh rhs at the coarse node times (mlsdc.py:68-77)
     rt.check(rt.lib.sisdc_eval_rhs_nodes(lower.ctx.h, Mc, v.data_ptr(), None, fr.data_ptr()), "eval_rhs_nodes")
-    Wc = lower.weights.w_nn
+    Wc = lower.weights.w_nn if inc else lower.weights.w_0n
     wca, wcp = _lib.darr(Wc)
-    rt.check(rt.lib.sisdc_collocation_defect(lower.ctx.h, Mc, wcp, float(dt), 1, lower.u0.data_ptr(), v.data_ptr(),
+    rt.check(rt.lib.sisdc_collocation_defect(lower.ctx.h, Mc, wcp, float(dt), inc, lower.u0.data_ptr(), v.data_ptr(),
                                              fr.data_ptr(), 1.0, rr.data_ptr(), g.data_ptr()), "fas_compose")
     return g
 
@@ -305,7 +306,7 @@ def integrate_mlsdc(hier: Hierarchy, u0_fine, t0: float, dt: float, n_steps: int
 
 def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes: str = "radau_right",
                       n_coarse: int = 2, n_sweep: int = 1, post_sweep_on_finest: bool = True,
-                      restriction: str = None) -> Hierarchy:
+                      restriction: str = None, form: str = "incremental") -> Hierarchy:
     """Hierarchy of p-levels on one mesh as the reference CLI builds it
     (``cli.py:776-815``); ``make_op(degree)`` returns a DGOperator."""
     from .transfer import build_spatial_p_transfer, build_spatial_p_transfer_2d
@@ -324,5 +325,5 @@ def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes:
             spatial = build_spatial_p_transfer(degrees[lo], degrees[hi], ops[lo].mesh.n_elem, ops[lo].ncomp,
                                                restriction=restriction or "transpose")
         transfers.append(SpaceTimeTransfer(pair, spatial))
-    return Hierarchy(levels, transfers, n_coarse=n_coarse, n_sweep=n_sweep, form="incremental",
+    return Hierarchy(levels, transfers, n_coarse=n_coarse, n_sweep=n_sweep, form=form,
                      post_sweep_on_finest=post_sweep_on_finest)

@@ -97,6 +97,16 @@ class Runtime:
         self.bind_stream()
         self.check(self.lib.sisdc_copy(self.h, dst.data_ptr(), src.data_ptr(), dst.numel()), "copy")
 
+    def lincomb(self, out, *terms):
+        """out = sum c_k v_k over up to four (c, v) pairs, on the device."""
+        if not 1 <= len(terms) <= 4:
+            raise ValueError("one to four terms")
+        cs = (C.c_double * 4)(*([float(c) for c, _ in terms] + [0.0] * (4 - len(terms))))
+        vs = [v.data_ptr() for _, v in terms] + [None] * (4 - len(terms))
+        self.bind_stream()
+        self.check(self.lib.sisdc_lincomb(self.h, out.numel(), cs, *vs, out.data_ptr()), "lincomb")
+        return out
+
     # ------------------------------------------------------------- buffers
     def empty(self, *shape):
         return self.torch.empty(*shape, dtype=self.torch.float64, device=self.device)

@@ -168,7 +168,7 @@ def sweep(ctx, rule: CollocationRule, weights: QuadratureWeights, dt: float, sch
           out: Optional[NodalSolution] = None) -> NodalSolution:
     """One correction sweep (``sdc.py:190-242``); returns the next iterate."""
     if form == "nonincremental":
-        return _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g)
+        return _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g, out)
     if form != "incremental":
         raise ValueError(f"unknown sweep form {form!r}")
     rt = _rt(ctx)
@@ -191,8 +191,55 @@ def sweep(ctx, rule: CollocationRule, weights: QuadratureWeights, dt: float, sch
     return new
 
 
-def _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g):
-    raise NotImplementedError("the non-incremental sweep form is next-tier on the GPU path (SURVEY 8f)")
+def _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g, out=None):
+    """Non-incremental correction sweep (``sdc.py:245-284``): every node is
+    built from u0 plus the zero-to-node quadrature Q0[m] = dt w_0n[m] f and
+    the running sum S of the substep differences; the si2 internal stage keeps
+    the node-to-node quadrature (with g differenced).  B = u0 + S is carried
+    as one device vector; the same fused stage / solve / cache kernels as the
+    incremental sweep, plus ``lincomb`` for the S updates."""
+    rt = _rt(ctx)
+    rt.bind_stream()
+    new = out if out is not None else _alloc(ctx, sol.u0, rule.M, scheme, sol.t0)
+    if out is not None:
+        rt.copy(new.u0, sol.u0)
+        new.t0 = sol.t0
+    dts = _dts(rule, dt)
+    s = ctx.scratch()
+    B = rt.empty(sol.u0.numel())
+    rt.copy(B, sol.u0)
+    conv_up, conv_st, tmp = rt.empty(B.numel()), rt.empty(B.numel()), rt.empty(B.numel())
+    for m in range(rule.M):
+        gm = None if g is None else g[m]
+        dtm = dts[m]
+        if dtm == 0.0:
+            _stage(ctx, B, B, 0.0, sol.f, weights.w_0n[m], dt, gm, None, new.u[m], None)
+            _caches(ctx, scheme, new, rule.M, m, 1, dts)
+            continue
+        up = new.u0 if m == 0 else new.u[m - 1]
+        c = _coef(ctx, scheme, up, dtm)
+        if scheme in ("euler", "si1"):
+            _stage(ctx, B, up, dtm, sol.f, weights.w_0n[m], dt, gm, sol.h1[m], s["rhs"], conv_up)
+            _solve(ctx, c, dtm, s["rhs"], new.u[m])
+            _caches(ctx, scheme, new, rule.M, m, 1, dts, conv_up)
+            rt.lincomb(B, (1.0, B), (1.0, new.h1[m]), (-1.0, sol.h1[m]))      # S += h1_new - h1_old
+        elif scheme == "si2":
+            gnn = None
+            if g is not None:
+                gnn = g[m] if m == 0 else rt.lincomb(tmp, (1.0, g[m]), (-1.0, g[m - 1]))
+            _stage(ctx, up, up, dtm, sol.f, weights.w_nn[m], dt, gnn, sol.h1[m], s["rhs"], conv_up)
+            _solve(ctx, c, dtm, s["rhs"], s["stage"])
+            _stage(ctx, B, s["stage"], dtm, sol.f, weights.w_0n[m], dt, gm, sol.h2[m], s["rhs"], conv_st)
+            _solve(ctx, c, dtm, s["rhs"], new.u[m])
+            _caches(ctx, scheme, new, rule.M, m, 1, dts, conv_up)
+            # S += dt_m (conv(stage) + D[C] u_m) - h2_old  (sdc.py:281)
+            rt.check(rt.lib.sisdc_apply_diffusion(ctx.h, c, new.u[m].data_ptr(), 0.0, tmp.data_ptr()),
+                     "apply_diffusion")
+            rt.lincomb(tmp, (1.0, conv_st), (1.0, tmp))
+            rt.lincomb(B, (1.0, B), (dtm, tmp), (-1.0, sol.h2[m]))
+        else:
+            raise ValueError(f"unknown scheme {scheme!r}")
+    return new
 
 
 def collocation_defect(rule, weights, dt, sol: NodalSolution, form: Form = "incremental", ctx=None,

@@ -190,6 +190,33 @@ def test_mlsdc_step_parity(rt, golden, tag, w):
     rt.raise_on_failure()
 
 
+@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2)])
+def test_nonincremental_form_parity(rt, golden, tag, w):
+    """Non-incremental sweep form (sdc.py:245-284) on the GPU: predictor + 2
+    sweeps (si2, si1) and one non-incremental SI-MLSDC step against the
+    reference goldens; the MLSDC step takes the reference-with-PCG iteration
+    sequence."""
+    from paper_2504_18526_b200 import collocation, mlsdc, sdc
+    G, T = golden["nonincremental"], golden["trajectories"]
+    dt, u0 = float(T[f"{tag}_dt"]), T[f"{tag}_u0"]
+    op = gpu_op(w, w.p_fine)
+    rule = collocation.make_nodes("radau_right", w.m_fine)
+    wts = collocation.make_weights(rule)
+    for scheme in ("si2", "si1"):
+        s = sdc.run_sdc(op, rule, wts, dt, scheme, u0, 0.0, 2, form="nonincremental")
+        assert l2rel(s.u, G[f"{tag}_ni_{scheme}_u"]) < 1e-11
+        assert rel(s.h1, G[f"{tag}_ni_{scheme}_h1"]) < 1e-11
+    h = mlsdc.build_p_hierarchy(lambda P: gpu_op(w, P), [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine],
+                                form="nonincremental")
+    n0 = rt.status()[2]
+    sol = mlsdc.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, strategy="fmg")
+    its, _ = new_log_slice(rt, n0)
+    assert its == G[f"{tag}_ni_mlsdc_pcg_iters1"].tolist()
+    assert l2rel(sol.u[-1], G[f"{tag}_ni_mlsdc_pcg_u1"]) < 1e-11
+    assert l2rel(sol.u[-1], G[f"{tag}_ni_mlsdc_lu_u1"]) < 1e-11
+    rt.raise_on_failure()
+
+
 def test_graph_replay_equals_eager(rt, golden):
     from paper_2504_18526_b200 import mlsdc
     w = CFG2

@@ -98,3 +98,26 @@ def test_single_level_sdc(golden):
     # f = eval_rhs(u) amplifies state roundoff by ||D[nu]|| ~ 1e4: looser bound
     for k, tol in (("u", 1e-13), ("f", 1e-10), ("h1", 1e-12), ("h2", 1e-12)):
         assert rel(getattr(s, k), G[f"cfg1_sdc2_{k}"]) < tol
+
+
+@pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2)])
+def test_nonincremental_form(golden, tag, w):
+    """The reference's non-incremental sweep (sdc.py:245-284) and
+    non-incremental MLSDC (mlsdc.py:68-101): single-level predictor + 2 sweeps
+    (si2, si1) and one MLSDC step, LU vs the reference as shipped, PCG vs the
+    reference with the pinned PCG (identical iterations)."""
+    G, T = golden["nonincremental"], golden["trajectories"]
+    dt, u0 = float(T[f"{tag}_dt"]), T[f"{tag}_u0"]
+    op = dg1d.Op1D(w.x_left, w.x_right, w.n_elem, w.p_fine, workloads.make_problem(w), solver="lu")
+    rule = sweeper.Rule("radau_right", w.m_fine)
+    for scheme in ("si2", "si1"):
+        s = sweeper.run_sdc(op, rule, dt, scheme, u0, 0.0, 2, form="nonincremental")
+        assert rel(s.u, G[f"{tag}_ni_{scheme}_u"]) < 1e-12
+        assert rel(s.h1, G[f"{tag}_ni_{scheme}_h1"]) < 1e-12
+    for solver, key in (("lu", "lu"), ("pcg", "pcg")):
+        h, log = workloads.build_hierarchy(w, solver=solver, form="nonincremental")
+        sol = sweeper.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, "fmg")
+        ref = G[f"{tag}_ni_mlsdc_{key}_u1"]
+        assert np.linalg.norm(sol.u[-1] - ref) / np.linalg.norm(ref) < 1e-12
+        if solver == "pcg":
+            assert [it for it, _ in log] == G[f"{tag}_ni_mlsdc_pcg_iters1"].tolist()
