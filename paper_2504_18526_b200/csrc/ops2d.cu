@@ -1471,6 +1471,94 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
   }
 }
 
+// P = 7 (P1 = 8) stage rhs (k2_stage semantics), one warp per element: the
+// convective term of conv_in on the fp64 tensor cores (wpe_conv), Rusanov
+// fluxes from the neighbours' face nodes read directly (no neighbour
+// staging: convection needs only the face traces), the quadrature of f_old
+// and the base / g / h terms per node pair with 16-byte accesses.
+template <int NC>
+struct Stg {                 // per-warp shared region (doubles)
+  static constexpr int RP = 10, NP = 80;
+  static constexpr int OWN = 0;                  // [NC][NP] conv_in element
+  static constexpr int FX = OWN + NC * NP, FY = FX + NP;
+  static constexpr int FH = FY + NP;             // [32][NC] face fluxes
+  static constexpr int WARP = FH + 32 * NC;
+};
+template <int NC>
+__global__ void __launch_bounds__(EV_WARPS * 32) k2_stage8(Op2DDev op, Stage2Args a) {
+  extern __shared__ double sm[];
+  using W = Stg<NC>;
+  constexpr int RP = 10, P = 7;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ws = sm + warp * W::WARP;
+  const long long nn = op.nn;
+  MmaLane K;
+  mma_lane_init(op, K);
+  const int g = lane >> 2, n0 = 2 * (lane & 3);
+  const int f = lane >> 3, k = lane & 7;
+  const int fnode = f == FR ? k * 8 : f == FL ? k * 8 + 7 : f == FT ? k : 56 + k;      // neighbour's face node
+  const int ownf = f == FR ? k * RP + P : f == FL ? k * RP : f == FT ? P * RP + k : k;   // own face node (padded)
+  const int ne = op.nex * op.ney;
+  for (int e = blockIdx.x * EV_WARPS + warp; e < ne; e += gridDim.x * EV_WARPS) {
+    const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
+    const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
+    const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
+    const unsigned eo = ((unsigned)ey * op.nex + ex) * 64u;
+    const unsigned nbf = (f == FR ? ((unsigned)ey * op.nex + exr) : f == FL ? ((unsigned)ey * op.nex + exl)
+                          : f == FT ? ((unsigned)eyt * op.nex + ex) : ((unsigned)eyb * op.nex + ex)) * 64u + fnode;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) cp_async16(ws + W::OWN + c * W::NP + g * RP + n0, a.conv_in + c * nn + eo + 2 * lane);
+    double sn[NC_MAX];
+#pragma unroll
+    for (int c = 0; c < NC_MAX; ++c) sn[c] = c < NC ? a.conv_in[c * nn + nbf] : 1.0;
+    cp_async_wait_all();
+    __syncwarp();
+    {
+      double so[NC_MAX], fh[NC_MAX];
+#pragma unroll
+      for (int c = 0; c < NC_MAX; ++c) so[c] = c < NC ? ws[W::OWN + c * W::NP + ownf] : 1.0;
+      const int axis = f < FT ? 0 : 1;
+      if (f == FR || f == FT) rusanov2d(op, so, sn, axis, fh); else rusanov2d(op, sn, so, axis, fh);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) ws[W::FH + lane * NC + c] = fh[c];
+    }
+    __syncwarp();
+    const long long gi = (long long)eo + g * 8 + n0;
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c) {
+      double cv0, cv1;
+      wpe_conv<NC>(op, K, ws + W::OWN, ws + W::FH, c, ws + W::FX, ws + W::FY, cv0, cv1);
+      const long long gc = c * nn + gi;
+      if (a.conv_out) *reinterpret_cast<double2*>(a.conv_out + gc) = make_double2(cv0, cv1);
+      double q0 = 0.0, q1 = 0.0;
+      if (a.f_old) {
+        double acc0 = 0.0, acc1 = 0.0;
+        for (int jj = 0; jj < a.M; ++jj) {
+          const double2 fo = *reinterpret_cast<const double2*>(a.f_old + (size_t)jj * op.ns + gc);
+          acc0 = fma(a.w[jj], fo.x, acc0);
+          acc1 = fma(a.w[jj], fo.y, acc1);
+        }
+        q0 = a.dt * acc0;
+        q1 = a.dt * acc1;
+      }
+      if (a.g) {
+        const double2 gv = *reinterpret_cast<const double2*>(a.g + gc);
+        q0 = q0 + gv.x;
+        q1 = q1 + gv.y;
+      }
+      const double2 bv = *reinterpret_cast<const double2*>(a.base + gc);
+      double r0 = (bv.x + q0) + a.dt_m * cv0, r1 = (bv.y + q1) + a.dt_m * cv1;
+      if (a.h) {
+        const double2 hv = *reinterpret_cast<const double2*>(a.h + gc);
+        r0 = r0 - hv.x;
+        r1 = r1 - hv.y;
+      }
+      *reinterpret_cast<double2*>(a.rhs + gc) = make_double2(r0, r1);
+    }
+    __syncwarp();   // the next element overwrites the staged data
+  }
+}
+
 template <int P1, int NC>
 __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   extern __shared__ double sm[];
@@ -2184,6 +2272,22 @@ int launch2_stage(Ctx* c, const Op2DDev& op, const double* base, const double* c
   a.base = base; a.conv_in = conv_in; a.dt_m = dt_m; a.f_old = f_old; a.M = M; a.dt = dt;
   for (int j = 0; j < M; ++j) a.w[j] = (f_old && w_row) ? w_row[j] : 0.0;
   a.g = g; a.h = h; a.rhs = rhs; a.conv_out = conv_out;
+  const bool al16 = ((reinterpret_cast<uintptr_t>(base) | reinterpret_cast<uintptr_t>(conv_in) |
+                      reinterpret_cast<uintptr_t>(f_old) | reinterpret_cast<uintptr_t>(g) |
+                      reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(rhs) |
+                      reinterpret_cast<uintptr_t>(conv_out)) & 15) == 0;
+  if (op.p1 == 8 && op.nc == 4 && al16) {   // tensor-core warp-per-element path
+    const size_t smem = sizeof(double) * EV_WARPS * Stg<4>::WARP;
+    const int ne = op.nex * op.ney;
+    int nb = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2_stage8<4>, EV_WARPS * 32, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    long long gx = (long long)(nb > 0 ? nb : 1) * sms * 4;
+    const long long need = (ne + EV_WARPS - 1) / EV_WARPS;
+    if (gx > need) gx = need;
+    k2_stage8<4><<<(unsigned)gx, EV_WARPS * 32, smem, c->stream>>>(op, a);
+    return c->after_launch("k2_stage8");
+  }
   SISDC_P1_SWITCH(op.p1, {
     set_smem<P1>(k2_stage<P1>);
     k2_stage<P1><<<grid2<P1>(op), Blk<P1>::NT, smem2<P1>(), c->stream>>>(op, a);
