@@ -30,8 +30,9 @@ class ConvDiff:
     ncomp = 1
     linear = True
 
-    def __init__(self, speed=1.0, nu=0.0):
+    def __init__(self, speed=1.0, nu=0.0, boundary=None):
         self.v, self.nu = float(speed), float(nu)
+        self.boundary = boundary
 
     def flux(self, u):
         return self.v * u
@@ -51,8 +52,9 @@ class Burgers:
     ncomp = 1
     linear = False
 
-    def __init__(self, nu=0.0):
+    def __init__(self, nu=0.0, boundary=None):
         self.nu = float(nu)
+        self.boundary = boundary   # t -> (left state, right state), problems.py:66
 
     def flux(self, u):
         return 0.5 * u * u
@@ -137,11 +139,14 @@ def kind_of(c):
 
 # ---------------------------------------------------------------- operator
 class Op1D:
-    """Oracle DG operator on a uniform periodic 1-D mesh
-    (``dgsem.py:117-151``; periodic faces ``:179-201``)."""
+    """Oracle DG operator on a uniform 1-D mesh (``dgsem.py:117-151``),
+    periodic or Dirichlet faces (``:179-201``): with ``bc="dirichlet"`` the
+    outer faces take the problem's boundary states g(t) on the outside, the
+    one-sided interior flux q and coefficient, and face weight 1 in the
+    adjoint lift; the diffusion operator is then affine in u."""
 
     def __init__(self, x_left, x_right, n_elem, degree, problem, penalty=2.0,
-                 solver="pcg", rtol=1e-14, maxit=1000, av=None, cg_log=None):
+                 solver="pcg", rtol=1e-14, maxit=1000, av=None, cg_log=None, bc="periodic"):
         self.xl, self.xr = float(x_left), float(x_right)
         self.ne, self.P = int(n_elem), int(degree)
         self.p1 = self.P + 1
@@ -162,6 +167,15 @@ class Op1D:
         self._last_dt = None
         V = np.stack([quad._leg(k, self.xi)[0] for k in range(self.p1)], axis=1)
         self._vinv = np.linalg.inv(V)
+        if bc not in ("periodic", "dirichlet"):
+            raise ValueError(bc)
+        if bc == "dirichlet" and getattr(problem, "boundary", None) is None:
+            raise ValueError("dirichlet mesh needs a problem with boundary_state(t)")   # dgsem.py:150-151
+        self.bc = bc
+
+    def _bstate(self, t):
+        gl, gr = self.prob.boundary(t)
+        return np.asarray(gl, dtype=float).reshape(self.nc), np.asarray(gr, dtype=float).reshape(self.nc)
 
     # layout -------------------------------------------------------------
     def u3(self, u):
@@ -193,8 +207,19 @@ class Op1D:
                          self.prob.speed(up[:, :, None])[..., 0])
         fh = 0.5 * (self.prob.flux(um[:, :, None])[..., 0] + self.prob.flux(up[:, :, None])[..., 0]) \
             - 0.5 * lam[None] * (up - um)
-        out[:, :, -1] -= fh
-        out[:, :, 0] += np.roll(fh, 1, axis=-1)
+        if self.bc == "periodic":
+            out[:, :, -1] -= fh
+            out[:, :, 0] += np.roll(fh, 1, axis=-1)
+            return (out / self.mass).reshape(-1)
+        # Dirichlet (dgsem.py:212-216): faces 0..ne, outside states g_l(t), g_r(t)
+        gl, gr = self._bstate(t)
+        um_f = np.concatenate([gl[:, None], u3[:, :, -1]], axis=1)
+        up_f = np.concatenate([u3[:, :, 0], gr[:, None]], axis=1)
+        lam = np.maximum(self.prob.speed(um_f[:, :, None])[..., 0], self.prob.speed(up_f[:, :, None])[..., 0])
+        fh = 0.5 * (self.prob.flux(um_f[:, :, None])[..., 0] + self.prob.flux(up_f[:, :, None])[..., 0]) \
+            - 0.5 * lam[None] * (up_f - um_f)
+        out[:, :, -1] -= fh[:, 1:]
+        out[:, :, 0] += fh[:, :-1]
         return (out / self.mass).reshape(-1)
 
     # diffusion (dgsem.py:251-309) ---------------------------------------
@@ -232,11 +257,33 @@ class Op1D:
             lm = 0.5 * Cm[None] * jump
             lp = 0.5 * Cp[None] * jump
         G = pen - 0.5 * (qm + qp)
-        B[:, :, -1] += G
-        B[:, :, 0] -= np.roll(G, 1, axis=-1)
-        # adjoint lift with each side's own coefficient (dgsem.py:296-308)
-        B -= s * lm[:, :, None] * self.D[-1][None, None, :]
-        B -= s * np.roll(lp, 1, axis=-1)[:, :, None] * self.D[0][None, None, :]
+        if self.bc == "periodic":
+            B[:, :, -1] += G
+            B[:, :, 0] -= np.roll(G, 1, axis=-1)
+            # adjoint lift with each side's own coefficient (dgsem.py:296-308)
+            B -= s * lm[:, :, None] * self.D[-1][None, None, :]
+            B -= s * np.roll(lp, 1, axis=-1)[:, :, None] * self.D[0][None, None, :]
+            return (-B / self.mass).reshape(-1)
+        if k == "matrix":
+            raise NotImplementedError("Dirichlet faces with matrix coefficients")
+        # Dirichlet (dgsem.py:282-308): faces 0..ne; outside states g(t), q and C
+        # one-sided at the outer faces, adjoint-lift weight 1 there
+        gl, gr = self._bstate(t)
+        uf_m = np.concatenate([gl[:, None], u3[:, :, -1]], axis=1)
+        uf_p = np.concatenate([u3[:, :, 0], gr[:, None]], axis=1)
+        qf_m = np.concatenate([q[:, :1, 0], q[:, :, -1]], axis=1)
+        qf_p = np.concatenate([q[:, :, 0], q[:, -1:, -1]], axis=1)
+        cf_m = np.concatenate([C[:1, 0], C[:, -1]])
+        cf_p = np.concatenate([C[:, 0], C[-1:, -1]])
+        wf = np.full(self.ne + 1, 0.5)
+        wf[0] = wf[-1] = 1.0
+        jump = uf_m - uf_p
+        pen = self.mu0 * (0.5 * (cf_m + cf_p))[None] * jump
+        Gf = -0.5 * (qf_m + qf_p) + pen
+        B[:, :, -1] += Gf[:, 1:]
+        B[:, :, 0] -= Gf[:, :-1]
+        B -= s * ((wf * cf_m)[None] * jump)[:, 1:, None] * self.D[-1][None, None, :]
+        B -= s * ((wf * cf_p)[None] * jump)[:, :-1, None] * self.D[0][None, None, :]
         return (-B / self.mass).reshape(-1)
 
     # rhs (dgsem.py:313-352) ---------------------------------------------
@@ -317,7 +364,7 @@ class Op1D:
         cols = [np.broadcast_to(gid.transpose(1, 0, 2)[:, None, None, :, :], V.shape).ravel()]
         vals = [V.ravel()]
         # face between eL=e and eR=e+1: local ordering [a, eL node] + [a, eR node]
-        eL = np.arange(ne)
+        eL = np.arange(ne) if self.bc == "periodic" else np.arange(ne - 1)
         eR = (eL + 1) % ne
         CL, CR = C[eL, -1], C[eR, 0]                     # (ne, nc, nc)
         npair = 2 * nc * p1
@@ -325,8 +372,8 @@ class Op1D:
         for a in range(nc):
             J[a, a * p1 + p1 - 1] = 1.0
             J[a, nc * p1 + a * p1] = -1.0
-        Q = np.zeros((ne, nc, npair))
-        QT = np.zeros((ne, nc, npair))
+        Q = np.zeros((len(eL), nc, npair))
+        QT = np.zeros((len(eL), nc, npair))
         for b in range(nc):
             Q[:, :, b * p1:(b + 1) * p1] = 0.5 * s * CL[:, :, b, None] * D[-1][None, None, :]
             Q[:, :, nc * p1 + b * p1:nc * p1 + (b + 1) * p1] = 0.5 * s * CR[:, :, b, None] * D[0][None, None, :]
@@ -335,11 +382,28 @@ class Op1D:
         muC = self.mu0 * 0.5 * (CL + CR)
         blk = -(np.einsum("ai,eaj->eij", J, Q) + np.einsum("eai,aj->eij", QT, J)) \
             + np.einsum("ai,eab,bj->eij", J, muC, J)
-        ids = np.concatenate([gid[:, eL, :].transpose(1, 0, 2).reshape(ne, -1),
-                              gid[:, eR, :].transpose(1, 0, 2).reshape(ne, -1)], axis=1)
+        nfc = len(eL)
+        ids = np.concatenate([gid[:, eL, :].transpose(1, 0, 2).reshape(nfc, -1),
+                              gid[:, eR, :].transpose(1, 0, 2).reshape(nfc, -1)], axis=1)
         rows.append(np.repeat(ids, npair, axis=1).ravel())
         cols.append(np.tile(ids, (1, npair)).ravel())
         vals.append(blk.ravel())
+        if self.bc == "dirichlet":   # outer faces, one-sided (dgsem.py:460-481)
+            nh = nc * p1
+            for e, Cb, drow, sgn, endpos in ((0, C[0, 0], D[0], -1.0, 0), (ne - 1, C[ne - 1, -1], D[-1], 1.0, p1 - 1)):
+                Jb = np.zeros((nc, nh))
+                Qb = np.zeros((nc, nh))
+                QTb = np.zeros((nc, nh))
+                for a in range(nc):
+                    Jb[a, a * p1 + endpos] = sgn
+                    for b2 in range(nc):
+                        Qb[a, b2 * p1:(b2 + 1) * p1] = s * Cb[a, b2] * drow
+                        QTb[a, b2 * p1:(b2 + 1) * p1] = s * Cb[b2, a] * drow
+                blkb = -(Jb.T @ Qb + QTb.T @ Jb) + Jb.T @ (self.mu0 * Cb) @ Jb
+                idb = gid[:, e, :].ravel()
+                rows.append(np.repeat(idb, nh))
+                cols.append(np.tile(idb, nh))
+                vals.append(blkb.ravel())
         B = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                           shape=(self.n, self.n))
         return B.tocsc()
@@ -355,8 +419,14 @@ class Op1D:
         Cm = C[:, -1]
         Cp = np.roll(C, -1, axis=0)[:, 0]
         muC = self.mu0 * 0.5 * (Cm + Cp)                # face e+1/2
-        d[:, -1] += muC - s * Cm * self.D[-1, -1]
-        d[:, 0] += np.roll(muC + s * Cp * self.D[0, 0], 1)
+        if self.bc == "periodic":
+            d[:, -1] += muC - s * Cm * self.D[-1, -1]
+            d[:, 0] += np.roll(muC + s * Cp * self.D[0, 0], 1)
+        else:   # interior faces, then the outer faces with weight 1 (dgsem.py:460-481)
+            d[:-1, -1] += (muC - s * Cm * self.D[-1, -1])[:-1]
+            d[1:, 0] += (muC + s * Cp * self.D[0, 0])[:-1]
+            d[0, 0] += self.mu0 * C[0, 0] + 2.0 * s * C[0, 0] * self.D[0, 0]
+            d[-1, -1] += self.mu0 * C[-1, -1] - 2.0 * s * C[-1, -1] * self.D[-1, -1]
         return np.tile(d.reshape(-1), self.nc)
 
     # implicit solve (dgsem.py:503-533) ----------------------------------
@@ -371,9 +441,18 @@ class Op1D:
             return self._solve_lu(coeff, a, b, t).reshape(rhs.shape)
         diag = self.mflat + a * self.stiffness_diag(coeff)
         m = self.mflat
+        if self.bc == "dirichlet":
+            # affine SIP: D(x; t) = D_lin(x) + d_bc(t), d_bc = D(0; t).  Solve the
+            # linear system (M + a B_lin) x = M rhs + a M d_bc (the solution of the
+            # reference's defect iteration, dgsem.py:517-529)
+            dbc = self.apply_diffusion(coeff, np.zeros(self.n), t)
+            b = b + a * m * dbc
 
-        def A(x):
-            return m * x - a * m * self.apply_diffusion(coeff, x, t)
+            def A(x):
+                return m * x - a * m * (self.apply_diffusion(coeff, x, t) - dbc)
+        else:
+            def A(x):
+                return m * x - a * m * self.apply_diffusion(coeff, x, t)
 
         x, it, margin = pcg(A, diag, b, rhs.reshape(-1).copy(), self.rtol, self.maxit)
         if it < 0:
@@ -392,7 +471,7 @@ class Op1D:
         x = ent[0].solve(b)
         same = (np.isscalar(coeff) and np.isscalar(ent[1]) and float(coeff) == float(ent[1])) \
             or coeff is ent[1]
-        if same:
+        if same and self.bc == "periodic":
             return x
         bn = np.linalg.norm(b)
         m = self.mflat

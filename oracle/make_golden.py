@@ -69,7 +69,12 @@ class PcgPatch:
                 return np.zeros_like(rhs)
             Amat = op.assemble_implicit(coeff, a)
             diag = np.asarray(Amat.diagonal())
-            A = lambda x: m * x - a * m * op.apply_diffusion(coeff, x, t)
+            if op.mesh.bc == "dirichlet":   # affine SIP: linear part + boundary data on the rhs
+                dbc = op.apply_diffusion(coeff, np.zeros(op.ndof), t)
+                b = b + a * m * dbc
+                A = lambda x: m * x - a * m * (op.apply_diffusion(coeff, x, t) - dbc)
+            else:
+                A = lambda x: m * x - a * m * op.apply_diffusion(coeff, x, t)
             x, it, margin = patch.solver(A, diag, b, rhs.reshape(-1).copy(), patch.rtol, 1000)
             assert it >= 0
             patch.log.append((it, margin))
@@ -217,14 +222,92 @@ def gen_nonincremental():
     np.savez_compressed(os.path.join(OUT, "nonincremental.npz"), **out)
 
 
+# Dirichlet workload: the paper's Burgers moving front (problems.py:284-291,
+# PAPER.md "Burgers moving front"): nu = 1e-2 on [-1, 1], exact-front trace data
+DIRICHLET = dict(nu=1e-2, n_elem=20, p_fine=8, p_coarse=4, m_fine=5, m_coarse=3, cfl=1.0, t0=0.0)
+AV_CASE = dict(n_elem=16, p_fine=4, p_coarse=2)
+
+
+def dirichlet_ref(av=None, form="incremental", **over):
+    d = {**DIRICHLET, **over}
+    prob, exact = rp.burgers_front_problem(d["nu"])
+    ops = [rd.DGOperator(rd.Mesh1D(-1.0, 1.0, d["n_elem"], p, bc="dirichlet"), prob, av=av)
+           for p in (d["p_coarse"], d["p_fine"])]
+    rules = [rc.make_nodes("radau_right", M) for M in (d["m_coarse"], d["m_fine"])]
+    wts = [rc.make_weights(r) for r in rules]
+    levels = [rm.Level(o, r, ww, "si2") for o, r, ww in zip(ops, rules, wts)]
+    pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_only")
+    spat = rt.build_spatial_p_transfer(d["p_coarse"], d["p_fine"], d["n_elem"], 1, "embedded")
+    hier = rm.Hierarchy(levels, [rt.SpaceTimeTransfer(pair, spat)], n_coarse=2, n_sweep=1, form=form,
+                        post_sweep_on_finest=True)
+    return hier, ops, exact
+
+
+def gen_dirichlet():
+    """Dirichlet faces with time-dependent trace data (dgsem.py:179-201,212-216,
+    282-289, assembly :460-481): operators at two times, implicit solves, a
+    single-level SDC slab and two SI-MLSDC steps (SuperLU as shipped; with the
+    pinned PCG: iteration counts), plus one step with Persson-Peraire AV."""
+    d = DIRICHLET
+    out = {}
+    hier, ops, exact = dirichlet_ref()
+    fine = ops[1]
+    x = fine.mesh.nodes_x
+    u0 = fine.flat(exact(x, d["t0"])[None])
+    lam = float(np.abs(u0).max())
+    dt = rd.dt_from_cfl(d["cfl"], fine.mesh.dx, lam, d["p_fine"])
+    out["u0"], out["dt"] = u0, np.array(dt)
+    rng = np.random.default_rng(11)
+    us = u0 + 1e-3 * rng.standard_normal(u0.shape)
+    out["us"] = us
+    for j, t in enumerate((0.013, 0.071)):
+        out[f"t{j}"] = np.array(t)
+        out[f"conv{j}"] = fine.apply_convection(us, t)
+        C = fine.modified_diffusion_matrix(us, 0.4 * dt, "si2")
+        out[f"coef{j}"] = np.asarray(C)
+        out[f"diff{j}"] = fine.apply_diffusion(C, us, t)
+        out[f"rhs{j}"] = fine.eval_rhs(us, t)
+        out[f"solve{j}"] = fine.implicit_solve(C, 0.4 * dt, us, t)
+    rule = rc.make_nodes("radau_right", d["m_fine"])
+    sol = rs.run_sdc(fine, rule, rc.make_weights(rule), dt, "si2", u0, d["t0"], 2)
+    out["sdc2_u"], out["sdc2_h1"] = sol.u, sol.h1
+    u = u0
+    for step in range(2):
+        u = rm.run_mlsdc(hier, u, d["t0"] + step * dt, dt, 3, strategy="fmg").end_value.copy()
+        out[f"mlsdc_lu_u{step + 1}"] = u
+    hier, ops, _ = dirichlet_ref()
+    with PcgPatch(1e-14, pcg) as pp:
+        u = u0
+        for step in range(2):
+            n0 = len(pp.log)
+            u = rm.run_mlsdc(hier, u, d["t0"] + step * dt, dt, 3, strategy="fmg").end_value.copy()
+            out[f"mlsdc_pcg_u{step + 1}"] = u
+            out[f"mlsdc_pcg_iters{step + 1}"] = np.array([it for it, _ in pp.log[n0:]])
+    # under-resolved front (16 elements, P 4/2) with the Persson-Peraire viscosity
+    # (PAPER.md: kappa_s = c_s = 0.5), frozen per slab by begin_slab
+    hier, ops, _ = dirichlet_ref(av=rd.ArtificialViscosityParams(0.5, 0.5), **AV_CASE)
+    ua = ops[1].flat(exact(ops[1].mesh.nodes_x, d["t0"])[None])
+    dta = rd.dt_from_cfl(d["cfl"], ops[1].mesh.dx, float(np.abs(ua).max()), AV_CASE["p_fine"])
+    out["av_u0"], out["av_dt"] = ua, np.array(dta)
+    out["av_nu_art"] = ops[1].persson_viscosity(ua)
+    with PcgPatch(1e-14, pcg) as pp:
+        out["av_mlsdc_pcg_u1"] = rm.run_mlsdc(hier, ua, d["t0"], dta, 3, strategy="fmg").end_value.copy()
+        out["av_mlsdc_pcg_iters1"] = np.array([it for it, _ in pp.log])
+    np.savez_compressed(os.path.join(OUT, "dirichlet.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     if len(sys.argv) > 1 and sys.argv[1] == "nonincremental":
         gen_nonincremental()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "dirichlet":
+        gen_dirichlet()
+        sys.exit(0)
     gen_tables()
     gen_operators()
     gen_trajectories()
     gen_nonincremental()
+    gen_dirichlet()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -179,3 +179,37 @@ CFG3 = Workload2D("cfg3_euler_vortex_128x128_P7", "vortex", 128, 128, 7, 3, 4, 2
 CFG4 = Workload2D("cfg4_ns_shear_256x256_P7", "shear", 256, 256, 7, 3, 5, 3, TWO_PI, seed=4, nu=1e-4)
 CFG5 = Workload2D("cfg5_ns_shear_1024x1024_P7", "shear", 1024, 1024, 7, 3, 5, 3, TWO_PI, seed=5, nu=1e-4)
 WORKLOADS.update({"cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5})
+
+
+# ------------------------------------------------ Dirichlet front
+def burgers_front_exact(nu):
+    """u = 1 - tanh((x + 1/2 - t) / (2 nu)) (``problems.py:268-277``)."""
+    def exact(x, t=0.0):
+        return 1.0 - np.tanh((np.asarray(x) + 0.5 - t) / (2.0 * nu))
+    return exact
+
+
+def burgers_front_boundary(nu):
+    """Trace data of the exact front at x = -1, 1 (``problems.py:280-291``)."""
+    ex = burgers_front_exact(nu)
+    return lambda t: (np.array([ex(-1.0, t)]), np.array([ex(1.0, t)]))
+
+
+@dataclass(frozen=True)
+class FrontWorkload:
+    """The paper's Burgers moving front on [-1, 1] with time-dependent
+    Dirichlet data (PAPER.md "Burgers moving front"); the parity workload of
+    the Dirichlet faces (oracle/make_golden.py ``DIRICHLET`` / ``AV_CASE``)."""
+    nu: float = 1e-2
+    n_elem: int = 20
+    p_fine: int = 8
+    p_coarse: int = 4
+    m_fine: int = 5
+    m_coarse: int = 3
+    cfl: float = 1.0
+    n_cycles: int = 3
+    av: tuple = None          # (kappa_s, c_s) or None
+
+
+FRONT = FrontWorkload()
+FRONT_AV = FrontWorkload(n_elem=16, p_fine=4, p_coarse=2, av=(0.5, 0.5))

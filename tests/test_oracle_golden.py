@@ -121,3 +121,57 @@ def test_nonincremental_form(golden, tag, w):
         assert np.linalg.norm(sol.u[-1] - ref) / np.linalg.norm(ref) < 1e-12
         if solver == "pcg":
             assert [it for it, _ in log] == G[f"{tag}_ni_mlsdc_pcg_iters1"].tolist()
+
+
+# ------------------------------------------------ Dirichlet faces (moving front)
+def _front_oracle(w, solver, log=None):
+    from paper_2504_18526_b200.configs import burgers_front_boundary
+    bnd = burgers_front_boundary(w.nu)
+
+    def mk(lvl):
+        P = w.p_coarse if lvl == "coarse" else w.p_fine
+        return dg1d.Op1D(-1.0, 1.0, w.n_elem, P, dg1d.Burgers(w.nu, boundary=bnd), solver=solver,
+                         bc="dirichlet", av=w.av, cg_log=log)
+    return mk
+
+
+def test_dirichlet_front(golden):
+    """Dirichlet faces with time-dependent trace data vs the reference
+    (burgers_front_problem): operators at two times, implicit solves (LU and
+    the pinned PCG on the affine system), single-level SDC, two SI-MLSDC
+    steps (PCG: identical iteration sequence), and the AV case."""
+    from paper_2504_18526_b200.configs import FRONT, FRONT_AV
+    G = golden["dirichlet"]
+    w = FRONT
+    op = _front_oracle(w, "lu")("fine")
+    dt, us = float(G["dt"]), G["us"]
+    for j in (0, 1):
+        t = float(G[f"t{j}"])
+        assert rel(op.apply_convection(us, t), G[f"conv{j}"]) < 1e-13
+        C = op.modified_coeff(us, 0.4 * dt)
+        assert rel(C, G[f"coef{j}"]) < 1e-15
+        assert rel(op.apply_diffusion(C, us, t), G[f"diff{j}"]) < 1e-13
+        assert rel(op.eval_rhs(us, t), G[f"rhs{j}"]) < 1e-13
+        assert rel(op.implicit_solve(C, 0.4 * dt, us, t), G[f"solve{j}"]) < 1e-12
+        opc = _front_oracle(w, "pcg")("fine")
+        assert rel(opc.implicit_solve(C, 0.4 * dt, us, t), G[f"solve{j}"]) < 1e-11
+    rule = sweeper.Rule("radau_right", w.m_fine)
+    s = sweeper.run_sdc(op, rule, dt, "si2", G["u0"], 0.0, 2)
+    assert rel(s.u, G["sdc2_u"]) < 1e-12 and rel(s.h1, G["sdc2_h1"]) < 1e-11
+    log = []
+    mk = _front_oracle(w, "pcg", log)
+    h = sweeper.build_two_level(mk, sweeper.Rule("radau_right", w.m_coarse), rule)
+    u = G["u0"]
+    for step in (1, 2):
+        n0 = len(log)
+        u = sweeper.run_mlsdc(h, u, (step - 1) * dt, dt, w.n_cycles, "fmg").u[-1]
+        assert [it for it, _ in log[n0:]] == G[f"mlsdc_pcg_iters{step}"].tolist()
+        assert np.linalg.norm(u - G[f"mlsdc_pcg_u{step}"]) / np.linalg.norm(G[f"mlsdc_pcg_u{step}"]) < 1e-12
+    wa = FRONT_AV
+    log = []
+    mk = _front_oracle(wa, "pcg", log)
+    h = sweeper.build_two_level(mk, sweeper.Rule("radau_right", wa.m_coarse), sweeper.Rule("radau_right", wa.m_fine))
+    assert rel(h.levels[1].ctx.persson_viscosity(G["av_u0"]), G["av_nu_art"]) < 1e-13
+    u = sweeper.run_mlsdc(h, G["av_u0"], 0.0, float(G["av_dt"]), wa.n_cycles, "fmg").u[-1]
+    assert [it for it, _ in log] == G["av_mlsdc_pcg_iters1"].tolist()
+    assert np.linalg.norm(u - G["av_mlsdc_pcg_u1"]) / np.linalg.norm(G["av_mlsdc_pcg_u1"]) < 1e-12
