@@ -45,7 +45,7 @@ enum sisdc_problem {
   SISDC_EULER2D = 2,                            /* 2-D Euler / NS (isotropic viscosity)  */
   SISDC_ADVECTION2D = 3, SISDC_BURGERS2D = 4    /* 2-D scalar (cross-dimension checks)   */
 };
-enum sisdc_bc { SISDC_PERIODIC = 0 };                            /* Mesh1D.bc         */
+enum sisdc_bc { SISDC_PERIODIC = 0, SISDC_DIRICHLET = 1 };       /* Mesh1D.bc         */
 enum sisdc_scheme { SISDC_EULER = 0, SISDC_SI1 = 1, SISDC_SI2 = 2 }; /* integrators.py:26 */
 
 /* Coefficient descriptor: the reference's opaque coefficient object
@@ -69,7 +69,7 @@ typedef struct {
   int n_elem;
   int degree;        /* P, 1..15                         */
   int ncomp;         /* 1 for the scalar problems         */
-  int bc;            /* SISDC_PERIODIC                    */
+  int bc;            /* SISDC_PERIODIC / SISDC_DIRICHLET  */
   int problem;       /* sisdc_problem                     */
   double x_left, x_right;
   double speed;      /* ConvectionDiffusion.speed         */
@@ -134,6 +134,12 @@ int  sisdc_op1d_tables(const sisdc_op1d* op, double* nodes, double* weights, dou
 /* Per-element artificial viscosity nu_art (device, n_elem) or NULL
  * (DGOperator.nu_art, frozen per slab by begin_slab, dgsem.py:563-571). */
 int  sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art);
+/* Dirichlet trace data (problem.boundary_state(t), dgsem.py:212-216,282-284):
+ * register the outside states g_l(t_j), g_r(t_j) for n times (merged into the
+ * operator's table).  Every entry point that takes a time t (or node times)
+ * on a Dirichlet operator looks its data up here and fails with
+ * SISDC_ERR_ARG for an unregistered time. */
+int  sisdc_op1d_set_boundary(sisdc_op1d* op, int n, const double* times, const double* gl, const double* gr);
 /* Persson-Peraire modal sensor (dgsem.py:537-559) -> nu_art (device, n_elem). */
 int  sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, double c_s, double* nu_art);
 

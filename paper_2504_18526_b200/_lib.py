@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libsisdc_b200.so")
 
 OK, ERR_ARG, ERR_CUDA, ERR_NONFINITE, ERR_NOCONV, ERR_UNSUPPORTED = range(6)
 CONVDIFF, BURGERS, EULER2D, ADVECTION2D, BURGERS2D = 0, 1, 2, 3, 4
-PERIODIC = 0
+PERIODIC, DIRICHLET = 0, 1
 SCHEMES = {"euler": 0, "si1": 1, "si2": 2}
 COEF_NONE, COEF_CONST, COEF_FIELD, COEF_SI, COEF_PHYS = range(5)
 
@@ -75,6 +75,7 @@ SIGNATURES = {
     "sisdc_op1d_destroy": (None, [P]),
     "sisdc_op1d_tables": (I, [P, DP, DP, DP]),
     "sisdc_op1d_set_nu_art": (I, [P, P]),
+    "sisdc_op1d_set_boundary": (I, [P, I, DP, DP, DP]),
     "sisdc_persson_viscosity": (I, [P, P, D, D, P]),
     "sisdc_apply_convection": (I, [P, P, D, P]),
     "sisdc_apply_diffusion": (I, [P, Coef, P, D, P]),

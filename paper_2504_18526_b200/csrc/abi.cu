@@ -94,6 +94,20 @@ bool invert(std::vector<double> A, int n, std::vector<double>& inv) {
   return true;
 }
 
+// Dirichlet trace data of time t from the operator's table (exact match)
+int bc_at(sisdc_op1d* op, double t, double& gl, double& gr) {
+  gl = gr = 0.0;
+  if (op->dim != 1 || op->dev.bc != SISDC_DIRICHLET) return SISDC_OK;
+  for (size_t j = 0; j + 2 < op->btab.size(); j += 3)
+    if (op->btab[j] == t) { gl = op->btab[j + 1]; gr = op->btab[j + 2]; return SISDC_OK; }
+  return C(op)->fail(SISDC_ERR_ARG, "no Dirichlet boundary data registered for t = " + std::to_string(t));
+}
+// the operator with its boundary states at time t
+int dev_at(sisdc_op1d* op, double t, Op1DDev& d) {
+  d = op->dev;
+  return bc_at(op, t, d.gl, d.gr);
+}
+
 int check_coef(Ctx* c, sisdc_coef k) {
   if (k.kind < SISDC_COEF_NONE || k.kind > SISDC_COEF_PHYS) return c->fail(SISDC_ERR_ARG, "unknown coefficient kind");
   if ((k.kind == SISDC_COEF_FIELD || k.kind == SISDC_COEF_SI) && !k.ptr)
@@ -235,7 +249,7 @@ int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) 
   if (d->n_elem < 1 || d->degree < 1) return c.fail(SISDC_ERR_ARG, "need at least one element and degree >= 1");
   if (d->degree + 1 > MAXP1) return c.fail(SISDC_ERR_UNSUPPORTED, "degree above 15");
   if (d->ncomp != 1) return c.fail(SISDC_ERR_UNSUPPORTED, "only scalar problems (ncomp == 1) are built");
-  if (d->bc != SISDC_PERIODIC) return c.fail(SISDC_ERR_UNSUPPORTED, "only periodic meshes are built");
+  if (d->bc != SISDC_PERIODIC && d->bc != SISDC_DIRICHLET) return c.fail(SISDC_ERR_ARG, "unknown boundary condition");
   if (d->problem != SISDC_CONVDIFF && d->problem != SISDC_BURGERS) return c.fail(SISDC_ERR_ARG, "unknown problem");
   if (d->nu < 0) return c.fail(SISDC_ERR_ARG, "diffusion coefficient must be nonnegative");
   sisdc_op1d* op = new (std::nothrow) sisdc_op1d();
@@ -275,6 +289,7 @@ int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) 
   v.ne = d->n_elem; v.p1 = p1; v.n = d->n_elem * p1; v.problem = d->problem;
   v.dx = dx; v.s = 2.0 / dx; v.mu0 = d->penalty * p1 * p1 / dx;   // dgsem.py:137
   v.speed = d->speed; v.nu = d->nu; v.tab = op->d_tab; v.nu_art = nullptr;
+  v.bc = d->bc; v.gl = 0.0; v.gr = 0.0;
   *out = op;
   return SISDC_OK;
 }
@@ -389,29 +404,47 @@ int sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, dou
   return launch_persson(C(op), op->dev, u, kappa_s, c_s, nu_art);
 }
 
-int sisdc_apply_convection(sisdc_op1d* op, const double* u, double, double* out) {
+int sisdc_op1d_set_boundary(sisdc_op1d* op, int n, const double* times, const double* gl, const double* gr) {
+  if (!op || n < 0 || (n > 0 && (!times || !gl || !gr))) return SISDC_ERR_ARG;
+  for (int j = 0; j < n; ++j) {
+    bool found = false;
+    for (size_t q = 0; q + 2 < op->btab.size(); q += 3)
+      if (op->btab[q] == times[j]) { op->btab[q + 1] = gl[j]; op->btab[q + 2] = gr[j]; found = true; break; }
+    if (!found) { op->btab.push_back(times[j]); op->btab.push_back(gl[j]); op->btab.push_back(gr[j]); }
+  }
+  if (op->btab.size() > 3 * 4096) op->btab.erase(op->btab.begin(), op->btab.end() - 3 * 1024);   // keep recent times
+  return SISDC_OK;
+}
+
+int sisdc_apply_convection(sisdc_op1d* op, const double* u, double t, double* out) {
   if (!op || !u || !out) return SISDC_ERR_ARG;
   if (op->parted()) return part2_conv(op, u, out);
   if (op->dim == 2) return launch2_conv(C(op), op->dev2, u, out);
-  return launch_apply_convection(C(op), op->dev, u, out);
+  Op1DDev d;
+  if (int rc = dev_at(op, t, d)) return rc;
+  return launch_apply_convection(C(op), d, u, out);
 }
 
-int sisdc_apply_diffusion(sisdc_op1d* op, sisdc_coef k, const double* u, double, double* out) {
+int sisdc_apply_diffusion(sisdc_op1d* op, sisdc_coef k, const double* u, double t, double* out) {
   if (!op || !u || !out) return SISDC_ERR_ARG;
   if (int rc = check_coef(C(op), k)) return rc;
   if (k.kind == SISDC_COEF_NONE || (k.kind == SISDC_COEF_CONST && k.value == 0.0))
     return C(op)->cuda(cudaMemsetAsync(out, 0, op->n() * sizeof(double), C(op)->stream), "zero");
   if (op->parted()) return part2_sip(op, coef(k), u, out);
   if (op->dim == 2) return launch2_sip(C(op), op->dev2, coef(k), u, out);
-  return launch_apply_diffusion(C(op), op->dev, coef(k), u, out);
+  Op1DDev d;
+  if (int rc = dev_at(op, t, d)) return rc;
+  return launch_apply_diffusion(C(op), d, coef(k), u, out);
 }
 
-int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double, double* out) {
+int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double t, double* out) {
   if (!op || !u || !out) return SISDC_ERR_ARG;
   if (op->parted()) return part2_eval_nodes(op, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
-  return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
+  Op1DDev d;
+  if (int rc = dev_at(op, t, d)) return rc;
+  return launch_node_eval(C(op), d, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
 }
 
 int sisdc_coef_field(sisdc_op1d* op, sisdc_coef k, double* out) {
@@ -422,7 +455,7 @@ int sisdc_coef_field(sisdc_op1d* op, sisdc_coef k, double* out) {
   return launch_coef_field(C(op), op->dev, coef(k), out);
 }
 
-int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* rhs, double, double* x) {
+int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* rhs, double t, double* x) {
   if (!op || !rhs || !x) return SISDC_ERR_ARG;
   if (int rc = check_coef(C(op), k)) return rc;
   if (a == 0.0) {   // dgsem.py:505-506
@@ -432,20 +465,24 @@ int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* r
   if (k.kind == SISDC_COEF_NONE) return C(op)->fail(SISDC_ERR_ARG, "cannot assemble a zero coefficient");
   if (op->parted()) return part2_solve(op, coef(k), a, rhs, x);
   if (op->dim == 2) return launch2_cg(C(op), op->dev2, coef(k), a, rhs, x, op->d_cgws, op->cg_blocks);
-  return launch_cg1d(C(op), op->dev, coef(k), a, rhs, x);
+  Op1DDev d;
+  if (int rc = dev_at(op, t, d)) return rc;
+  return launch_cg1d(C(op), d, coef(k), a, rhs, x);
 }
 
 int sisdc_stage_rhs(sisdc_op1d* op, const double* base, const double* conv_in, double dt_m, const double* f_old,
-                    int M, const double* w_row, double dt, const double* g_m, const double* h_old, double,
+                    int M, const double* w_row, double dt, const double* g_m, const double* h_old, double t,
                     double* rhs, double* conv_out) {
   if (!op || !base || !conv_in || !rhs || M < 0 || M > MAXM || (f_old && !w_row)) return SISDC_ERR_ARG;
   if (op->parted()) return part2_stage(op, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
   if (op->dim == 2) return launch2_stage(C(op), op->dev2, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
-  return launch_stage_rhs(C(op), op->dev, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
+  Op1DDev d;
+  if (int rc = dev_at(op, t, d)) return rc;
+  return launch_stage_rhs(C(op), d, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
 }
 
 int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_count, const double* u0,
-                      const double* u, const double* conv_prev, const double* dts, double, const double*,
+                      const double* u, const double* conv_prev, const double* dts, double t0, const double* times,
                       double* f, double* h1, double* h2) {
   if (!op || !u0 || !u || !dts || !f || !h1) return SISDC_ERR_ARG;
   if (scheme < SISDC_EULER || scheme > SISDC_SI2) return C(op)->fail(SISDC_ERR_ARG, "unknown scheme");
@@ -453,13 +490,30 @@ int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_coun
   if (op->parted()) return part2_eval_nodes(op, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
+  if (op->dev.bc == SISDC_DIRICHLET) {   // boundary data at t_m and t_{m-1} per node
+    if (!times) return C(op)->fail(SISDC_ERR_ARG, "Dirichlet node caches need the node times");
+    if (M > MAXM) return C(op)->fail(SISDC_ERR_ARG, "too many collocation nodes");
+    double bnd[4 * MAXM] = {};
+    for (int m = m_first; m < m_first + m_count && m < M; ++m) {
+      if (int rc = bc_at(op, times[m], bnd[m], bnd[M + m])) return rc;
+      if (int rc = bc_at(op, m == 0 ? t0 : times[m - 1], bnd[2 * M + m], bnd[3 * M + m])) return rc;
+    }
+    return launch_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2, bnd);
+  }
   return launch_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
 }
 
-int sisdc_eval_rhs_nodes(sisdc_op1d* op, int M, const double* u, const double*, double* f) {
+int sisdc_eval_rhs_nodes(sisdc_op1d* op, int M, const double* u, const double* times, double* f) {
   if (!op || !u || !f || M < 1 || M > MAXM) return SISDC_ERR_ARG;
   if (op->parted()) return part2_eval_nodes(op, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
   if (op->dim == 2) return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
+  if (op->dev.bc == SISDC_DIRICHLET) {
+    if (!times) return C(op)->fail(SISDC_ERR_ARG, "Dirichlet evaluations need the node times");
+    double bnd[4 * MAXM] = {};
+    for (int m = 0; m < M; ++m)
+      if (int rc = bc_at(op, times[m], bnd[m], bnd[M + m])) return rc;
+    return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr, bnd);
+  }
   return launch_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
 }
 

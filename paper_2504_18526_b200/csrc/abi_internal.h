@@ -33,6 +33,7 @@ struct sisdc_op1d {   // dimension-tagged operator handle (1-D or 2-D)
   double* d_cgws = nullptr;   // 2-D CG workspace (allocated at creation: graph-safe)
   int cg_blocks = 0;
   std::vector<double> nodes, weights, D;
+  std::vector<double> btab;    // Dirichlet trace table: (t, g_l, g_r) triples
   // partitioned 2-D operator (empty parts: single periodic domain)
   std::vector<Part2D> parts;
   sisdc_comm* comm = nullptr;  // NULL: every partition is local (in-process)

@@ -194,23 +194,27 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   const double* DTW = s.st + TabOff::DTW(P1);
   const double mi = s.st[TabOff::m(P1) + i];
   const double sc = op.s, mu0 = op.mu0, a = A.a;
-  const double cR = last ? s.Cs[NL + 1] : s.Cs[min((el + 1) * P1, NL - 1)];
-  const double cL = first ? s.Cs[NL] : s.Cs[min(max(el * P1 - 1, 0), NL - 1)];
   const double cP = s.Cs[min(el * P1 + P, NL - 1)], c0 = s.Cs[min(el * P1, NL - 1)];
+  // Dirichlet outer faces (dgsem.py:282-289): outside value 0 in the operator (the
+  // boundary data moves to the right-hand side), one-sided q and C, lift weight 1
+  const bool dirL = op.bc == SISDC_DIRICHLET && e0 + el == 0;
+  const bool dirR = op.bc == SISDC_DIRICHLET && e0 + el == op.ne - 1;
+  const double cR = dirR ? cP : (last ? s.Cs[NL + 1] : s.Cs[min((el + 1) * P1, NL - 1)]);
+  const double cL = dirL ? c0 : (first ? s.Cs[NL] : s.Cs[min(max(el * P1 - 1, 0), NL - 1)]);
   double dg = 1.0;
   if (own) {   // Jacobi diagonal diag(M + a B[C]) (closed form of dgsem.py:414-490)
     double d = 0.0;
 #pragma unroll
     for (int k = 0; k < P1; ++k) d = fma(s.st[TabOff::D2W(P1) + i * P1 + k], s.Cs[el * P1 + k], d);
     d = sc * d;
-    if (i == P) d += mu0 * (0.5 * (cP + cR)) - sc * cP * D[P * P1 + P];
-    if (i == 0) d += mu0 * (0.5 * (cL + c0)) + sc * c0 * D[0];
+    if (i == P) d += dirR ? mu0 * cP - 2.0 * sc * cP * D[P * P1 + P] : mu0 * (0.5 * (cP + cR)) - sc * cP * D[P * P1 + P];
+    if (i == 0) d += dirL ? mu0 * c0 + 2.0 * sc * c0 * D[0] : mu0 * (0.5 * (cL + c0)) + sc * c0 * D[0];
     dg = mi + a * d;
   }
   const double dinv = 1.0 / dg;
   // per-node face constants of the SIP operator (dgsem.py:290-308)
   const double muR = mu0 * (0.5 * (cP + cR)), muL = mu0 * (0.5 * (cL + c0));
-  const double kR = sc * (0.5 * cP), kL = sc * (0.5 * c0);
+  const double kR = sc * ((dirR ? 1.0 : 0.5) * cP), kL = sc * ((dirL ? 1.0 : 0.5) * c0);
   const double DPi = D[P * P1 + i], D0i = D[i];
 
   // ---- push targets (boundary nodes) and reduction targets (warp 0 lanes)
@@ -323,16 +327,16 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     __syncthreads();
     if (!own) return 0.0;
     double B = erow(DTr, s.Q + ob);
-    const double pn = last ? hv[P1] : v[ob + P1P];
-    const double pp = first ? hv[P] : v[ob - P1P + P];
+    const double pn = dirR ? 0.0 : (last ? hv[P1] : v[ob + P1P]);
+    const double pp = dirL ? 0.0 : (first ? hv[P] : v[ob - P1P + P]);
     const double jr = v[ob + P] - pn;
     const double jl = pp - v[ob];
     if (i == P) {
-      const double qn = last ? cR * (sc * dot3<P1>(D, hv + P1)) : s.Q[ob + P1P];
+      const double qn = dirR ? s.Q[ob + P] : (last ? cR * (sc * dot3<P1>(D, hv + P1)) : s.Q[ob + P1P]);
       B += -(0.5 * (s.Q[ob + P] + qn)) + muR * jr;
     }
     if (i == 0) {
-      const double qp = first ? cL * (sc * dot3<P1>(D + P * P1, hv)) : s.Q[ob - P1P + P];
+      const double qp = dirL ? s.Q[ob] : (first ? cL * (sc * dot3<P1>(D + P * P1, hv)) : s.Q[ob - P1P + P]);
       B -= -(0.5 * (qp + s.Q[ob])) + muL * jl;
     }
     B -= (kR * jr) * DPi;
@@ -355,7 +359,11 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     s.HX[lane] = s.HXD[2 * lane];
     s.HD[lane] = s.HXD[2 * lane + 1];
   }
-  const double bi = mi * x;   // b = M rhs
+  // b = M rhs (+ a M D(0; t): the Dirichlet data of the affine SIP, dgsem.py:517-529)
+  const double b0 = mi * x;
+  double bi = b0;
+  if (dirL) bi += a * ((i == 0 ? mu0 * c0 * op.gl : 0.0) + sc * c0 * op.gl * D0i);
+  if (dirR) bi += a * ((i == P ? mu0 * cP * op.gr : 0.0) - sc * cP * op.gr * DPi);
   double r = bi - matvec(s.Xs, s.HX);
   double u = r * dinv;
   // ---- setup 2: halo u0 -> w0 = A u0
@@ -387,7 +395,7 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   push_rws(0);
   uint32_t ph[2] = {0, 0};
   double v6[NVS] = {own ? r * u : 0.0, own ? w * u : 0.0, own ? r * r : 0.0, own ? bi * bi : 0.0,
-                    (own && bi != 0.0) ? 1.0 : 0.0, 0.0};
+                    (own && b0 != 0.0) ? 1.0 : 0.0, 0.0};   // b == 0 test on M rhs (dgsem.py:509-511)
   if (stamp) A.timing[2] = clock64();
   csum(v6, std::integral_constant<int, 5>{}, std::integral_constant<int, NVS>{}, 0, ph[0]);
   if (stamp) A.timing[3] = clock64();

@@ -18,7 +18,7 @@ __global__ void k_apply_convection(Op1DDev op, const double* __restrict__ u, dou
   double* ut = st + TabOff::size(p1);
   int ebase = blockIdx.x * EB;
   load_tab(st, op.tab, p1);
-  load_tile(ut, u, ebase, EB, op.ne, p1);
+  load_tile(op, ut, u, ebase, EB);
   __syncthreads();
   int t = threadIdx.x, el = t / p1, i = t - el * p1;
   if (el < EB && ebase + el < op.ne) out[(ebase + el) * p1 + i] = conv_node(op, st, ut, el, i);
@@ -34,14 +34,14 @@ __global__ void k_apply_diffusion(Op1DDev op, CoefDev c, const double* __restric
   double* qt = ct + T;
   int ebase = blockIdx.x * EB;
   load_tab(st, op.tab, p1);
-  load_tile(ut, u, ebase, EB, op.ne, p1);
+  load_tile(op, ut, u, ebase, EB);
   coef_tile(op, c, ct, ebase, EB);
   __syncthreads();
-  flux_q_tile(op, st, ut, ct, qt, EB);
+  flux_q_tile(op, st, ut, ct, qt, EB, ebase);
   __syncthreads();
   int t = threadIdx.x, el = t / p1, i = t - el * p1;
   if (el < EB && ebase + el < op.ne)
-    out[(ebase + el) * p1 + i] = -sip_B_node(op, st, ut, ct, qt, el, i) * st[TabOff::minv(p1) + i];
+    out[(ebase + el) * p1 + i] = -sip_B_node(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i];
 }
 
 __global__ void k_coef_field(Op1DDev op, CoefDev c, double* __restrict__ out) {
@@ -58,21 +58,25 @@ struct CacheArgs {
   const double* conv_prev;  // nullable (single node)
   int scheme, m_first, mode;
   W16 dts;
+  W16 gl, gr, glp, grp;     // Dirichlet outside states at t_m and t_{m-1} per node
   double* f;
   double* h1;
   double* h2;               // nullable
   int* status;              // [0] first non-finite element
 };
 
-__global__ void k_node_eval(Op1DDev op, CacheArgs a) {
+__global__ void k_node_eval(Op1DDev op_in, CacheArgs a) {
   extern __shared__ double sm[];
+  const int m = a.m_first + blockIdx.y;
+  Op1DDev op = op_in, opp = op_in;   // boundary data at t_m (u_m) and t_{m-1} (conv of u_{m-1})
+  op.gl = a.gl.v[m]; op.gr = a.gr.v[m];
+  opp.gl = a.glp.v[m]; opp.gr = a.grp.v[m];
   const int p1 = op.p1, EB = eb_for(p1), T = (EB + 2) * p1, N = op.n;
   double* st = sm;
   double* ut = st + TabOff::size(p1);   // u_m tile
   double* ct = ut + T;                  // coefficient tile
   double* qt = ct + T;                  // flux tile
   double* pt = qt + T;                  // u_{m-1} tile
-  const int m = a.m_first + blockIdx.y;
   const int ebase = blockIdx.x * EB;
   const double* um = a.u + (size_t)m * N;
   const double* up = m == 0 ? a.u0 : a.u + (size_t)(m - 1) * N;
@@ -80,7 +84,7 @@ __global__ void k_node_eval(Op1DDev op, CacheArgs a) {
   const bool own = el < EB && ebase + el < op.ne;
   const int gi = (ebase + el) * p1 + i;
   load_tab(st, op.tab, p1);
-  load_tile(ut, um, ebase, EB, op.ne, p1);
+  load_tile(op, ut, um, ebase, EB);
   CoefDev phys{SISDC_COEF_PHYS, 0.0, nullptr};
   coef_tile(op, phys, ct, ebase, EB);
   double dummy;
@@ -90,9 +94,9 @@ __global__ void k_node_eval(Op1DDev op, CacheArgs a) {
   double cm = own ? conv_node(op, st, ut, el, i) : 0.0;
   double f = cm;
   if (has_phys) {
-    flux_q_tile(op, st, ut, ct, qt, EB);
+    flux_q_tile(op, st, ut, ct, qt, EB, ebase);
     __syncthreads();
-    if (own) f = cm + (-sip_B_node(op, st, ut, ct, qt, el, i) * st[TabOff::minv(p1) + i]);
+    if (own) f = cm + (-sip_B_node(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i]);
     __syncthreads();
   }
   if (own) {
@@ -111,13 +115,13 @@ __global__ void k_node_eval(Op1DDev op, CacheArgs a) {
   // C_m frozen at u_{m-1}: SI for si1/si2, physical for euler (dgsem.py:365-366)
   CoefDev cmod = a.scheme == SISDC_EULER ? phys : CoefDev{SISDC_COEF_SI, dtm, up};
   coef_tile(op, cmod, ct, ebase, EB);
-  if (a.conv_prev == nullptr) load_tile(pt, up, ebase, EB, op.ne, p1);
+  if (a.conv_prev == nullptr) load_tile(opp, pt, up, ebase, EB);
   __syncthreads();
-  flux_q_tile(op, st, ut, ct, qt, EB);
+  flux_q_tile(op, st, ut, ct, qt, EB, ebase);
   __syncthreads();
   if (!own) return;
-  double d = -sip_B_node(op, st, ut, ct, qt, el, i) * st[TabOff::minv(p1) + i];
-  double cp = a.conv_prev ? a.conv_prev[gi] : conv_node(op, st, pt, el, i);
+  double d = -sip_B_node(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i];
+  double cp = a.conv_prev ? a.conv_prev[gi] : conv_node(opp, st, pt, el, i);
   a.h1[(size_t)m * N + gi] = dtm * (cp + d);
   if (a.h2) a.h2[(size_t)m * N + gi] = dtm * (cm + d);
 }
@@ -144,7 +148,7 @@ __global__ void k_stage_rhs(Op1DDev op, StageArgs a) {
   double* ut = st + TabOff::size(p1);
   const int ebase = blockIdx.x * EB;
   load_tab(st, op.tab, p1);
-  load_tile(ut, a.conv_in, ebase, EB, op.ne, p1);
+  load_tile(op, ut, a.conv_in, ebase, EB);
   __syncthreads();
   const int t = threadIdx.x, el = t / p1, i = t - el * p1;
   if (!(el < EB && ebase + el < op.ne)) return;
@@ -389,13 +393,20 @@ int launch_coef_field(Ctx* c, const Op1DDev& op, CoefDev k, double* out) {
   k_coef_field<<<(n + 255) / 256, 256, 0, c->stream>>>(op, k, out);
   return c->after_launch("coef_field");
 }
+// bnd (nullable, Dirichlet): [4][M] outside states g_l(t_m), g_r(t_m), g_l(t_{m-1}), g_r(t_{m-1})
 int launch_node_eval(Ctx* c, const Op1DDev& op, int mode, int scheme, int M, int m_first, int m_count,
                      const double* u0, const double* u, const double* conv_prev, const double* dts,
-                     double* f, double* h1, double* h2) {
+                     double* f, double* h1, double* h2, const double* bnd) {
   if (M > MAXM || m_first < 0 || m_count < 1 || m_first + m_count > M) return c->fail(SISDC_ERR_ARG, "bad node range");
   CacheArgs a{};
   a.u0 = u0; a.u = u; a.conv_prev = conv_prev; a.scheme = scheme; a.m_first = m_first; a.mode = mode;
   for (int j = 0; j < M; ++j) a.dts.v[j] = dts ? dts[j] : 0.0;
+  for (int j = 0; j < M; ++j) {
+    a.gl.v[j] = bnd ? bnd[j] : op.gl;
+    a.gr.v[j] = bnd ? bnd[M + j] : op.gr;
+    a.glp.v[j] = bnd ? bnd[2 * M + j] : op.gl;
+    a.grp.v[j] = bnd ? bnd[3 * M + j] : op.gr;
+  }
   a.f = f; a.h1 = h1; a.h2 = h2; a.status = c->d_status;
   k_node_eval<<<tile_grid(op.ne, op.p1, m_count), tile_block(op.p1), tile_smem(op.p1, 4), c->stream>>>(op, a);
   return c->after_launch("node_eval");

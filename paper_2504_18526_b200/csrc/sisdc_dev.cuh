@@ -35,6 +35,8 @@ struct Op1DDev {
   double dx, s, mu0, speed, nu;
   const double* tab;      // device tables (TabOff layout)
   const double* nu_art;   // per element or nullptr
+  int bc;                 // SISDC_PERIODIC / SISDC_DIRICHLET (Mesh1D.bc)
+  double gl, gr;          // Dirichlet: outside states at the time of this evaluation
 };
 
 struct CoefDev {
@@ -86,13 +88,18 @@ __device__ __forceinline__ int wrap(int e, int ne) {
   return e < 0 ? e + ne : e;
 }
 
-// tile[(el+1)*p1 + i] = u[(ebase+el) wrapped, i] for el = -1..EB
-__device__ __forceinline__ void load_tile(double* tile, const double* __restrict__ u, int ebase, int EB,
-                                          int ne, int p1) {
+// tile[(el+1)*p1 + i] = u[(ebase+el) wrapped, i] for el = -1..EB.  Dirichlet:
+// the ghost elements outside the mesh hold the outside state g_l / g_r
+// (only their face node enters: dgsem.py:179-194, 212-216, 282-284)
+__device__ __forceinline__ void load_tile(const Op1DDev& op, double* tile, const double* __restrict__ u, int ebase,
+                                          int EB) {
+  const int p1 = op.p1, ne = op.ne;
   int tot = (EB + 2) * p1;
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
     int el = t / p1 - 1, i = t - (t / p1) * p1;
-    tile[t] = u[wrap(ebase + el, ne) * p1 + i];
+    const int eg = ebase + el;
+    if (op.bc == SISDC_DIRICHLET && (eg < 0 || eg >= ne)) tile[t] = eg < 0 ? op.gl : op.gr;
+    else tile[t] = u[wrap(eg, ne) * p1 + i];
   }
 }
 __device__ __forceinline__ void load_tab(double* stab, const double* __restrict__ tab, int p1) {
@@ -120,15 +127,21 @@ __device__ __forceinline__ double conv_node(const Op1DDev& op, const double* st,
   return v * st[TabOff::minv(p1) + i];
 }
 
-// q = C * (2/dx) D u for every node of the tile (incl. halo elements); C tile must be filled
+// q = C * (2/dx) D u for every node of the tile (incl. halo elements); C tile must be filled.
+// Dirichlet ghosts carry the interior boundary node's q (one-sided flux, dgsem.py:285-286)
 __device__ __forceinline__ void flux_q_tile(const Op1DDev& op, const double* st, const double* ut,
-                                            const double* ct, double* qt, int EB) {
+                                            const double* ct, double* qt, int EB, int ebase) {
   const int p1 = op.p1;
   const double* D = st + TabOff::D(p1);
   int tot = (EB + 2) * p1;
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
     int e = t / p1, i = t - e * p1;
     const double* ue = ut + e * p1;
+    if (op.bc == SISDC_DIRICHLET) {
+      const int eg = ebase + e - 1;
+      if (eg < 0) { ue = ut + p1; i = 0; }                          // interior element 0, node 0
+      else if (eg >= op.ne) { ue = ut + (e - 1) * p1; i = p1 - 1; }  // interior element ne-1, node P
+    }
     double g = 0.0;
 #pragma unroll 4
     for (int j = 0; j < p1; ++j) g = fma(D[i * p1 + j], ue[j], g);
@@ -136,9 +149,10 @@ __device__ __forceinline__ void flux_q_tile(const Op1DDev& op, const double* st,
   }
 }
 
-// SIP accumulator B_i (apply_diffusion = -B/m) at node (el,i); dgsem.py:270-308
+// SIP accumulator B_i (apply_diffusion = -B/m) at node (el,i); dgsem.py:270-308.
+// eg = global element; Dirichlet outer faces take adjoint-lift weight 1 (dgsem.py:196-201)
 __device__ __forceinline__ double sip_B_node(const Op1DDev& op, const double* st, const double* ut,
-                                             const double* ct, const double* qt, int el, int i) {
+                                             const double* ct, const double* qt, int el, int i, int eg) {
   const int p1 = op.p1, P = p1 - 1;
   const double* D = st + TabOff::D(p1);
   const double* DTW = st + TabOff::DTW(p1);
@@ -158,17 +172,23 @@ __device__ __forceinline__ double sip_B_node(const Op1DDev& op, const double* st
     double G = -(0.5 * (qt[b - 1] + qt[b])) + (op.mu0 * (0.5 * (ct[b - 1] + ct[b]))) * jl;
     B -= G;
   }
-  B -= (op.s * ((0.5 * ct[b + P]) * jr)) * D[P * p1 + i];
-  B -= (op.s * ((0.5 * ct[b]) * jl)) * D[i];
+  const bool dir = op.bc == SISDC_DIRICHLET;
+  const double wr = (dir && eg == op.ne - 1) ? 1.0 : 0.5, wl = (dir && eg == 0) ? 1.0 : 0.5;
+  B -= (op.s * ((wr * ct[b + P]) * jr)) * D[P * p1 + i];
+  B -= (op.s * ((wl * ct[b]) * jl)) * D[i];
   return B;
 }
 
-// fill a C tile from a coefficient descriptor (with halo)
+// fill a C tile from a coefficient descriptor (with halo); Dirichlet ghosts carry
+// the interior boundary node's coefficient (one-sided C, dgsem.py:287-288)
 __device__ __forceinline__ void coef_tile(const Op1DDev& op, const CoefDev& k, double* ct, int ebase, int EB) {
   int tot = (EB + 2) * op.p1;
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
     int el = t / op.p1 - 1, i = t - (t / op.p1) * op.p1;
-    ct[t] = coef_at(op, k, wrap(ebase + el, op.ne), i);
+    const int eg = ebase + el;
+    if (op.bc == SISDC_DIRICHLET && eg < 0) ct[t] = coef_at(op, k, 0, 0);
+    else if (op.bc == SISDC_DIRICHLET && eg >= op.ne) ct[t] = coef_at(op, k, op.ne - 1, op.p1 - 1);
+    else ct[t] = coef_at(op, k, wrap(eg, op.ne), i);
   }
 }
 

@@ -52,7 +52,7 @@ int launch_apply_diffusion(Ctx* c, const Op1DDev& op, CoefDev k, const double* u
 int launch_coef_field(Ctx* c, const Op1DDev& op, CoefDev k, double* out);
 int launch_node_eval(Ctx* c, const Op1DDev& op, int mode, int scheme, int M, int m_first, int m_count,
                      const double* u0, const double* u, const double* conv_prev, const double* dts,
-                     double* f, double* h1, double* h2);
+                     double* f, double* h1, double* h2, const double* bnd = nullptr);
 int launch_stage_rhs(Ctx* c, const Op1DDev& op, const double* base, const double* conv_in, double dt_m,
                      const double* f_old, int M, const double* w_row, double dt, const double* g,
                      const double* h, double* rhs, double* conv_out);

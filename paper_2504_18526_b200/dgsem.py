@@ -126,8 +126,8 @@ class DGOperator:
 
     def __init__(self, mesh: Mesh1D, problem, av: Optional[ArtificialViscosityParams] = None,
                  penalty_const: float = 2.0, device: int = 0, eager_checks: bool = True):
-        if mesh.bc != "periodic":
-            raise NotImplementedError("the GPU path is built for periodic meshes (Dirichlet is next, SURVEY 8f)")
+        if mesh.bc == "dirichlet" and getattr(problem, "boundary_state", None) is None:
+            raise ValueError("dirichlet mesh needs a problem with boundary_state(t)")   # dgsem.py:150-151
         if getattr(problem, "source", None) is not None:
             raise NotImplementedError("source terms are not built on the GPU path")
         self.mesh = mesh
@@ -140,7 +140,10 @@ class DGOperator:
         self.lib = self.rt.lib
         self.eager_checks = eager_checks
         kind = {"convdiff": _lib.CONVDIFF, "burgers": _lib.BURGERS}[problem.kind]
-        self._desc = _lib.Op1DDesc(mesh.n_elem, mesh.degree, self.ncomp, _lib.PERIODIC, kind,
+        self.dirichlet = mesh.bc == "dirichlet"
+        self._btimes = set()
+        self._desc = _lib.Op1DDesc(mesh.n_elem, mesh.degree, self.ncomp,
+                                   _lib.DIRICHLET if self.dirichlet else _lib.PERIODIC, kind,
                                    float(mesh.x_left), float(mesh.x_right), float(getattr(problem, "speed", 0.0)),
                                    float(problem.nu), float(penalty_const))
         h = C.c_void_p()
@@ -216,6 +219,24 @@ class DGOperator:
             return half + self.problem.nu if self.problem.nu > 0 else half
         return SICoefficient(self.rt.to_device(u_b).clone(), dt_m)
 
+    # --------------------------------------------------- Dirichlet trace data
+    def boundary_at(self, *times):
+        """Register problem.boundary_state(t) for the given times with the
+        library (dgsem.py:212-216): host evaluation, no device work."""
+        if not self.dirichlet:
+            return
+        new = [float(t) for t in times if float(t) not in self._btimes]
+        if not new:
+            return
+        gl, gr = zip(*[self.problem.boundary_state(t) for t in new])
+        ta, tp = _lib.darr(new)
+        la, lp = _lib.darr([float(np.asarray(g).reshape(-1)[0]) for g in gl])
+        ra, rp = _lib.darr([float(np.asarray(g).reshape(-1)[0]) for g in gr])
+        self.rt.check(self.lib.sisdc_op1d_set_boundary(self.h, len(new), tp, lp, rp), "set_boundary")
+        self._btimes.update(new)
+        if len(self._btimes) > 3000:
+            self._btimes = set(new)
+
     # ---------------------------------------------------------- operators
     def _out(self, out):
         self.rt.bind_stream()
@@ -224,6 +245,7 @@ class DGOperator:
     def apply_convection(self, u, t: float = 0.0, out=None):
         u = self.rt.to_device(u)
         out = self._out(out)
+        self.boundary_at(t)
         self.rt.check(self.lib.sisdc_apply_convection(self.h, u.data_ptr(), float(t), out.data_ptr()),
                       "apply_convection")
         return out
@@ -233,6 +255,7 @@ class DGOperator:
         c = self._coef(coeff, keep)
         u = self.rt.to_device(u)
         out = self._out(out)
+        self.boundary_at(t)
         self.rt.check(self.lib.sisdc_apply_diffusion(self.h, c, u.data_ptr(), float(t), out.data_ptr()),
                       "apply_diffusion")
         return out
@@ -242,6 +265,7 @@ class DGOperator:
         out = self._out(out)
         if self.eager_checks:
             self.rt.reset_status()
+        self.boundary_at(t)
         self.rt.check(self.lib.sisdc_eval_rhs(self.h, u.data_ptr(), float(t), out.data_ptr()), "eval_rhs")
         if self.eager_checks:
             self.rt.raise_on_failure()
@@ -269,6 +293,7 @@ class DGOperator:
         out = self._out(out)
         if self.eager_checks:
             self.rt.reset_status()
+        self.boundary_at(t)
         self.rt.check(self.lib.sisdc_implicit_solve(self.h, c, float(a), rhs.data_ptr(), float(t), out.data_ptr()),
                       "implicit_solve")
         if self.eager_checks:

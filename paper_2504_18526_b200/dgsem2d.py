@@ -384,3 +384,6 @@ class DGOperator2D:
 
     def begin_slab(self, u0, t0: float, dt: float) -> None:
         pass
+
+    def boundary_at(self, *times):
+        """Periodic 2-D meshes carry no trace data."""

@@ -108,7 +108,11 @@ def fas_rhs(hier: Hierarchy, i: int, dt: float):
         None if upper.g is None else upper.g.data_ptr(), v.data_ptr(), rr.data_ptr()), "fas_restrict")
     lower.v = v
     # coarse defect of v with fresh rhs at the coarse node times (mlsdc.py:68-77)
-    rt.check(rt.lib.sisdc_eval_rhs_nodes(lower.ctx.h, Mc, v.data_ptr(), None, fr.data_ptr()), "eval_rhs_nodes")
+    times = lower.t0 + dt * lower.rule.tau
+    if getattr(lower.ctx, "dirichlet", False):
+        lower.ctx.boundary_at(*times)
+    ta, tp = _lib.darr(times)
+    rt.check(rt.lib.sisdc_eval_rhs_nodes(lower.ctx.h, Mc, v.data_ptr(), tp, fr.data_ptr()), "eval_rhs_nodes")
     Wc = lower.weights.w_nn if inc else lower.weights.w_0n
     wca, wcp = _lib.darr(Wc)
     rt.check(rt.lib.sisdc_collocation_defect(lower.ctx.h, Mc, wcp, float(dt), inc, lower.u0.data_ptr(), v.data_ptr(),
@@ -258,6 +262,8 @@ class SlabGraph:
                  strategy: str = "fmg", c_fmg: int = 1):
         import torch
         fine = hier.fine
+        if any(getattr(lv.ctx, "dirichlet", False) for lv in hier.levels):
+            raise ValueError("time-dependent Dirichlet data cannot be captured into a replayed slab graph")
         rt = fine.ctx.rt
         self.rt, self.hier = rt, hier
         self.u = rt.to_device(u0_fine).clone()

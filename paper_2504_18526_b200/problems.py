@@ -43,3 +43,26 @@ class Burgers:
         self.source = source
         self.boundary_state = boundary
         self.speed = 0.0
+
+
+def burgers_front_exact(nu: float):
+    """Viscous front u = 1 - tanh((x + 1/2 - t) / (2 nu)) (``problems.py:268-277``)."""
+    import numpy as np
+    nu = float(nu)
+
+    def exact(x, t=0.0):
+        return 1.0 - np.tanh((np.asarray(x) + 0.5 - t) / (2.0 * nu))
+
+    return exact
+
+
+def burgers_front_problem(nu: float):
+    """Burgers with the exact front's trace data on [-1, 1] (``problems.py:280-291``):
+    returns (problem, exact)."""
+    import numpy as np
+    exact = burgers_front_exact(nu)
+
+    def boundary(t):
+        return np.array([exact(-1.0, t)]), np.array([exact(1.0, t)])
+
+    return Burgers(nu, boundary=boundary), exact

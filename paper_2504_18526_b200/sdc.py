@@ -80,12 +80,19 @@ def _coef(ctx, scheme, u_prev, dt_m) -> Coef:
     return Coef(_lib.COEF_SI, float(dt_m), u_prev.data_ptr())
 
 
-def _caches(ctx, scheme, sol, M, m_first, m_count, dts, conv_prev=None):
+def _register_times(ctx, t0, times):
+    """Dirichlet trace data for the slab's times (no-op on periodic meshes)."""
+    if getattr(ctx, "dirichlet", False):
+        ctx.boundary_at(t0, *times)
+
+
+def _caches(ctx, scheme, sol, M, m_first, m_count, dts, conv_prev=None, times=None):
     rt = _rt(ctx)
     arr, p = _lib.darr(dts)
+    ta, tp = _lib.darr(times if times is not None else np.zeros(M))
     rt.check(rt.lib.sisdc_node_caches(
         ctx.h, _scheme_id(scheme), M, m_first, m_count, sol.u0.data_ptr(), sol.u.data_ptr(),
-        None if conv_prev is None else conv_prev.data_ptr(), p, float(sol.t0), None,
+        None if conv_prev is None else conv_prev.data_ptr(), p, float(sol.t0), tp,
         sol.f.data_ptr(), sol.h1.data_ptr(), None if sol.h2 is None else sol.h2.data_ptr()), "node_caches")
 
 
@@ -93,37 +100,40 @@ def refresh_caches(ctx, rule: CollocationRule, dt: float, scheme: str, sol: Noda
     """Rebuild all caches after node values changed outside a sweep
     (``sdc.py:101-119``): one kernel over all M nodes."""
     _rt(ctx).bind_stream()
-    _caches(ctx, scheme, sol, rule.M, 0, rule.M, _dts(rule, dt))
+    times = _node_times(rule, dt, sol.t0)
+    _register_times(ctx, sol.t0, times)
+    _caches(ctx, scheme, sol, rule.M, 0, rule.M, _dts(rule, dt), times=times)
 
 
-def _stage(ctx, base, conv_in, dt_m, f_old, w_row, dt, g_m, h_old, rhs, conv_out):
+def _stage(ctx, base, conv_in, dt_m, f_old, w_row, dt, g_m, h_old, rhs, conv_out, t=0.0):
     rt = _rt(ctx)
     M = 0 if f_old is None else f_old.shape[0]
     wa, wp = _lib.darr(w_row if w_row is not None else np.zeros(1))
     rt.check(rt.lib.sisdc_stage_rhs(
         ctx.h, base.data_ptr(), conv_in.data_ptr(), float(dt_m),
         None if f_old is None else f_old.data_ptr(), M, wp if f_old is not None else None, float(dt),
-        None if g_m is None else g_m.data_ptr(), None if h_old is None else h_old.data_ptr(), 0.0,
+        None if g_m is None else g_m.data_ptr(), None if h_old is None else h_old.data_ptr(), float(t),
         rhs.data_ptr(), None if conv_out is None else conv_out.data_ptr()), "stage_rhs")
 
 
-def _solve(ctx, coef: Coef, a, rhs, out):
+def _solve(ctx, coef: Coef, a, rhs, out, t=0.0):
     rt = _rt(ctx)
-    rt.check(rt.lib.sisdc_implicit_solve(ctx.h, coef, float(a), rhs.data_ptr(), 0.0, out.data_ptr()),
+    rt.check(rt.lib.sisdc_implicit_solve(ctx.h, coef, float(a), rhs.data_ptr(), float(t), out.data_ptr()),
              "implicit_solve")
 
 
-def _substep(ctx, scheme, up, dtm, f_old, w_row, dt, g_m, h1_old, h2_old, out):
-    """One SI substep into ``out`` (predictor when f_old/h are None)."""
+def _substep(ctx, scheme, up, dtm, f_old, w_row, dt, g_m, h1_old, h2_old, out, t_prev=0.0, t_m=0.0):
+    """One SI substep into ``out`` (predictor when f_old/h are None):
+    conv(u_{m-1}) at t_{m-1}, the solves and conv(stage) at t_m (sdc.py:225-237)."""
     s = ctx.scratch()
     c = _coef(ctx, scheme, up, dtm)
-    _stage(ctx, up, up, dtm, f_old, w_row, dt, g_m, h1_old, s["rhs"], s["conv"])
+    _stage(ctx, up, up, dtm, f_old, w_row, dt, g_m, h1_old, s["rhs"], s["conv"], t_prev)
     if scheme in ("euler", "si1"):
-        _solve(ctx, c, dtm, s["rhs"], out)
+        _solve(ctx, c, dtm, s["rhs"], out, t_m)
     elif scheme == "si2":
-        _solve(ctx, c, dtm, s["rhs"], s["stage"])
-        _stage(ctx, up, s["stage"], dtm, f_old, w_row, dt, g_m, h2_old, s["rhs"], None)
-        _solve(ctx, c, dtm, s["rhs"], out)
+        _solve(ctx, c, dtm, s["rhs"], s["stage"], t_m)
+        _stage(ctx, up, s["stage"], dtm, f_old, w_row, dt, g_m, h2_old, s["rhs"], None, t_m)
+        _solve(ctx, c, dtm, s["rhs"], out, t_m)
     else:
         raise ValueError(f"unknown scheme {scheme!r}")
     return s["conv"]
@@ -137,14 +147,17 @@ def predict(ctx, rule, dt, scheme, u0, t0, out: Optional[NodalSolution] = None) 
         _rt(ctx).copy(sol.u0, _rt(ctx).to_device(u0))
         sol.t0 = t0
     dts = _dts(rule, dt)
+    times = _node_times(rule, dt, t0)
+    _register_times(ctx, t0, times)
     for m in range(rule.M):
         up = sol.u0 if m == 0 else sol.u[m - 1]
+        t_prev = t0 if m == 0 else times[m - 1]
         if dts[m] == 0.0:
             _rt(ctx).copy(sol.u[m], up)
-            _caches(ctx, scheme, sol, rule.M, m, 1, dts)
+            _caches(ctx, scheme, sol, rule.M, m, 1, dts, times=times)
             continue
-        conv = _substep(ctx, scheme, up, dts[m], None, None, 0.0, None, None, None, sol.u[m])
-        _caches(ctx, scheme, sol, rule.M, m, 1, dts, conv)
+        conv = _substep(ctx, scheme, up, dts[m], None, None, 0.0, None, None, None, sol.u[m], t_prev, times[m])
+        _caches(ctx, scheme, sol, rule.M, m, 1, dts, conv, times=times)
     return sol
 
 
@@ -178,16 +191,19 @@ def sweep(ctx, rule: CollocationRule, weights: QuadratureWeights, dt: float, sch
         rt.copy(new.u0, sol.u0)
         new.t0 = sol.t0
     dts = _dts(rule, dt)
+    times = _node_times(rule, dt, new.t0)
+    _register_times(ctx, new.t0, times)
     for m in range(rule.M):
         up = new.u0 if m == 0 else new.u[m - 1]
+        t_prev = new.t0 if m == 0 else times[m - 1]
         gm = None if g is None else g[m]
         if dts[m] == 0.0:
-            _stage(ctx, up, up, 0.0, sol.f, weights.w_nn[m], dt, gm, None, new.u[m], None)
-            _caches(ctx, scheme, new, rule.M, m, 1, dts)
+            _stage(ctx, up, up, 0.0, sol.f, weights.w_nn[m], dt, gm, None, new.u[m], None, t_prev)
+            _caches(ctx, scheme, new, rule.M, m, 1, dts, times=times)
             continue
         conv = _substep(ctx, scheme, up, dts[m], sol.f, weights.w_nn[m], dt, gm, sol.h1[m],
-                        None if sol.h2 is None else sol.h2[m], new.u[m])
-        _caches(ctx, scheme, new, rule.M, m, 1, dts, conv)
+                        None if sol.h2 is None else sol.h2[m], new.u[m], t_prev, times[m])
+        _caches(ctx, scheme, new, rule.M, m, 1, dts, conv, times=times)
     return new
 
 
@@ -205,6 +221,8 @@ def _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g, out=None):
         rt.copy(new.u0, sol.u0)
         new.t0 = sol.t0
     dts = _dts(rule, dt)
+    times = _node_times(rule, dt, new.t0)
+    _register_times(ctx, new.t0, times)
     s = ctx.scratch()
     B = rt.empty(sol.u0.numel())
     rt.copy(B, sol.u0)
@@ -212,28 +230,29 @@ def _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g, out=None):
     for m in range(rule.M):
         gm = None if g is None else g[m]
         dtm = dts[m]
+        t_prev = new.t0 if m == 0 else times[m - 1]
         if dtm == 0.0:
-            _stage(ctx, B, B, 0.0, sol.f, weights.w_0n[m], dt, gm, None, new.u[m], None)
-            _caches(ctx, scheme, new, rule.M, m, 1, dts)
+            _stage(ctx, B, B, 0.0, sol.f, weights.w_0n[m], dt, gm, None, new.u[m], None, t_prev)
+            _caches(ctx, scheme, new, rule.M, m, 1, dts, times=times)
             continue
         up = new.u0 if m == 0 else new.u[m - 1]
         c = _coef(ctx, scheme, up, dtm)
         if scheme in ("euler", "si1"):
-            _stage(ctx, B, up, dtm, sol.f, weights.w_0n[m], dt, gm, sol.h1[m], s["rhs"], conv_up)
-            _solve(ctx, c, dtm, s["rhs"], new.u[m])
-            _caches(ctx, scheme, new, rule.M, m, 1, dts, conv_up)
+            _stage(ctx, B, up, dtm, sol.f, weights.w_0n[m], dt, gm, sol.h1[m], s["rhs"], conv_up, t_prev)
+            _solve(ctx, c, dtm, s["rhs"], new.u[m], times[m])
+            _caches(ctx, scheme, new, rule.M, m, 1, dts, conv_up, times=times)
             rt.lincomb(B, (1.0, B), (1.0, new.h1[m]), (-1.0, sol.h1[m]))      # S += h1_new - h1_old
         elif scheme == "si2":
             gnn = None
             if g is not None:
                 gnn = g[m] if m == 0 else rt.lincomb(tmp, (1.0, g[m]), (-1.0, g[m - 1]))
-            _stage(ctx, up, up, dtm, sol.f, weights.w_nn[m], dt, gnn, sol.h1[m], s["rhs"], conv_up)
-            _solve(ctx, c, dtm, s["rhs"], s["stage"])
-            _stage(ctx, B, s["stage"], dtm, sol.f, weights.w_0n[m], dt, gm, sol.h2[m], s["rhs"], conv_st)
-            _solve(ctx, c, dtm, s["rhs"], new.u[m])
-            _caches(ctx, scheme, new, rule.M, m, 1, dts, conv_up)
+            _stage(ctx, up, up, dtm, sol.f, weights.w_nn[m], dt, gnn, sol.h1[m], s["rhs"], conv_up, t_prev)
+            _solve(ctx, c, dtm, s["rhs"], s["stage"], times[m])
+            _stage(ctx, B, s["stage"], dtm, sol.f, weights.w_0n[m], dt, gm, sol.h2[m], s["rhs"], conv_st, times[m])
+            _solve(ctx, c, dtm, s["rhs"], new.u[m], times[m])
+            _caches(ctx, scheme, new, rule.M, m, 1, dts, conv_up, times=times)
             # S += dt_m (conv(stage) + D[C] u_m) - h2_old  (sdc.py:281)
-            rt.check(rt.lib.sisdc_apply_diffusion(ctx.h, c, new.u[m].data_ptr(), 0.0, tmp.data_ptr()),
+            rt.check(rt.lib.sisdc_apply_diffusion(ctx.h, c, new.u[m].data_ptr(), float(times[m]), tmp.data_ptr()),
                      "apply_diffusion")
             rt.lincomb(tmp, (1.0, conv_st), (1.0, tmp))
             rt.lincomb(B, (1.0, B), (dtm, tmp), (-1.0, sol.h2[m]))
