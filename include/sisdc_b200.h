@@ -140,6 +140,11 @@ int  sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art);
  * on a Dirichlet operator looks its data up here and fails with
  * SISDC_ERR_ARG for an unregistered time. */
 int  sisdc_op1d_set_boundary(sisdc_op1d* op, int n, const double* times, const double* gl, const double* gr);
+/* smooth_start (dgsem.py:574-589): out = u with every interior interface's
+ * two traces replaced by their mean (the periodic wrap too), for M node vectors;
+ * the MLSDC presmoothing hook of the coarse-to-fine solution transfer
+ * (mlsdc.py:139-140). */
+int  sisdc_smooth_start(sisdc_op1d* op, int M, const double* u, double* out);
 /* Persson-Peraire modal sensor (dgsem.py:537-559) -> nu_art (device, n_elem). */
 int  sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, double c_s, double* nu_art);
 

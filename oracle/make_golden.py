@@ -296,6 +296,22 @@ def gen_dirichlet():
     np.savez_compressed(os.path.join(OUT, "dirichlet.npz"), **out)
 
 
+def gen_presmooth():
+    """smooth_start (dgsem.py:574-589) on a state, and one cfg1/cfg2 SI-MLSDC step
+    with the presmoothing hook (mlsdc.py:139-140) on the coarse level, pinned PCG."""
+    out = {}
+    for tag, w in (("cfg1", CFG1), ("cfg2", CFG2)):
+        hier, ops = build_ref_hier(w)
+        hier.presmooth = lambda u, op=ops[0]: rd.smooth_start(op, u)
+        u0 = w.initial_state(ops[1].mesh.ref_nodes)
+        dt, _ = w.time_step(u0, rd.compute_delta(w.p_fine))
+        out[f"{tag}_smooth_fine_u0"] = rd.smooth_start(ops[1], u0)
+        with PcgPatch(1e-14, pcg) as pp:
+            out[f"{tag}_ps_pcg_u1"] = rm.run_mlsdc(hier, u0, 0.0, dt, w.n_cycles, strategy="fmg").end_value.copy()
+            out[f"{tag}_ps_pcg_iters1"] = np.array([it for it, _ in pp.log])
+    np.savez_compressed(os.path.join(OUT, "presmooth.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     if len(sys.argv) > 1 and sys.argv[1] == "nonincremental":
@@ -304,10 +320,14 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "dirichlet":
         gen_dirichlet()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "presmooth":
+        gen_presmooth()
+        sys.exit(0)
     gen_tables()
     gen_operators()
     gen_trajectories()
     gen_nonincremental()
     gen_dirichlet()
+    gen_presmooth()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -76,6 +76,7 @@ SIGNATURES = {
     "sisdc_op1d_tables": (I, [P, DP, DP, DP]),
     "sisdc_op1d_set_nu_art": (I, [P, P]),
     "sisdc_op1d_set_boundary": (I, [P, I, DP, DP, DP]),
+    "sisdc_smooth_start": (I, [P, I, P, P]),
     "sisdc_persson_viscosity": (I, [P, P, D, D, P]),
     "sisdc_apply_convection": (I, [P, P, D, P]),
     "sisdc_apply_diffusion": (I, [P, Coef, P, D, P]),

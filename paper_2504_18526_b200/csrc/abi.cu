@@ -398,6 +398,12 @@ int sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art) {
   return SISDC_OK;
 }
 
+int sisdc_smooth_start(sisdc_op1d* op, int M, const double* u, double* out) {
+  if (!op || !u || !out || M < 1) return SISDC_ERR_ARG;
+  if (op->dim == 2) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "smooth_start is built for 1-D meshes");
+  return launch_smooth_start(C(op), op->dev, M, u, out);
+}
+
 int sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, double c_s, double* nu_art) {
   if (!op || !u || !nu_art || !(kappa_s > 0)) return SISDC_ERR_ARG;
   if (op->dim == 2) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "the modal sensor is built for 1-D meshes");

@@ -143,7 +143,7 @@ static size_t cg_smem_bytes(int p1, int E, int nt) {
                            TabOff::size(p1) + E * p1 + 2 + 8 * p1 + 2);
 }
 
-template <bool CL, int P1>
+template <bool CL, int P1, bool DIR>
 __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   extern __shared__ __align__(16) double sm[];
   constexpr int P = P1 - 1;
@@ -197,8 +197,9 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   const double cP = s.Cs[min(el * P1 + P, NL - 1)], c0 = s.Cs[min(el * P1, NL - 1)];
   // Dirichlet outer faces (dgsem.py:282-289): outside value 0 in the operator (the
   // boundary data moves to the right-hand side), one-sided q and C, lift weight 1
-  const bool dirL = op.bc == SISDC_DIRICHLET && e0 + el == 0;
-  const bool dirR = op.bc == SISDC_DIRICHLET && e0 + el == op.ne - 1;
+  // (DIR: a separate instantiation, so the periodic kernel is unchanged)
+  const bool dirL = DIR && e0 + el == 0;
+  const bool dirR = DIR && e0 + el == op.ne - 1;
   const double cR = dirR ? cP : (last ? s.Cs[NL + 1] : s.Cs[min((el + 1) * P1, NL - 1)]);
   const double cL = dirL ? c0 : (first ? s.Cs[NL] : s.Cs[min(max(el * P1 - 1, 0), NL - 1)]);
   double dg = 1.0;
@@ -475,20 +476,20 @@ static int choose_partition(const Ctx* c, int ne, int p1, int& K, int& E) {
   return E * p1 <= 384 ? 0 : -1;
 }
 
-template <int P1>
+template <int P1, bool DIR>
 static int launch_cg_t(Ctx* c, CgArgs& A, int threads, size_t smem) {
   static bool attr_done[2] = {false, false};
   if (A.K == 1) {
     if (!attr_done[0]) {
-      cudaFuncSetAttribute(k_cg1d<false, P1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(k_cg1d<false, P1, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr_done[0] = true;
     }
-    k_cg1d<false, P1><<<1, threads, smem, c->stream>>>(A);
+    k_cg1d<false, P1, DIR><<<1, threads, smem, c->stream>>>(A);
     return c->after_launch("cg1d");
   }
   if (!attr_done[1]) {
-    cudaFuncSetAttribute(k_cg1d<true, P1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_cg1d<true, P1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_cg1d<true, P1, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_cg1d<true, P1, DIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_done[1] = true;
   }
   cudaLaunchConfig_t cfg{};
@@ -503,7 +504,7 @@ static int launch_cg_t(Ctx* c, CgArgs& A, int threads, size_t smem) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_cg1d<true, P1>, A);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_cg1d<true, P1, DIR>, A);
   if (e != cudaSuccess) return c->cuda(e, "cg1d cluster launch");
   return c->after_launch("cg1d");
 }
@@ -523,21 +524,21 @@ int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rh
   A.status = c->d_status; A.log_it = c->d_log_it; A.log_margin = c->d_log_margin; A.log_cap = c->log_cap;
   A.timing = c->d_timing;
   switch (p1) {
-    case 2: return launch_cg_t<2>(c, A, threads, smem);
-    case 3: return launch_cg_t<3>(c, A, threads, smem);
-    case 4: return launch_cg_t<4>(c, A, threads, smem);
-    case 5: return launch_cg_t<5>(c, A, threads, smem);
-    case 6: return launch_cg_t<6>(c, A, threads, smem);
-    case 7: return launch_cg_t<7>(c, A, threads, smem);
-    case 8: return launch_cg_t<8>(c, A, threads, smem);
-    case 9: return launch_cg_t<9>(c, A, threads, smem);
-    case 10: return launch_cg_t<10>(c, A, threads, smem);
-    case 11: return launch_cg_t<11>(c, A, threads, smem);
-    case 12: return launch_cg_t<12>(c, A, threads, smem);
-    case 13: return launch_cg_t<13>(c, A, threads, smem);
-    case 14: return launch_cg_t<14>(c, A, threads, smem);
-    case 15: return launch_cg_t<15>(c, A, threads, smem);
-    case 16: return launch_cg_t<16>(c, A, threads, smem);
+    case 2: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<2, true>(c, A, threads, smem) : launch_cg_t<2, false>(c, A, threads, smem);
+    case 3: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<3, true>(c, A, threads, smem) : launch_cg_t<3, false>(c, A, threads, smem);
+    case 4: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<4, true>(c, A, threads, smem) : launch_cg_t<4, false>(c, A, threads, smem);
+    case 5: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<5, true>(c, A, threads, smem) : launch_cg_t<5, false>(c, A, threads, smem);
+    case 6: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<6, true>(c, A, threads, smem) : launch_cg_t<6, false>(c, A, threads, smem);
+    case 7: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<7, true>(c, A, threads, smem) : launch_cg_t<7, false>(c, A, threads, smem);
+    case 8: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<8, true>(c, A, threads, smem) : launch_cg_t<8, false>(c, A, threads, smem);
+    case 9: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<9, true>(c, A, threads, smem) : launch_cg_t<9, false>(c, A, threads, smem);
+    case 10: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<10, true>(c, A, threads, smem) : launch_cg_t<10, false>(c, A, threads, smem);
+    case 11: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<11, true>(c, A, threads, smem) : launch_cg_t<11, false>(c, A, threads, smem);
+    case 12: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<12, true>(c, A, threads, smem) : launch_cg_t<12, false>(c, A, threads, smem);
+    case 13: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<13, true>(c, A, threads, smem) : launch_cg_t<13, false>(c, A, threads, smem);
+    case 14: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<14, true>(c, A, threads, smem) : launch_cg_t<14, false>(c, A, threads, smem);
+    case 15: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<15, true>(c, A, threads, smem) : launch_cg_t<15, false>(c, A, threads, smem);
+    case 16: return A.op.bc == SISDC_DIRICHLET ? launch_cg_t<16, true>(c, A, threads, smem) : launch_cg_t<16, false>(c, A, threads, smem);
     default: return c->fail(SISDC_ERR_UNSUPPORTED, "degree outside 1..15");
   }
 }

@@ -11,6 +11,7 @@ __host__ __device__ inline int eb_for(int p1) { int eb = 128 / p1; return eb < 1
 struct W16 { double v[MAXM]; };   // small host arrays passed by value
 
 // ------------------------------------------------------------ operators
+template <bool DIR>
 __global__ void k_apply_convection(Op1DDev op, const double* __restrict__ u, double* __restrict__ out) {
   extern __shared__ double sm[];
   const int p1 = op.p1, EB = eb_for(p1);
@@ -18,13 +19,14 @@ __global__ void k_apply_convection(Op1DDev op, const double* __restrict__ u, dou
   double* ut = st + TabOff::size(p1);
   int ebase = blockIdx.x * EB;
   load_tab(st, op.tab, p1);
-  load_tile(op, ut, u, ebase, EB);
+  load_tile<DIR>(op, ut, u, ebase, EB);
   __syncthreads();
   int t = threadIdx.x, el = t / p1, i = t - el * p1;
   if (el < EB && ebase + el < op.ne) out[(ebase + el) * p1 + i] = conv_node(op, st, ut, el, i);
 }
 
 // out = -B[C]u / m  (apply_diffusion, dgsem.py:251-309)
+template <bool DIR>
 __global__ void k_apply_diffusion(Op1DDev op, CoefDev c, const double* __restrict__ u, double* __restrict__ out) {
   extern __shared__ double sm[];
   const int p1 = op.p1, EB = eb_for(p1), T = (EB + 2) * p1;
@@ -34,14 +36,14 @@ __global__ void k_apply_diffusion(Op1DDev op, CoefDev c, const double* __restric
   double* qt = ct + T;
   int ebase = blockIdx.x * EB;
   load_tab(st, op.tab, p1);
-  load_tile(op, ut, u, ebase, EB);
-  coef_tile(op, c, ct, ebase, EB);
+  load_tile<DIR>(op, ut, u, ebase, EB);
+  coef_tile<DIR>(op, c, ct, ebase, EB);
   __syncthreads();
-  flux_q_tile(op, st, ut, ct, qt, EB, ebase);
+  flux_q_tile<DIR>(op, st, ut, ct, qt, EB, ebase);
   __syncthreads();
   int t = threadIdx.x, el = t / p1, i = t - el * p1;
   if (el < EB && ebase + el < op.ne)
-    out[(ebase + el) * p1 + i] = -sip_B_node(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i];
+    out[(ebase + el) * p1 + i] = -sip_B_node<DIR>(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i];
 }
 
 __global__ void k_coef_field(Op1DDev op, CoefDev c, double* __restrict__ out) {
@@ -65,6 +67,7 @@ struct CacheArgs {
   int* status;              // [0] first non-finite element
 };
 
+template <bool DIR>
 __global__ void k_node_eval(Op1DDev op_in, CacheArgs a) {
   extern __shared__ double sm[];
   const int m = a.m_first + blockIdx.y;
@@ -84,9 +87,9 @@ __global__ void k_node_eval(Op1DDev op_in, CacheArgs a) {
   const bool own = el < EB && ebase + el < op.ne;
   const int gi = (ebase + el) * p1 + i;
   load_tab(st, op.tab, p1);
-  load_tile(op, ut, um, ebase, EB);
+  load_tile<DIR>(op, ut, um, ebase, EB);
   CoefDev phys{SISDC_COEF_PHYS, 0.0, nullptr};
-  coef_tile(op, phys, ct, ebase, EB);
+  coef_tile<DIR>(op, phys, ct, ebase, EB);
   double dummy;
   const bool has_phys = op.nu_art != nullptr || phys_coef(op, 0, dummy);
   __syncthreads();
@@ -94,9 +97,9 @@ __global__ void k_node_eval(Op1DDev op_in, CacheArgs a) {
   double cm = own ? conv_node(op, st, ut, el, i) : 0.0;
   double f = cm;
   if (has_phys) {
-    flux_q_tile(op, st, ut, ct, qt, EB, ebase);
+    flux_q_tile<DIR>(op, st, ut, ct, qt, EB, ebase);
     __syncthreads();
-    if (own) f = cm + (-sip_B_node(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i]);
+    if (own) f = cm + (-sip_B_node<DIR>(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i]);
     __syncthreads();
   }
   if (own) {
@@ -114,13 +117,13 @@ __global__ void k_node_eval(Op1DDev op_in, CacheArgs a) {
   }
   // C_m frozen at u_{m-1}: SI for si1/si2, physical for euler (dgsem.py:365-366)
   CoefDev cmod = a.scheme == SISDC_EULER ? phys : CoefDev{SISDC_COEF_SI, dtm, up};
-  coef_tile(op, cmod, ct, ebase, EB);
-  if (a.conv_prev == nullptr) load_tile(opp, pt, up, ebase, EB);
+  coef_tile<DIR>(op, cmod, ct, ebase, EB);
+  if (a.conv_prev == nullptr) load_tile<DIR>(opp, pt, up, ebase, EB);
   __syncthreads();
-  flux_q_tile(op, st, ut, ct, qt, EB, ebase);
+  flux_q_tile<DIR>(op, st, ut, ct, qt, EB, ebase);
   __syncthreads();
   if (!own) return;
-  double d = -sip_B_node(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i];
+  double d = -sip_B_node<DIR>(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i];
   double cp = a.conv_prev ? a.conv_prev[gi] : conv_node(opp, st, pt, el, i);
   a.h1[(size_t)m * N + gi] = dtm * (cp + d);
   if (a.h2) a.h2[(size_t)m * N + gi] = dtm * (cm + d);
@@ -141,6 +144,7 @@ struct StageArgs {
   double* conv_out;
 };
 
+template <bool DIR>
 __global__ void k_stage_rhs(Op1DDev op, StageArgs a) {
   extern __shared__ double sm[];
   const int p1 = op.p1, EB = eb_for(p1);
@@ -148,7 +152,7 @@ __global__ void k_stage_rhs(Op1DDev op, StageArgs a) {
   double* ut = st + TabOff::size(p1);
   const int ebase = blockIdx.x * EB;
   load_tab(st, op.tab, p1);
-  load_tile(op, ut, a.conv_in, ebase, EB);
+  load_tile<DIR>(op, ut, a.conv_in, ebase, EB);
   __syncthreads();
   const int t = threadIdx.x, el = t / p1, i = t - el * p1;
   if (!(el < EB && ebase + el < op.ne)) return;
@@ -206,6 +210,25 @@ __global__ void k_lincomb(long long n, LinArgs a) {
     for (int k = 1; k < 4; ++k)
       if (a.v[k]) acc = acc + a.c[k] * a.v[k][t];
     a.out[t] = acc;
+  }
+}
+
+// smooth_start (dgsem.py:574-589): every interior interface (and the periodic
+// wrap) gets the mean of its two traces; blockIdx.y = node vector
+__global__ void k_smooth_start(Op1DDev op, const double* __restrict__ u, double* __restrict__ out) {
+  const int p1 = op.p1, P = p1 - 1, ne = op.ne;
+  const size_t mo = (size_t)blockIdx.y * op.n;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < op.n; t += gridDim.x * blockDim.x) {
+    const int e = t / p1, i = t - e * p1;
+    double v = u[mo + t];
+    if (i == P && (e + 1 < ne || op.bc == SISDC_PERIODIC)) {
+      const int en = e + 1 < ne ? e + 1 : 0;
+      v = 0.5 * (v + u[mo + (size_t)en * p1]);
+    } else if (i == 0 && (e > 0 || op.bc == SISDC_PERIODIC)) {
+      const int ep = e > 0 ? e - 1 : ne - 1;
+      v = 0.5 * (u[mo + (size_t)ep * p1 + P] + v);
+    }
+    out[mo + t] = v;
   }
 }
 
@@ -381,11 +404,11 @@ static dim3 tile_grid(int ne, int p1, int ny = 1) { int EB = eb_for(p1); return 
 static dim3 tile_block(int p1) { int t = eb_for(p1) * p1; return dim3((t + 31) / 32 * 32); }
 
 int launch_apply_convection(Ctx* c, const Op1DDev& op, const double* u, double* out) {
-  k_apply_convection<<<tile_grid(op.ne, op.p1), tile_block(op.p1), tile_smem(op.p1, 1), c->stream>>>(op, u, out);
+  (op.bc == SISDC_DIRICHLET ? k_apply_convection<true> : k_apply_convection<false>)<<<tile_grid(op.ne, op.p1), tile_block(op.p1), tile_smem(op.p1, 1), c->stream>>>(op, u, out);
   return c->after_launch("apply_convection");
 }
 int launch_apply_diffusion(Ctx* c, const Op1DDev& op, CoefDev k, const double* u, double* out) {
-  k_apply_diffusion<<<tile_grid(op.ne, op.p1), tile_block(op.p1), tile_smem(op.p1, 3), c->stream>>>(op, k, u, out);
+  (op.bc == SISDC_DIRICHLET ? k_apply_diffusion<true> : k_apply_diffusion<false>)<<<tile_grid(op.ne, op.p1), tile_block(op.p1), tile_smem(op.p1, 3), c->stream>>>(op, k, u, out);
   return c->after_launch("apply_diffusion");
 }
 int launch_coef_field(Ctx* c, const Op1DDev& op, CoefDev k, double* out) {
@@ -408,7 +431,7 @@ int launch_node_eval(Ctx* c, const Op1DDev& op, int mode, int scheme, int M, int
     a.grp.v[j] = bnd ? bnd[3 * M + j] : op.gr;
   }
   a.f = f; a.h1 = h1; a.h2 = h2; a.status = c->d_status;
-  k_node_eval<<<tile_grid(op.ne, op.p1, m_count), tile_block(op.p1), tile_smem(op.p1, 4), c->stream>>>(op, a);
+  (op.bc == SISDC_DIRICHLET ? k_node_eval<true> : k_node_eval<false>)<<<tile_grid(op.ne, op.p1, m_count), tile_block(op.p1), tile_smem(op.p1, 4), c->stream>>>(op, a);
   return c->after_launch("node_eval");
 }
 int launch_stage_rhs(Ctx* c, const Op1DDev& op, const double* base, const double* conv_in, double dt_m,
@@ -419,7 +442,7 @@ int launch_stage_rhs(Ctx* c, const Op1DDev& op, const double* base, const double
   a.base = base; a.conv_in = conv_in; a.dt_m = dt_m; a.f_old = f_old; a.M = M; a.dt = dt;
   for (int j = 0; j < M; ++j) a.w.v[j] = (f_old && w_row) ? w_row[j] : 0.0;
   a.g = g; a.h = h; a.rhs = rhs; a.conv_out = conv_out;
-  k_stage_rhs<<<tile_grid(op.ne, op.p1), tile_block(op.p1), tile_smem(op.p1, 1), c->stream>>>(op, a);
+  (op.bc == SISDC_DIRICHLET ? k_stage_rhs<true> : k_stage_rhs<false>)<<<tile_grid(op.ne, op.p1), tile_block(op.p1), tile_smem(op.p1, 1), c->stream>>>(op, a);
   return c->after_launch("stage_rhs");
 }
 int launch_defect(Ctx* c, int N, int M, const double* W, double dt, int incremental, const double* u0,
@@ -442,6 +465,11 @@ int launch_lincomb(Ctx* c, long long n, const double* coef, const double* const*
   if (nb < 1) nb = 1;
   k_lincomb<<<(unsigned)nb, 256, 0, c->stream>>>(n, a);
   return c->after_launch("lincomb");
+}
+int launch_smooth_start(Ctx* c, const Op1DDev& op, int M, const double* u, double* out) {
+  if (u == out) return c->fail(SISDC_ERR_ARG, "smooth_start needs distinct input and output");
+  k_smooth_start<<<dim3((op.n + 255) / 256, M), 256, 0, c->stream>>>(op, u, out);
+  return c->after_launch("smooth_start");
 }
 int launch_xfer_spatial(Ctx* c, const XferDev& x, int dir, const double* in, double* out) {
   int n = x.ne * (dir == 0 ? x.pf : x.pc);

@@ -91,6 +91,7 @@ __device__ __forceinline__ int wrap(int e, int ne) {
 // tile[(el+1)*p1 + i] = u[(ebase+el) wrapped, i] for el = -1..EB.  Dirichlet:
 // the ghost elements outside the mesh hold the outside state g_l / g_r
 // (only their face node enters: dgsem.py:179-194, 212-216, 282-284)
+template <bool DIR>
 __device__ __forceinline__ void load_tile(const Op1DDev& op, double* tile, const double* __restrict__ u, int ebase,
                                           int EB) {
   const int p1 = op.p1, ne = op.ne;
@@ -98,7 +99,7 @@ __device__ __forceinline__ void load_tile(const Op1DDev& op, double* tile, const
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
     int el = t / p1 - 1, i = t - (t / p1) * p1;
     const int eg = ebase + el;
-    if (op.bc == SISDC_DIRICHLET && (eg < 0 || eg >= ne)) tile[t] = eg < 0 ? op.gl : op.gr;
+    if (DIR && (eg < 0 || eg >= ne)) tile[t] = eg < 0 ? op.gl : op.gr;
     else tile[t] = u[wrap(eg, ne) * p1 + i];
   }
 }
@@ -129,6 +130,7 @@ __device__ __forceinline__ double conv_node(const Op1DDev& op, const double* st,
 
 // q = C * (2/dx) D u for every node of the tile (incl. halo elements); C tile must be filled.
 // Dirichlet ghosts carry the interior boundary node's q (one-sided flux, dgsem.py:285-286)
+template <bool DIR>
 __device__ __forceinline__ void flux_q_tile(const Op1DDev& op, const double* st, const double* ut,
                                             const double* ct, double* qt, int EB, int ebase) {
   const int p1 = op.p1;
@@ -137,7 +139,7 @@ __device__ __forceinline__ void flux_q_tile(const Op1DDev& op, const double* st,
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
     int e = t / p1, i = t - e * p1;
     const double* ue = ut + e * p1;
-    if (op.bc == SISDC_DIRICHLET) {
+    if (DIR) {
       const int eg = ebase + e - 1;
       if (eg < 0) { ue = ut + p1; i = 0; }                          // interior element 0, node 0
       else if (eg >= op.ne) { ue = ut + (e - 1) * p1; i = p1 - 1; }  // interior element ne-1, node P
@@ -151,6 +153,7 @@ __device__ __forceinline__ void flux_q_tile(const Op1DDev& op, const double* st,
 
 // SIP accumulator B_i (apply_diffusion = -B/m) at node (el,i); dgsem.py:270-308.
 // eg = global element; Dirichlet outer faces take adjoint-lift weight 1 (dgsem.py:196-201)
+template <bool DIR>
 __device__ __forceinline__ double sip_B_node(const Op1DDev& op, const double* st, const double* ut,
                                              const double* ct, const double* qt, int el, int i, int eg) {
   const int p1 = op.p1, P = p1 - 1;
@@ -172,8 +175,7 @@ __device__ __forceinline__ double sip_B_node(const Op1DDev& op, const double* st
     double G = -(0.5 * (qt[b - 1] + qt[b])) + (op.mu0 * (0.5 * (ct[b - 1] + ct[b]))) * jl;
     B -= G;
   }
-  const bool dir = op.bc == SISDC_DIRICHLET;
-  const double wr = (dir && eg == op.ne - 1) ? 1.0 : 0.5, wl = (dir && eg == 0) ? 1.0 : 0.5;
+  const double wr = (DIR && eg == op.ne - 1) ? 1.0 : 0.5, wl = (DIR && eg == 0) ? 1.0 : 0.5;
   B -= (op.s * ((wr * ct[b + P]) * jr)) * D[P * p1 + i];
   B -= (op.s * ((wl * ct[b]) * jl)) * D[i];
   return B;
@@ -181,13 +183,14 @@ __device__ __forceinline__ double sip_B_node(const Op1DDev& op, const double* st
 
 // fill a C tile from a coefficient descriptor (with halo); Dirichlet ghosts carry
 // the interior boundary node's coefficient (one-sided C, dgsem.py:287-288)
+template <bool DIR>
 __device__ __forceinline__ void coef_tile(const Op1DDev& op, const CoefDev& k, double* ct, int ebase, int EB) {
   int tot = (EB + 2) * op.p1;
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
     int el = t / op.p1 - 1, i = t - (t / op.p1) * op.p1;
     const int eg = ebase + el;
-    if (op.bc == SISDC_DIRICHLET && eg < 0) ct[t] = coef_at(op, k, 0, 0);
-    else if (op.bc == SISDC_DIRICHLET && eg >= op.ne) ct[t] = coef_at(op, k, op.ne - 1, op.p1 - 1);
+    if (DIR && eg < 0) ct[t] = coef_at(op, k, 0, 0);
+    else if (DIR && eg >= op.ne) ct[t] = coef_at(op, k, op.ne - 1, op.p1 - 1);
     else ct[t] = coef_at(op, k, wrap(eg, op.ne), i);
   }
 }

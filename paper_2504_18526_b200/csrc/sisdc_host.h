@@ -64,6 +64,7 @@ int launch_fas_restrict(Ctx* c, const XferDev& x, const double* Wf, double dt, i
 int launch_xfer_down(Ctx* c, const XferDev& x, int sdir, int tdir, const double* in, double* out);
 int launch_xfer_interp(Ctx* c, const XferDev& x, int accumulate, const double* uc, const double* vc, double* uf);
 int launch_lincomb(Ctx* c, long long n, const double* coef, const double* const* v, double* out);
+int launch_smooth_start(Ctx* c, const Op1DDev& op, int M, const double* u, double* out);
 int launch_persson(Ctx* c, const Op1DDev& op, const double* u, double kappa, double cs, double* nu_art);
 int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x);
 // 2-D (ops2d.cu)

@@ -30,7 +30,7 @@ from .collocation import gauss_lobatto
 from .runtime import get_runtime
 
 __all__ = ["Mesh1D", "DGOperator", "SolverError", "ArtificialViscosityParams", "SICoefficient",
-           "compute_delta", "cfl_number", "dt_from_cfl", "max_wave_speed"]
+           "compute_delta", "cfl_number", "dt_from_cfl", "max_wave_speed", "smooth_start"]
 
 
 def _diff_matrix(x) -> np.ndarray:
@@ -331,6 +331,20 @@ class DGOperator:
     def norm_l2(self, u) -> float:
         u3 = self.as_nodes(u)
         return float(((u3 ** 2) * self.rt.to_device(self.mass_node)).sum().sqrt())
+
+
+def smooth_start(op: DGOperator, u, out=None):
+    """Average the two trace values at every interior interface
+    (``dgsem.py:574-589``; the periodic wrap too); u may be one state or an
+    (M, N) node array."""
+    import torch
+    u = op.rt.to_device(u)
+    M = u.numel() // op.ndof
+    if out is None:
+        out = torch.empty_like(u)
+    op.rt.bind_stream()
+    op.rt.check(op.lib.sisdc_smooth_start(op.h, M, u.data_ptr(), out.data_ptr()), "smooth_start")
+    return out
 
 
 def max_wave_speed(op: DGOperator, u) -> float:

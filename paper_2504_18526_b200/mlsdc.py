@@ -72,8 +72,6 @@ class Hierarchy:
             raise ValueError("need exactly one transfer per adjacent level pair")
         if self.form not in ("incremental", "nonincremental"):
             raise ValueError(f"unknown sweep form {self.form!r}")
-        if self.presmooth is not None:
-            raise NotImplementedError("presmoothing (smooth_start) is next-tier on the GPU path")
         self.fine_sweeps = 0
         self.coarse_passes = 0
 
@@ -160,7 +158,12 @@ def _interp_up(hier: Hierarchy, i: int, dt: float) -> None:
     rt = up.ctx.rt
     buf = up.next_buffer()
     rt.copy(buf.u0, up.u0)
-    rt.check(rt.lib.sisdc_xfer_interp(hier.transfers[i].handle.h, 0, lv.sol.u.data_ptr(), None,
+    src = lv.sol.u
+    if hier.presmooth is not None:   # mlsdc.py:139-140, e.g. lambda u: smooth_start(coarse_op, u)
+        src = lv.work("presmooth", *lv.sol.u.shape)
+        for m in range(lv.sol.u.shape[0]):
+            rt.copy(src[m], hier.presmooth(lv.sol.u[m]))
+    rt.check(rt.lib.sisdc_xfer_interp(hier.transfers[i].handle.h, 0, src.data_ptr(), None,
                                       buf.u.data_ptr()), "interp_solution")
     up.sol = from_nodes(up.ctx, up.rule, dt, up.scheme, up.u0, up.t0, buf.u, out=buf)
 
@@ -312,7 +315,7 @@ def integrate_mlsdc(hier: Hierarchy, u0_fine, t0: float, dt: float, n_steps: int
 
 def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes: str = "radau_right",
                       n_coarse: int = 2, n_sweep: int = 1, post_sweep_on_finest: bool = True,
-                      restriction: str = None, form: str = "incremental") -> Hierarchy:
+                      restriction: str = None, form: str = "incremental", presmooth=None) -> Hierarchy:
     """Hierarchy of p-levels on one mesh as the reference CLI builds it
     (``cli.py:776-815``); ``make_op(degree)`` returns a DGOperator."""
     from .transfer import build_spatial_p_transfer, build_spatial_p_transfer_2d
@@ -331,5 +334,9 @@ def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes:
             spatial = build_spatial_p_transfer(degrees[lo], degrees[hi], ops[lo].mesh.n_elem, ops[lo].ncomp,
                                                restriction=restriction or "transpose")
         transfers.append(SpaceTimeTransfer(pair, spatial))
-    return Hierarchy(levels, transfers, n_coarse=n_coarse, n_sweep=n_sweep, form=form,
+    if presmooth == "smooth_start":   # the reference's interface averaging on the lower level
+        from .dgsem import smooth_start
+        lo_op = ops[0]
+        presmooth = lambda u: smooth_start(lo_op, u)   # noqa: E731
+    return Hierarchy(levels, transfers, n_coarse=n_coarse, n_sweep=n_sweep, form=form, presmooth=presmooth,
                      post_sweep_on_finest=post_sweep_on_finest)
