@@ -296,6 +296,41 @@ def gen_dirichlet():
     np.savez_compressed(os.path.join(OUT, "dirichlet.npz"), **out)
 
 
+def gen_htransfer():
+    """Spatial h-transfer (transfer.py:248-317): the block operators applied to
+    seeded vectors for both jump policies and the l2 projection, the p-transfer
+    l2 projection, and one SI-MLSDC step of cfg1's conv-diff with 2:1 element
+    coarsening (64 -> 32 elements at P = 8; pinned PCG: iteration counts)."""
+    out = {}
+    rng = np.random.default_rng(21)
+    for pol, kind in (("linear_blend", "embedded"), ("average", "embedded"), ("linear_blend", "l2")):
+        st = rt.build_spatial_h_transfer(6, 5, 1, kind, pol)
+        uc, uf = rng.standard_normal(6 * 6), rng.standard_normal(12 * 6)
+        tag = f"h_{pol}_{kind}"
+        out[f"{tag}_uc"], out[f"{tag}_uf"] = uc, uf
+        for d in ("interp", "project", "restrict"):
+            out[f"{tag}_{d}"] = st.apply(d, uc if d == "interp" else uf)
+    sp = rt.build_spatial_p_transfer(3, 7, 5, 1, "l2")
+    ufp = rng.standard_normal(5 * 8)
+    out["p_l2_uf"], out["p_l2_project"] = ufp, sp.apply("project", ufp)
+    w = CFG1
+    ops = [rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, ne, w.p_fine), ref_problem(w))
+           for ne in (w.n_elem // 2, w.n_elem)]
+    rules = [rc.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
+    wts = [rc.make_weights(r) for r in rules]
+    levels = [rm.Level(o, r, ww, "si2") for o, r, ww in zip(ops, rules, wts)]
+    pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_only")
+    spat = rt.build_spatial_h_transfer(w.n_elem // 2, w.p_fine, 1, "embedded", "linear_blend")
+    hier = rm.Hierarchy(levels, [rt.SpaceTimeTransfer(pair, spat)], n_coarse=2, n_sweep=1,
+                        form="incremental", post_sweep_on_finest=True)
+    u0 = w.initial_state(ops[1].mesh.ref_nodes)
+    dt, _ = w.time_step(u0, rd.compute_delta(w.p_fine))
+    with PcgPatch(1e-14, pcg) as pp:
+        out["hml_pcg_u1"] = rm.run_mlsdc(hier, u0, 0.0, dt, w.n_cycles, strategy="fmg").end_value.copy()
+        out["hml_pcg_iters1"] = np.array([it for it, _ in pp.log])
+    np.savez_compressed(os.path.join(OUT, "htransfer.npz"), **out)
+
+
 def gen_presmooth():
     """smooth_start (dgsem.py:574-589) on a state, and one cfg1/cfg2 SI-MLSDC step
     with the presmoothing hook (mlsdc.py:139-140) on the coarse level, pinned PCG."""
@@ -323,11 +358,15 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "presmooth":
         gen_presmooth()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "htransfer":
+        gen_htransfer()
+        sys.exit(0)
     gen_tables()
     gen_operators()
     gen_trajectories()
     gen_nonincremental()
     gen_dirichlet()
     gen_presmooth()
+    gen_htransfer()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

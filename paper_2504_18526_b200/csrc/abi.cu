@@ -535,7 +535,8 @@ int sisdc_xfer_create(sisdc_ctx* x, int n_elem, int pc1, int pf1, int Mc, int Mf
                       sisdc_xfer** out) {
   if (!x || !It || !Pt || !Isp || !Psp || !out) return SISDC_ERR_ARG;
   *out = nullptr;
-  if (n_elem < 1 || pc1 < 1 || pf1 < pc1 || pf1 > MAXP1) return x->c.fail(SISDC_ERR_ARG, "bad element sizes");
+  // pf1 up to 2 MAXP1: an h-transfer parent maps to its contiguous pair of children
+  if (n_elem < 1 || pc1 < 1 || pf1 < pc1 || pf1 > 2 * MAXP1) return x->c.fail(SISDC_ERR_ARG, "bad element sizes");
   if (Mc < 1 || Mf < Mc || Mf > MAXM) return x->c.fail(SISDC_ERR_ARG, "bad node counts");
   sisdc_xfer* t = new (std::nothrow) sisdc_xfer();
   if (!t) return SISDC_ERR_ARG;

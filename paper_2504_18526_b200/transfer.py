@@ -91,6 +91,8 @@ class SpatialTransfer:
         h = _xfer_handle(self, None)
         dirn = {"interp": 0, "project": 1, "restrict": 2}[direction]
         npn = self.np_fine if dirn == 0 else self.np_coarse
+        if self.kind == "h" and dirn == 0:
+            npn = 2 * self.np_fine      # a parent's child pair
         out = rt.empty(self.ncomp * self.ne_coarse * (npn * npn if self.kind == "p2d" else npn))
         rt.bind_stream()
         rt.check(rt.lib.sisdc_xfer_spatial(h.h, dirn, u.data_ptr(), out.data_ptr()), "xfer_spatial")
@@ -135,6 +137,62 @@ def build_spatial_p_transfer(p_coarse: int, p_fine: int, n_elem: int, ncomp: int
                            {"interp": interp, "project": project, "restrict": restrict}, projection_kind)
 
 
+def build_spatial_h_transfer(ne_coarse: int, p: int, ncomp: int = 1, projection_kind: str = "embedded",
+                             jump_policy: str = "linear_blend") -> SpatialTransfer:
+    """2:1 element coarsening (``transfer.py:248-317``): each coarse parent owns
+    two children.  Interpolation evaluates the parent on each child half;
+    the embedded projection evaluates each child on its half of the parent
+    (averaging at the centre node) after a jump preprocessor on the child
+    pair (linear_blend: ramps removing the interface jump; average: mean of
+    the two interface values); the l2 projection is the Galerkin projection of
+    the piecewise child data.  On the GPU the pair of children is one
+    contiguous 2(P+1)-node block per parent, so the p-transfer kernels apply
+    the stacked blocks unchanged."""
+    from .collocation import gauss_legendre
+    p1 = p + 1
+    xi = _gll_reference(p1)
+    IL = lagrange_matrix(xi, 0.5 * (xi - 1.0))
+    IR = lagrange_matrix(xi, 0.5 * (xi + 1.0))
+    B = np.eye(2 * p1)
+    if jump_policy == "linear_blend":
+        d = np.zeros(2 * p1)
+        d[p1] = 1.0
+        d[p1 - 1] = -1.0
+        B[:p1] += np.outer(0.25 * (1.0 + xi), d)
+        B[p1:] -= np.outer(0.25 * (1.0 - xi), d)
+    elif jump_policy == "average":
+        B[p1 - 1] = 0.0
+        B[p1 - 1, p1 - 1] = B[p1 - 1, p1] = 0.5
+        B[p1] = B[p1 - 1]
+    else:
+        raise ValueError(f"unknown jump policy {jump_policy!r}")
+    if projection_kind == "embedded":
+        E = np.zeros((p1, 2 * p1))
+        for i, x in enumerate(xi):
+            if x < 0.0:
+                E[i, :p1] = lagrange_matrix(xi, np.array([2.0 * x + 1.0]))[0]
+            elif x > 0.0:
+                E[i, p1:] = lagrange_matrix(xi, np.array([2.0 * x - 1.0]))[0]
+            else:
+                E[i, p1 - 1] = E[i, p1] = 0.5
+        P = E @ B
+    elif projection_kind == "l2":
+        gx, gw = gauss_legendre(p1 + 3)
+        Lp = lagrange_matrix(xi, gx)
+        G = Lp.T @ (gw[:, None] * Lp)
+        BL = lagrange_matrix(xi, 0.5 * gx - 0.5).T @ (0.5 * gw[:, None] * lagrange_matrix(xi, gx))
+        BR = lagrange_matrix(xi, 0.5 * gx + 0.5).T @ (0.5 * gw[:, None] * lagrange_matrix(xi, gx))
+        Gi = np.linalg.inv(G)
+        P = np.concatenate((Gi @ BL, Gi @ BR), axis=1)
+    else:
+        raise ValueError(f"unknown projection kind {projection_kind!r}")
+    interp = np.concatenate((IL, IR), axis=0)          # (2 p1, p1): parent -> child pair
+    return SpatialTransfer("h", ncomp, ne_coarse, 2 * ne_coarse, p1, p1,
+                           {"interp_lr": np.stack((IL, IR)), "project_lr": (P[:, :p1], P[:, p1:]),
+                            "interp": interp, "project": P, "restrict": interp.T.copy()},
+                           projection_kind, jump_policy)
+
+
 class _XferHandle:
     def __init__(self, spatial: SpatialTransfer, temporal: Optional[TransferPair]):
         rt = get_runtime()
@@ -152,6 +210,9 @@ class _XferHandle:
         if spatial.kind == "p2d":   # element slabs of (P+1)^2 nodes, matrices applied in x and y
             rt.check(rt.lib.sisdc_xfer2d_create(rt.h, spatial.ne_fine * spatial.ncomp, spatial.np_coarse,
                                                 spatial.np_fine, Mc, Mf, *ptrs, C.byref(h)), "xfer2d_create")
+        elif spatial.kind == "h":   # parent element <-> contiguous child pair of 2 (P+1) nodes
+            rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_coarse, spatial.np_coarse, 2 * spatial.np_fine, Mc, Mf,
+                                              *ptrs, C.byref(h)), "xfer_create")
         else:
             rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_fine, spatial.np_coarse, spatial.np_fine, Mc, Mf,
                                               *ptrs, C.byref(h)), "xfer_create")
@@ -199,8 +260,8 @@ class SpaceTimeTransfer:
 
     @property
     def handle(self) -> _XferHandle:
-        if self.spatial.kind not in ("p", "p2d"):
-            raise NotImplementedError("the GPU path builds spatial p-transfers")
+        if self.spatial.kind not in ("p", "p2d", "h"):
+            raise NotImplementedError("identity spatial transfers have no GPU handle")
         return _xfer_handle(self.spatial, self.temporal)
 
     def _down(self, sdir, tdir, nodes):

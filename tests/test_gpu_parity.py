@@ -278,3 +278,35 @@ def test_presmooth_parity(rt, golden, tag, w):
     assert abs(sum(its) - sum(ref)) <= 1
     assert l2rel(sol.u[-1], G[f"{tag}_ps_pcg_u1"]) < 1e-11
     rt.raise_on_failure()
+
+
+def test_h_transfer_and_h_mlsdc(rt, golden):
+    """Spatial h-coarsening on the GPU (transfer.py:248-317): the transfer
+    kernels on the stacked child-pair blocks vs the reference's apply(), and one
+    SI-MLSDC step of cfg1 with 2:1 element coarsening (64 -> 32 elements, P = 8)
+    vs the reference with the pinned PCG (identical iteration sequence)."""
+    from paper_2504_18526_b200 import collocation, mlsdc
+    from paper_2504_18526_b200.transfer import (SpaceTimeTransfer, build_spatial_h_transfer,
+                                                build_temporal_transfer)
+    G = golden["htransfer"]
+    for pol, kind in (("linear_blend", "embedded"), ("average", "embedded"), ("linear_blend", "l2")):
+        st = build_spatial_h_transfer(6, 5, 1, kind, pol)
+        tag = f"h_{pol}_{kind}"
+        assert rel(st.apply("interp", G[f"{tag}_uc"]), G[f"{tag}_interp"]) < 1e-14
+        assert rel(st.apply("project", G[f"{tag}_uf"]), G[f"{tag}_project"]) < 1e-14
+        assert rel(st.apply("restrict", G[f"{tag}_uf"]), G[f"{tag}_restrict"]) < 1e-14
+    w = CFG1
+    T = golden["trajectories"]
+    dt, u0 = float(T["cfg1_dt"]), T["cfg1_u0"]
+    ops = [gpu_op(w, w.p_fine, ne) for ne in (w.n_elem // 2, w.n_elem)]
+    rules = [collocation.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
+    levels = [mlsdc.Level(o, r, collocation.make_weights(r), "si2") for o, r in zip(ops, rules)]
+    st = SpaceTimeTransfer(build_temporal_transfer(rules[0], rules[1]),
+                           build_spatial_h_transfer(w.n_elem // 2, w.p_fine))
+    h = mlsdc.Hierarchy(levels, [st], n_coarse=2, n_sweep=1)
+    n0 = rt.status()[2]
+    sol = mlsdc.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, strategy="fmg")
+    its, _ = new_log_slice(rt, n0)
+    assert its == G["hml_pcg_iters1"].tolist()
+    assert l2rel(sol.u[-1], G["hml_pcg_u1"]) < 1e-11
+    rt.raise_on_failure()

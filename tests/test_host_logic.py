@@ -62,3 +62,25 @@ def test_mesh_validation():
     with pytest.raises(ValueError):
         Mesh1D(0.0, 1.0, 4, 3, bc="outflow")
     assert dt_from_cfl(2.0, 0.1, 1.0, 8) == pytest.approx(2.0 * 0.1 / (2 * compute_delta(8)))
+
+
+def test_h_transfer_blocks_match_reference(golden):
+    """Host-side h-transfer blocks (transfer.py:248-317) applied per parent
+    element reproduce the reference's apply() for every jump policy and the l2
+    projection; the p-transfer l2 projection likewise."""
+    import numpy as np
+    from paper_2504_18526_b200.transfer import build_spatial_h_transfer, build_spatial_p_transfer
+    G = golden["htransfer"]
+    for pol, kind in (("linear_blend", "embedded"), ("average", "embedded"), ("linear_blend", "l2")):
+        st = build_spatial_h_transfer(6, 5, 1, kind, pol)
+        tag = f"h_{pol}_{kind}"
+        uc, uf = G[f"{tag}_uc"], G[f"{tag}_uf"]
+        I, P, R = st.blocks["interp"], st.blocks["project"], st.blocks["restrict"]
+        got = {"interp": np.einsum("ij,ej->ei", I, uc.reshape(6, 6)).reshape(-1),
+               "project": np.einsum("ij,ej->ei", P, uf.reshape(6, 12)).reshape(-1),
+               "restrict": np.einsum("ij,ej->ei", R, uf.reshape(6, 12)).reshape(-1)}
+        for d, v in got.items():
+            assert np.abs(v - G[f"{tag}_{d}"]).max() < 1e-13, (tag, d)
+    sp = build_spatial_p_transfer(3, 7, 5, 1, "l2")
+    v = np.einsum("ij,ej->ei", sp.blocks["project"], G["p_l2_uf"].reshape(5, 8)).reshape(-1)
+    assert np.abs(v - G["p_l2_project"]).max() < 1e-13
