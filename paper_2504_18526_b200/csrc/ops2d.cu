@@ -1760,27 +1760,11 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     double* const Un = (k & 1) ? A.U : A.U2;     // register selects: no local-memory array
     const double* const Up = (k & 1) ? A.U2 : A.U;
     double ru = 0.0, rr = 0.0;
-    if (vec) {   // blocks claim 1024-pair chunks dynamically (balance + DRAM page locality)
+    if (vec) {   // grid-stride over in-field pairs (no per-chunk block barrier)
       const long long nh = nn >> 1;
-      const unsigned nchunk = (unsigned)((nh + 1023) >> 10);
-      unsigned* ctr = reinterpret_cast<unsigned*>(A.scal) + (k & 1);
-      __shared__ unsigned chs[2];
-      if (threadIdx.x == 0) chs[0] = atomicAdd(ctr, 1u);
-      __syncthreads();
-      for (int it = 0;; ++it) {
-        const unsigned ch = chs[it & 1];
-        if (ch >= nchunk) break;
-        if (threadIdx.x == 0) chs[(it + 1) & 1] = atomicAdd(ctr, 1u);
-        const long long h0 = (long long)ch << 10;
-#pragma unroll 1
-        for (int i = 0; i < 4; ++i) {
-          const long long h = h0 + i * 256 + threadIdx.x;
-          if (h < nh) {
-            if constexpr (DEFER) cg_update2s<NC>(A, Un, h, nh, alpha, beta, ru, rr);
-            else cg_update2<NC>(A, Un, h, nh, alpha, beta, ru, rr);
-          }
-        }
-        __syncthreads();
+      for (long long h = gtid; h < nh; h += nthr) {
+        if constexpr (DEFER) cg_update2s<NC>(A, Un, h, nh, alpha, beta, ru, rr);
+        else cg_update2<NC>(A, Un, h, nh, alpha, beta, ru, rr);
       }
     } else {
       for (long long f = gtid; f < nn; f += nthr) {
