@@ -165,6 +165,15 @@ int  sisdc_stage_rhs(sisdc_op1d* op, const double* base, const double* conv_in, 
                      const double* f_old, int M, const double* w_row, double dt,
                      const double* g_m, const double* h_old, double t,
                      double* rhs, double* conv_out);
+/* sisdc_stage_rhs followed by sisdc_implicit_solve (coefficient k, shift a,
+ * the stage's convection at t_conv, the solve at t_solve): x = S(rhs).  On a
+ * 1-D operator the stage is computed inside the CG launch's prologue (one
+ * launch per substep half instead of two; same arithmetic); elsewhere it runs
+ * as the two calls, with the rhs in rhs_scratch. */
+int  sisdc_stage_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* base, const double* conv_in,
+                       double dt_m, const double* f_old, int M, const double* w_row, double dt,
+                       const double* g_m, const double* h_old, double t_conv, double t_solve,
+                       double* rhs_scratch, double* conv_out, double* x);
 /* Node caches f, h1, h2 for nodes m_first..m_first+m_count-1 (sdc.py:77-119):
  * f = eval_rhs(u_m); h1 = dt_m (conv(u_{m-1}) + D[C_m] u_m);
  * h2 = dt_m (conv(u_m) + D[C_m] u_m) with C_m the scheme's coefficient frozen

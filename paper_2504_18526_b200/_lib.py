@@ -84,6 +84,7 @@ SIGNATURES = {
     "sisdc_coef_field": (I, [P, Coef, P]),
     "sisdc_implicit_solve": (I, [P, Coef, D, P, D, P]),
     "sisdc_stage_rhs": (I, [P, P, P, D, P, I, DP, D, P, P, D, P, P]),
+    "sisdc_stage_solve": (I, [P, Coef, D, P, P, D, P, I, DP, D, P, P, D, D, P, P, P]),
     "sisdc_node_caches": (I, [P, I, I, I, I, P, P, P, DP, D, DP, P, P, P]),
     "sisdc_eval_rhs_nodes": (I, [P, I, P, DP, P]),
     "sisdc_collocation_defect": (I, [P, I, DP, D, I, P, P, P, D, P, P]),

@@ -476,6 +476,29 @@ int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* r
   return launch_cg1d(C(op), d, coef(k), a, rhs, x);
 }
 
+int sisdc_stage_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* base, const double* conv_in,
+                      double dt_m, const double* f_old, int M, const double* w_row, double dt, const double* g_m,
+                      const double* h_old, double t_conv, double t_solve, double* rhs_scratch, double* conv_out,
+                      double* x) {
+  if (!op || !base || !conv_in || !x || M < 0 || M > MAXM || (f_old && !w_row)) return SISDC_ERR_ARG;
+  if (int rc = check_coef(C(op), k)) return rc;
+  const bool fuse = op->dim == 1 && !op->parted() && a != 0.0 && k.kind != SISDC_COEF_NONE;
+  if (!fuse) {   // stage rhs into the scratch vector, then the solve
+    if (!rhs_scratch) return C(op)->fail(SISDC_ERR_ARG, "stage_solve needs a rhs scratch vector here");
+    if (int rc = sisdc_stage_rhs(op, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, t_conv, rhs_scratch,
+                                 conv_out))
+      return rc;
+    return sisdc_implicit_solve(op, k, a, rhs_scratch, t_solve, x);
+  }
+  Op1DDev d;
+  if (int rc = dev_at(op, t_solve, d)) return rc;
+  StageFuse sf{};
+  sf.base = base; sf.conv_in = conv_in; sf.f_old = f_old; sf.w_row = w_row; sf.g = g_m; sf.h = h_old;
+  sf.conv_out = conv_out; sf.dt_m = dt_m; sf.dt = dt; sf.M = M;
+  if (int rc = bc_at(op, t_conv, sf.gl, sf.gr)) return rc;
+  return launch_cg1d(C(op), d, coef(k), a, nullptr, x, &sf);
+}
+
 int sisdc_stage_rhs(sisdc_op1d* op, const double* base, const double* conv_in, double dt_m, const double* f_old,
                     int M, const double* w_row, double dt, const double* g_m, const double* h_old, double t,
                     double* rhs, double* conv_out) {

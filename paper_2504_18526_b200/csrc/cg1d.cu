@@ -29,7 +29,23 @@ namespace cg = cooperative_groups;
 
 namespace sisdc {
 
+// fused stage rhs (sdc.py:218-237): x0 = rhs = base + dt W f_old (+ g) + dt_m conv(conv_in) - h,
+// computed in the CG prologue with k_stage_rhs's exact operations (bitwise)
+struct CgStage {
+  const double* base;
+  const double* conv_in;
+  const double* f_old;
+  const double* g;
+  const double* h;
+  double* conv_out;
+  double dt_m, dt, gl, gr;   // gl / gr: Dirichlet outside states at conv_in's time
+  int M;
+  double w[MAXM];
+};
+
 struct CgArgs {
+  int stage;        // 1: x0 from the fused stage rhs (sg), else x0 = rhs
+  CgStage sg;
   Op1DDev op;
   CoefDev coef;
   double a;
@@ -179,9 +195,46 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   if (stamp) A.timing[0] = clock64();
   for (int t = threadIdx.x; t < TabOff::size(P1); t += blockDim.x) s.st[t] = op.tab[t];
   double ci = 0.0, x = 0.0;
+  if (A.stage) {   // x0 = the stage rhs of this substep, conv(conv_in) as conv_node (ops1d.cu)
+    const CgStage& g = A.sg;
+    const size_t gi = (size_t)e0 * P1 + L;
+    if (own) s.Ub[oL] = g.conv_in[gi];   // staging (s.Ub is rewritten with u0 after the setup barriers)
+    __syncthreads();
+    if (own) {
+      const double* ue = s.Ub + ob;
+      const double* DTWs = s.st + TabOff::DTW(P1);
+      double v = 0.0;
+#pragma unroll 4
+      for (int k = 0; k < P1; ++k) v = fma(DTWs[i * P1 + k], flux(op, ue[k]), v);
+      const int eg = e0 + el;
+      if (i == P) {
+        const double nb = (DIR && eg == op.ne - 1) ? g.gr
+                          : (last ? g.conv_in[(size_t)wrap(eg + 1, op.ne) * P1] : s.Ub[ob + P1P]);
+        v -= rusanov(op, ue[P], nb);
+      }
+      if (i == 0) {
+        const double nb = (DIR && eg == 0) ? g.gl
+                          : (first ? g.conv_in[(size_t)wrap(eg - 1, op.ne) * P1 + P] : s.Ub[ob - P1P + P]);
+        v += rusanov(op, nb, ue[0]);
+      }
+      const double cv = v * s.st[TabOff::minv(P1) + i];
+      if (g.conv_out) g.conv_out[gi] = cv;
+      double q = 0.0;
+      if (g.f_old) {
+        double acc = 0.0;
+        for (int j = 0; j < g.M; ++j) acc = fma(g.w[j], g.f_old[(size_t)j * op.n + gi], acc);
+        q = g.dt * acc;
+      }
+      if (g.g) q = q + g.g[gi];
+      double rr = (g.base[gi] + q) + g.dt_m * cv;
+      if (g.h) rr = rr - g.h[gi];
+      x = rr;
+    }
+  } else if (own) {
+    x = A.rhs[(size_t)e0 * P1 + L];   // x0 = rhs
+  }
   if (own) {
     ci = coef_at(op, A.coef, e0 + el, i);
-    x = A.rhs[(size_t)e0 * P1 + L];   // x0 = rhs
     s.Cs[L] = ci;
     s.Xs[oL] = x;
   }
@@ -509,7 +562,8 @@ static int launch_cg_t(Ctx* c, CgArgs& A, int threads, size_t smem) {
   return c->after_launch("cg1d");
 }
 
-int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x) {
+int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x,
+                const StageFuse* sf) {
   const int p1 = op.p1;
   int K, E;
   if (choose_partition(c, op.ne, p1, K, E))
@@ -520,6 +574,14 @@ int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rh
   size_t smem = cg_smem_bytes(p1, E, threads);
   CgArgs A{};
   A.op = op; A.coef = k; A.a = a; A.rhs = rhs; A.x = x;
+  if (sf) {
+    if (sf->M > MAXM) return c->fail(SISDC_ERR_ARG, "too many collocation nodes");
+    A.stage = 1;
+    A.sg.base = sf->base; A.sg.conv_in = sf->conv_in; A.sg.f_old = sf->f_old; A.sg.g = sf->g; A.sg.h = sf->h;
+    A.sg.conv_out = sf->conv_out; A.sg.dt_m = sf->dt_m; A.sg.dt = sf->dt; A.sg.gl = sf->gl; A.sg.gr = sf->gr;
+    A.sg.M = sf->M;
+    for (int j = 0; j < sf->M; ++j) A.sg.w[j] = (sf->f_old && sf->w_row) ? sf->w_row[j] : 0.0;
+  }
   A.rtol2 = c->rtol * c->rtol; A.maxit = c->maxit; A.E = E; A.K = K;
   A.status = c->d_status; A.log_it = c->d_log_it; A.log_margin = c->d_log_margin; A.log_cap = c->log_cap;
   A.timing = c->d_timing;

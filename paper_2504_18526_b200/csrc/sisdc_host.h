@@ -66,7 +66,20 @@ int launch_xfer_interp(Ctx* c, const XferDev& x, int accumulate, const double* u
 int launch_lincomb(Ctx* c, long long n, const double* coef, const double* const* v, double* out);
 int launch_smooth_start(Ctx* c, const Op1DDev& op, int M, const double* u, double* out);
 int launch_persson(Ctx* c, const Op1DDev& op, const double* u, double kappa, double cs, double* nu_art);
-int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x);
+// stage rhs fused into the 1-D CG prologue (sisdc_stage_solve)
+struct StageFuse {
+  const double* base;
+  const double* conv_in;
+  const double* f_old;
+  const double* w_row;
+  const double* g;
+  const double* h;
+  double* conv_out;
+  double dt_m, dt, gl, gr;
+  int M;
+};
+int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x,
+                const StageFuse* sf = nullptr);
 // 2-D (ops2d.cu)
 int launch2_conv(Ctx* c, const Op2DDev& op, const double* u, double* out);
 int launch2_sip(Ctx* c, const Op2DDev& op, CoefDev k, const double* u, double* out);

@@ -122,18 +122,32 @@ def _solve(ctx, coef: Coef, a, rhs, out, t=0.0):
              "implicit_solve")
 
 
+def _stage_solve(ctx, coef: Coef, a, base, conv_in, dt_m, f_old, w_row, dt, g_m, h_old, t_conv, t_solve,
+                 rhs, conv_out, out):
+    """Stage rhs + implicit solve; on 1-D levels the stage runs inside the CG
+    launch (``sisdc_stage_solve``), elsewhere as two calls."""
+    rt = _rt(ctx)
+    M = 0 if f_old is None else f_old.shape[0]
+    wa, wp = _lib.darr(w_row if w_row is not None else np.zeros(1))
+    rt.check(rt.lib.sisdc_stage_solve(
+        ctx.h, coef, float(a), base.data_ptr(), conv_in.data_ptr(), float(dt_m),
+        None if f_old is None else f_old.data_ptr(), M, wp if f_old is not None else None, float(dt),
+        None if g_m is None else g_m.data_ptr(), None if h_old is None else h_old.data_ptr(),
+        float(t_conv), float(t_solve), rhs.data_ptr(), None if conv_out is None else conv_out.data_ptr(),
+        out.data_ptr()), "stage_solve")
+
+
 def _substep(ctx, scheme, up, dtm, f_old, w_row, dt, g_m, h1_old, h2_old, out, t_prev=0.0, t_m=0.0):
     """One SI substep into ``out`` (predictor when f_old/h are None):
     conv(u_{m-1}) at t_{m-1}, the solves and conv(stage) at t_m (sdc.py:225-237)."""
     s = ctx.scratch()
     c = _coef(ctx, scheme, up, dtm)
-    _stage(ctx, up, up, dtm, f_old, w_row, dt, g_m, h1_old, s["rhs"], s["conv"], t_prev)
     if scheme in ("euler", "si1"):
-        _solve(ctx, c, dtm, s["rhs"], out, t_m)
+        _stage_solve(ctx, c, dtm, up, up, dtm, f_old, w_row, dt, g_m, h1_old, t_prev, t_m, s["rhs"], s["conv"], out)
     elif scheme == "si2":
-        _solve(ctx, c, dtm, s["rhs"], s["stage"], t_m)
-        _stage(ctx, up, s["stage"], dtm, f_old, w_row, dt, g_m, h2_old, s["rhs"], None, t_m)
-        _solve(ctx, c, dtm, s["rhs"], out, t_m)
+        _stage_solve(ctx, c, dtm, up, up, dtm, f_old, w_row, dt, g_m, h1_old, t_prev, t_m, s["rhs"], s["conv"],
+                     s["stage"])
+        _stage_solve(ctx, c, dtm, up, s["stage"], dtm, f_old, w_row, dt, g_m, h2_old, t_m, t_m, s["rhs"], None, out)
     else:
         raise ValueError(f"unknown scheme {scheme!r}")
     return s["conv"]
