@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SISDC_ABI_VERSION 1
+#define SISDC_ABI_VERSION 2
 
 enum sisdc_status {
   SISDC_OK = 0,
@@ -43,7 +43,8 @@ enum sisdc_status {
 enum sisdc_problem {
   SISDC_CONVDIFF = 0, SISDC_BURGERS = 1,        /* 1-D, problems.py:25-82               */
   SISDC_EULER2D = 2,                            /* 2-D Euler / NS (isotropic viscosity)  */
-  SISDC_ADVECTION2D = 3, SISDC_BURGERS2D = 4    /* 2-D scalar (cross-dimension checks)   */
+  SISDC_ADVECTION2D = 3, SISDC_BURGERS2D = 4,   /* 2-D scalar (cross-dimension checks)   */
+  SISDC_CNS1D = 5                               /* 1-D CompressibleFlow, problems.py:160-240 */
 };
 enum sisdc_bc { SISDC_PERIODIC = 0, SISDC_DIRICHLET = 1 };       /* Mesh1D.bc         */
 enum sisdc_scheme { SISDC_EULER = 0, SISDC_SI1 = 1, SISDC_SI2 = 2 }; /* integrators.py:26 */
@@ -56,7 +57,10 @@ enum sisdc_coef_kind {
   SISDC_COEF_FIELD = 2,     /* (n_elem, P+1) scalar field at ptr                 */
   SISDC_COEF_SI = 3,        /* (value/2) A_c(u_b)^2 + A_d + nu_art, u_b = ptr,
                                value = dt_m (dgsem.py:356-396, scheme si1/si2)    */
-  SISDC_COEF_PHYS = 4       /* physical A_d + nu_art (dgsem.py:313-326)          */
+  SISDC_COEF_PHYS = 4,      /* physical A_d + nu_art (dgsem.py:313-326); systems:
+                               A_d(u_b), u_b = ptr                               */
+  SISDC_COEF_MATRIX = 5     /* (n_elem, P+1, ncomp, ncomp) matrix field at ptr
+                               (dgsem.py:229-239 kind "matrix"; 1-D CNS only)    */
 };
 typedef struct { int kind; double value; const double* ptr; } sisdc_coef;
 
@@ -75,6 +79,10 @@ typedef struct {
   double speed;      /* ConvectionDiffusion.speed         */
   double nu;         /* physical viscosity (0 => None)    */
   double penalty;    /* DGOperator penalty_const (2.0)    */
+  /* SISDC_CNS1D (ncomp 3, periodic): CompressibleFlow(gamma, R_gas, eta, Pr),
+   * problems.py:171-187; the implicit system is non-symmetric, so its solve is
+   * the pinned Jacobi-BiCGStab of oracle/cg.py (replaces splu, dgsem.py:503-533) */
+  double gamma, eta, prandtl;
 } sisdc_op1d_desc;
 
 /* 2-D tensor-product DG-SEM on a uniform periodic nex x ney mesh of

@@ -84,3 +84,92 @@ def pcg_cg1(A, diag, b, x0, rtol=1e-14, maxit=1000):
 
 
 pcg = pcg_cg1
+
+
+def element_block_preconditioner(Amat, nc, ne, p1):
+    """Element-block Jacobi: y = inv(A_ee) v per element e, A_ee the
+    (nc (P+1))^2 diagonal block of the assembled M + a B[C] with rows/cols
+    ordered (field, node); y_r = sum_j inv(A_ee)[r, j] v_j."""
+    A = Amat.tocsr()
+    blocks = []
+    for e in range(ne):
+        ids = np.concatenate([(c * ne + e) * p1 + np.arange(p1) for c in range(nc)])
+        blocks.append((ids, np.linalg.inv(A[ids][:, ids].toarray())))
+
+    def prec(v):
+        out = np.empty_like(v)
+        for ids, Bi in blocks:
+            out[ids] = Bi @ v[ids]
+        return out
+    return prec
+
+
+RESTART_ETA = 1e-10
+
+
+def bicgstab(A, prec, b, x0, rtol=1e-14, maxit=1000):
+    """Pinned right-preconditioned BiCGStab for the NON-symmetric
+    implicit systems of the 1-D CNS problem (matrix-valued SI coefficient
+    (dt_m/2) A_c(u_b)^2 + A_d(u_b), ``dgsem.py:356-396``; the reference
+    factorises them with splu, ``dgsem.py:503-533``).  The CUDA kernel
+    (``csrc/cns1d.cu``) reproduces this iteration:
+
+    * A x = M x - a M apply_diffusion(C, x), b = M rhs, x0 = rhs,
+      y = K^-1 p, z = K^-1 s with K the element-block diagonal of M + a B[C]
+      (``element_block_preconditioner``; point Jacobi stagnates at the
+      reference's own CFL-256 acoustic test, cond ~ 1e10)
+    * shadow residual r^ = r0; rho_0 = (r^, r0)
+    * per iteration k: [k > 0: beta = (rho_k / rho_{k-1}) (alpha / omega),
+      p = r + beta (p - omega v)]; v = A y; alpha = rho / (r^, v);
+      s = r - alpha v; t = A z; omega = (t, s) / (t, t) (0 if (t, t) == 0);
+      x = x + alpha y + omega z; r = s - omega t;
+      rho_{k+1} = (r^, s) - omega (r^, t)   (== (r^, r), fused reduction)
+    * restart (r^ = p = r, rho = (r, r), same k) when |rho| <= 1e-10 |r^| |r|
+      after the p update: the shadow residual has become orthogonal to r
+      (Lanczos breakdown; without it the CFL-256 acoustic solves stagnate
+      in ~1 of 6 runs perturbed at 1e-14, with it all converge)
+    * stop at the first k with (r_k, r_k) <= rtol^2 (b, b) (checked before
+      each iteration); k > maxit or a non-finite (r_k, r_k) (breakdown,
+      overflow) -> failure (it = -1).
+
+    Returns (x, iterations, margin) like ``pcg``."""
+    x = x0.copy()
+    r = b - A(x)
+    rh = r.copy()
+    rr = float(r @ r)
+    rho = rr
+    rhrh = rr                  # (r^, r^)
+    thr = rtol * rtol * float(b @ b)
+    p = r.copy()
+    v = np.zeros_like(r)
+    alpha = omega = 1.0
+    rho_new = rho
+    k = 0
+    fresh = True
+    while rr > thr or not np.isfinite(rr):
+        if k >= maxit or not np.isfinite(rr):   # breakdown / overflow is a failure
+            return x, -1, np.sqrt(rr / thr)
+        if not fresh:
+            beta = (rho_new / rho) * (alpha / omega)
+            p = r + beta * (p - omega * v)
+            rho = rho_new
+        fresh = False
+        if abs(rho) <= RESTART_ETA * np.sqrt(rhrh * rr):   # Lanczos breakdown: r^ _|_ r
+            rh = r.copy()
+            rhrh = rr
+            rho = rr
+            p = r.copy()
+        y = prec(p)
+        v = A(y)
+        alpha = rho / float(rh @ v)
+        s = r - alpha * v
+        z = prec(s)
+        t = A(z)
+        tt = float(t @ t)
+        omega = float(t @ s) / tt if tt != 0.0 else 0.0
+        x = x + alpha * y + omega * z
+        r = s - omega * t
+        rho_new = float(rh @ s) - omega * float(rh @ t)
+        rr = float(r @ r)
+        k += 1
+    return x, k, float(np.sqrt(rr / thr)) if thr > 0 else 0.0

@@ -17,7 +17,7 @@ import scipy.sparse as sp
 from scipy.sparse.linalg import splu
 
 from . import quad
-from .cg import pcg
+from .cg import bicgstab, element_block_preconditioner, pcg
 
 
 class SolverError(RuntimeError):
@@ -439,7 +439,7 @@ class Op1D:
             return np.zeros_like(rhs)
         if self.solver == "lu":
             return self._solve_lu(coeff, a, b, t).reshape(rhs.shape)
-        diag = self.mflat + a * self.stiffness_diag(coeff)
+        diag = self.mflat + a * self.stiffness_diag(coeff) if self.nc == 1 else None
         m = self.mflat
         if self.bc == "dirichlet":
             # affine SIP: D(x; t) = D_lin(x) + d_bc(t), d_bc = D(0; t).  Solve the
@@ -454,7 +454,12 @@ class Op1D:
             def A(x):
                 return m * x - a * m * self.apply_diffusion(coeff, x, t)
 
-        x, it, margin = pcg(A, diag, b, rhs.reshape(-1).copy(), self.rtol, self.maxit)
+        if self.nc > 1:   # systems (1-D CNS): non-symmetric -> pinned element-block BiCGStab
+            prec = element_block_preconditioner(sp.diags(self.mflat) + a * self.stiffness(coeff), self.nc,
+                                                self.ne, self.p1)
+            x, it, margin = bicgstab(A, prec, b, rhs.reshape(-1).copy(), self.rtol, self.maxit)
+        else:
+            x, it, margin = pcg(A, diag, b, rhs.reshape(-1).copy(), self.rtol, self.maxit)
         if it < 0:
             raise SolverError("implicit CG solve did not converge")
         self.cg_log.append((it, margin))

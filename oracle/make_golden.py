@@ -23,8 +23,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from sisdc import collocation as rc, dgsem as rd, mlsdc as rm, problems as rp, sdc as rs, transfer as rt  # noqa: E402
 
-from oracle.cg import pcg, pcg_hs  # noqa: E402
-from paper_2504_18526_b200.configs import CFG1, CFG2  # noqa: E402
+from oracle.cg import bicgstab, element_block_preconditioner, pcg, pcg_hs  # noqa: E402
+from paper_2504_18526_b200.configs import CFG1, CFG2, CNS_CASES  # noqa: E402
 
 OUT = os.path.join(REPO, "tests", "golden")
 
@@ -75,6 +75,8 @@ class PcgPatch:
                 A = lambda x: m * x - a * m * (op.apply_diffusion(coeff, x, t) - dbc)
             else:
                 A = lambda x: m * x - a * m * op.apply_diffusion(coeff, x, t)
+            if op.ncomp > 1:   # systems: element-block Jacobi of the assembled matrix
+                diag = element_block_preconditioner(Amat, op.ncomp, op.mesh.n_elem, op.p1)
             x, it, margin = patch.solver(A, diag, b, rhs.reshape(-1).copy(), patch.rtol, 1000)
             assert it >= 0
             patch.log.append((it, margin))
@@ -347,8 +349,81 @@ def gen_presmooth():
     np.savez_compressed(os.path.join(OUT, "presmooth.npz"), **out)
 
 
+def gen_cns():
+    """1-D compressible flow (CompressibleFlow, matrix SI coefficients) on the
+    reference's acoustic wave (problems.py:294-316): the reference's own
+    test_dgsem.py:553-600 set-ups (single-level SDC at CFL 0.8 si1 and CFL 256
+    si2) and a two-level MLSDC step, each with SuperLU (as shipped) and with
+    the pinned Jacobi-BiCGStab swapped into DGOperator.implicit_solve."""
+    out = {}
+    for w in CNS_CASES:
+        def build():
+            prob = rp.CompressibleFlow(gamma=w.gamma, R_gas=w.R_gas, eta=w.eta, Pr=w.prandtl)
+            ops = [rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, w.n_elem, P), prob)
+                   for P in (w.p_coarse, w.p_fine)]
+            rules = [rc.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
+            return ops, rules
+        ops, rules = build()
+        u0 = w.initial_state(ops[1].mesh.ref_nodes)
+        dt = w.time_step(u0, rd.compute_delta(w.p_fine))
+        out[f"{w.name}_u0"] = u0
+        out[f"{w.name}_dt"] = np.array(dt)
+
+        def run(ops, rules):
+            if w.mlsdc:
+                wts = [rc.make_weights(r) for r in rules]
+                levels = [rm.Level(o, r, ww, w.scheme) for o, r, ww in zip(ops, rules, wts)]
+                pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_only")
+                spat = rt.build_spatial_p_transfer(w.p_coarse, w.p_fine, w.n_elem, 3, "embedded")
+                hier = rm.Hierarchy(levels, [rt.SpaceTimeTransfer(pair, spat)], n_coarse=2, n_sweep=1,
+                                    form="incremental", post_sweep_on_finest=True)
+                u, res = u0, []
+                for s_ in range(w.n_steps):
+                    u = rm.run_mlsdc(hier, u, s_ * dt, dt, w.n_cycles, strategy="fmg").end_value.copy()
+                    res.append(u)
+                return res
+            rule = rules[1]
+            wts = rc.make_weights(rule)
+            u, res = u0, []
+            for s_ in range(w.n_steps):
+                u = rs.run_sdc(ops[1], rule, wts, dt, w.scheme, u, s_ * dt, w.n_sweeps).end_value.copy()
+                res.append(u)
+            return res
+        for s_, u in enumerate(run(ops, rules)):
+            out[f"{w.name}_lu_u{s_ + 1}"] = u
+        ops, rules = build()
+        with PcgPatch(1e-14, bicgstab) as pp:
+            res = run(ops, rules)
+        for s_, u in enumerate(res):
+            out[f"{w.name}_bicg_u{s_ + 1}"] = u
+        out[f"{w.name}_bicg_iters"] = np.array([it for it, _ in pp.log])
+        out[f"{w.name}_bicg_margin"] = np.array([mg for _, mg in pp.log])
+        print(w.name, "solves", len(pp.log), "iters", out[f"{w.name}_bicg_iters"].tolist()[:40],
+              "rel(lu, bicg)", np.linalg.norm(res[-1] - out[f"{w.name}_lu_u{len(res)}"]) / np.linalg.norm(res[-1]))
+    # operator goldens on the acoustic state: SI coefficient and a solve
+    w = CNS_CASES[0]
+    prob = rp.CompressibleFlow(gamma=w.gamma, R_gas=w.R_gas, eta=w.eta, Pr=w.prandtl)
+    op = rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine), prob)
+    u0 = w.initial_state(op.mesh.ref_nodes)
+    dt = w.time_step(u0, rd.compute_delta(w.p_fine))
+    c = op.modified_diffusion_matrix(u0, 0.5 * dt, "si2")
+    out["op_u"] = u0
+    out["op_conv"] = op.apply_convection(u0)
+    out["op_rhs"] = op.eval_rhs(u0, 0.0)
+    out["op_modc"] = c
+    out["op_diff_modc"] = op.apply_diffusion(c, u0)
+    out["op_diagA"] = op.assemble_implicit(c, 0.5 * dt).diagonal()
+    rhs = u0 * (1.0 + 1e-3 * np.sin(np.arange(op.ndof)))
+    out["op_solve_rhs"] = rhs
+    out["op_solve"] = op.implicit_solve(c, 0.5 * dt, rhs)
+    np.savez_compressed(os.path.join(OUT, "cns.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "cns":
+        gen_cns()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "nonincremental":
         gen_nonincremental()
         sys.exit(0)
@@ -368,5 +443,6 @@ if __name__ == "__main__":
     gen_dirichlet()
     gen_presmooth()
     gen_htransfer()
+    gen_cns()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -16,10 +16,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsisdc_b200.so")
 
 OK, ERR_ARG, ERR_CUDA, ERR_NONFINITE, ERR_NOCONV, ERR_UNSUPPORTED = range(6)
-CONVDIFF, BURGERS, EULER2D, ADVECTION2D, BURGERS2D = 0, 1, 2, 3, 4
+CONVDIFF, BURGERS, EULER2D, ADVECTION2D, BURGERS2D, CNS1D = 0, 1, 2, 3, 4, 5
 PERIODIC, DIRICHLET = 0, 1
 SCHEMES = {"euler": 0, "si1": 1, "si2": 2}
-COEF_NONE, COEF_CONST, COEF_FIELD, COEF_SI, COEF_PHYS = range(5)
+COEF_NONE, COEF_CONST, COEF_FIELD, COEF_SI, COEF_PHYS, COEF_MATRIX = range(6)
 
 
 class SolverError(RuntimeError):
@@ -44,7 +44,8 @@ class Op2DDesc(C.Structure):
 class Op1DDesc(C.Structure):
     _fields_ = [("n_elem", C.c_int), ("degree", C.c_int), ("ncomp", C.c_int), ("bc", C.c_int),
                 ("problem", C.c_int), ("x_left", C.c_double), ("x_right", C.c_double),
-                ("speed", C.c_double), ("nu", C.c_double), ("penalty", C.c_double)]
+                ("speed", C.c_double), ("nu", C.c_double), ("penalty", C.c_double),
+                ("gamma", C.c_double), ("eta", C.c_double), ("prandtl", C.c_double)]
 
 
 P = C.c_void_p
@@ -120,7 +121,7 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.sisdc_abi_version() != 1:
+    if lib.sisdc_abi_version() != 2:
         raise LibraryError("ABI version mismatch")
     _lib = lib
     return lib

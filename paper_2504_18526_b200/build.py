@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsisdc_b200.so")
-SOURCES = ["abi.cu", "ops1d.cu", "cg1d.cu", "ops2d.cu", "part2d.cu"]
+SOURCES = ["abi.cu", "ops1d.cu", "cg1d.cu", "cns1d.cu", "ops2d.cu", "part2d.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -24,18 +24,25 @@ def _stale(target, deps):
 def build(verbose: bool = False, force: bool = False) -> str:
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + \
         [os.path.join(os.path.dirname(HERE), "include", "sisdc_b200.h")]
-    objs = []
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+    objs = [os.path.join(CSRC, src.replace(".cu", ".o")) for src in SOURCES]
+
+    def compile_one(src):
         s = os.path.join(CSRC, src)
         o = os.path.join(CSRC, src.replace(".cu", ".o"))
-        objs.append(o)
-        if force or _stale(o, deps):
-            cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if verbose or r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-            if r.returncode != 0:
-                raise RuntimeError(f"nvcc failed on {src}")
+        if not (force or _stale(o, deps)):
+            return src, None
+        return src, subprocess.run([NVCC, *FLAGS, "-c", s, "-o", o], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:   # independent translation units
+        results = list(ex.map(compile_one, SOURCES))
+    for src, r in results:
+        if r is None:
+            continue
+        if verbose or r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}")
     if force or _stale(LIB, objs):
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB, "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)

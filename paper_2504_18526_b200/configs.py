@@ -213,3 +213,70 @@ class FrontWorkload:
 
 FRONT = FrontWorkload()
 FRONT_AV = FrontWorkload(n_elem=16, p_fine=4, p_coarse=2, av=(0.5, 0.5))
+
+
+# ------------------------------------------------- 1-D compressible flow (CNS)
+@dataclass(frozen=True)
+class AcousticWorkload:
+    """1-D CompressibleFlow on the reference's right-running acoustic wave
+    (``problems.py:294-316`` restated; CLI defaults ``cli.py:400-409``:
+    gamma 1.4, R 287.28, Mach 0.1, p_inf 1000, T_inf 300, amp 1e-2) on a
+    periodic [0, 1] mesh.  The single-level cases are the reference's own
+    ``test_dgsem.py:553-600`` set-ups (eta 1e-5, 12 elements, P = 7)."""
+    name: str
+    n_elem: int = 12
+    p_fine: int = 7
+    p_coarse: int = 3
+    m_fine: int = 5
+    m_coarse: int = 3
+    scheme: str = "si2"
+    cfl: float = 0.8
+    n_steps: int = 2
+    n_sweeps: int = 4
+    mlsdc: bool = False
+    n_cycles: int = 3
+    gamma: float = 1.4
+    R_gas: float = 287.28
+    eta: float = 1e-5
+    prandtl: float = 0.75
+    mach: float = 0.1
+    p_inf: float = 1000.0
+    T_inf: float = 300.0
+    amp_frac: float = 1e-2
+    x_left: float = 0.0
+    x_right: float = 1.0
+
+    @property
+    def dx(self):
+        return (self.x_right - self.x_left) / self.n_elem
+
+    def initial_state(self, gll_nodes):
+        """Conservative (rho, rho v, rho E), flat (3, ne, P+1), on the fine nodes."""
+        e = self.x_left + self.dx * np.arange(self.n_elem)
+        x = e[:, None] + 0.5 * self.dx * (np.asarray(gll_nodes) + 1.0)[None, :]
+        g, R = self.gamma, self.R_gas
+        a_inf = math.sqrt(g * R * self.T_inf)
+        vp = self.amp_frac * a_inf * np.sin(2.0 * math.pi * x)
+        T = (a_inf + 0.5 * (g - 1.0) * vp) ** 2 / (g * R)
+        p = self.p_inf * (T / self.T_inf) ** (g / (g - 1.0))
+        v = self.mach * a_inf + vp
+        rho = p / (R * T)
+        ener = p / (g - 1.0) + 0.5 * rho * v * v
+        return np.ascontiguousarray(np.stack([rho, rho * v, ener]).reshape(-1), dtype=np.float64)
+
+    def time_step(self, u0, delta_p):
+        """dt_from_cfl(cfl, dx, max(|v| + c), P_fine) (dgsem.py:67-69)."""
+        u3 = np.asarray(u0).reshape(3, self.n_elem, -1)
+        rho, v = u3[0], u3[1] / u3[0]
+        p = (self.gamma - 1.0) * (u3[2] - 0.5 * u3[1] * v)
+        lam = float(np.max(np.abs(v) + np.sqrt(self.gamma * p / rho)))
+        return self.cfl * self.dx / (2.0 * delta_p * lam)
+
+
+CNS_CASES = (
+    AcousticWorkload("cns_resolved", m_fine=3, scheme="si1", cfl=0.8),      # test_dgsem.py:575-600
+    AcousticWorkload("cns_large", m_fine=5, scheme="si2", cfl=256.0, n_steps=1),  # test_dgsem.py:553-573
+    AcousticWorkload("cns_mlsdc", m_fine=5, m_coarse=3, scheme="si2", cfl=0.8, mlsdc=True, n_cycles=2),
+    AcousticWorkload("cns_mlsdc_visc", n_elem=16, p_fine=6, p_coarse=3, m_fine=4, m_coarse=2, scheme="si2",
+                     cfl=1.0, eta=2e-4, mlsdc=True, n_steps=1),
+)

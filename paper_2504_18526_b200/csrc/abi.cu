@@ -108,9 +108,17 @@ int dev_at(sisdc_op1d* op, double t, Op1DDev& d) {
   return bc_at(op, t, d.gl, d.gr);
 }
 
+int check_coef(Ctx* c, sisdc_coef k);
+int check_coef_op(sisdc_op1d* op, sisdc_coef k) {
+  if (k.kind == SISDC_COEF_MATRIX && !op->cns())
+    return C(op)->fail(SISDC_ERR_UNSUPPORTED, "matrix-valued coefficients are built for the 1-D CNS problem only");
+  if (op->cns() && (k.kind == SISDC_COEF_SI || k.kind == SISDC_COEF_PHYS) && !k.ptr)
+    return C(op)->fail(SISDC_ERR_ARG, "CNS coefficients need the frozen state u_b");
+  return check_coef(C(op), k);
+}
 int check_coef(Ctx* c, sisdc_coef k) {
-  if (k.kind < SISDC_COEF_NONE || k.kind > SISDC_COEF_PHYS) return c->fail(SISDC_ERR_ARG, "unknown coefficient kind");
-  if ((k.kind == SISDC_COEF_FIELD || k.kind == SISDC_COEF_SI) && !k.ptr)
+  if (k.kind < SISDC_COEF_NONE || k.kind > SISDC_COEF_MATRIX) return c->fail(SISDC_ERR_ARG, "unknown coefficient kind");
+  if ((k.kind == SISDC_COEF_FIELD || k.kind == SISDC_COEF_SI || k.kind == SISDC_COEF_MATRIX) && !k.ptr)
     return c->fail(SISDC_ERR_ARG, "coefficient needs a device pointer");
   return SISDC_OK;
 }
@@ -248,9 +256,16 @@ int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) 
   if (!(d->x_right > d->x_left)) return c.fail(SISDC_ERR_ARG, "empty domain");
   if (d->n_elem < 1 || d->degree < 1) return c.fail(SISDC_ERR_ARG, "need at least one element and degree >= 1");
   if (d->degree + 1 > MAXP1) return c.fail(SISDC_ERR_UNSUPPORTED, "degree above 15");
-  if (d->ncomp != 1) return c.fail(SISDC_ERR_UNSUPPORTED, "only scalar problems (ncomp == 1) are built");
+  const bool cns = d->problem == SISDC_CNS1D;
+  if (d->ncomp != (cns ? 3 : 1)) return c.fail(SISDC_ERR_ARG, "ncomp does not match the problem");
+  if (cns && d->bc != SISDC_PERIODIC)
+    return c.fail(SISDC_ERR_UNSUPPORTED, "1-D compressible flow is built for periodic meshes");
+  if (cns && d->n_elem < 2) return c.fail(SISDC_ERR_UNSUPPORTED, "1-D compressible flow needs >= 2 elements");
+  if (cns && !(d->gamma > 1.0)) return c.fail(SISDC_ERR_ARG, "gamma must exceed 1");
+  if (cns && !(d->prandtl > 0.0)) return c.fail(SISDC_ERR_ARG, "Prandtl number must be positive");
+  if (cns && d->eta < 0.0) return c.fail(SISDC_ERR_ARG, "viscosity must be nonnegative");
   if (d->bc != SISDC_PERIODIC && d->bc != SISDC_DIRICHLET) return c.fail(SISDC_ERR_ARG, "unknown boundary condition");
-  if (d->problem != SISDC_CONVDIFF && d->problem != SISDC_BURGERS) return c.fail(SISDC_ERR_ARG, "unknown problem");
+  if (d->problem != SISDC_CONVDIFF && d->problem != SISDC_BURGERS && !cns) return c.fail(SISDC_ERR_ARG, "unknown problem");
   if (d->nu < 0) return c.fail(SISDC_ERR_ARG, "diffusion coefficient must be nonnegative");
   sisdc_op1d* op = new (std::nothrow) sisdc_op1d();
   if (!op) return SISDC_ERR_ARG;
@@ -290,6 +305,19 @@ int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) 
   v.dx = dx; v.s = 2.0 / dx; v.mu0 = d->penalty * p1 * p1 / dx;   // dgsem.py:137
   v.speed = d->speed; v.nu = d->nu; v.tab = op->d_tab; v.nu_art = nullptr;
   v.bc = d->bc; v.gl = 0.0; v.gr = 0.0;
+  v.nc = d->ncomp; v.gamma = d->gamma; v.eta = d->eta; v.Pr = d->prandtl;
+  if (cns) {
+    const size_t nb = 3 * p1;
+    e = cudaMalloc(&op->d_pinv, (size_t)d->n_elem * nb * nb * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&op->d_c9, (size_t)d->n_elem * p1 * 9 * sizeof(double));
+    if (e != cudaSuccess) {
+      int rc = c.cuda(e, "cns block-Jacobi workspace");
+      cudaFree(op->d_tab);
+      cudaFree(op->d_pinv);
+      delete op;
+      return rc;
+    }
+  }
   *out = op;
   return SISDC_OK;
 }
@@ -378,6 +406,8 @@ void sisdc_op1d_destroy(sisdc_op1d* op) {
   if (op->parted()) part2_destroy(op);
   cudaFree(op->d_tab);
   cudaFree(op->d_cgws);
+  cudaFree(op->d_pinv);
+  cudaFree(op->d_c9);
   delete op;
 }
 
@@ -401,6 +431,7 @@ int sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art) {
 int sisdc_smooth_start(sisdc_op1d* op, int M, const double* u, double* out) {
   if (!op || !u || !out || M < 1) return SISDC_ERR_ARG;
   if (op->dim == 2) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "smooth_start is built for 1-D meshes");
+  if (op->cns()) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "smooth_start is built for the scalar 1-D problems");
   return launch_smooth_start(C(op), op->dev, M, u, out);
 }
 
@@ -426,6 +457,7 @@ int sisdc_apply_convection(sisdc_op1d* op, const double* u, double t, double* ou
   if (!op || !u || !out) return SISDC_ERR_ARG;
   if (op->parted()) return part2_conv(op, u, out);
   if (op->dim == 2) return launch2_conv(C(op), op->dev2, u, out);
+  if (op->cns()) return cns_conv(C(op), op->dev, u, out);
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_apply_convection(C(op), d, u, out);
@@ -433,11 +465,12 @@ int sisdc_apply_convection(sisdc_op1d* op, const double* u, double t, double* ou
 
 int sisdc_apply_diffusion(sisdc_op1d* op, sisdc_coef k, const double* u, double t, double* out) {
   if (!op || !u || !out) return SISDC_ERR_ARG;
-  if (int rc = check_coef(C(op), k)) return rc;
+  if (int rc = check_coef_op(op, k)) return rc;
   if (k.kind == SISDC_COEF_NONE || (k.kind == SISDC_COEF_CONST && k.value == 0.0))
     return C(op)->cuda(cudaMemsetAsync(out, 0, op->n() * sizeof(double), C(op)->stream), "zero");
   if (op->parted()) return part2_sip(op, coef(k), u, out);
   if (op->dim == 2) return launch2_sip(C(op), op->dev2, coef(k), u, out);
+  if (op->cns()) return cns_sip(C(op), op->dev, coef(k), u, out);
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_apply_diffusion(C(op), d, coef(k), u, out);
@@ -448,6 +481,7 @@ int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double t, double* out) {
   if (op->parted()) return part2_eval_nodes(op, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
+  if (op->cns()) return cns_node_eval(C(op), op->dev, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_node_eval(C(op), d, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
@@ -455,15 +489,16 @@ int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double t, double* out) {
 
 int sisdc_coef_field(sisdc_op1d* op, sisdc_coef k, double* out) {
   if (!op || !out) return SISDC_ERR_ARG;
-  if (int rc = check_coef(C(op), k)) return rc;
+  if (int rc = check_coef_op(op, k)) return rc;
   if (op->parted()) return part2_coef_field(op, coef(k), out);
   if (op->dim == 2) return launch2_coef(C(op), op->dev2, coef(k), out);
+  if (op->cns()) return cns_coef(C(op), op->dev, coef(k), out);   // (n_elem, P+1, 3, 3)
   return launch_coef_field(C(op), op->dev, coef(k), out);
 }
 
 int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* rhs, double t, double* x) {
   if (!op || !rhs || !x) return SISDC_ERR_ARG;
-  if (int rc = check_coef(C(op), k)) return rc;
+  if (int rc = check_coef_op(op, k)) return rc;
   if (a == 0.0) {   // dgsem.py:505-506
     if (x == rhs) return SISDC_OK;
     return sisdc_copy(op->ctx, x, rhs, op->n());
@@ -471,6 +506,10 @@ int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* r
   if (k.kind == SISDC_COEF_NONE) return C(op)->fail(SISDC_ERR_ARG, "cannot assemble a zero coefficient");
   if (op->parted()) return part2_solve(op, coef(k), a, rhs, x);
   if (op->dim == 2) return launch2_cg(C(op), op->dev2, coef(k), a, rhs, x, op->d_cgws, op->cg_blocks);
+  if (op->cns()) {
+    if (x == rhs) return C(op)->fail(SISDC_ERR_ARG, "implicit_solve: x must not alias rhs");
+    return cns_solve(C(op), op->dev, coef(k), a, rhs, x, op->d_c9, op->d_pinv);
+  }
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_cg1d(C(op), d, coef(k), a, rhs, x);
@@ -481,8 +520,8 @@ int sisdc_stage_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* base
                       const double* h_old, double t_conv, double t_solve, double* rhs_scratch, double* conv_out,
                       double* x) {
   if (!op || !base || !conv_in || !x || M < 0 || M > MAXM || (f_old && !w_row)) return SISDC_ERR_ARG;
-  if (int rc = check_coef(C(op), k)) return rc;
-  const bool fuse = op->dim == 1 && !op->parted() && a != 0.0 && k.kind != SISDC_COEF_NONE;
+  if (int rc = check_coef_op(op, k)) return rc;
+  const bool fuse = op->dim == 1 && !op->cns() && !op->parted() && a != 0.0 && k.kind != SISDC_COEF_NONE;
   if (!fuse) {   // stage rhs into the scratch vector, then the solve
     if (!rhs_scratch) return C(op)->fail(SISDC_ERR_ARG, "stage_solve needs a rhs scratch vector here");
     if (int rc = sisdc_stage_rhs(op, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, t_conv, rhs_scratch,
@@ -505,6 +544,7 @@ int sisdc_stage_rhs(sisdc_op1d* op, const double* base, const double* conv_in, d
   if (!op || !base || !conv_in || !rhs || M < 0 || M > MAXM || (f_old && !w_row)) return SISDC_ERR_ARG;
   if (op->parted()) return part2_stage(op, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
   if (op->dim == 2) return launch2_stage(C(op), op->dev2, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
+  if (op->cns()) return cns_stage(C(op), op->dev, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_stage_rhs(C(op), d, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
@@ -519,6 +559,7 @@ int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_coun
   if (op->parted()) return part2_eval_nodes(op, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
+  if (op->cns()) return cns_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
   if (op->dev.bc == SISDC_DIRICHLET) {   // boundary data at t_m and t_{m-1} per node
     if (!times) return C(op)->fail(SISDC_ERR_ARG, "Dirichlet node caches need the node times");
     if (M > MAXM) return C(op)->fail(SISDC_ERR_ARG, "too many collocation nodes");
@@ -536,6 +577,7 @@ int sisdc_eval_rhs_nodes(sisdc_op1d* op, int M, const double* u, const double* t
   if (!op || !u || !f || M < 1 || M > MAXM) return SISDC_ERR_ARG;
   if (op->parted()) return part2_eval_nodes(op, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
   if (op->dim == 2) return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
+  if (op->cns()) return cns_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
   if (op->dev.bc == SISDC_DIRICHLET) {
     if (!times) return C(op)->fail(SISDC_ERR_ARG, "Dirichlet evaluations need the node times");
     double bnd[4 * MAXM] = {};

@@ -44,7 +44,10 @@ struct sisdc_op1d {   // dimension-tagged operator handle (1-D or 2-D)
   int* h_done = nullptr;             // pinned [2]
   cudaEvent_t ev[2] = {nullptr, nullptr};
   bool parted() const { return !parts.empty(); }
-  long long n() const { return dim == 1 ? dev.n : (parted() ? n_total : dev2.n); }
+  long long n() const { return dim == 1 ? (long long)dev.n * dev.nc : (parted() ? n_total : dev2.n); }
+  bool cns() const { return dim == 1 && dev.problem == SISDC_CNS1D; }
+  double* d_pinv = nullptr;   // 1-D CNS: element-block Jacobi inverses (n_elem x (3(P+1))^2)
+  double* d_c9 = nullptr;     // 1-D CNS: materialised 3x3 coefficient per node (n x 9)
 };
 
 struct sisdc_xfer {

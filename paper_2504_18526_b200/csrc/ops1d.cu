@@ -1,6 +1,7 @@
 // Element kernels of the 1-D SI-SDC sweep: operator applications, fused
 // sweep stages, node caches and the space-time p-transfers (sm_100a, fp64).
 #include "sisdc_dev.cuh"
+#include "sisdc_cns.cuh"
 #include "sisdc_host.h"
 
 namespace sisdc {
@@ -385,7 +386,9 @@ __global__ void k_persson(Op1DDev op, const double* __restrict__ u, double kappa
     double en = mk * mk * (2.0 / (2.0 * k + 1.0));
     tot += en;
     if (k == P) top = en;
-    lam = fmax(lam, wave_speed(op, ue[k]));
+    lam = fmax(lam, op.problem == SISDC_CNS1D   // sensor on rho, max_speed of the system (dgsem.py:551-553)
+                        ? cns_speed(op, ue[k], u[op.n + (size_t)e * p1 + k], u[2 * (size_t)op.n + (size_t)e * p1 + k])
+                        : wave_speed(op, ue[k]));
   }
   double s = tot > 0.0 ? log10(fmax(top, 1e-300) / tot) : -INFINITY;
   double s0 = -4.0 * log10((double)P);

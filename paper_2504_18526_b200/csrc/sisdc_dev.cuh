@@ -37,6 +37,8 @@ struct Op1DDev {
   const double* nu_art;   // per element or nullptr
   int bc;                 // SISDC_PERIODIC / SISDC_DIRICHLET (Mesh1D.bc)
   double gl, gr;          // Dirichlet: outside states at the time of this evaluation
+  int nc;                 // components (1; 3 for SISDC_CNS1D, n counts one component)
+  double gamma, eta, Pr;  // SISDC_CNS1D gas (problems.py:171-187)
 };
 
 struct CoefDev {

@@ -12,7 +12,9 @@ Mirrors ``dgsem.py`` of the reference (``Mesh1D`` ``:72-106``, ``DGOperator``
 
 States are torch float64 CUDA tensors (numpy inputs are uploaded); results
 are returned as new CUDA tensors unless ``out=`` is given.  Scope of the
-built path: periodic meshes, scalar problems (ConvectionDiffusion, Burgers).
+built path: scalar problems (ConvectionDiffusion, Burgers) on periodic and
+Dirichlet meshes; 1-D CompressibleFlow (3 fields, matrix coefficients) on
+periodic meshes.
 """
 from __future__ import annotations
 
@@ -139,13 +141,16 @@ class DGOperator:
         self.rt = get_runtime(device)
         self.lib = self.rt.lib
         self.eager_checks = eager_checks
-        kind = {"convdiff": _lib.CONVDIFF, "burgers": _lib.BURGERS}[problem.kind]
+        kind = {"convdiff": _lib.CONVDIFF, "burgers": _lib.BURGERS, "cns": _lib.CNS1D}[problem.kind]
+        self.is_cns = problem.kind == "cns"
         self.dirichlet = mesh.bc == "dirichlet"
         self._btimes = set()
         self._desc = _lib.Op1DDesc(mesh.n_elem, mesh.degree, self.ncomp,
                                    _lib.DIRICHLET if self.dirichlet else _lib.PERIODIC, kind,
                                    float(mesh.x_left), float(mesh.x_right), float(getattr(problem, "speed", 0.0)),
-                                   float(problem.nu), float(penalty_const))
+                                   float(problem.nu), float(penalty_const),
+                                   float(getattr(problem, "gamma", 1.4)), float(getattr(problem, "eta", 0.0)),
+                                   float(getattr(problem, "Pr", 0.75)))
         h = C.c_void_p()
         self.rt.check(self.lib.sisdc_op1d_create(self.rt.h, C.byref(self._desc), C.byref(h)), "op1d_create")
         self.h = h
@@ -195,9 +200,13 @@ class DGOperator:
             return coeff.c()
         if np.isscalar(coeff):
             return Coef(_lib.COEF_CONST, float(coeff), None)
-        t = self.rt.to_device(coeff)
-        if t.numel() != self.mesh.n_elem * self.p1:
-            raise NotImplementedError("matrix-valued coefficients are not built on the GPU path")
+        t = self.rt.to_device(coeff).contiguous()
+        nn = self.mesh.n_elem * self.p1
+        if self.is_cns and t.numel() == nn * self.ncomp * self.ncomp:   # (n_elem, P+1, nc, nc)
+            keep.append(t)
+            return Coef(_lib.COEF_MATRIX, 0.0, t.data_ptr())
+        if t.numel() != nn:
+            raise NotImplementedError("matrix-valued coefficients are built for CompressibleFlow only")
         keep.append(t)
         return Coef(_lib.COEF_FIELD, 0.0, t.data_ptr())
 
@@ -209,6 +218,14 @@ class DGOperator:
         return SICoefficient(None, 0.0, _lib.COEF_PHYS)
 
     def modified_diffusion_matrix(self, u_b, dt_m: float, scheme: str) -> Any:
+        if self.is_cns:   # matrix-valued, frozen at u_b (dgsem.py:356-396)
+            if scheme == "euler":
+                if not self.problem.viscous and self.nu_art is None:
+                    return None
+                return SICoefficient(self.rt.to_device(u_b).clone(), 0.0, _lib.COEF_PHYS)
+            if scheme not in ("si1", "si2"):
+                raise ValueError(f"unknown scheme {scheme!r}")
+            return SICoefficient(self.rt.to_device(u_b).clone(), dt_m)
         if scheme == "euler":
             return self._phys()
         if scheme not in ("si1", "si2"):
@@ -275,16 +292,21 @@ class DGOperator:
         return self.rt.zeros(self.ndof)
 
     def coefficient_field(self, coeff):
-        """Materialise a coefficient as an (n_elem, P+1) device field."""
+        """Materialise a coefficient as an (n_elem, P+1) device field
+        ((n_elem, P+1, 3, 3) for CompressibleFlow)."""
         keep = []
         c = self._coef(coeff, keep)
-        out = self.rt.empty(self.mesh.n_elem * self.p1)
+        per = self.ncomp * self.ncomp if self.is_cns else 1
+        out = self.rt.empty(self.mesh.n_elem * self.p1 * per)
         self.rt.bind_stream()
         self.rt.check(self.lib.sisdc_coef_field(self.h, c, out.data_ptr()), "coef_field")
+        if self.is_cns:
+            return out.reshape(self.mesh.n_elem, self.p1, self.ncomp, self.ncomp)
         return out.reshape(self.mesh.n_elem, self.p1)
 
     def implicit_solve(self, coeff, a: float, rhs, t: float = 0.0, out=None):
-        """Solve (M + a B[coeff]) x = M rhs with the pinned Jacobi-PCG."""
+        """Solve (M + a B[coeff]) x = M rhs with the pinned Jacobi-PCG
+        (CompressibleFlow: the pinned element-block-Jacobi BiCGStab)."""
         if a == 0.0:
             return rhs
         keep = []
@@ -350,4 +372,10 @@ def smooth_start(op: DGOperator, u, out=None):
 def max_wave_speed(op: DGOperator, u) -> float:
     if op.problem.kind == "convdiff":
         return abs(op.problem.speed)
+    if op.problem.kind == "cns":   # max(|v| + c), problems.py:194-196
+        u3 = op.as_nodes(u)
+        g = op.problem.gamma
+        v = u3[1] / u3[0]
+        p = (g - 1.0) * (u3[2] - 0.5 * u3[1] * v)
+        return float((v.abs() + (g * p / u3[0]).sqrt()).max())
     return float(op.rt.to_device(u).abs().max())

@@ -1,4 +1,4 @@
-"""Problem descriptors (``problems.py:25-82`` of the reference).
+"""Problem descriptors (``problems.py:25-82,160-240`` of the reference).
 
 The pointwise physics -- flux, wave speed, convective Jacobian A_c and
 diffusion coefficient A_d -- is evaluated inside the sm_100a kernels
@@ -43,6 +43,39 @@ class Burgers:
         self.source = source
         self.boundary_state = boundary
         self.speed = 0.0
+
+
+class CompressibleFlow:
+    """1-D compressible Navier-Stokes in conservative variables (rho, rho v,
+    rho E) (``problems.py:160-240``); eta = 0 is Euler.  Built on periodic
+    meshes; the SI coefficient (dt_m/2) A_c(u_b)^2 + A_d(u_b) (+nu_art) is a
+    3x3 matrix per node, so the implicit solve is the pinned block-Jacobi
+    BiCGStab (``oracle/cg.py``) instead of the CG."""
+
+    ncomp = 3
+    is_linear = False
+    source = None
+    kind = "cns"
+    speed = 0.0
+    nu = 0.0
+
+    def __init__(self, gamma: float = 1.4, R_gas: float = 287.28, eta: float = 0.0, Pr: float = 0.75,
+                 boundary=None):
+        if gamma <= 1.0:
+            raise ValueError("gamma must exceed 1")
+        if Pr <= 0:
+            raise ValueError("Prandtl number must be positive")
+        if eta < 0:
+            raise ValueError("viscosity must be nonnegative")
+        self.gamma = float(gamma)
+        self.R_gas = float(R_gas)
+        self.eta = float(eta)
+        self.Pr = float(Pr)
+        self.boundary_state = boundary
+
+    @property
+    def viscous(self) -> bool:
+        return self.eta > 0
 
 
 def burgers_front_exact(nu: float):

@@ -75,8 +75,8 @@ def _scheme_id(scheme):
 
 def _coef(ctx, scheme, u_prev, dt_m) -> Coef:
     """C_m frozen at u_{m-1}: SI for si1/si2, physical for euler (dgsem.py:356-396)."""
-    if scheme == "euler":
-        return Coef(_lib.COEF_PHYS, 0.0, None)
+    if scheme == "euler":   # the state matters for systems (A_d(u_b)); scalar kernels ignore it
+        return Coef(_lib.COEF_PHYS, 0.0, u_prev.data_ptr())
     return Coef(_lib.COEF_SI, float(dt_m), u_prev.data_ptr())
 
 

@@ -211,10 +211,13 @@ class _XferHandle:
             rt.check(rt.lib.sisdc_xfer2d_create(rt.h, spatial.ne_fine * spatial.ncomp, spatial.np_coarse,
                                                 spatial.np_fine, Mc, Mf, *ptrs, C.byref(h)), "xfer2d_create")
         elif spatial.kind == "h":   # parent element <-> contiguous child pair of 2 (P+1) nodes
-            rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_coarse, spatial.np_coarse, 2 * spatial.np_fine, Mc, Mf,
+            rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_coarse * spatial.ncomp, spatial.np_coarse,
+                                              2 * spatial.np_fine, Mc, Mf,
                                               *ptrs, C.byref(h)), "xfer_create")
         else:
-            rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_fine, spatial.np_coarse, spatial.np_fine, Mc, Mf,
+            # (ncomp, n_elem, P+1): the component blocks are element-local transfers too
+            rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_fine * spatial.ncomp, spatial.np_coarse,
+                                              spatial.np_fine, Mc, Mf,
                                               *ptrs, C.byref(h)), "xfer_create")
         self.h = h
         self.Mc, self.Mf = Mc, Mf

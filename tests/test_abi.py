@@ -36,7 +36,7 @@ def test_header_symbols_bound_and_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.sisdc_abi_version() == 1
+    assert lib.sisdc_abi_version() == 2
 
 
 def test_sm100a_cubin():

@@ -175,3 +175,51 @@ def test_dirichlet_front(golden):
     u = sweeper.run_mlsdc(h, G["av_u0"], 0.0, float(G["av_dt"]), wa.n_cycles, "fmg").u[-1]
     assert [it for it, _ in log] == G["av_mlsdc_pcg_iters1"].tolist()
     assert np.linalg.norm(u - G["av_mlsdc_pcg_u1"]) / np.linalg.norm(G["av_mlsdc_pcg_u1"]) < 1e-12
+
+
+def _cns_oracle_run(w, log, solver="pcg", u0=None, dt=None):
+    """The oracle's restatement of the reference's SDC / MLSDC on the 1-D CNS
+    acoustic workloads (oracle/make_golden.py gen_cns)."""
+    prob = dg1d.CNS1D(gamma=w.gamma, R_gas=w.R_gas, eta=w.eta, Pr=w.prandtl)
+
+    def mk(P):
+        return dg1d.Op1D(w.x_left, w.x_right, w.n_elem, P, prob, solver=solver, cg_log=log)
+    fine = mk(w.p_fine)
+    if u0 is None:
+        u0 = w.initial_state(fine.xi)
+        dt = w.time_step(u0, quad.delta_of_degree(w.p_fine))
+    res = []
+    u = u0
+    if w.mlsdc:
+        h = sweeper.build_two_level(lambda lvl: mk(w.p_coarse if lvl == "coarse" else w.p_fine),
+                                    sweeper.Rule("radau_right", w.m_coarse), sweeper.Rule("radau_right", w.m_fine))
+        for s in range(w.n_steps):
+            u = sweeper.run_mlsdc(h, u, s * dt, dt, w.n_cycles).u[-1].copy()
+            res.append(u)
+    else:
+        rule = sweeper.Rule("radau_right", w.m_fine)
+        for s in range(w.n_steps):
+            u = sweeper.run_sdc(fine, rule, dt, w.scheme, u, s * dt, w.n_sweeps).u[-1].copy()
+            res.append(u)
+    return u0, dt, res
+
+
+@pytest.mark.parametrize("case", ["cns_resolved", "cns_mlsdc", "cns_mlsdc_visc"])
+def test_cns_oracle_pinned_to_reference(golden, case):
+    """1-D CompressibleFlow (matrix coefficients): the
+    oracle's block-Jacobi BiCGStab path reproduces the reference run with the
+    same solver swapped in (identical iteration sequence), and the reference
+    as shipped (SuperLU) to the conditioning of the acoustic system."""
+    from paper_2504_18526_b200.configs import CNS_CASES
+    G = golden["cns"]
+    w = {c.name: c for c in CNS_CASES}[case]
+    log = []
+    fine_xi = quad.gll(w.p_fine + 1)[0]
+    u0 = w.initial_state(fine_xi)   # the seeded IC on the oracle's own GLL nodes
+    assert np.abs(u0 - G[f"{case}_u0"]).max() <= 1e-13 * np.abs(u0).max()
+    assert abs(w.time_step(u0, quad.delta_of_degree(w.p_fine)) / float(G[f"{case}_dt"]) - 1.0) < 1e-13
+    u0, dt, res = _cns_oracle_run(w, log, u0=G[f"{case}_u0"], dt=float(G[f"{case}_dt"]))
+    assert [it for it, _ in log] == G[f"{case}_bicg_iters"].tolist()
+    for s, u in enumerate(res):
+        assert np.linalg.norm(u - G[f"{case}_bicg_u{s + 1}"]) / np.linalg.norm(u) < 1e-12
+        assert np.linalg.norm(u - G[f"{case}_lu_u{s + 1}"]) / np.linalg.norm(u) < 5e-11
