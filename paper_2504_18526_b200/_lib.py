@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsisdc_b200.so")
+LIB_PATH = os.environ.get("SISDC_LIB", os.path.join(HERE, "libsisdc_b200.so"))   # override: A/B experiments
 
 OK, ERR_ARG, ERR_CUDA, ERR_NONFINITE, ERR_NOCONV, ERR_UNSUPPORTED = range(6)
 CONVDIFF, BURGERS, EULER2D, ADVECTION2D, BURGERS2D, CNS1D = 0, 1, 2, 3, 4, 5

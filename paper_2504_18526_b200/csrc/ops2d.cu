@@ -587,7 +587,7 @@ struct CgSm {
   static constexpr int FQ = BY + NC * EB * NP;                  // [NC][EB][4][P1] neighbour face fluxes
   static constexpr int END0 = FQ + NC * EB * 4 * P1;
   // P1 = 8 runs phase B warp-per-element: 8 warps x Wpe<NC>::WARP (defined below)
-  static constexpr int WPE = 8 * (NC * 80 + 4 * NC * 64 + 80 + 160 + 32 + 64 + 32);
+  static constexpr int WPE = 8 * (2 * 80 + 2 * 4 * 64 + 2 * 80 + 64 + 160 + 32 + 64);
   static constexpr int END1 = P1 == 8 ? WPE : END0;
   static constexpr int RED = END1 > Sm2<P1>::FU ? END1 : Sm2<P1>::FU;   // [32][4]; setup scratch below
   static constexpr int SIZE = RED + 128;
@@ -1046,15 +1046,15 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
 }
 
 template <int NC>
-struct Wpe {                 // per-warp shared region (doubles)
+struct Wpe {                 // per-warp shared region (doubles): a two-stage pipeline of (element, field) tasks
   static constexpr int RP = 10, NP = 80, NN = 64;   // own element rows padded to 10 (16-byte aligned)
-  static constexpr int OWN = 0;                     // [NC][NP]
-  static constexpr int NBR = OWN + NC * NP;         // [4 faces][NC][64] neighbour elements
-  static constexpr int COEF = NBR + 4 * NC * NN;    // [NP] own coefficient
-  static constexpr int QX = COEF + NP, QY = QX + NP, DOT = QY + NP;   // [NP] [NP] [32]
+  static constexpr int OWN = 0;                     // [2 stages][NP] one field of the own element
+  static constexpr int NBR = OWN + 2 * NP;          // [2 stages][4 faces][64] that field's neighbour elements
+  static constexpr int COEF = NBR + 2 * 4 * NN;     // [2 element parities][NP] own coefficient
+  static constexpr int CFN = COEF + 2 * NP;         // [2 element parities][32] neighbour face coefficients
+  static constexpr int QX = CFN + 64, QY = QX + NP, DOT = QY + NP;   // [NP] [NP] [32]
   static constexpr int FCON = DOT + 32;             // [16][4] face constants per x-row / y-column
-  static constexpr int CFN = FCON + 64;             // [32] neighbour face coefficients (lane = face*8+k)
-  static constexpr int WARP = CFN + 32;
+  static constexpr int WARP = FCON + 64;
   static_assert(8 * WARP == CgSm<8, NC>::WPE, "keep CgSm::WPE in sync");
 };
 
@@ -1106,7 +1106,7 @@ __device__ __forceinline__ void mma_lane_init(const Op2DDev& op, MmaLane& K) {
 // (sip_block).  Ue: own element (padded rows), Nb: neighbour face lines of this
 // field, Ce / cfn: coefficient at the own nodes (padded rows) / at the
 // neighbour face nodes (lane = face*8 + k).  Scratch: QX, QY, DT, FC.
-template <int NC>
+template <int NC, int FS = NC * 64>   // FS: stride between the four faces' lines in Nb
 __device__ __forceinline__ void wpe_sip(const Op2DDev& op, const MmaLane& K, const double* Ue, const double* Nb,
                                         const double* Ce, const double* cfn, double* QX, double* QY, double* DT,
                                         double* FC, double& bx0, double& bx1, double& by0, double& by1) {
@@ -1126,7 +1126,7 @@ __device__ __forceinline__ void wpe_sip(const Op2DDev& op, const MmaLane& K, con
   // neighbour face fluxes: lane = face*8 + k, line k of face f
   {
     const int f = lane >> 3, k = lane & 7;
-    const double* ln = Nb + f * NC * 64 + k * 8;
+    const double* ln = Nb + f * FS + k * 8;
     double gd = 0.0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -1147,8 +1147,8 @@ __device__ __forceinline__ void wpe_sip(const Op2DDev& op, const MmaLane& K, con
     const bool yd = lane >= 8;
     const int r = lane & 7;
     const int up = yd ? P * RP + r : r * RP + P, u0 = yd ? r : r * RP;
-    const double jp = Ue[up] - Nb[(yd ? FT : FR) * NC * 64 + nsw(r, 0)];
-    const double jm = Nb[(yd ? FB : FL) * NC * 64 + nsw(r, P)] - Ue[u0];
+    const double jp = Ue[up] - Nb[(yd ? FT : FR) * FS + nsw(r, 0)];
+    const double jm = Nb[(yd ? FB : FL) * FS + nsw(r, P)] - Ue[u0];
     const double cP = Ce[up], c0 = Ce[u0];
     const double fcp = cfn[(yd ? 16 : 0) + r], fcm = cfn[(yd ? 24 : 8) + r];
     const double qP = (yd ? QY : QX)[up], q0 = (yd ? QY : QX)[u0];
@@ -1190,13 +1190,14 @@ struct PxArgs {
 // one field of a staged element: w = a (hwy Bx + hwx By) + hwx hwy v;
 // epi(g, w0, w1, v0, v1) for the lane's node pair.  With px.up, the field's
 // p / x operands are loaded before the contractions (their latency hides
-// behind the tensor-core work) and updated after.
+// behind the tensor-core work) and updated after.  sb: stage buffer of the
+// field, ep: element parity of the coefficient buffers.
 template <int NC, typename Epi>
-__device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const MmaLane& K, int c, double a,
-                                          long long gi, Epi&& epi, const PxArgs& px) {
+__device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, int sb, int ep, const MmaLane& K, int c,
+                                          double a, long long gi, Epi&& epi, const PxArgs& px) {
   using W = Wpe<NC>;
   const int lane = threadIdx.x & 31, g = lane >> 2, n0 = 2 * (lane & 3);
-  const double* Ue = ws + W::OWN + c * W::NP;
+  const double* Ue = ws + W::OWN + sb * W::NP;
   const long long gc = gi + c * op.nn;
   double2 pu, pp, px_;
   if (px.up) {
@@ -1205,8 +1206,8 @@ __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const M
     px_ = __ldcs(reinterpret_cast<const double2*>(px.x + gc));
   }
   double bx0, bx1, by0, by1;
-  wpe_sip<NC>(op, K, Ue, ws + W::NBR + c * 64, ws + W::COEF, ws + W::CFN, ws + W::QX, ws + W::QY, ws + W::DOT,
-              ws + W::FCON, bx0, bx1, by0, by1);
+  wpe_sip<NC, 64>(op, K, Ue, ws + W::NBR + sb * 4 * W::NN, ws + W::COEF + ep * W::NP, ws + W::CFN + ep * 32,
+                  ws + W::QX, ws + W::QY, ws + W::DOT, ws + W::FCON, bx0, bx1, by0, by1);
   const double2 v = *reinterpret_cast<const double2*>(Ue + g * W::RP + n0);
   epi(gc, fma(a, fma(K.hwy, bx0, K.hwx[0] * by0), K.hh[0] * v.x),
       fma(a, fma(K.hwy, bx1, K.hwx[1] * by1), K.hh[1] * v.y), v.x, v.y);
@@ -1220,7 +1221,15 @@ __device__ __forceinline__ void wpe_field(const Op2DDev& op, double* ws, const M
   }
 }
 
-// the block's share of phase B: warps stride over elements
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// the block's share of phase B: warps stride over elements; each warp runs a
+// two-stage cp.async pipeline over its (element, field) tasks -- the staging
+// of the next task (one field of the element and of its four face
+// neighbours; the coefficient with field 0) is in flight while the current
+// task's contractions run.  Same tasks, same order, same arithmetic as the
+// unpipelined version (bitwise).
 template <int NC, typename Epi>
 __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const double* src, const double* Cf,
                                           double a, Epi&& epi, long long* tacc = nullptr,
@@ -1235,44 +1244,62 @@ __device__ __forceinline__ void wpe_phase(const Op2DDev& op, double* sm, const d
   const int r = lane >> 2, cc = (lane & 3) * 2;
   const int f = lane >> 3, k = lane & 7;
   const int fnode = f == FR ? k * 8 : f == FL ? k * 8 + 7 : f == FT ? k : 56 + k;   // neighbour's face node
-  const double* srcc[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) srcc[c] = src + c * nn;
   const int swz = r * 8 + 2 * ((lane & 3) ^ (r >> 1));            // row r, chunk lane&3 (swizzled)
   const int tr0 = nsw(lane & 7, lane >> 3), tr1 = nsw(lane & 7, 4 + (lane >> 3));   // transposed: node v -> line v%8, pos v/8
-  for (int e = blockIdx.x * nwb + warp; e < ne; e += gridDim.x * nwb) {
+  const int stride = gridDim.x * nwb;
+  auto eoff = [&](int e) -> unsigned {
+    const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
+    return ((unsigned)ey * op.nex + ex) * 64u;
+  };
+  // stage field c of element e (and its neighbours' field c) into buffer sb;
+  // field 0 also stages the element's coefficients into parity ep
+  auto issue = [&](int e, int c, int sb, int ep) {
     const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
     const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
     const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
     const unsigned eo = ((unsigned)ey * op.nex + ex) * 64u;
-    const unsigned nb[4] = {((unsigned)ey * op.nex + exr) * 64u, ((unsigned)ey * op.nex + exl) * 64u,
-                            ((unsigned)eyt * op.nex + ex) * 64u, ((unsigned)eyb * op.nex + ex) * 64u};
-#pragma unroll
-    for (int c = 0; c < NC; ++c) cp_async16(ws + W::OWN + c * W::NP + r * W::RP + cc, srcc[c] + eo + 2 * lane);
-    cp_async16(ws + W::COEF + r * W::RP + cc, Cf + eo + 2 * lane);
+    const unsigned nbR = ((unsigned)ey * op.nex + exr) * 64u, nbL = ((unsigned)ey * op.nex + exl) * 64u;
+    const unsigned nbT = ((unsigned)eyt * op.nex + ex) * 64u, nbB = ((unsigned)eyb * op.nex + ex) * 64u;
+    const double* sc = src + c * nn;
+    double* nbr = ws + W::NBR + sb * 4 * W::NN;
+    cp_async16(ws + W::OWN + sb * W::NP + r * W::RP + cc, sc + eo + 2 * lane);
     // face lines in swizzled rows: R/L neighbours row-wise (16-byte copies), T/B
     // neighbours transposed (8-byte copies) so every face line is a row
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      cp_async16(ws + W::NBR + (FR * NC + c) * 64 + swz, srcc[c] + nb[FR] + 2 * lane);
-      cp_async16(ws + W::NBR + (FL * NC + c) * 64 + swz, srcc[c] + nb[FL] + 2 * lane);
-      cp_async8(ws + W::NBR + (FT * NC + c) * 64 + tr0, srcc[c] + nb[FT] + lane);
-      cp_async8(ws + W::NBR + (FT * NC + c) * 64 + tr1, srcc[c] + nb[FT] + 32 + lane);
-      cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr0, srcc[c] + nb[FB] + lane);
-      cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr1, srcc[c] + nb[FB] + 32 + lane);
+    cp_async16(nbr + FR * 64 + swz, sc + nbR + 2 * lane);
+    cp_async16(nbr + FL * 64 + swz, sc + nbL + 2 * lane);
+    cp_async8(nbr + FT * 64 + tr0, sc + nbT + lane);
+    cp_async8(nbr + FT * 64 + tr1, sc + nbT + 32 + lane);
+    cp_async8(nbr + FB * 64 + tr0, sc + nbB + lane);
+    cp_async8(nbr + FB * 64 + tr1, sc + nbB + 32 + lane);
+    if (c == 0) {
+      cp_async16(ws + W::COEF + ep * W::NP + r * W::RP + cc, Cf + eo + 2 * lane);
+      cp_async8(ws + W::CFN + ep * 32 + lane, Cf + (f == FR ? nbR : f == FL ? nbL : f == FT ? nbT : nbB) + fnode);
     }
-    // neighbour face coefficient: asynchronous too (a blocking load here stalled the warp)
-    cp_async8(ws + W::CFN + lane, Cf + (f == FR ? nb[FR] : f == FL ? nb[FL] : f == FT ? nb[FT] : nb[FB]) + fnode);
-    const long long c0 = clock64();
-    cp_async_wait_all();
-    const int g = lane >> 2, n0 = 2 * (lane & 3);
-    __syncwarp();
-    const long long gi = (long long)eo + g * 8 + n0;
-    const long long c1 = clock64();
+  };
+  int e = blockIdx.x * nwb + warp;
+  if (e >= ne) return;
+  issue(e, 0, 0, 0);
+  cp_async_commit();
+  int sb = 0, ep = 0;
+  const int g = lane >> 2, n0 = 2 * (lane & 3);
+  for (; e < ne; e += stride, ep ^= 1) {
+    const long long gi = (long long)eoff(e) + g * 8 + n0;
+    const long long c0 = tacc ? clock64() : 0;
 #pragma unroll 1
-    for (int c = 0; c < NC; ++c) wpe_field<NC>(op, ws, K, c, a, gi, epi, px);
-    if (tacc) { tacc[0] += c1 - c0; tacc[1] += clock64() - c1; tacc[2] += 1; }
+    for (int c = 0; c < NC; ++c) {
+      const bool last = c + 1 == NC;
+      const int en = last ? e + stride : e;
+      if (en < ne) issue(en, last ? 0 : c + 1, sb ^ 1, last ? ep ^ 1 : ep);
+      cp_async_commit();    // one group per task (possibly empty)
+      cp_async_wait_1();    // this task's group has landed
+      __syncwarp();
+      wpe_field<NC>(op, ws, sb, ep, K, c, a, gi, epi, px);
+      __syncwarp();         // buffer sb is refilled by the next task's prefetch
+      sb ^= 1;
+    }
+    if (tacc) { tacc[1] += clock64() - c0; tacc[2] += 1; }
   }
+  cp_async_wait_all();
 }
 
 // ------------------------------------------------------------------------
