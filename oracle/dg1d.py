@@ -52,9 +52,10 @@ class Burgers:
     ncomp = 1
     linear = False
 
-    def __init__(self, nu=0.0, boundary=None):
+    def __init__(self, nu=0.0, boundary=None, source=None):
         self.nu = float(nu)
         self.boundary = boundary   # t -> (left state, right state), problems.py:66
+        self.source = source       # (x, t, u3) -> values, problems.py:61-65
 
     def flux(self, u):
         return 0.5 * u * u
@@ -306,6 +307,11 @@ class Op1D:
         c = self.physical_coeff(self.u3(u))
         if kind_of(c) != "none":
             out = out + self.apply_diffusion(c, u, t)
+        src = getattr(self.prob, "source", None)   # dgsem.py:343-347
+        if src is not None:
+            vals = src(self.x_nodes, t, self.u3(u))
+            if vals is not None:
+                out = out + (np.asarray(vals) + np.zeros((self.nc, 1, 1))).reshape(-1)
         bad = ~np.isfinite(out.reshape(self.nc, self.ne, self.p1))
         if bad.any():
             e = int(np.nonzero(bad.any(axis=(0, 2)))[0][0])

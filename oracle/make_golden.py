@@ -24,7 +24,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from sisdc import collocation as rc, dgsem as rd, mlsdc as rm, problems as rp, sdc as rs, transfer as rt  # noqa: E402
 
 from oracle.cg import bicgstab, element_block_preconditioner, pcg, pcg_hs  # noqa: E402
-from paper_2504_18526_b200.configs import CFG1, CFG2, CNS_CASES  # noqa: E402
+from paper_2504_18526_b200.configs import CFG1, CFG2, CNS_CASES, MANUFACTURED  # noqa: E402
 
 OUT = os.path.join(REPO, "tests", "golden")
 
@@ -419,8 +419,70 @@ def gen_cns():
     np.savez_compressed(os.path.join(OUT, "cns.npz"), **out)
 
 
+def gen_sources():
+    """Burgers with a source term (problems.py:55-92, dgsem.py:328-347): the
+    reference's manufactured steady state (test_dgsem.py:365-380), eval_rhs and
+    apply_source on a manufactured unsteady solution, a single-level SDC slab
+    and two SI-MLSDC steps (SuperLU and the pinned PCG) on a Dirichlet mesh."""
+    out = {}
+    w = MANUFACTURED
+    nu0, ww = 0.05, 2 * np.pi
+
+    def src_ss(x, t, u=None):
+        return (2.0 + np.sin(ww * x)) * ww * np.cos(ww * x) + nu0 * ww * ww * np.sin(ww * x)
+    prob = rp.Burgers(nu0, source=src_ss, boundary=lambda t: (np.array([2.0 + np.sin(-ww)]),
+                                                               np.array([2.0 + np.sin(ww)])))
+    op = rd.DGOperator(rd.Mesh1D(-1.0, 1.0, 20, 12, bc="dirichlet"), prob)
+    u = op.flat((2.0 + np.sin(ww * op.mesh.nodes_x))[None])
+    out["ss_u"] = u
+    out["ss_rhs"] = op.eval_rhs(u, 0.0)
+
+    def mk(P):
+        return rd.DGOperator(rd.Mesh1D(-1.0, 1.0, w.n_elem, P, bc="dirichlet"),
+                             rp.Burgers(w.nu, source=w.source, boundary=w.boundary))
+    fine = mk(w.p_fine)
+    u0 = fine.flat(w.exact(fine.mesh.nodes_x, 0.0)[None])
+    lam = float(np.max(np.abs(u0)))
+    dt = rd.dt_from_cfl(w.cfl, fine.mesh.dx, lam, w.p_fine)
+    out["u0"], out["dt"] = u0, np.array(dt)
+    out["rhs_t03"] = fine.eval_rhs(u0, 0.3)
+    out["src_t03"] = fine.apply_source(u0, 0.3)
+    rule = rc.make_nodes("radau_right", w.m_fine)
+    sol = rs.run_sdc(fine, rule, rc.make_weights(rule), dt, "si2", u0, 0.0, 2)
+    out["sdc2_u"], out["sdc2_f"] = sol.u, sol.f
+
+    def hier():
+        ops = [mk(P) for P in (w.p_coarse, w.p_fine)]
+        rules = [rc.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
+        levels = [rm.Level(o, r, rc.make_weights(r), "si2") for o, r in zip(ops, rules)]
+        pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_only")
+        spat = rt.build_spatial_p_transfer(w.p_coarse, w.p_fine, w.n_elem, 1, "embedded")
+        return rm.Hierarchy(levels, [rt.SpaceTimeTransfer(pair, spat)], n_coarse=2, n_sweep=1,
+                            form="incremental", post_sweep_on_finest=True)
+    h = hier()
+    u = u0
+    for s_ in (1, 2):
+        u = rm.run_mlsdc(h, u, (s_ - 1) * dt, dt, w.n_cycles, strategy="fmg").end_value.copy()
+        out[f"mlsdc_lu_u{s_}"] = u
+    h = hier()
+    with PcgPatch(1e-14, pcg) as pp:
+        u = u0
+        for s_ in (1, 2):
+            n0 = len(pp.log)
+            u = rm.run_mlsdc(h, u, (s_ - 1) * dt, dt, w.n_cycles, strategy="fmg").end_value.copy()
+            out[f"mlsdc_pcg_u{s_}"] = u
+            out[f"mlsdc_pcg_iters{s_}"] = np.array([it for it, _ in pp.log[n0:]])
+    out["exact_t2"] = fine.flat(w.exact(fine.mesh.nodes_x, 2 * dt)[None])
+    print("sources: steady |rhs| max", np.abs(out["ss_rhs"]).max(), "mlsdc vs exact",
+          np.linalg.norm(out["mlsdc_lu_u2"] - out["exact_t2"]) / np.linalg.norm(out["exact_t2"]))
+    np.savez_compressed(os.path.join(OUT, "sources.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "sources":
+        gen_sources()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "cns":
         gen_cns()
         sys.exit(0)
@@ -444,5 +506,6 @@ if __name__ == "__main__":
     gen_presmooth()
     gen_htransfer()
     gen_cns()
+    gen_sources()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

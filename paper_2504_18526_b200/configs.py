@@ -280,3 +280,41 @@ CNS_CASES = (
     AcousticWorkload("cns_mlsdc_visc", n_elem=16, p_fine=6, p_coarse=3, m_fine=4, m_coarse=2, scheme="si2",
                      cfl=1.0, eta=2e-4, mlsdc=True, n_steps=1),
 )
+
+
+# --------------------------------------- Burgers with a manufactured source term
+@dataclass(frozen=True)
+class ManufacturedWorkload:
+    """Burgers with the source that makes u*(x, t) = 2 + a sin(k x + w t) an
+    exact solution (the reference's ``manufactured_burgers_source``,
+    ``problems.py:85-92``: src = u_t + u u_x - nu u_xx), Dirichlet trace data
+    from u* on [-1, 1]: the parity workload of the host-evaluated source term
+    (``dgsem.py:328-347``)."""
+    nu: float = 0.05
+    amp: float = 0.5
+    k: float = math.pi
+    w: float = 1.0
+    n_elem: int = 12
+    p_fine: int = 6
+    p_coarse: int = 3
+    m_fine: int = 4
+    m_coarse: int = 2
+    cfl: float = 1.0
+    n_cycles: int = 2
+
+    def exact(self, x, t=0.0):
+        return 2.0 + self.amp * np.sin(self.k * np.asarray(x) + self.w * t)
+
+    def source(self, x, t, u=None):
+        ph = self.k * np.asarray(x) + self.w * t
+        u_ = 2.0 + self.amp * np.sin(ph)
+        ut = self.amp * self.w * np.cos(ph)
+        ux = self.amp * self.k * np.cos(ph)
+        uxx = -self.amp * self.k * self.k * np.sin(ph)
+        return ut + u_ * ux - self.nu * uxx
+
+    def boundary(self, t):
+        return np.array([self.exact(-1.0, t)]), np.array([self.exact(1.0, t)])
+
+
+MANUFACTURED = ManufacturedWorkload()

@@ -31,6 +31,11 @@ from ._lib import Coef, SolverError
 from .collocation import gauss_lobatto
 from .runtime import get_runtime
 
+
+def torch_isfinite(t):
+    import torch
+    return torch.isfinite(t)
+
 __all__ = ["Mesh1D", "DGOperator", "SolverError", "ArtificialViscosityParams", "SICoefficient",
            "compute_delta", "cfl_number", "dt_from_cfl", "max_wave_speed", "smooth_start"]
 
@@ -130,8 +135,6 @@ class DGOperator:
                  penalty_const: float = 2.0, device: int = 0, eager_checks: bool = True):
         if mesh.bc == "dirichlet" and getattr(problem, "boundary_state", None) is None:
             raise ValueError("dirichlet mesh needs a problem with boundary_state(t)")   # dgsem.py:150-151
-        if getattr(problem, "source", None) is not None:
-            raise NotImplementedError("source terms are not built on the GPU path")
         self.mesh = mesh
         self.problem = problem
         self.av = av
@@ -163,6 +166,9 @@ class DGOperator:
         self.mass_node = 0.5 * mesh.dx * wts
         self.inv_mass = 1.0 / self.mass_node
         self.mu0 = penalty_const * self.p1 ** 2 / mesh.dx
+        # source(x, t, u3) (dgsem.py:328-352): a host callable, evaluated on the host
+        # at the node coordinates and added to f on the device (no graph capture)
+        self.source_fn = getattr(problem, "source", None)
         self.nu_art = None            # device tensor (n_elem,) when AV is active
         self._last_dt = None
         self._scratch = None
@@ -284,12 +290,42 @@ class DGOperator:
             self.rt.reset_status()
         self.boundary_at(t)
         self.rt.check(self.lib.sisdc_eval_rhs(self.h, u.data_ptr(), float(t), out.data_ptr()), "eval_rhs")
+        if self.source_fn is not None:
+            self.add_source(out, u, t)
+            self._check_finite(out)
         if self.eager_checks:
             self.rt.raise_on_failure()
         return out
 
+    def _source_values(self, u, t: float):
+        """src(x, t, u3) on the host (dgsem.py:328-335), broadcast over the
+        components, as a device vector; None when the source returns None."""
+        u3 = self.as_nodes(u).detach().cpu().numpy()
+        vals = self.source_fn(self.mesh.nodes_x, float(t), u3)
+        if vals is None:
+            return None
+        v = np.asarray(vals, dtype=np.float64) + np.zeros((self.ncomp, 1, 1))
+        return self.rt.to_device(np.ascontiguousarray(v.reshape(-1)))
+
+    def add_source(self, f, u, t: float) -> None:
+        """f += src(x, t, u) (the source term of eval_rhs, dgsem.py:343-347)."""
+        if self.source_fn is None:
+            return
+        v = self._source_values(u, t)
+        if v is not None:
+            f.add_(v)
+
+    def _check_finite(self, out) -> None:
+        bad = ~torch_isfinite(out.reshape(self.ncomp, self.mesh.n_elem, self.p1))
+        if bool(bad.any()):
+            e = int(bad.any(dim=0).any(dim=1).nonzero()[0, 0])
+            raise SolverError(f"non-finite right-hand side in element {e}")
+
     def apply_source(self, u, t: float):
-        return self.rt.zeros(self.ndof)
+        if self.source_fn is None:
+            return self.rt.zeros(self.ndof)
+        v = self._source_values(self.rt.to_device(u), t)
+        return self.rt.zeros(self.ndof) if v is None else v
 
     def coefficient_field(self, coeff):
         """Materialise a coefficient as an (n_elem, P+1) device field

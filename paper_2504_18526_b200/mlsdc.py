@@ -111,6 +111,9 @@ def fas_rhs(hier: Hierarchy, i: int, dt: float):
         lower.ctx.boundary_at(*times)
     ta, tp = _lib.darr(times)
     rt.check(rt.lib.sisdc_eval_rhs_nodes(lower.ctx.h, Mc, v.data_ptr(), tp, fr.data_ptr()), "eval_rhs_nodes")
+    if getattr(lower.ctx, "source_fn", None) is not None:
+        for m in range(Mc):
+            lower.ctx.add_source(fr[m], v[m], times[m])
     Wc = lower.weights.w_nn if inc else lower.weights.w_0n
     wca, wcp = _lib.darr(Wc)
     rt.check(rt.lib.sisdc_collocation_defect(lower.ctx.h, Mc, wcp, float(dt), inc, lower.u0.data_ptr(), v.data_ptr(),
@@ -267,6 +270,8 @@ class SlabGraph:
         fine = hier.fine
         if any(getattr(lv.ctx, "dirichlet", False) for lv in hier.levels):
             raise ValueError("time-dependent Dirichlet data cannot be captured into a replayed slab graph")
+        if any(getattr(lv.ctx, "source_fn", None) is not None for lv in hier.levels):
+            raise ValueError("a host-evaluated source term cannot be captured into a replayed slab graph")
         rt = fine.ctx.rt
         self.rt, self.hier = rt, hier
         self.u = rt.to_device(u0_fine).clone()

@@ -94,6 +94,9 @@ def _caches(ctx, scheme, sol, M, m_first, m_count, dts, conv_prev=None, times=No
         ctx.h, _scheme_id(scheme), M, m_first, m_count, sol.u0.data_ptr(), sol.u.data_ptr(),
         None if conv_prev is None else conv_prev.data_ptr(), p, float(sol.t0), tp,
         sol.f.data_ptr(), sol.h1.data_ptr(), None if sol.h2 is None else sol.h2.data_ptr()), "node_caches")
+    if getattr(ctx, "source_fn", None) is not None:   # f += src(x, t_m, u_m), host callable (dgsem.py:343-347)
+        for m in range(m_first, m_first + m_count):
+            ctx.add_source(sol.f[m], sol.u[m], times[m])
 
 
 def refresh_caches(ctx, rule: CollocationRule, dt: float, scheme: str, sol: NodalSolution) -> None:

@@ -223,3 +223,36 @@ def test_cns_oracle_pinned_to_reference(golden, case):
     for s, u in enumerate(res):
         assert np.linalg.norm(u - G[f"{case}_bicg_u{s + 1}"]) / np.linalg.norm(u) < 1e-12
         assert np.linalg.norm(u - G[f"{case}_lu_u{s + 1}"]) / np.linalg.norm(u) < 5e-11
+
+
+def test_source_terms_pinned_to_reference(golden):
+    """Burgers with a source term (dgsem.py:328-347):
+    the oracle restatement reproduces the reference's manufactured steady
+    state, eval_rhs with the unsteady manufactured source, and two SI-MLSDC
+    steps with the pinned PCG (identical iteration sequence)."""
+    from paper_2504_18526_b200.configs import MANUFACTURED as w
+    G = golden["sources"]
+    nu0, ww = 0.05, 2 * np.pi
+
+    def src_ss(x, t, u=None):
+        return (2.0 + np.sin(ww * x)) * ww * np.cos(ww * x) + nu0 * ww * ww * np.sin(ww * x)
+    op = dg1d.Op1D(-1.0, 1.0, 20, 12, dg1d.Burgers(nu0, source=src_ss, boundary=lambda t: (
+        np.array([2.0 + np.sin(-ww)]), np.array([2.0 + np.sin(ww)]))), bc="dirichlet")
+    assert np.abs(op.eval_rhs(G["ss_u"], 0.0) - G["ss_rhs"]).max() < 1e-9
+    log = []
+
+    def mk(P):
+        return dg1d.Op1D(-1.0, 1.0, w.n_elem, P, dg1d.Burgers(w.nu, boundary=w.boundary, source=w.source),
+                         bc="dirichlet", cg_log=log)
+    fine = mk(w.p_fine)
+    u0, dt = G["u0"], float(G["dt"])
+    assert rel(fine.eval_rhs(u0, 0.3), G["rhs_t03"]) < 1e-12
+    h = sweeper.build_two_level(lambda lvl: mk(w.p_coarse if lvl == "coarse" else w.p_fine),
+                                sweeper.Rule("radau_right", w.m_coarse), sweeper.Rule("radau_right", w.m_fine))
+    u = u0
+    for s in (1, 2):
+        n0 = len(log)
+        u = sweeper.run_mlsdc(h, u, (s - 1) * dt, dt, w.n_cycles).u[-1].copy()
+        assert [it for it, _ in log[n0:]] == G[f"mlsdc_pcg_iters{s}"].tolist()
+        assert np.linalg.norm(u - G[f"mlsdc_pcg_u{s}"]) / np.linalg.norm(u) < 1e-12
+        assert np.linalg.norm(u - G[f"mlsdc_lu_u{s}"]) / np.linalg.norm(u) < 1e-11
