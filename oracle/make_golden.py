@@ -478,8 +478,39 @@ def gen_sources():
     np.savez_compressed(os.path.join(OUT, "sources.npz"), **out)
 
 
+STUDY_CONFIG = {
+    "study": "cfl-sweep",
+    "problem": {"kind": "convection_diffusion", "speed": 1.0, "nu": 0.002},
+    "levels": [{"n_elem": 12, "degree": 3, "n_nodes": 2}, {"n_elem": 12, "degree": 6, "n_nodes": 4}],
+    "time": {"t_end": 0.05},
+    "sweep": {"cfl_values": [0.5, 1.0, 2.0, 4.0], "max_iterations": 6},
+    "reference": {"kind": "exact"},
+}
+
+
+def gen_study():
+    """The reference CLI's own cfl-sweep study (cli.py:1110-1194) on its
+    wave-packet convection-diffusion problem, run in-process: its
+    errors.csv / iterations.csv contents are the goldens of the GPU ensemble
+    dispatch (paper_2504_18526_b200/study.py)."""
+    import json
+    import tempfile
+    from sisdc import cli as rcli
+    cfg = rcli.parse_config(json.dumps(STUDY_CONFIG))
+    with tempfile.TemporaryDirectory() as d:
+        outputs, failures = rcli.run_study(cfg, d)
+        err = open(os.path.join(d, "errors.csv")).read()
+        its = open(os.path.join(d, "iterations.csv")).read()
+    out = {"config": np.array(json.dumps(STUDY_CONFIG)), "errors_csv": np.array(err), "iterations_csv": np.array(its)}
+    print(its)
+    np.savez_compressed(os.path.join(OUT, "study.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "study":
+        gen_study()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "sources":
         gen_sources()
         sys.exit(0)
@@ -507,5 +538,6 @@ if __name__ == "__main__":
     gen_htransfer()
     gen_cns()
     gen_sources()
+    gen_study()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -99,3 +99,26 @@ def burgers_front_problem(nu: float):
         return np.array([exact(-1.0, t)]), np.array([exact(1.0, t)])
 
     return Burgers(nu, boundary=boundary), exact
+
+
+def wave_packet_exact(nu, speed: float = 1.0, wave_numbers=None, amplitudes=None, shifts=None):
+    """Decaying multi-mode packet, exact for constant-coefficient
+    convection-diffusion on a periodic unit interval (``problems.py:247-270``;
+    the reference's default modes).  exact(x, t) = sum_j a_j exp(-k_j^2 nu t)
+    sin(k_j (x - s_j - v t))."""
+    import numpy as np
+    kap = np.asarray(2.0 * np.pi * np.array([1.0, 3.0, 5.0, 7.0, 9.0, 12.0, 15.0])
+                     if wave_numbers is None else wave_numbers, dtype=float)
+    amp = np.asarray(np.array([1.00, 1.50, 1.80, 1.70, 1.50, 1.30, 1.15])
+                     if amplitudes is None else amplitudes, dtype=float)
+    sft = np.asarray(np.array([0.00, 0.05, 0.10, 0.15, 0.20, 0.30, 0.18]) if shifts is None else shifts,
+                     dtype=float)
+    nu, speed = float(nu), float(speed)
+
+    def exact(x, t=0.0):
+        x = np.asarray(x)
+        phase = kap.reshape((-1,) + (1,) * x.ndim) * (x[None] - sft.reshape((-1,) + (1,) * x.ndim) - speed * t)
+        decay = np.exp(-(kap ** 2) * nu * t)
+        return np.tensordot(amp * decay, np.sin(phase), axes=(0, 0))
+
+    return exact

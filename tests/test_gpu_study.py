@@ -1,0 +1,49 @@
+"""The reference CLI's own cfl-sweep study (cli.py:1110-1194, wave-packet
+convection-diffusion, two p-levels, exact reference) run through the GPU
+ensemble dispatch (paper_2504_18526_b200/study.py): the same n_steps, stall
+iterations and status per CFL point, and the error series of
+errors.csv / iterations.csv to 1e-9 relative (tests/golden/study.npz)."""
+import json
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+def parse(text):
+    lines = text.strip().split("\n")
+    return lines[0], [ln.split(",") for ln in lines[1:]]
+
+
+def test_cfl_sweep_matches_reference_cli(golden):
+    from paper_2504_18526_b200 import dgsem, mlsdc, problems, study
+    G = golden["study"]
+    cfg = json.loads(str(G["config"]))
+    pr, lv = cfg["problem"], cfg["levels"]
+    prob = problems.ConvectionDiffusion(pr["speed"], pr["nu"])
+    exact = problems.wave_packet_exact(pr["nu"], pr["speed"])
+    h = mlsdc.build_p_hierarchy(lambda P: dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, lv[1]["n_elem"], P), prob),
+                                [lv[0]["degree"], lv[1]["degree"]], [lv[0]["n_nodes"], lv[1]["n_nodes"]])
+    op = h.fine.ctx
+    u0 = op.nodal_field(lambda x: exact(x, 0.0)[None])
+    u_ref = op.nodal_field(lambda x: exact(x, cfg["time"]["t_end"])[None])
+    st = study.MLSDCStudy(h, u0, u_ref, cfg["time"]["t_end"], dgsem.max_wave_speed(op, u0))
+    with tempfile.TemporaryDirectory() as d:
+        pts = study.cfl_sweep(st, cfg["sweep"]["cfl_values"], cfg["sweep"]["max_iterations"], out_dir=d)
+        it_text = open(os.path.join(d, "iterations.csv")).read()
+        err_text = open(os.path.join(d, "errors.csv")).read()
+    assert len(pts) == len(cfg["sweep"]["cfl_values"])
+    for mine, ref in ((it_text, str(G["iterations_csv"])), (err_text, str(G["errors_csv"]))):
+        h1, rows = parse(mine)
+        h2, rrows = parse(ref)
+        assert h1 == h2 and len(rows) == len(rrows)
+        for a, b in zip(rows, rrows):
+            assert a[:3] == b[:3]                     # cfl, n_steps, stall / iteration index
+            if len(a) > 4:
+                assert a[4] == b[4]                   # status
+            assert abs(float(a[3]) - float(b[3])) <= 1e-9 * abs(float(b[3]))
