@@ -144,7 +144,7 @@ int  sisdc_op1d_tables(const sisdc_op1d* op, double* nodes, double* weights, dou
 int  sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art);
 /* Dirichlet trace data (problem.boundary_state(t), dgsem.py:212-216,282-284):
  * register the outside states g_l(t_j), g_r(t_j) for n times (merged into the
- * operator's table).  Every entry point that takes a time t (or node times)
+ * operator's table); gl, gr are (n, ncomp) row-major (ncomp = 3 for CNS).  Every entry point that takes a time t (or node times)
  * on a Dirichlet operator looks its data up here and fails with
  * SISDC_ERR_ARG for an unregistered time. */
 int  sisdc_op1d_set_boundary(sisdc_op1d* op, int n, const double* times, const double* gl, const double* gr);

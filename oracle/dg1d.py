@@ -265,8 +265,6 @@ class Op1D:
             B -= s * lm[:, :, None] * self.D[-1][None, None, :]
             B -= s * np.roll(lp, 1, axis=-1)[:, :, None] * self.D[0][None, None, :]
             return (-B / self.mass).reshape(-1)
-        if k == "matrix":
-            raise NotImplementedError("Dirichlet faces with matrix coefficients")
         # Dirichlet (dgsem.py:282-308): faces 0..ne; outside states g(t), q and C
         # one-sided at the outer faces, adjoint-lift weight 1 there
         gl, gr = self._bstate(t)
@@ -279,12 +277,19 @@ class Op1D:
         wf = np.full(self.ne + 1, 0.5)
         wf[0] = wf[-1] = 1.0
         jump = uf_m - uf_p
-        pen = self.mu0 * (0.5 * (cf_m + cf_p))[None] * jump
+        if k == "matrix":   # (nf, nc, nc) face coefficients acting on the jump vectors
+            pen = self.mu0 * np.einsum("fab,bf->af", 0.5 * (cf_m + cf_p), jump)
+            lift_m = np.einsum("f,fab,bf->af", wf, cf_m, jump)
+            lift_p = np.einsum("f,fab,bf->af", wf, cf_p, jump)
+        else:
+            pen = self.mu0 * (0.5 * (cf_m + cf_p))[None] * jump
+            lift_m = (wf * cf_m)[None] * jump
+            lift_p = (wf * cf_p)[None] * jump
         Gf = -0.5 * (qf_m + qf_p) + pen
         B[:, :, -1] += Gf[:, 1:]
         B[:, :, 0] -= Gf[:, :-1]
-        B -= s * ((wf * cf_m)[None] * jump)[:, 1:, None] * self.D[-1][None, None, :]
-        B -= s * ((wf * cf_p)[None] * jump)[:, :-1, None] * self.D[0][None, None, :]
+        B -= s * lift_m[:, 1:, None] * self.D[-1][None, None, :]
+        B -= s * lift_p[:, :-1, None] * self.D[0][None, None, :]
         return (-B / self.mass).reshape(-1)
 
     # rhs (dgsem.py:313-352) ---------------------------------------------

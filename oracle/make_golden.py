@@ -24,7 +24,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from sisdc import collocation as rc, dgsem as rd, mlsdc as rm, problems as rp, sdc as rs, transfer as rt  # noqa: E402
 
 from oracle.cg import bicgstab, element_block_preconditioner, pcg, pcg_hs  # noqa: E402
-from paper_2504_18526_b200.configs import CFG1, CFG2, CNS_CASES, MANUFACTURED  # noqa: E402
+from paper_2504_18526_b200.configs import CFG1, CFG2, CNS_CASES, MANUFACTURED, SOD_CASES  # noqa: E402
 
 OUT = os.path.join(REPO, "tests", "golden")
 
@@ -478,6 +478,61 @@ def gen_sources():
     np.savez_compressed(os.path.join(OUT, "sources.npz"), **out)
 
 
+def gen_sod():
+    """1-D CompressibleFlow with Dirichlet faces: the reference CLI's Sod shock
+    tube (cli.py:766-772) with Persson-Peraire viscosity, two SI-MLSDC steps
+    with SuperLU (as shipped) and with the pinned BiCGStab, plus operators
+    (convection with the boundary states, eval_rhs, the modal sensor, the
+    affine matrix SIP and one implicit solve) at the initial state."""
+    out = {}
+    for w in SOD_CASES:
+        left, right = w.states()
+
+        def build():
+            prob = rp.CompressibleFlow(gamma=w.gamma, R_gas=w.R_gas, eta=w.eta, Pr=w.prandtl,
+                                       boundary=lambda t: (left, right))
+            av = rd.ArtificialViscosityParams(*w.av) if w.av else None
+            ops = [rd.DGOperator(rd.Mesh1D(0.0, 1.0, w.n_elem, P, bc="dirichlet"), prob, av=av)
+                   for P in (w.p_coarse, w.p_fine)]
+            rules = [rc.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
+            levels = [rm.Level(o, r, rc.make_weights(r), "si2") for o, r in zip(ops, rules)]
+            pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_only")
+            spat = rt.build_spatial_p_transfer(w.p_coarse, w.p_fine, w.n_elem, 3, "embedded")
+            return rm.Hierarchy(levels, [rt.SpaceTimeTransfer(pair, spat)], n_coarse=2, n_sweep=1,
+                                form="incremental", post_sweep_on_finest=True), ops
+        h, ops = build()
+        fine = ops[1]
+        u0 = fine.nodal_field(w.initial)
+        lam = rd.max_wave_speed(fine, u0)
+        dt = rd.dt_from_cfl(w.cfl, fine.mesh.dx, lam, w.p_fine)
+        k = w.name
+        out[k + "_u0"], out[k + "_dt"] = u0, np.array(dt)
+        op = rd.DGOperator(rd.Mesh1D(0.0, 1.0, w.n_elem, w.p_fine, bc="dirichlet"), fine.problem,
+                           av=rd.ArtificialViscosityParams(*w.av) if w.av else None)
+        out[k + "_conv"] = op.apply_convection(u0, 0.0)
+        op.begin_slab(u0, 0.0, dt)
+        out[k + "_nu_art"] = op.persson_viscosity(u0)
+        out[k + "_rhs"] = op.eval_rhs(u0, 0.0)
+        c = op.modified_diffusion_matrix(u0, 0.5 * dt, "si2")
+        out[k + "_modc"] = c
+        out[k + "_diff"] = op.apply_diffusion(c, u0, 0.0)
+        out[k + "_solve"] = op.implicit_solve(c, 0.5 * dt, u0, 0.0)
+        u = u0
+        for s_ in range(w.n_steps):
+            u = rm.run_mlsdc(h, u, s_ * dt, dt, w.n_cycles, strategy="fmg").end_value.copy()
+            out[f"{k}_lu_u{s_ + 1}"] = u
+        h, ops = build()
+        with PcgPatch(1e-14, bicgstab) as pp:
+            u = u0
+            for s_ in range(w.n_steps):
+                u = rm.run_mlsdc(h, u, s_ * dt, dt, w.n_cycles, strategy="fmg").end_value.copy()
+                out[f"{k}_bicg_u{s_ + 1}"] = u
+        out[k + "_bicg_iters"] = np.array([it for it, _ in pp.log])
+        print(k, "solves", len(pp.log), "max it", max(it for it, _ in pp.log), "lu vs bicg",
+              np.linalg.norm(out[f"{k}_lu_u{w.n_steps}"] - u) / np.linalg.norm(u))
+    np.savez_compressed(os.path.join(OUT, "sod.npz"), **out)
+
+
 STUDY_CONFIG = {
     "study": "cfl-sweep",
     "problem": {"kind": "convection_diffusion", "speed": 1.0, "nu": 0.002},
@@ -508,6 +563,9 @@ def gen_study():
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "sod":
+        gen_sod()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "study":
         gen_study()
         sys.exit(0)
@@ -539,5 +597,6 @@ if __name__ == "__main__":
     gen_cns()
     gen_sources()
     gen_study()
+    gen_sod()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

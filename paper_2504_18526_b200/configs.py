@@ -318,3 +318,48 @@ class ManufacturedWorkload:
 
 
 MANUFACTURED = ManufacturedWorkload()
+
+
+@dataclass(frozen=True)
+class SodWorkload:
+    """1-D CompressibleFlow on the reference CLI's Sod shock tube
+    (``cli.py:766-772``, ``problems.sod_init`` ``problems.py:319-331``):
+    (rho, v, p) = (1, 0, 1) left of the split, (0.125, 0, 0.1) right of it,
+    Dirichlet faces holding the two end states, Persson-Peraire viscosity."""
+    name: str
+    n_elem: int = 20
+    p_fine: int = 4
+    p_coarse: int = 2
+    m_fine: int = 3
+    m_coarse: int = 2
+    cfl: float = 0.5
+    n_cycles: int = 2
+    n_steps: int = 2
+    eta: float = 0.0
+    av: tuple = (0.5, 0.5)
+    gamma: float = 1.4
+    R_gas: float = 287.28
+    prandtl: float = 0.75
+    split: float = 0.5
+
+    def states(self):
+        g = self.gamma
+        left = np.array([1.0, 0.0, 1.0 / (g - 1.0)])
+        right = np.array([0.125, 0.0, 0.1 / (g - 1.0)])
+        return left, right
+
+    def initial(self, x):
+        """Conservative (3, ...) field of the shock-tube data at x."""
+        x = np.asarray(x, dtype=float)
+        left, right = self.states()
+        lt = x < self.split
+        return np.stack([np.where(lt, left[c], right[c]) for c in range(3)])
+
+    def boundary(self, t):
+        return self.states()
+
+
+SOD_CASES = (
+    SodWorkload("sod_euler_av"),
+    SodWorkload("sod_ns_av", n_elem=16, p_fine=5, p_coarse=3, eta=1e-3, av=(1.0, 1.0), cfl=0.4),
+)

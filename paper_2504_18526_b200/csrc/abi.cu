@@ -94,18 +94,33 @@ bool invert(std::vector<double> A, int n, std::vector<double>& inv) {
   return true;
 }
 
-// Dirichlet trace data of time t from the operator's table (exact match)
-int bc_at(sisdc_op1d* op, double t, double& gl, double& gr) {
-  gl = gr = 0.0;
+// Dirichlet trace data of time t from the operator's table (exact match);
+// table rows (t, g_l[nc], g_r[nc])
+int bc_at3(sisdc_op1d* op, double t, double* gl, double* gr) {
+  const int nc = op->dim == 1 ? op->dev.nc : 1, st = 1 + 2 * nc;
+  for (int c = 0; c < nc; ++c) gl[c] = gr[c] = 0.0;
   if (op->dim != 1 || op->dev.bc != SISDC_DIRICHLET) return SISDC_OK;
-  for (size_t j = 0; j + 2 < op->btab.size(); j += 3)
-    if (op->btab[j] == t) { gl = op->btab[j + 1]; gr = op->btab[j + 2]; return SISDC_OK; }
+  for (size_t j = 0; j + st - 1 < op->btab.size(); j += st)
+    if (op->btab[j] == t) {
+      for (int c = 0; c < nc; ++c) { gl[c] = op->btab[j + 1 + c]; gr[c] = op->btab[j + 1 + nc + c]; }
+      return SISDC_OK;
+    }
   return C(op)->fail(SISDC_ERR_ARG, "no Dirichlet boundary data registered for t = " + std::to_string(t));
+}
+int bc_at(sisdc_op1d* op, double t, double& gl, double& gr) {
+  double l[3], r[3];
+  int rc = bc_at3(op, t, l, r);
+  gl = l[0];
+  gr = r[0];
+  return rc;
 }
 // the operator with its boundary states at time t
 int dev_at(sisdc_op1d* op, double t, Op1DDev& d) {
   d = op->dev;
-  return bc_at(op, t, d.gl, d.gr);
+  if (int rc = bc_at3(op, t, d.gl3, d.gr3)) return rc;
+  d.gl = d.gl3[0];
+  d.gr = d.gr3[0];
+  return SISDC_OK;
 }
 
 int check_coef(Ctx* c, sisdc_coef k);
@@ -258,8 +273,6 @@ int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) 
   if (d->degree + 1 > MAXP1) return c.fail(SISDC_ERR_UNSUPPORTED, "degree above 15");
   const bool cns = d->problem == SISDC_CNS1D;
   if (d->ncomp != (cns ? 3 : 1)) return c.fail(SISDC_ERR_ARG, "ncomp does not match the problem");
-  if (cns && d->bc != SISDC_PERIODIC)
-    return c.fail(SISDC_ERR_UNSUPPORTED, "1-D compressible flow is built for periodic meshes");
   if (cns && d->n_elem < 2) return c.fail(SISDC_ERR_UNSUPPORTED, "1-D compressible flow needs >= 2 elements");
   if (cns && !(d->gamma > 1.0)) return c.fail(SISDC_ERR_ARG, "gamma must exceed 1");
   if (cns && !(d->prandtl > 0.0)) return c.fail(SISDC_ERR_ARG, "Prandtl number must be positive");
@@ -310,6 +323,8 @@ int sisdc_op1d_create(sisdc_ctx* x, const sisdc_op1d_desc* d, sisdc_op1d** out) 
     const size_t nb = 3 * p1;
     e = cudaMalloc(&op->d_pinv, (size_t)d->n_elem * nb * nb * sizeof(double));
     if (e == cudaSuccess) e = cudaMalloc(&op->d_c9, (size_t)d->n_elem * p1 * 9 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&op->d_cws, (size_t)2 * 3 * d->n_elem * p1 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemset(op->d_cws, 0, (size_t)3 * d->n_elem * p1 * sizeof(double));   // zero vector
     if (e != cudaSuccess) {
       int rc = c.cuda(e, "cns block-Jacobi workspace");
       cudaFree(op->d_tab);
@@ -408,6 +423,7 @@ void sisdc_op1d_destroy(sisdc_op1d* op) {
   cudaFree(op->d_cgws);
   cudaFree(op->d_pinv);
   cudaFree(op->d_c9);
+  cudaFree(op->d_cws);
   delete op;
 }
 
@@ -443,13 +459,22 @@ int sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, dou
 
 int sisdc_op1d_set_boundary(sisdc_op1d* op, int n, const double* times, const double* gl, const double* gr) {
   if (!op || n < 0 || (n > 0 && (!times || !gl || !gr))) return SISDC_ERR_ARG;
+  const int nc = op->dim == 1 ? op->dev.nc : 1, st = 1 + 2 * nc;   // gl, gr: (n, ncomp)
   for (int j = 0; j < n; ++j) {
     bool found = false;
-    for (size_t q = 0; q + 2 < op->btab.size(); q += 3)
-      if (op->btab[q] == times[j]) { op->btab[q + 1] = gl[j]; op->btab[q + 2] = gr[j]; found = true; break; }
-    if (!found) { op->btab.push_back(times[j]); op->btab.push_back(gl[j]); op->btab.push_back(gr[j]); }
+    for (size_t q = 0; q + st - 1 < op->btab.size(); q += st)
+      if (op->btab[q] == times[j]) {
+        for (int c = 0; c < nc; ++c) { op->btab[q + 1 + c] = gl[j * nc + c]; op->btab[q + 1 + nc + c] = gr[j * nc + c]; }
+        found = true;
+        break;
+      }
+    if (!found) {
+      op->btab.push_back(times[j]);
+      for (int c = 0; c < nc; ++c) op->btab.push_back(gl[j * nc + c]);
+      for (int c = 0; c < nc; ++c) op->btab.push_back(gr[j * nc + c]);
+    }
   }
-  if (op->btab.size() > 3 * 4096) op->btab.erase(op->btab.begin(), op->btab.end() - 3 * 1024);   // keep recent times
+  if (op->btab.size() > (size_t)st * 4096) op->btab.erase(op->btab.begin(), op->btab.end() - st * 1024);   // keep recent times
   return SISDC_OK;
 }
 
@@ -457,7 +482,11 @@ int sisdc_apply_convection(sisdc_op1d* op, const double* u, double t, double* ou
   if (!op || !u || !out) return SISDC_ERR_ARG;
   if (op->parted()) return part2_conv(op, u, out);
   if (op->dim == 2) return launch2_conv(C(op), op->dev2, u, out);
-  if (op->cns()) return cns_conv(C(op), op->dev, u, out);
+  if (op->cns()) {
+    Op1DDev d;
+    if (int rc = dev_at(op, t, d)) return rc;
+    return cns_conv(C(op), d, u, out);
+  }
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_apply_convection(C(op), d, u, out);
@@ -470,7 +499,11 @@ int sisdc_apply_diffusion(sisdc_op1d* op, sisdc_coef k, const double* u, double 
     return C(op)->cuda(cudaMemsetAsync(out, 0, op->n() * sizeof(double), C(op)->stream), "zero");
   if (op->parted()) return part2_sip(op, coef(k), u, out);
   if (op->dim == 2) return launch2_sip(C(op), op->dev2, coef(k), u, out);
-  if (op->cns()) return cns_sip(C(op), op->dev, coef(k), u, out);
+  if (op->cns()) {
+    Op1DDev d;
+    if (int rc = dev_at(op, t, d)) return rc;
+    return cns_sip(C(op), d, coef(k), u, out);
+  }
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_apply_diffusion(C(op), d, coef(k), u, out);
@@ -481,7 +514,12 @@ int sisdc_eval_rhs(sisdc_op1d* op, const double* u, double t, double* out) {
   if (op->parted()) return part2_eval_nodes(op, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
-  if (op->cns()) return cns_node_eval(C(op), op->dev, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
+  if (op->cns()) {
+    double bnd[12] = {};
+    if (int rc = bc_at3(op, t, bnd, bnd + 3)) return rc;
+    return cns_node_eval(C(op), op->dev, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr,
+                         op->dev.bc == SISDC_DIRICHLET ? bnd : nullptr);
+  }
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_node_eval(C(op), d, 0, SISDC_SI2, 1, 0, 1, u, u, nullptr, nullptr, out, nullptr, nullptr);
@@ -508,7 +546,16 @@ int sisdc_implicit_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* r
   if (op->dim == 2) return launch2_cg(C(op), op->dev2, coef(k), a, rhs, x, op->d_cgws, op->cg_blocks);
   if (op->cns()) {
     if (x == rhs) return C(op)->fail(SISDC_ERR_ARG, "implicit_solve: x must not alias rhs");
-    return cns_solve(C(op), op->dev, coef(k), a, rhs, x, op->d_c9, op->d_pinv);
+    Op1DDev d;
+    if (int rc = dev_at(op, t, d)) return rc;
+    const double* dbc = nullptr;
+    if (d.bc == SISDC_DIRICHLET) {   // affine SIP: D(0; t) moves to the right-hand side (dgsem.py:517-529)
+      double* zero = op->d_cws;
+      double* out = op->d_cws + 3 * (size_t)d.n;
+      if (int rc = cns_sip(C(op), d, coef(k), zero, out)) return rc;
+      dbc = out;
+    }
+    return cns_solve(C(op), d, coef(k), a, rhs, x, op->d_c9, op->d_pinv, dbc);
   }
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
@@ -544,7 +591,11 @@ int sisdc_stage_rhs(sisdc_op1d* op, const double* base, const double* conv_in, d
   if (!op || !base || !conv_in || !rhs || M < 0 || M > MAXM || (f_old && !w_row)) return SISDC_ERR_ARG;
   if (op->parted()) return part2_stage(op, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
   if (op->dim == 2) return launch2_stage(C(op), op->dev2, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
-  if (op->cns()) return cns_stage(C(op), op->dev, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
+  if (op->cns()) {
+    Op1DDev d;
+    if (int rc = dev_at(op, t, d)) return rc;
+    return cns_stage(C(op), d, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
+  }
   Op1DDev d;
   if (int rc = dev_at(op, t, d)) return rc;
   return launch_stage_rhs(C(op), d, base, conv_in, dt_m, f_old, M, w_row, dt, g_m, h_old, rhs, conv_out);
@@ -559,7 +610,18 @@ int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_coun
   if (op->parted()) return part2_eval_nodes(op, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
-  if (op->cns()) return cns_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
+  if (op->cns()) {
+    if (op->dev.bc != SISDC_DIRICHLET)
+      return cns_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
+    if (!times) return C(op)->fail(SISDC_ERR_ARG, "Dirichlet node caches need the node times");
+    if (M > MAXM) return C(op)->fail(SISDC_ERR_ARG, "too many collocation nodes");
+    double bnd[12 * MAXM] = {};
+    for (int m = m_first; m < m_first + m_count && m < M; ++m) {
+      if (int rc = bc_at3(op, times[m], bnd + 12 * m, bnd + 12 * m + 3)) return rc;
+      if (int rc = bc_at3(op, m == 0 ? t0 : times[m - 1], bnd + 12 * m + 6, bnd + 12 * m + 9)) return rc;
+    }
+    return cns_node_eval(C(op), op->dev, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2, bnd);
+  }
   if (op->dev.bc == SISDC_DIRICHLET) {   // boundary data at t_m and t_{m-1} per node
     if (!times) return C(op)->fail(SISDC_ERR_ARG, "Dirichlet node caches need the node times");
     if (M > MAXM) return C(op)->fail(SISDC_ERR_ARG, "too many collocation nodes");
@@ -577,7 +639,15 @@ int sisdc_eval_rhs_nodes(sisdc_op1d* op, int M, const double* u, const double* t
   if (!op || !u || !f || M < 1 || M > MAXM) return SISDC_ERR_ARG;
   if (op->parted()) return part2_eval_nodes(op, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
   if (op->dim == 2) return launch2_node_eval(C(op), op->dev2, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
-  if (op->cns()) return cns_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
+  if (op->cns()) {
+    if (op->dev.bc != SISDC_DIRICHLET)
+      return cns_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr);
+    if (!times) return C(op)->fail(SISDC_ERR_ARG, "Dirichlet evaluations need the node times");
+    double bnd[12 * MAXM] = {};
+    for (int m = 0; m < M; ++m)
+      if (int rc = bc_at3(op, times[m], bnd + 12 * m, bnd + 12 * m + 3)) return rc;
+    return cns_node_eval(C(op), op->dev, 0, SISDC_SI2, M, 0, M, u, u, nullptr, nullptr, f, nullptr, nullptr, bnd);
+  }
   if (op->dev.bc == SISDC_DIRICHLET) {
     if (!times) return C(op)->fail(SISDC_ERR_ARG, "Dirichlet evaluations need the node times");
     double bnd[4 * MAXM] = {};

@@ -48,6 +48,7 @@ struct sisdc_op1d {   // dimension-tagged operator handle (1-D or 2-D)
   bool cns() const { return dim == 1 && dev.problem == SISDC_CNS1D; }
   double* d_pinv = nullptr;   // 1-D CNS: element-block Jacobi inverses (n_elem x (3(P+1))^2)
   double* d_c9 = nullptr;     // 1-D CNS: materialised 3x3 coefficient per node (n x 9)
+  double* d_cws = nullptr;    // 1-D CNS: [zero vector | D(0; t)] (2 x 3n), Dirichlet solves
 };
 
 struct sisdc_xfer {

@@ -76,7 +76,11 @@ __device__ __forceinline__ void cns_load_tile(const Op1DDev& op, double* ut, con
   const int p1 = op.p1, T = (EB + 2) * p1;
   for (int t = threadIdx.x; t < 3 * T; t += blockDim.x) {
     const int c = t / T, r = t - c * T, el = r / p1 - 1, i = r - (r / p1) * p1;
-    ut[t] = u[(size_t)c * op.n + wrap(ebase + el, op.ne) * p1 + i];
+    const int eg = ebase + el;
+    if (op.bc == SISDC_DIRICHLET && (eg < 0 || eg >= op.ne))   // ghost element: the outside state g(t)
+      ut[t] = eg < 0 ? op.gl3[c] : op.gr3[c];
+    else
+      ut[t] = u[(size_t)c * op.n + wrap(eg, op.ne) * p1 + i];
   }
 }
 // ct[t*9 + ab] for every tile node
@@ -84,7 +88,10 @@ __device__ __forceinline__ void cns_coef_tile(const Op1DDev& op, const CoefDev& 
   const int p1 = op.p1, T = (EB + 2) * p1;
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     const int el = t / p1 - 1, i = t - (t / p1) * p1;
-    cns_coef_node(op, k, wrap(ebase + el, op.ne), i, ct + t * 9);
+    const int eg = ebase + el;
+    if (op.bc == SISDC_DIRICHLET && eg < 0) cns_coef_node(op, k, 0, 0, ct + t * 9);
+    else if (op.bc == SISDC_DIRICHLET && eg >= op.ne) cns_coef_node(op, k, op.ne - 1, p1 - 1, ct + t * 9);
+    else cns_coef_node(op, k, wrap(eg, op.ne), i, ct + t * 9);
   }
 }
 // ft[c*T + t] = flux(u) at every tile node
@@ -98,14 +105,20 @@ __device__ __forceinline__ void cns_flux_tile(const Op1DDev& op, const double* u
 }
 // q_a = sum_b C_ab (2/dx) (D u_b) at every tile node
 __device__ __forceinline__ void cns_q_tile(const Op1DDev& op, const double* st, const double* ut, const double* ct,
-                                           double* qt, int T) {
+                                           double* qt, int T, int ebase) {
   const int p1 = op.p1;
   const double* D = st + TabOff::D(p1);
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    const int e = t / p1, i = t - e * p1;
+    const int e = t / p1;
+    int i = t - e * p1, es = e;
+    if (op.bc == SISDC_DIRICHLET) {   // ghosts carry the interior boundary node's q (dgsem.py:285-286)
+      const int eg = ebase + e - 1;
+      if (eg < 0) { es = e + 1; i = 0; }
+      else if (eg >= op.ne) { es = e - 1; i = p1 - 1; }
+    }
     double g[3];
     for (int b = 0; b < 3; ++b) {
-      const double* ue = ut + b * T + e * p1;
+      const double* ue = ut + b * T + es * p1;
       double s = 0.0;
       for (int j = 0; j < p1; ++j) s = fma(D[i * p1 + j], ue[j], s);
       g[b] = op.s * s;
@@ -154,7 +167,10 @@ __device__ __forceinline__ void cns_conv_node(const Op1DDev& op, const double* s
 // coefficient; face penalty mu0 {C}[u], average flux, adjoint lift with each
 // side's own coefficient (dgsem.py:270-308)
 __device__ __forceinline__ void cns_B_node(const Op1DDev& op, const double* st, const double* ut, const double* ct,
-                                           const double* qt, int T, int el, int i, double* B) {
+                                           const double* qt, int T, int el, int i, double* B, int eg) {
+  // Dirichlet outer faces take adjoint-lift weight 1 (dgsem.py:196-201)
+  const double wr = (op.bc == SISDC_DIRICHLET && eg == op.ne - 1) ? 1.0 : 0.5;
+  const double wl = (op.bc == SISDC_DIRICHLET && eg == 0) ? 1.0 : 0.5;
   const int p1 = op.p1, P = p1 - 1, b = (el + 1) * p1;
   const double* D = st + TabOff::D(p1);
   const double* DTW = st + TabOff::DTW(p1);
@@ -183,8 +199,8 @@ __device__ __forceinline__ void cns_B_node(const Op1DDev& op, const double* st, 
       for (int c = 0; c < 3; ++c) pen += (0.5 * (Cml[a * 3 + c] + Cpl[a * 3 + c])) * jl[c];
       B[a] -= op.mu0 * pen - 0.5 * (qt[a * T + b - 1] + qt[a * T + b]);
     }
-    const double lm = 0.5 * ((Cmr[a * 3] * jr[0] + Cmr[a * 3 + 1] * jr[1]) + Cmr[a * 3 + 2] * jr[2]);
-    const double lp = 0.5 * ((Cpl[a * 3] * jl[0] + Cpl[a * 3 + 1] * jl[1]) + Cpl[a * 3 + 2] * jl[2]);
+    const double lm = wr * ((Cmr[a * 3] * jr[0] + Cmr[a * 3 + 1] * jr[1]) + Cmr[a * 3 + 2] * jr[2]);
+    const double lp = wl * ((Cpl[a * 3] * jl[0] + Cpl[a * 3 + 1] * jl[1]) + Cpl[a * 3 + 2] * jl[2]);
     B[a] -= (op.s * lm) * D[P * p1 + i];
     B[a] -= (op.s * lp) * D[i];
   }
@@ -221,12 +237,12 @@ __global__ void kc_sip(Op1DDev op, CoefDev k, const double* __restrict__ u, doub
   cns_load_tile(op, ut, u, ebase, EB);
   cns_coef_tile(op, k, ct, ebase, EB);
   __syncthreads();
-  cns_q_tile(op, st, ut, ct, qt, T);
+  cns_q_tile(op, st, ut, ct, qt, T, ebase);
   __syncthreads();
   const int t = threadIdx.x, el = t / p1, i = t - el * p1;
   if (!(el < EB && ebase + el < op.ne)) return;
   double B[3];
-  cns_B_node(op, st, ut, ct, qt, T, el, i, B);
+  cns_B_node(op, st, ut, ct, qt, T, el, i, B, ebase + el);
   const double mi = st[TabOff::minv(p1) + i];
   const size_t gi = (size_t)(ebase + el) * p1 + i;
   for (int c = 0; c < 3; ++c) out[c * op.n + gi] = -B[c] * mi;
@@ -251,10 +267,20 @@ struct CnsCacheArgs {
   double* h1;
   double* h2;               // nullable
   int* status;
+  int has_bnd;              // Dirichlet: outside states per node
+  double bnd[MAXM][12];     // g_l(t_m), g_r(t_m), g_l(t_{m-1}), g_r(t_{m-1}) (3 fields each)
 };
 
-__global__ void kc_eval(Op1DDev op, CnsCacheArgs a) {
+__global__ void kc_eval(Op1DDev op_in, CnsCacheArgs a) {
   extern __shared__ double sm[];
+  Op1DDev op = op_in, opp = op_in;   // boundary data at t_m (u_m) and t_{m-1} (conv of u_{m-1})
+  if (a.has_bnd) {
+    const int mm = a.m_first + blockIdx.y;
+    for (int c = 0; c < 3; ++c) {
+      op.gl3[c] = a.bnd[mm][c]; op.gr3[c] = a.bnd[mm][3 + c];
+      opp.gl3[c] = a.bnd[mm][6 + c]; opp.gr3[c] = a.bnd[mm][9 + c];
+    }
+  }
   const int p1 = op.p1, EB = cns_eb(p1), T = (EB + 2) * p1, ebase = blockIdx.x * EB;
   const size_t N = (size_t)3 * op.n;
   const int m = a.m_first + blockIdx.y;
@@ -271,7 +297,7 @@ __global__ void kc_eval(Op1DDev op, CnsCacheArgs a) {
   cns_coef_tile(op, phys, ct, ebase, EB);
   __syncthreads();
   cns_flux_tile(op, ut, ft, T);
-  cns_q_tile(op, st, ut, ct, qt, T);
+  cns_q_tile(op, st, ut, ct, qt, T, ebase);
   __syncthreads();
   const int t = threadIdx.x, el = t / p1, i = t - el * p1;
   const bool own = el < EB && ebase + el < op.ne;
@@ -281,7 +307,7 @@ __global__ void kc_eval(Op1DDev op, CnsCacheArgs a) {
   if (own) {
     cns_conv_node(op, st, ut, ft, T, el, i, cm);
     double B[3];
-    cns_B_node(op, st, ut, ct, qt, T, el, i, B);   // zero coefficient -> B = 0
+    cns_B_node(op, st, ut, ct, qt, T, el, i, B, ebase + el);   // zero coefficient -> B = 0
     for (int c = 0; c < 3; ++c) {
       f[c] = cm[c] + (-B[c] * mi);
       flag_nonfinite(a.status, f[c], ebase + el);
@@ -302,15 +328,15 @@ __global__ void kc_eval(Op1DDev op, CnsCacheArgs a) {
   // C_m frozen at u_{m-1}: SI for si1/si2, physical for euler (dgsem.py:365-366)
   CoefDev cmod = a.scheme == SISDC_EULER ? CoefDev{SISDC_COEF_PHYS, 0.0, up} : CoefDev{SISDC_COEF_SI, dtm, up};
   cns_coef_tile(op, cmod, ct, ebase, EB);
-  if (a.conv_prev == nullptr) cns_load_tile(op, ft, up, ebase, EB);   // u_{m-1} tile
+  if (a.conv_prev == nullptr) cns_load_tile(opp, ft, up, ebase, EB);   // u_{m-1} tile
   __syncthreads();
-  cns_q_tile(op, st, ut, ct, qt, T);
+  cns_q_tile(op, st, ut, ct, qt, T, ebase);
   __syncthreads();
   double* fpt = qt;   // reused below only after B is formed
   double d[3] = {0.0, 0.0, 0.0}, cp[3] = {0.0, 0.0, 0.0};
   if (own) {
     double B[3];
-    cns_B_node(op, st, ut, ct, qt, T, el, i, B);
+    cns_B_node(op, st, ut, ct, qt, T, el, i, B, ebase + el);
     for (int c = 0; c < 3; ++c) d[c] = -B[c] * mi;
   }
   if (a.conv_prev) {
@@ -318,9 +344,9 @@ __global__ void kc_eval(Op1DDev op, CnsCacheArgs a) {
       for (int c = 0; c < 3; ++c) cp[c] = a.conv_prev[c * op.n + gi];
   } else {
     __syncthreads();
-    cns_flux_tile(op, ft, fpt, T);
+    cns_flux_tile(opp, ft, fpt, T);
     __syncthreads();
-    if (own) cns_conv_node(op, st, ft, fpt, T, el, i, cp);
+    if (own) cns_conv_node(opp, st, ft, fpt, T, el, i, cp);
   }
   if (!own) return;
   for (int c = 0; c < 3; ++c) {
@@ -398,8 +424,12 @@ __global__ void kc_pinv(Op1DDev op, const double* __restrict__ C9, double a, dou
   const double* CLr = C9 + ((size_t)e * p1 + P) * 9;
   const double* CRr = C9 + ((size_t)wrap(e + 1, op.ne) * p1) * 9;
   const double* CLl = C9 + ((size_t)wrap(e - 1, op.ne) * p1 + P) * 9;
-  const double* CRl = C9 + ((size_t)e * p1) * 9;
-  const double s = op.s, hs = 0.5 * op.s;
+  const double* CRl = C9 + ((size_t)e * p1) * 9;   // (re-pointed one-sided at Dirichlet outer faces below)
+  const double s = op.s;
+  const bool dR = op.bc == SISDC_DIRICHLET && e == op.ne - 1, dL = op.bc == SISDC_DIRICHLET && e == 0;
+  const double hsR = dR ? op.s : 0.5 * op.s, hsL = dL ? op.s : 0.5 * op.s;   // outer faces: weight 1, one-sided C
+  if (dR) CRr = CLr;
+  if (dL) CLl = CRl;
   for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
     const int r = idx / nb, col = idx - r * nb;
     const int ca = r / p1, i = r - ca * p1, cb = col / p1, j = col - cb * p1;
@@ -407,11 +437,11 @@ __global__ void kc_pinv(Op1DDev op, const double* __restrict__ C9, double a, dou
     double v = 0.0;
     for (int k = 0; k < p1; ++k) v = fma(D[k * p1 + i] * w[k], C9[((size_t)e * p1 + k) * 9 + ab] * D[k * p1 + j], v);
     v = s * v;
-    if (i == P) v -= hs * CLr[ab] * D[P * p1 + j];
-    if (j == P) v -= hs * CLr[ab] * D[P * p1 + i];
+    if (i == P) v -= hsR * CLr[ab] * D[P * p1 + j];
+    if (j == P) v -= hsR * CLr[ab] * D[P * p1 + i];
     if (i == P && j == P) v += op.mu0 * (0.5 * (CLr[ab] + CRr[ab]));
-    if (i == 0) v += hs * CRl[ab] * D[j];
-    if (j == 0) v += hs * CRl[ab] * D[i];
+    if (i == 0) v += hsL * CRl[ab] * D[j];
+    if (j == 0) v += hsL * CRl[ab] * D[i];
     if (i == 0 && j == 0) v += op.mu0 * (0.5 * (CLl[ab] + CRl[ab]));
     double m = (r == col) ? st[TabOff::m(p1) + i] : 0.0;
     Ag[r * w2 + col] = m + a * v;
@@ -467,6 +497,7 @@ struct BicgArgs {
   Op1DDev op;
   const double* C9;     // materialised coefficient (n, 9)
   const double* pinv;   // element-block inverses (ne, nb, nb)
+  const double* dbc;    // Dirichlet: D(0; t) (affine part of the SIP), nullable
   double a;
   const double* rhs;
   double* x;
@@ -511,13 +542,18 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
   const double* D = st + TabOff::D(P1);
   const double* DTW = st + TabOff::DTW(P1);
   double Cn[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const double a_shift = A.a;
   double xv[3] = {0.0, 0.0, 0.0}, bv[3] = {0.0, 0.0, 0.0};
   const size_t gi = (size_t)e0 * P1 + L;
   __syncthreads();
   const double mi = st[TabOff::m(P1) + i];
   if (own) {
     for (int j = 0; j < 9; ++j) { Cn[j] = A.C9[gi * 9 + j]; Cs[L * 9 + j] = Cn[j]; }
-    for (int c = 0; c < 3; ++c) { xv[c] = A.rhs[c * op.n + gi]; bv[c] = mi * xv[c]; }
+    for (int c = 0; c < 3; ++c) {   // b = M rhs (+ a M D(0; t), dgsem.py:517-529)
+      xv[c] = A.rhs[c * op.n + gi];
+      bv[c] = mi * xv[c];
+      if (A.dbc) bv[c] = bv[c] + (a_shift * mi) * A.dbc[c * op.n + gi];
+    }
   }
   // face coefficients of the element's two faces (global field: no exchange needed)
   const int eg = e0 + el;
@@ -527,6 +563,8 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
     for (int j = 0; j < 9; ++j) { CRr[j] = own ? A.C9[ir * 9 + j] : 0.0; CLl[j] = own ? A.C9[il * 9 + j] : 0.0; }
   }
   const double* pinv_rows = A.pinv + (size_t)(own ? eg : 0) * NB * NB;
+  const bool dL = op.bc == SISDC_DIRICHLET && eg == 0, dR = op.bc == SISDC_DIRICHLET && eg == op.ne - 1;
+  const double wL = dL ? 1.0 : 0.5, wR = dR ? 1.0 : 0.5;   // adjoint-lift face weights (dgsem.py:196-201)
   const double sc = op.s, mu0 = op.mu0, a = A.a;
   __syncthreads();
 
@@ -582,9 +620,9 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
     const int ob = el * P1;
     double jr[3], jl[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      jr[c] = Ub[c * NL + ob + P] - UR[c * NL + oR];
-      jl[c] = UL[c * NL + oL] - Ub[c * NL + ob];
+    for (int c = 0; c < 3; ++c) {   // Dirichlet outer faces: outside value 0 in the linear operator
+      jr[c] = Ub[c * NL + ob + P] - (dR ? 0.0 : UR[c * NL + oR]);
+      jl[c] = (dL ? 0.0 : UL[c * NL + oL]) - Ub[c * NL + ob];
     }
     const double* Cmr = Cs + (ob + P) * 9;
     const double* Cpl = Cs + ob * 9;
@@ -593,18 +631,20 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
       double B = 0.0;
 #pragma unroll
       for (int k = 0; k < P1; ++k) B = fma(DTW[i * P1 + k], Qb[c * NL + ob + k], B);
-      if (i == P) {
+      if (i == P) {   // Dirichlet: one-sided q and C (dgsem.py:285-288)
         double pen = 0.0;
-        for (int b = 0; b < 3; ++b) pen += (0.5 * (Cmr[c * 3 + b] + CRr[c * 3 + b])) * jr[b];
-        B += mu0 * pen - 0.5 * (Qb[c * NL + ob + P] + QR[c * NL + oR]);
+        for (int b = 0; b < 3; ++b) pen += (0.5 * (Cmr[c * 3 + b] + (dR ? Cmr : CRr)[c * 3 + b])) * jr[b];
+        const double qo = Qb[c * NL + ob + P];
+        B += mu0 * pen - 0.5 * (qo + (dR ? qo : QR[c * NL + oR]));
       }
       if (i == 0) {
         double pen = 0.0;
-        for (int b = 0; b < 3; ++b) pen += (0.5 * (CLl[c * 3 + b] + Cpl[c * 3 + b])) * jl[b];
-        B -= mu0 * pen - 0.5 * (QL[c * NL + oL] + Qb[c * NL + ob]);
+        for (int b = 0; b < 3; ++b) pen += (0.5 * ((dL ? Cpl : CLl)[c * 3 + b] + Cpl[c * 3 + b])) * jl[b];
+        const double qo = Qb[c * NL + ob];
+        B -= mu0 * pen - 0.5 * ((dL ? qo : QL[c * NL + oL]) + qo);
       }
-      const double lm = 0.5 * ((Cmr[c * 3] * jr[0] + Cmr[c * 3 + 1] * jr[1]) + Cmr[c * 3 + 2] * jr[2]);
-      const double lp = 0.5 * ((Cpl[c * 3] * jl[0] + Cpl[c * 3 + 1] * jl[1]) + Cpl[c * 3 + 2] * jl[2]);
+      const double lm = wR * ((Cmr[c * 3] * jr[0] + Cmr[c * 3 + 1] * jr[1]) + Cmr[c * 3 + 2] * jr[2]);
+      const double lp = wL * ((Cpl[c * 3] * jl[0] + Cpl[c * 3 + 1] * jl[1]) + Cpl[c * 3 + 2] * jl[2]);
       B -= (sc * lm) * D[P * P1 + i];
       B -= (sc * lp) * D[i];
       w[c] = fma(a, B, mi * v[c]);
@@ -753,9 +793,14 @@ int cns_coef(Ctx* c, const Op1DDev& op, CoefDev k, double* out) {
 }
 int cns_node_eval(Ctx* c, const Op1DDev& op, int mode, int scheme, int M, int m_first, int m_count,
                   const double* u0, const double* u, const double* conv_prev, const double* dts, double* f,
-                  double* h1, double* h2) {
+                  double* h1, double* h2, const double* bnd) {
   if (M > MAXM || m_first + m_count > M) return c->fail(SISDC_ERR_ARG, "bad node range");
   CnsCacheArgs a{};
+  if (bnd) {
+    a.has_bnd = 1;
+    for (int m = 0; m < M; ++m)
+      for (int j = 0; j < 12; ++j) a.bnd[m][j] = bnd[m * 12 + j];
+  }
   a.u0 = u0; a.u = u; a.conv_prev = conv_prev; a.scheme = scheme; a.m_first = m_first; a.mode = mode;
   for (int m = 0; m < M; ++m) a.dts.v[m] = dts ? dts[m] : 0.0;
   a.f = f; a.h1 = h1; a.h2 = h2; a.status = c->d_status;
@@ -774,7 +819,7 @@ int cns_stage(Ctx* c, const Op1DDev& op, const double* base, const double* conv_
   return c->after_launch("cns_stage");
 }
 int cns_solve(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x, double* c9,
-              double* pinv) {
+              double* pinv, const double* dbc) {
   const int p1 = op.p1, nb = 3 * p1;
   // partition: one thread per node, <= 256 nodes per CTA, <= 16 CTAs
   int E = 256 / p1;
@@ -792,7 +837,7 @@ int cns_solve(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs,
   const size_t smem = sizeof(double) * (TabOff::size(p1) + 2 * 3 * NL + 2 * 3 * NL + 3 * NL + 9 * NL +
                                         nw * BNV + 2 * BNV);
   BicgArgs A{};
-  A.op = op; A.C9 = c9; A.pinv = pinv; A.a = a; A.rhs = rhs; A.x = x;
+  A.op = op; A.C9 = c9; A.pinv = pinv; A.dbc = dbc; A.a = a; A.rhs = rhs; A.x = x;
   A.rtol2 = c->rtol * c->rtol; A.maxit = c->maxit; A.E = E; A.K = K;
   A.status = c->d_status; A.log_it = c->d_log_it; A.log_margin = c->d_log_margin; A.log_cap = c->log_cap;
   switch (p1) {

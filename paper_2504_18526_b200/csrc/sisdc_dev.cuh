@@ -39,6 +39,7 @@ struct Op1DDev {
   double gl, gr;          // Dirichlet: outside states at the time of this evaluation
   int nc;                 // components (1; 3 for SISDC_CNS1D, n counts one component)
   double gamma, eta, Pr;  // SISDC_CNS1D gas (problems.py:171-187)
+  double gl3[3], gr3[3];  // SISDC_CNS1D Dirichlet: outside states (all components)
 };
 
 struct CoefDev {

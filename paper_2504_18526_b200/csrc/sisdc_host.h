@@ -86,12 +86,12 @@ int cns_sip(Ctx* c, const Op1DDev& op, CoefDev k, const double* u, double* out);
 int cns_coef(Ctx* c, const Op1DDev& op, CoefDev k, double* out);
 int cns_node_eval(Ctx* c, const Op1DDev& op, int mode, int scheme, int M, int m_first, int m_count,
                   const double* u0, const double* u, const double* conv_prev, const double* dts, double* f,
-                  double* h1, double* h2);
+                  double* h1, double* h2, const double* bnd = nullptr);   // bnd: (M, 12) Dirichlet states
 int cns_stage(Ctx* c, const Op1DDev& op, const double* base, const double* conv_in, double dt_m,
               const double* f_old, int M, const double* w_row, double dt, const double* g, const double* h,
               double* rhs, double* conv_out);
 int cns_solve(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs, double* x, double* c9,
-              double* pinv);
+              double* pinv, const double* dbc = nullptr);
 // 2-D (ops2d.cu)
 int launch2_conv(Ctx* c, const Op2DDev& op, const double* u, double* out);
 int launch2_sip(Ctx* c, const Op2DDev& op, CoefDev k, const double* u, double* out);

@@ -253,8 +253,9 @@ class DGOperator:
             return
         gl, gr = zip(*[self.problem.boundary_state(t) for t in new])
         ta, tp = _lib.darr(new)
-        la, lp = _lib.darr([float(np.asarray(g).reshape(-1)[0]) for g in gl])
-        ra, rp = _lib.darr([float(np.asarray(g).reshape(-1)[0]) for g in gr])
+        nc = self.ncomp   # (n, ncomp) outside states
+        la, lp = _lib.darr([float(v) for g in gl for v in np.asarray(g, dtype=float).reshape(-1)[:nc]])
+        ra, rp = _lib.darr([float(v) for g in gr for v in np.asarray(g, dtype=float).reshape(-1)[:nc]])
         self.rt.check(self.lib.sisdc_op1d_set_boundary(self.h, len(new), tp, lp, rp), "set_boundary")
         self._btimes.update(new)
         if len(self._btimes) > 3000:

@@ -24,4 +24,4 @@ def gpu_available():
 @pytest.fixture(scope="session")
 def golden():
     import numpy as np
-    return {name: np.load(os.path.join(GOLDEN, name + ".npz")) for name in ("tables", "operators", "trajectories", "nonincremental", "dirichlet", "presmooth", "htransfer", "cns", "sources", "study")}
+    return {name: np.load(os.path.join(GOLDEN, name + ".npz")) for name in ("tables", "operators", "trajectories", "nonincremental", "dirichlet", "presmooth", "htransfer", "cns", "sources", "study", "sod")}

@@ -170,12 +170,50 @@ def test_cns_mlsdc_steps(rt, golden, case):
 
 
 def test_cns_unsupported_paths(rt):
-    from paper_2504_18526_b200 import dgsem, problems
+    from paper_2504_18526_b200 import dgsem
     from paper_2504_18526_b200._lib import LibraryError
     w = CASES["cns_resolved"]
-    with pytest.raises(LibraryError, match="periodic"):
-        dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, 8, 4, bc="dirichlet"),
-                         problems.CompressibleFlow(boundary=lambda t: (np.ones(3), np.ones(3))))
     op = gpu_op(w, w.p_fine)
     with pytest.raises(LibraryError, match="scalar"):
         dgsem.smooth_start(op, w.initial_state(op.ref_nodes))
+
+
+SOD = None
+
+
+def sod_op(w, P):
+    from paper_2504_18526_b200 import dgsem, problems
+    prob = problems.CompressibleFlow(gamma=w.gamma, R_gas=w.R_gas, eta=w.eta, Pr=w.prandtl, boundary=w.boundary)
+    av = dgsem.ArtificialViscosityParams(*w.av) if w.av else None
+    return dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, w.n_elem, P, bc="dirichlet"), prob, av=av)
+
+
+@pytest.mark.parametrize("case", ["sod_euler_av", "sod_ns_av"])
+def test_cns_sod_dirichlet(rt, golden, case):
+    """CompressibleFlow with Dirichlet faces: the reference CLI's Sod shock
+    tube (cli.py:766-772) with Persson-Peraire viscosity -- operators with the
+    boundary states, the affine matrix SIP and its implicit solve, and two
+    SI-MLSDC steps with the reference-with-BiCGStab iteration sequence."""
+    from paper_2504_18526_b200 import mlsdc
+    from paper_2504_18526_b200.configs import SOD_CASES
+    G = golden["sod"]
+    w = {c.name: c for c in SOD_CASES}[case]
+    u0, dt = G[case + "_u0"], float(G[case + "_dt"])
+    op = sod_op(w, w.p_fine)
+    assert rel(op.apply_convection(u0, 0.0), G[case + "_conv"]) < 1e-12
+    op.begin_slab(u0, 0.0, dt)
+    assert rel(op.persson_viscosity(u0), G[case + "_nu_art"]) < 1e-12
+    assert rel(op.eval_rhs(u0, 0.0), G[case + "_rhs"]) < 1e-11
+    c = op.modified_diffusion_matrix(u0, 0.5 * dt, "si2")
+    assert rel(op.coefficient_field(c), G[case + "_modc"]) < 1e-13
+    assert rel(op.apply_diffusion(c, u0, 0.0), G[case + "_diff"]) < 1e-11
+    assert field_rel(op.implicit_solve(c, 0.5 * dt, u0, 0.0), G[case + "_solve"]) < 1e-12
+    h = mlsdc.build_p_hierarchy(lambda P: sod_op(w, P), [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+    n0 = rt.status()[2]
+    u = u0
+    for s in range(w.n_steps):
+        u = mlsdc.run_mlsdc(h, u, s * dt, dt, w.n_cycles, strategy="fmg").u[-1].clone()
+        assert field_rel(u, G[f"{case}_bicg_u{s + 1}"]) < 1e-11
+        assert field_rel(u, G[f"{case}_lu_u{s + 1}"]) < 1e-10
+    assert rt.cg_log()[0][n0:].tolist() == G[case + "_bicg_iters"].tolist()
+    rt.raise_on_failure()

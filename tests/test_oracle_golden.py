@@ -256,3 +256,36 @@ def test_source_terms_pinned_to_reference(golden):
         assert [it for it, _ in log[n0:]] == G[f"mlsdc_pcg_iters{s}"].tolist()
         assert np.linalg.norm(u - G[f"mlsdc_pcg_u{s}"]) / np.linalg.norm(u) < 1e-12
         assert np.linalg.norm(u - G[f"mlsdc_lu_u{s}"]) / np.linalg.norm(u) < 1e-11
+
+
+@pytest.mark.parametrize("case", ["sod_euler_av", "sod_ns_av"])
+def test_cns_dirichlet_sod_pinned_to_reference(golden, case):
+    """CompressibleFlow with Dirichlet faces (the oracle's matrix-coefficient
+    Dirichlet SIP, dgsem.py:282-308) on the reference CLI's Sod tube with AV:
+    operators and two SI-MLSDC steps with the identical BiCGStab sequence."""
+    from paper_2504_18526_b200.configs import SOD_CASES
+    G = golden["sod"]
+    w = {c.name: c for c in SOD_CASES}[case]
+
+    class Sod(dg1d.CNS1D):
+        def __init__(self):
+            super().__init__(gamma=w.gamma, R_gas=w.R_gas, eta=w.eta, Pr=w.prandtl)
+            self.boundary = w.boundary
+    log = []
+
+    def mk(P):
+        return dg1d.Op1D(0.0, 1.0, w.n_elem, P, Sod(), bc="dirichlet", av=w.av, cg_log=log)
+    u0, dt = G[case + "_u0"], float(G[case + "_dt"])
+    op = mk(w.p_fine)
+    assert rel(op.apply_convection(u0, 0.0), G[case + "_conv"]) < 1e-13
+    op.begin_slab(u0, 0.0, dt)
+    assert rel(op.persson_viscosity(u0), G[case + "_nu_art"]) < 1e-13
+    assert rel(op.eval_rhs(u0, 0.0), G[case + "_rhs"]) < 1e-12
+    h = sweeper.build_two_level(lambda lvl: mk(w.p_coarse if lvl == "coarse" else w.p_fine),
+                                sweeper.Rule("radau_right", w.m_coarse), sweeper.Rule("radau_right", w.m_fine))
+    log.clear()
+    u = u0
+    for s in range(w.n_steps):
+        u = sweeper.run_mlsdc(h, u, s * dt, dt, w.n_cycles).u[-1].copy()
+        assert np.linalg.norm(u - G[f"{case}_bicg_u{s + 1}"]) / np.linalg.norm(u) < 1e-12
+    assert [it for it, _ in log] == G[case + "_bicg_iters"].tolist()
