@@ -159,6 +159,8 @@ int sisdc_ctx_create(int device, sisdc_ctx** out) {
     delete x;
     return SISDC_ERR_CUDA;
   }
+  const char* pdl = getenv("SISDC_PDL");   // A/B switch for programmatic dependent launch
+  if (pdl && pdl[0] == '0') c.pdl = 0;
   const char* tm = getenv("SISDC_CG_TIMING");
   if (e == cudaSuccess && tm && tm[0] == '1') {
     e = cudaMalloc(&c.d_timing, 80 * sizeof(long long));

@@ -191,9 +191,12 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
+  pdl_launch_dependents();
   const bool stamp = A.timing != nullptr && rank == 0 && threadIdx.x == 0;
   if (stamp) A.timing[0] = clock64();
-  for (int t = threadIdx.x; t < TabOff::size(P1); t += blockDim.x) s.st[t] = op.tab[t];
+  for (int t = threadIdx.x; t < TabOff::size(P1); t += blockDim.x) s.st[t] = op.tab[t];   // constant tables
+  if constexpr (CL) cg::this_cluster().sync();   // mbarriers initialised cluster-wide (overlaps the predecessor)
+  pdl_wait();   // everything below may read the predecessor's output
   double ci = 0.0, x = 0.0;
   if (A.stage) {   // x0 = the stage rhs of this substep, conv(conv_in) as conv_node (ops1d.cu)
     const CgStage& g = A.sg;
@@ -240,8 +243,7 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   }
   if (L == 0) s.Cs[NL] = coef_at(op, A.coef, egL, P);
   if (L == 1) s.Cs[NL + 1] = coef_at(op, A.coef, egR, 0);
-  if constexpr (CL) cg::this_cluster().sync();   // mbarriers initialised cluster-wide
-  else __syncthreads();
+  __syncthreads();
 
   const double* D = s.st + TabOff::D(P1);
   const double* DTW = s.st + TabOff::DTW(P1);
@@ -537,7 +539,18 @@ static int launch_cg_t(Ctx* c, CgArgs& A, int threads, size_t smem) {
       cudaFuncSetAttribute(k_cg1d<false, P1, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr_done[0] = true;
     }
-    k_cg1d<false, P1, DIR><<<1, threads, smem, c->stream>>>(A);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = c->pdl;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_cg1d<false, P1, DIR>, A);
+    if (e != cudaSuccess) return c->cuda(e, "cg1d launch");
     return c->after_launch("cg1d");
   }
   if (!attr_done[1]) {
@@ -550,13 +563,15 @@ static int launch_cg_t(Ctx* c, CgArgs& A, int threads, size_t smem) {
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = A.K;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // overlap launch + prologue with the predecessor
+  at[1].val.programmaticStreamSerializationAllowed = c->pdl;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_cg1d<true, P1, DIR>, A);
   if (e != cudaSuccess) return c->cuda(e, "cg1d cluster launch");
   return c->after_launch("cg1d");

@@ -87,7 +87,9 @@ __global__ void k_node_eval(Op1DDev op_in, CacheArgs a) {
   const int t = threadIdx.x, el = t / p1, i = t - el * p1;
   const bool own = el < EB && ebase + el < op.ne;
   const int gi = (ebase + el) * p1 + i;
-  load_tab(st, op.tab, p1);
+  pdl_launch_dependents();
+  load_tab(st, op.tab, p1);   // constant tables
+  pdl_wait();                 // u, caches: the predecessor's output
   load_tile<DIR>(op, ut, um, ebase, EB);
   CoefDev phys{SISDC_COEF_PHYS, 0.0, nullptr};
   coef_tile<DIR>(op, phys, ct, ebase, EB);
@@ -434,7 +436,19 @@ int launch_node_eval(Ctx* c, const Op1DDev& op, int mode, int scheme, int M, int
     a.grp.v[j] = bnd ? bnd[3 * M + j] : op.gr;
   }
   a.f = f; a.h1 = h1; a.h2 = h2; a.status = c->d_status;
-  (op.bc == SISDC_DIRICHLET ? k_node_eval<true> : k_node_eval<false>)<<<tile_grid(op.ne, op.p1, m_count), tile_block(op.p1), tile_smem(op.p1, 4), c->stream>>>(op, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = tile_grid(op.ne, op.p1, m_count);
+  cfg.blockDim = tile_block(op.p1);
+  cfg.dynamicSmemBytes = tile_smem(op.p1, 4);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = c->pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = op.bc == SISDC_DIRICHLET ? cudaLaunchKernelEx(&cfg, k_node_eval<true>, op, a)
+                                           : cudaLaunchKernelEx(&cfg, k_node_eval<false>, op, a);
+  if (e != cudaSuccess) return c->cuda(e, "node_eval launch");
   return c->after_launch("node_eval");
 }
 int launch_stage_rhs(Ctx* c, const Op1DDev& op, const double* base, const double* conv_in, double dt_m,

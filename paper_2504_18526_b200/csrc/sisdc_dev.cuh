@@ -217,4 +217,13 @@ __host__ __device__ inline int xo_size(const XferDev& x) { return 2 * x.Mf * x.M
 
 __global__ void k_reset_status(int* status, int reset_log);
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; it lets its own successor launch at once
+// (launch_dependents) and waits for the predecessor's completion and memory
+// flush (wait) before touching anything the predecessor wrote.  Both are
+// no-ops without a programmatic dependency.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace sisdc

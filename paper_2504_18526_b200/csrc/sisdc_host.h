@@ -24,6 +24,7 @@ struct Ctx {
   double rtol = 1e-14;
   int maxit = 1000;
   int cluster_ctas = 0;
+  int pdl = 1;                    // programmatic dependent launch of the 1-D kernels (SISDC_PDL=0 disables)
   int64_t launches = 0;
   std::string err;
 
