@@ -217,3 +217,48 @@ def test_cns_sod_dirichlet(rt, golden, case):
         assert field_rel(u, G[f"{case}_lu_u{s + 1}"]) < 1e-10
     assert rt.cg_log()[0][n0:].tolist() == G[case + "_bicg_iters"].tolist()
     rt.raise_on_failure()
+
+
+@pytest.mark.parametrize("bc", ["periodic", "dirichlet"])
+def test_cns_multi_cta_cluster_solve(rt, bc):
+    """The BiCGStab cluster path with K > 1 CTAs (face halo through DSMEM,
+    rank-ordered cluster reductions): 100 elements at P = 7 span 4 CTAs.
+    Same iteration count as the oracle and <= 1e-12 per field; periodic and
+    Dirichlet (Sod states) faces."""
+    from paper_2504_18526_b200 import dgsem, problems
+    from paper_2504_18526_b200.configs import SOD_CASES
+    w = CASES["cns_mlsdc"]
+    ne, P = 100, 7
+    if bc == "periodic":
+        prob_g = problems.CompressibleFlow(eta=2e-4)
+        prob_o = dg1d.CNS1D(eta=2e-4)
+        op = dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, ne, P), prob_g)
+        u = AcousticState(w, ne, P, op.ref_nodes)
+    else:
+        sod = SOD_CASES[0]
+
+        class Sod(dg1d.CNS1D):
+            def __init__(self):
+                super().__init__(eta=2e-4)
+                self.boundary = sod.boundary
+        prob_g = problems.CompressibleFlow(eta=2e-4, boundary=sod.boundary)
+        prob_o = Sod()
+        op = dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, ne, P, bc="dirichlet"), prob_g)
+        u = host(op.nodal_field(lambda x: 0.5 * (sod.initial(x - 0.01) + sod.initial(x + 0.01)))).copy()
+    log = []
+    orc = dg1d.Op1D(0.0, 1.0, ne, P, prob_o, bc=bc, cg_log=log)
+    lam = dgsem.max_wave_speed(op, u)
+    a = 0.4 * dgsem.dt_from_cfl(2.0, 1.0 / ne, lam, P)
+    c = op.modified_diffusion_matrix(u, a, "si2")
+    rhs = u * (1.0 + 1e-3 * np.sin(np.arange(u.size)))
+    n0 = rt.status()[2]
+    x = op.implicit_solve(c, a, rhs, 0.0)
+    xo = orc.implicit_solve(orc.modified_coeff(u, a), a, rhs, 0.0)
+    assert rt.cg_log()[0][n0:].tolist() == [log[-1][0]]
+    assert field_rel(x, xo) < 1e-12
+    rt.raise_on_failure()
+
+
+def AcousticState(w, ne, P, nodes):
+    import dataclasses
+    return dataclasses.replace(w, n_elem=ne, p_fine=P).initial_state(nodes)
