@@ -543,6 +543,16 @@ STUDY_CONFIG = {
 }
 
 
+CONV_CONFIG = {
+    "study": "convergence",
+    "problem": {"kind": "convection_diffusion", "speed": 1.0, "nu": 0.002},
+    "levels": [{"degree": 3, "n_nodes": 2}, {"degree": 6, "n_nodes": 4}],
+    "time": {"t_end": 0.02},
+    "method": {"iterations": 3},
+    "convergence": {"element_counts": [[8, 8], [16, 16], [32, 32]], "cfl_values": [0.5, 1.0]},
+}
+
+
 def gen_study():
     """The reference CLI's own cfl-sweep study (cli.py:1110-1194) on its
     wave-packet convection-diffusion problem, run in-process: its
@@ -557,6 +567,13 @@ def gen_study():
         err = open(os.path.join(d, "errors.csv")).read()
         its = open(os.path.join(d, "iterations.csv")).read()
     out = {"config": np.array(json.dumps(STUDY_CONFIG)), "errors_csv": np.array(err), "iterations_csv": np.array(its)}
+    cfg = rcli.parse_config(json.dumps(CONV_CONFIG))
+    with tempfile.TemporaryDirectory() as d:
+        rcli.run_study(cfg, d)
+        out["conv_config"] = np.array(json.dumps(CONV_CONFIG))
+        out["conv_errors_csv"] = np.array(open(os.path.join(d, "errors.csv")).read())
+        out["conv_orders_csv"] = np.array(open(os.path.join(d, "orders.csv")).read())
+    print(str(out["conv_errors_csv"]), str(out["conv_orders_csv"]))
     print(its)
     np.savez_compressed(os.path.join(OUT, "study.npz"), **out)
 

@@ -1,6 +1,7 @@
 """Ensemble dispatch of independent study points across GPUs.
 
-The reference's CFL-sweep study (``cli.py:1110-1194``) computes, for every
+The reference's CFL-sweep study (``cli.py:1110-1194``; the convergence study
+``cli.py:1194-1256`` is dispatched the same way, ``convergence``) computes, for every
 CFL value, the error-vs-iterations series of a march to t_end and the
 iteration at which it stalls (``analysis.converged_iteration``,
 ``analysis.py:300-314``); its points are independent, and the reference runs
@@ -26,8 +27,8 @@ import numpy as np
 
 from ._lib import SolverError
 
-__all__ = ["converged_iteration", "write_csv", "SweepPoint", "MLSDCStudy", "SDCStudy", "sweep_one_cfl",
-           "cfl_sweep"]
+__all__ = ["converged_iteration", "observed_order", "write_csv", "SweepPoint", "MLSDCStudy", "SDCStudy",
+           "sweep_one_cfl", "cfl_sweep", "convergence"]
 
 
 def converged_iteration(error_series, threshold: float = 0.1) -> Optional[int]:
@@ -207,3 +208,58 @@ def cfl_sweep(study_or_factory, cfl_values: Sequence[float], max_iterations: int
                                         ("cfl", "n_steps", "converged_iteration", "error", "status"), it_rows),
         }
     return points
+
+
+def observed_order(e_coarse: float, e_fine: float, ratio: float = 2.0) -> float:
+    """log(e_c / e_f) / log(ratio) (``analysis.py:291-297``)."""
+    if e_coarse <= 0.0 or e_fine <= 0.0:
+        raise ValueError("observed order needs strictly positive errors")
+    if ratio <= 1.0:
+        raise ValueError("refinement ratio must exceed 1")
+    return float(np.log(e_coarse / e_fine) / np.log(ratio))
+
+
+def convergence(run_job: Callable, element_counts: Sequence[Sequence[int]], cfl_values: Sequence[float],
+                out_dir=None):
+    """The reference's convergence study (``cli.py:1194-1256``): one job per
+    (cfl, element-count family), each a full march at fixed iterations whose
+    terminal error against the exact solution is returned by
+    ``run_job(n_elems, cfl) -> (n_steps, error)`` on the rank that owns it
+    (job j on rank j % world); rank 0 writes errors.csv / orders.csv in the
+    reference's format.  Returns the ordered [(cfl, family, n_elem_fine,
+    n_steps, error)] rows on every rank."""
+    dist, rank, world = _group()
+    jobs = [(fi, tuple(ne), float(c)) for c in cfl_values for fi, ne in enumerate(element_counts)]
+    res = {}
+    for j, (fi, ne, c) in enumerate(jobs):
+        if j % world == rank:
+            n_steps, err = run_job(ne, c)
+            res[j] = (c, fi, ne[-1], int(n_steps), float(err))
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, res)
+        for part in gathered:
+            res.update(part)
+    err_rows = [res[j] for j in range(len(jobs))]
+    convergence.outputs = {}
+    if out_dir is not None and rank == 0:
+        table = {(r[0], r[1]): (r[2], r[4]) for r in err_rows}
+        order_rows = []
+        for c in cfl_values:
+            c = float(c)
+            for fi in range(1, len(element_counts)):
+                ne_c, e_c = table[(c, fi - 1)]
+                ne_f, e_f = table[(c, fi)]
+                if e_c <= 0 or e_f <= 0:
+                    order_rows.append((c, fi - 1, fi, ""))
+                    continue
+                order_rows.append((c, fi - 1, fi, observed_order(e_c, e_f, ratio=ne_f / ne_c)))
+        out = Path(out_dir)
+        out.mkdir(parents=True, exist_ok=True)
+        convergence.outputs = {
+            "errors.csv": write_csv(out / "errors.csv", ("cfl", "family", "n_elem_fine", "n_steps", "error"),
+                                    err_rows),
+            "orders.csv": write_csv(out / "orders.csv", ("cfl", "family_coarse", "family_fine", "order"),
+                                    order_rows),
+        }
+    return err_rows

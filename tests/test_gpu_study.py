@@ -47,3 +47,40 @@ def test_cfl_sweep_matches_reference_cli(golden):
             if len(a) > 4:
                 assert a[4] == b[4]                   # status
             assert abs(float(a[3]) - float(b[3])) <= 1e-9 * abs(float(b[3]))
+
+
+def test_convergence_study_matches_reference_cli(golden):
+    """The reference CLI's convergence study (cli.py:1194-1256): one GPU
+    SI-MLSDC march per (cfl, element-count family) at fixed iterations;
+    n_steps and the error table to 1e-9, observed orders to 1e-7."""
+    import math
+    from paper_2504_18526_b200 import dgsem, mlsdc, problems, study
+    G = golden["study"]
+    cfg = json.loads(str(G["conv_config"]))
+    pr, lv = cfg["problem"], cfg["levels"]
+    prob = problems.ConvectionDiffusion(pr["speed"], pr["nu"])
+    exact = problems.wave_packet_exact(pr["nu"], pr["speed"])
+    t_end = cfg["time"]["t_end"]
+
+    def run_job(n_elems, cfl):
+        h = mlsdc.build_p_hierarchy(lambda P: dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, n_elems[-1], P), prob),
+                                    [lv[0]["degree"], lv[1]["degree"]], [lv[0]["n_nodes"], lv[1]["n_nodes"]])
+        op = h.fine.ctx
+        u0 = op.nodal_field(lambda x: exact(x, 0.0)[None])
+        lam = dgsem.max_wave_speed(op, u0)
+        dt0 = dgsem.dt_from_cfl(cfl, op.mesh.dx, lam, op.mesh.degree)
+        n = max(1, math.ceil(t_end / dt0 - 1e-12))
+        u = mlsdc.integrate_mlsdc(h, u0, 0.0, t_end / n, n, cfg["method"]["iterations"], strategy="fmg")
+        ref = op.nodal_field(lambda x: exact(x, t_end)[None])
+        return n, op.norm_l2(u - ref) / op.norm_l2(ref)
+    with tempfile.TemporaryDirectory() as d:
+        study.convergence(run_job, cfg["convergence"]["element_counts"], cfg["convergence"]["cfl_values"], out_dir=d)
+        mine_e = open(os.path.join(d, "errors.csv")).read()
+        mine_o = open(os.path.join(d, "orders.csv")).read()
+    for mine, ref, tol in ((mine_e, str(G["conv_errors_csv"]), 1e-9), (mine_o, str(G["conv_orders_csv"]), 1e-7)):
+        h1, rows = parse(mine)
+        h2, rrows = parse(ref)
+        assert h1 == h2 and len(rows) == len(rrows)
+        for a, b in zip(rows, rrows):
+            assert a[:-1] == b[:-1]
+            assert abs(float(a[-1]) - float(b[-1])) <= tol * abs(float(b[-1]))

@@ -89,3 +89,23 @@ def test_round_robin_dispatch_over_gloo():
         it = open(os.path.join(d, "iterations.csv")).read().strip().split("\n")
         assert it[0] == "cfl,n_steps,converged_iteration,error,status" and len(it) == 6
         assert it[-1] == "8,1,,nan,failed"
+
+
+def test_observed_order_and_convergence_csv(golden):
+    """observed_order restates analysis.py:291-297; the orders.csv the
+    dispatch writes from the reference's own error table equals the
+    reference CLI's orders.csv byte for byte."""
+    G = golden["study"]
+    import json
+    cfg = json.loads(str(G["conv_config"]))
+    rows = [ln.split(",") for ln in str(G["conv_errors_csv"]).strip().split("\n")[1:]]
+    table = {(float(r[0]), tuple(cfg["convergence"]["element_counts"][int(r[1])])): (int(r[3]), float(r[4]))
+             for r in rows}
+    with tempfile.TemporaryDirectory() as d:
+        study.convergence(lambda ne, c: table[(c, tuple(ne))], cfg["convergence"]["element_counts"],
+                          cfg["convergence"]["cfl_values"], out_dir=d)
+        assert open(os.path.join(d, "orders.csv")).read() == str(G["conv_orders_csv"])
+        assert open(os.path.join(d, "errors.csv")).read() == str(G["conv_errors_csv"])
+    assert study.observed_order(0.4, 0.1, 2.0) == 2.0
+    with pytest.raises(ValueError):
+        study.observed_order(0.0, 0.1)
