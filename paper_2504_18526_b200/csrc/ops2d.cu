@@ -893,9 +893,11 @@ __device__ __forceinline__ void wph_phase(const Op2DDev& op, const double* src, 
 
 // phase A over in-field nodes [2h, 2h+2) of all fields: every load first, then
 // the updates and stores; accumulates the partials (r,u), (r,r)
+// first: the first iteration reads p = s = 0 and x = x0 = rhs instead of
+// initialised vectors (same operations as with zero-filled p, s and x = rhs)
 template <int NC>
 __device__ __forceinline__ void cg_update2(const Cg2Args& A, double* Un, long long h, long long nh, double alpha,
-                                           double beta, double& ru, double& rr) {
+                                           double beta, double& ru, double& rr, bool first) {
   const double2 di = reinterpret_cast<const double2*>(A.DINV)[h];
   double2 r[NC], pv[NC], sv[NC], wv[NC], xv[NC];
 #pragma unroll
@@ -903,7 +905,7 @@ __device__ __forceinline__ void cg_update2(const Cg2Args& A, double* Un, long lo
     const long long t = c * nh + h;
     r[c] = reinterpret_cast<const double2*>(A.R)[t];
     pv[c] = reinterpret_cast<const double2*>(A.Pv)[t];
-    sv[c] = reinterpret_cast<const double2*>(A.S)[t];
+    sv[c] = first ? make_double2(0.0, 0.0) : reinterpret_cast<const double2*>(A.S)[t];
     wv[c] = reinterpret_cast<const double2*>(A.W)[t];
     xv[c] = reinterpret_cast<const double2*>(A.x)[t];
   }
@@ -939,14 +941,14 @@ __device__ __forceinline__ void cg_update2(const Cg2Args& A, double* Un, long lo
 // issue-bound phase B, which has HBM bandwidth to spare; u is double-buffered.
 template <int NC>
 __device__ __forceinline__ void cg_update2s(const Cg2Args& A, double* Un, long long h, long long nh, double alpha,
-                                            double beta, double& ru, double& rr) {
+                                            double beta, double& ru, double& rr, bool first) {
   const double2 di = reinterpret_cast<const double2*>(A.DINV)[h];
   double2 r[NC], sv[NC], wv[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const long long t = c * nh + h;
     r[c] = reinterpret_cast<const double2*>(A.R)[t];
-    sv[c] = reinterpret_cast<const double2*>(A.S)[t];
+    sv[c] = first ? make_double2(0.0, 0.0) : reinterpret_cast<const double2*>(A.S)[t];
     wv[c] = reinterpret_cast<const double2*>(A.W)[t];
   }
 #pragma unroll
@@ -970,12 +972,12 @@ __device__ __forceinline__ void cg_update2s(const Cg2Args& A, double* Un, long l
 // scalar form (odd sizes / misaligned x)
 template <int NC>
 __device__ __forceinline__ void cg_update1s(const Cg2Args& A, double* Un, long long f, long long nn, double alpha,
-                                            double beta, double& ru, double& rr) {
+                                            double beta, double& ru, double& rr, bool first) {
   const double di = A.DINV[f];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const long long t = c * nn + f;
-    const double s = fma(beta, A.S[t], A.W[t]);
+    const double s = fma(beta, first ? 0.0 : A.S[t], A.W[t]);
     A.S[t] = s;
     const double r = fma(-alpha, s, A.R[t]);
     A.R[t] = r;
@@ -988,14 +990,14 @@ __device__ __forceinline__ void cg_update1s(const Cg2Args& A, double* Un, long l
 // full scalar update (p, x in phase A: the P != 7 levels, see k2_cg)
 template <int NC>
 __device__ __forceinline__ void cg_update1(const Cg2Args& A, double* Un, long long f, long long nn, double alpha,
-                                           double beta, double& ru, double& rr) {
+                                           double beta, double& ru, double& rr, bool first) {
   const double di = A.DINV[f];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const long long t = c * nn + f;
     double r = A.R[t];
     const double p = fma(beta, A.Pv[t], r * di);
-    const double s = fma(beta, A.S[t], A.W[t]);
+    const double s = fma(beta, first ? 0.0 : A.S[t], A.W[t]);
     A.Pv[t] = p;
     A.S[t] = s;
     A.x[t] = fma(alpha, p, A.x[t]);
@@ -1641,75 +1643,99 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   };
   double* slot0 = A.part;
   double* slot1 = A.part + 4 * G;
+  if (A.timing != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == G - 1))
+    A.timing[blockIdx.x == 0 ? 30 : 40] = gtimer();   // kernel start (setup stamps 30.. / 40..)
 
-  // ---- setup 1: C, dinv per in-field node (closed-form diag of M + a B2), x0 = rhs, p = s = 0
-  const int ntiles_el = (op.nex * op.ney + EB - 1) / EB;
-  for (int tile = blockIdx.x; tile < ntiles_el; tile += G) {
-    const Node2 n = node2<P1>(op, tile);
-    double* CS = sm + Sm2<P1>::CS + n.el * NN;
-    double* FCo = sm + Sm2<P1>::FC + n.el * 4 * P1;
-    const int exr = wrapi(n.ex + 1, op.nex), exl = wrapi(n.ex - 1, op.nex);
-    const int eyt = ynb(op, n.ey, 1), eyb = ynb(op, n.ey, -1);
-    __syncthreads();
-    if (n.valid) {
-      CS[n.nd] = coef2d(op, A.coef, n.ey, n.ex, n.j, n.i);
-      if (n.i == P) FCo[FR * P1 + n.j] = coef2d(op, A.coef, n.ey, exr, n.j, 0);
-      if (n.i == 0) FCo[FL * P1 + n.j] = coef2d(op, A.coef, n.ey, exl, n.j, P);
-      if (n.j == P) FCo[FT * P1 + n.i] = coef2d(op, A.coef, eyt, n.ex, 0, n.i);
-      if (n.j == 0) FCo[FB * P1 + n.i] = coef2d(op, A.coef, eyb, n.ex, P, n.i);
-    }
-    __syncthreads();
-    if (n.valid) {
-      const int i = n.i, j = n.j;
-      double dx_ = 0.0, dy_ = 0.0;
+  // ---- setup 1: C per in-field node (pointwise, every node in flight at once),
+  // then dinv = 1 / diag(M + a B2) in closed form from C (own element row and
+  // column, the four neighbours' face nodes); same values and operations as a
+  // per-element tile evaluation
+  const int ne_own = op.nex * op.ney;
+  const long long nown = (long long)ne_own * NN;
+  for (long long f0 = gtid; f0 < nown; f0 += 4 * nthr) {   // 4 nodes per thread in flight
+    double cv[4];
+    long long fs[4];
 #pragma unroll
-      for (int q = 0; q < P1; ++q) {
-        dx_ = fma(c_tab2[T::D2W + i * P1 + q], CS[j * P1 + q], dx_);
-        dy_ = fma(c_tab2[T::D2W + j * P1 + q], CS[q * P1 + i], dy_);
-      }
-      const double DPP = c_tab2[T::D + P * P1 + P], D00 = c_tab2[T::D];
-      dx_ *= op.sx;
-      dy_ *= op.sy;
-      if (i == P) dx_ += op.mux * (0.5 * (CS[j * P1 + P] + FCo[FR * P1 + j])) - op.sx * CS[j * P1 + P] * DPP;
-      if (i == 0) dx_ += op.mux * (0.5 * (FCo[FL * P1 + j] + CS[j * P1])) + op.sx * CS[j * P1] * D00;
-      if (j == P) dy_ += op.muy * (0.5 * (CS[P * P1 + i] + FCo[FT * P1 + i])) - op.sy * CS[P * P1 + i] * DPP;
-      if (j == 0) dy_ += op.muy * (0.5 * (FCo[FB * P1 + i] + CS[i])) + op.sy * CS[i] * D00;
-      const double hwx = 0.5 * op.dx * c_tab2[T::W + i], hwy = 0.5 * op.dy * c_tab2[T::W + j];
-      const long long f = (long long)n.es * NN + n.nd;
-      A.Cf[f] = CS[n.nd];
-      A.DINV[f] = 1.0 / (hwx * hwy + A.a * (hwy * dx_ + hwx * dy_));
+    for (int q = 0; q < 4; ++q) {
+      const long long f = f0 + q * nthr;
+      const long long fc = f < nown ? f : f0;
+      const int e = (int)(fc / NN), nd = (int)(fc - (long long)e * NN);
+      const int oy = e / op.nex, ex = e - oy * op.nex;
+      fs[q] = f < nown ? (long long)((oy + op.row0) * op.nex + ex) * NN + nd : -1;
+      cv[q] = coef2d(op, A.coef, oy + op.row0, ex, nd / P1, nd - (nd / P1) * P1);
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (fs[q] >= 0) A.Cf[fs[q]] = cv[q];
   }
-  for (long long t = gtid; t < op.n; t += nthr) {
-    A.x[t] = A.rhs[t];
-    A.Pv[t] = 0.0;
-    A.S[t] = 0.0;
+  grid.sync();
+  for (long long f = gtid; f < nown; f += nthr) {
+    const int e = (int)(f / NN), nd = (int)(f - (long long)e * NN);
+    const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
+    const int j = nd / P1, i = nd - j * P1;
+    const int exr = wrapi(ex + 1, op.nex), exl = wrapi(ex - 1, op.nex);
+    const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
+    const double* CS = A.Cf + (long long)(ey * op.nex + ex) * NN;
+    double dx_ = 0.0, dy_ = 0.0;
+#pragma unroll
+    for (int q = 0; q < P1; ++q) {
+      dx_ = fma(c_tab2[T::D2W + i * P1 + q], CS[j * P1 + q], dx_);
+      dy_ = fma(c_tab2[T::D2W + j * P1 + q], CS[q * P1 + i], dy_);
+    }
+    const double DPP = c_tab2[T::D + P * P1 + P], D00 = c_tab2[T::D];
+    dx_ *= op.sx;
+    dy_ *= op.sy;
+    if (i == P) dx_ += op.mux * (0.5 * (CS[j * P1 + P] + A.Cf[(long long)(ey * op.nex + exr) * NN + j * P1])) -
+                       op.sx * CS[j * P1 + P] * DPP;
+    if (i == 0) dx_ += op.mux * (0.5 * (A.Cf[(long long)(ey * op.nex + exl) * NN + j * P1 + P] + CS[j * P1])) +
+                       op.sx * CS[j * P1] * D00;
+    if (j == P) dy_ += op.muy * (0.5 * (CS[P * P1 + i] + A.Cf[(long long)(eyt * op.nex + ex) * NN + i])) -
+                       op.sy * CS[P * P1 + i] * DPP;
+    if (j == 0) dy_ += op.muy * (0.5 * (A.Cf[(long long)(eyb * op.nex + ex) * NN + P * P1 + i] + CS[i])) +
+                       op.sy * CS[i] * D00;
+    const double hwx = 0.5 * op.dx * c_tab2[T::W + i], hwy = 0.5 * op.dy * c_tab2[T::W + j];
+    A.DINV[(long long)(ey * op.nex + ex) * NN + nd] = 1.0 / (hwx * hwy + A.a * (hwy * dx_ + hwx * dy_));
   }
+  const bool stamps = A.timing != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == G - 1);
+  long long* ts = A.timing + (blockIdx.x == 0 ? 30 : 40);
+  if (stamps) ts[1] = gtimer();   // setup 1 tiles done
+  // (no initialisation pass: setup 2 writes x0 = rhs and p = 0, the first
+  // iteration's phase A' reads s = 0)
   if (blockIdx.x == 0 && threadIdx.x == 0) {   // phase-A chunk counters
     reinterpret_cast<unsigned*>(A.scal)[0] = 0u;
     reinterpret_cast<unsigned*>(A.scal)[1] = 0u;
   }
   grid.sync();
-  // ---- setup 2: r0 = b - A x0 (b = M rhs); partials (b,b), #nonzero -> slot 0
+  if (stamps) ts[2] = gtimer();
+  // ---- setup 2: r0 = b - A x0 (x0 = rhs, b = M rhs), u0 = r0 dinv in the same
+  // epilogue; partials (b,b), #nonzero -> slot 0; (r0,u0), (r0,r0) kept for setup 3
+  double ru0 = 0.0, rr0 = 0.0;
   {
     double bb = 0.0, nz = 0.0;
-    auto epi = [&](long long g, double ax, double) {
+    auto epi = [&](long long g, double ax, double v) {   // v = x0 at g = rhs[g]
       const int nd = (int)(g % NN);
       const double mi = (0.5 * op.dx * c_tab2[T::W + nd % P1]) * (0.5 * op.dy * c_tab2[T::W + nd / P1]);
-      const double b = mi * A.rhs[g];
-      A.R[g] = b - ax;
+      const double b = mi * v;
+      const double r = b - ax;
+      A.R[g] = r;
+      const double u = r * A.DINV[g % nn];
+      A.U[g] = u;
+      A.x[g] = v;      // x0 = rhs
+      A.Pv[g] = 0.0;   // p_{-1} = 0
+      ru0 = fma(r, u, ru0);
+      rr0 = fma(r, r, rr0);
       bb = fma(b, b, bb);
       nz += b != 0.0 ? 1.0 : 0.0;
     };
     if constexpr (P1 == 8) {
-      wpe_phase<NC>(op, sm, A.x, A.Cf, A.a, [&](long long g, double w0, double w1, double v0, double v1) {
+      wpe_phase<NC>(op, sm, A.rhs, A.Cf, A.a, [&](long long g, double w0, double w1, double v0, double v1) {
         epi(g, w0, v0);
         epi(g + 1, w1, v1);
       });
     } else if constexpr (P1 == 4) {
-      wph_phase<NC>(op, A.x, A.Cf, A.a, epi);
+      wph_phase<NC>(op, A.rhs, A.Cf, A.a, epi);
     } else {
-      for (int tile = blockIdx.x; tile < ntiles; tile += G) cg_tile<P1, NC>(op, sm, tile, tpr, A.x, nullptr, A.Cf, A.a, epi);
+      for (int tile = blockIdx.x; tile < ntiles; tile += G) cg_tile<P1, NC>(op, sm, tile, tpr, A.rhs, nullptr, A.Cf, A.a, epi);
     }
     block_part(bb, nz, 0.0, slot0);
   }
@@ -1752,25 +1778,14 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     }
     return wu;
   };
-  // ---- setup 3: u0 = r0 dinv; w0 = A u0; gamma, delta, rho -> slot 1
+  // ---- setup 3: w0 = A u0 (u0 from setup 2); gamma, delta, rho -> slot 1
   {
-    double ru = 0.0, rr = 0.0;
-    for (long long f = gtid; f < nn; f += nthr) {
-      const double di = A.DINV[f];
-#pragma unroll
-      for (int c = 0; c < NC_MAX; ++c)
-        if (c < nc) {
-          const double r = A.R[c * nn + f], u = r * di;
-          A.U[c * nn + f] = u;
-          ru = fma(r, u, ru);
-          rr = fma(r, r, rr);
-        }
-    }
-    grid.sync();
+    if (stamps) ts[3] = gtimer();
     const double wu = phase_B(A.U, nullptr, 0.0, 0.0);
-    block_part(ru, wu, rr, slot1);
+    block_part(ru0, wu, rr0, slot1);
   }
   grid.sync();
+  if (stamps) ts[4] = gtimer();
   grid_total(slot1, tot);
   double rho = tot[2];
   double alpha = tot[0] / tot[1], beta = 0.0;
@@ -1790,13 +1805,13 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     if (vec) {   // grid-stride over in-field pairs (no per-chunk block barrier)
       const long long nh = nn >> 1;
       for (long long h = gtid; h < nh; h += nthr) {
-        if constexpr (DEFER) cg_update2s<NC>(A, Un, h, nh, alpha, beta, ru, rr);
-        else cg_update2<NC>(A, Un, h, nh, alpha, beta, ru, rr);
+        if constexpr (DEFER) cg_update2s<NC>(A, Un, h, nh, alpha, beta, ru, rr, k == 0);
+        else cg_update2<NC>(A, Un, h, nh, alpha, beta, ru, rr, k == 0);
       }
     } else {
       for (long long f = gtid; f < nn; f += nthr) {
-        if constexpr (DEFER) cg_update1s<NC>(A, Un, f, nn, alpha, beta, ru, rr);
-        else cg_update1<NC>(A, Un, f, nn, alpha, beta, ru, rr);
+        if constexpr (DEFER) cg_update1s<NC>(A, Un, f, nn, alpha, beta, ru, rr, k == 0);
+        else cg_update1<NC>(A, Un, f, nn, alpha, beta, ru, rr, k == 0);
       }
     }
     if (stamp) tm[1] = gtimer();
@@ -1999,13 +2014,13 @@ __global__ void __launch_bounds__(256) k2p_update(Cg2Args A) {
   if (vec) {
     const long long nh = nn >> 1;
     for (long long h = (o0 >> 1) + g0; h < (o1 >> 1); h += nt) {
-      if (A.defer) cg_update2s<NC>(A, A.U, h, nh, alpha, beta, ru, rr);
-      else cg_update2<NC>(A, A.U, h, nh, alpha, beta, ru, rr);
+      if (A.defer) cg_update2s<NC>(A, A.U, h, nh, alpha, beta, ru, rr, false);
+      else cg_update2<NC>(A, A.U, h, nh, alpha, beta, ru, rr, false);
     }
   } else {
     for (long long f = o0 + g0; f < o1; f += nt) {
-      if (A.defer) cg_update1s<NC>(A, A.U, f, nn, alpha, beta, ru, rr);
-      else cg_update1<NC>(A, A.U, f, nn, alpha, beta, ru, rr);
+      if (A.defer) cg_update1s<NC>(A, A.U, f, nn, alpha, beta, ru, rr, false);
+      else cg_update1<NC>(A, A.U, f, nn, alpha, beta, ru, rr, false);
     }
   }
   blk_part3(ru, rr, 0.0, red, A.part);

@@ -52,6 +52,10 @@ if os.environ.get("SISDC_CG_TIMING") == "1":
         d = np.diff(t[o:o + 7]) / 1e3
         print(f"  {b} iteration 2 (us): phaseA {d[0]:.1f} sync {d[1]:.1f} phaseB {d[2]:.1f} part {d[3]:.1f} "
               f"sync {d[4]:.1f} total {d[5]:.1f}")
+    for b, o in (("block 0", 30), ("block G-1", 40)):
+        d = np.diff(np.array(buf[o:o + 5], dtype=np.float64)) / 1e3
+        print(f"  {b} setup (us): coef/dinv tiles {d[0]:.1f}, x/p/s init + sync {d[1]:.1f}, "
+              f"r0 = b - A x0 + u0 + sync {d[2]:.1f}, w0 = A u0 + reduction {d[3]:.1f}")
     t2 = np.array(buf[20:23], dtype=np.float64)
     if t2[2] > 0:
         print(f"  block0/warp0 phase B per element: wait {t2[0]/t2[2]:.0f} cycles, compute {t2[1]/t2[2]:.0f} cycles "
