@@ -1707,8 +1707,8 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   }
   grid.sync();
   if (stamps) ts[2] = gtimer();
-  // ---- setup 2: r0 = b - A x0 (x0 = rhs, b = M rhs), u0 = r0 dinv in the same
-  // epilogue; partials (b,b), #nonzero -> slot 0; (r0,u0), (r0,r0) kept for setup 3
+  // ---- setup 2: r0 = b - A x0 (x0 = rhs, b = M rhs), u0 = r0 dinv, x = x0 and
+  // p = 0 in the same epilogue; partials (b,b), #nonzero -> slot 0
   double ru0 = 0.0, rr0 = 0.0;
   {
     double bb = 0.0, nz = 0.0;
@@ -1722,8 +1722,6 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
       A.U[g] = u;
       A.x[g] = v;      // x0 = rhs
       A.Pv[g] = 0.0;   // p_{-1} = 0
-      ru0 = fma(r, u, ru0);
-      rr0 = fma(r, r, rr0);
       bb = fma(b, b, bb);
       nz += b != 0.0 ? 1.0 : 0.0;
     };
@@ -1778,8 +1776,20 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     }
     return wu;
   };
-  // ---- setup 3: w0 = A u0 (u0 from setup 2); gamma, delta, rho -> slot 1
+  // ---- setup 3: w0 = A u0 (u0 from setup 2); gamma, delta, rho -> slot 1.  The
+  // partials (r0,u0), (r0,r0) keep their node-major summation order (a read-only
+  // pass: u0 = r0 dinv is recomputed bitwise, not stored again)
   {
+    for (long long f = gtid; f < nn; f += nthr) {
+      const double di = A.DINV[f];
+#pragma unroll
+      for (int c = 0; c < NC_MAX; ++c)
+        if (c < nc) {
+          const double r = A.R[c * nn + f], u = r * di;
+          ru0 = fma(r, u, ru0);
+          rr0 = fma(r, r, rr0);
+        }
+    }
     if (stamps) ts[3] = gtimer();
     const double wu = phase_B(A.U, nullptr, 0.0, 0.0);
     block_part(ru0, wu, rr0, slot1);

@@ -193,3 +193,21 @@ def test_full_size_properties_cfg4(rt):
     free[3] = 2.5 + 0.5 * (0.3 ** 2 + 0.2 ** 2)
     conv = op.apply_convection(free.reshape(-1))
     assert float(conv.abs().max()) < 1e-11
+
+
+@pytest.mark.parametrize("nex,ney,P", [(5, 4, 2), (6, 5, 4), (4, 3, 5), (3, 5, 6), (7, 3, 1)])
+def test_implicit_solve_2d_other_degrees(rt, nex, ney, P):
+    """The strip-tile CG path of the degrees other than 3 and 7 (and the
+    scalar, odd-size phase-A update of P = 2 / 4 / 6 meshes): identical
+    iterations and solution vs the restatement; also the converged-at-x0 case
+    (rhs already solves the system) returns x = rhs."""
+    w = small(CFG4, nex, ney)
+    op, orc, u = pair(w, P)
+    for a in (2e-3, 5e-2):
+        c = op.modified_diffusion_matrix(u, a, "si2")
+        n0 = rt.status()[2]
+        x = op.implicit_solve(c, a, u)
+        xo = orc.implicit_solve(orc.modified_coeff(u, a), a, u)
+        assert rt.cg_log()[0][n0:].tolist() == [orc.cg_log[-1][0]]
+        assert rel(x, xo) < 1e-13
+    rt.raise_on_failure()
