@@ -442,6 +442,8 @@ __global__ void k2x_down(Xfer2Dev x, int sdir, int tdir, const double* __restric
   double* sr = su + Mf * nfs;      // [Mf][nfs]  residual (with_res)
   double* spu = sr + Mf * nfs;     // [Mf][ncs]  spatially transferred u
   double* spr = spu + Mf * ncs;    // [Mf][ncs]
+  double* tu = spr + Mf * ncs;     // [Mf][pf][pc] first (x) pass of the transfer
+  double* tr = tu + Mf * pf * pc;
   for (int t = threadIdx.x; t < Mf * nfs; t += blockDim.x) {
     const int m = t / nfs, nd = t - m * nfs;
     const long long gi = (long long)s * nfs + nd;
@@ -458,10 +460,29 @@ __global__ void k2x_down(Xfer2Dev x, int sdir, int tdir, const double* __restric
     }
   }
   __syncthreads();
+  // sum-factorised sp2 (two passes, the same operations in the same order):
+  // T[jb][ia] = sum_ib S[ia][ib] in[jb][ib], out[ja][ia] = sum_jb S[ja][jb] T[jb][ia]
+  const int sdu = with_res ? 1 : sdir;
+  for (int t = threadIdx.x; t < Mf * pf * pc; t += blockDim.x) {
+    const int m = t / (pf * pc), r = t - m * pf * pc, jb = r / pc, ia = r - jb * pc;
+    double a1 = 0.0, a2 = 0.0;
+    for (int ib = 0; ib < pf; ++ib) {
+      a1 = fma(xf_spatial_coef(x, sdu, ia, ib), su[m * nfs + jb * pf + ib], a1);
+      if (with_res) a2 = fma(xf_spatial_coef(x, 2, ia, ib), sr[m * nfs + jb * pf + ib], a2);
+    }
+    tu[t] = a1;
+    if (with_res) tr[t] = a2;
+  }
+  __syncthreads();
   for (int t = threadIdx.x; t < Mf * ncs; t += blockDim.x) {
     const int m = t / ncs, nd = t - m * ncs, ja = nd / pc, ia = nd % pc;
-    spu[t] = sp2(x, with_res ? 1 : sdir, su + m * nfs, pf, ja, ia);
-    if (with_res) spr[t] = sp2(x, 2, sr + m * nfs, pf, ja, ia);
+    double a1 = 0.0, a2 = 0.0;
+    for (int jb = 0; jb < pf; ++jb) {
+      a1 = fma(xf_spatial_coef(x, sdu, ja, jb), tu[(m * pf + jb) * pc + ia], a1);
+      if (with_res) a2 = fma(xf_spatial_coef(x, 2, ja, jb), tr[(m * pf + jb) * pc + ia], a2);
+    }
+    spu[t] = a1;
+    if (with_res) spr[t] = a2;
   }
   __syncthreads();
   const double* It = x.tab;
@@ -488,6 +509,7 @@ __global__ void k2x_interp(Xfer2Dev x, int accumulate, const double* __restrict_
   const int nfs = pf * pf, ncs = pc * pc;
   double* sd = sm;              // [Mc][ncs]
   double* stt = sd + Mc * ncs;  // [Mf][ncs]
+  double* tt = stt + Mf * ncs;  // [Mf][pc][pf] first (x) pass of the interpolation
   for (int t = threadIdx.x; t < Mc * ncs; t += blockDim.x) {
     const int m = t / ncs, nd = t - m * ncs;
     const long long gi = m * Nc + (long long)s * ncs + nd;
@@ -502,9 +524,18 @@ __global__ void k2x_interp(Xfer2Dev x, int accumulate, const double* __restrict_
     stt[t] = acc;
   }
   __syncthreads();
+  // sum-factorised sp2 (same operations, same order as the direct form)
+  for (int t = threadIdx.x; t < Mf * pc * pf; t += blockDim.x) {
+    const int m = t / (pc * pf), r = t - m * pc * pf, jb = r / pf, ia = r - jb * pf;
+    double row = 0.0;
+    for (int ib = 0; ib < pc; ++ib) row = fma(xf_spatial_coef(x, 0, ia, ib), stt[m * ncs + jb * pc + ib], row);
+    tt[t] = row;
+  }
+  __syncthreads();
   for (int t = threadIdx.x; t < Mf * nfs; t += blockDim.x) {
     const int m = t / nfs, nd = t - m * nfs, ja = nd / pf, ia = nd % pf;
-    const double v = sp2(x, 0, stt + m * ncs, pc, ja, ia);
+    double v = 0.0;
+    for (int jb = 0; jb < pc; ++jb) v = fma(xf_spatial_coef(x, 0, ja, jb), tt[(m * pc + jb) * pf + ia], v);
     const long long gi = m * Nf + (long long)s * nfs + nd;
     uf[gi] = accumulate ? uf[gi] + v : v;
   }
@@ -2338,7 +2369,7 @@ int launch2x_spatial(Ctx* c, const Xfer2Dev& x, int dir, const double* in, doubl
   return c->after_launch("k2x_spatial");
 }
 int launch2x_down(Ctx* c, const Xfer2Dev& x, int sdir, int tdir, const double* in, double* out) {
-  const size_t sm = sizeof(double) * (2 * x.Mf * x.pf * x.pf + 2 * x.Mf * x.pc * x.pc);
+  const size_t sm = sizeof(double) * (2 * x.Mf * x.pf * x.pf + 2 * x.Mf * x.pc * x.pc + 2 * x.Mf * x.pf * x.pc);
   Fas2Args fa{};
   k2x_down<<<x.nslab, 128, sm, c->stream>>>(x, sdir, tdir, in, out, (long long)x.nslab * x.pf * x.pf,
                                             (long long)x.nslab * x.pc * x.pc, 0, fa, nullptr);
@@ -2349,13 +2380,13 @@ int launch2x_fas(Ctx* c, const Xfer2Dev& x, const double* Wf, double dt, int inc
   Fas2Args fa{};
   for (int i = 0; i < x.Mf * x.Mf; ++i) fa.Wf[i] = Wf[i];
   fa.dt = dt; fa.incremental = incremental; fa.u0f = u0f; fa.uf = uf; fa.ff = ff; fa.gf = gf;
-  const size_t sm = sizeof(double) * (2 * x.Mf * x.pf * x.pf + 2 * x.Mf * x.pc * x.pc);
+  const size_t sm = sizeof(double) * (2 * x.Mf * x.pf * x.pf + 2 * x.Mf * x.pc * x.pc + 2 * x.Mf * x.pf * x.pc);
   k2x_down<<<x.nslab, 128, sm, c->stream>>>(x, 1, 1, nullptr, v, (long long)x.nslab * x.pf * x.pf,
                                             (long long)x.nslab * x.pc * x.pc, 1, fa, rr);
   return c->after_launch("k2x_fas");
 }
 int launch2x_interp(Ctx* c, const Xfer2Dev& x, int accumulate, const double* uc, const double* vc, double* uf) {
-  const size_t sm = sizeof(double) * (x.Mc * x.pc * x.pc + x.Mf * x.pc * x.pc);
+  const size_t sm = sizeof(double) * (x.Mc * x.pc * x.pc + x.Mf * x.pc * x.pc + x.Mf * x.pc * x.pf);
   k2x_interp<<<x.nslab, 128, sm, c->stream>>>(x, accumulate, uc, vc, uf, (long long)x.nslab * x.pf * x.pf,
                                               (long long)x.nslab * x.pc * x.pc);
   return c->after_launch("k2x_interp");
