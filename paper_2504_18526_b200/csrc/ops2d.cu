@@ -297,7 +297,7 @@ struct Cache2Args {
   int* status;
 };
 template <int P1>
-__global__ void __launch_bounds__(256) k2_node_eval(Op2DDev op, Cache2Args a) {
+__global__ void __launch_bounds__(256, 3) k2_node_eval(Op2DDev op, Cache2Args a) {
   extern __shared__ double sm[];
   load_tab2<P1>(sm + Sm2<P1>::ST, op.tab);
   __syncthreads();
@@ -366,7 +366,7 @@ struct Stage2Args {
   double* conv_out;
 };
 template <int P1>
-__global__ void __launch_bounds__(256) k2_stage(Op2DDev op, Stage2Args a) {
+__global__ void __launch_bounds__(256, 3) k2_stage(Op2DDev op, Stage2Args a) {
   extern __shared__ double sm[];
   load_tab2<P1>(sm + Sm2<P1>::ST, op.tab);
   __syncthreads();
