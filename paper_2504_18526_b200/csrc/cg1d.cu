@@ -166,7 +166,6 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   const Op1DDev& op = A.op;
   int rank = 0;
   if constexpr (CL) rank = (int)cg::this_cluster().block_rank();
-  const int nw = (blockDim.x + 31) >> 5;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int P1P = padded(P1);
   const CgShared<P1> s = carve<P1>(sm, A.E, blockDim.x);
@@ -333,8 +332,8 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
           for (int m = 0; m + w2 < MAXW; m += 2 * w2) e[m] += e[m + w2];
         t[j] = warp_sum(e[0]);
       }
-      double* slots = s.slots + par * 16 * NVS;
       if constexpr (CL) {
+        const double* slots = s.slots + par * 16 * NVS;
         if (lane < K)
 #pragma unroll
           for (int j = 0; j < NV; j += 2) st_async2(rslot[par] + 8 * j, t[j], t[j + 1], rmb[par]);
