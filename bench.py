@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
-    ap.add_argument("--cpu-sample-steps", type=int, default=20)
+    ap.add_argument("--cpu-sample-steps", type=int, default=100)   # ~10 s of host work
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cluster-ctas", type=int, default=0)
     ap.add_argument("--cycles", type=int, default=None, help="override the V-cycles per step")
