@@ -120,7 +120,7 @@ class ClockSampler:
 
 def measured_traffic(kind="1d"):
     """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    name = "r01_cg_traffic.json" if kind == "1d" else "r01d_cg2_traffic.json"
+    name = "r01g_cg_traffic.json" if kind == "1d" else "r01d_cg2_traffic.json"
     try:
         with open(os.path.join(HERE, "profiles", name)) as f:
             return float(json.load(f)["dram_bytes_per_launch"])
