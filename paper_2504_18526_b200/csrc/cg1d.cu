@@ -309,7 +309,9 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   // (structure of arrays), warp 0 reduces them in a fixed order, pushes the
   // CTA total to every CTA (NV slots, NR <= NV real values), waits for the K
   // totals, reduces them in rank order and broadcasts through shared memory.
-  auto csum = [&](auto& v, auto nr_tag, auto nv_tag, int par, uint32_t& phase) {
+  // idle(): warp 0 work placed in the shadow of the cluster wait (before the
+  // final broadcast barrier)
+  auto csum = [&](auto& v, auto nr_tag, auto nv_tag, int par, uint32_t& phase, auto&& idle) {
     constexpr int NR = decltype(nr_tag)::value;
     constexpr int NV = decltype(nv_tag)::value;
     constexpr int MAXW = 12;   // <= 384 threads
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
 #pragma unroll
           for (int j = 0; j < NV; j += 2) st_async2(rslot[par] + 8 * j, t[j], t[j + 1], rmb[par]);
         if (lane == 0) mbar_expect(mb[par], 8u * K * NV + halo_rws_bytes);
+        idle();
         mbar_wait(mb[par], phase);
 #pragma unroll
         for (int j = 0; j < NR; ++j) {   // K <= 16 slots: 4 butterfly levels
@@ -346,6 +349,8 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
           for (int o = 8; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
           t[j] = q;
         }
+      } else {
+        idle();
       }
       if (lane == 0)
 #pragma unroll
@@ -452,7 +457,7 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   double v6[NVS] = {own ? r * u : 0.0, own ? w * u : 0.0, own ? r * r : 0.0, own ? bi * bi : 0.0,
                     (own && b0 != 0.0) ? 1.0 : 0.0, 0.0};   // b == 0 test on M rhs (dgsem.py:509-511)
   if (stamp) A.timing[2] = clock64();
-  csum(v6, std::integral_constant<int, 5>{}, std::integral_constant<int, NVS>{}, 0, ph[0]);
+  csum(v6, std::integral_constant<int, 5>{}, std::integral_constant<int, NVS>{}, 0, ph[0], [] {});
   if (stamp) A.timing[3] = clock64();
   double gamma = v6[0], rho = v6[2];
   const double thr = A.rtol2 * v6[3];
@@ -461,7 +466,7 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     return;
   }
   double alpha = gamma / v6[1], beta = 0.0;
-  double rgamma = 1.0 / gamma, ralpha = 1.0 / alpha;   // reciprocals off the critical path
+  double rgamma, ralpha;   // formed by warp 0 inside each loop reduction
   int k = 0;
   bool ok = true;
   while (rho > thr) {
@@ -490,7 +495,18 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     if (sub) A.timing[72] = clock64();
     push_rws(par ^ 1);
     double v4[NVL] = {own ? r * u : 0.0, own ? w * u : 0.0, own ? r * r : 0.0, 0.0};
-    csum(v4, std::integral_constant<int, 3>{}, std::integral_constant<int, NVL>{}, par ^ 1, ph[par ^ 1]);
+    // 1 / alpha and 1 / gamma (needed by the scalar recurrence below) are
+    // formed once, by warp 0 while it waits for the cluster's partials, and
+    // broadcast with the sums: the other warps skip the two reciprocal
+    // sequences (same operations on the same values: bitwise)
+    csum(v4, std::integral_constant<int, 3>{}, std::integral_constant<int, NVL>{}, par ^ 1, ph[par ^ 1], [&] {
+      if (lane == 0) {
+        s.bcast[3] = 1.0 / alpha;
+        s.bcast[4] = 1.0 / gamma;
+      }
+    });
+    ralpha = s.bcast[3];
+    rgamma = s.bcast[4];
     if (sub) A.timing[73] = clock64();
     ++k;
     if (stamp && k < 60) A.timing[4 + k] = clock64();
@@ -499,9 +515,7 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     const double gn = v4[0];
     beta = __dmul_rn(gn, rgamma);   // one division on the critical path
     alpha = gn / __dsub_rn(v4[1], __dmul_rn(beta, __dmul_rn(gn, ralpha)));
-    ralpha = 1.0 / alpha;
     gamma = gn;
-    rgamma = 1.0 / gamma;
     if (sub) A.timing[74] = clock64();
   }
   if (own) A.x[(size_t)e0 * P1 + L] = x;
