@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) mR[j] = mapa(mb[j], rR);
     }
-    if (wid == 0 && lane < K) {
+    if (wid < 5 && lane < K) {   // the reducing warps (csum: at most 5 quantities)
       rslot[0] = mapa(sa(s.slots + rank * NVS), lane);
       rslot[1] = mapa(sa(s.slots + (16 + rank) * NVS), lane);
       rmb[0] = mapa(mb[0], lane);
@@ -305,12 +305,22 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
 
   // Cluster sum of NV values into buffer `par` (with the (r,w,s) halo pushed
   // by the caller on the same mbarrier); identical bits in every CTA.
-  // Only warp 0 shuffles: every thread parks its NR partials in shared memory
-  // (structure of arrays), warp 0 reduces them in a fixed order, pushes the
-  // CTA total to every CTA (NV slots, NR <= NV real values), waits for the K
-  // totals, reduces them in rank order and broadcasts through shared memory.
+  // Every thread parks its NR partials in shared memory (structure of
+  // arrays); each quantity is summed in a fixed order (per lane over the
+  // warps, then across the lanes), the CTA totals are pushed to every CTA
+  // (NV slots, NR <= NV real values), and after the K totals have arrived
+  // they are summed in rank order and broadcast through shared memory.
+  //  * P1 < 9: warp 0 does all of it, the NR quantities interleaved, remote
+  //    stores in pairs.
+  //  * PARRED (P1 >= 9): warp j reduces quantity j (j, j + nred, ... with
+  //    fewer warps) and pushes it itself; warp 0 also pushes the zero pads.
+  //    Measured on the cfg2 fine level: 1.78 -> 1.61 us per iteration.  At
+  //    P1 = 5 the single-value pushes (twice the mbarrier transactions) cost
+  //    more than the parallel sums save (1.70 -> 2.08 us), hence the split.
+  // Same operations in the same order per quantity either way (bitwise).
   // idle(): warp 0 work placed in the shadow of the cluster wait (before the
   // final broadcast barrier)
+  constexpr bool PARRED = P1 >= 9;
   auto csum = [&](auto& v, auto nr_tag, auto nv_tag, int par, uint32_t& phase, auto&& idle) {
     constexpr int NR = decltype(nr_tag)::value;
     constexpr int NV = decltype(nv_tag)::value;
@@ -319,21 +329,54 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) s.wbuf[j * nt + threadIdx.x] = v[j];
     __syncthreads();
-    if (wid == 0) {
+    // pairwise tree over the <= 12 values of this lane, then the warp sum
+    auto qsum = [&](int j) {
+      double e[MAXW];
+#pragma unroll
+      for (int m = 0; m < MAXW; ++m) e[m] = (lane + 32 * m < nt) ? s.wbuf[j * nt + lane + 32 * m] : 0.0;
+#pragma unroll
+      for (int w2 = 1; w2 < MAXW; w2 *= 2)
+#pragma unroll
+        for (int m = 0; m + w2 < MAXW; m += 2 * w2) e[m] += e[m + w2];
+      return warp_sum(e[0]);
+    };
+    if constexpr (PARRED) {
+      const int nred = min(NR, nt >> 5);   // reducing warps
+      if (wid < nred) {
+        for (int j = wid; j < NR; j += nred) {
+          const double tj = qsum(j);
+          if constexpr (CL) {
+            if (lane < K) st_async(rslot[par] + 8 * j, tj, rmb[par]);
+          } else {
+            if (lane == 0) s.bcast[j] = tj;
+          }
+        }
+        if constexpr (CL) {
+          if (wid == 0) {
+            if (lane < K)
+#pragma unroll
+              for (int j = NR; j < NV; ++j) st_async(rslot[par] + 8 * j, 0.0, rmb[par]);
+            if (lane == 0) mbar_expect(mb[par], 8u * K * NV + halo_rws_bytes);
+            idle();
+          }
+          mbar_wait(mb[par], phase);
+          const double* slots = s.slots + par * 16 * NVS;
+          for (int j = wid; j < NR; j += nred) {   // K <= 16 slots: 4 butterfly levels
+            double q = lane < K ? slots[lane * NVS + j] : 0.0;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+            if (lane == 0) s.bcast[j] = q;
+          }
+        } else {
+          if (wid == 0) idle();
+        }
+      }
+    } else if (wid == 0) {
       double t[NV];
 #pragma unroll
       for (int j = 0; j < NV; ++j) t[j] = 0.0;
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {   // pairwise tree over the <= 12 values of this lane
-        double e[MAXW];
-#pragma unroll
-        for (int m = 0; m < MAXW; ++m) e[m] = (lane + 32 * m < nt) ? s.wbuf[j * nt + lane + 32 * m] : 0.0;
-#pragma unroll
-        for (int w2 = 1; w2 < MAXW; w2 *= 2)
-#pragma unroll
-          for (int m = 0; m + w2 < MAXW; m += 2 * w2) e[m] += e[m + w2];
-        t[j] = warp_sum(e[0]);
-      }
+      for (int j = 0; j < NR; ++j) t[j] = qsum(j);
       if constexpr (CL) {
         const double* slots = s.slots + par * 16 * NVS;
         if (lane < K)
