@@ -321,6 +321,10 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   // idle(): warp 0 work placed in the shadow of the cluster wait (before the
   // final broadcast barrier)
   constexpr bool PARRED = P1 >= 9;
+#ifndef SISDC_CG1_GATHER
+#define SISDC_CG1_GATHER 1
+#endif
+  constexpr bool GATHER = SISDC_CG1_GATHER;
   auto csum = [&](auto& v, auto nr_tag, auto nv_tag, int par, uint32_t& phase, auto&& idle) {
     constexpr int NR = decltype(nr_tag)::value;
     constexpr int NV = decltype(nv_tag)::value;
@@ -369,6 +373,36 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
           }
         } else {
           if (wid == 0) idle();
+        }
+      }
+    } else if (GATHER && CL && min(NR, nt >> 5) > 1) {
+      // P1 < 9 variant: parallel sums, totals gathered to warp 0 through shared
+      // memory and a named barrier of the reducing warps, paired pushes by warp
+      // 0 (the transaction count of a single reducing warp), parallel receives
+      const int nred = min(NR, nt >> 5);
+      if (wid < nred) {
+        for (int j = wid; j < NR; j += nred) {
+          const double tj = qsum(j);
+          if (lane == 0) s.wbuf[j * nt] = tj;   // region j is read by this warp only
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(nred * 32) : "memory");
+        if (wid == 0) {
+          double t[NV];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) t[j] = j < NR ? s.wbuf[j * nt] : 0.0;
+          if (lane < K)
+#pragma unroll
+            for (int j = 0; j < NV; j += 2) st_async2(rslot[par] + 8 * j, t[j], t[j + 1], rmb[par]);
+          if (lane == 0) mbar_expect(mb[par], 8u * K * NV + halo_rws_bytes);
+          idle();
+        }
+        mbar_wait(mb[par], phase);
+        const double* slots = s.slots + par * 16 * NVS;
+        for (int j = wid; j < NR; j += nred) {   // K <= 16 slots: 4 butterfly levels
+          double q = lane < K ? slots[lane * NVS + j] : 0.0;
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+          if (lane == 0) s.bcast[j] = q;
         }
       }
     } else if (wid == 0) {
