@@ -16,9 +16,10 @@
 //    store completes a transaction count on the RECEIVER's mbarrier.  After
 //    its own mbarrier phase completes a CTA sums the K slots in rank order
 //    -> bitwise-identical scalars everywhere, no cluster barrier.
-//  * the face halo: boundary nodes push (r, w, s) with the partials; the
-//    receiver forms s' = fma(beta, s, w), r' = fma(-alpha, s', r), u' = r' dinv
-//    with exactly the owner's operations, so u's halo needs no extra exchange.
+//  * the face halo: boundary nodes push w with the partials (r0, w0 once with
+//    the setup reduction); the receiver advances the neighbours' s and r
+//    itself, s' = fma(beta, s, w), r' = fma(-alpha, s', r), u' = r' dinv, with
+//    exactly the owner's operations, so u's halo needs no extra exchange.
 // One mbarrier wait per iteration; slot/halo buffers alternate by parity.
 #include <cooperative_groups.h>
 #include <type_traits>
@@ -301,7 +302,10 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
       rmb[1] = mapa(mb[1], lane);
     }
   }
-  const uint32_t halo_rws_bytes = 2u * P1 * 32u;
+  // halo bytes riding on a reduction's mbarrier: (r0, w0) pairs with the setup
+  // reduction, then w alone per iteration (the receiver advances the
+  // neighbours' r and s itself, see the loop)
+  uint32_t halo_rws_bytes = 2u * P1 * 16u;
 
   // Cluster sum of NV values into buffer `par` (with the (r,w,s) halo pushed
   // by the caller on the same mbarrier); identical bits in every CTA.
@@ -515,23 +519,31 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   if (stamp) A.timing[1] = clock64();
   double w = matvec(s.Ub, s.HU0);
   double p = 0.0, sv = 0.0;   // p_{-1} = s_{-1} = 0
-  // push (r0, w0, s_{-1} = 0) with the setup reduction (parity 0)
-  auto push_rws = [&](int par) {
+  // push (r0, w0) with the setup reduction (parity 0; s_{-1} = 0 is implied),
+  // then w alone with every loop reduction: one mbarrier transaction per
+  // boundary node instead of two
+  auto push_rws = [&](int par, bool setup) {
     if constexpr (CL) {
-      if (pushL) { st_async2(tL[2 + par], r, w, mL[par]); st_async2(tL[2 + par] + 16, sv, 0.0, mL[par]); }
-      if (pushR) { st_async2(tR[2 + par], r, w, mR[par]); st_async2(tR[2 + par] + 16, sv, 0.0, mR[par]); }
+      if (setup) {
+        if (pushL) st_async2(tL[2 + par], r, w, mL[par]);
+        if (pushR) st_async2(tR[2 + par], r, w, mR[par]);
+      } else {
+        if (pushL) st_async(tL[2 + par] + 8, w, mL[par]);
+        if (pushR) st_async(tR[2 + par] + 8, w, mR[par]);
+      }
     } else {
       double* h = s.HRWS + par * 8 * P1;
       if (own && last) { h[4 * i] = r; h[4 * i + 1] = w; h[4 * i + 2] = sv; }
       if (own && first) { h[4 * (P1 + i)] = r; h[4 * (P1 + i) + 1] = w; h[4 * (P1 + i) + 2] = sv; }
     }
   };
-  push_rws(0);
+  push_rws(0, true);
   uint32_t ph[2] = {0, 0};
   double v6[NVS] = {own ? r * u : 0.0, own ? w * u : 0.0, own ? r * r : 0.0, own ? bi * bi : 0.0,
                     (own && b0 != 0.0) ? 1.0 : 0.0, 0.0};   // b == 0 test on M rhs (dgsem.py:509-511)
   if (stamp) A.timing[2] = clock64();
   csum(v6, std::integral_constant<int, 5>{}, std::integral_constant<int, NVS>{}, 0, ph[0], [] {});
+  halo_rws_bytes = 2u * P1 * 8u;
   if (stamp) A.timing[3] = clock64();
   double gamma = v6[0], rho = v6[2];
   const double thr = A.rtol2 * v6[3];
@@ -541,18 +553,23 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   }
   double alpha = gamma / v6[1], beta = 0.0;
   double rgamma, ralpha;   // formed by warp 0 inside each loop reduction
+  double hr = 0.0, hs = 0.0;   // helper lanes: the neighbours' r and s at halo node `lane`
   int k = 0;
   bool ok = true;
   while (rho > thr) {
     if (k >= A.maxit) { ok = false; break; }
     const int par = k & 1;          // halo data from the previous reduction
     // neighbour u_{k+1} from its pushed (r, w, s): the owner's exact operations
-    if (helper) {   // warp 0 rebuilds the neighbours' u from their pushed (r, w, s)
+    if (helper) {   // warp 0 rebuilds the neighbours' u: their s and r advanced here, w pushed
       if (lane < 2 * P1) {
         const double* h = s.HRWS + par * 8 * P1 + 4 * lane;
-        const double sh = fma(beta, h[2], h[1]);
-        const double rh = fma(-alpha, sh, h[0]);
-        s.HU[lane] = rh * s.HD[lane];
+        if (k == 0) {   // r0 from the setup push, s_{-1} = 0
+          hr = h[0];
+          hs = 0.0;
+        }
+        hs = fma(beta, hs, h[1]);
+        hr = fma(-alpha, hs, hr);
+        s.HU[lane] = hr * s.HD[lane];
       }
     }
     p = fma(beta, p, u);
@@ -567,7 +584,7 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     if (sub) A.timing[71] = clock64();
     w = matvec(s.Ub, s.HU);
     if (sub) A.timing[72] = clock64();
-    push_rws(par ^ 1);
+    push_rws(par ^ 1, false);
     double v4[NVL] = {own ? r * u : 0.0, own ? w * u : 0.0, own ? r * r : 0.0, 0.0};
     // 1 / alpha and 1 / gamma (needed by the scalar recurrence below) are
     // formed once, by warp 0 while it waits for the cluster's partials, and
