@@ -1,21 +1,26 @@
 #!/usr/bin/env python
 """SI-MLSDC sweep-path benchmark (BASELINE.json metric).
 
-Headline workload: BASELINE configs[1] (1-D viscous Burgers, 512 elements,
-P 8/4, M 5/3, nu=5e-3, CFL 1) -- the config the metric is quoted on that fits
-one GPU.  A "step" is one SI-MLSDC time slab (FMG start, 3 V-cycles, closing
-fine sweep: 4 fine sweeps + 8 coarse passes), replayed from a CUDA graph with
-the state resident in HBM.  value = DOF-sweep updates/s summed over ranks.
-At N=1 the line also carries "secondary": the same contract measured on
-BASELINE configs[3] (2-D Navier-Stokes shear layer, 256^2 elements, P 7/3),
-whose fine level is HBM resident (the roofline the north star grades).
+Headline workload at N=1: BASELINE configs[1] (1-D viscous Burgers, 512
+elements, P 8/4, M 5/3, nu=5e-3, CFL 1) -- the config the metric is quoted on
+that fits one GPU.  A "step" is one SI-MLSDC time slab (FMG start, 3 V-cycles,
+closing fine sweep: 4 fine sweeps + 8 coarse passes), replayed from a CUDA
+graph with the state resident in HBM.  value = DOF-sweep updates/s.  At N=1
+the line also carries "secondary": the same contract on BASELINE configs[3]
+(256^2) and configs[4] (1024^2, the scaling config), whose fine levels are HBM
+resident (the roofline the north star grades).
+
+At N > 1 (torchrun) the headline is BASELINE configs[4] with its element rows
+partitioned over the ranks (NCCL face halo + one allreduce per CG
+iteration): strong scaling, value = the whole problem's DOF-sweeps/s.
 
   python bench.py [--gpus N --steps K --warmup W] [--workload cfgN] [--no-2d]
-  python bench.py --impl reference                       # reference algorithm on CPU
+  python bench.py --impl reference     # the reference package itself on the host CPU
 
-Multi-GPU (torchrun): each rank advances an independent seeded replica of the
-workload (weak scaling, "replicas"): DESIGN.md "Multi-GPU" gives the status
-of the element-partitioned 2-D path.
+The reference arm and ``cpu_baseline`` run the unmodified reference package
+(installed into oracle/_ref by oracle/build_ref.py) through
+``sisdc.mlsdc.run_mlsdc``; for the 2-D configs, which the reference cannot
+run, the oracle's 2-D restatement on a bounded 16x16-element sample.
 """
 from __future__ import annotations
 
@@ -43,8 +48,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
-    ap.add_argument("--cpu-sample-steps", type=int, default=100)   # ~10 s of host work
+    ap.add_argument("--workload", default=None, choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cluster-ctas", type=int, default=0)
     ap.add_argument("--cycles", type=int, default=None, help="override the V-cycles per step")
@@ -118,12 +122,15 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def measured_traffic(kind="1d"):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    name = "r01g_cg_traffic.json" if kind == "1d" else "r01d_cg2_traffic.json"
+def measured_traffic(workload, alg_bytes):
+    """DRAM bytes (read + write) of one launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/traffic.json), rescaled to this
+    run's launch by algorithmic bytes (the captured solve may take a different
+    iteration count); None when no capture of this workload is committed."""
     try:
-        with open(os.path.join(HERE, "profiles", name)) as f:
-            return float(json.load(f)["dram_bytes_per_launch"])
+        with open(os.path.join(HERE, "profiles", "traffic.json")) as f:
+            rec = json.load(f)[workload.split("_")[0]]
+        return float(rec["dram_bytes_per_launch"]) * alg_bytes / float(rec["algorithmic_bytes_per_launch"])
     except Exception:
         return None
 
@@ -137,25 +144,105 @@ def measured_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-# ---------------------------------------------------------- CPU (oracle)
-def cpu_port_rate(w, n_steps, threads_limit=1):
-    """Time the oracle's restatement of the reference algorithm (SuperLU +
-    defect iteration, dgsem.py:503-533) on the host: the reference port."""
+# ------------------------------------------------------ CPU (reference)
+def workload_config(w):
+    """The workload as both arms describe it (identical dicts; run-measured
+    quantities go to "stats")."""
+    is2d = hasattr(w, "nex")
+    U, _ = w.dof_sweeps_per_step()
+    return {
+        "workload": w.name + (" (BASELINE configs[1])" if w.name.startswith("cfg2") else
+                              " (BASELINE configs[4])" if w.name.startswith("cfg5") else ""),
+        "n_elem": (w.nex * w.ney) if is2d else w.n_elem,
+        "degrees": [w.p_coarse, w.p_fine], "nodes": [w.m_coarse, w.m_fine],
+        "schedule": f"SI(2) incremental, radau_right, fmg start, {w.n_cycles} V-cycles + closing fine sweep"
+                    + ("; FAS residual restricted mass-consistently (DESIGN.md)" if is2d else
+                       " (the reference itself diverges with >= 4 cycles on cfg2, DESIGN.md)"),
+        "fine_sweeps_per_step": w.n_cycles + 1, "coarse_passes_per_step": 2 + 2 * w.n_cycles,
+        "dof_sweeps_per_step": U, "cg_rtol": 1e-14,
+    }
+
+
+def host_cpu():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_rate(w, budget_s, threads, max_steps=10 ** 6, warmup=1):
+    """Time the CPU path of workload ``w`` on the host; returns
+    (DOF-sweeps/s, cpu_baseline dict without "value").
+
+    1-D: the UNMODIFIED reference package (``oracle/_ref``, built by
+    ``oracle/build_ref.py``) through ``sisdc.mlsdc.run_mlsdc`` with its SuperLU
+    implicit solve (kind "reference"); the oracle port only if that install is
+    missing (kind "port").  2-D: the reference has no 2-D path,
+    so the oracle's 2-D restatement runs on a 16 x 16-element mesh of the same
+    physics, degrees and schedule (kind "port")."""
     from threadpoolctl import threadpool_limits
-    from oracle import sweeper as osw, workloads
-    from paper_2504_18526_b200.dgsem import Mesh1D, compute_delta
-    u0 = w.initial_state(Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes)
-    dt, _ = w.time_step(u0, compute_delta(w.p_fine))
-    with threadpool_limits(limits=threads_limit):
-        h, _ = workloads.build_hierarchy(w, solver="lu")
-        u = u0
-        osw.run_mlsdc(h, u, 0.0, dt, w.n_cycles, "fmg")   # warm caches (LU factorisation)
-        t0 = time.perf_counter()
-        for s in range(n_steps):
-            u = osw.run_mlsdc(h, u, s * dt, dt, w.n_cycles, "fmg").u[-1].copy()
-        el = time.perf_counter() - t0
     U = w.dof_sweeps_per_step()[0]
-    return U * n_steps / el, el / n_steps
+    with threadpool_limits(limits=threads):
+        if not hasattr(w, "nex"):
+            try:
+                from oracle import refrun
+                tstep, n, _ = refrun.time_steps(w, max_steps, warmup=warmup, budget_s=budget_s)
+                return U / tstep, {
+                    "unit": UNIT, "cores": threads, "kind": "reference",
+                    "sample": f"{n} SI-MLSDC steps of {w.name} from the seeded IC after {warmup} warm-up step(s), "
+                              f"{tstep * 1e3:.1f} ms/step: the unmodified reference package (oracle/_ref) via "
+                              f"sisdc.mlsdc.run_mlsdc, SuperLU implicit solves; host CPU {host_cpu()}, "
+                              f"{threads} thread(s)"}
+            except ImportError as e:
+                why = str(e)
+            from oracle import sweeper as osw, workloads
+            from paper_2504_18526_b200.dgsem import Mesh1D, compute_delta
+            u = w.initial_state(Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes)
+            dt, _ = w.time_step(u, compute_delta(w.p_fine))
+            h, _ = workloads.build_hierarchy(w, solver="lu")
+            s = 0
+            for _ in range(warmup):
+                u = osw.run_mlsdc(h, u, s * dt, dt, w.n_cycles, "fmg").u[-1].copy()
+                s += 1
+            t0, n = time.perf_counter(), 0
+            while n < max_steps and (n < 3 or time.perf_counter() - t0 < budget_s):
+                u = osw.run_mlsdc(h, u, s * dt, dt, w.n_cycles, "fmg").u[-1].copy()
+                s += 1
+                n += 1
+            tstep = (time.perf_counter() - t0) / n
+            return U / tstep, {
+                "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": f"{n} SI-MLSDC steps of {w.name}, {tstep * 1e3:.1f} ms/step: oracle restatement of the "
+                          f"reference algorithm (SuperLU + defect iteration) -- reference install missing ({why}); "
+                          f"host CPU {host_cpu()}, {threads} thread(s)"}
+        import dataclasses
+        from oracle import dg2d, sweeper as osw, workloads
+        from paper_2504_18526_b200.dgsem import compute_delta
+        ws = dataclasses.replace(w, nex=16, ney=16)
+        h, _ = workloads.build_hierarchy_2d(lambda: dg2d.Euler2D(ws.gamma, ws.nu), 0.0, ws.length, 0.0, ws.ly,
+                                            ws.nex, ws.ney, ws.p_coarse, ws.p_fine, ws.m_coarse, ws.m_fine)
+        X, Y = h.levels[-1].ctx.nodes()
+        u = ws.initial_state(X, Y)
+        dt = ws.time_step(u, compute_delta(ws.p_fine))
+        t0, n = time.perf_counter(), 0
+        while n < max_steps and (n < 1 or time.perf_counter() - t0 < budget_s):
+            u = osw.run_mlsdc(h, u, n * dt, dt, ws.n_cycles, "fmg").u[-1].copy()
+            n += 1
+        tstep = (time.perf_counter() - t0) / n
+        Us = ws.dof_sweeps_per_step()[0]
+        return Us / tstep, {
+            "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n} SI-MLSDC step(s) of {w.name}'s physics/degrees/schedule on a 16x16-element mesh "
+                      f"({Us} DOF-sweeps per step, {tstep:.1f} s/step): the oracle's numpy 2-D restatement -- the "
+                      f"reference has no 2-D implementation (SURVEY 8c); host CPU {host_cpu()}, {threads} thread(s)"}
+
+
+def default_workload(args, world):
+    return args.workload or ("cfg2" if world == 1 else "cfg5")
 
 
 def run_reference(args):
@@ -163,38 +250,23 @@ def run_reference(args):
     if rank != 0:
         return 0
     from paper_2504_18526_b200.configs import WORKLOADS
-    w = WORKLOADS[args.workload]
+    w = WORKLOADS[default_workload(args, world)]
     if args.cycles is not None:
         import dataclasses
         w = dataclasses.replace(w, n_cycles=args.cycles)
     cores = os.cpu_count() or 1
-    from threadpoolctl import threadpool_limits
-    from oracle import sweeper as osw, workloads
-    from paper_2504_18526_b200.dgsem import Mesh1D, compute_delta
-    u0 = w.initial_state(Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes)
-    dt, _ = w.time_step(u0, compute_delta(w.p_fine))
-    with threadpool_limits(limits=cores):
-        h, _ = workloads.build_hierarchy(w, solver="lu")
-        u = u0
-        for s in range(args.warmup):
-            u = osw.run_mlsdc(h, u, s * dt, dt, w.n_cycles, "fmg").u[-1].copy()
-        t0 = time.perf_counter()
-        for s in range(args.steps):
-            u = osw.run_mlsdc(h, u, (args.warmup + s) * dt, dt, w.n_cycles, "fmg").u[-1].copy()
-        el = time.perf_counter() - t0
-    U = w.dof_sweeps_per_step()[0]
-    val = U * args.steps / el
+    if hasattr(w, "nex"):
+        val, cb = cpu_rate(w, budget_s=30.0, threads=cores, max_steps=max(1, args.steps))
+    else:
+        val, cb = cpu_rate(w, budget_s=120.0, threads=cores, max_steps=args.steps, warmup=args.warmup)
+    tstep = w.dof_sweeps_per_step()[0] / val
     out = {
-        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name + " (BASELINE configs[1])", "dof_sweeps_per_step": U,
-                   "fine_sweeps_per_step": w.n_cycles + 1,
-                   "schedule": f"fmg + {w.n_cycles} V-cycles + closing sweep"},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} SI-MLSDC steps of {w.name} after {args.warmup} warm-up steps; "
-                                   "oracle restatement of the reference (SuperLU + defect iteration), "
-                                   "Python/numpy/scipy (the reference itself is not on the GPU box)"},
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tstep,
+        "higher_is_better": True, "scaling": "strong" if hasattr(w, "nex") and world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": f"synthetic seeded IC (SURVEY 8d): {w.name}, no dataset",
+        "config": workload_config(w),
+        "cpu_baseline": {"value": val, **cb},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -239,7 +311,7 @@ def cg_roofline(hier, rt, torch, dt, reps=64):
     return t, k, bytes_per
 
 
-def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True):
+def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True, e2e_steps=None):
     """Time `steps` SI-MLSDC slabs of workload `w` (CUDA-graph replays, L2
     flushed between steps, CUDA events, max over ranks); e2e through the slab
     API with pinned host buffers; live roofline of the dominant kernel."""
@@ -305,7 +377,7 @@ def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True):
     h_in = torch.empty(hier.fine.ctx.ndof, dtype=torch.float64, pin_memory=True)
     h_out = torch.empty_like(h_in)
     h_in.copy_(torch.as_tensor(np.ascontiguousarray(u0).reshape(-1)))
-    ke = max(3, min(steps, 50))
+    ke = e2e_steps or max(3, min(steps, 50))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -338,22 +410,18 @@ def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True):
     res = {
         "value": value, "ms_per_step": 1e3 * t_max / steps, "steps": steps, "warmup": warmup, "data": data,
         "config": {
-            "workload": w.name, "n_elem": (w.nex * w.ney) if is2d else w.n_elem,
-            "degrees": [w.p_coarse, w.p_fine], "nodes": [w.m_coarse, w.m_fine],
-            "dt": dt, "steps_to_t_end": n_total,
-            "schedule": f"SI(2) incremental, radau_right, fmg start, {w.n_cycles} V-cycles + closing fine sweep"
-                        + ("; FAS residual restricted mass-consistently (DESIGN.md)" if is2d else
-                           " (the reference itself diverges with >= 4 cycles on cfg2, DESIGN.md)"),
-            "fine_sweeps_per_step": w.n_cycles + 1, "coarse_passes_per_step": 2 + 2 * w.n_cycles,
-            "dof_sweeps_per_step": U, "fine_dof_sweeps_per_s": U_fine * steps * world / t_max,
-            "cg_solves_per_step": solves_per_step,
-            "cg_mean_iterations": float(np.mean(step_its)) if len(step_its) else None,
-            "cg_rtol": 1e-14, "l2": "256 MiB buffer written between timed steps, outside the CUDA events",
+            **workload_config(w),
+            "l2": "256 MiB buffer written between timed steps, outside the CUDA events",
             "parallelism": "replicas" if world > 1 else "single GPU",
             "timing": "CUDA events around each CUDA-graph slab replay, summed; max over ranks",
         },
+        "stats": {
+            "dt": dt, "steps_to_t_end": n_total, "fine_dof_sweeps_per_s": U_fine * steps * world / t_max,
+            "cg_solves_per_step": solves_per_step,
+            "cg_mean_iterations": float(np.mean(step_its)) if len(step_its) else None,
+        },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": measured_traffic("2d" if is2d else "1d"),
+                     "frac": achieved / peak, "traffic": measured_traffic(w.name, bytes_cg),
                      "peak_kind": peak_kind, "kernel": kern, "kernel_us": t_cg * 1e6,
                      "kernel_mean_iterations": k_cg, "algorithmic_bytes_per_launch": bytes_cg, "note": note},
         "clocks": clk.summary(),
@@ -477,15 +545,15 @@ def measure_part(w, args, torch, rt, rank, world, local, steps, warmup, emulate=
         "n_gpus": world, "scaling": "strong",
         "data": f"synthetic seeded IC (SURVEY 8d): {w.name}, no dataset",
         "config": {
-            "workload": w.name, "n_elem": w.nex * w.ney, "degrees": [w.p_coarse, w.p_fine],
-            "nodes": [w.m_coarse, w.m_fine], "dt": dt,
-            "schedule": f"SI(2) incremental, radau_right, fmg start, {w.n_cycles} V-cycles + closing fine sweep; "
-                        "FAS residual restricted mass-consistently (DESIGN.md)",
-            "dof_sweeps_per_step": U, "fine_dof_sweeps_per_s": U_fine * steps / t_max,
+            **workload_config(w),
+            "l2": "256 MiB buffer written between timed steps, outside the CUDA events",
+            "parallelism": how,
+            "timing": "CUDA events around each slab, summed; max over ranks",
+        },
+        "stats": {
+            "dt": dt, "fine_dof_sweeps_per_s": U_fine * steps / t_max,
             "cg_solves_per_step": len(its) / steps, "cg_mean_iterations": float(np.mean(its)) if len(its) else None,
-            "cg_rtol": 1e-14, "l2": "256 MiB buffer written between timed steps, outside the CUDA events",
-            "parallelism": how, "rows_per_rank": [r for _, r, _ in fine.parts] if world == 1 else None,
-            "timing": "CUDA events around each eager slab, summed; max over ranks",
+            "rows_per_rank": [r for _, r, _ in fine.parts] if world == 1 else None,
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_kind": peak_kind,
@@ -508,62 +576,53 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # the driver's rank check reads NCCL's init log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2504_18526_b200.configs import WORKLOADS
     from paper_2504_18526_b200.runtime import get_runtime
-    w = WORKLOADS[args.workload]
+    w = WORKLOADS[default_workload(args, world)]
     if args.cycles is not None:
         import dataclasses
         w = dataclasses.replace(w, n_cycles=args.cycles)
+    is2d = hasattr(w, "nex")
     rt = get_runtime(local)
     rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=args.cluster_ctas)
-    if hasattr(w, "nex") and (world > 1 or args.partition):
+    if is2d and (world > 1 or args.partition):
+        # the scaling config: element rows partitioned over the ranks (NCCL face halo + CG allreduce)
         r = measure_part(w, args, torch, rt, rank, world, local, args.steps, args.warmup, emulate=args.partition)
-        if rank == 0:
-            print(json.dumps({k: v for k, v in r.items()}), flush=True)
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return 0
-    r = measure(w, args, torch, rt, rank, world, local, args.steps, args.warmup)
+    else:
+        r = measure(w, args, torch, rt, rank, world, local, args.steps, args.warmup)
+        r = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64", "n_gpus": world,
+             "scaling": "weak", **r}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not hasattr(w, "nex"):
-        rate, tstep = cpu_port_rate(w, args.cpu_sample_steps, threads_limit=1)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_sample_steps} SI-MLSDC steps of {w.name} from the seeded IC, "
-                         f"{tstep * 1e3:.1f} ms/step: oracle restatement of the reference algorithm "
-                         "(SuperLU + defect iteration), numpy/scipy, 1 thread"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cb = cpu_rate(w, budget_s=15.0 if not is2d else 20.0, threads=1)
+        cpu = {"value": rate, **cb}
     secondary = {}
-    if world == 1 and args.also_2d and not hasattr(w, "nex"):
+    if world == 1 and args.also_2d and not is2d:
         torch.cuda.empty_cache()
-        w2 = WORKLOADS["cfg4"]
-        r2 = measure(w2, args, torch, rt, rank, world, local, 3, 3)
+        r2 = measure(WORKLOADS["cfg4"], args, torch, rt, rank, world, local, args.steps, args.warmup)
         secondary["cfg4"] = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64", **r2,
                              "note": "BASELINE configs[3] (2-D Navier-Stokes shear layer 256^2, P 7/3, M 5/3), "
                                      "same contract as the main line; reported beside it because the headline "
                                      "config is 1-D"}
-    if args.also_2d and args.also_cfg5 and not hasattr(w, "nex"):
-        # BASELINE configs[4], the scaling config: single domain on 1 GPU (CUDA graph), element rows
-        # partitioned over the ranks (NCCL halo + CG allreduce) on N GPUs -- strong scaling
-        torch.cuda.empty_cache()
-        w5 = WORKLOADS["cfg5"]
-        if world == 1:
-            r5 = measure(w5, args, torch, rt, rank, world, local, 3, 3)
-            r5 = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64", "n_gpus": 1,
-                  "scaling": "strong", **r5}
-        else:
-            r5 = measure_part(w5, args, torch, rt, rank, world, local, 3, 3)
-        r5["note"] = ("BASELINE configs[4] (1024^2 elements, P 7/3, 268M fine DOF): the multi-GPU scaling config; "
-                      "value is the whole problem's DOF-sweeps/s (strong scaling over n_gpus)")
-        secondary["cfg5"] = r5
+        if args.also_cfg5:
+            # BASELINE configs[4], the scaling config, single domain (CUDA graph); at N > 1 it is the
+            # headline, element-row partitioned over the ranks (strong scaling)
+            torch.cuda.empty_cache()
+            r5 = measure(WORKLOADS["cfg5"], args, torch, rt, rank, world, local, args.steps, args.warmup,
+                         e2e_steps=3)
+            secondary["cfg5"] = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64",
+                                 "n_gpus": 1, "scaling": "strong", **r5,
+                                 "note": "BASELINE configs[4] (1024^2 elements, P 7/3, 268M fine DOF): the "
+                                         "multi-GPU scaling config (the headline at --gpus N > 1)"}
     if rank == 0:
         out = {
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": r["data"],
-            "config": {**r["config"], "workload": r["config"]["workload"]
-                       + (" (BASELINE configs[1])" if args.workload == "cfg2" else "")},
-            "roofline": r["roofline"], "cpu_baseline": cpu, "clocks": r["clocks"], "e2e": r["e2e"],
-            "gpu_launches": r["gpu_launches"],
+            "scaling": r["scaling"], "vs_baseline": None, "dtype": "f64", "data": r["data"],
+            "config": r["config"], "stats": r["stats"], "roofline": r["roofline"], "cpu_baseline": cpu,
+            "clocks": r["clocks"], "e2e": r["e2e"], "gpu_launches": r["gpu_launches"],
         }
         if secondary:
             out["secondary"] = secondary
