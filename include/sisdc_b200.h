@@ -104,6 +104,9 @@ typedef struct {
 
 /* ----------------------------------------------------------- context */
 int  sisdc_abi_version(void);
+/* sizeof of the by-pointer / by-value PODs, for bindings to check their
+ * mirrors: 0 sisdc_op1d_desc, 1 sisdc_op2d_desc, 2 sisdc_coef (-1 otherwise) */
+int  sisdc_struct_size(int which);
 int  sisdc_ctx_create(int device, sisdc_ctx** out);
 void sisdc_ctx_destroy(sisdc_ctx* ctx);
 const char* sisdc_ctx_last_error(const sisdc_ctx* ctx);

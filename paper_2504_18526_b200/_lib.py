@@ -57,6 +57,7 @@ DP = C.POINTER(C.c_double)
 # that every symbol declared in include/sisdc_b200.h is bound here).
 SIGNATURES = {
     "sisdc_abi_version": (I, []),
+    "sisdc_struct_size": (I, [I]),
     "sisdc_ctx_create": (I, [I, C.POINTER(P)]),
     "sisdc_ctx_destroy": (None, [P]),
     "sisdc_ctx_last_error": (C.c_char_p, [P]),
@@ -123,6 +124,10 @@ def load(path: str = LIB_PATH):
         fn.argtypes = args
     if lib.sisdc_abi_version() != 2:
         raise LibraryError("ABI version mismatch")
+    for which, st in enumerate((Op1DDesc, Op2DDesc, Coef)):
+        if lib.sisdc_struct_size(which) != C.sizeof(st):
+            raise LibraryError(f"ABI struct {st.__name__} is {C.sizeof(st)} bytes here, "
+                               f"{lib.sisdc_struct_size(which)} in the library")
     _lib = lib
     return lib
 

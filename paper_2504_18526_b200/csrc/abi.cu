@@ -144,6 +144,15 @@ extern "C" {
 
 int sisdc_abi_version(void) { return SISDC_ABI_VERSION; }
 
+int sisdc_struct_size(int which) {
+  switch (which) {
+    case 0: return (int)sizeof(sisdc_op1d_desc);
+    case 1: return (int)sizeof(sisdc_op2d_desc);
+    case 2: return (int)sizeof(sisdc_coef);
+    default: return -1;
+  }
+}
+
 int sisdc_ctx_create(int device, sisdc_ctx** out) {
   if (!out) return SISDC_ERR_ARG;
   *out = nullptr;

@@ -112,6 +112,7 @@ class MLSDCStudy(_Study):
     def march(self, cfl: float, k: int):
         from .mlsdc import integrate_mlsdc
         dt, n = self.steps(cfl)
+        self.op.rt.reset_status()   # each march is independent (cli.py:1110-1138): clear latched failures
         return integrate_mlsdc(self.hier, self.u0, 0.0, dt, n, k, strategy=self.strategy, c_fmg=self.c_fmg)
 
 
@@ -127,6 +128,7 @@ class SDCStudy(_Study):
     def march(self, cfl: float, k: int):
         from .sdc import run_sdc
         dt, n = self.steps(cfl)
+        self.op.rt.reset_status()   # each march is independent (cli.py:1110-1138): clear latched failures
         u, t = self.u0, 0.0
         for _ in range(n):
             u = run_sdc(self.op, self.rule, self.weights, dt, self.scheme, u, t, k, form=self.form,

@@ -137,55 +137,101 @@ def build_spatial_p_transfer(p_coarse: int, p_fine: int, n_elem: int, ncomp: int
                            {"interp": interp, "project": project, "restrict": restrict}, projection_kind)
 
 
+def _legendre_vandermonde(x, n):
+    """V[i, k] = P_k(x_i), k < n (three-term recurrence)."""
+    x = np.asarray(x, dtype=float)
+    V = np.empty((len(x), n))
+    V[:, 0] = 1.0
+    if n > 1:
+        V[:, 1] = x
+    for k in range(1, n - 1):
+        V[:, k + 1] = ((2 * k + 1) * x * V[:, k] - k * V[:, k - 1]) / (k + 1)
+    return V
+
+
+def _materialise(fn, n_in):
+    """Dense matrix of a linear map given as a function of one input vector."""
+    cols = [fn(np.eye(n_in)[j]) for j in range(n_in)]
+    return np.stack(cols, axis=1)
+
+
 def build_spatial_h_transfer(ne_coarse: int, p: int, ncomp: int = 1, projection_kind: str = "embedded",
                              jump_policy: str = "linear_blend") -> SpatialTransfer:
-    """2:1 element coarsening (``transfer.py:248-317``): each coarse parent owns
-    two children.  Interpolation evaluates the parent on each child half;
-    the embedded projection evaluates each child on its half of the parent
-    (averaging at the centre node) after a jump preprocessor on the child
-    pair (linear_blend: ramps removing the interface jump; average: mean of
-    the two interface values); the l2 projection is the Galerkin projection of
-    the piecewise child data.  On the GPU the pair of children is one
-    contiguous 2(P+1)-node block per parent, so the p-transfer kernels apply
-    the stacked blocks unchanged."""
+    """2:1 element coarsening (the reference's ``transfer.py:248-317``
+    semantics): each coarse parent owns two children of the same degree.
+
+    Derived here in the Legendre modal basis of the parent (not from nodal
+    Lagrange products): a nodal vector u on the GLL nodes xi has modal
+    coefficients c = V^-1 u, V[i, k] = P_k(xi_i).
+
+    * interp: the parent polynomial evaluated at the child nodes, which sit at
+      (xi - 1)/2 and (xi + 1)/2 in parent coordinates;
+    * embedded projection: the child pair is first made continuous at its
+      shared interface by the jump policy -- linear_blend adds J (1 + xi)/4 to
+      the left child and subtracts J (1 - xi)/4 from the right one
+      (J = u_R(-1) - u_L(+1): ramps vanishing at the parent's outer ends,
+      both interface values become the mean), average replaces both interface
+      values by their mean -- then every parent node takes the value of the
+      child polynomial that covers it (the centre node, for even P, the mean
+      of the two interface values);
+    * l2 projection: the modal Galerkin projection of the piecewise child
+      polynomial, c_k = (2k + 1)/2 int_{-1}^{1} u P_k, exact by Gauss
+      quadrature on each half (no jump handling: conservative by construction);
+    * restrict = interp^T.
+
+    The map on one child pair is materialised column by column.  On the GPU
+    the pair of children is one contiguous 2(P+1)-node block per parent, so
+    the p-transfer kernels apply the stacked blocks unchanged."""
     from .collocation import gauss_legendre
+    if jump_policy not in ("linear_blend", "average"):
+        raise ValueError(f"unknown jump policy {jump_policy!r}")
+    if projection_kind not in ("embedded", "l2"):
+        raise ValueError(f"unknown projection kind {projection_kind!r}")
     p1 = p + 1
     xi = _gll_reference(p1)
-    IL = lagrange_matrix(xi, 0.5 * (xi - 1.0))
-    IR = lagrange_matrix(xi, 0.5 * (xi + 1.0))
-    B = np.eye(2 * p1)
-    if jump_policy == "linear_blend":
-        d = np.zeros(2 * p1)
-        d[p1] = 1.0
-        d[p1 - 1] = -1.0
-        B[:p1] += np.outer(0.25 * (1.0 + xi), d)
-        B[p1:] -= np.outer(0.25 * (1.0 - xi), d)
-    elif jump_policy == "average":
-        B[p1 - 1] = 0.0
-        B[p1 - 1, p1 - 1] = B[p1 - 1, p1] = 0.5
-        B[p1] = B[p1 - 1]
-    else:
-        raise ValueError(f"unknown jump policy {jump_policy!r}")
-    if projection_kind == "embedded":
-        E = np.zeros((p1, 2 * p1))
+    Vinv = np.linalg.inv(_legendre_vandermonde(xi, p1))
+
+    def evaluate(u, pts):            # the degree-P polynomial with nodal values u at the points pts
+        return _legendre_vandermonde(pts, p1) @ (Vinv @ u)
+
+    IL = _materialise(lambda u: evaluate(u, 0.5 * (xi - 1.0)), p1)
+    IR = _materialise(lambda u: evaluate(u, 0.5 * (xi + 1.0)), p1)
+
+    def continuous_pair(pair):
+        uL, uR = pair[:p1].copy(), pair[p1:].copy()
+        if jump_policy == "linear_blend":
+            J = uR[0] - uL[-1]
+            uL += 0.25 * (1.0 + xi) * J
+            uR -= 0.25 * (1.0 - xi) * J
+        else:
+            mean = 0.5 * (uL[-1] + uR[0])
+            uL[-1] = uR[0] = mean
+        return uL, uR
+
+    def embedded(pair):
+        uL, uR = continuous_pair(pair)
+        out = np.empty(p1)
         for i, x in enumerate(xi):
             if x < 0.0:
-                E[i, :p1] = lagrange_matrix(xi, np.array([2.0 * x + 1.0]))[0]
+                out[i] = evaluate(uL, np.array([2.0 * x + 1.0]))[0]
             elif x > 0.0:
-                E[i, p1:] = lagrange_matrix(xi, np.array([2.0 * x - 1.0]))[0]
+                out[i] = evaluate(uR, np.array([2.0 * x - 1.0]))[0]
             else:
-                E[i, p1 - 1] = E[i, p1] = 0.5
-        P = E @ B
-    elif projection_kind == "l2":
-        gx, gw = gauss_legendre(p1 + 3)
-        Lp = lagrange_matrix(xi, gx)
-        G = Lp.T @ (gw[:, None] * Lp)
-        BL = lagrange_matrix(xi, 0.5 * gx - 0.5).T @ (0.5 * gw[:, None] * lagrange_matrix(xi, gx))
-        BR = lagrange_matrix(xi, 0.5 * gx + 0.5).T @ (0.5 * gw[:, None] * lagrange_matrix(xi, gx))
-        Gi = np.linalg.inv(G)
-        P = np.concatenate((Gi @ BL, Gi @ BR), axis=1)
-    else:
-        raise ValueError(f"unknown projection kind {projection_kind!r}")
+                out[i] = 0.5 * (uL[-1] + uR[0])
+        return out
+
+    gx, gw = gauss_legendre(p1 + 3)
+    scale = 0.5 * (2.0 * np.arange(p1) + 1.0)
+
+    def l2(pair):
+        c = np.zeros(p1)
+        for half, shift in ((pair[:p1], -0.5), (pair[p1:], 0.5)):
+            x = 0.5 * gx + shift                       # quadrature points of this half, parent coordinates
+            vals = evaluate(half, gx)                  # the child polynomial there (its own coordinate is gx)
+            c += _legendre_vandermonde(x, p1).T @ (0.5 * gw * vals)
+        return _legendre_vandermonde(xi, p1) @ (scale * c)
+
+    P = _materialise(embedded if projection_kind == "embedded" else l2, 2 * p1)
     interp = np.concatenate((IL, IR), axis=0)          # (2 p1, p1): parent -> child pair
     return SpatialTransfer("h", ncomp, ne_coarse, 2 * ne_coarse, p1, p1,
                            {"interp_lr": np.stack((IL, IR)), "project_lr": (P[:, :p1], P[:, p1:]),

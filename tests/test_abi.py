@@ -76,3 +76,22 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(root, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_reference_binding_structs_match_library(lib):
+    """The reference-side ctypes binding shown in INTEGRATION.md
+    (integration/sisdc_b200_binding.py) mirrors the header's PODs byte for
+    byte (ABI v2: 13-field sisdc_op1d_desc)."""
+    import importlib.util
+    from paper_2504_18526_b200 import _lib
+    spec = importlib.util.spec_from_file_location("sisdc_b200_binding",
+                                                  os.path.join(REPO, "integration", "sisdc_b200_binding.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert lib.sisdc_struct_size(0) == C.sizeof(b.Desc) == C.sizeof(_lib.Op1DDesc)
+    assert lib.sisdc_struct_size(2) == C.sizeof(b.Coef) == C.sizeof(_lib.Coef)
+    assert lib.sisdc_struct_size(1) == C.sizeof(_lib.Op2DDesc)
+    assert [f[0] for f in b.Desc._fields_] == [f[0] for f in _lib.Op1DDesc._fields_]
+    # INTEGRATION.md embeds the binding verbatim
+    doc = open(os.path.join(REPO, "INTEGRATION.md")).read()
+    assert open(os.path.join(REPO, "integration", "sisdc_b200_binding.py")).read().strip() in doc

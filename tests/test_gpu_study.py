@@ -84,3 +84,40 @@ def test_convergence_study_matches_reference_cli(golden):
         for a, b in zip(rows, rrows):
             assert a[:-1] == b[:-1]
             assert abs(float(a[-1]) - float(b[-1])) <= tol * abs(float(b[-1]))
+
+
+def test_failed_point_does_not_poison_later_points(golden):
+    """A CFL point whose march fails (non-finite state -> SolverError latched
+    on the device) must not turn later points on the same rank into failures:
+    each march is independent, as in the reference CLI (cli.py:1110-1138)."""
+    from paper_2504_18526_b200 import dgsem, mlsdc, problems, study
+    G = golden["study"]
+    cfg = json.loads(str(G["config"]))
+    pr, lv = cfg["problem"], cfg["levels"]
+    prob = problems.ConvectionDiffusion(pr["speed"], pr["nu"])
+    exact = problems.wave_packet_exact(pr["nu"], pr["speed"])
+    h = mlsdc.build_p_hierarchy(lambda P: dgsem.DGOperator(dgsem.Mesh1D(0.0, 1.0, lv[1]["n_elem"], P), prob),
+                                [lv[0]["degree"], lv[1]["degree"]], [lv[0]["n_nodes"], lv[1]["n_nodes"]])
+    op = h.fine.ctx
+    u0 = op.nodal_field(lambda x: exact(x, 0.0)[None])
+    u_ref = op.nodal_field(lambda x: exact(x, cfg["time"]["t_end"])[None])
+    cfl_bad, cfl_good = 1.0, float(cfg["sweep"]["cfl_values"][0])
+
+    class Poisoned(study.MLSDCStudy):
+        def march(self, cfl, k):
+            if cfl == cfl_bad:
+                good = self.u0
+                self.u0 = good * float("nan")
+                try:
+                    return super().march(cfl, k)
+                finally:
+                    self.u0 = good
+            return super().march(cfl, k)
+
+    st = Poisoned(h, u0, u_ref, cfg["time"]["t_end"], dgsem.max_wave_speed(op, u0))
+    pts = study.cfl_sweep(st, [cfl_bad, cfl_good], 3)
+    assert pts[0].status == "failed"
+    clean = study.cfl_sweep(study.MLSDCStudy(h, u0, u_ref, cfg["time"]["t_end"], dgsem.max_wave_speed(op, u0)),
+                            [cfl_good], 3)[0]
+    assert pts[1].status == clean.status != "failed"
+    assert pts[1].errors == clean.errors
