@@ -578,6 +578,109 @@ def gen_study():
     np.savez_compressed(os.path.join(OUT, "study.npz"), **out)
 
 
+# ------------------------------------------------ multilevel (L = 3) hierarchies
+# The paper's Burgers moving front (cli.py:751-755 front on
+# [-1, 1], nu = 1e-2, exact solution as reference), high-resolution hierarchies
+# of tab:burgers_iterations_cfl_hires: MLSDC-SI(2,2)_{3,5,7} with p-coarsening
+# {5,10,15} on 200 elements and h-coarsening {50,100,200} at P = 15.
+ML_LEVELS = {
+    "p3": [(200, 5, 3), (200, 10, 5), (200, 15, 7)],
+    "h3": [(50, 15, 3), (100, 15, 5), (200, 15, 7)],
+    "i3": [(200, 15, 3), (200, 15, 5), (200, 15, 7)],   # time-only coarsening (identity spatial)
+    "sdc": [(200, 15, 7)],
+}
+ML_STEP_CASES = {   # one SI-MLSDC step at CFL 4, 3 V-cycles, from the exact state at t = 0
+    "p3_fmg1": ("p3", "fmg", 1), "p3_fmg2": ("p3", "fmg", 2), "p3_cascade": ("p3", "cascade", 1),
+    "p3_predictor": ("p3", "predictor", 1), "p3_constant": ("p3", "constant", 1),
+    "h3_fmg1": ("h3", "fmg", 1), "h3_fmg2": ("h3", "fmg", 2), "h3_cascade": ("h3", "cascade", 1),
+    "i3_fmg1": ("i3", "fmg", 1),
+}
+ML_STUDY_CASES = {   # rows of tab:burgers_iterations_cfl_hires
+    "sdc": ("sdc", "predictor", 1), "i3_fmg1": ("i3", "fmg", 1), "h3_fmg2": ("h3", "fmg", 2),
+    "h3_fmg1": ("h3", "fmg", 1), "h3_cascade": ("h3", "cascade", 1), "p3_fmg1": ("p3", "fmg", 1),
+}
+ML_STUDY_CFL = (8.0, 16.0, 32.0, 64.0)
+
+
+def ml_config(levels, start, c_fmg, cfl_values=(4.0,), max_iterations=16):
+    lv = [{"n_elem": ne, "degree": P, "n_nodes": M} for ne, P, M in ML_LEVELS[levels]]
+    method = {"start": start, "c_fmg": c_fmg} if len(lv) > 1 else {"start": start}
+    return {"study": "cfl-sweep", "problem": {"kind": "burgers", "nu": 0.01}, "levels": lv,
+            "time": {"t_end": 0.1}, "method": method,
+            "sweep": {"cfl_values": list(cfl_values), "max_iterations": max_iterations},
+            "reference": {"kind": "exact"}}
+
+
+def gen_multilevel_steps():
+    """One SI-MLSDC step per 3-level case, built by the reference CLI's own
+    _build_operators/_build_hierarchy (cli.py:776-815): the reference as
+    shipped (SuperLU) and with the pinned PCG (iteration sequence)."""
+    import json
+    from sisdc import cli as rcli
+    out = {}
+    for name, (levels, start, c_fmg) in ML_STEP_CASES.items():
+        cfg = rcli.parse_config(json.dumps(ml_config(levels, start, c_fmg)))
+        bundle = rcli.build_problem(cfg.problem)
+        res = {}
+        for solver in ("lu", "pcg"):
+            ops, rules, weights = rcli._build_operators(cfg, bundle)
+            hier = rcli._build_hierarchy(cfg, ops, rules, weights)
+            op = ops[-1]
+            u0 = rcli._initial_state(op, bundle)
+            lam = rd.max_wave_speed(op, u0)
+            dt = rd.dt_from_cfl(4.0, op.mesh.dx, lam, op.mesh.degree)
+            if solver == "lu":
+                res["lu"] = rm.run_mlsdc(hier, u0, 0.0, dt, 3, strategy=start, c_fmg=c_fmg).end_value.copy()
+            else:
+                with PcgPatch(1e-14, pcg) as pp:
+                    res["pcg"] = rm.run_mlsdc(hier, u0, 0.0, dt, 3, strategy=start, c_fmg=c_fmg).end_value.copy()
+                res["iters"] = np.array([it for it, _ in pp.log])
+        out[f"{name}_u0"], out[f"{name}_dt"] = u0, np.array(dt)
+        out[f"{name}_lu_u1"], out[f"{name}_pcg_u1"], out[f"{name}_pcg_iters1"] = res["lu"], res["pcg"], res["iters"]
+        print(name, len(res["iters"]), int(res["iters"].sum()),
+              np.linalg.norm(res["lu"] - res["pcg"]) / np.linalg.norm(res["lu"]), flush=True)
+    out["config"] = np.array(json.dumps({k: list(v) for k, v in ML_STEP_CASES.items()}))
+    out["levels"] = np.array(json.dumps(ML_LEVELS))
+    np.savez_compressed(os.path.join(OUT, "multilevel.npz"), **out)
+
+
+def _ml_study_job(args):
+    import json
+    import tempfile
+    name, cfl = args
+    from sisdc import cli as rcli
+    levels, start, c_fmg = ML_STUDY_CASES[name]
+    cfg = rcli.parse_config(json.dumps(ml_config(levels, start, c_fmg, (cfl,))))
+    with tempfile.TemporaryDirectory() as d:
+        rcli.run_study(cfg, d)
+        return name, cfl, open(os.path.join(d, "errors.csv")).read(), open(os.path.join(d, "iterations.csv")).read()
+
+
+def gen_multilevel_study(procs=8):
+    """The reference CLI's cfl-sweep study (cli.py:1110-1194) on the paper's
+    high-resolution Burgers front hierarchies, one process per (case, CFL):
+    the iterations.csv / errors.csv rows the GPU study must reproduce, and
+    the paper's own table values next to them."""
+    import json
+    from multiprocessing import Pool
+    jobs = [(n, c) for n in ML_STUDY_CASES for c in ML_STUDY_CFL]
+    with Pool(procs) as pool:
+        res = pool.map(_ml_study_job, jobs, chunksize=1)
+    out = {"config": np.array(json.dumps({"cases": {k: list(v) for k, v in ML_STUDY_CASES.items()},
+                                          "levels": ML_LEVELS, "cfl": list(ML_STUDY_CFL),
+                                          "max_iterations": 16, "t_end": 0.1, "nu": 0.01}))}
+    for name in ML_STUDY_CASES:
+        errs = [r for r in res if r[0] == name]
+        errs.sort(key=lambda r: r[1])
+        head_e, head_i = errs[0][2].split("\n")[0], errs[0][3].split("\n")[0]
+        out[f"{name}_errors_csv"] = np.array("\n".join([head_e] + [ln for r in errs
+                                                                    for ln in r[2].strip().split("\n")[1:]]) + "\n")
+        out[f"{name}_iterations_csv"] = np.array("\n".join([head_i] + [ln for r in errs
+                                                                        for ln in r[3].strip().split("\n")[1:]]) + "\n")
+        print(name, str(out[f"{name}_iterations_csv"]), flush=True)
+    np.savez_compressed(os.path.join(OUT, "multilevel_study.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     if len(sys.argv) > 1 and sys.argv[1] == "sod":
@@ -585,6 +688,12 @@ if __name__ == "__main__":
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "study":
         gen_study()
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "multilevel":
+        gen_multilevel_steps()
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "multilevel_study":
+        gen_multilevel_study()
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "sources":
         gen_sources()
@@ -615,5 +724,7 @@ if __name__ == "__main__":
     gen_sources()
     gen_study()
     gen_sod()
+    gen_multilevel_steps()
+    gen_multilevel_study()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

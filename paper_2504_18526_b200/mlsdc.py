@@ -345,3 +345,33 @@ def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes:
         presmooth = lambda u: smooth_start(lo_op, u)   # noqa: E731
     return Hierarchy(levels, transfers, n_coarse=n_coarse, n_sweep=n_sweep, form=form, presmooth=presmooth,
                      post_sweep_on_finest=post_sweep_on_finest)
+
+
+def build_hierarchy(make_op, levels, scheme: str = "si2", nodes: str = "radau_right", n_coarse: int = 2,
+                    n_sweep: int = 1, post_sweep_on_finest: bool = True, form: str = "incremental",
+                    projection: str = "embedded", jump_policy: str = "linear_blend") -> Hierarchy:
+    """Hierarchy from per-level (n_elem, degree, n_nodes), coarsest first, as
+    the reference CLI's ``_build_hierarchy`` (``cli.py:789-815``) builds it:
+    h-transfer where the element counts differ (2:1), p-transfer where the
+    degrees differ, the identity (time-only coarsening) otherwise.
+    ``make_op(n_elem, degree)`` returns a 1-D DGOperator."""
+    from .transfer import build_identity_spatial, build_spatial_h_transfer, build_spatial_p_transfer
+    ops = [make_op(ne, P) for ne, P, _ in levels]
+    rules = [make_nodes(nodes, M) for _, _, M in levels]
+    lv = [Level(o, r, make_weights(r), scheme) for o, r in zip(ops, rules)]
+    transfers = []
+    for lo in range(len(ops) - 1):
+        hi = lo + 1
+        pair = build_temporal_transfer(rules[lo], rules[hi], projection)
+        (nc, pc, _), (nf, pf, _) = levels[lo], levels[hi]
+        if nc != nf:
+            if nf != 2 * nc or pc != pf:
+                raise ValueError("h-coarsening fuses two elements of the same degree into one")
+            spatial = build_spatial_h_transfer(nc, pc, ops[lo].ncomp, projection, jump_policy)
+        elif pc != pf:
+            spatial = build_spatial_p_transfer(pc, pf, nc, ops[lo].ncomp, projection)
+        else:
+            spatial = build_identity_spatial(ops[lo].ndof)
+        transfers.append(SpaceTimeTransfer(pair, spatial))
+    return Hierarchy(lv, transfers, n_coarse=n_coarse, n_sweep=n_sweep, form=form,
+                     post_sweep_on_finest=post_sweep_on_finest)

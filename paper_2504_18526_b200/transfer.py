@@ -249,13 +249,19 @@ class _XferHandle:
         else:
             It, Pt = temporal.interp, temporal.project
             Mf, Mc = It.shape
-        Isp, Psp, Rsp = spatial.blocks["interp"], spatial.blocks["project"], spatial.blocks["restrict"]
+        if spatial.kind == "identity":   # same mesh and degree (time-only coarsening): unit blocks per DOF
+            Isp = Psp = Rsp = np.ones((1, 1))
+        else:
+            Isp, Psp, Rsp = spatial.blocks["interp"], spatial.blocks["project"], spatial.blocks["restrict"]
         self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (It, Pt, Isp, Psp, Rsp)]
         h = C.c_void_p()
         ptrs = [a.ctypes.data_as(_lib.DP) for a in self._keep]
         if spatial.kind == "p2d":   # element slabs of (P+1)^2 nodes, matrices applied in x and y
             rt.check(rt.lib.sisdc_xfer2d_create(rt.h, spatial.ne_fine * spatial.ncomp, spatial.np_coarse,
                                                 spatial.np_fine, Mc, Mf, *ptrs, C.byref(h)), "xfer2d_create")
+        elif spatial.kind == "identity":
+            rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ncomp * spatial.ne_fine * spatial.np_fine, 1, 1, Mc, Mf,
+                                              *ptrs, C.byref(h)), "xfer_create")
         elif spatial.kind == "h":   # parent element <-> contiguous child pair of 2 (P+1) nodes
             rt.check(rt.lib.sisdc_xfer_create(rt.h, spatial.ne_coarse * spatial.ncomp, spatial.np_coarse,
                                               2 * spatial.np_fine, Mc, Mf,
@@ -309,8 +315,6 @@ class SpaceTimeTransfer:
 
     @property
     def handle(self) -> _XferHandle:
-        if self.spatial.kind not in ("p", "p2d", "h"):
-            raise NotImplementedError("identity spatial transfers have no GPU handle")
         return _xfer_handle(self.spatial, self.temporal)
 
     def _down(self, sdir, tdir, nodes):

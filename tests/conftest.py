@@ -25,3 +25,15 @@ def gpu_available():
 def golden():
     import numpy as np
     return {name: np.load(os.path.join(GOLDEN, name + ".npz")) for name in ("tables", "operators", "trajectories", "nonincremental", "dirichlet", "presmooth", "htransfer", "cns", "sources", "study", "sod")}
+
+
+@pytest.fixture(scope="session")
+def golden_ml():
+    import numpy as np
+    return np.load(os.path.join(GOLDEN, "multilevel.npz"))
+
+
+@pytest.fixture(scope="session")
+def golden_mls():
+    import numpy as np
+    return np.load(os.path.join(GOLDEN, "multilevel_study.npz"))

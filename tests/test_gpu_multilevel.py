@@ -1,0 +1,121 @@
+"""Three-level MLSDC on the GPU (the intermediate
+level of v_cycle, multi-level FAS, and every start strategy) against the
+reference itself (tests/golden/multilevel.npz, oracle/make_golden.py
+``gen_multilevel_steps``): the paper's MLSDC-SI(2,2)_{3,5,7} hierarchies on
+the Burgers moving front, p-coarsening {5,10,15} and
+h-coarsening {50,100,200} at P = 15 plus time-only coarsening, with the FMG
+(c_fmg = 1, 2), cascade, predictor and constant starts.  One step each:
+the identical CG iteration sequence of the reference-with-PCG and <= 1e-11
+relative L2 (<= 1e-9 against the reference's SuperLU as shipped).
+
+The study test reproduces the reference CLI's cfl-sweep output
+(cli.py:1110-1194) for the paper's high-resolution table rows at CFL 8-64
+(tests/golden/multilevel_study.npz)."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+def l2rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def rt():
+    from paper_2504_18526_b200.runtime import get_runtime
+    r = get_runtime()
+    r.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=0)
+    r.reset_status()
+    return r
+
+
+def front_hierarchy(levels):
+    from paper_2504_18526_b200 import dgsem, mlsdc, problems
+    prob, exact = problems.burgers_front_problem(0.01)
+    h = mlsdc.build_hierarchy(
+        lambda ne, P: dgsem.DGOperator(dgsem.Mesh1D(-1.0, 1.0, ne, P, bc="dirichlet"), prob),
+        [tuple(x) for x in levels])
+    return h, exact
+
+
+CASES = ["p3_fmg1", "p3_fmg2", "p3_cascade", "p3_predictor", "p3_constant", "h3_fmg1", "h3_fmg2", "h3_cascade",
+         "i3_fmg1"]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_three_level_step(rt, golden_ml, case):
+    from paper_2504_18526_b200 import mlsdc
+    G = golden_ml
+    cfg = json.loads(str(G["config"]))[case]
+    levels = json.loads(str(G["levels"]))[cfg[0]]
+    h, _ = front_hierarchy(levels)
+    assert len(h.levels) == 3
+    n0 = rt.status()[2]
+    sol = mlsdc.run_mlsdc(h, G[f"{case}_u0"], 0.0, float(G[f"{case}_dt"]), 3, strategy=cfg[1], c_fmg=cfg[2])
+    its = rt.cg_log()[0][n0:].tolist()
+    rt.raise_on_failure()
+    ref_its = G[f"{case}_pcg_iters1"].tolist()
+    assert len(its) == len(ref_its) and sum(its) == sum(ref_its)
+    assert its == ref_its
+    assert l2rel(sol.u[-1], G[f"{case}_pcg_u1"]) < 1e-11
+    assert l2rel(sol.u[-1], G[f"{case}_lu_u1"]) < 1e-9
+
+
+def parse(text):
+    lines = str(text).strip().split("\n")
+    return lines[0], [ln.split(",") for ln in lines[1:]]
+
+
+STUDY = ["sdc", "i3_fmg1", "h3_fmg2", "h3_fmg1", "h3_cascade", "p3_fmg1"]
+
+
+@pytest.mark.parametrize("case", STUDY)
+def test_paper_table_rows_match_reference_cli(rt, golden_mls, case):
+    """GPU cfl-sweep of one row of tab:burgers_iterations_cfl_hires vs the
+    reference CLI's iterations.csv (identical n_steps, converged iteration,
+    status) and errors.csv (every error of the series to 1e-8 relative)."""
+    import os
+    import tempfile
+    from paper_2504_18526_b200 import collocation, dgsem, study
+    G = golden_mls
+    cfg = json.loads(str(G["config"]))
+    levels_name, start, c_fmg = cfg["cases"][case]
+    levels = cfg["levels"][levels_name]
+    t_end = cfg["t_end"]
+    if len(levels) == 1:
+        from paper_2504_18526_b200 import problems
+        prob, exact = problems.burgers_front_problem(cfg["nu"])
+        ne, P, M = levels[0]
+        op = dgsem.DGOperator(dgsem.Mesh1D(-1.0, 1.0, ne, P, bc="dirichlet"), prob)
+        rule = collocation.make_nodes("radau_right", M)
+        u0 = op.nodal_field(lambda x: exact(x, 0.0)[None])
+        uref = op.nodal_field(lambda x: exact(x, t_end)[None])
+        st = study.SDCStudy(op, rule, collocation.make_weights(rule), "si2", u0, uref, t_end,
+                            dgsem.max_wave_speed(op, u0))
+    else:
+        h, exact = front_hierarchy(levels)
+        op = h.fine.ctx
+        u0 = op.nodal_field(lambda x: exact(x, 0.0)[None])
+        uref = op.nodal_field(lambda x: exact(x, t_end)[None])
+        st = study.MLSDCStudy(h, u0, uref, t_end, dgsem.max_wave_speed(op, u0), strategy=start, c_fmg=c_fmg)
+    with tempfile.TemporaryDirectory() as d:
+        study.cfl_sweep(st, cfg["cfl"], cfg["max_iterations"], out_dir=d)
+        mine_i = open(os.path.join(d, "iterations.csv")).read()
+        mine_e = open(os.path.join(d, "errors.csv")).read()
+    h1, rows = parse(mine_i)
+    h2, rrows = parse(G[f"{case}_iterations_csv"])
+    assert h1 == h2 and len(rows) == len(rrows)
+    for a, b in zip(rows, rrows):
+        assert a[:3] == b[:3] and a[4] == b[4], (a, b)     # cfl, n_steps, converged iteration, status
+    h1, rows = parse(mine_e)
+    h2, rrows = parse(G[f"{case}_errors_csv"])
+    assert h1 == h2 and len(rows) == len(rrows)
+    for a, b in zip(rows, rrows):
+        assert a[:3] == b[:3]
+        assert abs(float(a[3]) - float(b[3])) <= 1e-8 * abs(float(b[3])), (a, b)
