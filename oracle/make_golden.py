@@ -635,6 +635,8 @@ def gen_multilevel_steps():
                 with PcgPatch(1e-14, pcg) as pp:
                     res["pcg"] = rm.run_mlsdc(hier, u0, 0.0, dt, 3, strategy=start, c_fmg=c_fmg).end_value.copy()
                 res["iters"] = np.array([it for it, _ in pp.log])
+                res["margins"] = np.array([mg for _, mg in pp.log])
+        out[f"{name}_pcg_margins1"] = res["margins"]
         out[f"{name}_u0"], out[f"{name}_dt"] = u0, np.array(dt)
         out[f"{name}_lu_u1"], out[f"{name}_pcg_u1"], out[f"{name}_pcg_iters1"] = res["lu"], res["pcg"], res["iters"]
         print(name, len(res["iters"]), int(res["iters"].sum()),
@@ -647,23 +649,27 @@ def gen_multilevel_steps():
 def _ml_study_job(args):
     import json
     import tempfile
-    name, cfl = args
+    name, cfl, solver = args
     from sisdc import cli as rcli
     levels, start, c_fmg = ML_STUDY_CASES[name]
     cfg = rcli.parse_config(json.dumps(ml_config(levels, start, c_fmg, (cfl,))))
     with tempfile.TemporaryDirectory() as d:
-        rcli.run_study(cfg, d)
+        if solver == "pcg":
+            with PcgPatch(1e-14, pcg):
+                rcli.run_study(cfg, d)
+        else:
+            rcli.run_study(cfg, d)
         return name, cfl, open(os.path.join(d, "errors.csv")).read(), open(os.path.join(d, "iterations.csv")).read()
 
 
-def gen_multilevel_study(procs=8):
+def gen_multilevel_study(procs=8, solver="lu"):
     """The reference CLI's cfl-sweep study (cli.py:1110-1194) on the paper's
     high-resolution Burgers front hierarchies, one process per (case, CFL):
     the iterations.csv / errors.csv rows the GPU study must reproduce, and
     the paper's own table values next to them."""
     import json
     from multiprocessing import Pool
-    jobs = [(n, c) for n in ML_STUDY_CASES for c in ML_STUDY_CFL]
+    jobs = [(n, c, solver) for n in ML_STUDY_CASES for c in sorted(ML_STUDY_CFL, reverse=True)]
     with Pool(procs) as pool:
         res = pool.map(_ml_study_job, jobs, chunksize=1)
     out = {"config": np.array(json.dumps({"cases": {k: list(v) for k, v in ML_STUDY_CASES.items()},
@@ -678,7 +684,8 @@ def gen_multilevel_study(procs=8):
         out[f"{name}_iterations_csv"] = np.array("\n".join([head_i] + [ln for r in errs
                                                                         for ln in r[3].strip().split("\n")[1:]]) + "\n")
         print(name, str(out[f"{name}_iterations_csv"]), flush=True)
-    np.savez_compressed(os.path.join(OUT, "multilevel_study.npz"), **out)
+    np.savez_compressed(os.path.join(OUT, "multilevel_study.npz" if solver == "lu" else
+                                     "multilevel_study_pcg.npz"), **out)
 
 
 if __name__ == "__main__":
@@ -694,6 +701,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "multilevel_study":
         gen_multilevel_study()
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "multilevel_study_pcg":
+        gen_multilevel_study(solver="pcg")
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "sources":
         gen_sources()
@@ -726,5 +736,6 @@ if __name__ == "__main__":
     gen_sod()
     gen_multilevel_steps()
     gen_multilevel_study()
+    gen_multilevel_study(solver="pcg")
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -44,6 +44,27 @@ def front_hierarchy(levels):
     return h, exact
 
 
+def assert_same_iterations(its, margins, ref_its, ref_margins, borderline=0.85):
+    """Identical CG iteration counts, solve by solve, except where the
+    stopping test (||r_k|| <= rtol ||b||, rtol = 1e-14) was decided within
+    roundoff: there the counts may differ by one, and the side that stopped
+    first must have crossed the threshold with margin ||r_k|| / (rtol ||b||)
+    >= ``borderline``.  At P = 15 the recursive residual at 1e-14 sits at the
+    attainable-accuracy floor, where a different summation order (warp /
+    cluster reductions here, numpy pairwise sums in the reference run) moves
+    it by up to ~12% (measured: 10 of 186 solves on h3_fmg1 flip, all with
+    margin 0.89-1.0 on the side that stopped first)."""
+    flips = 0
+    for k, (a, b, ma, mb) in enumerate(zip(its, ref_its, margins, ref_margins)):
+        if a == b:
+            continue
+        flips += 1
+        assert abs(a - b) == 1, (k, a, b)
+        first = ma if a < b else mb
+        assert first >= borderline, (k, a, b, ma, mb)
+    assert flips <= len(its) // 8, flips
+
+
 CASES = ["p3_fmg1", "p3_fmg2", "p3_cascade", "p3_predictor", "p3_constant", "h3_fmg1", "h3_fmg2", "h3_cascade",
          "i3_fmg1"]
 
@@ -58,11 +79,12 @@ def test_three_level_step(rt, golden_ml, case):
     assert len(h.levels) == 3
     n0 = rt.status()[2]
     sol = mlsdc.run_mlsdc(h, G[f"{case}_u0"], 0.0, float(G[f"{case}_dt"]), 3, strategy=cfg[1], c_fmg=cfg[2])
-    its = rt.cg_log()[0][n0:].tolist()
+    its, margins = rt.cg_log()
+    its, margins = its[n0:].tolist(), margins[n0:].tolist()
     rt.raise_on_failure()
-    ref_its = G[f"{case}_pcg_iters1"].tolist()
-    assert len(its) == len(ref_its) and sum(its) == sum(ref_its)
-    assert its == ref_its
+    ref_its, ref_margins = G[f"{case}_pcg_iters1"].tolist(), G[f"{case}_pcg_margins1"].tolist()
+    assert len(its) == len(ref_its)
+    assert_same_iterations(its, margins, ref_its, ref_margins)
     assert l2rel(sol.u[-1], G[f"{case}_pcg_u1"]) < 1e-11
     assert l2rel(sol.u[-1], G[f"{case}_lu_u1"]) < 1e-9
 
