@@ -223,7 +223,7 @@ def cpu_rate(w, budget_s, threads, max_steps=10 ** 6, warmup=1):
         from oracle import dg2d, sweeper as osw, workloads
         from paper_2504_18526_b200.dgsem import compute_delta
         ws = dataclasses.replace(w, nex=16, ney=16)
-        h, _ = workloads.build_hierarchy_2d(lambda: dg2d.Euler2D(ws.gamma, ws.nu), 0.0, ws.length, 0.0, ws.ly,
+        h, _ = workloads.build_hierarchy_2d(lambda: workloads.problem2d(ws), 0.0, ws.length, 0.0, ws.ly,
                                             ws.nex, ws.ney, ws.p_coarse, ws.p_fine, ws.m_coarse, ws.m_fine)
         X, Y = h.levels[-1].ctx.nodes()
         u = ws.initial_state(X, Y)
@@ -322,7 +322,7 @@ def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True, e
 
         def make_op(P):
             mesh = dgsem2d.Mesh2D(0.0, w.length, 0.0, w.ly, w.nex, w.ney, P)
-            return dgsem2d.DGOperator2D(mesh, dgsem2d.CompressibleEuler2D(w.gamma, w.nu), device=local)
+            return dgsem2d.DGOperator2D(mesh, w.gpu_problem(), device=local)
 
         hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
         X, Y = hier.fine.ctx.mesh.nodes_xy
@@ -454,7 +454,7 @@ def measure_part(w, args, torch, rt, rank, world, local, steps, warmup, emulate=
 
     def make_op(P):
         mesh = dgsem2d.Mesh2D(0.0, w.length, 0.0, w.ly, w.nex, w.ney, P)
-        return dgsem2d.DGOperator2D(mesh, dgsem2d.CompressibleEuler2D(w.gamma, w.nu), device=local, partition=part)
+        return dgsem2d.DGOperator2D(mesh, w.gpu_problem(), device=local, partition=part)
 
     hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
     fine = hier.fine.ctx

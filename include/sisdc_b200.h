@@ -42,9 +42,11 @@ enum sisdc_status {
 
 enum sisdc_problem {
   SISDC_CONVDIFF = 0, SISDC_BURGERS = 1,        /* 1-D, problems.py:25-82               */
-  SISDC_EULER2D = 2,                            /* 2-D Euler / NS (isotropic viscosity)  */
+  SISDC_EULER2D = 2,                            /* 2-D Euler (+ isotropic nu Laplacian)  */
   SISDC_ADVECTION2D = 3, SISDC_BURGERS2D = 4,   /* 2-D scalar (cross-dimension checks)   */
-  SISDC_CNS1D = 5                               /* 1-D CompressibleFlow, problems.py:160-240 */
+  SISDC_CNS1D = 5,                              /* 1-D CompressibleFlow, problems.py:160-240 */
+  SISDC_NS2D = 6                                /* 2-D compressible Navier-Stokes: Stokes stress +
+                                                   Fourier heat flux (desc nu = eta, prandtl)  */
 };
 enum sisdc_bc { SISDC_PERIODIC = 0, SISDC_DIRICHLET = 1 };       /* Mesh1D.bc         */
 enum sisdc_scheme { SISDC_EULER = 0, SISDC_SI1 = 1, SISDC_SI2 = 2 }; /* integrators.py:26 */
@@ -89,17 +91,20 @@ typedef struct {
  * [x_left,x_right] x [y_bottom,y_top] (BASELINE configs 3-5; the reference is
  * 1-D only).  State layout (ncomp, ney, nex, P+1 [y], P+1 [x]).  Every
  * operator entry point below accepts a 2-D handle; the SI coefficient is the
- * isotropic (dt_m/2) lambda(u_b)^2 + nu, lambda = |v| + c. */
+ * isotropic (dt_m/2) lambda(u_b)^2 + nu (SISDC_NS2D: + eta/rho_b max(4/3,
+ * gamma/Pr)), lambda = |v| + c. */
 typedef struct {
   int nex, ney;
   int degree;        /* P, 1..8                                   */
   int ncomp;         /* 4 for Euler/NS, 1 for the scalar problems  */
-  int problem;       /* SISDC_EULER2D / SISDC_ADVECTION2D / SISDC_BURGERS2D */
+  int problem;       /* SISDC_EULER2D / SISDC_NS2D / SISDC_ADVECTION2D / SISDC_BURGERS2D */
   double x_left, x_right, y_bottom, y_top;
   double gamma;      /* ideal gas                                  */
-  double nu;         /* isotropic kinematic viscosity (0 => Euler) */
+  double nu;         /* EULER2D: isotropic kinematic viscosity (0 => Euler);
+                        NS2D: dynamic viscosity eta                  */
   double ax, ay;     /* advection velocity (SISDC_ADVECTION2D)     */
   double penalty;    /* SIP penalty constant (2.0)                 */
+  double prandtl;    /* NS2D Prandtl number (ABI version 2, appended) */
 } sisdc_op2d_desc;
 
 /* ----------------------------------------------------------- context */

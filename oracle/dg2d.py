@@ -66,6 +66,67 @@ class Euler2D:
         return np.sqrt(vx * vx + vy * vy) + np.sqrt(self.g * p / rho)
 
 
+class NS2D(Euler2D):
+    """2-D compressible Navier-Stokes in conservative variables: the Euler
+    flux plus the physical viscous flux (Stokes stress with dynamic viscosity
+    eta, Fourier heat flux with kappa = eta c_p / Pr), the 2-D generalisation
+    of the reference's ``CompressibleFlow.diffusion_coeff`` (``problems.py:
+    221-237``: nu = eta / rho, mu = 4/3 nu, gamma kappa = gamma nu / Pr, heat
+    flux in terms of the specific internal energy, R cancels).
+
+    F^x = (0, t_xx, t_xy, u t_xx + v t_xy + k rho e_x),
+    F^y = (0, t_xy, t_yy, u t_xy + v t_yy + k rho e_y),  k = gamma nu / Pr,
+    t_xx = nu (4/3 (m_x - u rho_x) - 2/3 (n_y - v rho_y)), t_yy likewise,
+    t_xy = nu ((m_y - u rho_y) + (n_x - v rho_x)),
+    rho e_. = E_. - E/rho rho_. - u (m_. - u rho_.) - v (n_. - v rho_.).
+    With v = 0 and y-invariant data this is the reference's 1-D A_d u_x.
+
+    The implicit (semi-implicit) part stays the isotropic SPD scalar
+    (dt_m/2) lambda^2 + nu_b, nu_b = eta / rho max(4/3, gamma / Pr) (the
+    spectral bound of the viscous matrices), shared by the four fields."""
+
+    viscous = True
+
+    def __init__(self, gamma=1.4, eta=0.0, prandtl=0.72):
+        super().__init__(gamma, 0.0)
+        self.eta, self.pr = float(eta), float(prandtl)
+
+    def _p(self, u):
+        rho = u[0]
+        return rho, u[1] / rho, u[2] / rho, u[3] / rho, self.eta / rho
+
+    def visc_flux(self, u, gx, gy):
+        rho, vx, vy, Es, nu = self._p(u)
+        k = self.g * nu / self.pr
+        dxm, dym = gx[1] - vx * gx[0], gy[1] - vx * gy[0]   # rho u_x, rho u_y (velocity u)
+        dxn, dyn = gx[2] - vy * gx[0], gy[2] - vy * gy[0]   # rho v_x, rho v_y
+        txx = nu * ((4.0 / 3.0) * dxm - (2.0 / 3.0) * dyn)
+        tyy = nu * ((4.0 / 3.0) * dyn - (2.0 / 3.0) * dxm)
+        txy = nu * (dym + dxn)
+        ex = gx[3] - Es * gx[0] - vx * dxm - vy * dxn
+        ey = gy[3] - Es * gy[0] - vx * dym - vy * dyn
+        z = np.zeros_like(rho)
+        Fx = np.stack([z, txx, txy, vx * txx + vy * txy + k * ex])
+        Fy = np.stack([z, txy, tyy, vx * txy + vy * tyy + k * ey])
+        return Fx, Fy
+
+    def apply_gnn(self, u, v, axis):
+        """G_nn v: the normal-normal viscous block at state u applied to v
+        (penalty and adjoint terms; the 1-D reference's A_d for axis 0)."""
+        rho, vx, vy, Es, nu = self._p(u)
+        k = self.g * nu / self.pr
+        a = v[1] - vx * v[0]
+        b = v[2] - vy * v[0]
+        r1 = nu * ((4.0 / 3.0) * a if axis == 0 else a)
+        r2 = nu * (b if axis == 0 else (4.0 / 3.0) * b)
+        r3 = vx * r1 + vy * r2 + k * (v[3] - Es * v[0] - vx * a - vy * b)
+        return np.stack([np.zeros_like(rho), r1, r2, r3])
+
+    def nu_si(self, u):
+        rho = u[0]
+        return (self.eta / rho) * max(4.0 / 3.0, self.g / self.pr)
+
+
 class Advection2D:
     """Scalar u_t + a.grad u = nu lap u (cross-dimension checks)."""
     ncomp = 1
@@ -201,6 +262,36 @@ class Op2D:
             out += self._from_end(-B / (0.5 * h * self.w), axis)
         return out.reshape(-1)
 
+    # physical viscous operator of NS2D (tensor SIP, see NS2D) -------------
+    def apply_viscous(self, u, t=0.0):
+        """f_visc = -M^-1 (B_x + B_y): per direction the reference's matrix
+        SIP (``dgsem.py:251-309``) with the full viscous flux (cross terms
+        included) as q, the normal-normal block G_nn in the penalty
+        mu0 {G_nn}[u] and in the adjoint lift (each side's own G_nn)."""
+        pr = self.prob
+        u5 = self.u5(u)
+        gx = (2.0 / self.dx) * np.einsum("ij,...bj->...bi", self.D, u5)
+        gy = (2.0 / self.dy) * np.einsum("ij,...jb->...ib", self.D, u5)
+        Fx, Fy = pr.visc_flux(u5, gx, gy)
+        out = np.zeros_like(u5)
+        for axis, h, F in ((0, self.dx, Fx), (1, self.dy, Fy)):
+            ue = self._to_end(u5, axis)
+            Fe = self._to_end(F, axis)
+            s = 2.0 / h
+            mu0 = self.penalty * self.p1 ** 2 / h
+            B = np.einsum("ki,k,...ek->...ei", self.D, self.w, Fe)
+            um, up = ue[..., :, -1], np.roll(ue, -1, axis=-2)[..., :, 0]
+            qm, qp = Fe[..., :, -1], np.roll(Fe, -1, axis=-2)[..., :, 0]
+            jump = um - up
+            gm, gp = pr.apply_gnn(um, jump, axis), pr.apply_gnn(up, jump, axis)
+            G = mu0 * (0.5 * (gm + gp)) - 0.5 * (qm + qp)
+            B[..., -1] += G
+            B[..., 0] -= np.roll(G, 1, axis=-1)
+            B -= s * (0.5 * gm)[..., None] * self.D[-1]
+            B -= s * np.roll(0.5 * gp, 1, axis=-1)[..., None] * self.D[0]
+            out += self._from_end(-B / (0.5 * h * self.w), axis)
+        return out.reshape(-1)
+
     def stiffness_diag(self, C):
         """diag of M * (-apply_diffusion) per node (shape (n,)), closed form."""
         C5 = self._coef5(C)
@@ -224,7 +315,9 @@ class Op2D:
     # rhs / SI coefficient / implicit solve --------------------------------
     def eval_rhs(self, u, t=0.0):
         out = self.apply_convection(u, t)
-        if self.prob.nu > 0:
+        if getattr(self.prob, "viscous", False):
+            out = out + self.apply_viscous(u, t)
+        elif self.prob.nu > 0:
             out = out + self.apply_diffusion(self.prob.nu, u, t)
         if not np.all(np.isfinite(out)):
             bad = ~np.isfinite(out.reshape(self.nc, self.ney * self.nex, -1))
@@ -235,6 +328,8 @@ class Op2D:
     def modified_coeff(self, u_b, dt_m, scheme="si2"):
         lam = self.prob.max_speed(self.u5(u_b))
         c = 0.5 * dt_m * (lam * lam)
+        if getattr(self.prob, "viscous", False):
+            return c + self.prob.nu_si(self.u5(u_b))
         return c + self.prob.nu if self.prob.nu > 0 else c
 
     def implicit_solve(self, C, a, rhs, t=0.0):

@@ -40,3 +40,11 @@ def build_hierarchy_2d(make_problem2d, x0, x1, y0, y1, nex, ney, p_coarse, p_fin
     rc, rf = sweeper.Rule("radau_right", m_coarse), sweeper.Rule("radau_right", m_fine)
     levels = [sweeper.Lev(cc, rc), sweeper.Lev(cf, rf)]
     return sweeper.Hier(levels, [dg2d.PTransfer2D(cc, cf, rc, rf)], n_coarse, 1, "incremental", True), log
+
+
+def problem2d(w):
+    """Oracle physics of a configs.Workload2D: NS2D (eta, Pr) when viscous, else Euler2D."""
+    from . import dg2d
+    if w.eta > 0:
+        return dg2d.NS2D(w.gamma, w.eta, w.prandtl)
+    return dg2d.Euler2D(w.gamma, 0.0)

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SISDC_LIB", os.path.join(HERE, "libsisdc_b200.so"))   # override: A/B experiments
 
 OK, ERR_ARG, ERR_CUDA, ERR_NONFINITE, ERR_NOCONV, ERR_UNSUPPORTED = range(6)
-CONVDIFF, BURGERS, EULER2D, ADVECTION2D, BURGERS2D, CNS1D = 0, 1, 2, 3, 4, 5
+CONVDIFF, BURGERS, EULER2D, ADVECTION2D, BURGERS2D, CNS1D, NS2D = 0, 1, 2, 3, 4, 5, 6
 PERIODIC, DIRICHLET = 0, 1
 SCHEMES = {"euler": 0, "si1": 1, "si2": 2}
 COEF_NONE, COEF_CONST, COEF_FIELD, COEF_SI, COEF_PHYS, COEF_MATRIX = range(6)
@@ -38,7 +38,7 @@ class Op2DDesc(C.Structure):
     _fields_ = [("nex", C.c_int), ("ney", C.c_int), ("degree", C.c_int), ("ncomp", C.c_int), ("problem", C.c_int),
                 ("x_left", C.c_double), ("x_right", C.c_double), ("y_bottom", C.c_double), ("y_top", C.c_double),
                 ("gamma", C.c_double), ("nu", C.c_double), ("ax", C.c_double), ("ay", C.c_double),
-                ("penalty", C.c_double)]
+                ("penalty", C.c_double), ("prandtl", C.c_double)]
 
 
 class Op1DDesc(C.Structure):

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsisdc_b200.so")
-SOURCES = ["abi.cu", "ops1d.cu", "cg1d.cu", "cns1d.cu", "ops2d.cu", "part2d.cu"]
+SOURCES = ["abi.cu", "ops1d.cu", "cg1d.cu", "cns1d.cu", "ops2d.cu", "part2d.cu", "visc2d.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -117,7 +117,8 @@ class Workload2D:
     length: float
     seed: int
     gamma: float = 1.4
-    nu: float = 0.0
+    eta: float = 0.0          # dynamic viscosity (rho = 1: 1/Re); 0 -> Euler
+    prandtl: float = 0.72
     mach: float = 0.1
     cfl: float = 1.0
     n_cycles: int = 3
@@ -127,6 +128,14 @@ class Workload2D:
     @property
     def ncomp(self):
         return 4
+
+    def gpu_problem(self):
+        """CompressibleNS2D (Stokes stress + Fourier heat flux, eta, Pr) for the
+        viscous configs, CompressibleEuler2D for cfg3."""
+        from . import dgsem2d
+        if self.eta > 0:
+            return dgsem2d.CompressibleNS2D(self.gamma, self.eta, self.prandtl)
+        return dgsem2d.CompressibleEuler2D(self.gamma, 0.0)
 
     @property
     def ly(self):
@@ -176,8 +185,8 @@ class Workload2D:
 
 
 CFG3 = Workload2D("cfg3_euler_vortex_128x128_P7", "vortex", 128, 128, 7, 3, 4, 2, 10.0, seed=3)
-CFG4 = Workload2D("cfg4_ns_shear_256x256_P7", "shear", 256, 256, 7, 3, 5, 3, TWO_PI, seed=4, nu=1e-4)
-CFG5 = Workload2D("cfg5_ns_shear_1024x1024_P7", "shear", 1024, 1024, 7, 3, 5, 3, TWO_PI, seed=5, nu=1e-4)
+CFG4 = Workload2D("cfg4_ns_shear_256x256_P7", "shear", 256, 256, 7, 3, 5, 3, TWO_PI, seed=4, eta=1e-4)
+CFG5 = Workload2D("cfg5_ns_shear_1024x1024_P7", "shear", 1024, 1024, 7, 3, 5, 3, TWO_PI, seed=5, eta=1e-4)
 WORKLOADS.update({"cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5})
 
 

@@ -1,5 +1,6 @@
 // C ABI of libsisdc_b200.so: contexts, operators, transfers and the exported
 // OperatorContext / sweep-stage entry points (include/sisdc_b200.h).
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -358,7 +359,8 @@ int op2d_create_impl(sisdc_ctx* x, const sisdc_op2d_desc* d, bool alloc_cg, sisd
   if (!(d->x_right > d->x_left) || !(d->y_top > d->y_bottom)) return c.fail(SISDC_ERR_ARG, "empty domain");
   if (d->nex < 1 || d->ney < 1 || d->degree < 1) return c.fail(SISDC_ERR_ARG, "need elements and degree >= 1");
   if (d->degree + 1 > 9) return c.fail(SISDC_ERR_UNSUPPORTED, "2-D degree above 8");
-  const bool euler = d->problem == SISDC_EULER2D;
+  const bool euler = d->problem == SISDC_EULER2D || d->problem == SISDC_NS2D;
+  if (d->problem == SISDC_NS2D && !(d->prandtl > 0.0)) return c.fail(SISDC_ERR_ARG, "Prandtl number must be positive");
   if (!euler && d->problem != SISDC_ADVECTION2D && d->problem != SISDC_BURGERS2D)
     return c.fail(SISDC_ERR_ARG, "unknown 2-D problem");
   if ((euler && d->ncomp != 4) || (!euler && d->ncomp != 1)) return c.fail(SISDC_ERR_ARG, "ncomp does not match the problem");
@@ -393,6 +395,8 @@ int op2d_create_impl(sisdc_ctx* x, const sisdc_op2d_desc* d, bool alloc_cg, sisd
   v.dx = dx; v.dy = dy; v.sx = 2.0 / dx; v.sy = 2.0 / dy;
   v.mux = d->penalty * p1 * p1 / dx; v.muy = d->penalty * p1 * p1 / dy;
   v.gamma = d->gamma; v.nu = d->nu; v.ax = d->ax; v.ay = d->ay;
+  v.pr = d->problem == SISDC_NS2D ? d->prandtl : 1.0;
+  v.nsi = d->problem == SISDC_NS2D ? std::max(4.0 / 3.0, d->gamma / d->prandtl) : 0.0;
   v.nu_art = nullptr;
   cudaError_t e = cudaMalloc(&op->d_tab, tab.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(op->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);

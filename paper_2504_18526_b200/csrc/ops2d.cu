@@ -1455,11 +1455,12 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
         for (int q = 0; q < NC_MAX; ++q) st[q] = q < NC ? ws[W::UPO + q * W::NP + g * RP + n0 + i] : 1.0;
         const double lam = lam_max2d(op, st);
         const double half = 0.5 * dtm * (lam * lam);
-        ws[W::CSI + g * RP + n0 + i] = has_phys ? half + ph : half;
+        ws[W::CSI + g * RP + n0 + i] = op.problem == SISDC_NS2D ? half + (op.nu / st[0]) * op.nsi   // coef2d
+                                                                : (has_phys ? half + ph : half);
       }
       const double lam = lam_max2d(op, upf);
       const double half = 0.5 * dtm * (lam * lam);
-      ws[W::CFS + lane] = has_phys ? half + ph : half;
+      ws[W::CFS + lane] = op.problem == SISDC_NS2D ? half + (op.nu / upf[0]) * op.nsi : (has_phys ? half + ph : half);
     }
     // Rusanov fluxes at this lane's face node for u_m (and u_{m-1})
     {
@@ -2288,6 +2289,8 @@ int launch2_conv(Ctx* c, const Op2DDev& op, const double* u, double* out) {
   return c->after_launch("k2_conv");
 }
 int launch2_sip(Ctx* c, const Op2DDev& op, CoefDev k, const double* u, double* out) {
+  if (op.problem == SISDC_NS2D && k.kind == SISDC_COEF_PHYS)   // the physical term is the NS viscous operator
+    return launch2_visc(c, op, u, out, 0, 1, 0);
   SISDC_P1_SWITCH(op.p1, {
     set_smem<P1>(k2_sip<P1>);
     k2_sip<P1><<<grid2<P1>(op), Blk<P1>::NT, smem2<P1>(), c->stream>>>(op, k, u, out);
@@ -2323,13 +2326,15 @@ int launch2_node_eval(Ctx* c, const Op2DDev& op, int mode, int scheme, int M, in
     const long long need = (ne + EV_WARPS - 1) / EV_WARPS;
     if (gx > need) gx = need;
     k2_eval8<4><<<dim3((unsigned)gx, m_count), EV_WARPS * 32, smem, c->stream>>>(op, a);
-    return c->after_launch("k2_eval8");
+    if (int rc = c->after_launch("k2_eval8")) return rc;
+    return launch2_visc(c, op, u, f, m_first, m_count, 1);   // NS2D: f += physical viscous term
   }
   SISDC_P1_SWITCH(op.p1, {
     set_smem<P1>(k2_node_eval<P1>);
     k2_node_eval<P1><<<grid2<P1>(op, m_count), Blk<P1>::NT, smem2<P1>(), c->stream>>>(op, a);
   });
-  return c->after_launch("k2_node_eval");
+  if (int rc = c->after_launch("k2_node_eval")) return rc;
+  return launch2_visc(c, op, u, f, m_first, m_count, 1);   // NS2D: f += physical viscous term
 }
 int launch2_stage(Ctx* c, const Op2DDev& op, const double* base, const double* conv_in, double dt_m,
                   const double* f_old, int M, const double* w_row, double dt, const double* g,

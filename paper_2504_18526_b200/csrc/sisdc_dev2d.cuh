@@ -21,7 +21,8 @@ struct Op2DDev {
   long long ns;          // node-array stride: u[m] = u + m * ns (n unless partitions are concatenated)
   int problem;
   double dx, dy, sx, sy, mux, muy;
-  double gamma, nu, ax, ay;
+  double gamma, nu, ax, ay;   // NS2D: nu = dynamic viscosity eta
+  double pr, nsi;        // NS2D: Prandtl number, max(4/3, gamma / Pr) (SI coefficient bound)
   const double* tab;     // 1-D element tables (TabOff layout)
   const double* nu_art;  // per element (ney*nex) or nullptr
 };
@@ -51,9 +52,12 @@ __device__ __forceinline__ int ynb(const Op2DDev& op, int sy, int d) {
   return op.row0 ? sy + d : wrapi(sy + d, op.ney);
 }
 
-// physics (Euler / NS isotropic, scalar advection, scalar Burgers along x) --
+// physics (Euler / NS, scalar advection, scalar Burgers along x) -----------
+__device__ __forceinline__ bool euler_like(const Op2DDev& op) {
+  return op.problem == SISDC_EULER2D || op.problem == SISDC_NS2D;
+}
 __device__ __forceinline__ void flux2d(const Op2DDev& op, const double* s, int axis, double* f) {
-  if (op.problem == SISDC_EULER2D) {
+  if (euler_like(op)) {
     const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
     const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
     const double vn = axis == 0 ? vx : vy;
@@ -68,7 +72,7 @@ __device__ __forceinline__ void flux2d(const Op2DDev& op, const double* s, int a
   }
 }
 __device__ __forceinline__ double speed2d(const Op2DDev& op, const double* s, int axis) {
-  if (op.problem == SISDC_EULER2D) {
+  if (euler_like(op)) {
     const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
     const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
     return fabs(axis == 0 ? vx : vy) + sqrt(op.gamma * p / rho);
@@ -77,7 +81,7 @@ __device__ __forceinline__ double speed2d(const Op2DDev& op, const double* s, in
   return axis == 0 ? fabs(s[0]) : 0.0;
 }
 __device__ __forceinline__ double lam_max2d(const Op2DDev& op, const double* s) {
-  if (op.problem == SISDC_EULER2D) {
+  if (euler_like(op)) {
     const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
     const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
     return sqrt(vx * vx + vy * vy) + sqrt(op.gamma * p / rho);
@@ -87,7 +91,13 @@ __device__ __forceinline__ double lam_max2d(const Op2DDev& op, const double* s) 
 }
 
 // coefficient at a node (element eg = ey*nex+ex, in-field node index) --------
+// (NS2D: the physical viscous term is the tensor operator of visc2d.cu, not a
+// scalar coefficient, so its scalar physical coefficient is zero)
 __device__ __forceinline__ bool phys2d(const Op2DDev& op, int eg, double& c) {
+  if (op.problem == SISDC_NS2D) {
+    c = 0.0;
+    return false;
+  }
   if (op.nu_art) {
     c = (op.nu > 0.0 ? op.nu : 0.0) + op.nu_art[eg];
     return true;
@@ -106,6 +116,7 @@ __device__ __forceinline__ double coef2d(const Op2DDev& op, const CoefDev& k, in
       for (int c = 0; c < NC_MAX; ++c) s[c] = c < op.nc ? k.ptr[nidx(op, c, ey, ex, j, i)] : 1.0;
       const double lam = lam_max2d(op, s);
       const double half = 0.5 * k.value * (lam * lam);
+      if (op.problem == SISDC_NS2D) return half + (op.nu / s[0]) * op.nsi;   // oracle NS2D.nu_si
       double ph;
       return phys2d(op, eg, ph) ? half + ph : half;
     }

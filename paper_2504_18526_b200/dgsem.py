@@ -147,7 +147,7 @@ class DGOperator:
         kind = {"convdiff": _lib.CONVDIFF, "burgers": _lib.BURGERS, "cns": _lib.CNS1D}[problem.kind]
         self.is_cns = problem.kind == "cns"
         self.dirichlet = mesh.bc == "dirichlet"
-        self._btimes = set()
+        self._btimes = {}   # insertion-ordered mirror of the library's trace table (abi.cu set_boundary)
         self._desc = _lib.Op1DDesc(mesh.n_elem, mesh.degree, self.ncomp,
                                    _lib.DIRICHLET if self.dirichlet else _lib.PERIODIC, kind,
                                    float(mesh.x_left), float(mesh.x_right), float(getattr(problem, "speed", 0.0)),
@@ -248,7 +248,7 @@ class DGOperator:
         library (dgsem.py:212-216): host evaluation, no device work."""
         if not self.dirichlet:
             return
-        new = [float(t) for t in times if float(t) not in self._btimes]
+        new = list(dict.fromkeys(float(t) for t in times if float(t) not in self._btimes))
         if not new:
             return
         gl, gr = zip(*[self.problem.boundary_state(t) for t in new])
@@ -257,9 +257,10 @@ class DGOperator:
         la, lp = _lib.darr([float(v) for g in gl for v in np.asarray(g, dtype=float).reshape(-1)[:nc]])
         ra, rp = _lib.darr([float(v) for g in gr for v in np.asarray(g, dtype=float).reshape(-1)[:nc]])
         self.rt.check(self.lib.sisdc_op1d_set_boundary(self.h, len(new), tp, lp, rp), "set_boundary")
-        self._btimes.update(new)
-        if len(self._btimes) > 3000:
-            self._btimes = set(new)
+        for t in new:
+            self._btimes[t] = None
+        if len(self._btimes) > 4096:   # the library keeps its 1024 most recent times past 4096 (same rule)
+            self._btimes = dict.fromkeys(list(self._btimes)[-1024:])
 
     # ---------------------------------------------------------- operators
     def _out(self, out):

@@ -83,6 +83,30 @@ class CompressibleEuler2D:
         self.gamma, self.nu = float(gamma), float(nu)
 
 
+class CompressibleNS2D:
+    """2-D compressible Navier-Stokes, ideal gas: the Euler flux plus the
+    physical viscous flux with dynamic viscosity ``eta`` (Stokes stress) and
+    Fourier heat flux with Prandtl number ``prandtl`` -- the 2-D
+    generalisation of the reference's ``CompressibleFlow`` viscous term
+    (``problems.py:221-237``; restated in ``oracle/dg2d.py`` ``NS2D``).  The
+    semi-implicit coefficient is the isotropic scalar (dt_m/2) lambda^2 +
+    eta/rho max(4/3, gamma/Pr) shared by the four fields (SPD: CG-solvable)."""
+    ncomp = 4
+    is_linear = False
+    source = None
+    kind = "ns2d"
+
+    def __init__(self, gamma: float = 1.4, eta: float = 0.0, prandtl: float = 0.72):
+        if gamma <= 1.0:
+            raise ValueError("gamma must exceed 1")
+        if eta < 0:
+            raise ValueError("viscosity must be nonnegative")
+        if prandtl <= 0:
+            raise ValueError("Prandtl number must be positive")
+        self.gamma, self.eta, self.prandtl = float(gamma), float(eta), float(prandtl)
+        self.nu = self.eta   # the descriptor's viscosity slot carries eta for NS2D
+
+
 class Advection2D:
     ncomp = 1
     is_linear = True
@@ -103,7 +127,7 @@ class Burgers2D:
         self.nu = float(nu)
 
 
-_KIND = {"euler2d": _lib.EULER2D, "advection2d": _lib.ADVECTION2D, "burgers2d": _lib.BURGERS2D}
+_KIND = {"euler2d": _lib.EULER2D, "ns2d": _lib.NS2D, "advection2d": _lib.ADVECTION2D, "burgers2d": _lib.BURGERS2D}
 
 
 def rank_rows(ney: int, nranks: int, rank: int):
@@ -237,7 +261,8 @@ class DGOperator2D:
         d = _lib.Op2DDesc(mesh.nex, mesh.ney, mesh.degree, self.ncomp, _KIND[problem.kind],
                           float(mesh.x_left), float(mesh.x_right), float(mesh.y_bottom), float(mesh.y_top),
                           float(getattr(problem, "gamma", 1.4)), float(problem.nu),
-                          float(getattr(problem, "ax", 0.0)), float(getattr(problem, "ay", 0.0)), float(penalty_const))
+                          float(getattr(problem, "ax", 0.0)), float(getattr(problem, "ay", 0.0)), float(penalty_const),
+                          float(getattr(problem, "prandtl", 1.0)))
         self._desc = d
         h = C.c_void_p()
         self.parts = None
@@ -327,6 +352,9 @@ class DGOperator2D:
 
     def modified_diffusion_matrix(self, u_b, dt_m: float, scheme: str):
         if scheme == "euler":
+            if self.problem.kind == "ns2d":
+                raise ValueError("the 'euler' substep scheme needs the (non-SPD) NS viscous operator in the implicit "
+                                 "solve; NS2D runs the si1 / si2 schemes")
             return self.problem.nu if self.problem.nu > 0 else None
         if scheme not in ("si1", "si2"):
             raise ValueError(f"unknown scheme {scheme!r}")
@@ -344,6 +372,18 @@ class DGOperator2D:
         u = self.rt.to_device(u)
         out = self._out(out)
         self.rt.check(self.lib.sisdc_apply_diffusion(self.h, c, u.data_ptr(), float(t), out.data_ptr()), "apply_diffusion")
+        return out
+
+    def apply_viscous(self, u, t: float = 0.0, out=None):
+        """NS2D physical viscous term (Stokes stress + heat flux; oracle
+        ``Op2D.apply_viscous``): ``sisdc_apply_diffusion`` with the physical
+        coefficient kind."""
+        if self.problem.kind != "ns2d":
+            raise ValueError("apply_viscous is the NS2D viscous operator")
+        u = self.rt.to_device(u)
+        out = self._out(out)
+        self.rt.check(self.lib.sisdc_apply_diffusion(self.h, Coef(_lib.COEF_PHYS, 0.0, None), u.data_ptr(), float(t),
+                                                     out.data_ptr()), "apply_viscous")
         return out
 
     def eval_rhs(self, u, t: float = 0.0, out=None):

@@ -45,7 +45,7 @@ def ops(w, P, partition):
     from paper_2504_18526_b200 import dgsem2d
     L = w.length
     mesh = dgsem2d.Mesh2D(0.0, L, 0.0, L, w.nex, w.ney, P)
-    prob = dgsem2d.CompressibleEuler2D(w.gamma, w.nu)
+    prob = w.gpu_problem()
     one = dgsem2d.DGOperator2D(mesh, prob)
     part = dgsem2d.DGOperator2D(mesh, prob, partition=partition)
     X, Y = mesh.nodes_xy
@@ -134,7 +134,7 @@ def run_step(w, partition, rt):
     from paper_2504_18526_b200 import dgsem, dgsem2d, mlsdc
     L = w.length
     mk = lambda P: dgsem2d.DGOperator2D(dgsem2d.Mesh2D(0.0, L, 0.0, L, w.nex, w.ney, P),
-                                        dgsem2d.CompressibleEuler2D(w.gamma, w.nu), partition=partition)
+                                        w.gpu_problem(), partition=partition)
     h = mlsdc.build_p_hierarchy(mk, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
     X, Y = h.fine.ctx.mesh.nodes_xy
     u0 = w.initial_state(X, Y)

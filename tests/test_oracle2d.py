@@ -60,3 +60,66 @@ def test_euler_conservation_and_free_stream():
     const = np.stack([np.full(X.shape, 1.2), np.full(X.shape, 0.6), np.full(X.shape, -0.3),
                       np.full(X.shape, 3.0)]).reshape(-1)
     assert np.abs(op.apply_convection(const)).max() < 1e-12
+
+
+def _lift3(u1, ne, p1, ney):
+    """1-D (rho, rho u, E) on (ne, p1) -> y-invariant 2-D (rho, rho u, 0, E)."""
+    u3 = u1.reshape(3, ne, p1)
+    z = np.zeros_like(u3[0])
+    u4 = np.stack([u3[0], u3[1], z, u3[2]])
+    return np.broadcast_to(u4[:, None, :, None, :], (4, ney, ne, p1, p1)).reshape(-1)
+
+
+def _check_reduces(v2, ref1, ne, p1, ney, tol):
+    v = v2.reshape(4, ney, ne, p1, p1)
+    r3 = ref1.reshape(3, ne, p1)
+    for j in range(ney):
+        for k in range(p1):
+            for c2, c1 in ((0, 0), (1, 1), (3, 2)):
+                a, b = v[c2, j, :, k, :], r3[c1]
+                assert np.abs(a - b).max() <= tol * max(1e-300, np.abs(b).max()), (c2, j, k)
+            assert np.abs(v[2, j, :, k, :]).max() <= tol * np.abs(r3[1]).max() + 1e-300
+
+
+def test_ns2d_y_invariant_reduces_to_reference_cns(golden):
+    """NS2D / Euler2D on y-invariant data with v = 0 reproduce the reference's
+    1-D CompressibleFlow (problems.py:160-240): convection (Rusanov with
+    lambda = |v| + c), the physical viscous operator (matrix SIP with A_d,
+    dgsem.py:251-309) and eval_rhs, per field (rho v stays ~0)."""
+    G = golden["operators"]          # CompressibleFlow(eta=1e-3), 8 elements, P = 5 on [0, 1]
+    ne, P, ney = 8, 5, 2
+    p1 = P + 1
+    op = dg2d.Op2D(0.0, 1.0, 0.0, 0.7, ne, ney, P, dg2d.NS2D(1.4, 1e-3, 0.75))
+    u2 = _lift3(G["cns_u"], ne, p1, ney)
+    _check_reduces(op.apply_convection(u2), G["cns_conv"], ne, p1, ney, 1e-13)
+    _check_reduces(op.apply_viscous(u2), G["cns_diff"], ne, p1, ney, 1e-13)
+    _check_reduces(op.eval_rhs(u2), G["cns_rhs"], ne, p1, ney, 1e-13)
+    # the reference's acoustic wave (eta = 1e-5, Pr 0.75, 12 elements, P = 7): p ~ 1e3 against
+    # O(1e2) outputs, so the flux differences cancel ~10 digits (measured 7e-12 on rho u)
+    C = golden["cns"]
+    ne, P = 12, 7
+    p1 = P + 1
+    op = dg2d.Op2D(0.0, 1.0, 0.0, 0.3, ne, ney, P, dg2d.NS2D(1.4, 1e-5, 0.75))
+    u2 = _lift3(C["op_u"], ne, p1, ney)
+    _check_reduces(op.apply_convection(u2), C["op_conv"], ne, p1, ney, 2e-11)
+    _check_reduces(op.eval_rhs(u2), C["op_rhs"], ne, p1, ney, 2e-11)
+
+
+def test_ns2d_viscous_consistency():
+    """The NS viscous operator: zero on constant states, conserves mass and
+    momentum on a periodic mesh, and decays kinetic energy of a shear wave at
+    the Stokes rate nu k^2 (resolved mesh)."""
+    op = dg2d.Op2D(0.0, 2 * np.pi, 0.0, 2 * np.pi, 4, 4, 7, dg2d.NS2D(1.4, 1e-2, 0.72))
+    X, Y = op.nodes()
+    const = np.stack([np.full(X.shape, 1.1), np.full(X.shape, 0.3), np.full(X.shape, -0.2),
+                      np.full(X.shape, 2.5)]).reshape(-1)
+    assert np.abs(op.apply_viscous(const)).max() < 1e-12
+    rho = 1.0 + 0.1 * np.sin(X + 2 * Y)
+    u = np.stack([rho, rho * np.sin(Y), rho * 0.2 * np.cos(X), 2.5 + 0.1 * np.cos(X - Y)])
+    fv = op.apply_viscous(u.reshape(-1)).reshape(4, 4, 4, 8, 8)
+    for c in range(3):
+        assert abs(float((fv[c] * op.m2).sum())) < 1e-12
+    # shear wave rho = 1, u = sin y: d(rho u)/dt = nu u_yy = -nu sin y
+    sw = np.stack([np.ones(X.shape), np.sin(Y), np.zeros(X.shape), np.full(X.shape, 2.5)])
+    fv = op.apply_viscous(sw.reshape(-1)).reshape(4, 4, 4, 8, 8)
+    assert np.abs(fv[1] + 1e-2 * np.sin(Y)).max() < 1e-6

@@ -20,7 +20,7 @@ rt = get_runtime()
 rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=0)
 npart = int(os.environ.get("SISDC_PART", "0"))   # > 0: split CG of an R-partition operator
 op = dgsem2d.DGOperator2D(dgsem2d.Mesh2D(0.0, w.length, 0.0, w.length, w.nex, w.ney, P),
-                          dgsem2d.CompressibleEuler2D(w.gamma, w.nu),
+                          w.gpu_problem(),
                           partition=dgsem2d.Partition(npart) if npart > 0 else None)
 X, Y = op.mesh.nodes_xy
 u = op.scatter(w.initial_state(X, Y))

@@ -20,7 +20,7 @@ rt.set_cg(rtol=1e-14, maxit=1000, cluster_ctas=0)
 
 def make_op(P):
     mesh = dgsem2d.Mesh2D(0.0, w.length, 0.0, w.length, w.nex, w.ney, P)
-    return dgsem2d.DGOperator2D(mesh, dgsem2d.CompressibleEuler2D(w.gamma, w.nu))
+    return dgsem2d.DGOperator2D(mesh, w.gpu_problem())
 
 
 hier = mlsdc.build_p_hierarchy(make_op, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
