@@ -601,7 +601,10 @@ def run_ours(args):
     secondary = {}
     if world == 1 and args.also_2d and not is2d:
         torch.cuda.empty_cache()
-        r2 = measure(WORKLOADS["cfg4"], args, torch, rt, rank, world, local, args.steps, args.warmup)
+        # the secondaries honour --steps / --warmup up to a cap that keeps the default run within
+        # minutes (a cfg5 slab is ~7 s): their own "steps" / "warmup" keys say what was timed
+        r2 = measure(WORKLOADS["cfg4"], args, torch, rt, rank, world, local, min(args.steps, 20),
+                     min(args.warmup, 3))
         secondary["cfg4"] = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64", **r2,
                              "note": "BASELINE configs[3] (2-D Navier-Stokes shear layer 256^2, P 7/3, M 5/3), "
                                      "same contract as the main line; reported beside it because the headline "
@@ -610,8 +613,8 @@ def run_ours(args):
             # BASELINE configs[4], the scaling config, single domain (CUDA graph); at N > 1 it is the
             # headline, element-row partitioned over the ranks (strong scaling)
             torch.cuda.empty_cache()
-            r5 = measure(WORKLOADS["cfg5"], args, torch, rt, rank, world, local, args.steps, args.warmup,
-                         e2e_steps=3)
+            r5 = measure(WORKLOADS["cfg5"], args, torch, rt, rank, world, local, min(args.steps, 5),
+                         min(args.warmup, 3), e2e_steps=3)
             secondary["cfg5"] = {"metric": METRIC, "unit": UNIT, "higher_is_better": True, "dtype": "f64",
                                  "n_gpus": 1, "scaling": "strong", **r5,
                                  "note": "BASELINE configs[4] (1024^2 elements, P 7/3, 268M fine DOF): the "
