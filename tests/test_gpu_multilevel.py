@@ -133,11 +133,22 @@ def test_paper_table_rows_match_reference_cli(rt, golden_mls, case):
     h1, rows = parse(mine_i)
     h2, rrows = parse(G[f"{case}_iterations_csv"])
     assert h1 == h2 and len(rows) == len(rrows)
+    # Below FLOOR the error series is rounding noise of the implicit solves (the
+    # reference's SuperLU vs the pinned PCG), e.g. 3.6e-13 vs 8.6e-13 at CFL 32:
+    # there the stall index may differ, and entries only have to be below FLOOR too.
+    FLOOR = 1e-11
     for a, b in zip(rows, rrows):
-        assert a[:3] == b[:3] and a[4] == b[4], (a, b)     # cfl, n_steps, converged iteration, status
+        assert a[:2] == b[:2] and a[4] == b[4], (a, b)     # cfl, n_steps, status
+        if a[2] != b[2]:                                   # converged iteration
+            assert float(a[3]) < FLOOR and float(b[3]) < FLOOR, (a, b)
     h1, rows = parse(mine_e)
     h2, rrows = parse(G[f"{case}_errors_csv"])
-    assert h1 == h2 and len(rows) == len(rrows)
-    for a, b in zip(rows, rrows):
-        assert a[:3] == b[:3]
-        assert abs(float(a[3]) - float(b[3])) <= 1e-8 * abs(float(b[3])), (a, b)
+    assert h1 == h2
+    mine = {tuple(r[:3]): float(r[3]) for r in rows}
+    ref = {tuple(r[:3]): float(r[3]) for r in rrows}
+    for key in sorted(set(mine) | set(ref)):
+        if key in mine and key in ref:
+            ea, eb = mine[key], ref[key]
+            assert abs(ea - eb) <= 1e-8 * abs(eb) or (ea < FLOOR and eb < FLOOR), (key, ea, eb)
+        else:   # one series stopped earlier: only inside the noise floor
+            assert (mine.get(key, ref.get(key))) < FLOOR, key
