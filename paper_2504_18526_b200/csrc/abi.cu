@@ -413,7 +413,7 @@ int op2d_create_impl(sisdc_ctx* x, const sisdc_op2d_desc* d, bool alloc_cg, sisd
     *out = op;
     return SISDC_OK;
   }
-  const size_t ws = 6 * (size_t)v.n + 2 * (size_t)v.nn + 16 + 8 * (size_t)op->cg_blocks;
+  const size_t ws = cg2_ws_doubles(v, op->cg_blocks);
   e = cudaMalloc(&op->d_cgws, ws * sizeof(double));
   if (e != cudaSuccess) {
     rc = c.cuda(e, "op2d CG workspace");

@@ -585,6 +585,12 @@ struct Cg2Args {
   const struct CgPScal* sc;
   int px;              // split matvec: also advance p, x (p = u_prev + beta p, x += alpha p)
   int defer;           // split solve: p / x deferred to the matvec (P = 7), else in the update
+  // fused single-pass iteration (k2_cgf): the second (r, s, w) buffers and the
+  // setup-only mode of k2_cg (1: stop after setup 3 and leave the scalars in scal[2..7])
+  double* R2;
+  double* S2;
+  double* W2;
+  int mode;
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -1776,6 +1782,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   if (tot[1] == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
     for (long long t = gtid; t < op.n; t += nthr) A.x[t] = 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (A.mode == 1) A.scal[7] = 0.0;   // nothing left for k2_cgf
       int idx = atomicAdd(&A.status[2], 1);
       if (idx < A.log_cap) { A.log_it[idx] = 0; A.log_margin[idx] = 0.0; }
     }
@@ -1832,6 +1839,12 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   double rho = tot[2];
   double alpha = tot[0] / tot[1], beta = 0.0;
   double rgam = 1.0 / tot[0], ralpha = 1.0 / alpha;
+  if (A.mode == 1) {   // setup only: the iterations run in k2_cgf
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      A.scal[2] = thr; A.scal[3] = rho; A.scal[4] = alpha; A.scal[5] = rgam; A.scal[6] = ralpha; A.scal[7] = 1.0;
+    }
+    return;
+  }
   int k = 0;
   bool ok = true;
   const bool stampb = A.timing != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == G - 1);
@@ -1876,6 +1889,420 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
     alpha = al;
     beta = be;
     rgam = 1.0 / gn;
+    ralpha = 1.0 / al;
+    ++k;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int idx = atomicAdd(&A.status[2], 1);
+    if (idx < A.log_cap) {
+      A.log_it[idx] = ok ? k : -1;
+      A.log_margin[idx] = thr > 0.0 ? sqrt(rho / thr) : 0.0;
+    }
+    if (!ok) atomicAdd(&A.status[1], 1);
+  }
+}
+
+// ------------------------------------------------------------------------
+// P = 7 fused single-pass PCG iteration (k2_cgf).  k2_cg streams every vector
+// twice per iteration (phase A' then phase B: 13.5 vector passes = 108 B/DOF).
+// Here ONE pass per iteration does the vector update and the matvec:
+//   s' = w + beta s, r' = r - alpha s', u' = r' dinv, p = u + beta p,
+//   x += alpha p, w' = (M + a B2) u', partials (r',u'), (w',u'), (r',r')
+// -- 10.5 vector passes = 84 B/DOF.  w' at an element needs u' of its four face
+// neighbours, which do not exist in memory: every u' is REBUILT on chip from
+// (r, s, w, dinv) with the owner's exact operations (bitwise the same u', as
+// the 1-D cluster CG does for its halo); r, s, w are double-buffered across
+// iterations so that neighbours always read the previous iterate.
+//   A block marches a band of 8 element rows (one warp per row) along a strip
+// of SL elements of one field, one element column per step.  Warp y builds u'
+// of element (y, j+1) once -- into its private 3-slot ring (x-neighbours: the
+// ring holds columns j-1, j, j+1) and, transposed, into the block's ring RT,
+// where the warps of rows y-1 / y+1 read it as their top / bottom neighbour.
+// Only the two rows bordering the band are rebuilt redundantly (by a warp
+// that rotates with the step).  One block barrier per step.  Operands arrive
+// by TMA bulk copies (cp.async.bulk, one 512-byte run per element vector, five
+// per warp and step from one lane) on per-warp mbarriers, two steps ahead.
+template <int NC>
+struct Fz {
+  static constexpr int SL = 16;                     // strip length (elements)
+  static constexpr int NW = 8;                      // warps per block = rows per band
+  static constexpr int RP = 10, NP = 80, NN = 64;
+  // per-warp region (doubles)
+  static constexpr int RAW = 0;                     // [2 stages][r, s, w, dinv of column j+1 | cf of column j][64]
+  static constexpr int COEF = RAW + 2 * 5 * NN;     // [NP] own coefficient, rows padded to 10
+  static constexpr int CFN = COEF + NP;             // [32] neighbour face coefficients
+  static constexpr int RING = CFN + 32;             // [3][NP] u' of columns j-1, j, j+1 (rows padded to 10)
+  static constexpr int QX = RING + 3 * NP, QY = QX + NP, DOT = QY + NP, FCON = DOT + 32;
+  static constexpr int WARP = FCON + 64;
+  // block region
+  static constexpr int RT = NW * WARP;              // [3 slots][NW + 2 rows][64] u' transposed + swizzled
+  static constexpr int HRAW = RT + 3 * (NW + 2) * NN;   // [2 halo rows][2 stages][r, s, w, dinv][64]
+  static constexpr int RED = HRAW + 2 * 2 * 4 * NN; // [32][4] block reduction scratch
+  static constexpr int MBAR = RED + 128;            // [NW][2] own stages, [2][2] halo stages
+  static constexpr int SIZE = MBAR + 2 * NW + 4;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar2_init(uint32_t m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(m), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar2_expect(uint32_t m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar2_wait(uint32_t m, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(m),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on the mbarrier (UBLKCP)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const double* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+// wpe_sip for the fused pass: own element Ue and the x-neighbours UR / UL in
+// padded rows (ring slots), the y-neighbours UT / UB transposed and swizzled
+// (face lines are rows).  Same operations and order as wpe_sip.
+__device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, const double* Ue, const double* UR,
+                                       const double* UL, const double* UT, const double* UB, const double* Ce,
+                                       const double* cfn, double* QX, double* QY, double* DT, double* FC,
+                                       double& bx0, double& bx1, double& by0, double& by1) {
+  constexpr int RP = 10, P = 7;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, n0 = 2 * t;
+  double qx0 = 0.0, qx1 = 0.0, qy0 = 0.0, qy1 = 0.0;
+  dmma(qx0, qx1, Ue[g * RP + t], K.d0);
+  dmma(qx0, qx1, Ue[g * RP + 4 + t], K.d1);
+  dmma(qy0, qy1, K.d0, Ue[t * RP + g]);
+  dmma(qy0, qy1, K.d1, Ue[(4 + t) * RP + g]);
+  {
+    const double2 cg = *reinterpret_cast<const double2*>(Ce + g * RP + n0);
+    *reinterpret_cast<double2*>(QX + g * RP + n0) = make_double2(cg.x * (op.sx * qx0), cg.y * (op.sx * qx1));
+    *reinterpret_cast<double2*>(QY + g * RP + n0) = make_double2(cg.x * (op.sy * qy0), cg.y * (op.sy * qy1));
+  }
+  {
+    const int f = lane >> 3, k = lane & 7;
+    const double* ln = f == FR ? UR + k * RP : f == FL ? UL + k * RP : (f == FT ? UT : UB) + k * 8;
+    const int sw = f < FT ? 0 : (k >> 1);
+    double gd = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2 v = *reinterpret_cast<const double2*>(ln + 2 * (j ^ sw));
+      gd = fma(K.drow[2 * j], v.x, gd);
+      gd = fma(K.drow[2 * j + 1], v.y, gd);
+    }
+    DT[lane] = cfn[lane] * ((f < FT ? op.sx : op.sy) * gd);
+  }
+  __syncwarp();
+  bx0 = bx1 = by0 = by1 = 0.0;
+  dmma(bx0, bx1, QX[g * RP + t], K.w0);
+  dmma(bx0, bx1, QX[g * RP + 4 + t], K.w1);
+  dmma(by0, by1, K.w0, QY[t * RP + g]);
+  dmma(by0, by1, K.w1, QY[(4 + t) * RP + g]);
+  if (lane < 16) {
+    const bool yd = lane >= 8;
+    const int r = lane & 7;
+    const int up = yd ? P * RP + r : r * RP + P, u0 = yd ? r : r * RP;
+    const double jp = Ue[up] - (yd ? UT[nsw(r, 0)] : UR[r * RP]);
+    const double jm = (yd ? UB[nsw(r, P)] : UL[r * RP + P]) - Ue[u0];
+    const double cP = Ce[up], c0 = Ce[u0];
+    const double fcp = cfn[(yd ? 16 : 0) + r], fcm = cfn[(yd ? 24 : 8) + r];
+    const double qP = (yd ? QY : QX)[up], q0 = (yd ? QY : QX)[u0];
+    const double qnp = DT[(yd ? 16 : 0) + r], qnm = DT[(yd ? 24 : 8) + r];
+    const double mu = yd ? op.muy : op.mux, sc = yd ? op.sy : op.sx;
+    const double fp = -(0.5 * (qP + qnp)) + (mu * (0.5 * (cP + fcp))) * jp;
+    const double fm = -(0.5 * (qnm + q0)) + (mu * (0.5 * (fcm + c0))) * jm;
+    *reinterpret_cast<double4*>(FC + lane * 4) = make_double4(fp, fm, sc * ((0.5 * cP) * jp), sc * ((0.5 * c0) * jm));
+  }
+  __syncwarp();
+  {
+    const double4 rx = *reinterpret_cast<const double4*>(FC + g * 4);
+    if (n0 + 1 == P) bx1 += rx.x;
+    if (n0 == 0) bx0 -= rx.y;
+    bx0 -= rx.z * K.dPn[0];
+    bx1 -= rx.z * K.dPn[1];
+    bx0 -= rx.w * K.d0n[0];
+    bx1 -= rx.w * K.d0n[1];
+    const double4 ca = *reinterpret_cast<const double4*>(FC + (8 + n0) * 4);
+    const double4 cb = *reinterpret_cast<const double4*>(FC + (9 + n0) * 4);
+    if (g == P) { by0 += ca.x; by1 += cb.x; }
+    if (g == 0) { by0 -= ca.y; by1 -= cb.y; }
+    by0 -= ca.z * K.dPg;
+    by1 -= cb.z * K.dPg;
+    by0 -= ca.w * K.d0g;
+    by1 -= cb.w * K.d0g;
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
+  extern __shared__ double sm[];
+  using F = Fz<NC>;
+  cg::grid_group grid = cg::this_grid();
+  const Op2DDev& op = A.op;
+  constexpr int SL = F::SL, RP = F::RP, NP = F::NP, NW = F::NW;
+  const long long nn = op.nn;
+  const int G = gridDim.x;
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);   // warp-uniform for the compiler
+  double* ws = sm + warp * F::WARP;
+  double* red = sm + F::RED;
+  double* RT = sm + F::RT;
+  const uint32_t mb_own = smem_u32(reinterpret_cast<unsigned long long*>(sm + F::MBAR) + 2 * warp);   // + 8 stage
+  const uint32_t mb_halo = smem_u32(reinterpret_cast<unsigned long long*>(sm + F::MBAR) + 2 * NW);    // + 16 h + 8 stage
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2 * NW + 4; ++i) mbar2_init(smem_u32(reinterpret_cast<unsigned long long*>(sm + F::MBAR) + i), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (A.scal[7] == 0.0) return;   // b == 0: the setup kernel wrote x = 0 and logged the solve
+  const double thr = A.scal[2];
+  double rho = A.scal[3], alpha = A.scal[4], beta = 0.0, rgam = A.scal[5], ralpha = A.scal[6];
+  MmaLane K;
+  mma_lane_init(op, K);
+  double* slot0 = A.part;
+  double* slot1 = A.part + 4 * G;
+  const int g = lane >> 2, n0 = 2 * (lane & 3);
+  const int f = lane >> 3, kf = lane & 7;
+  const int fnode = f == FR ? kf * 8 : f == FL ? kf * 8 + 7 : f == FT ? kf : 56 + kf;   // neighbour's face node
+  const int tr0 = nsw(lane & 7, lane >> 3), tr1 = nsw(lane & 7, 4 + (lane >> 3));   // node v -> line v%8, pos v/8
+  // transposed position of this lane's own node pair (row g, columns n0, n0+1); odd rows store the second
+  // node first so that one store instruction hits all 16 bank pairs
+  const int ta = (g & 1) ? nsw(n0 + 1, g) : nsw(n0, g), tb = (g & 1) ? nsw(n0, g) : nsw(n0 + 1, g);
+  const int nstr = (op.nex + SL - 1) / SL, nbands = (op.ney + NW - 1) / NW;
+  const long long nunits = (long long)nbands * nstr * NC;
+  unsigned oc = 0, hc = 0;   // completed uses of this warp's own stages / of the halo stages (stage = use & 1)
+  int k = 0;
+  bool ok = true;
+  const bool stampb = A.timing != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == G - 1);
+  long long* tm = A.timing + (blockIdx.x == 0 ? 0 : 10);
+  const int maxit = A.dbg ? 10 : A.maxit;
+  while (rho > thr) {
+    if (k >= maxit) { ok = false; break; }
+    const bool stamp = stampb && k == 2;
+    if (stamp) tm[0] = tm[1] = tm[2] = gtimer();
+    const bool first = k == 0;
+    const double* const Ro = (k & 1) ? A.R2 : A.R;
+    const double* const So = (k & 1) ? A.S2 : A.S;
+    const double* const Wo = (k & 1) ? A.W2 : A.W;
+    double* const Rn = (k & 1) ? A.R : A.R2;
+    double* const Sn = (k & 1) ? A.S : A.S2;
+    double* const Wn = (k & 1) ? A.W : A.W2;
+    double ru = 0.0, rr = 0.0, wu = 0.0;
+    for (long long un = blockIdx.x; un < nunits; un += G) {
+      const int c = (int)(un % NC);
+      const long long tq = un / NC;
+      const int sx = (int)(tq % nstr), band = (int)(tq / nstr);
+      const int y0 = band * NW, nrows = op.ney - y0 < NW ? op.ney - y0 : NW;
+      const bool valid = warp < nrows;
+      const int ey = valid ? y0 + warp : y0;
+      const int x0 = sx * SL, x1 = x0 + SL < op.nex ? x0 + SL : op.nex;
+      // offsets in doubles fit 32 bits (checked by the launcher: n < 2^32)
+      const unsigned fo = (unsigned)(c * nn);
+      const unsigned rowC = (unsigned)ey * op.nex * 64u;
+      const unsigned rowT = (unsigned)(ey + 1 == op.ney ? 0 : ey + 1) * op.nex * 64u;
+      const unsigned rowB = (unsigned)(ey == 0 ? op.ney - 1 : ey - 1) * op.nex * 64u;
+      const unsigned hrow0 = (unsigned)(y0 + nrows == op.ney ? 0 : y0 + nrows) * op.nex * 64u;   // above the band
+      const unsigned hrow1 = (unsigned)(y0 == 0 ? op.ney - 1 : y0 - 1) * op.nex * 64u;            // below the band
+      const unsigned oC = fo + rowC + 2 * lane;
+      const unsigned cfb = (f == FT ? rowT : f == FB ? rowB : rowC) + fnode;   // this lane's face coefficient row
+      // own stage of step js: r, s, w, dinv of column js+1, cf of column js (js >= x0)
+      auto issue_own = [&](int js, unsigned use) {
+        if (lane == 0) {
+          const uint32_t mb = mb_own + 8u * (use & 1u);
+          const uint32_t dst = smem_u32(ws + F::RAW + (use & 1u) * 320);
+          int en = js + 1;
+          en = en < 0 ? op.nex - 1 : en >= op.nex ? 0 : en;
+          const unsigned e1 = fo + rowC + (unsigned)en * 64u;
+          const bool cf = js >= x0;
+          mbar2_expect(mb, cf ? 2560u : 2048u);
+          bulk_g2s(dst, Ro + e1, 512u, mb);
+          bulk_g2s(dst + 512u, So + e1, 512u, mb);
+          bulk_g2s(dst + 1024u, Wo + e1, 512u, mb);
+          bulk_g2s(dst + 1536u, A.DINV + (e1 - fo), 512u, mb);
+          if (cf) bulk_g2s(dst + 2048u, A.Cf + (rowC + (unsigned)js * 64u), 512u, mb);
+        }
+      };
+      // halo stage h (0 above, 1 below the band) of step js: r, s, w, dinv of column js+1
+      auto issue_halo = [&](int h, int js, unsigned use) {
+        if (lane == 0) {
+          const uint32_t mb = mb_halo + 16u * h + 8u * (use & 1u);
+          const uint32_t dst = smem_u32(sm + F::HRAW + (h * 2 + (use & 1u)) * 256);
+          const unsigned e1 = fo + (h ? hrow1 : hrow0) + (unsigned)(js + 1) * 64u;
+          mbar2_expect(mb, 2048u);
+          bulk_g2s(dst, Ro + e1, 512u, mb);
+          bulk_g2s(dst + 512u, So + e1, 512u, mb);
+          bulk_g2s(dst + 1024u, Wo + e1, 512u, mb);
+          bulk_g2s(dst + 1536u, A.DINV + (e1 - fo), 512u, mb);
+        }
+      };
+      auto cfn_load = [&](int col) {   // neighbour face coefficients of column col
+        const int exr = col + 1 == op.nex ? 0 : col + 1, exl = col == 0 ? op.nex - 1 : col - 1;
+        return A.Cf[cfb + (unsigned)(f == FR ? exr : f == FL ? exl : col) * 64u];
+      };
+      __syncthreads();   // the previous unit's last step has read RT
+      // halo steps: js + 1 in [x0, x1 - 1]; two uses ahead
+      if (valid) {
+        issue_own(x0 - 2, oc);
+        issue_own(x0 - 1, oc + 1);
+      }
+      if (warp == 0) {
+        issue_halo(0, x0 - 1, hc);
+        issue_halo(1, x0 - 1, hc);
+        if (x0 + 1 < x1) {
+          issue_halo(0, x0, hc + 1);
+          issue_halo(1, x0, hc + 1);
+        }
+      }
+      double cfn_reg = cfn_load(x0);
+      double2 pp = make_double2(0.0, 0.0), xx = pp;
+      int sl = 0;   // ring slot of column j - 1 (slots advance with j)
+      for (int j = x0 - 2; j < x1; ++j) {
+        const int jn = j + 1;
+        const bool own = jn >= x0 && jn < x1, sip = j >= x0;
+        const int sN = sl == 0 ? 2 : sl - 1;        // slot of column j + 1: (sl + 2) % 3
+        const int sJ = sl == 2 ? 0 : sl + 1;        // slot of column j
+        __syncthreads();   // every warp is past step j - 1: RT column j is complete, RT slot sN is free
+        if (valid) {
+          const unsigned gn = oC + (unsigned)jn * 64u;   // used inside the strip only
+          const double* raw = ws + F::RAW + (oc & 1u) * 320;
+          mbar2_wait(mb_own + 8u * (oc & 1u), (oc >> 1) & 1u);
+          {   // u' of column j + 1 (and, inside the strip, its s', r', p, x)
+            const double2 r = *reinterpret_cast<const double2*>(raw + 2 * lane);
+            double2 s = *reinterpret_cast<const double2*>(raw + 64 + 2 * lane);
+            const double2 w = *reinterpret_cast<const double2*>(raw + 128 + 2 * lane);
+            const double2 di = *reinterpret_cast<const double2*>(raw + 192 + 2 * lane);
+            if (first) s = make_double2(0.0, 0.0);
+            double2 sn, rn, uu;
+            sn.x = fma(beta, s.x, w.x);
+            sn.y = fma(beta, s.y, w.y);
+            rn.x = fma(-alpha, sn.x, r.x);
+            rn.y = fma(-alpha, sn.y, r.y);
+            uu.x = rn.x * di.x;
+            uu.y = rn.y * di.y;
+            *reinterpret_cast<double2*>(ws + F::RING + sN * NP + g * RP + n0) = uu;
+            if (own) {
+              double* rt = RT + (sN * (NW + 2) + warp) * 64;
+              rt[ta] = (g & 1) ? uu.y : uu.x;
+              rt[tb] = (g & 1) ? uu.x : uu.y;
+              *reinterpret_cast<double2*>(Sn + gn) = sn;
+              *reinterpret_cast<double2*>(Rn + gn) = rn;
+              ru = fma(rn.x, uu.x, ru);
+              rr = fma(rn.x, rn.x, rr);
+              ru = fma(rn.y, uu.y, ru);
+              rr = fma(rn.y, rn.y, rr);
+              pp.x = fma(beta, pp.x, r.x * di.x);   // p = u_prev + beta p, u_prev = r_old dinv
+              pp.y = fma(beta, pp.y, r.y * di.y);
+              xx.x = fma(alpha, pp.x, xx.x);
+              xx.y = fma(alpha, pp.y, xx.y);
+              __stcs(reinterpret_cast<double2*>(A.Pv + gn), pp);
+              __stcs(reinterpret_cast<double2*>(A.x + gn), xx);
+            }
+          }
+          if (sip) {   // coefficients of column j
+            *reinterpret_cast<double2*>(ws + F::COEF + g * RP + n0) =
+                *reinterpret_cast<const double2*>(raw + 256 + 2 * lane);
+            ws[F::CFN + lane] = cfn_reg;
+          }
+          __syncwarp();
+          if (j + 2 < x1) {   // this stage is free: refill it for step j + 2
+            issue_own(j + 2, oc + 2);
+          }
+          ++oc;
+        }
+        {   // register prefetches for the next step: p, x of column j + 2, face coefficients of column
+            // j + 1.  Unconditional (clamped columns): a load inside a branch makes the compiler wait
+            // for it at the join, which serialised the whole step on these loads
+          const int j2 = j + 2 < x0 ? x0 : j + 2 < x1 ? j + 2 : x1 - 1;
+          const unsigned g2 = oC + (unsigned)j2 * 64u;
+          pp = __ldcs(reinterpret_cast<const double2*>(A.Pv + g2));
+          xx = __ldcs(reinterpret_cast<const double2*>(A.x + g2));
+          cfn_reg = cfn_load(j + 1 < x0 ? x0 : j + 1 < x1 ? j + 1 : x1 - 1);
+        }
+        if (own) {   // u' of the rows above / below the band at column j + 1, by a warp that rotates with j
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (warp == ((j + 4 * h) & (NW - 1))) {
+              const double* raw = sm + F::HRAW + (h * 2 + (hc & 1u)) * 256;
+              mbar2_wait(mb_halo + 16u * h + 8u * (hc & 1u), (hc >> 1) & 1u);
+              double* rt = RT + (sN * (NW + 2) + NW + h) * 64;
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                const int v = lane + 32 * q;
+                const double s = first ? 0.0 : raw[64 + v];
+                const double sn = fma(beta, s, raw[128 + v]);
+                const double rn = fma(-alpha, sn, raw[v]);
+                rt[q ? tr1 : tr0] = rn * raw[192 + v];
+              }
+              __syncwarp();
+              if (j + 3 < x1) issue_halo(h, j + 2, hc + 2);
+            }
+          }
+          ++hc;
+        }
+        if (sip && valid) {
+          const double* Ue = ws + F::RING + sJ * NP;
+          const double* rtj = RT + sJ * (NW + 2) * 64;
+          double bx0, bx1, by0, by1;
+          fz_sip(op, K, Ue, ws + F::RING + sN * NP, ws + F::RING + sl * NP,
+                 rtj + (warp + 1 < nrows ? warp + 1 : NW) * 64, rtj + (warp > 0 ? warp - 1 : NW + 1) * 64,
+                 ws + F::COEF, ws + F::CFN, ws + F::QX, ws + F::QY, ws + F::DOT, ws + F::FCON, bx0, bx1, by0, by1);
+          const double2 v = *reinterpret_cast<const double2*>(Ue + g * RP + n0);
+          const double w0 = fma(A.a, fma(K.hwy, bx0, K.hwx[0] * by0), K.hh[0] * v.x);
+          const double w1 = fma(A.a, fma(K.hwy, bx1, K.hwx[1] * by1), K.hh[1] * v.y);
+          *reinterpret_cast<double2*>(Wn + (oC + (unsigned)j * 64u)) = make_double2(w0, w1);   // g * 8 + n0 == 2 lane
+          wu = fma(w0, v.x, wu);
+          wu = fma(w1, v.y, wu);
+          __syncwarp();   // scratch is rewritten by the next step
+        }
+        sl = sJ;
+      }
+    }
+    if (stamp) tm[3] = gtimer();
+    double* slot = (k & 1) ? slot1 : slot0;
+    {   // per-block partials -> slot[blockIdx]
+      double v0 = ru, v1 = wu, v2 = rr;
+      for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      __syncthreads();
+      if (lane == 0) { red[warp * 4] = v0; red[warp * 4 + 1] = v1; red[warp * 4 + 2] = v2; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+        for (int ww = 0; ww < NW; ++ww) { t0 += red[ww * 4]; t1 += red[ww * 4 + 1]; t2 += red[ww * 4 + 2]; }
+        slot[blockIdx.x * 4] = t0; slot[blockIdx.x * 4 + 1] = t1; slot[blockIdx.x * 4 + 2] = t2;
+      }
+    }
+    if (stamp) tm[4] = gtimer();
+    grid.sync();
+    if (stamp) tm[5] = gtimer();
+    double tot[3];
+    {   // every block sums all slots in the same fixed order
+      double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+      for (int b = threadIdx.x; b < G; b += blockDim.x) { v0 += slot[b * 4]; v1 += slot[b * 4 + 1]; v2 += slot[b * 4 + 2]; }
+      for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      __syncthreads();
+      if (lane == 0) { red[warp * 4] = v0; red[warp * 4 + 1] = v1; red[warp * 4 + 2] = v2; }
+      __syncthreads();
+      tot[0] = tot[1] = tot[2] = 0.0;
+      for (int ww = 0; ww < NW; ++ww) { tot[0] += red[ww * 4]; tot[1] += red[ww * 4 + 1]; tot[2] += red[ww * 4 + 2]; }
+    }
+    if (stamp) tm[6] = gtimer();
+    const double gn_ = tot[0];
+    const double be = gn_ * rgam;
+    const double al = gn_ / (tot[1] - be * (gn_ * ralpha));
+    rho = tot[2];
+    alpha = al;
+    beta = be;
+    rgam = 1.0 / gn_;
     ralpha = 1.0 / al;
     ++k;
   }
@@ -2259,6 +2686,29 @@ static cudaError_t cg_occupancy(int* per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k2_cg<P1, NC>, Blk<P1>::NT, smem_cg<P1, NC>());
 }
 
+// fused pass: resident blocks x SMs (at most the setup kernel's grid: the partial
+// slots are sized for it), capped by the (band, strip, field) units
+template <int NC>
+static cudaError_t launch_cgf(int device, void** args, const Op2DDev& op, int max_blocks, cudaStream_t st) {
+  using F = Fz<NC>;
+  constexpr int smem = (int)(sizeof(double) * F::SIZE);
+  static int resident = 0;
+  if (resident == 0) {
+    int per_sm = 0, sms = 0;
+    cudaError_t e = cudaFuncSetAttribute(k2_cgf<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_cgf<NC>, F::NW * 32, smem);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    resident = per_sm * sms;
+  }
+  long long nb = (long long)((op.ney + F::NW - 1) / F::NW) * ((op.nex + F::SL - 1) / F::SL) * NC;   // units
+  if (nb > resident) nb = resident;
+  if (nb > max_blocks) nb = max_blocks;
+  if (nb < 1) nb = 1;
+  return cudaLaunchCooperativeKernel((void*)k2_cgf<NC>, dim3((unsigned)nb), dim3(F::NW * 32), args, smem, st);
+}
+
 #define SISDC_P1_SWITCH(p1, ...)                                 \
   switch (p1) {                                                  \
     case 2: { constexpr int P1 = 2; __VA_ARGS__; } break;        \
@@ -2412,10 +2862,13 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
   A.Pv = p; p += op.n;
   A.S = p; p += op.n;
   A.U2 = p; p += op.n;
+  A.W2 = p; p += op.n;   // fused pass only (cg2_ws_doubles)
   A.DINV = p; p += op.nn;
   A.Cf = p; p += op.nn;
   A.scal = p; p += 16;
   A.part = p;
+  A.R2 = A.U2;           // fused pass: (r, s, w) double-buffered; u0 of the setup lives in the second s buffer
+  A.S2 = A.U;
   A.status = c->d_status; A.log_it = c->d_log_it; A.log_margin = c->d_log_margin; A.log_cap = c->log_cap;
   A.timing = c->d_timing;
   if (c->d_timing) {
@@ -2424,12 +2877,31 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
   }
   void* args[] = {&A};
   cudaError_t e = cudaSuccess;
+  // P = 7: setup by k2_cg (mode 1), iterations by the fused single-pass kernel
+  // (SISDC_CG_FUSED=0 keeps the two-phase iteration for A/B runs)
+  static const bool fused_on = [] {
+    const char* v = getenv("SISDC_CG_FUSED");
+    return !(v && v[0] == '0');
+  }();
+  const bool fused = fused_on && op.p1 == 8 && op.row0 == 0;
+  if (fused) A.mode = 1;
   SISDC_P1_SWITCH(op.p1, {
     if (op.nc == 4) e = launch_cg_coop<P1, 4>(args, nblocks, c->stream);
     else e = launch_cg_coop<P1, 1>(args, nblocks, c->stream);
   });
   if (e != cudaSuccess) return c->cuda(e, "k2_cg cooperative launch");
+  if (fused) {
+    int rc = c->after_launch("k2_cg (setup)");
+    if (rc) return rc;
+    e = op.nc == 4 ? launch_cgf<4>(c->device, args, op, nblocks, c->stream)
+                   : launch_cgf<1>(c->device, args, op, nblocks, c->stream);
+    if (e != cudaSuccess) return c->cuda(e, "k2_cgf cooperative launch");
+    return c->after_launch("k2_cgf");
+  }
   return c->after_launch("k2_cg");
+}
+size_t cg2_ws_doubles(const Op2DDev& op, int nblocks) {
+  return 7 * (size_t)op.n + 2 * (size_t)op.nn + 16 + 8 * (size_t)nblocks;
 }
 // blocks for the cooperative CG: resident blocks x SMs, capped by the element tiles
 int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks) {

@@ -112,6 +112,7 @@ int launch2x_fas(Ctx* c, const Xfer2Dev& x, const double* Wf, double dt, int inc
 int launch2x_interp(Ctx* c, const Xfer2Dev& x, int accumulate, const double* uc, const double* vc, double* uf);
 int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int nblocks);
 int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks);
+size_t cg2_ws_doubles(const Op2DDev& op, int nblocks);
 int set_cg2_tables(Ctx* c, int p1, const double* tab);
 // partitioned (ghost-row) 2-D operators: split CG phases, reductions, halo (ops2d.cu)
 struct CgPScal;
