@@ -1,6 +1,7 @@
 // 2-D sweep-path kernels (BASELINE configs 3-5): operators, fused sweep
 // stages, tensor-product space-time transfers and the grid-persistent
 // Chronopoulos-Gear PCG over HBM-resident vectors.
+#include <type_traits>
 #include <cooperative_groups.h>
 #include <vector>
 #include <cstdlib>
@@ -1919,7 +1920,10 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
 // ring holds columns j-1, j, j+1) and, transposed, into the block's ring RT,
 // where the warps of rows y-1 / y+1 read it as their top / bottom neighbour.
 // Only the two rows bordering the band are rebuilt redundantly (by a warp
-// that rotates with the step).  One block barrier per step.  Operands arrive
+// that rotates with the step).  The warps of a block are coupled by ONE mbarrier
+// per step, split into arrive (column j+1 written) and wait (before the
+// matvec of column j reads the neighbours' column j), so a warp only waits when
+// a neighbour is a whole step behind; RT has four slots for that.  Operands arrive
 // by TMA bulk copies (cp.async.bulk, one 512-byte run per element vector, five
 // per warp and step from one lane) on per-warp mbarriers, two steps ahead.
 template <int NC>
@@ -1935,11 +1939,11 @@ struct Fz {
   static constexpr int QX = RING + 3 * NP, QY = QX + NP, DOT = QY + NP, FCON = DOT + 32;
   static constexpr int WARP = FCON + 64;
   // block region
-  static constexpr int RT = NW * WARP;              // [3 slots][NW + 2 rows][64] u' transposed + swizzled
-  static constexpr int HRAW = RT + 3 * (NW + 2) * NN;   // [2 halo rows][2 stages][r, s, w, dinv][64]
+  static constexpr int RT = NW * WARP;              // [4 slots][NW + 2 rows][64] u' transposed + swizzled
+  static constexpr int HRAW = RT + 4 * (NW + 2) * NN;   // [2 halo rows][2 stages][r, s, w, dinv][64]
   static constexpr int RED = HRAW + 2 * 2 * 4 * NN; // [32][4] block reduction scratch
-  static constexpr int MBAR = RED + 128;            // [NW][2] own stages, [2][2] halo stages
-  static constexpr int SIZE = MBAR + 2 * NW + 4;
+  static constexpr int MBAR = RED + 128;            // [NW][2] own stages, [2][2] halo stages, column barrier
+  static constexpr int SIZE = MBAR + 2 * NW + 6;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -1957,7 +1961,7 @@ __device__ __forceinline__ void mbar2_wait(uint32_t m, uint32_t parity) {
 }
 // TMA bulk copy global -> shared, completion counted on the mbarrier (UBLKCP)
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const double* src, uint32_t bytes, uint32_t mbar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(mbar)
                : "memory");
 }
@@ -2051,8 +2055,10 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   double* RT = sm + F::RT;
   const uint32_t mb_own = smem_u32(reinterpret_cast<unsigned long long*>(sm + F::MBAR) + 2 * warp);   // + 8 stage
   const uint32_t mb_halo = smem_u32(reinterpret_cast<unsigned long long*>(sm + F::MBAR) + 2 * NW);    // + 16 h + 8 stage
+  const uint32_t mb_col = mb_halo + 32u;   // NW arrivals (one per warp) per step
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2 * NW + 4; ++i) mbar2_init(smem_u32(reinterpret_cast<unsigned long long*>(sm + F::MBAR) + i), 1);
+    mbar2_init(mb_col, NW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -2073,6 +2079,8 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   const int nstr = (op.nex + SL - 1) / SL, nbands = (op.ney + NW - 1) / NW;
   const long long nunits = (long long)nbands * nstr * NC;
   unsigned oc = 0, hc = 0;   // completed uses of this warp's own stages / of the halo stages (stage = use & 1)
+  unsigned ac = 0;           // this warp's arrivals on the column barrier (= steps done)
+  int st = 0;                // RT slot of column j (slots advance with j, four of them)
   int k = 0;
   bool ok = true;
   const bool stampb = A.timing != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == G - 1);
@@ -2141,7 +2149,8 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
         const int exr = col + 1 == op.nex ? 0 : col + 1, exl = col == 0 ? op.nex - 1 : col - 1;
         return A.Cf[cfb + (unsigned)(f == FR ? exr : f == FL ? exl : col) * 64u];
       };
-      __syncthreads();   // the previous unit's last step has read RT
+      // (no block barrier between units: warp 0 issues the halo stages below after its last wait on the
+      // column barrier, which every warp passed after its last halo rebuild)
       // halo steps: js + 1 in [x0, x1 - 1]; two uses ahead
       if (valid) {
         issue_own(x0 - 2, oc);
@@ -2158,12 +2167,14 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       double cfn_reg = cfn_load(x0);
       double2 pp = make_double2(0.0, 0.0), xx = pp;
       int sl = 0;   // ring slot of column j - 1 (slots advance with j)
-      for (int j = x0 - 2; j < x1; ++j) {
+      // one step, specialised at compile time on own (column j + 1 lies inside the strip: its s', r',
+      // p, x are written, the rows bordering the band are rebuilt) and sip (column j gets its w')
+      auto step = [&](const int j, auto own_c, auto sip_c) {
+        constexpr bool own = decltype(own_c)::value, sip = decltype(sip_c)::value;
         const int jn = j + 1;
-        const bool own = jn >= x0 && jn < x1, sip = j >= x0;
         const int sN = sl == 0 ? 2 : sl - 1;        // slot of column j + 1: (sl + 2) % 3
         const int sJ = sl == 2 ? 0 : sl + 1;        // slot of column j
-        __syncthreads();   // every warp is past step j - 1: RT column j is complete, RT slot sN is free
+        const int tN = (st + 1) & 3;                // RT slot of column j + 1 (free: see the column barrier below)
         if (valid) {
           const unsigned gn = oC + (unsigned)jn * 64u;   // used inside the strip only
           const double* raw = ws + F::RAW + (oc & 1u) * 320;
@@ -2183,7 +2194,7 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
             uu.y = rn.y * di.y;
             *reinterpret_cast<double2*>(ws + F::RING + sN * NP + g * RP + n0) = uu;
             if (own) {
-              double* rt = RT + (sN * (NW + 2) + warp) * 64;
+              double* rt = RT + (tN * (NW + 2) + warp) * 64;
               rt[ta] = (g & 1) ? uu.y : uu.x;
               rt[tb] = (g & 1) ? uu.x : uu.y;
               *reinterpret_cast<double2*>(Sn + gn) = sn;
@@ -2206,9 +2217,7 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
             ws[F::CFN + lane] = cfn_reg;
           }
           __syncwarp();
-          if (j + 2 < x1) {   // this stage is free: refill it for step j + 2
-            issue_own(j + 2, oc + 2);
-          }
+          if (j + 2 < x1) issue_own(j + 2, oc + 2);   // this stage is free: refill it for step j + 2
           ++oc;
         }
         {   // register prefetches for the next step: p, x of column j + 2, face coefficients of column
@@ -2226,7 +2235,7 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
             if (warp == ((j + 4 * h) & (NW - 1))) {
               const double* raw = sm + F::HRAW + (h * 2 + (hc & 1u)) * 256;
               mbar2_wait(mb_halo + 16u * h + 8u * (hc & 1u), (hc >> 1) & 1u);
-              double* rt = RT + (sN * (NW + 2) + NW + h) * 64;
+              double* rt = RT + (tN * (NW + 2) + NW + h) * 64;
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int v = lane + 32 * q;
@@ -2241,9 +2250,16 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           }
           ++hc;
         }
+        // column barrier.  Wait: every warp has arrived for step j - 1, i.e. written column j (and is
+        // past the matvec of column j - 2, whose RT slot the NEXT step overwrites).  Then arrive for
+        // this step (column j + 1 written).  Waiting before arriving keeps the phase parity unambiguous.
+        if (ac > 0) mbar2_wait(mb_col, (ac - 1) & 1u);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb_col) : "memory");
+        ++ac;
         if (sip && valid) {
           const double* Ue = ws + F::RING + sJ * NP;
-          const double* rtj = RT + sJ * (NW + 2) * 64;
+          const double* rtj = RT + st * (NW + 2) * 64;
           double bx0, bx1, by0, by1;
           fz_sip(op, K, Ue, ws + F::RING + sN * NP, ws + F::RING + sl * NP,
                  rtj + (warp + 1 < nrows ? warp + 1 : NW) * 64, rtj + (warp > 0 ? warp - 1 : NW + 1) * 64,
@@ -2257,7 +2273,15 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           __syncwarp();   // scratch is rewritten by the next step
         }
         sl = sJ;
-      }
+        st = tN;
+      };
+      using T_ = std::true_type;
+      using F_ = std::false_type;
+      step(x0 - 2, F_{}, F_{});
+      step(x0 - 1, T_{}, F_{});
+#pragma unroll 1
+      for (int j = x0; j < x1 - 1; ++j) step(j, T_{}, T_{});
+      step(x1 - 1, F_{}, T_{});
     }
     if (stamp) tm[3] = gtimer();
     double* slot = (k & 1) ? slot1 : slot0;
