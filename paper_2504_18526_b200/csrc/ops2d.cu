@@ -1691,6 +1691,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   // per-element tile evaluation
   const int ne_own = op.nex * op.ney;
   const long long nown = (long long)ne_own * NN;
+  if (A.mode != 2) {   // mode 2: Cf and DINV were filled by k2_coef / k2p_dinv at full occupancy
   for (long long f0 = gtid; f0 < nown; f0 += 4 * nthr) {   // 4 nodes per thread in flight
     double cv[4];
     long long fs[4];
@@ -1734,6 +1735,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
                        op.sy * CS[i] * D00;
     const double hwx = 0.5 * op.dx * c_tab2[T::W + i], hwy = 0.5 * op.dy * c_tab2[T::W + j];
     A.DINV[(long long)(ey * op.nex + ex) * NN + nd] = 1.0 / (hwx * hwy + A.a * (hwy * dx_ + hwx * dy_));
+  }
   }
   const bool stamps = A.timing != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == G - 1);
   long long* ts = A.timing + (blockIdx.x == 0 ? 30 : 40);
@@ -1783,7 +1785,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   if (tot[1] == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
     for (long long t = gtid; t < op.n; t += nthr) A.x[t] = 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (A.mode == 1) A.scal[7] = 0.0;   // nothing left for k2_cgf
+      if (A.mode != 0) A.scal[7] = 0.0;   // nothing left for k2_cgf
       int idx = atomicAdd(&A.status[2], 1);
       if (idx < A.log_cap) { A.log_it[idx] = 0; A.log_margin[idx] = 0.0; }
     }
@@ -1840,7 +1842,7 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   double rho = tot[2];
   double alpha = tot[0] / tot[1], beta = 0.0;
   double rgam = 1.0 / tot[0], ralpha = 1.0 / alpha;
-  if (A.mode == 1) {   // setup only: the iterations run in k2_cgf
+  if (A.mode != 0) {   // setup only: the iterations run in k2_cgf
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       A.scal[2] = thr; A.scal[3] = rho; A.scal[4] = alpha; A.scal[5] = rgam; A.scal[6] = ralpha; A.scal[7] = 1.0;
     }
@@ -2406,10 +2408,12 @@ __global__ void k2p_dinv(Cg2Args A) {
     const long long es = (long long)ey * op.nex + ex;
     const double* CS = A.Cf + es * NN;
     double dx_ = 0.0, dy_ = 0.0;
+    // lane-varying table rows from the global operator table (divergent constant-bank reads serialise)
+    const double* d2w = op.tab + TabOff::D2W(P1);
 #pragma unroll
     for (int q = 0; q < P1; ++q) {
-      dx_ = fma(c_tab2[T::D2W + i * P1 + q], CS[j * P1 + q], dx_);
-      dy_ = fma(c_tab2[T::D2W + j * P1 + q], CS[q * P1 + i], dy_);
+      dx_ = fma(__ldg(d2w + i * P1 + q), CS[j * P1 + q], dx_);
+      dy_ = fma(__ldg(d2w + j * P1 + q), CS[q * P1 + i], dy_);
     }
     const double DPP = c_tab2[T::D + P * P1 + P], D00 = c_tab2[T::D];
     dx_ *= op.sx;
@@ -2430,7 +2434,7 @@ __global__ void k2p_dinv(Cg2Args A) {
       const double fb = A.Cf[((long long)eyb * op.nex + ex) * NN + P * P1 + i];
       dy_ += op.muy * (0.5 * (fb + CS[i])) + op.sy * CS[i] * D00;
     }
-    const double hwx = 0.5 * op.dx * c_tab2[T::W + i], hwy = 0.5 * op.dy * c_tab2[T::W + j];
+    const double hwx = 0.5 * op.dx * __ldg(op.tab + TabOff::w(P1) + i), hwy = 0.5 * op.dy * __ldg(op.tab + TabOff::w(P1) + j);
     A.DINV[es * NN + nd] = 1.0 / (hwx * hwy + A.a * (hwy * dx_ + hwx * dy_));
   }
 }
@@ -2908,7 +2912,18 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
     return !(v && v[0] == '0');
   }();
   const bool fused = fused_on && op.p1 == 8 && op.row0 == 0;
-  if (fused) A.mode = 1;
+  if (fused) {
+    // coefficient and Jacobi diagonal at full occupancy (fp64 sqrt / division chains want more warps
+    // than the 128-register cooperative kernel has), then k2_cg's setup 2 / 3 only (mode 2)
+    const unsigned nb1 = (unsigned)((op.nn + 255) / 256);
+    k2_coef<8><<<nb1, 256, 0, c->stream>>>(op, k, A.Cf);
+    int rc = c->after_launch("k2_coef (CG setup)");
+    if (rc) return rc;
+    k2p_dinv<8><<<nb1, 256, 0, c->stream>>>(A);
+    rc = c->after_launch("k2p_dinv (CG setup)");
+    if (rc) return rc;
+    A.mode = 2;
+  }
   SISDC_P1_SWITCH(op.p1, {
     if (op.nc == 4) e = launch_cg_coop<P1, 4>(args, nblocks, c->stream);
     else e = launch_cg_coop<P1, 1>(args, nblocks, c->stream);
