@@ -1932,13 +1932,12 @@ template <int NC>
 struct Fz {
   static constexpr int SL = 16;                     // strip length (elements)
   static constexpr int NW = 8;                      // warps per block = rows per band
-  static constexpr int RP = 10, NP = 80, NN = 64;
+  static constexpr int NN = 64;
   // per-warp region (doubles)
   static constexpr int RAW = 0;                     // [2 stages][r, s, w, dinv of column j+1 | cf of column j][64]
-  static constexpr int COEF = RAW + 2 * 5 * NN;     // [NP] own coefficient, rows padded to 10
-  static constexpr int CFN = COEF + NP;             // [32] neighbour face coefficients
-  static constexpr int RING = CFN + 32;             // [3][NP] u' of columns j-1, j, j+1 (rows padded to 10)
-  static constexpr int QX = RING + 3 * NP, QY = QX + NP, DOT = QY + NP, FCON = DOT + 32;
+  static constexpr int CFN = RAW + 2 * 5 * NN;      // [32] neighbour face coefficients
+  static constexpr int RING = CFN + 32;             // [3][64] u' of columns j-1, j, j+1 (sw8 layout)
+  static constexpr int QX = RING + 3 * NN, QY = QX + NN, DOT = QY + NN, FCON = DOT + 32;
   static constexpr int WARP = FCON + 64;
   // block region
   static constexpr int RT = NW * WARP;              // [4 slots][NW + 2 rows][64] u' transposed + swizzled
@@ -1968,29 +1967,43 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const double* src, uint32
                : "memory");
 }
 
-// wpe_sip for the fused pass: own element Ue and the x-neighbours UR / UL in
-// padded rows (ring slots), the y-neighbours UT / UB transposed and swizzled
-// (face lines are rows).  Same operations and order as wpe_sip.
+// 8 x 8 tiles of the fused pass (ring slots, RT rows, QX / QY): node (row, col) at
+// row * 8 + 16-byte chunk (col / 2) ^ S(row), S = (0, 2, 1, 3)[row / 2].  Bank-conflict
+// free for every access pattern of fz_sip: the lane's node pair (128-bit, rows g), the
+// tensor-core A fragments (row g, col t / t + 4) and B fragments (row t / t + 4, col g)
+// as 64-bit loads, and whole rows read by eight lanes (face lines).  Rows padded to 10
+// cost two wavefronts per quarter warp on the 128-bit pair accesses and 4 instead of 2
+// on the fragment loads (ncu: 36% excessive shared wavefronts, l1tex pipe at 79%).
+__device__ __forceinline__ int sw8(int row, int col) {
+  const int sr = ((row >> 1) & 1) * 2 + ((row >> 2) & 1);
+  return row * 8 + ((((col >> 1) ^ sr)) << 1) + (col & 1);
+}
+
+// wpe_sip for the fused pass: own element Ue and the x-neighbours UR / UL (ring
+// slots), the y-neighbours UT / UB transposed (face lines are rows), all in the
+// sw8 layout; Ce row-major as the bulk copy delivers it.  FC: [16 lines][fp, fm]
+// then [16 lines][adjoint + , adjoint -].  Same operations and order as wpe_sip.
 __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, const double* Ue, const double* UR,
                                        const double* UL, const double* UT, const double* UB, const double* Ce,
                                        const double* cfn, double* QX, double* QY, double* DT, double* FC,
                                        double& bx0, double& bx1, double& by0, double& by1) {
-  constexpr int RP = 10, P = 7;
+  constexpr int P = 7;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, n0 = 2 * t;
+  const int oA0 = sw8(g, t), oA1 = sw8(g, t + 4), oB0 = sw8(t, g), oB1 = sw8(t + 4, g), oP = sw8(g, n0);
   double qx0 = 0.0, qx1 = 0.0, qy0 = 0.0, qy1 = 0.0;
-  dmma(qx0, qx1, Ue[g * RP + t], K.d0);
-  dmma(qx0, qx1, Ue[g * RP + 4 + t], K.d1);
-  dmma(qy0, qy1, K.d0, Ue[t * RP + g]);
-  dmma(qy0, qy1, K.d1, Ue[(4 + t) * RP + g]);
+  dmma(qx0, qx1, Ue[oA0], K.d0);
+  dmma(qx0, qx1, Ue[oA1], K.d1);
+  dmma(qy0, qy1, K.d0, Ue[oB0]);
+  dmma(qy0, qy1, K.d1, Ue[oB1]);
   {
-    const double2 cg = *reinterpret_cast<const double2*>(Ce + g * RP + n0);
-    *reinterpret_cast<double2*>(QX + g * RP + n0) = make_double2(cg.x * (op.sx * qx0), cg.y * (op.sx * qx1));
-    *reinterpret_cast<double2*>(QY + g * RP + n0) = make_double2(cg.x * (op.sy * qy0), cg.y * (op.sy * qy1));
+    const double2 cg = *reinterpret_cast<const double2*>(Ce + 2 * lane);   // row g, columns n0, n0 + 1
+    *reinterpret_cast<double2*>(QX + oP) = make_double2(cg.x * (op.sx * qx0), cg.y * (op.sx * qx1));
+    *reinterpret_cast<double2*>(QY + oP) = make_double2(cg.x * (op.sy * qy0), cg.y * (op.sy * qy1));
   }
   {
     const int f = lane >> 3, k = lane & 7;
-    const double* ln = f == FR ? UR + k * RP : f == FL ? UL + k * RP : (f == FT ? UT : UB) + k * 8;
-    const int sw = f < FT ? 0 : (k >> 1);
+    const double* ln = (f == FR ? UR : f == FL ? UL : f == FT ? UT : UB) + k * 8;
+    const int sw = ((k >> 1) & 1) * 2 + ((k >> 2) & 1);
     double gd = 0.0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -2002,42 +2015,46 @@ __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, cons
   }
   __syncwarp();
   bx0 = bx1 = by0 = by1 = 0.0;
-  dmma(bx0, bx1, QX[g * RP + t], K.w0);
-  dmma(bx0, bx1, QX[g * RP + 4 + t], K.w1);
-  dmma(by0, by1, K.w0, QY[t * RP + g]);
-  dmma(by0, by1, K.w1, QY[(4 + t) * RP + g]);
+  dmma(bx0, bx1, QX[oA0], K.w0);
+  dmma(bx0, bx1, QX[oA1], K.w1);
+  dmma(by0, by1, K.w0, QY[oB0]);
+  dmma(by0, by1, K.w1, QY[oB1]);
   if (lane < 16) {
     const bool yd = lane >= 8;
     const int r = lane & 7;
-    const int up = yd ? P * RP + r : r * RP + P, u0 = yd ? r : r * RP;
-    const double jp = Ue[up] - (yd ? UT[nsw(r, 0)] : UR[r * RP]);
-    const double jm = (yd ? UB[nsw(r, P)] : UL[r * RP + P]) - Ue[u0];
-    const double cP = Ce[up], c0 = Ce[u0];
+    const int up = yd ? sw8(P, r) : sw8(r, P), u0 = yd ? sw8(0, r) : sw8(r, 0);   // own face nodes
+    const int cu = yd ? P * 8 + r : r * 8 + P, c0_ = yd ? r : r * 8;              // the same, row-major (Ce)
+    const double jp = Ue[up] - (yd ? UT : UR)[sw8(r, 0)];
+    const double jm = (yd ? UB : UL)[sw8(r, P)] - Ue[u0];
+    const double cP = Ce[cu], c0 = Ce[c0_];
     const double fcp = cfn[(yd ? 16 : 0) + r], fcm = cfn[(yd ? 24 : 8) + r];
     const double qP = (yd ? QY : QX)[up], q0 = (yd ? QY : QX)[u0];
     const double qnp = DT[(yd ? 16 : 0) + r], qnm = DT[(yd ? 24 : 8) + r];
     const double mu = yd ? op.muy : op.mux, sc = yd ? op.sy : op.sx;
     const double fp = -(0.5 * (qP + qnp)) + (mu * (0.5 * (cP + fcp))) * jp;
     const double fm = -(0.5 * (qnm + q0)) + (mu * (0.5 * (fcm + c0))) * jm;
-    *reinterpret_cast<double4*>(FC + lane * 4) = make_double4(fp, fm, sc * ((0.5 * cP) * jp), sc * ((0.5 * c0) * jm));
+    *reinterpret_cast<double2*>(FC + lane * 2) = make_double2(fp, fm);
+    *reinterpret_cast<double2*>(FC + 32 + lane * 2) = make_double2(sc * ((0.5 * cP) * jp), sc * ((0.5 * c0) * jm));
   }
   __syncwarp();
   {
-    const double4 rx = *reinterpret_cast<const double4*>(FC + g * 4);
+    const double2 rx = *reinterpret_cast<const double2*>(FC + g * 2);
+    const double2 rz = *reinterpret_cast<const double2*>(FC + 32 + g * 2);
     if (n0 + 1 == P) bx1 += rx.x;
     if (n0 == 0) bx0 -= rx.y;
-    bx0 -= rx.z * K.dPn[0];
-    bx1 -= rx.z * K.dPn[1];
-    bx0 -= rx.w * K.d0n[0];
-    bx1 -= rx.w * K.d0n[1];
-    const double4 ca = *reinterpret_cast<const double4*>(FC + (8 + n0) * 4);
-    const double4 cb = *reinterpret_cast<const double4*>(FC + (9 + n0) * 4);
-    if (g == P) { by0 += ca.x; by1 += cb.x; }
-    if (g == 0) { by0 -= ca.y; by1 -= cb.y; }
-    by0 -= ca.z * K.dPg;
-    by1 -= cb.z * K.dPg;
-    by0 -= ca.w * K.d0g;
-    by1 -= cb.w * K.d0g;
+    bx0 -= rz.x * K.dPn[0];
+    bx1 -= rz.x * K.dPn[1];
+    bx0 -= rz.y * K.d0n[0];
+    bx1 -= rz.y * K.d0n[1];
+    // y-columns n0, n0 + 1: (fp, fm) of both in one 32-byte run, likewise the adjoint pair
+    const double4 cf = *reinterpret_cast<const double4*>(FC + (8 + n0) * 2);
+    const double4 cz = *reinterpret_cast<const double4*>(FC + 32 + (8 + n0) * 2);
+    if (g == P) { by0 += cf.x; by1 += cf.z; }
+    if (g == 0) { by0 -= cf.y; by1 -= cf.w; }
+    by0 -= cz.x * K.dPg;
+    by1 -= cz.z * K.dPg;
+    by0 -= cz.y * K.d0g;
+    by1 -= cz.w * K.d0g;
   }
 }
 
@@ -2047,7 +2064,7 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   using F = Fz<NC>;
   cg::grid_group grid = cg::this_grid();
   const Op2DDev& op = A.op;
-  constexpr int SL = F::SL, RP = F::RP, NP = F::NP, NW = F::NW;
+  constexpr int SL = F::SL, NW = F::NW;
   const long long nn = op.nn;
   const int G = gridDim.x;
   const int lane = threadIdx.x & 31;
@@ -2074,10 +2091,11 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   const int g = lane >> 2, n0 = 2 * (lane & 3);
   const int f = lane >> 3, kf = lane & 7;
   const int fnode = f == FR ? kf * 8 : f == FL ? kf * 8 + 7 : f == FT ? kf : 56 + kf;   // neighbour's face node
-  const int tr0 = nsw(lane & 7, lane >> 3), tr1 = nsw(lane & 7, 4 + (lane >> 3));   // node v -> line v%8, pos v/8
+  const int tr0 = sw8(lane & 7, lane >> 3), tr1 = sw8(lane & 7, 4 + (lane >> 3));   // node v -> line v%8, pos v/8
+  const int oP = sw8(g, n0);   // this lane's node pair in a tile
   // transposed position of this lane's own node pair (row g, columns n0, n0+1); odd rows store the second
   // node first so that one store instruction hits all 16 bank pairs
-  const int ta = (g & 1) ? nsw(n0 + 1, g) : nsw(n0, g), tb = (g & 1) ? nsw(n0, g) : nsw(n0 + 1, g);
+  const int ta = (g & 1) ? sw8(n0 + 1, g) : sw8(n0, g), tb = (g & 1) ? sw8(n0, g) : sw8(n0 + 1, g);
   const int nstr = (op.nex + SL - 1) / SL, nbands = (op.ney + NW - 1) / NW;
   const long long nunits = (long long)nbands * nstr * NC;
   unsigned oc = 0, hc = 0;   // completed uses of this warp's own stages / of the halo stages (stage = use & 1)
@@ -2194,7 +2212,7 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
             rn.y = fma(-alpha, sn.y, r.y);
             uu.x = rn.x * di.x;
             uu.y = rn.y * di.y;
-            *reinterpret_cast<double2*>(ws + F::RING + sN * NP + g * RP + n0) = uu;
+            *reinterpret_cast<double2*>(ws + F::RING + sN * 64 + oP) = uu;
             if (own) {
               double* rt = RT + (tN * (NW + 2) + warp) * 64;
               rt[ta] = (g & 1) ? uu.y : uu.x;
@@ -2213,14 +2231,8 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
               __stcs(reinterpret_cast<double2*>(A.x + gn), xx);
             }
           }
-          if (sip) {   // coefficients of column j
-            *reinterpret_cast<double2*>(ws + F::COEF + g * RP + n0) =
-                *reinterpret_cast<const double2*>(raw + 256 + 2 * lane);
-            ws[F::CFN + lane] = cfn_reg;
-          }
+          if (sip) ws[F::CFN + lane] = cfn_reg;   // face coefficients of column j
           __syncwarp();
-          if (j + 2 < x1) issue_own(j + 2, oc + 2);   // this stage is free: refill it for step j + 2
-          ++oc;
         }
         {   // register prefetches for the next step: p, x of column j + 2, face coefficients of column
             // j + 1.  Unconditional (clamped columns): a load inside a branch makes the compiler wait
@@ -2260,19 +2272,23 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb_col) : "memory");
         ++ac;
         if (sip && valid) {
-          const double* Ue = ws + F::RING + sJ * NP;
+          const double* Ue = ws + F::RING + sJ * 64;
           const double* rtj = RT + st * (NW + 2) * 64;
           double bx0, bx1, by0, by1;
-          fz_sip(op, K, Ue, ws + F::RING + sN * NP, ws + F::RING + sl * NP,
+          fz_sip(op, K, Ue, ws + F::RING + sN * 64, ws + F::RING + sl * 64,
                  rtj + (warp + 1 < nrows ? warp + 1 : NW) * 64, rtj + (warp > 0 ? warp - 1 : NW + 1) * 64,
-                 ws + F::COEF, ws + F::CFN, ws + F::QX, ws + F::QY, ws + F::DOT, ws + F::FCON, bx0, bx1, by0, by1);
-          const double2 v = *reinterpret_cast<const double2*>(Ue + g * RP + n0);
+                 ws + F::RAW + (oc & 1u) * 320 + 256, ws + F::CFN, ws + F::QX, ws + F::QY, ws + F::DOT, ws + F::FCON, bx0, bx1, by0, by1);
+          const double2 v = *reinterpret_cast<const double2*>(Ue + oP);
           const double w0 = fma(A.a, fma(K.hwy, bx0, K.hwx[0] * by0), K.hh[0] * v.x);
           const double w1 = fma(A.a, fma(K.hwy, bx1, K.hwx[1] * by1), K.hh[1] * v.y);
           *reinterpret_cast<double2*>(Wn + (oC + (unsigned)j * 64u)) = make_double2(w0, w1);   // g * 8 + n0 == 2 lane
           wu = fma(w0, v.x, wu);
           wu = fma(w1, v.y, wu);
           __syncwarp();   // scratch is rewritten by the next step
+        }
+        if (valid) {   // this step's stage (its cf was read by the matvec) is free: refill it for step j + 2
+          if (j + 2 < x1) issue_own(j + 2, oc + 2);
+          ++oc;
         }
         sl = sJ;
         st = tN;
