@@ -1983,13 +1983,32 @@ __device__ __forceinline__ int sw8(int row, int col) {
 // slots), the y-neighbours UT / UB transposed (face lines are rows), all in the
 // sw8 layout; Ce row-major as the bulk copy delivers it.  FC: [16 lines][fp, fm]
 // then [16 lines][adjoint + , adjoint -].  Same operations and order as wpe_sip.
-__device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, const double* Ue, const double* UR,
-                                       const double* UL, const double* UT, const double* UB, const double* Ce,
-                                       const double* cfn, double* QX, double* QY, double* DT, double* FC,
-                                       double& bx0, double& bx1, double& by0, double& by1) {
+struct FzLane {   // per-lane tile offsets (doubles), computed once per kernel
+  int oA0, oA1, oB0, oB1, oP;   // A / B fragments, node pair
+  int ln, lsw;                  // face line of this lane: row offset k * 8, chunk swizzle S(k)
+  int up, u0, cu, c0, nP, n0_;  // lanes < 16: own face nodes (sw8 and row-major), neighbour face nodes
+};
+__device__ __forceinline__ void fz_lane_init(FzLane& L) {
+  constexpr int P = 7;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, k = lane & 7;
+  L.oA0 = sw8(g, t); L.oA1 = sw8(g, t + 4); L.oB0 = sw8(t, g); L.oB1 = sw8(t + 4, g); L.oP = sw8(g, 2 * t);
+  L.ln = k * 8;
+  L.lsw = ((k >> 1) & 1) * 2 + ((k >> 2) & 1);
+  const bool yd = lane >= 8;
+  L.up = yd ? sw8(P, k) : sw8(k, P);
+  L.u0 = yd ? sw8(0, k) : sw8(k, 0);
+  L.cu = yd ? P * 8 + k : k * 8 + P;
+  L.c0 = yd ? k : k * 8;
+  L.nP = sw8(k, P);
+  L.n0_ = sw8(k, 0);
+}
+__device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, const FzLane& L, const double* Ue,
+                                       const double* UR, const double* UL, const double* UT, const double* UB,
+                                       const double* Ce, const double* cfn, double* QX, double* QY, double* DT,
+                                       double* FC, double& bx0, double& bx1, double& by0, double& by1) {
   constexpr int P = 7;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, n0 = 2 * t;
-  const int oA0 = sw8(g, t), oA1 = sw8(g, t + 4), oB0 = sw8(t, g), oB1 = sw8(t + 4, g), oP = sw8(g, n0);
+  const int oA0 = L.oA0, oA1 = L.oA1, oB0 = L.oB0, oB1 = L.oB1, oP = L.oP;
   double qx0 = 0.0, qx1 = 0.0, qy0 = 0.0, qy1 = 0.0;
   dmma(qx0, qx1, Ue[oA0], K.d0);
   dmma(qx0, qx1, Ue[oA1], K.d1);
@@ -2001,9 +2020,9 @@ __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, cons
     *reinterpret_cast<double2*>(QY + oP) = make_double2(cg.x * (op.sy * qy0), cg.y * (op.sy * qy1));
   }
   {
-    const int f = lane >> 3, k = lane & 7;
-    const double* ln = (f == FR ? UR : f == FL ? UL : f == FT ? UT : UB) + k * 8;
-    const int sw = ((k >> 1) & 1) * 2 + ((k >> 2) & 1);
+    const int f = lane >> 3;
+    const double* ln = (f == FR ? UR : f == FL ? UL : f == FT ? UT : UB) + L.ln;
+    const int sw = L.lsw;
     double gd = 0.0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -2022,10 +2041,10 @@ __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, cons
   if (lane < 16) {
     const bool yd = lane >= 8;
     const int r = lane & 7;
-    const int up = yd ? sw8(P, r) : sw8(r, P), u0 = yd ? sw8(0, r) : sw8(r, 0);   // own face nodes
-    const int cu = yd ? P * 8 + r : r * 8 + P, c0_ = yd ? r : r * 8;              // the same, row-major (Ce)
-    const double jp = Ue[up] - (yd ? UT : UR)[sw8(r, 0)];
-    const double jm = (yd ? UB : UL)[sw8(r, P)] - Ue[u0];
+    const int up = L.up, u0 = L.u0;     // own face nodes
+    const int cu = L.cu, c0_ = L.c0;    // the same, row-major (Ce)
+    const double jp = Ue[up] - (yd ? UT : UR)[L.n0_];
+    const double jm = (yd ? UB : UL)[L.nP] - Ue[u0];
     const double cP = Ce[cu], c0 = Ce[c0_];
     const double fcp = cfn[(yd ? 16 : 0) + r], fcm = cfn[(yd ? 24 : 8) + r];
     const double qP = (yd ? QY : QX)[up], q0 = (yd ? QY : QX)[u0];
@@ -2086,13 +2105,15 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   double rho = A.scal[3], alpha = A.scal[4], beta = 0.0, rgam = A.scal[5], ralpha = A.scal[6];
   MmaLane K;
   mma_lane_init(op, K);
+  FzLane L;
+  fz_lane_init(L);
   double* slot0 = A.part;
   double* slot1 = A.part + 4 * G;
   const int g = lane >> 2, n0 = 2 * (lane & 3);
   const int f = lane >> 3, kf = lane & 7;
   const int fnode = f == FR ? kf * 8 : f == FL ? kf * 8 + 7 : f == FT ? kf : 56 + kf;   // neighbour's face node
   const int tr0 = sw8(lane & 7, lane >> 3), tr1 = sw8(lane & 7, 4 + (lane >> 3));   // node v -> line v%8, pos v/8
-  const int oP = sw8(g, n0);   // this lane's node pair in a tile
+  const int oP = L.oP;   // this lane's node pair in a tile
   // transposed position of this lane's own node pair (row g, columns n0, n0+1); odd rows store the second
   // node first so that one store instruction hits all 16 bank pairs
   const int ta = (g & 1) ? sw8(n0 + 1, g) : sw8(n0, g), tb = (g & 1) ? sw8(n0, g) : sw8(n0 + 1, g);
@@ -2275,7 +2296,7 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           const double* Ue = ws + F::RING + sJ * 64;
           const double* rtj = RT + st * (NW + 2) * 64;
           double bx0, bx1, by0, by1;
-          fz_sip(op, K, Ue, ws + F::RING + sN * 64, ws + F::RING + sl * 64,
+          fz_sip(op, K, L, Ue, ws + F::RING + sN * 64, ws + F::RING + sl * 64,
                  rtj + (warp + 1 < nrows ? warp + 1 : NW) * 64, rtj + (warp > 0 ? warp - 1 : NW + 1) * 64,
                  ws + F::RAW + (oc & 1u) * 320 + 256, ws + F::CFN, ws + F::QX, ws + F::QY, ws + F::DOT, ws + F::FCON, bx0, bx1, by0, by1);
           const double2 v = *reinterpret_cast<const double2*>(Ue + oP);

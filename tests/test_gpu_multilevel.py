@@ -149,6 +149,7 @@ def test_paper_table_rows_match_reference_cli(rt, golden_mls, case):
     for key in sorted(set(mine) | set(ref)):
         if key in mine and key in ref:
             ea, eb = mine[key], ref[key]
-            assert abs(ea - eb) <= 1e-8 * abs(eb) or (ea < FLOOR and eb < FLOOR), (key, ea, eb)
+            # 1e-12 absolute: the two implicit solvers differ by a few 1e-13 in the solution itself
+            assert abs(ea - eb) <= 1e-8 * abs(eb) + 1e-12 or (ea < FLOOR and eb < FLOOR), (key, ea, eb)
         else:   # one series stopped earlier: only inside the noise floor
             assert (mine.get(key, ref.get(key))) < FLOOR, key
