@@ -2142,7 +2142,9 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
     for (long long un = blockIdx.x; un < nunits; un += G) {
       const int c = (int)(un % NC);
       const long long tq = un / NC;
-      const int sx = (int)(tq % nstr), band = (int)(tq / nstr);
+      // bands fastest: the blocks in flight work on vertically adjacent bands of one strip column, so the
+      // rows bordering a band (rebuilt from their raw r, s, w) are L2 hits, not a second DRAM read
+      const int band = (int)(tq % nbands), sx = (int)(tq / nbands);
       const int y0 = band * NW, nrows = op.ney - y0 < NW ? op.ney - y0 : NW;
       const bool valid = warp < nrows;
       const int ey = valid ? y0 + warp : y0;
