@@ -13,9 +13,9 @@
 //
 // One thread per node; a block stages EB elements and their four face
 // neighbours (all four fields) in shared memory, forms every own node's
-// viscous flux, the face fluxes of its element (computing the neighbour's
-// flux at the shared face nodes from the staged neighbour), then the
-// divergence.  Not on the CG hot path: it runs once per right-hand-side
+// viscous flux, the face fluxes of its element ((face node, side) work items
+// spread over all threads; the neighbour's flux at the shared face nodes is
+// computed from the staged neighbour), then the divergence.  Not on the CG hot path: it runs once per right-hand-side
 // evaluation (node caches, FAS defects), after the convection/SI kernels.
 #include "sisdc_dev2d.cuh"
 #include "sisdc_host.h"
@@ -36,7 +36,9 @@ struct Vb {
   static constexpr int FX = U + EB * US, FY = FX + EB * NCV * NN;   // own fluxes [EB][NCV][NN]
   static constexpr int GF = FY + EB * NCV * NN;             // face fluxes [EB][4 faces][P1][NCV]
   static constexpr int LF = GF + EB * 4 * P1 * NCV;         // own lifts   [EB][4 faces][P1][NCV]
-  static constexpr int SIZE = LF + EB * 4 * P1 * NCV;
+  static constexpr int XS = LF + EB * 4 * P1 * NCV;         // plus-side (q, g) of every face node [EB][4][P1][2 NCV]
+  static constexpr int SIZE = XS + EB * 4 * P1 * 2 * NCV;
+  static constexpr int DP = P1 + 1;                         // padded table rows (lane-varying row index: conflict free)
 };
 
 struct Prim {
@@ -86,42 +88,25 @@ __device__ __forceinline__ void grad_at(const Op2DDev& op, const double* X, cons
     double ax = 0.0, ay = 0.0;
 #pragma unroll
     for (int q = 0; q < P1; ++q) {
-      ax = fma(D[i * P1 + q], X[c * NN + j * P1 + q], ax);
-      ay = fma(D[j * P1 + q], X[c * NN + q * P1 + i], ay);
+      ax = fma(D[i * (P1 + 1) + q], X[c * NN + j * P1 + q], ax);
+      ay = fma(D[j * (P1 + 1) + q], X[c * NN + q * P1 + i], ay);
     }
     gx[c] = op.sx * ax;
     gy[c] = op.sy * ay;
   }
 }
 
-// face flux Gf between the staged elements A (minus side) and B (plus side)
-// at A's node (ja, ia) and B's node (jb, ib); also the minus / plus lifts
+// one side of a face node: the normal viscous flux q of the staged element X at its node
+// (jx, ix) and g = G_nn(s) [u] with the jump [u] = u- - u+ (sm, sp: the minus / plus states)
 template <int P1>
-__device__ __forceinline__ void face_terms(const Op2DDev& op, const double* A, const double* B, const double* D, int ja,
-                                           int ia, int jb, int ib, int axis, double* Gf, double* gm_out, double* gp_out) {
-  constexpr int NN = P1 * P1;
-  double sa[NCV], sb[NCV], jmp[NCV], gx[NCV], gy[NCV], Fxa[NCV], Fya[NCV], Fxb[NCV], Fyb[NCV];
+__device__ __forceinline__ void face_side(const Op2DDev& op, const double* X, const double* D, int jx, int ix,
+                                          const double* s_mine, const double* jmp, int axis, double* q, double* g) {
+  double gx[NCV], gy[NCV], Fx[NCV], Fy[NCV];
+  grad_at<P1>(op, X, D, jx, ix, gx, gy);
+  visc_flux(op, s_mine, gx, gy, Fx, Fy);
+  apply_gnn(op, s_mine, jmp, axis, g);
 #pragma unroll
-  for (int c = 0; c < NCV; ++c) {
-    sa[c] = A[c * NN + ja * P1 + ia];
-    sb[c] = B[c * NN + jb * P1 + ib];
-    jmp[c] = sa[c] - sb[c];
-  }
-  grad_at<P1>(op, A, D, ja, ia, gx, gy);
-  visc_flux(op, sa, gx, gy, Fxa, Fya);
-  grad_at<P1>(op, B, D, jb, ib, gx, gy);
-  visc_flux(op, sb, gx, gy, Fxb, Fyb);
-  double gm[NCV], gp[NCV];
-  apply_gnn(op, sa, jmp, axis, gm);
-  apply_gnn(op, sb, jmp, axis, gp);
-  const double mu0 = axis == 0 ? op.mux : op.muy;
-#pragma unroll
-  for (int c = 0; c < NCV; ++c) {
-    const double qa = axis == 0 ? Fxa[c] : Fya[c], qb = axis == 0 ? Fxb[c] : Fyb[c];
-    Gf[c] = mu0 * (0.5 * (gm[c] + gp[c])) - 0.5 * (qa + qb);
-    gm_out[c] = gm[c];
-    gp_out[c] = gp[c];
-  }
+  for (int c = 0; c < NCV; ++c) q[c] = axis == 0 ? Fx[c] : Fy[c];
 }
 
 template <int P1>
@@ -130,13 +115,13 @@ __global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* 
   using L = Vb<P1>;
   constexpr int NN = P1 * P1, P = P1 - 1;
   extern __shared__ double sm[];
-  __shared__ double sD[P1 * P1], sDTW[P1 * P1], sW[P1];
+  __shared__ double sD[P1 * (P1 + 1)], sDTW[P1 * (P1 + 1)], sW[P1];
   const int m = m_first + blockIdx.y;
   const double* um = u + (size_t)m * op.ns;
   double* fm = f + (size_t)m * op.ns;
   for (int t = threadIdx.x; t < NN; t += blockDim.x) {
-    sD[t] = op.tab[TabOff::D(P1) + t];
-    sDTW[t] = op.tab[TabOff::DTW(P1) + t];
+    sD[(t / P1) * (P1 + 1) + t % P1] = op.tab[TabOff::D(P1) + t];
+    sDTW[(t / P1) * (P1 + 1) + t % P1] = op.tab[TabOff::DTW(P1) + t];
   }
   for (int t = threadIdx.x; t < P1; t += blockDim.x) sW[t] = op.tab[TabOff::w(P1) + t];
   const int ne = op.nex * op.ney;
@@ -177,26 +162,49 @@ __global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* 
       sm[L::FY + (el * NCV + c) * NN + nd] = Fy[c];
     }
   }
-  // ---- face terms of this element: threads of row / column 0 own the four faces' lines
+  // ---- face terms of this element.  4 faces x P1 nodes x 2 sides: every (face node, side) is one
+  // unit of work (gradient, flux, G_nn [u] of that side's element), spread over all threads of the
+  // element instead of the P1 threads of row / column 0 (which left 7/8 of each warp idle through
+  // four full flux evaluations).  The plus side hands (q, g) to the minus side through XS.
   {
-    double Gf[NCV], gm[NCV], gp[NCV];
     double* GF = sm + L::GF + el * 4 * P1 * NCV;
     double* LF = sm + L::LF + el * 4 * P1 * NCV;
-    if (i == 0) {   // x-faces of row j: right (own minus, R plus), left (L minus, own plus)
-      face_terms<P1>(op, Uo, Uo + 1 * NCV * NN, sD, j, P, j, 0, 0, Gf, gm, gp);
+    double* XS = sm + L::XS + el * 4 * P1 * 2 * NCV;
+    for (int w0 = 0; w0 < 4 * P1 * 2; w0 += NN) {   // uniform trip count: block barrier inside
+      const bool act = w0 + nd < 4 * P1 * 2;
+      const int w = act ? w0 + nd : 0;
+      const int fc = w / (2 * P1), k = (w >> 1) % P1, side = w & 1;   // side 0: minus, 1: plus
+      const int axis = fc >= FT ? 1 : 0;
+      // minus / plus elements (0 own, 1 R, 2 L, 3 T, 4 B) and their face nodes
+      const int em = fc == FL ? 2 : fc == FB ? 4 : 0, ep = fc == FR ? 1 : fc == FT ? 3 : 0;
+      const int jm = axis ? P : k, im = axis ? k : P, jp = axis ? 0 : k, ip = axis ? k : 0;
+      const double* Xm = Uo + em * NCV * NN;
+      const double* Xp = Uo + ep * NCV * NN;
+      double sm_[NCV], sp_[NCV], jmp[NCV], q[NCV], g[NCV];
 #pragma unroll
-      for (int c = 0; c < NCV; ++c) { GF[(FR * P1 + j) * NCV + c] = Gf[c]; LF[(FR * P1 + j) * NCV + c] = gm[c]; }
-      face_terms<P1>(op, Uo + 2 * NCV * NN, Uo, sD, j, P, j, 0, 0, Gf, gm, gp);
+      for (int c = 0; c < NCV; ++c) {
+        sm_[c] = Xm[c * NN + jm * P1 + im];
+        sp_[c] = Xp[c * NN + jp * P1 + ip];
+        jmp[c] = sm_[c] - sp_[c];
+      }
+      if (side) face_side<P1>(op, Xp, sD, jp, ip, sp_, jmp, axis, q, g);
+      else face_side<P1>(op, Xm, sD, jm, im, sm_, jmp, axis, q, g);
+      double* xs = XS + (fc * P1 + k) * 2 * NCV;
+      if (act && side) {
 #pragma unroll
-      for (int c = 0; c < NCV; ++c) { GF[(FL * P1 + j) * NCV + c] = Gf[c]; LF[(FL * P1 + j) * NCV + c] = gp[c]; }
-    }
-    if (j == 0) {   // y-faces of column i: top (own minus, T plus), bottom (B minus, own plus)
-      face_terms<P1>(op, Uo, Uo + 3 * NCV * NN, sD, P, i, 0, i, 1, Gf, gm, gp);
+        for (int c = 0; c < NCV; ++c) { xs[c] = q[c]; xs[NCV + c] = g[c]; }
+      }
+      __syncthreads();   // the two sides of a face node may sit in different warps (odd P1)
+      if (act && !side) {
+        const double mu0 = axis == 0 ? op.mux : op.muy;
+        const bool own_minus = fc == FR || fc == FT;   // the own element's lift uses its own side's g
 #pragma unroll
-      for (int c = 0; c < NCV; ++c) { GF[(FT * P1 + i) * NCV + c] = Gf[c]; LF[(FT * P1 + i) * NCV + c] = gm[c]; }
-      face_terms<P1>(op, Uo + 4 * NCV * NN, Uo, sD, P, i, 0, i, 1, Gf, gm, gp);
-#pragma unroll
-      for (int c = 0; c < NCV; ++c) { GF[(FB * P1 + i) * NCV + c] = Gf[c]; LF[(FB * P1 + i) * NCV + c] = gp[c]; }
+        for (int c = 0; c < NCV; ++c) {
+          const double qb = xs[c], gp = xs[NCV + c];
+          GF[(fc * P1 + k) * NCV + c] = mu0 * (0.5 * (g[c] + gp)) - 0.5 * (q[c] + qb);
+          LF[(fc * P1 + k) * NCV + c] = own_minus ? g[c] : gp;
+        }
+      }
     }
   }
   __syncthreads();
@@ -213,16 +221,16 @@ __global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* 
     double bx = 0.0, by = 0.0;
 #pragma unroll
     for (int q = 0; q < P1; ++q) {
-      bx = fma(sDTW[i * P1 + q], Fx[j * P1 + q], bx);
-      by = fma(sDTW[j * P1 + q], Fy[q * P1 + i], by);
+      bx = fma(sDTW[i * (P1 + 1) + q], Fx[j * P1 + q], bx);
+      by = fma(sDTW[j * (P1 + 1) + q], Fy[q * P1 + i], by);
     }
     if (i == P) bx += GF[(FR * P1 + j) * NCV + c];
     if (i == 0) bx -= GF[(FL * P1 + j) * NCV + c];
-    bx -= op.sx * (0.5 * LF[(FR * P1 + j) * NCV + c]) * sD[P * P1 + i];
+    bx -= op.sx * (0.5 * LF[(FR * P1 + j) * NCV + c]) * sD[P * (P1 + 1) + i];
     bx -= op.sx * (0.5 * LF[(FL * P1 + j) * NCV + c]) * sD[i];
     if (j == P) by += GF[(FT * P1 + i) * NCV + c];
     if (j == 0) by -= GF[(FB * P1 + i) * NCV + c];
-    by -= op.sy * (0.5 * LF[(FT * P1 + i) * NCV + c]) * sD[P * P1 + j];
+    by -= op.sy * (0.5 * LF[(FT * P1 + i) * NCV + c]) * sD[P * (P1 + 1) + j];
     by -= op.sy * (0.5 * LF[(FB * P1 + i) * NCV + c]) * sD[j];
     const double fv = -bx / (hx * sW[i]) + -by / (hy * sW[j]);
     const long long g = nidx(op, c, ey, ex, j, i);
