@@ -45,15 +45,15 @@ struct Prim {
   double rho, vx, vy, Es, nu;
 };
 __device__ __forceinline__ Prim prim(const Op2DDev& op, const double* s) {
-  const double rho = s[0];
-  return Prim{rho, s[1] / rho, s[2] / rho, s[3] / rho, op.nu / rho};
+  const double rho = s[0], ir = 1.0 / rho;   // one division per state (the oracle divides four times: <= 1 ulp apart)
+  return Prim{rho, s[1] * ir, s[2] * ir, s[3] * ir, op.nu * ir};
 }
 
 // viscous flux at a node from the state and its gradients (oracle NS2D.visc_flux)
-__device__ __forceinline__ void visc_flux(const Op2DDev& op, const double* s, const double* gx, const double* gy,
-                                          double* Fx, double* Fy) {
+__device__ __forceinline__ void visc_flux(const Op2DDev& op, double gpr, const double* s, const double* gx,
+                                          const double* gy, double* Fx, double* Fy) {
   const Prim q = prim(op, s);
-  const double k = op.gamma * q.nu / op.pr;
+  const double k = q.nu * gpr;   // gpr = gamma / Pr
   const double dxm = gx[1] - q.vx * gx[0], dym = gy[1] - q.vx * gy[0];
   const double dxn = gx[2] - q.vy * gx[0], dyn = gy[2] - q.vy * gy[0];
   const double txx = q.nu * ((4.0 / 3.0) * dxm - (2.0 / 3.0) * dyn);
@@ -66,9 +66,10 @@ __device__ __forceinline__ void visc_flux(const Op2DDev& op, const double* s, co
 }
 
 // G_nn(s) v (oracle NS2D.apply_gnn); axis 0: x-faces, 1: y-faces
-__device__ __forceinline__ void apply_gnn(const Op2DDev& op, const double* s, const double* v, int axis, double* r) {
+__device__ __forceinline__ void apply_gnn(const Op2DDev& op, double gpr, const double* s, const double* v, int axis,
+                                          double* r) {
   const Prim q = prim(op, s);
-  const double k = op.gamma * q.nu / op.pr;
+  const double k = q.nu * gpr;   // gpr = gamma / Pr
   const double a = v[1] - q.vx * v[0], b = v[2] - q.vy * v[0];
   const double r1 = q.nu * (axis == 0 ? (4.0 / 3.0) * a : a);
   const double r2 = q.nu * (axis == 0 ? b : (4.0 / 3.0) * b);
@@ -99,31 +100,36 @@ __device__ __forceinline__ void grad_at(const Op2DDev& op, const double* X, cons
 // one side of a face node: the normal viscous flux q of the staged element X at its node
 // (jx, ix) and g = G_nn(s) [u] with the jump [u] = u- - u+ (sm, sp: the minus / plus states)
 template <int P1>
-__device__ __forceinline__ void face_side(const Op2DDev& op, const double* X, const double* D, int jx, int ix,
-                                          const double* s_mine, const double* jmp, int axis, double* q, double* g) {
+__device__ __forceinline__ void face_side(const Op2DDev& op, double gpr, const double* X, const double* D, int jx,
+                                          int ix, const double* s_mine, const double* jmp, int axis, double* q,
+                                          double* g) {
   double gx[NCV], gy[NCV], Fx[NCV], Fy[NCV];
   grad_at<P1>(op, X, D, jx, ix, gx, gy);
-  visc_flux(op, s_mine, gx, gy, Fx, Fy);
-  apply_gnn(op, s_mine, jmp, axis, g);
+  visc_flux(op, gpr, s_mine, gx, gy, Fx, Fy);
+  apply_gnn(op, gpr, s_mine, jmp, axis, g);
 #pragma unroll
   for (int c = 0; c < NCV; ++c) q[c] = axis == 0 ? Fx[c] : Fy[c];
 }
 
 template <int P1>
-__global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* __restrict__ u, double* __restrict__ f,
+__global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 1) k2_visc(Op2DDev op, const double* __restrict__ u, double* __restrict__ f,
                                                       int m_first, int accumulate, int* status) {
   using L = Vb<P1>;
   constexpr int NN = P1 * P1, P = P1 - 1;
   extern __shared__ double sm[];
-  __shared__ double sD[P1 * (P1 + 1)], sDTW[P1 * (P1 + 1)], sW[P1];
+  __shared__ double sD[P1 * (P1 + 1)], sDTW[P1 * (P1 + 1)], sW[P1], sWy[P1];
   const int m = m_first + blockIdx.y;
+  const double gpr = op.gamma / op.pr;
   const double* um = u + (size_t)m * op.ns;
   double* fm = f + (size_t)m * op.ns;
   for (int t = threadIdx.x; t < NN; t += blockDim.x) {
     sD[(t / P1) * (P1 + 1) + t % P1] = op.tab[TabOff::D(P1) + t];
     sDTW[(t / P1) * (P1 + 1) + t % P1] = op.tab[TabOff::DTW(P1) + t];
   }
-  for (int t = threadIdx.x; t < P1; t += blockDim.x) sW[t] = op.tab[TabOff::w(P1) + t];
+  for (int t = threadIdx.x; t < P1; t += blockDim.x) {   // 1 / (h w_i): the divergence divides by the mass
+    sW[t] = 1.0 / (0.5 * op.dx * op.tab[TabOff::w(P1) + t]);
+    sWy[t] = 1.0 / (0.5 * op.dy * op.tab[TabOff::w(P1) + t]);
+  }
   const int ne = op.nex * op.ney;
   const int e0 = blockIdx.x * L::EB;
   // ---- stage own + face neighbours, all fields (coalesced element runs)
@@ -132,18 +138,20 @@ __global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* 
     const int k = r / (NCV * NN), r2 = r - k * (NCV * NN);
     const int c = r2 / NN, nd = r2 - c * NN;
     const int eg = e0 + el;
-    double v = 0.0;
-    if (eg < ne) {
+    if (eg < ne) {   // asynchronous copies: all of a thread's loads in flight at once
       const int oy = eg / op.nex, ex = eg - oy * op.nex, ey = oy + op.row0;
       int sx_ = ex, sy_ = ey;
       if (k == 1) sx_ = ex + 1 == op.nex ? 0 : ex + 1;
       if (k == 2) sx_ = ex == 0 ? op.nex - 1 : ex - 1;
       if (k == 3) sy_ = ynb(op, ey, 1);
       if (k == 4) sy_ = ynb(op, ey, -1);
-      v = um[nidx(op, c, sy_, sx_, 0, 0) + nd];
+      const unsigned d = (unsigned)__cvta_generic_to_shared(sm + L::U + t);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(um + nidx(op, c, sy_, sx_, 0, 0) + nd) : "memory");
+    } else {
+      sm[L::U + t] = 0.0;
     }
-    sm[L::U + t] = v;
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int el = threadIdx.x / NN, nd = threadIdx.x - el * NN;
   const int j = nd / P1, i = nd - j * P1;
@@ -155,7 +163,7 @@ __global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* 
 #pragma unroll
     for (int c = 0; c < NCV; ++c) s[c] = Uo[c * NN + nd];
     grad_at<P1>(op, Uo, sD, j, i, gx, gy);
-    visc_flux(op, s, gx, gy, Fx, Fy);
+    visc_flux(op, gpr, s, gx, gy, Fx, Fy);
 #pragma unroll
     for (int c = 0; c < NCV; ++c) {
       sm[L::FX + (el * NCV + c) * NN + nd] = Fx[c];
@@ -187,8 +195,8 @@ __global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* 
         sp_[c] = Xp[c * NN + jp * P1 + ip];
         jmp[c] = sm_[c] - sp_[c];
       }
-      if (side) face_side<P1>(op, Xp, sD, jp, ip, sp_, jmp, axis, q, g);
-      else face_side<P1>(op, Xm, sD, jm, im, sm_, jmp, axis, q, g);
+      if (side) face_side<P1>(op, gpr, Xp, sD, jp, ip, sp_, jmp, axis, q, g);
+      else face_side<P1>(op, gpr, Xm, sD, jm, im, sm_, jmp, axis, q, g);
       double* xs = XS + (fc * P1 + k) * 2 * NCV;
       if (act && side) {
 #pragma unroll
@@ -212,7 +220,6 @@ __global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* 
   const int oy = eg / op.nex, ex = eg - oy * op.nex, ey = oy + op.row0;
   const double* GF = sm + L::GF + el * 4 * P1 * NCV;
   const double* LF = sm + L::LF + el * 4 * P1 * NCV;
-  const double hx = 0.5 * op.dx, hy = 0.5 * op.dy;
   bool bad = false;
 #pragma unroll
   for (int c = 0; c < NCV; ++c) {
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(Vb<P1>::NT) k2_visc(Op2DDev op, const double* 
     if (j == 0) by -= GF[(FB * P1 + i) * NCV + c];
     by -= op.sy * (0.5 * LF[(FT * P1 + i) * NCV + c]) * sD[P * (P1 + 1) + j];
     by -= op.sy * (0.5 * LF[(FB * P1 + i) * NCV + c]) * sD[j];
-    const double fv = -bx / (hx * sW[i]) + -by / (hy * sW[j]);
+    const double fv = -bx * sW[i] + -by * sWy[j];
     const long long g = nidx(op, c, ey, ex, j, i);
     const double out = accumulate ? fm[g] + fv : fv;
     fm[g] = out;
