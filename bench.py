@@ -398,7 +398,10 @@ def measure(w, args, torch, rt, rank, world, local, steps, warmup, clock=True, e
     peak, peak_kind = measured_hbm_peak()
     achieved = bytes_cg / t_cg / 1e9
     if is2d:
-        kern = "k2_cg<8,4> (grid-persistent cooperative Jacobi-PCG; phase B warp-per-element on fp64 mma.m8n8k4)"
+        kern = ("one P=7 implicit solve = k2_coef + k2p_dinv + k2_cg<8,4> (setup) + k2_cgf<4> (grid-persistent "
+                "fused single-pass Jacobi-PCG iterations: vector update + matvec in one pass per iteration, u rebuilt "
+                "on chip from double-buffered r/s/w, TMA bulk staging, fp64 mma.m8n8k4 contractions); kernel_us "
+                "and traffic are per solve, summed over the four launches")
         note = ("8N[(3+V)+k(10+V)] bytes per solve (SURVEY 8d), V=1/4: one scalar coefficient per node shared by "
                 f"the 4 fields; fine level {8 * hier.fine.ctx.ndof / 1e6:.0f} MB per vector, HBM resident")
         data = f"synthetic seeded IC (SURVEY 8d): {w.name}, no dataset"

@@ -165,6 +165,7 @@ int sisdc_ctx_create(int device, sisdc_ctx** out) {
   if (e == cudaSuccess) e = cudaMalloc(&c.d_status, 4 * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&c.d_log_it, c.log_cap * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&c.d_log_margin, c.log_cap * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c.d_cg1g, CG1G_DOUBLES * sizeof(double));   // at creation: graph-safe
   if (e != cudaSuccess) {
     delete x;
     return SISDC_ERR_CUDA;
@@ -188,6 +189,7 @@ void sisdc_ctx_destroy(sisdc_ctx* x) {
   cudaFree(x->c.d_log_it);
   cudaFree(x->c.d_log_margin);
   cudaFree(x->c.d_timing);
+  cudaFree(x->c.d_cg1g);
   delete x;
 }
 

@@ -22,6 +22,7 @@
 //    exactly the owner's operations, so u's halo needs no extra exchange.
 // One mbarrier wait per iteration; slot/halo buffers alternate by parity.
 #include <cooperative_groups.h>
+#include <string>
 #include <type_traits>
 #include "sisdc_dev.cuh"
 #include "sisdc_host.h"
@@ -59,6 +60,10 @@ struct CgArgs {
   double* log_margin;
   int log_cap;
   long long* timing;   // diagnostics: clock64 stamps of CTA 0 (nullable)
+  // grid mode (levels beyond one cluster: K > 16 CTAs of a cooperative launch, CL = false): halo and
+  // reduction exchange through global memory, one grid barrier per exchange.  Layout (doubles):
+  // HXD [K][4 P1] | HU0 [K][2 P1] | HRWS [2][K][8 P1] | slots [2][K][NVS]
+  double* gws;
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -167,6 +172,13 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   const Op1DDev& op = A.op;
   int rank = 0;
   if constexpr (CL) rank = (int)cg::this_cluster().block_rank();
+  const bool GM = !CL && A.K > 1;   // grid mode
+  if (GM) rank = blockIdx.x;
+  cg::grid_group grid = cg::this_grid();
+  double* const gHXD = A.gws;
+  double* const gHU0 = gHXD + (size_t)A.K * 4 * P1;
+  double* const gHRWS = gHU0 + (size_t)A.K * 2 * P1;
+  double* const gSLOT = gHRWS + (size_t)2 * A.K * 8 * P1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int P1P = padded(P1);
   const CgShared<P1> s = carve<P1>(sm, A.E, blockDim.x);
@@ -436,6 +448,23 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     }
     if constexpr (CL) phase ^= 1;
     __syncthreads();
+    if (GM) {   // CTA totals -> global slots, grid barrier (also publishes the halo), sum in rank order
+      double* slots = gSLOT + (size_t)par * K * NVS;
+      if (threadIdx.x < NR) slots[(size_t)rank * NVS + threadIdx.x] = s.bcast[threadIdx.x];
+      __threadfence();
+      grid.sync();
+      if (wid == 0) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {   // lane-strided over the ranks, then the butterfly: one fixed order everywhere
+          double q = 0.0;
+          for (int m = lane; m < K; m += 32) q += __ldcg(slots + (size_t)m * NVS + j);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+          if (lane == 0) s.bcast[j] = q;
+        }
+      }
+      __syncthreads();
+    }
 #pragma unroll
     for (int j = 0; j < NR; ++j) v[j] = s.bcast[j];
   };
@@ -488,6 +517,13 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     if (pushL) st_async2(tL[0], x, dinv, mL[2]);
     if (pushR) st_async2(tR[0], x, dinv, mR[2]);
     mbar_wait(mb[2], 0);
+  } else if (GM) {   // my last element is the right neighbour's left halo, my first the left one's right halo
+    if (own && last) { double* g = gHXD + (size_t)rR * 4 * P1; g[2 * i] = x; g[2 * i + 1] = dinv; }
+    if (own && first) { double* g = gHXD + (size_t)rL * 4 * P1; g[2 * (P1 + i)] = x; g[2 * (P1 + i) + 1] = dinv; }
+    __threadfence();
+    grid.sync();
+    if (threadIdx.x < 4 * P1) s.HXD[threadIdx.x] = __ldcg(gHXD + (size_t)rank * 4 * P1 + threadIdx.x);
+    __syncthreads();
   } else {
     if (own && last) { s.HXD[2 * i] = x; s.HXD[2 * i + 1] = dinv; }
     if (own && first) { s.HXD[2 * (P1 + i)] = x; s.HXD[2 * (P1 + i) + 1] = dinv; }
@@ -511,6 +547,12 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     if (pushL) st_async(tL[1], u, mL[3]);
     if (pushR) st_async(tR[1], u, mR[3]);
     mbar_wait(mb[3], 0);
+  } else if (GM) {
+    if (own && last) gHU0[(size_t)rR * 2 * P1 + i] = u;
+    if (own && first) gHU0[(size_t)rL * 2 * P1 + P1 + i] = u;
+    __threadfence();
+    grid.sync();
+    if (threadIdx.x < 2 * P1) s.HU0[threadIdx.x] = __ldcg(gHU0 + (size_t)rank * 2 * P1 + threadIdx.x);
   } else {
     if (own && last) s.HU0[i] = u;
     if (own && first) s.HU0[P1 + i] = u;
@@ -530,6 +572,13 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
       } else {
         if (pushL) st_async(tL[2 + par] + 8, w, mL[par]);
         if (pushR) st_async(tR[2 + par] + 8, w, mR[par]);
+      }
+    } else if (GM) {   // published by the grid barrier of the reduction that follows
+      if (own && last) { double* h = gHRWS + ((size_t)par * K + rR) * 8 * P1; h[4 * i] = r; h[4 * i + 1] = w; }
+      if (own && first) {
+        double* h = gHRWS + ((size_t)par * K + rL) * 8 * P1;
+        h[4 * (P1 + i)] = r;
+        h[4 * (P1 + i) + 1] = w;
       }
     } else {
       double* h = s.HRWS + par * 8 * P1;
@@ -562,12 +611,13 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     // neighbour u_{k+1} from its pushed (r, w, s): the owner's exact operations
     if (helper) {   // warp 0 rebuilds the neighbours' u: their s and r advanced here, w pushed
       if (lane < 2 * P1) {
-        const double* h = s.HRWS + par * 8 * P1 + 4 * lane;
+        const double* h = GM ? gHRWS + ((size_t)par * K + rank) * 8 * P1 + 4 * lane : s.HRWS + par * 8 * P1 + 4 * lane;
+        const double h0 = GM ? __ldcg(h) : h[0], h1 = GM ? __ldcg(h + 1) : h[1];   // L1 may hold the line of two iterations ago
         if (k == 0) {   // r0 from the setup push, s_{-1} = 0
-          hr = h[0];
+          hr = h0;
           hs = 0.0;
         }
-        hs = fma(beta, hs, h[1]);
+        hs = fma(beta, hs, h1);
         hr = fma(-alpha, hs, hr);
         s.HU[lane] = hr * s.HD[lane];
       }
@@ -621,7 +671,8 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   }
 }
 
-// Partition: one thread per node, at most 384 nodes per CTA and 16 CTAs.
+// Partition: one thread per node, at most 384 nodes per CTA and 16 CTAs (one cluster).
+// Returns -1 when the level needs more: the caller falls back to the grid mode.
 static int choose_partition(const Ctx* c, int ne, int p1, int& K, int& E) {
   int want = c->cluster_ctas > 0 ? c->cluster_ctas : (ne * p1 + 287) / 288;   // ~288 nodes per CTA
   K = want < 1 ? 1 : (want > 16 ? 16 : want);
@@ -635,9 +686,42 @@ static int choose_partition(const Ctx* c, int ne, int p1, int& K, int& E) {
   return E * p1 <= 384 ? 0 : -1;
 }
 
+// resident blocks of the non-cluster instantiation (grid mode: cooperative launch)
+template <int P1, bool DIR>
+static int cg_grid_capacity(Ctx* c, int threads, size_t smem, int* cap) {
+  int per_sm = 0, sms = 0;
+  cudaError_t e = cudaFuncSetAttribute(k_cg1d<false, P1, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg1d<false, P1, DIR>, threads, smem);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  if (e != cudaSuccess) return c->cuda(e, "cg1d grid occupancy");
+  *cap = per_sm * sms;
+  return SISDC_OK;
+}
+
 template <int P1, bool DIR>
 static int launch_cg_t(Ctx* c, CgArgs& A, int threads, size_t smem) {
   static bool attr_done[2] = {false, false};
+  if (A.gws != nullptr) {   // grid mode: K > 16 blocks of a cooperative launch
+    int cap = 0;
+    if (int rc = cg_grid_capacity<P1, DIR>(c, threads, smem, &cap)) return rc;
+    if (A.K > cap || A.K > CG1G_MAXK)
+      return c->fail(SISDC_ERR_UNSUPPORTED, "implicit_solve: level too large for the grid-mode CG (" +
+                                                std::to_string(A.K) + " blocks of 384 nodes, " +
+                                                std::to_string(cap < CG1G_MAXK ? cap : CG1G_MAXK) + " resident)");
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(A.K);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_cg1d<false, P1, DIR>, A);
+    if (e != cudaSuccess) return c->cuda(e, "cg1d grid-mode launch");
+    return c->after_launch("cg1d (grid mode)");
+  }
   if (A.K == 1) {
     if (!attr_done[0]) {
       cudaFuncSetAttribute(k_cg1d<false, P1, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -685,14 +769,21 @@ int launch_cg1d(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rh
                 const StageFuse* sf) {
   const int p1 = op.p1;
   int K, E;
-  if (choose_partition(c, op.ne, p1, K, E))
-    return c->fail(SISDC_ERR_UNSUPPORTED, "implicit_solve: level too large for the cluster-resident CG "
-                                          "(more than 16 CTAs x 384 nodes)");
+  bool grid_mode = false;
+  if (choose_partition(c, op.ne, p1, K, E)) {
+    // beyond one cluster (16 CTAs x 384 nodes): the same kernel in grid mode, ~384 nodes per block
+    E = 384 / p1;
+    K = (op.ne + E - 1) / E;
+    E = (op.ne + K - 1) / K;   // balanced, no empty block
+    K = (op.ne + E - 1) / E;
+    grid_mode = true;
+  }
   int threads = ((E * p1 + 31) / 32) * 32;
   if (threads < 64) threads = 64;
   size_t smem = cg_smem_bytes(p1, E, threads);
   CgArgs A{};
   A.op = op; A.coef = k; A.a = a; A.rhs = rhs; A.x = x;
+  A.gws = grid_mode ? c->d_cg1g : nullptr;
   if (sf) {
     if (sf->M > MAXM) return c->fail(SISDC_ERR_ARG, "too many collocation nodes");
     A.stage = 1;

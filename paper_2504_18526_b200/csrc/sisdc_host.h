@@ -21,6 +21,7 @@ struct Ctx {
   double* d_log_margin = nullptr; // per-solve ||r||/(rtol ||b||)
   int log_cap = 1 << 16;
   long long* d_timing = nullptr;  // SISDC_CG_TIMING=1: CG clock64 stamps [66]
+  double* d_cg1g = nullptr;       // grid-mode 1-D CG: halo / reduction exchange buffers (CG1G_DOUBLES)
   double rtol = 1e-14;
   int maxit = 1000;
   int cluster_ctas = 0;
@@ -47,6 +48,9 @@ struct Ctx {
     return SISDC_OK;
   }
 };
+
+constexpr int CG1G_MAXK = 1024;                       // grid-mode 1-D CG: most blocks of one solve
+constexpr size_t CG1G_DOUBLES = (size_t)CG1G_MAXK * (22 * 16 + 12);
 
 int launch_apply_convection(Ctx* c, const Op1DDev& op, const double* u, double* out);
 int launch_apply_diffusion(Ctx* c, const Op1DDev& op, CoefDev k, const double* u, double* out);
