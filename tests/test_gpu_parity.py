@@ -181,6 +181,28 @@ def test_grid_mode_cg_beyond_one_cluster(rt, ne, P, bc):
     rt.raise_on_failure()
 
 
+def test_mlsdc_step_on_a_level_beyond_one_cluster(rt):
+    """One SI-MLSDC step of the cfg2 workload on 1024 elements (fine level 9216
+    DOFs: grid-mode CG; coarse level 5120: cluster CG) against the oracle
+    sweeper with the pinned PCG: <= 1e-11, the same CG iteration sequence."""
+    import dataclasses
+    from paper_2504_18526_b200 import dgsem, mlsdc
+    w = dataclasses.replace(CFG2, n_elem=1024)
+    hier = gpu_hier(w)
+    u0 = w.initial_state(dgsem.Mesh1D(w.x_left, w.x_right, w.n_elem, w.p_fine).ref_nodes)
+    dt, _ = w.time_step(u0, dgsem.compute_delta(w.p_fine))
+    n0 = rt.status()[2]
+    sol = mlsdc.run_mlsdc(hier, u0, 0.0, dt, w.n_cycles, strategy="fmg")
+    rt.raise_on_failure()
+    its, mg = new_log_slice(rt, n0)
+    h, log = workloads.build_hierarchy(w, solver="pcg")
+    ref = osw.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, "fmg").u[-1]
+    assert l2rel(sol.u[-1], ref) < 1e-11
+    assert len(its) == len(log)
+    for k, (a, (b, mb)) in enumerate(zip(its, log)):
+        assert a == b or (abs(a - b) == 1 and max(float(mg[k]), mb) >= 0.85), (k, a, b, float(mg[k]), mb)
+
+
 # ---------------------------------------------------- sweeps and slabs
 @pytest.mark.parametrize("tag,w", [("cfg1", CFG1), ("cfg2", CFG2)])
 def test_predict_and_sweeps_vs_oracle(rt, golden, tag, w):
