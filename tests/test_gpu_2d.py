@@ -125,10 +125,12 @@ def test_mlsdc_step_2d_shapes(rt, base, nex, ney):
     rt.raise_on_failure()
 
 
-@pytest.mark.parametrize("nex,ney,P", [(16, 12, 7), (13, 9, 3), (9, 17, 7)])
+@pytest.mark.parametrize("nex,ney,P", [(16, 12, 7), (13, 9, 3), (9, 17, 7), (33, 8, 7), (1, 9, 7), (40, 17, 7), (2, 1, 7)])
 def test_implicit_solve_2d_larger(rt, nex, ney, P):
     """Implicit solves on meshes with many strip tiles / warps (and strips that
-    do not divide the row): identical iterations and solution vs restatement."""
+    do not divide the row): identical iterations and solution vs restatement.
+    P = 7 runs the fused single-pass kernel: ragged bands (ney % 8), ragged and
+    single-element strips (nex % 16, nex = 1), one-row meshes."""
     w = small(CFG4, nex, ney)
     op, orc, u = pair(w, P)
     for a in (2e-3, 5e-2):
