@@ -19,6 +19,7 @@ from typing import Callable, Optional
 
 import numpy as np
 
+from .trace import traced
 from . import _lib
 from .collocation import CollocationRule, QuadratureWeights, make_nodes, make_weights
 from .sdc import NodalSolution, _alloc, from_nodes, predict, refresh_caches, sweep
@@ -87,6 +88,7 @@ def fas_residual(level: Level, dt: float, form: str = "incremental"):
                               sign=-1.0, add=level.g)
 
 
+@traced("sisdc.fas_rhs")
 def fas_rhs(hier: Hierarchy, i: int, dt: float):
     """Compose the FAS right-hand side of level i from level i+1 and store the
     restricted solution v on level i (``mlsdc.py:90-101``)."""
@@ -121,6 +123,7 @@ def fas_rhs(hier: Hierarchy, i: int, dt: float):
     return g
 
 
+@traced("sisdc.sweep_level")
 def _sweep_level(hier: Hierarchy, i: int, dt: float, n: int) -> None:
     lv = hier.levels[i]
     for _ in range(n):
@@ -132,6 +135,7 @@ def _sweep_level(hier: Hierarchy, i: int, dt: float, n: int) -> None:
             hier.coarse_passes += 1
 
 
+@traced("sisdc.v_cycle")
 def v_cycle(hier: Hierarchy, dt: float, top: Optional[int] = None, final: bool = False) -> None:
     """One multigrid cycle over levels[0..top] (``mlsdc.py:110-131``)."""
     if top is None:
@@ -171,6 +175,7 @@ def _interp_up(hier: Hierarchy, i: int, dt: float) -> None:
     up.sol = from_nodes(up.ctx, up.rule, dt, up.scheme, up.u0, up.t0, buf.u, out=buf)
 
 
+@traced("sisdc.start")
 def start(hier: Hierarchy, strategy: str, dt: float, c_fmg: int = 1) -> None:
     """Initial iterates on every level (``mlsdc.py:145-182``)."""
     L = len(hier.levels)
@@ -209,6 +214,7 @@ def start(hier: Hierarchy, strategy: str, dt: float, c_fmg: int = 1) -> None:
     raise ValueError(f"unknown start strategy {strategy!r}")
 
 
+@traced("sisdc.begin_slab")
 def begin_slab(hier: Hierarchy, u0_fine, t0: float, dt: float) -> None:
     """Slab-start states on all levels, coarse ones by spatial projection
     (``mlsdc.py:185-200``)."""
@@ -236,6 +242,7 @@ def begin_slab(hier: Hierarchy, u0_fine, t0: float, dt: float) -> None:
             lv.ctx.begin_slab(lv.u0, t0, dt)
 
 
+@traced("sisdc.run_mlsdc")
 def run_mlsdc(hier: Hierarchy, u0_fine, t0: float, dt: float, n_cycles: int, strategy: str = "predictor",
               c_fmg: int = 1, observer: Optional[Callable] = None) -> NodalSolution:
     """One slab: start, n_cycles V-cycles, closing fine sweep (``mlsdc.py:203-234``)."""

@@ -20,6 +20,7 @@ from typing import Callable, Optional
 
 import numpy as np
 
+from .trace import traced
 from . import _lib
 from ._lib import Coef
 from .collocation import CollocationRule, QuadratureWeights
@@ -99,6 +100,7 @@ def _caches(ctx, scheme, sol, M, m_first, m_count, dts, conv_prev=None, times=No
             ctx.add_source(sol.f[m], sol.u[m], times[m])
 
 
+@traced("sisdc.refresh_caches")
 def refresh_caches(ctx, rule: CollocationRule, dt: float, scheme: str, sol: NodalSolution) -> None:
     """Rebuild all caches after node values changed outside a sweep
     (``sdc.py:101-119``): one kernel over all M nodes."""
@@ -119,12 +121,14 @@ def _stage(ctx, base, conv_in, dt_m, f_old, w_row, dt, g_m, h_old, rhs, conv_out
         rhs.data_ptr(), None if conv_out is None else conv_out.data_ptr()), "stage_rhs")
 
 
+@traced("sisdc.solve")
 def _solve(ctx, coef: Coef, a, rhs, out, t=0.0):
     rt = _rt(ctx)
     rt.check(rt.lib.sisdc_implicit_solve(ctx.h, coef, float(a), rhs.data_ptr(), float(t), out.data_ptr()),
              "implicit_solve")
 
 
+@traced("sisdc.stage_solve")
 def _stage_solve(ctx, coef: Coef, a, base, conv_in, dt_m, f_old, w_row, dt, g_m, h_old, t_conv, t_solve,
                  rhs, conv_out, out):
     """Stage rhs + implicit solve; on 1-D levels the stage runs inside the CG
@@ -156,6 +160,7 @@ def _substep(ctx, scheme, up, dtm, f_old, w_row, dt, g_m, h1_old, h2_old, out, t
     return s["conv"]
 
 
+@traced("sisdc.predict")
 def predict(ctx, rule, dt, scheme, u0, t0, out: Optional[NodalSolution] = None) -> NodalSolution:
     """0-th iterate by marching the substepper (``sdc.py:122-156``)."""
     _rt(ctx).bind_stream()
@@ -193,6 +198,7 @@ def from_nodes(ctx, rule, dt, scheme, u0, t0, u_nodes, out: Optional[NodalSoluti
     return sol
 
 
+@traced("sisdc.sweep")
 def sweep(ctx, rule: CollocationRule, weights: QuadratureWeights, dt: float, scheme: str,
           sol: NodalSolution, g=None, form: Form = "incremental",
           out: Optional[NodalSolution] = None) -> NodalSolution:
@@ -302,6 +308,7 @@ def residual(rule, weights, dt, sol, g=None, form: Form = "incremental", ctx=Non
     return collocation_defect(rule, weights, dt, sol, form, ctx=ctx, sign=-1.0, add=g)
 
 
+@traced("sisdc.run_sdc")
 def run_sdc(ctx, rule, weights, dt, scheme, u0, t0, n_sweeps, form: Form = "incremental",
             start: str = "predictor", observer: Optional[Callable] = None) -> NodalSolution:
     """Predictor (or constant start) plus n_sweeps corrections (``sdc.py:322-354``)."""

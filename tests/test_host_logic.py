@@ -84,3 +84,26 @@ def test_h_transfer_blocks_match_reference(golden):
     sp = build_spatial_p_transfer(3, 7, 5, 1, "l2")
     v = np.einsum("ij,ej->ei", sp.blocks["project"], G["p_l2_uf"].reshape(5, 8)).reshape(-1)
     assert np.abs(v - G["p_l2_project"]).max() < 1e-13
+
+
+def test_nvtx_ranges_wrap_the_sweep_entry_points(monkeypatch):
+    """SISDC_NVTX=1 puts every host entry point of the sweep path in a named NVTX range."""
+    import importlib
+    import torch
+    from paper_2504_18526_b200 import trace
+    calls = []
+    monkeypatch.setattr(torch.cuda.nvtx, "range_push", lambda n: calls.append(("push", n)))
+    monkeypatch.setattr(torch.cuda.nvtx, "range_pop", lambda: calls.append(("pop", None)))
+    monkeypatch.setattr(trace, "ENABLED", True)
+    f = trace.traced("sisdc.unit")(lambda x: x + 1)
+    assert f(1) == 2 and calls == [("push", "sisdc.unit"), ("pop", None)]
+    with pytest.raises(ZeroDivisionError):
+        trace.traced("sisdc.err")(lambda: 1 / 0)()
+    assert calls[-1] == ("pop", None)          # the range closes on exceptions too
+    monkeypatch.setattr(trace, "ENABLED", False)
+    g = lambda: 0                               # noqa: E731
+    assert trace.traced("x")(g) is g            # disabled: the function itself, no wrapper
+    from paper_2504_18526_b200 import mlsdc, sdc
+    src = open(mlsdc.__file__).read() + open(sdc.__file__).read()
+    for name in ("v_cycle", "start", "run_mlsdc", "sweep", "predict", "solve"):
+        assert f'@traced("sisdc.{name}")' in src
