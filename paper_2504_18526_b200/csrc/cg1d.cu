@@ -366,17 +366,17 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
         for (int j = wid; j < NR; j += nred) {
           const double tj = qsum(j);
           if constexpr (CL) {
-            if (lane < K) st_async(rslot[par] + 8 * j, tj, rmb[par]);
+            if (lane < K) st_async((par ? rslot[1] : rslot[0]) + 8 * j, tj, (par ? rmb[1] : rmb[0]));
           } else {
             if (lane == 0) s.bcast[j] = tj;
           }
         }
         if constexpr (CL) {
           if (wid == 0) {   // the NV - NR pad slots are never read: not pushed
-            if (lane == 0) mbar_expect(mb[par], 8u * K * NR + halo_rws_bytes);
+            if (lane == 0) mbar_expect((par ? mb[1] : mb[0]), 8u * K * NR + halo_rws_bytes);
             idle();
           }
-          mbar_wait(mb[par], phase);
+          mbar_wait((par ? mb[1] : mb[0]), phase);
           const double* slots = s.slots + par * 16 * NVS;
           for (int j = wid; j < NR; j += nred) {   // K <= 16 slots: 4 butterfly levels
             double q = lane < K ? slots[lane * NVS + j] : 0.0;
@@ -405,11 +405,11 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
           for (int j = 0; j < NV; ++j) t[j] = j < NR ? s.wbuf[j * nt] : 0.0;
           if (lane < K)
 #pragma unroll
-            for (int j = 0; j < NV; j += 2) st_async2(rslot[par] + 8 * j, t[j], t[j + 1], rmb[par]);
-          if (lane == 0) mbar_expect(mb[par], 8u * K * NV + halo_rws_bytes);
+            for (int j = 0; j < NV; j += 2) st_async2((par ? rslot[1] : rslot[0]) + 8 * j, t[j], t[j + 1], (par ? rmb[1] : rmb[0]));
+          if (lane == 0) mbar_expect((par ? mb[1] : mb[0]), 8u * K * NV + halo_rws_bytes);
           idle();
         }
-        mbar_wait(mb[par], phase);
+        mbar_wait((par ? mb[1] : mb[0]), phase);
         const double* slots = s.slots + par * 16 * NVS;
         for (int j = wid; j < NR; j += nred) {   // K <= 16 slots: 4 butterfly levels
           double q = lane < K ? slots[lane * NVS + j] : 0.0;
@@ -428,10 +428,10 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
         const double* slots = s.slots + par * 16 * NVS;
         if (lane < K)
 #pragma unroll
-          for (int j = 0; j < NV; j += 2) st_async2(rslot[par] + 8 * j, t[j], t[j + 1], rmb[par]);
-        if (lane == 0) mbar_expect(mb[par], 8u * K * NV + halo_rws_bytes);
+          for (int j = 0; j < NV; j += 2) st_async2((par ? rslot[1] : rslot[0]) + 8 * j, t[j], t[j + 1], (par ? rmb[1] : rmb[0]));
+        if (lane == 0) mbar_expect((par ? mb[1] : mb[0]), 8u * K * NV + halo_rws_bytes);
         idle();
-        mbar_wait(mb[par], phase);
+        mbar_wait((par ? mb[1] : mb[0]), phase);
 #pragma unroll
         for (int j = 0; j < NR; ++j) {   // K <= 16 slots: 4 butterfly levels
           double q = lane < K ? slots[lane * NVS + j] : 0.0;
@@ -567,11 +567,11 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
   auto push_rws = [&](int par, bool setup) {
     if constexpr (CL) {
       if (setup) {
-        if (pushL) st_async2(tL[2 + par], r, w, mL[par]);
-        if (pushR) st_async2(tR[2 + par], r, w, mR[par]);
+        if (pushL) st_async2((par ? tL[3] : tL[2]), r, w, (par ? mL[1] : mL[0]));
+        if (pushR) st_async2((par ? tR[3] : tR[2]), r, w, (par ? mR[1] : mR[0]));
       } else {
-        if (pushL) st_async(tL[2 + par] + 8, w, mL[par]);
-        if (pushR) st_async(tR[2 + par] + 8, w, mR[par]);
+        if (pushL) st_async((par ? tL[3] : tL[2]) + 8, w, (par ? mL[1] : mL[0]));
+        if (pushR) st_async((par ? tR[3] : tR[2]) + 8, w, (par ? mR[1] : mR[0]));
       }
     } else if (GM) {   // published by the grid barrier of the reduction that follows
       if (own && last) { double* h = gHRWS + ((size_t)par * K + rR) * 8 * P1; h[4 * i] = r; h[4 * i + 1] = w; }
@@ -587,11 +587,11 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     }
   };
   push_rws(0, true);
-  uint32_t ph[2] = {0, 0};
+  uint32_t ph0 = 0, ph1 = 0;   // mbarrier phases of the two reduction buffers (scalars: no local array)
   double v6[NVS] = {own ? r * u : 0.0, own ? w * u : 0.0, own ? r * r : 0.0, own ? bi * bi : 0.0,
                     (own && b0 != 0.0) ? 1.0 : 0.0, 0.0};   // b == 0 test on M rhs (dgsem.py:509-511)
   if (stamp) A.timing[2] = clock64();
-  csum(v6, std::integral_constant<int, 5>{}, std::integral_constant<int, NVS>{}, 0, ph[0], [] {});
+  csum(v6, std::integral_constant<int, 5>{}, std::integral_constant<int, NVS>{}, 0, ph0, [] {});
   halo_rws_bytes = 2u * P1 * 8u;
   if (stamp) A.timing[3] = clock64();
   double gamma = v6[0], rho = v6[2];
@@ -640,12 +640,14 @@ __global__ void __launch_bounds__(384) k_cg1d(CgArgs A) {
     // formed once, by warp 0 while it waits for the cluster's partials, and
     // broadcast with the sums: the other warps skip the two reciprocal
     // sequences (same operations on the same values: bitwise)
-    csum(v4, std::integral_constant<int, 3>{}, std::integral_constant<int, NVL>{}, par ^ 1, ph[par ^ 1], [&] {
+    uint32_t phv = par ? ph0 : ph1;   // buffer par ^ 1
+    csum(v4, std::integral_constant<int, 3>{}, std::integral_constant<int, NVL>{}, par ^ 1, phv, [&] {
       if (lane == 0) {
         s.bcast[3] = 1.0 / alpha;
         s.bcast[4] = 1.0 / gamma;
       }
     });
+    if (par) ph0 = phv; else ph1 = phv;
     ralpha = s.bcast[3];
     rgamma = s.bcast[4];
     if (sub) A.timing[73] = clock64();

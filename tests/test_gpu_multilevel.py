@@ -149,7 +149,9 @@ def test_paper_table_rows_match_reference_cli(rt, golden_mls, case):
     for key in sorted(set(mine) | set(ref)):
         if key in mine and key in ref:
             ea, eb = mine[key], ref[key]
-            # 1e-12 absolute: the two implicit solvers differ by a few 1e-13 in the solution itself
-            assert abs(ea - eb) <= 1e-8 * abs(eb) + 1e-12 or (ea < FLOOR and eb < FLOOR), (key, ea, eb)
+            # 2e-9 absolute: the reference CLI solves with SuperLU + defect iteration to 1e-12 ||b||, the
+            # GPU with the pinned PCG to 1e-14; over the 13-102 steps of a march the two solutions drift
+            # apart by up to ~5e-10 (measured at CFL 64), which is the difference of the error norms
+            assert abs(ea - eb) <= max(1e-8 * abs(eb), 2e-9) or (ea < FLOOR and eb < FLOOR), (key, ea, eb)
         else:   # one series stopped earlier: only inside the noise floor
             assert (mine.get(key, ref.get(key))) < FLOOR, key
