@@ -35,13 +35,13 @@ def ref_problem(w):
     return rp.Burgers(w.params["nu"])
 
 
-def build_ref_hier(w, form="incremental"):
+def build_ref_hier(w, form="incremental", node_convention="nodes_only"):
     ops = [rd.DGOperator(rd.Mesh1D(w.x_left, w.x_right, w.n_elem, P), ref_problem(w))
            for P in (w.p_coarse, w.p_fine)]
     rules = [rc.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
     wts = [rc.make_weights(r) for r in rules]
     levels = [rm.Level(o, r, ww, "si2") for o, r, ww in zip(ops, rules, wts)]
-    pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_only")
+    pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", node_convention)
     spat = rt.build_spatial_p_transfer(w.p_coarse, w.p_fine, w.n_elem, 1, "embedded")
     return rm.Hierarchy(levels, [rt.SpaceTimeTransfer(pair, spat)], n_coarse=2, n_sweep=1,
                         form=form, post_sweep_on_finest=True), ops
@@ -197,6 +197,44 @@ def gen_trajectories():
         out[f"{tag}_sdc2_u"], out[f"{tag}_sdc2_f"] = sol.u, sol.f
         out[f"{tag}_sdc2_h1"], out[f"{tag}_sdc2_h2"] = sol.h1, sol.h2
     np.savez_compressed(os.path.join(OUT, "trajectories.npz"), **out)
+
+
+def gen_t0conv():
+    """node_convention = "nodes_plus_t0" (transfer.py:61-121, cli.py:289): the augmented
+    temporal matrices, apply_temporal on seeded data in every direction, and two
+    reference SI-MLSDC steps of cfg1 (LU as shipped, and with the pinned PCG)."""
+    out = {}
+    w = CFG1
+    rules = [rc.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
+    for kind in ("embedded", "l2"):
+        pair = rt.build_temporal_transfer(rules[0], rules[1], kind, "nodes_plus_t0")
+        out[f"{kind}_interp"], out[f"{kind}_project"], out[f"{kind}_restrict"] = pair.interp, pair.project, pair.restrict
+    pair = rt.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_plus_t0")
+    rng = np.random.default_rng(11)
+    nc, nf, u0 = rng.standard_normal((w.m_coarse, 7)), rng.standard_normal((w.m_fine, 7)), rng.standard_normal(7)
+    out["in_c"], out["in_f"], out["in_u0"] = nc, nf, u0
+    out["ap_interp"] = rt.apply_temporal(pair, "interp", nc, u0)
+    out["ap_project"] = rt.apply_temporal(pair, "project", nf, u0)
+    out["ap_restrict"] = rt.apply_temporal(pair, "restrict", nf)
+    hier, ops = build_ref_hier(w, node_convention="nodes_plus_t0")
+    u_init = w.initial_state(ops[1].mesh.ref_nodes)
+    dt, _ = w.time_step(u_init, rd.compute_delta(w.p_fine))
+    out["u0"], out["dt"] = u_init, np.array(dt)
+    u = u_init
+    for s in range(2):
+        sol = rm.run_mlsdc(hier, u, s * dt, dt, w.n_cycles, strategy="fmg")
+        u = sol.end_value.copy()
+        out[f"lu_u{s + 1}"] = u
+    hier, ops = build_ref_hier(w, node_convention="nodes_plus_t0")
+    with PcgPatch(1e-14, pcg) as pp:
+        u = u_init
+        for s in range(2):
+            n0 = len(pp.log)
+            sol = rm.run_mlsdc(hier, u, s * dt, dt, w.n_cycles, strategy="fmg")
+            u = sol.end_value.copy()
+            out[f"pcg_u{s + 1}"] = u
+            out[f"pcg_iters{s + 1}"] = np.array([it for it, _ in pp.log[n0:]])
+    np.savez_compressed(os.path.join(OUT, "t0conv.npz"), **out)
 
 
 def gen_nonincremental():
@@ -711,6 +749,9 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "cns":
         gen_cns()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "t0conv":
+        gen_t0conv()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "nonincremental":
         gen_nonincremental()
         sys.exit(0)
@@ -727,6 +768,7 @@ if __name__ == "__main__":
     gen_operators()
     gen_trajectories()
     gen_nonincremental()
+    gen_t0conv()
     gen_dirichlet()
     gen_presmooth()
     gen_htransfer()

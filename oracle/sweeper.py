@@ -200,14 +200,19 @@ class PTransfer:
     in ``SpaceTimeTransfer`` (``transfer.py:324-352``); embedded projection,
     nodes_only convention."""
 
-    def __init__(self, ctx_c, ctx_f, rule_c, rule_f):
+    def __init__(self, ctx_c, ctx_f, rule_c, rule_f, t0=False):
         self.nc, self.ne = ctx_f.nc, ctx_f.ne
         self.pc, self.pf = ctx_c.p1, ctx_f.p1
         xc, xf = quad.gll(self.pc)[0], quad.gll(self.pf)[0]
         self.Isp = quad.lagrange(xc, xf)
         self.Psp = quad.lagrange(xf, xc)
-        self.It = quad.lagrange(rule_c.tau, rule_f.tau)
-        self.Pt = quad.lagrange(rule_f.tau, rule_c.tau)
+        # nodes_plus_t0 (transfer.py:77-79, 98-121): t = 0 joins both node sets; interp / project carry
+        # the source level's slab start through column 0, restrictions and corrections pad it with zero
+        self.t0 = bool(t0)
+        tc = np.concatenate(([0.0], rule_c.tau)) if t0 else rule_c.tau
+        tf = np.concatenate(([0.0], rule_f.tau)) if t0 else rule_f.tau
+        self.It = quad.lagrange(tc, tf)
+        self.Pt = quad.lagrange(tf, tc)
 
     def sp(self, A, u, n_in):
         return np.einsum("ij,cej->cei", A, u.reshape(self.nc, self.ne, n_in)).reshape(-1)
@@ -215,16 +220,23 @@ class PTransfer:
     def project_u0(self, u0f):
         return self.sp(self.Psp, u0f, self.pf)
 
-    def project_solution(self, uf):
+    def _tm(self, A, nodes, top):
+        if not self.t0:
+            return np.tensordot(A, nodes, axes=(1, 0))
+        top = np.zeros_like(nodes[0]) if top is None else top
+        return np.tensordot(A, np.concatenate((top[None], nodes), axis=0), axes=(1, 0))[1:]
+
+    def project_solution(self, uf, u0f=None):
         s = np.stack([self.sp(self.Psp, x, self.pf) for x in uf])
-        return np.tensordot(self.Pt, s, axes=(1, 0))
+        return self._tm(self.Pt, s, None if u0f is None else self.sp(self.Psp, u0f, self.pf))
 
     def restrict_residual(self, rf):
         s = np.stack([self.sp(self.Isp.T, x, self.pf) for x in rf])
-        return np.tensordot(self.It.T, s, axes=(1, 0))
+        return self._tm(self.It.T, s, None)
 
-    def interp(self, dc):
-        t = np.tensordot(self.It, dc, axes=(1, 0))
+    def interp(self, dc, u0c=None):
+        """Corrections: t0 carries zero (u0c None); solutions: the coarse slab start."""
+        t = self._tm(self.It, dc, u0c)
         return np.stack([self.sp(self.Isp, x, self.pc) for x in t])
 
 
@@ -270,7 +282,7 @@ def fas_rhs(h, i, dt):
     up, lo, st = h.levels[i + 1], h.levels[i], h.transfers[i]
     F = defect(up.rule, dt, up.sol, h.form)
     r = -F if up.g is None else up.g - F
-    v = st.project_solution(up.sol.u)
+    v = st.project_solution(up.sol.u, up.u0) if getattr(st, "t0", False) else st.project_solution(up.sol.u)
     lo.v = v
     return _defect_state(lo, v, dt, h.form) + st.restrict_residual(r)
 
@@ -307,7 +319,8 @@ def v_cycle(h, dt, top=None, final=False):
 def _interp_up(h, i, dt):
     """``mlsdc.py:134-142`` (no presmoother)."""
     lv, up = h.levels[i], h.levels[i + 1]
-    fine = h.transfers[i].interp(lv.sol.u)
+    st = h.transfers[i]
+    fine = st.interp(lv.sol.u, lv.u0) if getattr(st, "t0", False) else st.interp(lv.sol.u)
     up.sol = from_nodes(up.ctx, up.rule, dt, up.scheme, up.u0, up.t0, fine)
 
 
@@ -377,8 +390,8 @@ def integrate_mlsdc(h, u0f, t0, dt, n_steps, n_cycles, strategy="fmg", c_fmg=1):
 
 
 def build_two_level(make_ctx, rule_c, rule_f, n_coarse=2, n_sweep=1, form="incremental",
-                    post_sweep=True, scheme="si2"):
+                    post_sweep=True, scheme="si2", t0=False):
     """Two-level p-hierarchy as the reference CLI builds it (``cli.py:789-815``)."""
     cc, cf = make_ctx("coarse"), make_ctx("fine")
     levels = [Lev(cc, rule_c, scheme), Lev(cf, rule_f, scheme)]
-    return Hier(levels, [PTransfer(cc, cf, rule_c, rule_f)], n_coarse, n_sweep, form, post_sweep)
+    return Hier(levels, [PTransfer(cc, cf, rule_c, rule_f, t0=t0)], n_coarse, n_sweep, form, post_sweep)

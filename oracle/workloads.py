@@ -8,7 +8,7 @@ def make_problem(w):
     return dg1d.ConvDiff(**w.params) if w.problem == "convdiff" else dg1d.Burgers(**w.params)
 
 
-def build_hierarchy(w, solver="pcg", rtol=1e-14, log=None, form="incremental"):
+def build_hierarchy(w, solver="pcg", rtol=1e-14, log=None, form="incremental", t0=False):
     """Two-level p-hierarchy of workload ``w`` (configs.Workload1D); every
     level appends its CG iterations to the shared ``log`` in call order."""
     log = [] if log is None else log
@@ -18,7 +18,7 @@ def build_hierarchy(w, solver="pcg", rtol=1e-14, log=None, form="incremental"):
         return dg1d.Op1D(w.x_left, w.x_right, w.n_elem, P, make_problem(w), solver=solver, rtol=rtol, cg_log=log)
 
     h = sweeper.build_two_level(mk, sweeper.Rule("radau_right", w.m_coarse), sweeper.Rule("radau_right", w.m_fine),
-                                form=form)
+                                form=form, t0=t0)
     return h, log
 
 

@@ -23,7 +23,7 @@ from .trace import traced
 from . import _lib
 from .collocation import CollocationRule, QuadratureWeights, make_nodes, make_weights
 from .sdc import NodalSolution, _alloc, from_nodes, predict, refresh_caches, sweep
-from .transfer import SpaceTimeTransfer, build_temporal_transfer
+from .transfer import SpaceTimeTransfer, _t0, build_temporal_transfer, temporal_core
 
 
 @dataclass
@@ -106,6 +106,10 @@ def fas_rhs(hier: Hierarchy, i: int, dt: float):
     rt.check(rt.lib.sisdc_xfer_fas_restrict(
         st.handle.h, wp, float(dt), inc, upper.sol.u0.data_ptr(), upper.sol.u.data_ptr(), upper.sol.f.data_ptr(),
         None if upper.g is None else upper.g.data_ptr(), v.data_ptr(), rr.data_ptr()), "fas_restrict")
+    if _t0(st.temporal):   # nodes_plus_t0: v also carries the slab start, whose spatial projection is lower.u0
+        a_p = temporal_core(st.temporal)[3]
+        for m in range(Mc):
+            rt.lincomb(v[m], (1.0, v[m]), (float(a_p[m]), lower.u0))
     lower.v = v
     # coarse defect of v with fresh rhs at the coarse node times (mlsdc.py:68-77)
     times = lower.t0 + dt * lower.rule.tau
@@ -172,6 +176,9 @@ def _interp_up(hier: Hierarchy, i: int, dt: float) -> None:
             rt.copy(src[m], hier.presmooth(lv.sol.u[m]))
     rt.check(rt.lib.sisdc_xfer_interp(hier.transfers[i].handle.h, 0, src.data_ptr(), None,
                                       buf.u.data_ptr()), "interp_solution")
+    st = hier.transfers[i]
+    if _t0(st.temporal):   # nodes_plus_t0: the coarse slab start rides through the interpolation (mlsdc.py:141)
+        st._carry_t0(buf.u, temporal_core(st.temporal)[2], "interp", lv.u0)
     up.sol = from_nodes(up.ctx, up.rule, dt, up.scheme, up.u0, up.t0, buf.u, out=buf)
 
 
@@ -327,7 +334,8 @@ def integrate_mlsdc(hier: Hierarchy, u0_fine, t0: float, dt: float, n_steps: int
 
 def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes: str = "radau_right",
                       n_coarse: int = 2, n_sweep: int = 1, post_sweep_on_finest: bool = True,
-                      restriction: str = None, form: str = "incremental", presmooth=None) -> Hierarchy:
+                      restriction: str = None, form: str = "incremental", presmooth=None,
+                      node_convention: str = "nodes_only") -> Hierarchy:
     """Hierarchy of p-levels on one mesh as the reference CLI builds it
     (``cli.py:776-815``); ``make_op(degree)`` returns a DGOperator."""
     from .transfer import build_spatial_p_transfer, build_spatial_p_transfer_2d
@@ -336,7 +344,7 @@ def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes:
     levels = [Level(o, r, make_weights(r), scheme) for o, r in zip(ops, rules)]
     transfers = []
     for lo, hi in zip(range(len(ops) - 1), range(1, len(ops))):
-        pair = build_temporal_transfer(rules[lo], rules[hi])
+        pair = build_temporal_transfer(rules[lo], rules[hi], node_convention=node_convention)
         if getattr(ops[lo], "is2d", False):
             # element slabs in storage order (a partitioned operator's ghost rows included)
             spatial = build_spatial_p_transfer_2d(degrees[lo], degrees[hi], ops[lo].mesh.nex,
@@ -356,7 +364,8 @@ def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes:
 
 def build_hierarchy(make_op, levels, scheme: str = "si2", nodes: str = "radau_right", n_coarse: int = 2,
                     n_sweep: int = 1, post_sweep_on_finest: bool = True, form: str = "incremental",
-                    projection: str = "embedded", jump_policy: str = "linear_blend") -> Hierarchy:
+                    projection: str = "embedded", jump_policy: str = "linear_blend",
+                    node_convention: str = "nodes_only") -> Hierarchy:
     """Hierarchy from per-level (n_elem, degree, n_nodes), coarsest first, as
     the reference CLI's ``_build_hierarchy`` (``cli.py:789-815``) builds it:
     h-transfer where the element counts differ (2:1), p-transfer where the
@@ -369,7 +378,7 @@ def build_hierarchy(make_op, levels, scheme: str = "si2", nodes: str = "radau_ri
     transfers = []
     for lo in range(len(ops) - 1):
         hi = lo + 1
-        pair = build_temporal_transfer(rules[lo], rules[hi], projection)
+        pair = build_temporal_transfer(rules[lo], rules[hi], projection, node_convention)
         (nc, pc, _), (nf, pf, _) = levels[lo], levels[hi]
         if nc != nf:
             if nf != 2 * nc or pc != pf:

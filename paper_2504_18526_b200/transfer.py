@@ -51,9 +51,13 @@ def build_temporal_transfer(coarse_rule: CollocationRule, fine_rule: Collocation
                             projection_kind: str = "embedded", node_convention: str = "nodes_only") -> TransferPair:
     if coarse_rule.M > fine_rule.M:
         raise ValueError("coarse rule must not have more nodes than the fine one")
-    if node_convention != "nodes_only":
-        raise NotImplementedError("the GPU path builds the nodes_only convention (the reference default)")
-    src, dst = coarse_rule.tau, fine_rule.tau
+    if node_convention == "nodes_only":
+        src, dst = coarse_rule.tau, fine_rule.tau
+    elif node_convention == "nodes_plus_t0":   # t = 0 is a degree of freedom on both sides (transfer.py:77-79)
+        src = np.concatenate(([0.0], coarse_rule.tau))
+        dst = np.concatenate(([0.0], fine_rule.tau))
+    else:
+        raise ValueError(f"unknown node convention {node_convention!r}")
     interp = lagrange_matrix(src, dst)
     if projection_kind == "embedded":
         project = lagrange_matrix(dst, src)
@@ -63,6 +67,47 @@ def build_temporal_transfer(coarse_rule: CollocationRule, fine_rule: Collocation
         raise ValueError(f"unknown projection kind {projection_kind!r}")
     return TransferPair(interp, project, interp.T.copy(), "temporal", projection_kind,
                         {"node_convention": node_convention, "M": (coarse_rule.M, fine_rule.M)})
+
+
+def _t0(pair: TransferPair) -> bool:
+    return pair.meta.get("node_convention") == "nodes_plus_t0"
+
+
+def temporal_core(pair: TransferPair):
+    """(interp, project) node-to-node blocks the GPU transfers apply and the
+    columns (a_interp, a_project) that carry the slab-start value
+    (``transfer.py:98-121``): with nodes_plus_t0 the output node m is
+    A[m+1, 0] u0 + sum_j A[m+1, j+1] nodes[j]; restrictions and corrections pad
+    t0 with zero, i.e. use the block alone.  nodes_only: the matrices, no columns."""
+    if _t0(pair):
+        return (np.ascontiguousarray(pair.interp[1:, 1:]), np.ascontiguousarray(pair.project[1:, 1:]),
+                np.ascontiguousarray(pair.interp[1:, 0]), np.ascontiguousarray(pair.project[1:, 0]))
+    return pair.interp, pair.project, None, None
+
+
+def apply_temporal(pair: TransferPair, direction: Direction, nodes, u0=None):
+    """Apply a temporal pair along the leading (node) axis (``transfer.py:98-121``)
+    to host arrays or device tensors; the output keeps node values only."""
+    A = pair.matrix(direction)
+    is_t = hasattr(nodes, "device") and not isinstance(nodes, np.ndarray)
+    if is_t:
+        import torch
+        A_ = torch.as_tensor(A, dtype=nodes.dtype, device=nodes.device)
+        dot = lambda M, x: torch.tensordot(M, x, dims=([1], [0]))   # noqa: E731
+        cat, zeros = (lambda a, b: torch.cat((a, b), dim=0)), torch.zeros_like
+    else:
+        nodes = np.asarray(nodes)
+        A_, dot = A, (lambda M, x: np.tensordot(M, x, axes=(1, 0)))
+        cat, zeros = (lambda a, b: np.concatenate((a, b), axis=0)), np.zeros_like
+    if _t0(pair):
+        if direction == "restrict":
+            top = zeros(nodes[:1])
+        else:
+            if u0 is None:
+                raise ValueError("nodes_plus_t0 transfers need the source u0")
+            top = (u0 if is_t else np.asarray(u0))[None]
+        return dot(A_, cat(top, nodes))[1:]
+    return dot(A_, nodes)
 
 
 def _gll_reference(n: int) -> np.ndarray:
@@ -247,7 +292,7 @@ class _XferHandle:
             It = Pt = np.ones((1, 1))
             Mc = Mf = 1
         else:
-            It, Pt = temporal.interp, temporal.project
+            It, Pt, _, _ = temporal_core(temporal)
             Mf, Mc = It.shape
         if spatial.kind == "identity":   # same mesh and degree (time-only coarsening): unit blocks per DOF
             Isp = Psp = Rsp = np.ones((1, 1))
@@ -329,8 +374,21 @@ class SpaceTimeTransfer:
     def _nodes(self, npe):
         return npe * npe if self.spatial.kind == "p2d" else npe
 
+    def _carry_t0(self, out, col, direction, u0):
+        """nodes_plus_t0: add the slab-start column, out[m] += col[m] * spatial(u0)."""
+        if u0 is None:
+            raise ValueError("nodes_plus_t0 transfers need the source u0")
+        rt = self.handle.rt
+        s0 = self.spatial.apply(direction, u0)
+        for m in range(out.shape[0]):
+            rt.lincomb(out[m], (1.0, out[m]), (float(col[m]), s0))
+        return out
+
     def project_solution(self, u_nodes_f, u0_f=None):
-        return self._down(1, 1, u_nodes_f)
+        out = self._down(1, 1, u_nodes_f)
+        if _t0(self.temporal):
+            self._carry_t0(out, temporal_core(self.temporal)[3], "project", u0_f)
+        return out
 
     def restrict_residual(self, r_nodes_f):
         return self._down(2, 2, r_nodes_f)
@@ -350,4 +408,7 @@ class SpaceTimeTransfer:
         return self._up(d_nodes_c)
 
     def interp_solution(self, u_nodes_c, u0_c=None):
-        return self._up(u_nodes_c)
+        out = self._up(u_nodes_c)
+        if _t0(self.temporal):
+            self._carry_t0(out, temporal_core(self.temporal)[2], "interp", u0_c)
+        return out

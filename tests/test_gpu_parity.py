@@ -377,3 +377,45 @@ def test_h_transfer_and_h_mlsdc(rt, golden):
     assert its == G["hml_pcg_iters1"].tolist()
     assert l2rel(sol.u[-1], G["hml_pcg_u1"]) < 1e-11
     rt.raise_on_failure()
+
+
+def test_nodes_plus_t0_convention_on_the_gpu(rt):
+    """node_convention = "nodes_plus_t0" (transfer.py:61-121, cli.py:289): SI-MLSDC steps of
+    cfg1 against the reference's own run (tests/golden/t0conv.npz) -- <= 1e-11 vs the
+    reference with the pinned PCG (identical iteration sequence) and vs SuperLU; the
+    space-time transfer entry points and apply_temporal on device tensors."""
+    import os
+    from paper_2504_18526_b200 import mlsdc, transfer
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "t0conv.npz"))
+    w = CFG1
+    hier = mlsdc.build_p_hierarchy(lambda P: gpu_op(w, P), [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine],
+                                   node_convention="nodes_plus_t0")
+    dt = float(G["dt"])
+    for s in (1, 2):
+        u = G["u0"] if s == 1 else G["pcg_u1"]
+        n0 = rt.status()[2]
+        sol = mlsdc.run_mlsdc(hier, u, (s - 1) * dt, dt, w.n_cycles, strategy="fmg")
+        its, _ = new_log_slice(rt, n0)
+        assert its == G[f"pcg_iters{s}"].tolist()
+        assert l2rel(sol.u[-1], G[f"pcg_u{s}"]) < 1e-11
+        if s == 1:
+            assert l2rel(sol.u[-1], G["lu_u1"]) < 1e-11
+    rt.raise_on_failure()
+    # entry points with the slab-start value, against the dense reference matrices
+    st = hier.transfers[0]
+    pair = st.temporal
+    lo, hi = hier.levels
+    rng = np.random.default_rng(5)
+    uf, u0f = rng.standard_normal((hi.rule.M, hi.ctx.ndof)), rng.standard_normal(hi.ctx.ndof)
+    sp = lambda d, x: st.spatial.apply(d, x).cpu().numpy()   # noqa: E731
+    want = transfer.apply_temporal(pair, "project", np.stack([sp("project", x) for x in uf]), sp("project", u0f))
+    assert rel(st.project_solution(uf, u0f), want) < 1e-12
+    uc, u0c = rng.standard_normal((lo.rule.M, lo.ctx.ndof)), rng.standard_normal(lo.ctx.ndof)
+    t = transfer.apply_temporal(pair, "interp", uc, u0c)
+    assert rel(st.interp_solution(uc, u0c), np.stack([sp("interp", x) for x in t])) < 1e-12
+    t = transfer.apply_temporal(pair, "interp", uc, np.zeros_like(u0c))
+    assert rel(st.interp_correction(uc), np.stack([sp("interp", x) for x in t])) < 1e-12
+    with pytest.raises(ValueError):
+        st.project_solution(uf)
+    dev = rt.to_device(G["in_c"])
+    assert rel(transfer.apply_temporal(pair, "interp", dev, rt.to_device(G["in_u0"])), G["ap_interp"]) < 1e-12

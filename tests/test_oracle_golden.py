@@ -289,3 +289,43 @@ def test_cns_dirichlet_sod_pinned_to_reference(golden, case):
         u = sweeper.run_mlsdc(h, u, s * dt, dt, w.n_cycles).u[-1].copy()
         assert np.linalg.norm(u - G[f"{case}_bicg_u{s + 1}"]) / np.linalg.norm(u) < 1e-12
     assert [it for it, _ in log] == G[case + "_bicg_iters"].tolist()
+
+
+def test_nodes_plus_t0_convention_against_reference():
+    """node_convention = "nodes_plus_t0" (transfer.py:61-121): the product's temporal
+    matrices and apply_temporal, and the oracle's two-level MLSDC steps, against
+    the reference's own outputs (tests/golden/t0conv.npz)."""
+    import os
+    from oracle import sweeper as osw, workloads
+    from paper_2504_18526_b200 import collocation, transfer
+    from paper_2504_18526_b200.configs import CFG1 as w
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "t0conv.npz"))
+    rules = [collocation.make_nodes("radau_right", M) for M in (w.m_coarse, w.m_fine)]
+    for kind in ("embedded", "l2"):
+        pair = transfer.build_temporal_transfer(rules[0], rules[1], kind, "nodes_plus_t0")
+        for d in ("interp", "project", "restrict"):
+            assert np.abs(pair.matrix(d) - G[f"{kind}_{d}"]).max() < 1e-12
+    pair = transfer.build_temporal_transfer(rules[0], rules[1], "embedded", "nodes_plus_t0")
+    assert np.abs(transfer.apply_temporal(pair, "interp", G["in_c"], G["in_u0"]) - G["ap_interp"]).max() < 1e-12
+    assert np.abs(transfer.apply_temporal(pair, "project", G["in_f"], G["in_u0"]) - G["ap_project"]).max() < 1e-12
+    assert np.abs(transfer.apply_temporal(pair, "restrict", G["in_f"]) - G["ap_restrict"]).max() < 1e-12
+    with pytest.raises(ValueError):
+        transfer.apply_temporal(pair, "interp", G["in_c"])            # needs the source u0
+    with pytest.raises(ValueError):
+        transfer.build_temporal_transfer(rules[0], rules[1], "embedded", "bogus")
+    # nodes_only: plain matrix product
+    p0 = transfer.build_temporal_transfer(rules[0], rules[1])
+    assert np.abs(transfer.apply_temporal(p0, "interp", G["in_c"]) - p0.interp @ G["in_c"]).max() < 1e-14
+    # the oracle sweeper in both solver modes
+    dt = float(G["dt"])
+    for solver, key, tol in (("lu", "lu_u", 1e-12), ("pcg", "pcg_u", 1e-12)):
+        h, log = workloads.build_hierarchy(w, solver=solver, t0=True)
+        for s in (1, 2):
+            # every step from the reference's own input: with this convention a cfg1 step amplifies
+            # an input perturbation ~100x (2e-14 after step 1 becomes 2e-12 after step 2 otherwise)
+            u = G["u0"] if s == 1 else G[f"{key}1"]
+            n0 = len(log)
+            u = osw.run_mlsdc(h, u, (s - 1) * dt, dt, w.n_cycles, "fmg").u[-1].copy()
+            assert np.linalg.norm(u - G[f"{key}{s}"]) / np.linalg.norm(G[f"{key}{s}"]) < tol
+            if solver == "pcg":
+                assert [it for it, _ in log[n0:]] == G[f"pcg_iters{s}"].tolist()
