@@ -464,7 +464,6 @@ int sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art) {
 int sisdc_smooth_start(sisdc_op1d* op, int M, const double* u, double* out) {
   if (!op || !u || !out || M < 1) return SISDC_ERR_ARG;
   if (op->dim == 2) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "smooth_start is built for 1-D meshes");
-  if (op->cns()) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "smooth_start is built for the scalar 1-D problems");
   return launch_smooth_start(C(op), op->dev, M, u, out);
 }
 

@@ -220,16 +220,19 @@ __global__ void k_lincomb(long long n, LinArgs a) {
 // wrap) gets the mean of its two traces; blockIdx.y = node vector
 __global__ void k_smooth_start(Op1DDev op, const double* __restrict__ u, double* __restrict__ out) {
   const int p1 = op.p1, P = p1 - 1, ne = op.ne;
-  const size_t mo = (size_t)blockIdx.y * op.n;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < op.n; t += gridDim.x * blockDim.x) {
-    const int e = t / p1, i = t - e * p1;
+  const int N = op.n * op.nc;   // op.n counts one component
+  const size_t mo = (size_t)blockIdx.y * N;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N; t += gridDim.x * blockDim.x) {
+    const int eg = t / p1, i = t - eg * p1;
+    const int c = eg / ne, e = eg - c * ne;          // field-major (ncomp, ne, p1): every field on its own
+    const size_t fo = mo + (size_t)c * ne * p1;
     double v = u[mo + t];
     if (i == P && (e + 1 < ne || op.bc == SISDC_PERIODIC)) {
       const int en = e + 1 < ne ? e + 1 : 0;
-      v = 0.5 * (v + u[mo + (size_t)en * p1]);
+      v = 0.5 * (v + u[fo + (size_t)en * p1]);
     } else if (i == 0 && (e > 0 || op.bc == SISDC_PERIODIC)) {
       const int ep = e > 0 ? e - 1 : ne - 1;
-      v = 0.5 * (u[mo + (size_t)ep * p1 + P] + v);
+      v = 0.5 * (u[fo + (size_t)ep * p1 + P] + v);
     }
     out[mo + t] = v;
   }
@@ -485,7 +488,7 @@ int launch_lincomb(Ctx* c, long long n, const double* coef, const double* const*
 }
 int launch_smooth_start(Ctx* c, const Op1DDev& op, int M, const double* u, double* out) {
   if (u == out) return c->fail(SISDC_ERR_ARG, "smooth_start needs distinct input and output");
-  k_smooth_start<<<dim3((op.n + 255) / 256, M), 256, 0, c->stream>>>(op, u, out);
+  k_smooth_start<<<dim3((op.n * op.nc + 255) / 256, M), 256, 0, c->stream>>>(op, u, out);
   return c->after_launch("smooth_start");
 }
 int launch_xfer_spatial(Ctx* c, const XferDev& x, int dir, const double* in, double* out) {

@@ -174,13 +174,23 @@ def test_cns_mlsdc_steps(rt, golden, case):
     assert np.array_equal(host(g.u), host(eager))
 
 
-def test_cns_unsupported_paths(rt):
+def test_cns_smooth_start_all_fields(rt):
+    """smooth_start works for any ncomp (dgsem.py:574-589): interface averaging per field,
+    periodic wrap included, against the reference's formula restated on the host."""
     from paper_2504_18526_b200 import dgsem
-    from paper_2504_18526_b200._lib import LibraryError
     w = CASES["cns_resolved"]
     op = gpu_op(w, w.p_fine)
-    with pytest.raises(LibraryError, match="scalar"):
-        dgsem.smooth_start(op, w.initial_state(op.ref_nodes))
+    rng = np.random.default_rng(3)
+    u = w.initial_state(op.ref_nodes) + 0.01 * rng.standard_normal(op.ndof)
+    u3 = u.reshape(3, op.mesh.n_elem, op.p1).copy()
+    mean = 0.5 * (u3[:, :-1, -1] + u3[:, 1:, 0])
+    u3[:, :-1, -1] = mean
+    u3[:, 1:, 0] = mean
+    wrap = 0.5 * (u3[:, -1, -1] + u3[:, 0, 0])
+    u3[:, -1, -1] = wrap
+    u3[:, 0, 0] = wrap
+    got = dgsem.smooth_start(op, u).cpu().numpy()
+    assert np.abs(got - u3.reshape(-1)).max() == 0.0
 
 
 SOD = None
