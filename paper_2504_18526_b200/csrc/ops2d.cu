@@ -1356,30 +1356,44 @@ struct Ev {                 // per-warp shared region (doubles)
   static constexpr int CSI = UPO + NC * NP, CFS = CSI + NP;   // SI coefficient own / face
   static constexpr int CPH = CFS + 32, CFP = CPH + NP;        // physical coefficient own / face
   static constexpr int QX = CFP + 32, QY = QX + NP, DOT = QY + NP, FCON = DOT + 32;
-  static constexpr int FX = FCON + 64, FY = FX + NP;
-  static constexpr int FHM = FY + NP, FHP = FHM + 32 * NC;   // Rusanov fluxes [lane][NC]
+  static constexpr int FX = FCON + 64, FY = FX + NC * NP;     // fluxes of all fields [NC][NP]
+  static constexpr int FHM = FY + NC * NP, FHP = FHM + 32 * NC;   // Rusanov fluxes [lane][NC]
   static constexpr int WARP = FHP + 32 * NC;
 };
 constexpr int EV_WARPS = 4;
 
-// convective term of field c at the lane's node pair from the staged element
-// (state rows in `own`, padded) and the face fluxes fh[lane*NC + c]
+// fluxes F^x, F^y of ALL fields at the lane's node pair of a staged element (state rows in
+// `own`, padded) -> FX4 / FY4 [NC][80]: one flux evaluation per node and axis (the per-field
+// version re-evaluated the full flux, divisions included, for every field it picked)
 template <int NC>
-__device__ __forceinline__ void wpe_conv(const Op2DDev& op, const MmaLane& K, const double* own, const double* fh,
-                                         int c, double* FX, double* FY, double& r0, double& r1) {
-  constexpr int RP = 10, P = 7;
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, n0 = 2 * t;
+__device__ __forceinline__ void wpe_flux_all(const Op2DDev& op, const double* own, double* FX4, double* FY4) {
+  constexpr int RP = 10;
+  const int lane = threadIdx.x & 31, g = lane >> 2, n0 = 2 * (lane & 3);
+  double fx[2][NC_MAX], fy[2][NC_MAX];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    double st[NC_MAX], fl[NC_MAX];
+    double st[NC_MAX];
 #pragma unroll
     for (int q = 0; q < NC_MAX; ++q) st[q] = q < NC ? own[q * 80 + g * RP + n0 + i] : 1.0;
-    flux2d(op, st, 0, fl);
-    FX[g * RP + n0 + i] = pick4(fl, c);
-    flux2d(op, st, 1, fl);
-    FY[g * RP + n0 + i] = pick4(fl, c);
+    flux2d(op, st, 0, fx[i]);
+    flux2d(op, st, 1, fy[i]);
+  }
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    *reinterpret_cast<double2*>(FX4 + q * 80 + g * RP + n0) = make_double2(fx[0][q], fx[1][q]);
+    *reinterpret_cast<double2*>(FY4 + q * 80 + g * RP + n0) = make_double2(fy[0][q], fy[1][q]);
   }
   __syncwarp();
+}
+
+// convective term of field c at the lane's node pair from the staged fluxes FX / FY of that
+// field (wpe_flux_all) and the face fluxes fh[lane*NC + c]; rx[i] = sx / w[n0+i], ry = sy / w[g]
+template <int NC>
+__device__ __forceinline__ void wpe_conv(const MmaLane& K, const double* fh, int c, const double* FX,
+                                         const double* FY, const double (&rx)[2], double ry, double& r0,
+                                         double& r1) {
+  constexpr int RP = 10, P = 7;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, n0 = 2 * t;
   double vx0 = 0.0, vx1 = 0.0, vy0 = 0.0, vy1 = 0.0;
   dmma(vx0, vx1, FX[g * RP + t], K.w0);
   dmma(vx0, vx1, FX[g * RP + 4 + t], K.w1);
@@ -1389,9 +1403,8 @@ __device__ __forceinline__ void wpe_conv(const Op2DDev& op, const MmaLane& K, co
   if (n0 == 0) vx0 += fh[(FL * 8 + g) * NC + c];
   if (g == P) { vy0 -= fh[(FT * 8 + n0) * NC + c]; vy1 -= fh[(FT * 8 + n0 + 1) * NC + c]; }
   if (g == 0) { vy0 += fh[(FB * 8 + n0) * NC + c]; vy1 += fh[(FB * 8 + n0 + 1) * NC + c]; }
-  r0 = vx0 * op.sx / K.wn[0] + vy0 * op.sy / K.wg;
-  r1 = vx1 * op.sx / K.wn[1] + vy1 * op.sy / K.wg;
-  __syncwarp();   // FX / FY are rewritten by the next call
+  r0 = vx0 * rx[0] + vy0 * ry;
+  r1 = vx1 * rx[1] + vy1 * ry;
 }
 
 template <int NC>
@@ -1416,6 +1429,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
   const bool conv_up = need_h && a.conv_prev == nullptr;
   MmaLane K;
   mma_lane_init(op, K);
+  // reciprocal lane constants: the divisions by the mass weights were ~15% of this kernel's samples
+  const double rcx[2] = {op.sx / K.wn[0], op.sx / K.wn[1]}, rcy = op.sy / K.wg;
+  const double rhx[2] = {1.0 / K.hwx[0], 1.0 / K.hwx[1]}, rhy = 1.0 / K.hwy;
   const int g = lane >> 2, n0 = 2 * (lane & 3), r = g, cc = n0;
   const int f = lane >> 3, k = lane & 7;
   const int fnode = f == FR ? k * 8 : f == FL ? k * 8 + 7 : f == FT ? k : 56 + k;
@@ -1491,7 +1507,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
     }
     __syncwarp();
     const long long gi = (long long)eo + g * 8 + n0;
-#pragma unroll 1
+    wpe_flux_all<NC>(op, ws + W::OWN, ws + W::FX, ws + W::FY);   // fluxes of u_m, all fields, once
+    double dsv[NC][2];   // SI-coefficient diffusion per field (needed again if conv(u_{m-1}) is rebuilt below)
+#pragma unroll
     for (int c = 0; c < NC; ++c) {
       const double* Ue = ws + W::OWN + c * W::NP;
       const double* Nb = ws + W::NBR + c * 64;
@@ -1500,20 +1518,22 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
       if (has_phys) {
         wpe_sip<NC>(op, K, Ue, Nb, ws + W::CPH, ws + W::CFP, ws + W::QX, ws + W::QY, ws + W::DOT, ws + W::FCON,
                     bx0, bx1, by0, by1);
-        dp0 = -(bx0 / K.hwx[0]) - by0 / K.hwy;
-        dp1 = -(bx1 / K.hwx[1]) - by1 / K.hwy;
+        dp0 = -(bx0 * rhx[0]) - by0 * rhy;
+        dp1 = -(bx1 * rhx[1]) - by1 * rhy;
       }
       if (need_si) {
         wpe_sip<NC>(op, K, Ue, Nb, ws + W::CSI, ws + W::CFS, ws + W::QX, ws + W::QY, ws + W::DOT, ws + W::FCON,
                     bx0, bx1, by0, by1);
-        ds0 = -(bx0 / K.hwx[0]) - by0 / K.hwy;
-        ds1 = -(bx1 / K.hwx[1]) - by1 / K.hwy;
+        ds0 = -(bx0 * rhx[0]) - by0 * rhy;
+        ds1 = -(bx1 * rhx[1]) - by1 * rhy;
       } else if (need_h) {   // implicit-Euler scheme: modified coefficient = physical
         ds0 = dp0;
         ds1 = dp1;
       }
+      dsv[c][0] = ds0;
+      dsv[c][1] = ds1;
       double cm0, cm1;
-      wpe_conv<NC>(op, K, ws + W::OWN, ws + W::FHM, c, ws + W::FX, ws + W::FY, cm0, cm1);
+      wpe_conv<NC>(K, ws + W::FHM, c, ws + W::FX + c * W::NP, ws + W::FY + c * W::NP, rcx, rcy, cm0, cm1);
       const long long go = (size_t)m * op.ns + c * nn + gi;
       const double f0 = has_phys ? cm0 + dp0 : cm0, f1 = has_phys ? cm1 + dp1 : cm1;
       if (!isfinite(f0) || !isfinite(f1)) atomicMin(a.status, (int)(op.e0 + e));
@@ -1524,16 +1544,22 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
         if (a.h2) *reinterpret_cast<double2*>(a.h2 + go) = make_double2(0.0, 0.0);
         continue;
       }
-      double cp0, cp1;
+      if (a.h2) *reinterpret_cast<double2*>(a.h2 + go) = make_double2(dtm * (cm0 + ds0), dtm * (cm1 + ds1));
       if (a.conv_prev) {
         const double2 v = *reinterpret_cast<const double2*>(a.conv_prev + c * nn + gi);
-        cp0 = v.x;
-        cp1 = v.y;
-      } else {
-        wpe_conv<NC>(op, K, ws + W::UPO, ws + W::FHP, c, ws + W::FX, ws + W::FY, cp0, cp1);
+        *reinterpret_cast<double2*>(a.h1 + go) = make_double2(dtm * (v.x + ds0), dtm * (v.y + ds1));
       }
-      *reinterpret_cast<double2*>(a.h1 + go) = make_double2(dtm * (cp0 + ds0), dtm * (cp1 + ds1));
-      if (a.h2) *reinterpret_cast<double2*>(a.h2 + go) = make_double2(dtm * (cm0 + ds0), dtm * (cm1 + ds1));
+    }
+    if (conv_up) {   // no cached conv(u_{m-1}) (cache refresh): rebuild it from the staged u_{m-1}
+      __syncwarp();
+      wpe_flux_all<NC>(op, ws + W::UPO, ws + W::FX, ws + W::FY);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double cp0, cp1;
+        wpe_conv<NC>(K, ws + W::FHP, c, ws + W::FX + c * W::NP, ws + W::FY + c * W::NP, rcx, rcy, cp0, cp1);
+        const long long go = (size_t)m * op.ns + c * nn + gi;
+        *reinterpret_cast<double2*>(a.h1 + go) = make_double2(dtm * (cp0 + dsv[c][0]), dtm * (cp1 + dsv[c][1]));
+      }
     }
     __syncwarp();   // the next element overwrites the staged data
   }
@@ -1548,8 +1574,8 @@ template <int NC>
 struct Stg {                 // per-warp shared region (doubles)
   static constexpr int RP = 10, NP = 80;
   static constexpr int OWN = 0;                  // [NC][NP] conv_in element
-  static constexpr int FX = OWN + NC * NP, FY = FX + NP;
-  static constexpr int FH = FY + NP;             // [32][NC] face fluxes
+  static constexpr int FX = OWN + NC * NP, FY = FX + NC * NP;   // fluxes of all fields [NC][NP]
+  static constexpr int FH = FY + NC * NP;        // [32][NC] face fluxes
   static constexpr int WARP = FH + 32 * NC;
 };
 template <int NC>
@@ -1562,6 +1588,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_stage8(Op2DDev op, Stage2Arg
   const long long nn = op.nn;
   MmaLane K;
   mma_lane_init(op, K);
+  const double rcx[2] = {op.sx / K.wn[0], op.sx / K.wn[1]}, rcy = op.sy / K.wg;
   const int g = lane >> 2, n0 = 2 * (lane & 3);
   const int f = lane >> 3, k = lane & 7;
   const int fnode = f == FR ? k * 8 : f == FL ? k * 8 + 7 : f == FT ? k : 56 + k;      // neighbour's face node
@@ -1592,10 +1619,11 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_stage8(Op2DDev op, Stage2Arg
     }
     __syncwarp();
     const long long gi = (long long)eo + g * 8 + n0;
+    wpe_flux_all<NC>(op, ws + W::OWN, ws + W::FX, ws + W::FY);
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
       double cv0, cv1;
-      wpe_conv<NC>(op, K, ws + W::OWN, ws + W::FH, c, ws + W::FX, ws + W::FY, cv0, cv1);
+      wpe_conv<NC>(K, ws + W::FH, c, ws + W::FX + c * W::NP, ws + W::FY + c * W::NP, rcx, rcy, cv0, cv1);
       const long long gc = c * nn + gi;
       if (a.conv_out) *reinterpret_cast<double2*>(a.conv_out + gc) = make_double2(cv0, cv1);
       double q0 = 0.0, q1 = 0.0;

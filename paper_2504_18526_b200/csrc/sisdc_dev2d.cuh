@@ -58,7 +58,7 @@ __device__ __forceinline__ bool euler_like(const Op2DDev& op) {
 }
 __device__ __forceinline__ void flux2d(const Op2DDev& op, const double* s, int axis, double* f) {
   if (euler_like(op)) {
-    const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
+    const double ir = 1.0 / s[0], vx = s[1] * ir, vy = s[2] * ir;   // one division per state
     const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
     const double vn = axis == 0 ? vx : vy;
     f[0] = s[1 + axis];
@@ -73,18 +73,18 @@ __device__ __forceinline__ void flux2d(const Op2DDev& op, const double* s, int a
 }
 __device__ __forceinline__ double speed2d(const Op2DDev& op, const double* s, int axis) {
   if (euler_like(op)) {
-    const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
+    const double ir = 1.0 / s[0], vx = s[1] * ir, vy = s[2] * ir;
     const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
-    return fabs(axis == 0 ? vx : vy) + sqrt(op.gamma * p / rho);
+    return fabs(axis == 0 ? vx : vy) + sqrt(op.gamma * p * ir);
   }
   if (op.problem == SISDC_ADVECTION2D) return fabs(axis == 0 ? op.ax : op.ay);
   return axis == 0 ? fabs(s[0]) : 0.0;
 }
 __device__ __forceinline__ double lam_max2d(const Op2DDev& op, const double* s) {
   if (euler_like(op)) {
-    const double rho = s[0], vx = s[1] / rho, vy = s[2] / rho;
+    const double ir = 1.0 / s[0], vx = s[1] * ir, vy = s[2] * ir;
     const double p = (op.gamma - 1.0) * (s[3] - 0.5 * (s[1] * vx + s[2] * vy));
-    return sqrt(vx * vx + vy * vy) + sqrt(op.gamma * p / rho);
+    return sqrt(vx * vx + vy * vy) + sqrt(op.gamma * p * ir);
   }
   if (op.problem == SISDC_ADVECTION2D) return hypot(op.ax, op.ay);
   return fabs(s[0]);
