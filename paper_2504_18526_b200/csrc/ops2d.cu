@@ -2105,6 +2105,24 @@ __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, cons
   }
 }
 
+// per-block partials of three sums -> slot[blockIdx] (fixed order)
+__device__ __forceinline__ void blk_part3(double v0, double v1, double v2, double* red, double* slot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+  }
+  __syncthreads();
+  if (lane == 0) { red[wid * 4] = v0; red[wid * 4 + 1] = v1; red[wid * 4 + 2] = v2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int ww = 0; ww < nw; ++ww) { t0 += red[ww * 4]; t1 += red[ww * 4 + 1]; t2 += red[ww * 4 + 2]; }
+    slot[blockIdx.x * 4] = t0; slot[blockIdx.x * 4 + 1] = t1; slot[blockIdx.x * 4 + 2] = t2;
+  }
+}
+
 template <int NC>
 __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   extern __shared__ double sm[];
@@ -2128,9 +2146,13 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (A.scal[7] == 0.0) return;   // b == 0: the setup kernel wrote x = 0 and logged the solve
-  const double thr = A.scal[2];
-  double rho = A.scal[3], alpha = A.scal[4], beta = 0.0, rgam = A.scal[5], ralpha = A.scal[6];
+  // single-pass mode (A.sc set: the split solve of an element-row partition, part2d.cu): ONE pass with the
+  // scalars of the solve's CgPScal, buffer parity A.px, block partials to part / part2; no grid barrier
+  const bool single = A.sc != nullptr;
+  if (single ? A.sc->done != 0 : A.scal[7] == 0.0) return;   // converged / b == 0 (x = 0 written by the setup)
+  const double thr = single ? 0.0 : A.scal[2];
+  double rho = single ? 1.0 : A.scal[3], alpha = single ? A.sc->alpha : A.scal[4], beta = single ? A.sc->beta : 0.0;
+  double rgam = single ? 0.0 : A.scal[5], ralpha = single ? 0.0 : A.scal[6];
   MmaLane K;
   mma_lane_init(op, K);
   FzLane L;
@@ -2159,13 +2181,14 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
     if (k >= maxit) { ok = false; break; }
     const bool stamp = stampb && k == 2;
     if (stamp) tm[0] = tm[1] = tm[2] = gtimer();
-    const bool first = k == 0;
-    const double* const Ro = (k & 1) ? A.R2 : A.R;
-    const double* const So = (k & 1) ? A.S2 : A.S;
-    const double* const Wo = (k & 1) ? A.W2 : A.W;
-    double* const Rn = (k & 1) ? A.R : A.R2;
-    double* const Sn = (k & 1) ? A.S : A.S2;
-    double* const Wn = (k & 1) ? A.W : A.W2;
+    const bool first = single ? A.sc->k == 0 : k == 0;
+    const int par = single ? A.px : (k & 1);
+    const double* const Ro = par ? A.R2 : A.R;
+    const double* const So = par ? A.S2 : A.S;
+    const double* const Wo = par ? A.W2 : A.W;
+    double* const Rn = par ? A.R : A.R2;
+    double* const Sn = par ? A.S : A.S2;
+    double* const Wn = par ? A.W : A.W2;
     double ru = 0.0, rr = 0.0, wu = 0.0;
     for (long long un = blockIdx.x; un < nunits; un += G) {
       const int c = (int)(un % NC);
@@ -2175,15 +2198,15 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       const int band = (int)(tq % nbands), sx = (int)(tq / nbands);
       const int y0 = band * NW, nrows = op.ney - y0 < NW ? op.ney - y0 : NW;
       const bool valid = warp < nrows;
-      const int ey = valid ? y0 + warp : y0;
+      const int ey = (valid ? y0 + warp : y0) + op.row0;   // storage row (a partition's ghost rows: ynb)
       const int x0 = sx * SL, x1 = x0 + SL < op.nex ? x0 + SL : op.nex;
       // offsets in doubles fit 32 bits (checked by the launcher: n < 2^32)
       const unsigned fo = (unsigned)(c * nn);
       const unsigned rowC = (unsigned)ey * op.nex * 64u;
-      const unsigned rowT = (unsigned)(ey + 1 == op.ney ? 0 : ey + 1) * op.nex * 64u;
-      const unsigned rowB = (unsigned)(ey == 0 ? op.ney - 1 : ey - 1) * op.nex * 64u;
-      const unsigned hrow0 = (unsigned)(y0 + nrows == op.ney ? 0 : y0 + nrows) * op.nex * 64u;   // above the band
-      const unsigned hrow1 = (unsigned)(y0 == 0 ? op.ney - 1 : y0 - 1) * op.nex * 64u;            // below the band
+      const unsigned rowT = (unsigned)ynb(op, ey, 1) * op.nex * 64u;
+      const unsigned rowB = (unsigned)ynb(op, ey, -1) * op.nex * 64u;
+      const unsigned hrow0 = (unsigned)ynb(op, op.row0 + y0 + nrows - 1, 1) * op.nex * 64u;   // above the band
+      const unsigned hrow1 = (unsigned)ynb(op, op.row0 + y0, -1) * op.nex * 64u;              // below the band
       const unsigned oC = fo + rowC + 2 * lane;
       const unsigned cfb = (f == FT ? rowT : f == FB ? rowB : rowC) + fnode;   // this lane's face coefficient row
       // own stage of step js: r, s, w, dinv of column js+1, cf of column js (js >= x0)
@@ -2353,6 +2376,11 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       step(x1 - 1, F_{}, T_{});
     }
     if (stamp) tm[3] = gtimer();
+    if (single) {   // block partials in the split solve's slots: part (r,u), (r,r); part2 (w,u)
+      blk_part3(ru, rr, 0.0, red, A.part);
+      blk_part3(wu, 0.0, 0.0, red, A.part2);
+      return;
+    }
     double* slot = (k & 1) ? slot1 : slot0;
     {   // per-block partials -> slot[blockIdx]
       double v0 = ru, v1 = wu, v2 = rr;
@@ -2421,22 +2449,6 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
 // lock step.  Kernels launched after convergence return immediately.
 // Workspace per partition (doubles): R W U P S (n each) | DINV Cf (nn each) |
 // partA partB (4 G each).
-__device__ __forceinline__ void blk_part3(double v0, double v1, double v2, double* red, double* slot) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) {
-    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-    v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-  }
-  __syncthreads();
-  if (lane == 0) { red[wid * 4] = v0; red[wid * 4 + 1] = v1; red[wid * 4 + 2] = v2; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    for (int ww = 0; ww < nw; ++ww) { t0 += red[ww * 4]; t1 += red[ww * 4 + 1]; t2 += red[ww * 4 + 2]; }
-    slot[blockIdx.x * 4] = t0; slot[blockIdx.x * 4 + 1] = t1; slot[blockIdx.x * 4 + 2] = t2;
-  }
-}
 __device__ __forceinline__ long long own0(const Op2DDev& op) { return (long long)op.row0 * op.nex * op.p1 * op.p1; }
 __device__ __forceinline__ long long nown(const Op2DDev& op) { return (long long)op.ney * op.nex * op.p1 * op.p1; }
 
@@ -3028,21 +3040,48 @@ int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks) {
 
 
 // ------------------------------------------------ partitioned solve launchers
-size_t cg2p_ws_doubles(const Op2DDev& op, int G) { return 6 * (size_t)op.n + 2 * (size_t)op.nn + 8 * (size_t)G; }
-// the two u buffers of the split solve: which 0 -> U, 1 -> U2
-double* cg2p_U(const Op2DDev& op, double* ws, int which) { return ws + (which ? 5 : 2) * op.n; }
+// P = 7 partitions iterate with the fused single pass (k2_cgf in single-pass mode):
+// workspace R0 S0 W0 R1 S1 W1 P (n each; the setup's u0 lives in S1) | DINV Cf | partA partB
+bool cg2p_fused(const Op2DDev& op) {
+  static const bool on = [] {
+    const char* v = getenv("SISDC_CG_FUSED");
+    return !(v && v[0] == '0');
+  }();
+  return on && op.p1 == 8;
+}
+size_t cg2p_ws_doubles(const Op2DDev& op, int G) { return 7 * (size_t)op.n + 2 * (size_t)op.nn + 8 * (size_t)G; }
+size_t cg2p_part_off(const Op2DDev& op) { return (cg2p_fused(op) ? 7 : 6) * (size_t)op.n + 2 * (size_t)op.nn; }
+size_t cg2p_dinv_off(const Op2DDev& op) { return (cg2p_fused(op) ? 7 : 6) * (size_t)op.n; }
+// the two u buffers of the split solve: which 0 -> U, 1 -> U2 (fused: the setup's u0 only, in S1)
+double* cg2p_U(const Op2DDev& op, double* ws, int which) {
+  if (cg2p_fused(op)) return ws + 4 * op.n;
+  return ws + (which ? 5 : 2) * op.n;
+}
+// fused: the (r, s, w) triple of parity par, three consecutive vectors (one halo call)
+double* cg2p_RSW(const Op2DDev& op, double* ws, int par) { return ws + (par ? 3 : 0) * op.n; }
 
 static Cg2Args cg2p_args(const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int G,
                          const CgPScal* sc, int ucur) {
   Cg2Args A{};
   A.op = op; A.coef = k; A.a = a; A.rhs = rhs; A.x = x;
   double* p = ws;
-  A.R = p; p += op.n;
-  A.W = p; p += op.n;
-  A.U = p; p += op.n;
-  A.Pv = p; p += op.n;
-  A.S = p; p += op.n;
-  A.U2 = p; p += op.n;
+  if (cg2p_fused(op)) {
+    A.R = p; p += op.n;
+    A.S = p; p += op.n;
+    A.W = p; p += op.n;
+    A.R2 = p; p += op.n;
+    A.S2 = p; A.U = p; p += op.n;   // u0 of the setup
+    A.W2 = p; p += op.n;
+    A.Pv = p; p += op.n;
+    A.U2 = nullptr;
+  } else {
+    A.R = p; p += op.n;
+    A.W = p; p += op.n;
+    A.U = p; p += op.n;
+    A.Pv = p; p += op.n;
+    A.S = p; p += op.n;
+    A.U2 = p; p += op.n;
+  }
   A.DINV = p; p += op.nn;
   A.Cf = p; p += op.nn;
   A.part = p; p += 4 * G;
@@ -3050,7 +3089,7 @@ static Cg2Args cg2p_args(const Op2DDev& op, CoefDev k, double a, const double* r
   A.sc = sc;
   // ucur: 0 / 1 = which buffer holds this iteration's u (the other the previous u);
   // -1: setup (u0 into buffer 0, no p / x update)
-  if (ucur == 1) {
+  if (ucur == 1 && !cg2p_fused(op)) {
     double* t = A.U;
     A.U = A.U2;
     A.U2 = t;
@@ -3093,12 +3132,38 @@ int launch2p_phase(Ctx* c, int phase, const Op2DDev& op, CoefDev k, double a, co
   return SISDC_OK;
 }
 
+// one fused iteration pass on a partition (k2_cgf in single-pass mode); par: parity of the (r, s, w) read
+int launch2p_fpass(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int G,
+                   const CgPScal* sc, int par) {
+  Cg2Args A = cg2p_args(op, k, a, rhs, x, ws, G, sc, -1);
+  A.px = par;
+  A.maxit = c->maxit;
+  cudaError_t e = cudaSuccess;
+  if (op.nc == 4) {
+    using F = Fz<4>;
+    constexpr int smem = (int)(sizeof(double) * F::SIZE);
+    cudaFuncSetAttribute(k2_cgf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k2_cgf<4><<<G, F::NW * 32, smem, c->stream>>>(A);
+  } else if (op.nc == 1) {
+    using F = Fz<1>;
+    constexpr int smem = (int)(sizeof(double) * F::SIZE);
+    cudaFuncSetAttribute(k2_cgf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k2_cgf<1><<<G, F::NW * 32, smem, c->stream>>>(A);
+  } else {
+    return c->fail(SISDC_ERR_UNSUPPORTED, "fused 2-D pass: 1 or 4 fields");
+  }
+  e = cudaGetLastError();
+  ++c->launches;
+  if (e != cudaSuccess) return c->cuda(e, "k2_cgf single-pass launch");
+  return SISDC_OK;
+}
+
 int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out) {
   if (nparts < 1 || nparts > MAXPART) return c->fail(SISDC_ERR_ARG, "partition count");
   RedPArgs R{};
   R.nparts = nparts; R.G = G; R.mode = mode; R.out = out;
   for (int p = 0; p < nparts; ++p) {
-    const double* base = ws[p] + 6 * ops[p].n + 2 * ops[p].nn;
+    const double* base = ws[p] + cg2p_part_off(ops[p]);
     R.pa[p] = base;
     R.pb[p] = base + 4 * G;
   }

@@ -248,8 +248,44 @@ int halo_u(sisdc_op1d* op, int which) {
   return halo(op, cg2p_U(P.dev, P.ws, which) - P.off, 1, 0, false);
 }
 
+// ghost rows of one vector of every local partition's CG workspace; which: 0 / 1 / 2 = r / s / w of
+// parity par, 3 = dinv (one field).  Partitions differ in size, so the offsets are per partition.
+int halo_ws(sisdc_op1d* op, int which, int par) {
+  Ctx* c = C(op);
+  const int np = (int)op->parts.size();
+  const bool scalar = which == 3;
+  auto vec = [&](const Part2D& P) {
+    return scalar ? P.ws + cg2p_dinv_off(P.dev) : cg2p_RSW(P.dev, P.ws, par) + (size_t)which * P.dev.n;
+  };
+  if (!op->comm) {
+    Op2DDev ops[MAXPART];
+    double* base[MAXPART];
+    for (int p = 0; p < np; ++p) {
+      ops[p] = op->parts[p].dev;
+      base[p] = vec(op->parts[p]);
+    }
+    return launch2p_halo(c, np, ops, base, scalar ? 1 : ops[0].nc, 1, 0);
+  }
+  const Part2D& P = op->parts[0];   // one local partition: halo() adds P.off / P.offc back
+  return halo(op, vec(P) - (scalar ? P.offc : P.off), 1, 0, scalar);
+}
+
+// fused iteration j (P = 7): the (r, s, w) of parity j & 1 get their ghost rows, then ONE pass per
+// partition does update + matvec (k2_cgf single-pass mode) and writes parity (j + 1) & 1
+int iterate_fused(sisdc_op1d* op, int j, const CoefDev& k, double a, const double* rhs, double* x) {
+  const int par = j & 1;
+  for (int v = 0; v < 3; ++v)
+    if (int rc = halo_ws(op, v, par)) return rc;
+  for (const Part2D& P : op->parts)
+    if (int rc = launch2p_fpass(C(op), P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc, par))
+      return rc;
+  if (int rc = reduce_all(op, 1)) return rc;
+  return launch2p_scalar(C(op), 2, op->d_red + 4, op->d_sc);
+}
+
 // iteration j: u_prev in buffer j & 1 (the setup's u0 in buffer 0), u_new in the other
 int iterate(sisdc_op1d* op, int j, const CoefDev& k, double a, const double* rhs, double* x) {
+  if (cg2p_fused(op->parts[0].dev)) return iterate_fused(op, j, k, a, rhs, x);
   const int ucur = (j + 1) & 1;
   if (int rc = phase_all(op, P2_UPDATE, k, a, rhs, x, ucur)) return rc;
   if (int rc = halo_u(op, ucur)) return rc;
@@ -272,6 +308,8 @@ int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* 
   if (int rc = halo(op, rhs, 1, 0, false)) return rc;
   if (int rc = phase_all(op, P2_INIT, k, a, rhs, x)) return rc;
   if (int rc = phase_all(op, P2_DINV, k, a, rhs, x)) return rc;
+  if (cg2p_fused(op->parts[0].dev))   // the fused pass rebuilds the neighbour rows' u = r dinv: dinv ghost rows, once
+    if (int rc = halo_ws(op, 3, 0)) return rc;
   if (int rc = phase_all(op, P2_RESID, k, a, rhs, x)) return rc;
   if (int rc = reduce_all(op, 0)) return rc;
   if (int rc = launch2p_scalar(c, 0, op->d_red + 4, op->d_sc)) return rc;

@@ -122,6 +122,11 @@ int set_cg2_tables(Ctx* c, int p1, const double* tab);
 struct CgPScal;
 enum { P2_INIT = 0, P2_DINV, P2_RESID, P2_U0, P2_UPDATE, P2_MATVEC };
 size_t cg2p_ws_doubles(const Op2DDev& op, int G);
+bool cg2p_fused(const Op2DDev& op);
+size_t cg2p_dinv_off(const Op2DDev& op);
+double* cg2p_RSW(const Op2DDev& op, double* ws, int par);
+int launch2p_fpass(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int G,
+                   const CgPScal* sc, int par);
 double* cg2p_U(const Op2DDev& op, double* ws, int which);
 int cg2p_blocks(Ctx* c, const Op2DDev& op, int* G);
 int launch2p_phase(Ctx* c, int phase, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x,
