@@ -2679,7 +2679,7 @@ __global__ void __launch_bounds__(256) k2p_reduce(RedPArgs R) {
 }
 
 // solve scalars from the allreduced sums (k2_cg's recurrences and stopping
-// rule); mode 0 after r0, 1 after w0, 2 after every iteration.  One thread.
+// rule); mode 0 after r0, 1 after w0, 2 after every iteration, 3 closes a captured batch.  One thread.
 struct ScalPArgs {
   int mode, maxit;
   double rtol2;
@@ -2706,6 +2706,15 @@ __global__ void k2p_scalar(ScalPArgs S) {
     s.rho = 0.0;
     s.alpha = s.beta = 0.0;
     if (s.zero) log(0, 0.0);
+    return;
+  }
+  if (S.mode == 3) {   // end of a captured fixed-length iteration batch: not converged = failure
+    if (!s.done) {
+      s.done = 1;
+      s.ok = 0;
+      log(-1, s.thr > 0.0 ? sqrt(s.rho / s.thr) : 0.0);
+      atomicAdd(&S.status[1], 1);
+    }
     return;
   }
   if (s.done) return;
@@ -2742,7 +2751,7 @@ __global__ void k2p_scalar(ScalPArgs S) {
 // row of r+1 (periodic in y), for nc fields and mcount node vectors
 struct HaloPArgs {
   int nparts, nc, nex, nnod, mcount;
-  long long mstride;
+  long long mstride;             // vector stride, or (mstride < 0) n of each partition: its own state size
   double* base[MAXPART];
   int ney[MAXPART];
   long long nn[MAXPART];
@@ -2753,9 +2762,9 @@ __global__ void k2p_halo(HaloPArgs H) {
   const int src = side == 0 ? (r + 1) % H.nparts : (r + H.nparts - 1) % H.nparts;
   const long long so = side == 0 ? row : (long long)H.ney[src] * row;        // first / last owned row
   const long long dof = side == 0 ? (long long)(H.ney[r] + 1) * row : 0;    // top / bottom ghost row
-  const long long mo = (long long)blockIdx.z * H.mstride;
-  const double* s = H.base[src] + mo + c * H.nn[src] + so;
-  double* d = H.base[r] + mo + c * H.nn[r] + dof;
+  const long long ms = H.mstride < 0 ? H.nn[src] * H.nc : H.mstride, md = H.mstride < 0 ? H.nn[r] * H.nc : H.mstride;
+  const double* s = H.base[src] + blockIdx.z * ms + c * H.nn[src] + so;
+  double* d = H.base[r] + blockIdx.z * md + c * H.nn[r] + dof;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < row; t += (long long)gridDim.x * blockDim.x)
     d[t] = s[t];
 }
@@ -3103,8 +3112,10 @@ template <int P1, int NC>
 static cudaError_t p2_phase(int phase, const Cg2Args& A, int G, cudaStream_t st) {
   const size_t smem = smem_cg<P1, NC>();
   switch (phase) {
-    case P2_INIT: k2p_init<P1><<<G, 256, 0, st>>>(A); break;
-    case P2_DINV: k2p_dinv<P1><<<G, 256, 0, st>>>(A); break;
+    // pointwise passes with fp64 sqrt / division chains: one thread per node, full occupancy
+    // (no per-block partials, so the grid is free)
+    case P2_INIT: k2p_init<P1><<<(unsigned)((A.op.n + 255) / 256), 256, 0, st>>>(A); break;
+    case P2_DINV: k2p_dinv<P1><<<(unsigned)((A.op.nn + 255) / 256), 256, 0, st>>>(A); break;
     case P2_RESID:
       cudaFuncSetAttribute(k2p_resid<P1, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k2p_resid<P1, NC><<<G, Blk<P1>::NT, smem, st>>>(A);

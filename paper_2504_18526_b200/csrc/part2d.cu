@@ -16,9 +16,12 @@
 // The implicit solve is the split Chronopoulos-Gear PCG (ops2d.cu k2p_*): per
 // iteration phase A, halo(u), phase B, a fixed-order reduction, one NCCL
 // allreduce of three doubles, and the scalar recurrences on the device.  The
-// host polls the convergence flag one batch behind the launches.
+// host polls the convergence flag one batch behind the launches; inside a
+// CUDA-graph capture a fixed-length batch is recorded instead (kernels return
+// at once after convergence), so partitioned slabs replay as graphs too.
 // Elementwise work (defects, transfers, copies) runs over the concatenated
 // storage of the local partitions unchanged.
+#include <cstdlib>
 #include <cstring>
 #include <dlfcn.h>
 #include <new>
@@ -248,15 +251,13 @@ int halo_u(sisdc_op1d* op, int which) {
   return halo(op, cg2p_U(P.dev, P.ws, which) - P.off, 1, 0, false);
 }
 
-// ghost rows of one vector of every local partition's CG workspace; which: 0 / 1 / 2 = r / s / w of
-// parity par, 3 = dinv (one field).  Partitions differ in size, so the offsets are per partition.
-int halo_ws(sisdc_op1d* op, int which, int par) {
+// ghost rows of CG workspace vectors of every local partition: the (r, s, w) triple of parity par
+// (three consecutive state-sized vectors: one halo call) or, dinv = true, the Jacobi reciprocal (one
+// field).  Partitions differ in size, so bases and strides are per partition (mstride -1).
+int halo_ws(sisdc_op1d* op, bool dinv, int par) {
   Ctx* c = C(op);
   const int np = (int)op->parts.size();
-  const bool scalar = which == 3;
-  auto vec = [&](const Part2D& P) {
-    return scalar ? P.ws + cg2p_dinv_off(P.dev) : cg2p_RSW(P.dev, P.ws, par) + (size_t)which * P.dev.n;
-  };
+  auto vec = [&](const Part2D& P) { return dinv ? P.ws + cg2p_dinv_off(P.dev) : cg2p_RSW(P.dev, P.ws, par); };
   if (!op->comm) {
     Op2DDev ops[MAXPART];
     double* base[MAXPART];
@@ -264,18 +265,17 @@ int halo_ws(sisdc_op1d* op, int which, int par) {
       ops[p] = op->parts[p].dev;
       base[p] = vec(op->parts[p]);
     }
-    return launch2p_halo(c, np, ops, base, scalar ? 1 : ops[0].nc, 1, 0);
+    return launch2p_halo(c, np, ops, base, dinv ? 1 : ops[0].nc, dinv ? 1 : 3, -1);
   }
   const Part2D& P = op->parts[0];   // one local partition: halo() adds P.off / P.offc back
-  return halo(op, vec(P) - (scalar ? P.offc : P.off), 1, 0, scalar);
+  return halo(op, vec(P) - (dinv ? P.offc : P.off), dinv ? 1 : 3, P.dev.n, dinv);
 }
 
 // fused iteration j (P = 7): the (r, s, w) of parity j & 1 get their ghost rows, then ONE pass per
 // partition does update + matvec (k2_cgf single-pass mode) and writes parity (j + 1) & 1
 int iterate_fused(sisdc_op1d* op, int j, const CoefDev& k, double a, const double* rhs, double* x) {
   const int par = j & 1;
-  for (int v = 0; v < 3; ++v)
-    if (int rc = halo_ws(op, v, par)) return rc;
+  if (int rc = halo_ws(op, false, par)) return rc;
   for (const Part2D& P : op->parts)
     if (int rc = launch2p_fpass(C(op), P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc, par))
       return rc;
@@ -299,8 +299,7 @@ int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* 
   Ctx* c = C(op);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(c->stream, &cap);
-  if (cap != cudaStreamCaptureStatusNone)
-    return c->fail(SISDC_ERR_UNSUPPORTED, "a partitioned implicit solve polls its convergence flag and cannot be captured");
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
   if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(rhs)) & 15))
     return c->fail(SISDC_ERR_ARG, "2-D implicit solve: rhs and x must be 16-byte aligned");
   // coefficient source and rhs (x0 = rhs feeds the first matvec)
@@ -309,7 +308,7 @@ int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* 
   if (int rc = phase_all(op, P2_INIT, k, a, rhs, x)) return rc;
   if (int rc = phase_all(op, P2_DINV, k, a, rhs, x)) return rc;
   if (cg2p_fused(op->parts[0].dev))   // the fused pass rebuilds the neighbour rows' u = r dinv: dinv ghost rows, once
-    if (int rc = halo_ws(op, 3, 0)) return rc;
+    if (int rc = halo_ws(op, true, 0)) return rc;
   if (int rc = phase_all(op, P2_RESID, k, a, rhs, x)) return rc;
   if (int rc = reduce_all(op, 0)) return rc;
   if (int rc = launch2p_scalar(c, 0, op->d_red + 4, op->d_sc)) return rc;
@@ -318,6 +317,19 @@ int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* 
   if (int rc = phase_all(op, P2_MATVEC, k, a, rhs, x)) return rc;
   if (int rc = reduce_all(op, 1)) return rc;
   if (int rc = launch2p_scalar(c, 1, op->d_red + 4, op->d_sc)) return rc;
+  if (capturing) {
+    // inside a CUDA-graph capture the host cannot poll: a fixed number of iterations is recorded (kernels
+    // after convergence return at once: device-side convergence), and the closing scalar kernel latches a
+    // failure if the batch was too short (SISDC_PART_CAPTURE_ITERS, default 32; cfg4 / cfg5 solves take 6-25)
+    static const int cap_iters = [] {
+      const char* v = getenv("SISDC_PART_CAPTURE_ITERS");
+      const int n = v ? atoi(v) : 32;
+      return n > 0 ? n : 32;
+    }();
+    for (int j = 0; j < cap_iters; ++j)
+      if (int rc = iterate(op, j, k, a, rhs, x)) return rc;
+    return launch2p_scalar(c, 3, op->d_red + 4, op->d_sc);
+  }
   // iterations in batches of B; the flag of batch j-1 is read while batch j runs
   constexpr int B = 2;
   const int max_batches = c->maxit / B + 3;
