@@ -441,8 +441,11 @@ def measure_part(w, args, torch, rt, rank, world, local, steps, warmup, emulate=
     owns one block of element rows (NCCL face halo + one NCCL allreduce per CG
     iteration); with world == 1, `emulate` in-process partitions on one GPU
     (emulate == -1: one rank through NCCL).  Strong scaling: value = the whole
-    problem's DOF-sweeps per step x steps / max-over-ranks time.  Eager slabs
-    (the partitioned solve polls its convergence flag, so it is not captured)."""
+    problem's DOF-sweeps per step x steps / max-over-ranks time.  Eager slabs:
+    the kernels are long (a cfg5 slab is seconds), so launch overhead is
+    noise; partitioned slabs are capturable too (fixed-length device-side
+    converging batches, tests/test_gpu_partition.py), which a multi-rank NCCL
+    run cannot be validated with on the one GPU of this pool."""
     import dataclasses as _dc
     from paper_2504_18526_b200 import dgsem, dgsem2d, mlsdc
     if world > 1:
@@ -560,8 +563,8 @@ def measure_part(w, args, torch, rt, rank, world, local, steps, warmup, emulate=
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "split PCG of one fine solve (k2p_update + halo + k2p_matvec + reduce/allreduce "
-                               "per iteration), this rank's partition",
+                     "kernel": "split PCG of one fine solve, this rank's partition: per iteration halo(r, s, w) + "
+                               "k2_cgf single pass (update + matvec fused) + reduce / allreduce + scalars",
                      "kernel_us": t_cg * 1e6, "kernel_mean_iterations": k_cg, "algorithmic_bytes_per_launch": bytes_cg,
                      "note": "8N[(3+V)+k(10+V)] bytes per solve over this rank's owned DOFs, V=1/4"},
         "clocks": clk.summary(),

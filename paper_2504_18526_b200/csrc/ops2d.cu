@@ -868,10 +868,16 @@ __device__ __forceinline__ void wph_phase(const Op2DDev& op, const double* src, 
     const double fcp_x = Cf[oR + j * P1], fcm_x = Cf[oL + j * P1 + P];
     const double fcp_y = Cf[oT + i], fcm_y = Cf[oB + P * P1 + i];
     const double cPx = sh(cc, j * 4 + P), c0x = sh(cc, j * 4), cPy = sh(cc, P * 4 + i), c0y = sh(cc, i);
+    // the next field's five loads are issued before this field's shuffle / FMA chain (the chain
+    // consumed its own loads at once: 60% of the samples waited on them at 25% occupancy)
+    double pv = src[eo + t], pR = src[oR + t], pL = src[oL + t], pT = src[oT + t], pB = src[oB + t];
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
-      const double* sc = src + c * nn;
-      const double v = sc[eo + t], nR = sc[oR + t], nL = sc[oL + t], nT = sc[oT + t], nB = sc[oB + t];
+      const double v = pv, nR = pR, nL = pL, nT = pT, nB = pB;
+      if (c + 1 < NC) {
+        const double* sn = src + (c + 1) * nn;
+        pv = sn[eo + t]; pR = sn[oR + t]; pL = sn[oL + t]; pT = sn[oT + t]; pB = sn[oB + t];
+      }
       // q = C s D u along the row (x) and the column (y) of this node
       double gx = 0.0, gy = 0.0, row0, rowP, col0, colP;
 #pragma unroll
