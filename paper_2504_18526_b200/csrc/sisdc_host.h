@@ -19,7 +19,7 @@ struct Ctx {
   int* d_status = nullptr;        // [0] first non-finite element (INT_MAX: none), [1] CG failures, [2] log count
   int* d_log_it = nullptr;        // per-solve CG iterations
   double* d_log_margin = nullptr; // per-solve ||r||/(rtol ||b||)
-  int log_cap = 1 << 16;
+  int log_cap = 1 << 20;          // per-solve log entries kept (a long test session logs > 65k solves)
   long long* d_timing = nullptr;  // SISDC_CG_TIMING=1: CG clock64 stamps [66]
   double* d_cg1g = nullptr;       // grid-mode 1-D CG: halo / reduction exchange buffers (CG1G_DOUBLES)
   double rtol = 1e-14;

@@ -66,6 +66,12 @@ class Runtime:
         self.bind_stream()
         self.check(self.lib.sisdc_ctx_reset_status(self.h), "reset_status")
 
+    def reset_log(self):
+        """Forget the per-solve CG log (the device counter restarts at 0); the log keeps the first
+        2^20 solves after a reset, so long sessions (studies, test suites) reset it per run."""
+        self.bind_stream()
+        self.check(self.lib.sisdc_ctx_reset_log(self.h), "reset_log")
+
     def status(self):
         e, f, n = C.c_int(), C.c_int(), C.c_int()
         self.check(self.lib.sisdc_ctx_status(self.h, C.byref(e), C.byref(f), C.byref(n)), "status")
@@ -84,7 +90,7 @@ class Runtime:
     def cg_log(self):
         n = C.c_int()
         self.check(self.lib.sisdc_ctx_cg_log(self.h, 0, None, None, C.byref(n)), "cg_log")
-        cnt = min(n.value, 1 << 16)
+        cnt = min(n.value, 1 << 20)   # Ctx::log_cap
         it = (C.c_int * max(cnt, 1))()
         mg = (C.c_double * max(cnt, 1))()
         self.check(self.lib.sisdc_ctx_cg_log(self.h, cnt, it, mg, C.byref(n)), "cg_log")

@@ -37,3 +37,13 @@ def golden_ml():
 def golden_mls():
     import numpy as np
     return np.load(os.path.join(GOLDEN, "multilevel_study.npz"))
+
+
+@pytest.fixture(autouse=True)
+def _fresh_cg_log(request):
+    """GPU tests slice the per-solve CG log from a count they read themselves; the log keeps a
+    bounded number of entries, so every GPU test starts from an empty one."""
+    if request.node.get_closest_marker("gpu") is not None and gpu_available():
+        from paper_2504_18526_b200.runtime import get_runtime
+        get_runtime().reset_log()
+    yield
