@@ -1962,9 +1962,16 @@ __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
 // a neighbour is a whole step behind; RT has four slots for that.  Operands arrive
 // by TMA bulk copies (cp.async.bulk, one 512-byte run per element vector, five
 // per warp and step from one lane) on per-warp mbarriers, two steps ahead.
-template <int NC>
+// SUB = 2 (P = 3 levels with even nex, ney): a tile is a 2 x 2 block of 4 x 4-node elements.  With
+// block-diagonal D / DTW (blockdiag(D4, D4)) the 8 x 8 contractions are the four elements' own
+// contractions (the zero blocks add exact zeros), the tile's outer faces are handled as for SUB = 1
+// (the zero half of the face rows drops the far sub-element) and the faces BETWEEN the sub-elements
+// are extra lines whose both sides sit in the tile.  Per node the operations and their order are
+// wph_phase's; the coarse level gets the single pass, the band / strip pipeline and the tensor-core
+// contractions instead of ~30 shuffles per node and field.
+template <int NC, int SUB = 1>
 struct Fz {
-  static constexpr int SL = 16;                     // strip length (elements)
+  static constexpr int SL = SUB == 1 ? 16 : 8;      // strip length (tiles)
   static constexpr int NW = 8;                      // warps per block = rows per band
   static constexpr int NN = 64;
   // per-warp region (doubles)
@@ -1972,7 +1979,7 @@ struct Fz {
   static constexpr int CFN = RAW + 2 * 5 * NN;      // [32] neighbour face coefficients
   static constexpr int RING = CFN + 32;             // [3][64] u' of columns j-1, j, j+1 (sw8 layout)
   static constexpr int QX = RING + 3 * NN, QY = QX + NN, DOT = QY + NN, FCON = DOT + 32;
-  static constexpr int WARP = FCON + 64;
+  static constexpr int WARP = FCON + 64 * SUB;      // SUB = 2: + the internal faces' constants
   // block region
   static constexpr int RT = NW * WARP;              // [4 slots][NW + 2 rows][64] u' transposed + swizzled
   static constexpr int HRAW = RT + 4 * (NW + 2) * NN;   // [2 halo rows][2 stages][r, s, w, dinv][64]
@@ -2020,22 +2027,66 @@ __device__ __forceinline__ int sw8(int row, int col) {
 struct FzLane {   // per-lane tile offsets (doubles), computed once per kernel
   int oA0, oA1, oB0, oB1, oP;   // A / B fragments, node pair
   int ln, lsw;                  // face line of this lane: row offset k * 8, chunk swizzle S(k)
-  int up, u0, cu, c0, nP, n0_;  // lanes < 16: own face nodes (sw8 and row-major), neighbour face nodes
+  int up, u0, cu, c0, nP, n0_;  // lanes < 16: own face nodes (sw8 and raw order), neighbour face nodes
+  int lraw;                     // this lane's node pair in the raw stage order (SUB = 1: 2 lane)
+  int i3, i4, ci3, ci4;         // SUB = 2, lanes 16..31: the internal face's two nodes (sw8 / raw order)
 };
+// raw (memory) order of tile node (row, col): SUB = 1 row-major; SUB = 2 [element row][element][4][4]
+template <int SUB>
+__device__ __forceinline__ int raw_idx(int row, int col) {
+  if constexpr (SUB == 1) return row * 8 + col;
+  return (row >> 2) * 32 + (col >> 2) * 16 + (row & 3) * 4 + (col & 3);
+}
+template <int SUB>
 __device__ __forceinline__ void fz_lane_init(FzLane& L) {
   constexpr int P = 7;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, k = lane & 7;
   L.oA0 = sw8(g, t); L.oA1 = sw8(g, t + 4); L.oB0 = sw8(t, g); L.oB1 = sw8(t + 4, g); L.oP = sw8(g, 2 * t);
   L.ln = k * 8;
   L.lsw = ((k >> 1) & 1) * 2 + ((k >> 2) & 1);
-  const bool yd = lane >= 8;
+  const bool yd = (lane & 8) != 0;   // lanes 8..15 / 24..31: y-lines
   L.up = yd ? sw8(P, k) : sw8(k, P);
   L.u0 = yd ? sw8(0, k) : sw8(k, 0);
-  L.cu = yd ? P * 8 + k : k * 8 + P;
-  L.c0 = yd ? k : k * 8;
+  L.cu = yd ? raw_idx<SUB>(P, k) : raw_idx<SUB>(k, P);
+  L.c0 = yd ? raw_idx<SUB>(0, k) : raw_idx<SUB>(k, 0);
   L.nP = sw8(k, P);
   L.n0_ = sw8(k, 0);
+  L.lraw = raw_idx<SUB>(g, 2 * t);
+  L.i3 = yd ? sw8(3, k) : sw8(k, 3);
+  L.i4 = yd ? sw8(4, k) : sw8(k, 4);
+  L.ci3 = yd ? raw_idx<SUB>(3, k) : raw_idx<SUB>(k, 3);
+  L.ci4 = yd ? raw_idx<SUB>(4, k) : raw_idx<SUB>(k, 4);
 }
+// MmaLane of a SUB = 2 tile from the P = 3 tables: block-diagonal D / DTW, the weights repeated
+__device__ __forceinline__ void mma_lane_init_sub2(const Op2DDev& op, MmaLane& K) {
+  const double* D = op.tab + TabOff::D(4);
+  const double* DTW = op.tab + TabOff::DTW(4);
+  const double* w = op.tab + TabOff::w(4);
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, f = lane >> 3, n0 = 2 * t;
+  auto d8 = [&](const double* M, int r, int c) { return (r >> 2) == (c >> 2) ? M[(r & 3) * 4 + (c & 3)] : 0.0; };
+  K.d0 = d8(D, g, t);
+  K.d1 = d8(D, g, 4 + t);
+  K.w0 = d8(DTW, g, t);
+  K.w1 = d8(DTW, g, 4 + t);
+  const int rr = (f == FL || f == FB) ? 7 : 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) K.drow[q] = d8(D, rr, q);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {   // per sub-element: D[P][.] and D[0][.] at this node's local column
+    K.dPn[i] = D[3 * 4 + ((n0 + i) & 3)];
+    K.d0n[i] = D[(n0 + i) & 3];
+    K.hwx[i] = 0.5 * op.dx * w[(n0 + i) & 3];
+  }
+  K.dPg = D[3 * 4 + (g & 3)];
+  K.d0g = D[g & 3];
+  K.hwy = 0.5 * op.dy * w[g & 3];
+  K.hh[0] = K.hwx[0] * K.hwy;
+  K.hh[1] = K.hwx[1] * K.hwy;
+  K.wn[0] = w[n0 & 3];
+  K.wn[1] = w[(n0 + 1) & 3];
+  K.wg = w[g & 3];
+}
+template <int SUB>
 __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, const FzLane& L, const double* Ue,
                                        const double* UR, const double* UL, const double* UT, const double* UB,
                                        const double* Ce, const double* cfn, double* QX, double* QY, double* DT,
@@ -2049,7 +2100,7 @@ __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, cons
   dmma(qy0, qy1, K.d0, Ue[oB0]);
   dmma(qy0, qy1, K.d1, Ue[oB1]);
   {
-    const double2 cg = *reinterpret_cast<const double2*>(Ce + 2 * lane);   // row g, columns n0, n0 + 1
+    const double2 cg = *reinterpret_cast<const double2*>(Ce + L.lraw);   // row g, columns n0, n0 + 1
     *reinterpret_cast<double2*>(QX + oP) = make_double2(cg.x * (op.sx * qx0), cg.y * (op.sx * qx1));
     *reinterpret_cast<double2*>(QY + oP) = make_double2(cg.x * (op.sy * qy0), cg.y * (op.sy * qy1));
   }
@@ -2076,7 +2127,7 @@ __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, cons
     const bool yd = lane >= 8;
     const int r = lane & 7;
     const int up = L.up, u0 = L.u0;     // own face nodes
-    const int cu = L.cu, c0_ = L.c0;    // the same, row-major (Ce)
+    const int cu = L.cu, c0_ = L.c0;    // the same in raw order (Ce)
     const double jp = Ue[up] - (yd ? UT : UR)[L.n0_];
     const double jm = (yd ? UB : UL)[L.nP] - Ue[u0];
     const double cP = Ce[cu], c0 = Ce[c0_];
@@ -2088,9 +2139,23 @@ __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, cons
     const double fm = -(0.5 * (qnm + q0)) + (mu * (0.5 * (fcm + c0))) * jm;
     *reinterpret_cast<double2*>(FC + lane * 2) = make_double2(fp, fm);
     *reinterpret_cast<double2*>(FC + 32 + lane * 2) = make_double2(sc * ((0.5 * cP) * jp), sc * ((0.5 * c0) * jm));
+  } else if constexpr (SUB == 2) {
+    // the face between the two sub-elements of line r (lanes 16..23: x-row r, 24..31: y-column r): both
+    // sides in the tile.  Seen from the lower / left element it is the P face (own node 3, neighbour
+    // node 4), from the upper / right one the 0 face; the numerical flux is the same expression with
+    // the same operands in the same order for both (wph_phase's fpx and fmx), so it is formed once
+    const bool yd = lane >= 24;
+    const int ll = lane - 16;
+    const double u3 = Ue[L.i3], u4 = Ue[L.i4], c3 = Ce[L.ci3], c4 = Ce[L.ci4];
+    const double q3 = (yd ? QY : QX)[L.i3], q4 = (yd ? QY : QX)[L.i4];
+    const double mu = yd ? op.muy : op.mux, sc = yd ? op.sy : op.sx;
+    const double jmp = u3 - u4;
+    const double fi = -(0.5 * (q3 + q4)) + (mu * (0.5 * (c3 + c4))) * jmp;
+    *reinterpret_cast<double2*>(FC + 64 + ll * 2) = make_double2(fi, 0.0);
+    *reinterpret_cast<double2*>(FC + 96 + ll * 2) = make_double2(sc * ((0.5 * c3) * jmp), sc * ((0.5 * c4) * jmp));
   }
   __syncwarp();
-  {
+  if constexpr (SUB == 1) {
     const double2 rx = *reinterpret_cast<const double2*>(FC + g * 2);
     const double2 rz = *reinterpret_cast<const double2*>(FC + 32 + g * 2);
     if (n0 + 1 == P) bx1 += rx.x;
@@ -2108,6 +2173,42 @@ __device__ __forceinline__ void fz_sip(const Op2DDev& op, const MmaLane& K, cons
     by1 -= cz.z * K.dPg;
     by0 -= cz.y * K.d0g;
     by1 -= cz.w * K.d0g;
+  } else {
+    // per sub-element: P-face terms then 0-face terms (wph_phase's order).  Left / lower element: P face =
+    // the internal one, 0 face = the tile's outer L / B; right / upper element: P face = outer R / T, 0 face
+    // = internal.  K.dPn / d0n / dPg / d0g hold D4[3][.] / D4[0][.] at the node's local index.
+    {
+      const double2 ox = *reinterpret_cast<const double2*>(FC + g * 2);        // outer (fp R, fm L) of x-row g
+      const double2 oz = *reinterpret_cast<const double2*>(FC + 32 + g * 2);   // outer adjoint (R, L)
+      const double2 ix = *reinterpret_cast<const double2*>(FC + 64 + g * 2);   // internal flux
+      const double2 iz = *reinterpret_cast<const double2*>(FC + 96 + g * 2);   // internal adjoint (node 3 side, node 4 side)
+      const bool left = n0 < 4;
+      const double fP = left ? ix.x : ox.x, f0 = left ? ox.y : ix.x;
+      const double lP = left ? iz.x : oz.x, l0 = left ? oz.y : iz.y;
+      if (((n0 + 1) & 3) == 3) bx1 += fP;
+      if ((n0 & 3) == 0) bx0 -= f0;
+      bx0 -= lP * K.dPn[0];
+      bx1 -= lP * K.dPn[1];
+      bx0 -= l0 * K.d0n[0];
+      bx1 -= l0 * K.d0n[1];
+    }
+    {
+      const double4 of = *reinterpret_cast<const double4*>(FC + (8 + n0) * 2);        // outer (fp T, fm B) of columns n0, n0+1
+      const double4 oz = *reinterpret_cast<const double4*>(FC + 32 + (8 + n0) * 2);
+      const double4 iy = *reinterpret_cast<const double4*>(FC + 64 + (8 + n0) * 2);   // internal flux of columns n0, n0+1
+      const double4 iz = *reinterpret_cast<const double4*>(FC + 96 + (8 + n0) * 2);
+      const bool low = g < 4;
+      const double fP0 = low ? iy.x : of.x, fP1 = low ? iy.z : of.z;
+      const double f00 = low ? of.y : iy.x, f01 = low ? of.w : iy.z;
+      const double lP0 = low ? iz.x : oz.x, lP1 = low ? iz.z : oz.z;
+      const double l00 = low ? oz.y : iz.y, l01 = low ? oz.w : iz.w;
+      if ((g & 3) == 3) { by0 += fP0; by1 += fP1; }
+      if ((g & 3) == 0) { by0 -= f00; by1 -= f01; }
+      by0 -= lP0 * K.dPg;
+      by1 -= lP1 * K.dPg;
+      by0 -= l00 * K.d0g;
+      by1 -= l01 * K.d0g;
+    }
   }
 }
 
@@ -2129,10 +2230,13 @@ __device__ __forceinline__ void blk_part3(double v0, double v1, double v2, doubl
   }
 }
 
-template <int NC>
+template <int NC, int SUB = 1>
 __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   extern __shared__ double sm[];
-  using F = Fz<NC>;
+  using F = Fz<NC, SUB>;
+  // tile geometry: a tile is SUB x SUB elements of EN nodes; TW doubles of one element row per tile
+  constexpr unsigned EN = 64u / (SUB * SUB), TW = 64u / SUB;
+  constexpr uint32_t RUN = 512u / SUB;   // bytes of one contiguous run of a tile vector (SUB runs)
   cg::grid_group grid = cg::this_grid();
   const Op2DDev& op = A.op;
   constexpr int SL = F::SL, NW = F::NW;
@@ -2160,20 +2264,29 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   double rho = single ? 1.0 : A.scal[3], alpha = single ? A.sc->alpha : A.scal[4], beta = single ? A.sc->beta : 0.0;
   double rgam = single ? 0.0 : A.scal[5], ralpha = single ? 0.0 : A.scal[6];
   MmaLane K;
-  mma_lane_init(op, K);
+  if constexpr (SUB == 1) mma_lane_init(op, K); else mma_lane_init_sub2(op, K);
   FzLane L;
-  fz_lane_init(L);
+  fz_lane_init<SUB>(L);
+  const unsigned epitch = (unsigned)op.nex * EN;   // doubles of one element row of one field
+  // offset of tile node (row, col) from the tile's first node in memory
+  auto toff = [&](int row, int col) -> unsigned {
+    if constexpr (SUB == 1) return (unsigned)(row * 8 + col);
+    return (unsigned)(row >> 2) * epitch + (unsigned)((col >> 2) * 16 + (row & 3) * 4 + (col & 3));
+  };
+  const unsigned lglob = toff(lane >> 2, 2 * (lane & 3));   // this lane's node pair
   double* slot0 = A.part;
   double* slot1 = A.part + 4 * G;
   const int g = lane >> 2, n0 = 2 * (lane & 3);
   const int f = lane >> 3, kf = lane & 7;
-  const int fnode = f == FR ? kf * 8 : f == FL ? kf * 8 + 7 : f == FT ? kf : 56 + kf;   // neighbour's face node
+  const unsigned fnode = f == FR ? toff(kf, 0) : f == FL ? toff(kf, 7) : f == FT ? toff(0, kf) : toff(7, kf);   // neighbour's face node
   const int tr0 = sw8(lane & 7, lane >> 3), tr1 = sw8(lane & 7, 4 + (lane >> 3));   // node v -> line v%8, pos v/8
+  const int hr0 = raw_idx<SUB>(lane >> 3, lane & 7), hr1 = raw_idx<SUB>(4 + (lane >> 3), lane & 7);   // the same nodes, raw order
   const int oP = L.oP;   // this lane's node pair in a tile
   // transposed position of this lane's own node pair (row g, columns n0, n0+1); odd rows store the second
   // node first so that one store instruction hits all 16 bank pairs
   const int ta = (g & 1) ? sw8(n0 + 1, g) : sw8(n0, g), tb = (g & 1) ? sw8(n0, g) : sw8(n0 + 1, g);
-  const int nstr = (op.nex + SL - 1) / SL, nbands = (op.ney + NW - 1) / NW;
+  const int nexT = op.nex / SUB, neyT = op.ney / SUB;   // tiles per row / tile rows (SUB = 2: even sizes only)
+  const int nstr = (nexT + SL - 1) / SL, nbands = (neyT + NW - 1) / NW;
   const long long nunits = (long long)nbands * nstr * NC;
   unsigned oc = 0, hc = 0;   // completed uses of this warp's own stages / of the halo stages (stage = use & 1)
   unsigned ac = 0;           // this warp's arrivals on the column barrier (= steps done)
@@ -2202,18 +2315,23 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       // bands fastest: the blocks in flight work on vertically adjacent bands of one strip column, so the
       // rows bordering a band (rebuilt from their raw r, s, w) are L2 hits, not a second DRAM read
       const int band = (int)(tq % nbands), sx = (int)(tq / nbands);
-      const int y0 = band * NW, nrows = op.ney - y0 < NW ? op.ney - y0 : NW;
+      const int y0 = band * NW, nrows = neyT - y0 < NW ? neyT - y0 : NW;
       const bool valid = warp < nrows;
-      const int ey = (valid ? y0 + warp : y0) + op.row0;   // storage row (a partition's ghost rows: ynb)
-      const int x0 = sx * SL, x1 = x0 + SL < op.nex ? x0 + SL : op.nex;
+      const int ey = (valid ? y0 + warp : y0) + op.row0;   // (storage) tile row; a partition's ghost rows: ynb
+      const int x0 = sx * SL, x1 = x0 + SL < nexT ? x0 + SL : nexT;
       // offsets in doubles fit 32 bits (checked by the launcher: n < 2^32)
       const unsigned fo = (unsigned)(c * nn);
-      const unsigned rowC = (unsigned)ey * op.nex * 64u;
-      const unsigned rowT = (unsigned)ynb(op, ey, 1) * op.nex * 64u;
-      const unsigned rowB = (unsigned)ynb(op, ey, -1) * op.nex * 64u;
-      const unsigned hrow0 = (unsigned)ynb(op, op.row0 + y0 + nrows - 1, 1) * op.nex * 64u;   // above the band
-      const unsigned hrow1 = (unsigned)ynb(op, op.row0 + y0, -1) * op.nex * 64u;              // below the band
-      const unsigned oC = fo + rowC + 2 * lane;
+      // first node of a tile row: SUB = 1 the element row (ghost rows of a partition through ynb); SUB = 2
+      // (single domain only) the lower of its two element rows, periodic in tile rows
+      auto trow = [&](int ty, int d) -> unsigned {
+        if constexpr (SUB == 1) return (unsigned)(d == 0 ? ty : ynb(op, ty, d)) * epitch;
+        const int t2 = ty + d;
+        return (unsigned)((t2 < 0 ? neyT - 1 : t2 >= neyT ? 0 : t2) * SUB) * epitch;
+      };
+      const unsigned rowC = trow(ey, 0), rowT = trow(ey, 1), rowB = trow(ey, -1);
+      const unsigned hrow0 = trow(op.row0 + y0 + nrows - 1, 1);   // above the band
+      const unsigned hrow1 = trow(op.row0 + y0, -1);              // below the band
+      const unsigned oC = fo + rowC + lglob;
       const unsigned cfb = (f == FT ? rowT : f == FB ? rowB : rowC) + fnode;   // this lane's face coefficient row
       // own stage of step js: r, s, w, dinv of column js+1, cf of column js (js >= x0)
       auto issue_own = [&](int js, unsigned use) {
@@ -2221,15 +2339,20 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           const uint32_t mb = mb_own + 8u * (use & 1u);
           const uint32_t dst = smem_u32(ws + F::RAW + (use & 1u) * 320);
           int en = js + 1;
-          en = en < 0 ? op.nex - 1 : en >= op.nex ? 0 : en;
-          const unsigned e1 = fo + rowC + (unsigned)en * 64u;
+          en = en < 0 ? nexT - 1 : en >= nexT ? 0 : en;
+          const unsigned e1 = fo + rowC + (unsigned)en * TW;
           const bool cf = js >= x0;
           mbar2_expect(mb, cf ? 2560u : 2048u);
-          bulk_g2s(dst, Ro + e1, 512u, mb);
-          bulk_g2s(dst + 512u, So + e1, 512u, mb);
-          bulk_g2s(dst + 1024u, Wo + e1, 512u, mb);
-          bulk_g2s(dst + 1536u, A.DINV + (e1 - fo), 512u, mb);
-          if (cf) bulk_g2s(dst + 2048u, A.Cf + (rowC + (unsigned)js * 64u), 512u, mb);
+#pragma unroll
+          for (int rn = 0; rn < SUB; ++rn) {   // SUB runs per tile vector (one per element row)
+            const unsigned eo_ = e1 + rn * epitch;
+            const uint32_t d = dst + rn * RUN;
+            bulk_g2s(d, Ro + eo_, RUN, mb);
+            bulk_g2s(d + 512u, So + eo_, RUN, mb);
+            bulk_g2s(d + 1024u, Wo + eo_, RUN, mb);
+            bulk_g2s(d + 1536u, A.DINV + (eo_ - fo), RUN, mb);
+            if (cf) bulk_g2s(d + 2048u, A.Cf + (rowC + rn * epitch + (unsigned)js * TW), RUN, mb);
+          }
         }
       };
       // halo stage h (0 above, 1 below the band) of step js: r, s, w, dinv of column js+1
@@ -2237,17 +2360,22 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
         if (lane == 0) {
           const uint32_t mb = mb_halo + 16u * h + 8u * (use & 1u);
           const uint32_t dst = smem_u32(sm + F::HRAW + (h * 2 + (use & 1u)) * 256);
-          const unsigned e1 = fo + (h ? hrow1 : hrow0) + (unsigned)(js + 1) * 64u;
+          const unsigned e1 = fo + (h ? hrow1 : hrow0) + (unsigned)(js + 1) * TW;
           mbar2_expect(mb, 2048u);
-          bulk_g2s(dst, Ro + e1, 512u, mb);
-          bulk_g2s(dst + 512u, So + e1, 512u, mb);
-          bulk_g2s(dst + 1024u, Wo + e1, 512u, mb);
-          bulk_g2s(dst + 1536u, A.DINV + (e1 - fo), 512u, mb);
+#pragma unroll
+          for (int rn = 0; rn < SUB; ++rn) {
+            const unsigned eo_ = e1 + rn * epitch;
+            const uint32_t d = dst + rn * RUN;
+            bulk_g2s(d, Ro + eo_, RUN, mb);
+            bulk_g2s(d + 512u, So + eo_, RUN, mb);
+            bulk_g2s(d + 1024u, Wo + eo_, RUN, mb);
+            bulk_g2s(d + 1536u, A.DINV + (eo_ - fo), RUN, mb);
+          }
         }
       };
       auto cfn_load = [&](int col) {   // neighbour face coefficients of column col
-        const int exr = col + 1 == op.nex ? 0 : col + 1, exl = col == 0 ? op.nex - 1 : col - 1;
-        return A.Cf[cfb + (unsigned)(f == FR ? exr : f == FL ? exl : col) * 64u];
+        const int exr = col + 1 == nexT ? 0 : col + 1, exl = col == 0 ? nexT - 1 : col - 1;
+        return A.Cf[cfb + (unsigned)(f == FR ? exr : f == FL ? exl : col) * TW];
       };
       // (no block barrier between units: warp 0 issues the halo stages below after its last wait on the
       // column barrier, which every warp passed after its last halo rebuild)
@@ -2276,14 +2404,14 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
         const int sJ = sl == 2 ? 0 : sl + 1;        // slot of column j
         const int tN = (st + 1) & 3;                // RT slot of column j + 1 (free: see the column barrier below)
         if (valid) {
-          const unsigned gn = oC + (unsigned)jn * 64u;   // used inside the strip only
+          const unsigned gn = oC + (unsigned)jn * TW;   // used inside the strip only
           const double* raw = ws + F::RAW + (oc & 1u) * 320;
           mbar2_wait(mb_own + 8u * (oc & 1u), (oc >> 1) & 1u);
           {   // u' of column j + 1 (and, inside the strip, its s', r', p, x)
-            const double2 r = *reinterpret_cast<const double2*>(raw + 2 * lane);
-            double2 s = *reinterpret_cast<const double2*>(raw + 64 + 2 * lane);
-            const double2 w = *reinterpret_cast<const double2*>(raw + 128 + 2 * lane);
-            const double2 di = *reinterpret_cast<const double2*>(raw + 192 + 2 * lane);
+            const double2 r = *reinterpret_cast<const double2*>(raw + L.lraw);
+            double2 s = *reinterpret_cast<const double2*>(raw + 64 + L.lraw);
+            const double2 w = *reinterpret_cast<const double2*>(raw + 128 + L.lraw);
+            const double2 di = *reinterpret_cast<const double2*>(raw + 192 + L.lraw);
             if (first) s = make_double2(0.0, 0.0);
             double2 sn, rn, uu;
             sn.x = fma(beta, s.x, w.x);
@@ -2318,7 +2446,7 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
             // j + 1.  Unconditional (clamped columns): a load inside a branch makes the compiler wait
             // for it at the join, which serialised the whole step on these loads
           const int j2 = j + 2 < x0 ? x0 : j + 2 < x1 ? j + 2 : x1 - 1;
-          const unsigned g2 = oC + (unsigned)j2 * 64u;
+          const unsigned g2 = oC + (unsigned)j2 * TW;
           pp = __ldcs(reinterpret_cast<const double2*>(A.Pv + g2));
           xx = __ldcs(reinterpret_cast<const double2*>(A.x + g2));
           cfn_reg = cfn_load(j + 1 < x0 ? x0 : j + 1 < x1 ? j + 1 : x1 - 1);
@@ -2332,7 +2460,7 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
               double* rt = RT + (tN * (NW + 2) + NW + h) * 64;
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
-                const int v = lane + 32 * q;
+                const int v = q ? hr1 : hr0;   // node lane + 32 q of the tile, in raw order
                 const double s = first ? 0.0 : raw[64 + v];
                 const double sn = fma(beta, s, raw[128 + v]);
                 const double rn = fma(-alpha, sn, raw[v]);
@@ -2355,13 +2483,13 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           const double* Ue = ws + F::RING + sJ * 64;
           const double* rtj = RT + st * (NW + 2) * 64;
           double bx0, bx1, by0, by1;
-          fz_sip(op, K, L, Ue, ws + F::RING + sN * 64, ws + F::RING + sl * 64,
+          fz_sip<SUB>(op, K, L, Ue, ws + F::RING + sN * 64, ws + F::RING + sl * 64,
                  rtj + (warp + 1 < nrows ? warp + 1 : NW) * 64, rtj + (warp > 0 ? warp - 1 : NW + 1) * 64,
                  ws + F::RAW + (oc & 1u) * 320 + 256, ws + F::CFN, ws + F::QX, ws + F::QY, ws + F::DOT, ws + F::FCON, bx0, bx1, by0, by1);
           const double2 v = *reinterpret_cast<const double2*>(Ue + oP);
           const double w0 = fma(A.a, fma(K.hwy, bx0, K.hwx[0] * by0), K.hh[0] * v.x);
           const double w1 = fma(A.a, fma(K.hwy, bx1, K.hwx[1] * by1), K.hh[1] * v.y);
-          *reinterpret_cast<double2*>(Wn + (oC + (unsigned)j * 64u)) = make_double2(w0, w1);   // g * 8 + n0 == 2 lane
+          *reinterpret_cast<double2*>(Wn + (oC + (unsigned)j * TW)) = make_double2(w0, w1);
           wu = fma(w0, v.x, wu);
           wu = fma(w1, v.y, wu);
           __syncwarp();   // scratch is rewritten by the next step
@@ -2810,25 +2938,25 @@ static cudaError_t cg_occupancy(int* per_sm) {
 
 // fused pass: resident blocks x SMs (at most the setup kernel's grid: the partial
 // slots are sized for it), capped by the (band, strip, field) units
-template <int NC>
+template <int NC, int SUB>
 static cudaError_t launch_cgf(int device, void** args, const Op2DDev& op, int max_blocks, cudaStream_t st) {
-  using F = Fz<NC>;
+  using F = Fz<NC, SUB>;
   constexpr int smem = (int)(sizeof(double) * F::SIZE);
   static int resident = 0;
   if (resident == 0) {
     int per_sm = 0, sms = 0;
-    cudaError_t e = cudaFuncSetAttribute(k2_cgf<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_cgf<NC>, F::NW * 32, smem);
+    cudaError_t e = cudaFuncSetAttribute(k2_cgf<NC, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_cgf<NC, SUB>, F::NW * 32, smem);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     resident = per_sm * sms;
   }
-  long long nb = (long long)((op.ney + F::NW - 1) / F::NW) * ((op.nex + F::SL - 1) / F::SL) * NC;   // units
+  long long nb = (long long)((op.ney / SUB + F::NW - 1) / F::NW) * ((op.nex / SUB + F::SL - 1) / F::SL) * NC;   // units
   if (nb > resident) nb = resident;
   if (nb > max_blocks) nb = max_blocks;
   if (nb < 1) nb = 1;
-  return cudaLaunchCooperativeKernel((void*)k2_cgf<NC>, dim3((unsigned)nb), dim3(F::NW * 32), args, smem, st);
+  return cudaLaunchCooperativeKernel((void*)k2_cgf<NC, SUB>, dim3((unsigned)nb), dim3(F::NW * 32), args, smem, st);
 }
 
 #define SISDC_P1_SWITCH(p1, ...)                                 \
@@ -3005,15 +3133,23 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
     const char* v = getenv("SISDC_CG_FUSED");
     return !(v && v[0] == '0');
   }();
-  const bool fused = fused_on && op.p1 == 8 && op.row0 == 0;
+  // P = 7 elements, or P = 3 elements in 2 x 2 tiles (even mesh; SISDC_CG_FUSED3=0 keeps the two-phase kernel)
+  static const bool fused3_on = [] {
+    const char* v = getenv("SISDC_CG_FUSED3");
+    return !(v && v[0] == '0');
+  }();
+  const bool sub2 = op.p1 == 4 && fused3_on && op.nex % 2 == 0 && op.ney % 2 == 0 && op.nex >= 2 && op.ney >= 2;
+  const bool fused = fused_on && (op.p1 == 8 || sub2) && op.row0 == 0 && (op.nc == 4 || op.nc == 1);
   if (fused) {
     // coefficient and Jacobi diagonal at full occupancy (fp64 sqrt / division chains want more warps
     // than the 128-register cooperative kernel has), then k2_cg's setup 2 / 3 only (mode 2)
     const unsigned nb1 = (unsigned)((op.nn + 255) / 256);
-    k2_coef<8><<<nb1, 256, 0, c->stream>>>(op, k, A.Cf);
+    if (sub2) k2_coef<4><<<nb1, 256, 0, c->stream>>>(op, k, A.Cf);
+    else k2_coef<8><<<nb1, 256, 0, c->stream>>>(op, k, A.Cf);
     int rc = c->after_launch("k2_coef (CG setup)");
     if (rc) return rc;
-    k2p_dinv<8><<<nb1, 256, 0, c->stream>>>(A);
+    if (sub2) k2p_dinv<4><<<nb1, 256, 0, c->stream>>>(A);
+    else k2p_dinv<8><<<nb1, 256, 0, c->stream>>>(A);
     rc = c->after_launch("k2p_dinv (CG setup)");
     if (rc) return rc;
     A.mode = 2;
@@ -3026,8 +3162,12 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
   if (fused) {
     int rc = c->after_launch("k2_cg (setup)");
     if (rc) return rc;
-    e = op.nc == 4 ? launch_cgf<4>(c->device, args, op, nblocks, c->stream)
-                   : launch_cgf<1>(c->device, args, op, nblocks, c->stream);
+    if (sub2)
+      e = op.nc == 4 ? launch_cgf<4, 2>(c->device, args, op, nblocks, c->stream)
+                     : launch_cgf<1, 2>(c->device, args, op, nblocks, c->stream);
+    else
+      e = op.nc == 4 ? launch_cgf<4, 1>(c->device, args, op, nblocks, c->stream)
+                     : launch_cgf<1, 1>(c->device, args, op, nblocks, c->stream);
     if (e != cudaSuccess) return c->cuda(e, "k2_cgf cooperative launch");
     return c->after_launch("k2_cgf");
   }
