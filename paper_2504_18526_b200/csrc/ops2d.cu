@@ -2230,7 +2230,14 @@ __device__ __forceinline__ void blk_part3(double v0, double v1, double v2, doubl
   }
 }
 
-template <int NC, int SUB = 1>
+// MODE 0: the iterations.  MODE 1 / 2: the two setup passes of a solve as single passes of the same
+// pipeline (separate instantiations = separate launches, registers and code):
+//   1  r0 = b - A x0 (x0 = rhs, b = M rhs) -> R, partials (b,b), #nonzero b -> slot 2
+//   2  u0 = r0 dinv (rebuilt on chip), w0 = A u0 -> W, partials (r0,u0), (w0,u0), (r0,r0) -> slot 3
+// MODE 0 then derives thr, rho, alpha from slots 2 / 3 itself (every block, one fixed order), reads x0 = rhs
+// and p = 0 in its first iteration (no initialisation pass) and zero-fills x when b == 0.  With A.mode == 2
+// (setup by k2_cg) it reads the scalars k2_cg left instead.
+template <int NC, int SUB = 1, int MODE = 0>
 __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   extern __shared__ double sm[];
   using F = Fz<NC, SUB>;
@@ -2258,11 +2265,59 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   __syncthreads();
   // single-pass mode (A.sc set: the split solve of an element-row partition, part2d.cu): ONE pass with the
   // scalars of the solve's CgPScal, buffer parity A.px, block partials to part / part2; no grid barrier
-  const bool single = A.sc != nullptr;
-  if (single ? A.sc->done != 0 : A.scal[7] == 0.0) return;   // converged / b == 0 (x = 0 written by the setup)
-  const double thr = single ? 0.0 : A.scal[2];
-  double rho = single ? 1.0 : A.scal[3], alpha = single ? A.sc->alpha : A.scal[4], beta = single ? A.sc->beta : 0.0;
-  double rgam = single ? 0.0 : A.scal[5], ralpha = single ? 0.0 : A.scal[6];
+  const bool single = MODE != 0 || A.sc != nullptr;   // one pass, then block partials and return
+  const bool own_setup = MODE == 0 && A.sc == nullptr && A.mode == 3;   // the solve was set up by MODE 1 / 2 launches
+  double* const slot2 = A.part + 8 * G;    // MODE 1 partials
+  double* const slot3 = A.part + 12 * G;   // MODE 2 partials
+  // every block sums G slots of three values in one fixed order (bitwise-identical totals everywhere)
+  auto slot_total = [&](const double* slot, double (&t)[3]) {
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int b = threadIdx.x; b < G; b += blockDim.x) { v0 += slot[b * 4]; v1 += slot[b * 4 + 1]; v2 += slot[b * 4 + 2]; }
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+      v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+    }
+    __syncthreads();
+    if (lane == 0) { red[warp * 4] = v0; red[warp * 4 + 1] = v1; red[warp * 4 + 2] = v2; }
+    __syncthreads();
+    t[0] = t[1] = t[2] = 0.0;
+    for (int ww = 0; ww < NW; ++ww) { t[0] += red[ww * 4]; t[1] += red[ww * 4 + 1]; t[2] += red[ww * 4 + 2]; }
+    __syncthreads();
+  };
+  double thr = 0.0, rho = 1.0, alpha = 0.0, beta = 0.0, rgam = 0.0, ralpha = 0.0;
+  if constexpr (MODE == 0) {
+    if (A.sc != nullptr) {   // split solve of a partition: scalars of the solve's CgPScal
+      if (A.sc->done != 0) return;
+      alpha = A.sc->alpha;
+      beta = A.sc->beta;
+    } else if (own_setup) {
+      double t2[3], t3[3];
+      slot_total(slot2, t2);
+      if (t2[1] == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
+        const long long nthr = (long long)G * blockDim.x;
+        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < op.n; t += nthr) A.x[t] = 0.0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+          int idx = atomicAdd(&A.status[2], 1);
+          if (idx < A.log_cap) { A.log_it[idx] = 0; A.log_margin[idx] = 0.0; }
+        }
+        return;
+      }
+      slot_total(slot3, t3);
+      thr = A.dbg ? -1.0 : A.rtol2 * t2[0];
+      rho = t3[2];
+      alpha = t3[0] / t3[1];
+      rgam = 1.0 / t3[0];
+      ralpha = 1.0 / alpha;
+    } else {                 // setup by k2_cg (mode 2)
+      if (A.scal[7] == 0.0) return;   // b == 0 (x = 0 written by the setup)
+      thr = A.scal[2]; rho = A.scal[3]; alpha = A.scal[4]; rgam = A.scal[5]; ralpha = A.scal[6];
+    }
+  } else if constexpr (MODE == 2) {
+    double t2[3];
+    slot_total(slot2, t2);
+    if (t2[1] == 0.0) return;   // b == 0: MODE 0 writes x = 0
+  }
   MmaLane K;
   if constexpr (SUB == 1) mma_lane_init(op, K); else mma_lane_init_sub2(op, K);
   FzLane L;
@@ -2300,8 +2355,10 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
     if (k >= maxit) { ok = false; break; }
     const bool stamp = stampb && k == 2;
     if (stamp) tm[0] = tm[1] = tm[2] = gtimer();
-    const bool first = single ? A.sc->k == 0 : k == 0;
-    const int par = single ? A.px : (k & 1);
+    const bool first = MODE != 0 ? true : (A.sc != nullptr ? A.sc->k == 0 : k == 0);
+    const int par = MODE != 0 ? 0 : (A.sc != nullptr ? A.px : (k & 1));
+    const bool x_from_rhs = own_setup && k == 0;   // x0 = rhs, p = 0: read, never initialised
+    double bb = 0.0, nz = 0.0;                     // MODE 1 partials
     const double* const Ro = par ? A.R2 : A.R;
     const double* const So = par ? A.S2 : A.S;
     const double* const Wo = par ? A.W2 : A.W;
@@ -2342,15 +2399,18 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           en = en < 0 ? nexT - 1 : en >= nexT ? 0 : en;
           const unsigned e1 = fo + rowC + (unsigned)en * TW;
           const bool cf = js >= x0;
-          mbar2_expect(mb, cf ? 2560u : 2048u);
+          constexpr uint32_t NV = MODE == 0 ? 4u : MODE == 1 ? 1u : 2u;   // r s w dinv | rhs | r dinv
+          mbar2_expect(mb, (cf ? NV + 1u : NV) * 512u);
 #pragma unroll
           for (int rn = 0; rn < SUB; ++rn) {   // SUB runs per tile vector (one per element row)
             const unsigned eo_ = e1 + rn * epitch;
             const uint32_t d = dst + rn * RUN;
-            bulk_g2s(d, Ro + eo_, RUN, mb);
-            bulk_g2s(d + 512u, So + eo_, RUN, mb);
-            bulk_g2s(d + 1024u, Wo + eo_, RUN, mb);
-            bulk_g2s(d + 1536u, A.DINV + (eo_ - fo), RUN, mb);
+            bulk_g2s(d, (MODE == 1 ? A.rhs : Ro) + eo_, RUN, mb);
+            if constexpr (MODE == 0) {
+              bulk_g2s(d + 512u, So + eo_, RUN, mb);
+              bulk_g2s(d + 1024u, Wo + eo_, RUN, mb);
+            }
+            if constexpr (MODE != 1) bulk_g2s(d + 1536u, A.DINV + (eo_ - fo), RUN, mb);
             if (cf) bulk_g2s(d + 2048u, A.Cf + (rowC + rn * epitch + (unsigned)js * TW), RUN, mb);
           }
         }
@@ -2361,15 +2421,18 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           const uint32_t mb = mb_halo + 16u * h + 8u * (use & 1u);
           const uint32_t dst = smem_u32(sm + F::HRAW + (h * 2 + (use & 1u)) * 256);
           const unsigned e1 = fo + (h ? hrow1 : hrow0) + (unsigned)(js + 1) * TW;
-          mbar2_expect(mb, 2048u);
+          constexpr uint32_t NV = MODE == 0 ? 4u : MODE == 1 ? 1u : 2u;
+          mbar2_expect(mb, NV * 512u);
 #pragma unroll
           for (int rn = 0; rn < SUB; ++rn) {
             const unsigned eo_ = e1 + rn * epitch;
             const uint32_t d = dst + rn * RUN;
-            bulk_g2s(d, Ro + eo_, RUN, mb);
-            bulk_g2s(d + 512u, So + eo_, RUN, mb);
-            bulk_g2s(d + 1024u, Wo + eo_, RUN, mb);
-            bulk_g2s(d + 1536u, A.DINV + (eo_ - fo), RUN, mb);
+            bulk_g2s(d, (MODE == 1 ? A.rhs : Ro) + eo_, RUN, mb);
+            if constexpr (MODE == 0) {
+              bulk_g2s(d + 512u, So + eo_, RUN, mb);
+              bulk_g2s(d + 1024u, Wo + eo_, RUN, mb);
+            }
+            if constexpr (MODE != 1) bulk_g2s(d + 1536u, A.DINV + (eo_ - fo), RUN, mb);
           }
         }
       };
@@ -2407,7 +2470,27 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           const unsigned gn = oC + (unsigned)jn * TW;   // used inside the strip only
           const double* raw = ws + F::RAW + (oc & 1u) * 320;
           mbar2_wait(mb_own + 8u * (oc & 1u), (oc >> 1) & 1u);
-          {   // u' of column j + 1 (and, inside the strip, its s', r', p, x)
+          if constexpr (MODE != 0) {   // setup passes: u' = x0 (MODE 1) or r0 dinv (MODE 2), nothing written here
+            const double2 r = *reinterpret_cast<const double2*>(raw + L.lraw);
+            double2 uu = r;
+            if constexpr (MODE == 2) {
+              const double2 di = *reinterpret_cast<const double2*>(raw + 192 + L.lraw);
+              uu.x = r.x * di.x;
+              uu.y = r.y * di.y;
+            }
+            *reinterpret_cast<double2*>(ws + F::RING + sN * 64 + oP) = uu;
+            if (own) {
+              double* rt = RT + (tN * (NW + 2) + warp) * 64;
+              rt[ta] = (g & 1) ? uu.y : uu.x;
+              rt[tb] = (g & 1) ? uu.x : uu.y;
+              if constexpr (MODE == 2) {
+                ru = fma(r.x, uu.x, ru);
+                rr = fma(r.x, r.x, rr);
+                ru = fma(r.y, uu.y, ru);
+                rr = fma(r.y, r.y, rr);
+              }
+            }
+          } else {   // u' of column j + 1 (and, inside the strip, its s', r', p, x)
             const double2 r = *reinterpret_cast<const double2*>(raw + L.lraw);
             double2 s = *reinterpret_cast<const double2*>(raw + 64 + L.lraw);
             const double2 w = *reinterpret_cast<const double2*>(raw + 128 + L.lraw);
@@ -2447,8 +2530,11 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
             // for it at the join, which serialised the whole step on these loads
           const int j2 = j + 2 < x0 ? x0 : j + 2 < x1 ? j + 2 : x1 - 1;
           const unsigned g2 = oC + (unsigned)j2 * TW;
-          pp = __ldcs(reinterpret_cast<const double2*>(A.Pv + g2));
-          xx = __ldcs(reinterpret_cast<const double2*>(A.x + g2));
+          if constexpr (MODE == 0) {
+            pp = __ldcs(reinterpret_cast<const double2*>(A.Pv + g2));                      // (p = 0 in the first
+            xx = __ldcs(reinterpret_cast<const double2*>((x_from_rhs ? A.rhs : A.x) + g2));   // iteration: below)
+            if (x_from_rhs) pp = make_double2(0.0, 0.0);
+          }
           cfn_reg = cfn_load(j + 1 < x0 ? x0 : j + 1 < x1 ? j + 1 : x1 - 1);
         }
         if (own) {   // u' of the rows above / below the band at column j + 1, by a warp that rotates with j
@@ -2461,10 +2547,16 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int v = q ? hr1 : hr0;   // node lane + 32 q of the tile, in raw order
-                const double s = first ? 0.0 : raw[64 + v];
-                const double sn = fma(beta, s, raw[128 + v]);
-                const double rn = fma(-alpha, sn, raw[v]);
-                rt[q ? tr1 : tr0] = rn * raw[192 + v];
+                if constexpr (MODE == 1) {
+                  rt[q ? tr1 : tr0] = raw[v];
+                } else if constexpr (MODE == 2) {
+                  rt[q ? tr1 : tr0] = raw[v] * raw[192 + v];
+                } else {
+                  const double s = first ? 0.0 : raw[64 + v];
+                  const double sn = fma(beta, s, raw[128 + v]);
+                  const double rn = fma(-alpha, sn, raw[v]);
+                  rt[q ? tr1 : tr0] = rn * raw[192 + v];
+                }
               }
               __syncwarp();
               if (j + 3 < x1) issue_halo(h, j + 2, hc + 2);
@@ -2489,9 +2581,18 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           const double2 v = *reinterpret_cast<const double2*>(Ue + oP);
           const double w0 = fma(A.a, fma(K.hwy, bx0, K.hwx[0] * by0), K.hh[0] * v.x);
           const double w1 = fma(A.a, fma(K.hwy, bx1, K.hwx[1] * by1), K.hh[1] * v.y);
-          *reinterpret_cast<double2*>(Wn + (oC + (unsigned)j * TW)) = make_double2(w0, w1);
-          wu = fma(w0, v.x, wu);
-          wu = fma(w1, v.y, wu);
+          if constexpr (MODE == 1) {   // r0 = b - A x0, b = M rhs (v = x0 = rhs at this node pair)
+            const double b0 = K.hh[0] * v.x, b1 = K.hh[1] * v.y;
+            *reinterpret_cast<double2*>(A.R + (oC + (unsigned)j * TW)) = make_double2(b0 - w0, b1 - w1);
+            bb = fma(b0, b0, bb);
+            nz += b0 != 0.0 ? 1.0 : 0.0;
+            bb = fma(b1, b1, bb);
+            nz += b1 != 0.0 ? 1.0 : 0.0;
+          } else {
+            *reinterpret_cast<double2*>((MODE == 2 ? A.W : Wn) + (oC + (unsigned)j * TW)) = make_double2(w0, w1);
+            wu = fma(w0, v.x, wu);
+            wu = fma(w1, v.y, wu);
+          }
           __syncwarp();   // scratch is rewritten by the next step
         }
         if (valid) {   // this step's stage (its cf was read by the matvec) is free: refill it for step j + 2
@@ -2510,7 +2611,14 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       step(x1 - 1, F_{}, T_{});
     }
     if (stamp) tm[3] = gtimer();
-    if (single) {   // block partials in the split solve's slots: part (r,u), (r,r); part2 (w,u)
+    if constexpr (MODE == 1) {
+      blk_part3(bb, nz, 0.0, red, slot2);
+      return;
+    } else if constexpr (MODE == 2) {
+      blk_part3(ru, wu, rr, red, slot3);
+      return;
+    }
+    if (A.sc != nullptr) {   // block partials in the split solve's slots: part (r,u), (r,r); part2 (w,u)
       blk_part3(ru, rr, 0.0, red, A.part);
       blk_part3(wu, 0.0, 0.0, red, A.part2);
       return;
@@ -2560,6 +2668,10 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
     rgam = 1.0 / gn_;
     ralpha = 1.0 / al;
     ++k;
+  }
+  if (own_setup && k == 0) {   // converged before the first iteration: x = x0 = rhs was never written
+    const long long nthr = (long long)G * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < op.n; t += nthr) A.x[t] = A.rhs[t];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     int idx = atomicAdd(&A.status[2], 1);
@@ -2936,27 +3048,49 @@ static cudaError_t cg_occupancy(int* per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k2_cg<P1, NC>, Blk<P1>::NT, smem_cg<P1, NC>());
 }
 
-// fused pass: resident blocks x SMs (at most the setup kernel's grid: the partial
-// slots are sized for it), capped by the (band, strip, field) units
+// fused solve: resident blocks x SMs (the partial slots are sized for cg_blocks), capped by the
+// (band, strip, field) units; the two setup passes (MODE 1, 2) and the iterations (MODE 0) use the
+// same grid, so that the slot sums cover exactly the blocks that wrote them
 template <int NC, int SUB>
-static cudaError_t launch_cgf(int device, void** args, const Op2DDev& op, int max_blocks, cudaStream_t st) {
+static cudaError_t cgf_grid(int device, const Op2DDev& op, int max_blocks, int* nb_out) {
   using F = Fz<NC, SUB>;
   constexpr int smem = (int)(sizeof(double) * F::SIZE);
   static int resident = 0;
   if (resident == 0) {
-    int per_sm = 0, sms = 0;
-    cudaError_t e = cudaFuncSetAttribute(k2_cgf<NC, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_cgf<NC, SUB>, F::NW * 32, smem);
+    int per_sm = 0, p1 = 0, p2 = 0, sms = 0;
+    cudaError_t e = cudaFuncSetAttribute(k2_cgf<NC, SUB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2_cgf<NC, SUB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2_cgf<NC, SUB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_cgf<NC, SUB, 0>, F::NW * 32, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k2_cgf<NC, SUB, 1>, F::NW * 32, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k2_cgf<NC, SUB, 2>, F::NW * 32, smem);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-    resident = per_sm * sms;
+    if (per_sm < 1 || p1 < 1 || p2 < 1) return cudaErrorLaunchOutOfResources;
+    resident = per_sm * sms;   // only MODE 0 needs co-residency (grid barrier)
   }
   long long nb = (long long)((op.ney / SUB + F::NW - 1) / F::NW) * ((op.nex / SUB + F::SL - 1) / F::SL) * NC;   // units
   if (nb > resident) nb = resident;
   if (nb > max_blocks) nb = max_blocks;
   if (nb < 1) nb = 1;
-  return cudaLaunchCooperativeKernel((void*)k2_cgf<NC, SUB>, dim3((unsigned)nb), dim3(F::NW * 32), args, smem, st);
+  *nb_out = (int)nb;
+  return cudaSuccess;
+}
+template <int NC, int SUB>
+static cudaError_t launch_cgf(int device, Cg2Args& A, void** args, const Op2DDev& op, int max_blocks, bool own_setup,
+                              cudaStream_t st) {
+  using F = Fz<NC, SUB>;
+  constexpr int smem = (int)(sizeof(double) * F::SIZE);
+  int nb = 0;
+  cudaError_t e = cgf_grid<NC, SUB>(device, op, max_blocks, &nb);
+  if (e != cudaSuccess) return e;
+  if (own_setup) {
+    k2_cgf<NC, SUB, 1><<<nb, F::NW * 32, smem, st>>>(A);
+    k2_cgf<NC, SUB, 2><<<nb, F::NW * 32, smem, st>>>(A);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaLaunchCooperativeKernel((void*)k2_cgf<NC, SUB, 0>, dim3((unsigned)nb), dim3(F::NW * 32), args, smem, st);
 }
 
 #define SISDC_P1_SWITCH(p1, ...)                                 \
@@ -3141,6 +3275,8 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
   const bool sub2 = op.p1 == 4 && fused3_on && op.nex % 2 == 0 && op.ney % 2 == 0 && op.nex >= 2 && op.ney >= 2;
   const bool fused = fused_on && (op.p1 == 8 || sub2) && op.row0 == 0 && (op.nc == 4 || op.nc == 1);
   if (fused) {
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(rhs)) & 15))
+      return c->fail(SISDC_ERR_ARG, "2-D implicit solve: rhs and x must be 16-byte aligned");
     // coefficient and Jacobi diagonal at full occupancy (fp64 sqrt / division chains want more warps
     // than the 128-register cooperative kernel has), then k2_cg's setup 2 / 3 only (mode 2)
     const unsigned nb1 = (unsigned)((op.nn + 255) / 256);
@@ -3152,7 +3288,24 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
     else k2p_dinv<8><<<nb1, 256, 0, c->stream>>>(A);
     rc = c->after_launch("k2p_dinv (CG setup)");
     if (rc) return rc;
-    A.mode = 2;
+    // setup passes: the fused pipeline itself (A.mode 3; SISDC_CG_SETUP=0: k2_cg in mode 2)
+    static const bool own_setup_on = [] {
+      const char* v = getenv("SISDC_CG_SETUP");
+      return !(v && v[0] == '0');
+    }();
+    A.mode = own_setup_on ? 3 : 2;
+  }
+  if (A.mode == 3) {
+    cudaError_t e3;
+    if (sub2)
+      e3 = op.nc == 4 ? launch_cgf<4, 2>(c->device, A, args, op, nblocks, true, c->stream)
+                      : launch_cgf<1, 2>(c->device, A, args, op, nblocks, true, c->stream);
+    else
+      e3 = op.nc == 4 ? launch_cgf<4, 1>(c->device, A, args, op, nblocks, true, c->stream)
+                      : launch_cgf<1, 1>(c->device, A, args, op, nblocks, true, c->stream);
+    if (e3 != cudaSuccess) return c->cuda(e3, "k2_cgf solve launch");
+    c->launches += 2;
+    return c->after_launch("k2_cgf");
   }
   SISDC_P1_SWITCH(op.p1, {
     if (op.nc == 4) e = launch_cg_coop<P1, 4>(args, nblocks, c->stream);
@@ -3163,18 +3316,18 @@ int launch2_cg(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs
     int rc = c->after_launch("k2_cg (setup)");
     if (rc) return rc;
     if (sub2)
-      e = op.nc == 4 ? launch_cgf<4, 2>(c->device, args, op, nblocks, c->stream)
-                     : launch_cgf<1, 2>(c->device, args, op, nblocks, c->stream);
+      e = op.nc == 4 ? launch_cgf<4, 2>(c->device, A, args, op, nblocks, false, c->stream)
+                     : launch_cgf<1, 2>(c->device, A, args, op, nblocks, false, c->stream);
     else
-      e = op.nc == 4 ? launch_cgf<4, 1>(c->device, args, op, nblocks, c->stream)
-                     : launch_cgf<1, 1>(c->device, args, op, nblocks, c->stream);
+      e = op.nc == 4 ? launch_cgf<4, 1>(c->device, A, args, op, nblocks, false, c->stream)
+                     : launch_cgf<1, 1>(c->device, A, args, op, nblocks, false, c->stream);
     if (e != cudaSuccess) return c->cuda(e, "k2_cgf cooperative launch");
     return c->after_launch("k2_cgf");
   }
   return c->after_launch("k2_cg");
 }
-size_t cg2_ws_doubles(const Op2DDev& op, int nblocks) {
-  return 7 * (size_t)op.n + 2 * (size_t)op.nn + 16 + 8 * (size_t)nblocks;
+size_t cg2_ws_doubles(const Op2DDev& op, int nblocks) {   // part: four slot arrays of [nblocks][4]
+  return 7 * (size_t)op.n + 2 * (size_t)op.nn + 16 + 16 * (size_t)nblocks;
 }
 // blocks for the cooperative CG: resident blocks x SMs, capped by the element tiles
 int cg2_blocks(Ctx* c, const Op2DDev& op, int* nblocks) {
