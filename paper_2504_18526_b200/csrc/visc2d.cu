@@ -132,23 +132,38 @@ __global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 1) k2_visc(Op2DDev o
   }
   const int ne = op.nex * op.ney;
   const int e0 = blockIdx.x * L::EB;
-  // ---- stage own + face neighbours, all fields (coalesced element runs)
-  for (int t = threadIdx.x; t < L::EB * 5 * NCV * NN; t += blockDim.x) {
-    const int el = t / (5 * NCV * NN), r = t - el * (5 * NCV * NN);
-    const int k = r / (NCV * NN), r2 = r - k * (NCV * NN);
-    const int c = r2 / NN, nd = r2 - c * NN;
-    const int eg = e0 + el;
-    if (eg < ne) {   // asynchronous copies: all of a thread's loads in flight at once
-      const int oy = eg / op.nex, ex = eg - oy * op.nex, ey = oy + op.row0;
-      int sx_ = ex, sy_ = ey;
-      if (k == 1) sx_ = ex + 1 == op.nex ? 0 : ex + 1;
-      if (k == 2) sx_ = ex == 0 ? op.nex - 1 : ex - 1;
-      if (k == 3) sy_ = ynb(op, ey, 1);
-      if (k == 4) sy_ = ynb(op, ey, -1);
-      const unsigned d = (unsigned)__cvta_generic_to_shared(sm + L::U + t);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(um + nidx(op, c, sy_, sx_, 0, 0) + nd) : "memory");
-    } else {
-      sm[L::U + t] = 0.0;
+  // ---- stage own + face neighbours, all fields: EB * 5 * NCV contiguous runs of NN doubles, one run per
+  // warp pass with the index arithmetic per RUN (it was per 8-byte element: a runtime division, a modulo
+  // and a 64-bit index per copy, 35% of the kernel's samples)
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int run = wid; run < L::EB * 5 * NCV; run += nw) {
+      const int el_ = run / (5 * NCV), r = run - el_ * (5 * NCV);
+      const int k = r / NCV, c = r - k * NCV;
+      const int eg_ = e0 + el_;
+      double* dst = sm + L::U + run * NN;
+      if (eg_ < ne) {
+        const int oy = eg_ / op.nex, ex = eg_ - oy * op.nex, ey = oy + op.row0;
+        int sx_ = ex, sy_ = ey;
+        if (k == 1) sx_ = ex + 1 == op.nex ? 0 : ex + 1;
+        if (k == 2) sx_ = ex == 0 ? op.nex - 1 : ex - 1;
+        if (k == 3) sy_ = ynb(op, ey, 1);
+        if (k == 4) sy_ = ynb(op, ey, -1);
+        const double* src = um + nidx(op, c, sy_, sx_, 0, 0);
+        if constexpr (NN % 2 == 0) {   // 16-byte copies (element runs are 16-byte aligned when NN is even)
+          for (int t = 2 * lane; t < NN; t += 64) {
+            const unsigned d = (unsigned)__cvta_generic_to_shared(dst + t);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + t) : "memory");
+          }
+        } else {
+          for (int t = lane; t < NN; t += 32) {
+            const unsigned d = (unsigned)__cvta_generic_to_shared(dst + t);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + t) : "memory");
+          }
+        }
+      } else {
+        for (int t = lane; t < NN; t += 32) dst[t] = 0.0;
+      }
     }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -169,6 +184,14 @@ __global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 1) k2_visc(Op2DDev o
       sm[L::FX + (el * NCV + c) * NN + nd] = Fx[c];
       sm[L::FY + (el * NCV + c) * NN + nd] = Fy[c];
     }
+  }
+  // accumulate mode: this node's f values are read now, behind the face work (the read-modify-write at
+  // the end stalled 10% of the samples on them)
+  double facc[NCV] = {0.0, 0.0, 0.0, 0.0};
+  if (accumulate && eg < ne) {
+    const int oy_ = eg / op.nex, ex_ = eg - oy_ * op.nex;
+#pragma unroll
+    for (int c = 0; c < NCV; ++c) facc[c] = fm[nidx(op, c, oy_ + op.row0, ex_, j, i)];
   }
   // ---- face terms of this element.  4 faces x P1 nodes x 2 sides: every (face node, side) is one
   // unit of work (gradient, flux, G_nn [u] of that side's element), spread over all threads of the
@@ -241,7 +264,7 @@ __global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 1) k2_visc(Op2DDev o
     by -= op.sy * (0.5 * LF[(FB * P1 + i) * NCV + c]) * sD[j];
     const double fv = -bx * sW[i] + -by * sWy[j];
     const long long g = nidx(op, c, ey, ex, j, i);
-    const double out = accumulate ? fm[g] + fv : fv;
+    const double out = accumulate ? facc[c] + fv : fv;
     fm[g] = out;
     bad |= !isfinite(out);
   }
