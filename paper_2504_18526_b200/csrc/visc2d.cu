@@ -112,7 +112,7 @@ __device__ __forceinline__ void face_side(const Op2DDev& op, double gpr, const d
 }
 
 template <int P1>
-__global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 1) k2_visc(Op2DDev op, const double* __restrict__ u, double* __restrict__ f,
+__global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 2) k2_visc(Op2DDev op, const double* __restrict__ u, double* __restrict__ f,
                                                       int m_first, int accumulate, int* status) {
   using L = Vb<P1>;
   constexpr int NN = P1 * P1, P = P1 - 1;
@@ -137,7 +137,14 @@ __global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 1) k2_visc(Op2DDev o
   // and a 64-bit index per copy, 35% of the kernel's samples)
   {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int run = wid; run < L::EB * 5 * NCV; run += nw) {
+    // lanes per run: NN / 2 sixteen-byte copies (NN even) or NN eight-byte copies; short runs (low degrees)
+    // share a warp pass, GPW runs side by side
+    constexpr int CPR = NN % 2 == 0 ? NN / 2 : NN;           // copies per run
+    constexpr int GL = CPR < 32 ? CPR : 32;                  // lanes per run
+    constexpr int GPW = 32 / GL;                             // runs per warp pass
+    const int grp = lane / GL, gl = lane - grp * GL;
+    for (int run = wid * GPW + grp; run < L::EB * 5 * NCV; run += nw * GPW) {
+      if (grp >= GPW) break;
       const int el_ = run / (5 * NCV), r = run - el_ * (5 * NCV);
       const int k = r / NCV, c = r - k * NCV;
       const int eg_ = e0 + el_;
@@ -151,18 +158,18 @@ __global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 1) k2_visc(Op2DDev o
         if (k == 4) sy_ = ynb(op, ey, -1);
         const double* src = um + nidx(op, c, sy_, sx_, 0, 0);
         if constexpr (NN % 2 == 0) {   // 16-byte copies (element runs are 16-byte aligned when NN is even)
-          for (int t = 2 * lane; t < NN; t += 64) {
+          for (int t = 2 * gl; t < NN; t += 2 * GL) {
             const unsigned d = (unsigned)__cvta_generic_to_shared(dst + t);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + t) : "memory");
           }
         } else {
-          for (int t = lane; t < NN; t += 32) {
+          for (int t = gl; t < NN; t += GL) {
             const unsigned d = (unsigned)__cvta_generic_to_shared(dst + t);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + t) : "memory");
           }
         }
       } else {
-        for (int t = lane; t < NN; t += 32) dst[t] = 0.0;
+        for (int t = gl; t < NN; t += GL) dst[t] = 0.0;
       }
     }
   }
