@@ -19,6 +19,7 @@
 //
 // The implicit system is non-symmetric (C = (dt_m/2) A_c^2 + A_d is not
 // symmetric), so the CG of cg1d.cu does not apply.
+#include <string>
 #include <cooperative_groups.h>
 #include "sisdc_cns.cuh"
 #include "sisdc_host.h"
@@ -507,6 +508,10 @@ struct BicgArgs {
   int* log_it;
   double* log_margin;
   int log_cap;
+  // grid mode (levels beyond one cluster: K > 16 CTAs of a cooperative launch): the face-node halo
+  // and the reduction slots go through global memory, grid barriers replace the cluster barriers.
+  // Layout (doubles): halo [2 buf][K][2 sides][U0 U1 U2 Q0 Q1 Q2] | slots [2][K][BNV]
+  double* gws;
 };
 
 constexpr int BNV = 4;   // reduction width
@@ -517,8 +522,21 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
   constexpr int P = P1 - 1, NB = 3 * P1;
   const Op1DDev& op = A.op;
   cgx::cluster_group cl = cgx::this_cluster();
-  const int rank = (int)cl.block_rank();
+  cgx::grid_group grid = cgx::this_grid();
+  const bool GM = A.gws != nullptr;
+  const int rank = GM ? (int)blockIdx.x : (int)cl.block_rank();
   const int K = A.K, E = A.E, NL = E * P1;
+  double* const gH = A.gws;                         // [2][K][12]
+  double* const gS = A.gws + (size_t)2 * K * 12;    // [2][K][BNV]
+  unsigned nsum = 0;                                // reductions done (slot parity)
+  auto csync = [&]() {   // every CTA's shared data (cluster) / published halo and slots (grid) visible
+    if (GM) {
+      __threadfence();
+      grid.sync();
+    } else {
+      cl.sync();
+    }
+  };
   const int e0 = rank * E, e1 = min(op.ne, e0 + E);
   const int nl = (e1 - e0) * P1;
   const int L = threadIdx.x, el = L / P1, i = L - el * P1;
@@ -605,24 +623,43 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) Qb[c * NL + L] = (Cn[c * 3] * g[0] + Cn[c * 3 + 1] * g[1]) + Cn[c * 3 + 2] * g[2];
     }
-    cl.sync();   // U, Q of every CTA visible (DSMEM)
+    if (GM && own) {   // publish this CTA's two outer face nodes (its first node, its last node)
+      double* h = gH + ((size_t)buf * K + rank) * 12;
+      if (L == 0)
+        for (int c = 0; c < 3; ++c) { h[c] = Ub[c * NL]; h[3 + c] = Qb[c * NL]; }
+      if (L == nl - 1)
+        for (int c = 0; c < 3; ++c) { h[6 + c] = Ub[c * NL + L]; h[9 + c] = Qb[c * NL + L]; }
+    }
+    csync();   // U, Q of every CTA visible (DSMEM / the published face nodes)
     if (!own) { w[0] = w[1] = w[2] = 0.0; return; }
     // neighbour face node values: right (el+1, 0), left (el-1, P)
-    const double* UR;
-    const double* QR;
-    const double* UL;
-    const double* QL;
-    int oR, oL;
-    if (!last) { UR = Ub; QR = Qb; oR = (el + 1) * P1; }
-    else { UR = cl.map_shared_rank(Ub, rR); QR = cl.map_shared_rank(Qb, rR); oR = 0; }
-    if (!first) { UL = Ub; QL = Qb; oL = (el - 1) * P1 + P; }
-    else { UL = cl.map_shared_rank(Ub, rL); QL = cl.map_shared_rank(Qb, rL); oL = lastL * P1 + P; }
+    double nuR[3], nqR[3], nuL[3], nqL[3];
+    if (!last) {
+      for (int c = 0; c < 3; ++c) { nuR[c] = Ub[c * NL + (el + 1) * P1]; nqR[c] = Qb[c * NL + (el + 1) * P1]; }
+    } else if (GM) {
+      const double* h = gH + ((size_t)buf * K + rR) * 12;
+      for (int c = 0; c < 3; ++c) { nuR[c] = __ldcg(h + c); nqR[c] = __ldcg(h + 3 + c); }
+    } else {
+      const double* UR = cl.map_shared_rank(Ub, rR);
+      const double* QR = cl.map_shared_rank(Qb, rR);
+      for (int c = 0; c < 3; ++c) { nuR[c] = UR[c * NL]; nqR[c] = QR[c * NL]; }
+    }
+    if (!first) {
+      for (int c = 0; c < 3; ++c) { nuL[c] = Ub[c * NL + (el - 1) * P1 + P]; nqL[c] = Qb[c * NL + (el - 1) * P1 + P]; }
+    } else if (GM) {
+      const double* h = gH + ((size_t)buf * K + rL) * 12;
+      for (int c = 0; c < 3; ++c) { nuL[c] = __ldcg(h + 6 + c); nqL[c] = __ldcg(h + 9 + c); }
+    } else {
+      const double* UL = cl.map_shared_rank(Ub, rL);
+      const double* QL = cl.map_shared_rank(Qb, rL);
+      for (int c = 0; c < 3; ++c) { nuL[c] = UL[c * NL + lastL * P1 + P]; nqL[c] = QL[c * NL + lastL * P1 + P]; }
+    }
     const int ob = el * P1;
     double jr[3], jl[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {   // Dirichlet outer faces: outside value 0 in the linear operator
-      jr[c] = Ub[c * NL + ob + P] - (dR ? 0.0 : UR[c * NL + oR]);
-      jl[c] = (dL ? 0.0 : UL[c * NL + oL]) - Ub[c * NL + ob];
+      jr[c] = Ub[c * NL + ob + P] - (dR ? 0.0 : nuR[c]);
+      jl[c] = (dL ? 0.0 : nuL[c]) - Ub[c * NL + ob];
     }
     const double* Cmr = Cs + (ob + P) * 9;
     const double* Cpl = Cs + ob * 9;
@@ -635,13 +672,13 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
         double pen = 0.0;
         for (int b = 0; b < 3; ++b) pen += (0.5 * (Cmr[c * 3 + b] + (dR ? Cmr : CRr)[c * 3 + b])) * jr[b];
         const double qo = Qb[c * NL + ob + P];
-        B += mu0 * pen - 0.5 * (qo + (dR ? qo : QR[c * NL + oR]));
+        B += mu0 * pen - 0.5 * (qo + (dR ? qo : nqR[c]));
       }
       if (i == 0) {
         double pen = 0.0;
         for (int b = 0; b < 3; ++b) pen += (0.5 * ((dL ? Cpl : CLl)[c * 3 + b] + Cpl[c * 3 + b])) * jl[b];
         const double qo = Qb[c * NL + ob];
-        B -= mu0 * pen - 0.5 * ((dL ? qo : QL[c * NL + oL]) + qo);
+        B -= mu0 * pen - 0.5 * ((dL ? qo : nqL[c]) + qo);
       }
       const double lm = wR * ((Cmr[c * 3] * jr[0] + Cmr[c * 3 + 1] * jr[1]) + Cmr[c * 3 + 2] * jr[2]);
       const double lp = wL * ((Cpl[c * 3] * jl[0] + Cpl[c * 3 + 1] * jl[1]) + Cpl[c * 3 + 2] * jl[2]);
@@ -662,13 +699,20 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
       double t = 0.0;
       for (int q = 0; q < nw; ++q) t += wsum[q * BNV + threadIdx.x];
       slot[threadIdx.x] = t;
+      if (GM) gS[((size_t)(nsum & 1u) * K + rank) * BNV + threadIdx.x] = t;
     }
-    cl.sync();
+    csync();
     if (threadIdx.x < nv) {
       double t = 0.0;
-      for (int q = 0; q < K; ++q) t += cl.map_shared_rank(slot, q)[threadIdx.x];
+      if (GM) {
+        const double* gs = gS + (size_t)(nsum & 1u) * K * BNV + threadIdx.x;
+        for (int q = 0; q < K; ++q) t += __ldcg(gs + (size_t)q * BNV);
+      } else {
+        for (int q = 0; q < K; ++q) t += cl.map_shared_rank(slot, q)[threadIdx.x];
+      }
       bc[threadIdx.x] = t;
     }
+    ++nsum;
     __syncthreads();
     for (int j = 0; j < nv; ++j) v[j] = bc[j];
   };
@@ -686,7 +730,7 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
   if (red[1] == 0.0) {   // b == 0 -> zeros (dgsem.py:510-511)
     if (own)
       for (int c = 0; c < 3; ++c) A.x[c * op.n + gi] = 0.0;
-    cl.sync();   // no CTA leaves while a peer may still read its shared memory
+    if (!GM) cl.sync();   // no CTA leaves while a peer may still read its shared memory
     return;
   }
   const double thr = A.rtol2 * red[0];
@@ -736,7 +780,7 @@ __global__ void __launch_bounds__(256) kc_bicgstab(BicgArgs A) {
   }
   if (own)
     for (int c = 0; c < 3; ++c) A.x[c * op.n + gi] = xv[c];
-  cl.sync();   // no CTA leaves while a peer may still read its shared memory
+  if (!GM) cl.sync();   // no CTA leaves while a peer may still read its shared memory
   if (rank == 0 && threadIdx.x == 0) {
     const int idx = atomicAdd(&A.status[2], 1);
     if (idx < A.log_cap) {
@@ -764,6 +808,24 @@ int launch_bicg_t(Ctx* c, BicgArgs& A, int threads, size_t smem) {
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
+  if (A.gws != nullptr) {   // grid mode: cooperative launch, every block resident
+    int per_sm = 0, sms = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc_bicgstab<P1>, threads, smem);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    if (e != cudaSuccess) return c->cuda(e, "cns bicgstab occupancy");
+    if (A.K > per_sm * sms || A.K > CG1G_MAXK)
+      return c->fail(SISDC_ERR_UNSUPPORTED, "implicit_solve: 1-D CNS level too large for the grid-mode BiCGStab (" +
+                                                std::to_string(A.K) + " blocks of 256 nodes, " +
+                                                std::to_string(per_sm * sms) + " resident)");
+    cudaLaunchAttribute atc[1];
+    atc[0].id = cudaLaunchAttributeCooperative;
+    atc[0].val.cooperative = 1;
+    cfg.attrs = atc;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kc_bicgstab<P1>, A);
+    if (e != cudaSuccess) return c->cuda(e, "cns bicgstab grid-mode launch");
+    return c->after_launch("cns_bicgstab (grid mode)");
+  }
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = A.K;
@@ -824,7 +886,7 @@ int cns_solve(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs,
   // partition: one thread per node, <= 256 nodes per CTA, <= 16 CTAs
   int E = 256 / p1;
   int K = (op.ne + E - 1) / E;
-  if (K > 16) return c->fail(SISDC_ERR_UNSUPPORTED, "implicit_solve: 1-D CNS level larger than 16 CTAs x 256 nodes");
+  const bool grid_mode = K > 16;   // beyond one cluster: the same kernel as a cooperative launch
   E = (op.ne + K - 1) / K;
   K = (op.ne + E - 1) / E;
   if (int rc = cns_coef(c, op, k, c9)) return rc;
@@ -840,6 +902,7 @@ int cns_solve(Ctx* c, const Op1DDev& op, CoefDev k, double a, const double* rhs,
   A.op = op; A.C9 = c9; A.pinv = pinv; A.dbc = dbc; A.a = a; A.rhs = rhs; A.x = x;
   A.rtol2 = c->rtol * c->rtol; A.maxit = c->maxit; A.E = E; A.K = K;
   A.status = c->d_status; A.log_it = c->d_log_it; A.log_margin = c->d_log_margin; A.log_cap = c->log_cap;
+  A.gws = grid_mode ? c->d_cg1g : nullptr;
   switch (p1) {
     case 2: return launch_bicg_t<2>(c, A, threads, smem);
     case 3: return launch_bicg_t<3>(c, A, threads, smem);

@@ -277,3 +277,32 @@ def test_cns_multi_cta_cluster_solve(rt, bc):
 def AcousticState(w, ne, P, nodes):
     import dataclasses
     return dataclasses.replace(w, n_elem=ne, p_fine=P).initial_state(nodes)
+
+
+@pytest.mark.parametrize("ne,P", [(700, 7), (1100, 3)])
+def test_cns_grid_mode_beyond_one_cluster(rt, ne, P):
+    """Levels above 16 CTAs x 256 nodes (dgsem.py:503-533 solves any size): the cluster BiCGStab
+    as a cooperative launch (face-node halo and reduction slots through global memory, grid
+    barriers).  Same iteration count as the oracle's pinned BiCGStab, <= 1e-11 per field."""
+    from paper_2504_18526_b200 import dgsem, problems
+    w = CASES["cns_resolved"]
+    op = dgsem.DGOperator(dgsem.Mesh1D(w.x_left, w.x_right, ne, P),
+                          problems.CompressibleFlow(gamma=w.gamma, R_gas=w.R_gas, eta=1e-3, Pr=w.prandtl))
+    assert ne * (P + 1) > 16 * 256
+    log = []
+    orc = dg1d.Op1D(w.x_left, w.x_right, ne, P, dg1d.CNS1D(gamma=w.gamma, R_gas=w.R_gas, eta=1e-3, Pr=w.prandtl),
+                    cg_log=log)
+    x = np.asarray(op.mesh.nodes_x)
+    L = w.x_right - w.x_left
+    s = np.sin(2 * np.pi * (x - w.x_left) / L)
+    rho, v, p = 1.2 * (1.0 + 0.05 * s), 30.0 * s, 1.0e5 * (1.0 + 0.05 * s)
+    u = np.stack([rho, rho * v, p / (w.gamma - 1.0) + 0.5 * rho * v * v]).reshape(-1)
+    dt = 0.2 * (L / ne) / (P + 1) ** 2 / 350.0
+    rhs = u * (1.0 + 0.01 * np.cos(3 * 2 * np.pi * np.tile(x.reshape(-1), 3) / L))
+    n0 = rt.status()[2]
+    xg = op.implicit_solve(op.modified_diffusion_matrix(u, dt, "si2"), dt, rhs)
+    xo = orc.implicit_solve(orc.modified_coeff(u, dt), dt, rhs)
+    its = rt.cg_log()[0][n0:].tolist()
+    assert its == [log[-1][0]], (its, log[-1])
+    assert field_rel(xg, xo) < 1e-11
+    rt.raise_on_failure()
