@@ -1661,6 +1661,218 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_stage8(Op2DDev op, Stage2Arg
   }
 }
 
+// ------------------------------------------------------------------------
+// P = 7 (P1 = 8) NS2D physical viscous operator (visc2d.cu k2_visc semantics:
+// Stokes stress + Fourier heat flux as a tensor SIP, problems.py:221-237
+// generalised to 2-D, oracle/dg2d.py apply_viscous), one warp per element on the
+// fp64 tensor cores:
+//   * own-node gradients of the four fields as the 8 x 8 contractions U D^T and
+//     D U (mma.m8n8k4.f64, the lane's node pair in the accumulator fragment), one
+//     viscous-flux evaluation per node, fluxes to the warp's shared region;
+//   * faces: lane = face * 8 + k owns one face node.  The OWN side's flux is the one
+//     the node pass just stored; only the neighbour side is evaluated here (normal
+//     derivative: the D row dotted with the neighbour's line through the node;
+//     tangential derivative: D[k][.] dotted with the neighbour's face trace), then
+//     G_nn [u] of both sides.  The line-formulated kernel evaluated both sides of
+//     every face node from scratch (twice the gradient work of the node pass);
+//   * divergence: F^x DTW^T and DTW F^y on the tensor cores, face and adjoint-lift
+//     terms per node pair, 16-byte stores.
+// The warp runs a two-stage cp.async pipeline over its elements (the next
+// element and its four face neighbours land while this one is contracted).
+struct Vs8 {                 // per-warp shared region (doubles)
+  static constexpr int RP = 10, NP = 80, NC = 4;
+  static constexpr int OWN = 0;                       // [2 stages][NC][NP] own element (padded rows)
+  static constexpr int NBR = OWN + 2 * NC * NP;       // [2 stages][4 faces][NC][64] neighbour lines (swizzled)
+  static constexpr int FX = NBR + 2 * 4 * NC * 64;    // [NC][NP] viscous fluxes F^x, F^y at the own nodes
+  static constexpr int FY = FX + NC * NP;
+  static constexpr int GF = FY + NC * NP;             // [32 face nodes][NC] face fluxes
+  static constexpr int LF = GF + 32 * NC;             // [32 face nodes][NC] own-side G_nn [u] (adjoint lifts)
+  static constexpr int WARP = LF + 32 * NC;
+};
+constexpr int VS_WARPS = 4;
+
+__global__ void __launch_bounds__(VS_WARPS * 32, 2) k2_visc8(Op2DDev op, const double* __restrict__ u,
+                                                             double* __restrict__ fo, int m_first, int accumulate,
+                                                             int* status) {
+  extern __shared__ double sm[];
+  using W = Vs8;
+  constexpr int RP = 10, P = 7, NC = 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ws = sm + warp * W::WARP;
+  const int m = m_first + blockIdx.y;
+  const long long nn = op.nn;
+  const double* um = u + (size_t)m * op.ns;
+  double* fm = fo + (size_t)m * op.ns;
+  const double gpr = op.gamma / op.pr;
+  MmaLane K;
+  mma_lane_init(op, K);
+  const double rhx[2] = {1.0 / K.hwx[0], 1.0 / K.hwx[1]}, rhy = 1.0 / K.hwy;   // 1 / (h w / 2): the mass
+  const int g = lane >> 2, t = lane & 3, n0 = 2 * t, cc = n0;
+  const int f = lane >> 3, k = lane & 7;
+  const int axis = f < FT ? 0 : 1;
+  const bool own_minus = f == FR || f == FT;
+  const int ownf = f == FR ? k * RP + P : f == FL ? k * RP : f == FT ? P * RP + k : k;   // own face node (padded)
+  const int fpos = own_minus ? 0 : P;                   // the neighbour's face node on each of its lines
+  const int npos = nsw(k, fpos);
+  const int swz = g * 8 + 2 * ((lane & 3) ^ (g >> 1));
+  const int tr0 = nsw(lane & 7, lane >> 3), tr1 = nsw(lane & 7, 4 + (lane >> 3));
+  double dtan[8];   // D[k][.]: tangential derivative along the face at this lane's face node
+  {
+    const double* D = op.tab + TabOff::D(8);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dtan[q] = D[k * 8 + q];
+  }
+  const int ne = op.nex * op.ney;
+  const int stride = gridDim.x * VS_WARPS;
+  auto issue = [&](int e, int sb) {
+    const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
+    const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
+    const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
+    const unsigned eo = ((unsigned)ey * op.nex + ex) * 64u;
+    const unsigned nbR = ((unsigned)ey * op.nex + exr) * 64u, nbL = ((unsigned)ey * op.nex + exl) * 64u;
+    const unsigned nbT = ((unsigned)eyt * op.nex + ex) * 64u, nbB = ((unsigned)eyb * op.nex + ex) * 64u;
+    double* own = ws + W::OWN + sb * NC * W::NP;
+    double* nbr = ws + W::NBR + sb * 4 * NC * 64;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double* uc = um + c * nn;
+      cp_async16(own + c * W::NP + g * RP + cc, uc + eo + 2 * lane);
+      cp_async16(nbr + (FR * NC + c) * 64 + swz, uc + nbR + 2 * lane);
+      cp_async16(nbr + (FL * NC + c) * 64 + swz, uc + nbL + 2 * lane);
+      cp_async8(nbr + (FT * NC + c) * 64 + tr0, uc + nbT + lane);
+      cp_async8(nbr + (FT * NC + c) * 64 + tr1, uc + nbT + 32 + lane);
+      cp_async8(nbr + (FB * NC + c) * 64 + tr0, uc + nbB + lane);
+      cp_async8(nbr + (FB * NC + c) * 64 + tr1, uc + nbB + 32 + lane);
+    }
+  };
+  int e = blockIdx.x * VS_WARPS + warp;
+  if (e >= ne) return;
+  issue(e, 0);
+  cp_async_commit();
+  int sb = 0;
+  for (; e < ne; e += stride, sb ^= 1) {
+    if (e + stride < ne) issue(e + stride, sb ^ 1);
+    cp_async_commit();    // one group per element (possibly empty)
+    cp_async_wait_1();    // this element's group has landed
+    __syncwarp();
+    const double* own = ws + W::OWN + sb * NC * W::NP;
+    const double* nbr = ws + W::NBR + sb * 4 * NC * 64;
+    const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
+    const long long gi = (long long)(((unsigned)ey * op.nex + ex) * 64u) + g * 8 + n0;
+    // accumulate mode: this node pair's f values are fetched now, behind the contractions
+    double2 facc[NC];
+    if (accumulate) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) facc[c] = *reinterpret_cast<const double2*>(fm + c * nn + gi);
+    }
+    // ---- own nodes: gradients on the tensor cores, one flux evaluation per node
+    {
+      double gx[2][NC], gy[2][NC], s[2][NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double* Ue = own + c * W::NP;
+        double qx0 = 0.0, qx1 = 0.0, qy0 = 0.0, qy1 = 0.0;
+        dmma(qx0, qx1, Ue[g * RP + t], K.d0);
+        dmma(qx0, qx1, Ue[g * RP + 4 + t], K.d1);
+        dmma(qy0, qy1, K.d0, Ue[t * RP + g]);
+        dmma(qy0, qy1, K.d1, Ue[(4 + t) * RP + g]);
+        gx[0][c] = op.sx * qx0; gx[1][c] = op.sx * qx1;
+        gy[0][c] = op.sy * qy0; gy[1][c] = op.sy * qy1;
+        const double2 v = *reinterpret_cast<const double2*>(Ue + g * RP + n0);
+        s[0][c] = v.x; s[1][c] = v.y;
+      }
+      double Fx[2][NC], Fy[2][NC];
+      visc_flux(op, gpr, s[0], gx[0], gy[0], Fx[0], Fy[0]);
+      visc_flux(op, gpr, s[1], gx[1], gy[1], Fx[1], Fy[1]);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        *reinterpret_cast<double2*>(ws + W::FX + c * W::NP + g * RP + n0) = make_double2(Fx[0][c], Fx[1][c]);
+        *reinterpret_cast<double2*>(ws + W::FY + c * W::NP + g * RP + n0) = make_double2(Fy[0][c], Fy[1][c]);
+      }
+    }
+    __syncwarp();
+    // ---- faces: this lane's face node (face f, line k)
+    {
+      double so[NC], sn[NC], jmp[NC], gn[NC], gt[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double* ln = nbr + (f * NC + c) * 64 + k * 8;       // the neighbour's line through the node
+        double an = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {                              // nodes 2j, 2j + 1 of the line, in order
+          const double2 v = *reinterpret_cast<const double2*>(ln + 2 * (j ^ (k >> 1)));
+          an = fma(K.drow[2 * j], v.x, an);
+          an = fma(K.drow[2 * j + 1], v.y, an);
+        }
+        const double* fc = nbr + (f * NC + c) * 64;                // its face trace: node fpos of every line
+        double at = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) at = fma(dtan[q], fc[nsw(q, fpos)], at);
+        gn[c] = an;
+        gt[c] = at;
+        so[c] = own[c * W::NP + ownf];
+        sn[c] = fc[npos];
+        jmp[c] = own_minus ? so[c] - sn[c] : sn[c] - so[c];        // [u] = u- - u+
+      }
+      double gxn[NC], gyn[NC], Fxn[NC], Fyn[NC], g_nb[NC], g_own[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        gxn[c] = op.sx * (axis == 0 ? gn[c] : gt[c]);
+        gyn[c] = op.sy * (axis == 0 ? gt[c] : gn[c]);
+      }
+      visc_flux(op, gpr, sn, gxn, gyn, Fxn, Fyn);
+      apply_gnn(op, gpr, sn, jmp, axis, g_nb);
+      apply_gnn(op, gpr, so, jmp, axis, g_own);
+      const double mu0 = axis == 0 ? op.mux : op.muy;
+      const double* Fo = ws + (axis == 0 ? W::FX : W::FY);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double q_own = Fo[c * W::NP + ownf], q_nb = axis == 0 ? Fxn[c] : Fyn[c];
+        // minus side first, as the line-formulated kernel sums them
+        const double gsum = own_minus ? g_own[c] + g_nb[c] : g_nb[c] + g_own[c];
+        const double qsum = own_minus ? q_own + q_nb : q_nb + q_own;
+        ws[W::GF + lane * NC + c] = mu0 * (0.5 * gsum) - 0.5 * qsum;
+        ws[W::LF + lane * NC + c] = g_own[c];
+      }
+    }
+    __syncwarp();
+    // ---- divergence
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double* FX = ws + W::FX + c * W::NP;
+      const double* FY = ws + W::FY + c * W::NP;
+      double bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
+      dmma(bx0, bx1, FX[g * RP + t], K.w0);
+      dmma(bx0, bx1, FX[g * RP + 4 + t], K.w1);
+      dmma(by0, by1, K.w0, FY[t * RP + g]);
+      dmma(by0, by1, K.w1, FY[(4 + t) * RP + g]);
+      const double* GF = ws + W::GF + c;
+      const double* LF = ws + W::LF + c;
+      if (n0 + 1 == P) bx1 += GF[(FR * 8 + g) * NC];
+      if (n0 == 0) bx0 -= GF[(FL * 8 + g) * NC];
+      const double lr = op.sx * (0.5 * LF[(FR * 8 + g) * NC]), ll = op.sx * (0.5 * LF[(FL * 8 + g) * NC]);
+      bx0 -= lr * K.dPn[0];
+      bx1 -= lr * K.dPn[1];
+      bx0 -= ll * K.d0n[0];
+      bx1 -= ll * K.d0n[1];
+      if (g == P) { by0 += GF[(FT * 8 + n0) * NC]; by1 += GF[(FT * 8 + n0 + 1) * NC]; }
+      if (g == 0) { by0 -= GF[(FB * 8 + n0) * NC]; by1 -= GF[(FB * 8 + n0 + 1) * NC]; }
+      by0 -= (op.sy * (0.5 * LF[(FT * 8 + n0) * NC])) * K.dPg;
+      by1 -= (op.sy * (0.5 * LF[(FT * 8 + n0 + 1) * NC])) * K.dPg;
+      by0 -= (op.sy * (0.5 * LF[(FB * 8 + n0) * NC])) * K.d0g;
+      by1 -= (op.sy * (0.5 * LF[(FB * 8 + n0 + 1) * NC])) * K.d0g;
+      const double fv0 = -bx0 * rhx[0] + -by0 * rhy, fv1 = -bx1 * rhx[1] + -by1 * rhy;
+      const double o0 = accumulate ? facc[c].x + fv0 : fv0, o1 = accumulate ? facc[c].y + fv1 : fv1;
+      *reinterpret_cast<double2*>(fm + c * nn + gi) = make_double2(o0, o1);
+      bad |= !isfinite(o0) || !isfinite(o1);
+    }
+    if (bad && status) atomicMin(status, (int)(op.e0 + e));
+    __syncwarp();   // FX / FY / GF / LF and stage sb are rewritten by the next element
+  }
+  cp_async_wait_all();
+}
+
 template <int P1, int NC>
 __global__ void __launch_bounds__(256, 2) k2_cg(Cg2Args A) {
   extern __shared__ double sm[];
@@ -3131,6 +3343,30 @@ int launch2_sip(Ctx* c, const Op2DDev& op, CoefDev k, const double* u, double* o
   });
   return c->after_launch("k2_sip");
 }
+// P = 7 viscous operator on the tensor cores (called by launch2_visc, visc2d.cu); returns
+// SISDC_ERR_UNSUPPORTED-free: the caller checks the shape (p1 == 8, four fields, 16-byte alignment)
+int launch2_visc8(Ctx* c, const Op2DDev& op, const double* u, double* f, int m_first, int m_count, int accumulate) {
+  const size_t smem = sizeof(double) * VS_WARPS * Vs8::WARP;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(k2_visc8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_visc8, VS_WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int ne = op.nex * op.ney;
+  // a few elements per warp (the pipeline needs a next element to prefetch), grid a multiple of the
+  // resident block count
+  long long gx = (long long)per_sm * sms * 2 / m_count;
+  if (gx < per_sm * sms / 2) gx = per_sm * sms / 2;
+  const long long need = (ne + VS_WARPS - 1) / VS_WARPS;
+  if (gx > need) gx = need;
+  if (gx < 1) gx = 1;
+  k2_visc8<<<dim3((unsigned)gx, m_count), VS_WARPS * 32, smem, c->stream>>>(op, u, f, m_first, accumulate, c->d_status);
+  return c->after_launch("k2_visc8");
+}
+
 int launch2_coef(Ctx* c, const Op2DDev& op, CoefDev k, double* out) {
   SISDC_P1_SWITCH(op.p1, {
     k2_coef<P1><<<(unsigned)((op.nn + 255) / 256), 256, 0, c->stream>>>(op, k, out);

@@ -146,4 +146,46 @@ __device__ __forceinline__ void rusanov2d(const Op2DDev& op, const double* um, c
     if (c < op.nc) fh[c] = 0.5 * (fm[c] + fp[c]) - 0.5 * lam * (up[c] - um[c]);
 }
 
+// ------------------------------------------------- NS2D viscous physics
+// (shared by the line-formulated k2_visc of visc2d.cu and the warp-per-element
+// tensor-core kernel k2_visc8 of ops2d.cu)
+constexpr int NCV = 4;   // (rho, rho u, rho v, rho E)
+struct Prim {
+  double rho, vx, vy, Es, nu;
+};
+__device__ __forceinline__ Prim prim(const Op2DDev& op, const double* s) {
+  const double rho = s[0], ir = 1.0 / rho;   // one division per state (the oracle divides four times: <= 1 ulp apart)
+  return Prim{rho, s[1] * ir, s[2] * ir, s[3] * ir, op.nu * ir};
+}
+
+// viscous flux at a node from the state and its gradients (oracle NS2D.visc_flux)
+__device__ __forceinline__ void visc_flux(const Op2DDev& op, double gpr, const double* s, const double* gx,
+                                          const double* gy, double* Fx, double* Fy) {
+  const Prim q = prim(op, s);
+  const double k = q.nu * gpr;   // gpr = gamma / Pr
+  const double dxm = gx[1] - q.vx * gx[0], dym = gy[1] - q.vx * gy[0];
+  const double dxn = gx[2] - q.vy * gx[0], dyn = gy[2] - q.vy * gy[0];
+  const double txx = q.nu * ((4.0 / 3.0) * dxm - (2.0 / 3.0) * dyn);
+  const double tyy = q.nu * ((4.0 / 3.0) * dyn - (2.0 / 3.0) * dxm);
+  const double txy = q.nu * (dym + dxn);
+  const double ex = gx[3] - q.Es * gx[0] - q.vx * dxm - q.vy * dxn;
+  const double ey = gy[3] - q.Es * gy[0] - q.vx * dym - q.vy * dyn;
+  Fx[0] = 0.0; Fx[1] = txx; Fx[2] = txy; Fx[3] = q.vx * txx + q.vy * txy + k * ex;
+  Fy[0] = 0.0; Fy[1] = txy; Fy[2] = tyy; Fy[3] = q.vx * txy + q.vy * tyy + k * ey;
+}
+
+// G_nn(s) v (oracle NS2D.apply_gnn); axis 0: x-faces, 1: y-faces
+__device__ __forceinline__ void apply_gnn(const Op2DDev& op, double gpr, const double* s, const double* v, int axis,
+                                          double* r) {
+  const Prim q = prim(op, s);
+  const double k = q.nu * gpr;   // gpr = gamma / Pr
+  const double a = v[1] - q.vx * v[0], b = v[2] - q.vy * v[0];
+  const double r1 = q.nu * (axis == 0 ? (4.0 / 3.0) * a : a);
+  const double r2 = q.nu * (axis == 0 ? b : (4.0 / 3.0) * b);
+  r[0] = 0.0;
+  r[1] = r1;
+  r[2] = r2;
+  r[3] = q.vx * r1 + q.vy * r2 + k * (v[3] - q.Es * v[0] - q.vx * a - q.vy * b);
+}
+
 }  // namespace sisdc

@@ -17,13 +17,14 @@
 // spread over all threads; the neighbour's flux at the shared face nodes is
 // computed from the staged neighbour), then the divergence.  Not on the CG hot path: it runs once per right-hand-side
 // evaluation (node caches, FAS defects), after the convection/SI kernels.
+#include <cstdint>
+#include <cstdlib>
 #include "sisdc_dev2d.cuh"
 #include "sisdc_host.h"
 
 namespace sisdc {
 namespace {
 
-constexpr int NCV = 4;   // (rho, rho u, rho v, rho E)
 enum { FR = 0, FL = 1, FT = 2, FB = 3 };   // right, left, top, bottom faces
 
 template <int P1>
@@ -40,44 +41,6 @@ struct Vb {
   static constexpr int SIZE = XS + EB * 4 * P1 * 2 * NCV;
   static constexpr int DP = P1 + 1;                         // padded table rows (lane-varying row index: conflict free)
 };
-
-struct Prim {
-  double rho, vx, vy, Es, nu;
-};
-__device__ __forceinline__ Prim prim(const Op2DDev& op, const double* s) {
-  const double rho = s[0], ir = 1.0 / rho;   // one division per state (the oracle divides four times: <= 1 ulp apart)
-  return Prim{rho, s[1] * ir, s[2] * ir, s[3] * ir, op.nu * ir};
-}
-
-// viscous flux at a node from the state and its gradients (oracle NS2D.visc_flux)
-__device__ __forceinline__ void visc_flux(const Op2DDev& op, double gpr, const double* s, const double* gx,
-                                          const double* gy, double* Fx, double* Fy) {
-  const Prim q = prim(op, s);
-  const double k = q.nu * gpr;   // gpr = gamma / Pr
-  const double dxm = gx[1] - q.vx * gx[0], dym = gy[1] - q.vx * gy[0];
-  const double dxn = gx[2] - q.vy * gx[0], dyn = gy[2] - q.vy * gy[0];
-  const double txx = q.nu * ((4.0 / 3.0) * dxm - (2.0 / 3.0) * dyn);
-  const double tyy = q.nu * ((4.0 / 3.0) * dyn - (2.0 / 3.0) * dxm);
-  const double txy = q.nu * (dym + dxn);
-  const double ex = gx[3] - q.Es * gx[0] - q.vx * dxm - q.vy * dxn;
-  const double ey = gy[3] - q.Es * gy[0] - q.vx * dym - q.vy * dyn;
-  Fx[0] = 0.0; Fx[1] = txx; Fx[2] = txy; Fx[3] = q.vx * txx + q.vy * txy + k * ex;
-  Fy[0] = 0.0; Fy[1] = txy; Fy[2] = tyy; Fy[3] = q.vx * txy + q.vy * tyy + k * ey;
-}
-
-// G_nn(s) v (oracle NS2D.apply_gnn); axis 0: x-faces, 1: y-faces
-__device__ __forceinline__ void apply_gnn(const Op2DDev& op, double gpr, const double* s, const double* v, int axis,
-                                          double* r) {
-  const Prim q = prim(op, s);
-  const double k = q.nu * gpr;   // gpr = gamma / Pr
-  const double a = v[1] - q.vx * v[0], b = v[2] - q.vy * v[0];
-  const double r1 = q.nu * (axis == 0 ? (4.0 / 3.0) * a : a);
-  const double r2 = q.nu * (axis == 0 ? b : (4.0 / 3.0) * b);
-  r[0] = 0.0;
-  r[1] = r1;
-  r[2] = r2;
-  r[3] = q.vx * r1 + q.vy * r2 + k * (v[3] - q.Es * v[0] - q.vx * a - q.vy * b);
-}
 
 // gradients (all fields) at node (j, i) of a staged element X = [NCV][NN]
 template <int P1>
@@ -283,6 +246,11 @@ __global__ void __launch_bounds__(Vb<P1>::NT, P1 == 8 ? 3 : 2) k2_visc(Op2DDev o
 int launch2_visc(Ctx* c, const Op2DDev& op, const double* u, double* f, int m_first, int m_count, int accumulate) {
   if (op.problem != SISDC_NS2D) return SISDC_OK;
   if (op.nc != 4) return c->fail(SISDC_ERR_ARG, "NS2D needs four fields");
+  // P = 7: warp-per-element tensor-core kernel (ops2d.cu); SISDC_VISC_LINE=1 keeps the line formulation (A/B)
+  static const bool line_only = [] { const char* v = getenv("SISDC_VISC_LINE"); return v && v[0] == '1'; }();
+  if (op.p1 == 8 && !line_only && ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(f)) & 15) == 0 &&
+      (op.ns & 1) == 0)
+    return launch2_visc8(c, op, u, f, m_first, m_count, accumulate);
 #define SISDC_VISC(P1_)                                                                                       \
   case P1_: {                                                                                                 \
     using L = Vb<P1_>;                                                                                        \
