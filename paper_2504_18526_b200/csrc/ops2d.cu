@@ -1579,13 +1579,18 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
 template <int NC>
 struct Stg {                 // per-warp shared region (doubles)
   static constexpr int RP = 10, NP = 80;
-  static constexpr int OWN = 0;                  // [NC][NP] conv_in element
-  static constexpr int FX = OWN + NC * NP, FY = FX + NC * NP;   // fluxes of all fields [NC][NP]
+  static constexpr int OWN = 0;                  // [2 stages][NC][NP] conv_in element
+  static constexpr int FX = OWN + 2 * NC * NP, FY = FX + NC * NP;   // fluxes of all fields [NC][NP]
   static constexpr int FH = FY + NC * NP;        // [32][NC] face fluxes
   static constexpr int WARP = FH + 32 * NC;
 };
-template <int NC>
-__global__ void __launch_bounds__(EV_WARPS * 32) k2_stage8(Op2DDev op, Stage2Args a) {
+// MQ: the number of quadrature nodes when it is a compile-time count (the streamed operands of a field --
+// f_old of every node, g, base, h -- are then all requested BEFORE the field's tensor-core contractions
+// and consumed after them; with the loads behind the contractions 60% of the kernel's samples waited on
+// them, ncu r02w); MQ = 0: runtime count, loads in the quadrature loop.  The own element and the
+// neighbours' face nodes of the NEXT element are requested one element ahead (two-stage cp.async).
+template <int NC, int MQ>
+__global__ void __launch_bounds__(EV_WARPS * 32, 3) k2_stage8(Op2DDev op, Stage2Args a) {
   extern __shared__ double sm[];
   using W = Stg<NC>;
   constexpr int RP = 10, P = 7;
@@ -1600,7 +1605,9 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_stage8(Op2DDev op, Stage2Arg
   const int fnode = f == FR ? k * 8 : f == FL ? k * 8 + 7 : f == FT ? k : 56 + k;      // neighbour's face node
   const int ownf = f == FR ? k * RP + P : f == FL ? k * RP : f == FT ? P * RP + k : k;   // own face node (padded)
   const int ne = op.nex * op.ney;
-  for (int e = blockIdx.x * EV_WARPS + warp; e < ne; e += gridDim.x * EV_WARPS) {
+  const int stride = gridDim.x * EV_WARPS;
+  // request element e: own nodes into stage sb, the neighbours' face-node states into sn
+  auto issue = [&](int e, int sb, double (&sn)[NC_MAX]) {
     const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
     const int exr = ex + 1 == op.nex ? 0 : ex + 1, exl = ex == 0 ? op.nex - 1 : ex - 1;
     const int eyt = ynb(op, ey, 1), eyb = ynb(op, ey, -1);
@@ -1608,16 +1615,31 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_stage8(Op2DDev op, Stage2Arg
     const unsigned nbf = (f == FR ? ((unsigned)ey * op.nex + exr) : f == FL ? ((unsigned)ey * op.nex + exl)
                           : f == FT ? ((unsigned)eyt * op.nex + ex) : ((unsigned)eyb * op.nex + ex)) * 64u + fnode;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) cp_async16(ws + W::OWN + c * W::NP + g * RP + n0, a.conv_in + c * nn + eo + 2 * lane);
-    double sn[NC_MAX];
+    for (int c = 0; c < NC; ++c)
+      cp_async16(ws + W::OWN + (sb * NC + c) * W::NP + g * RP + n0, a.conv_in + c * nn + eo + 2 * lane);
 #pragma unroll
     for (int c = 0; c < NC_MAX; ++c) sn[c] = c < NC ? a.conv_in[c * nn + nbf] : 1.0;
-    cp_async_wait_all();
+  };
+  int e = blockIdx.x * EV_WARPS + warp;
+  if (e >= ne) return;
+  double sn[NC_MAX], snn[NC_MAX];
+  issue(e, 0, sn);
+  cp_async_commit();
+  int sb = 0;
+  for (; e < ne; e += stride, sb ^= 1) {
+#pragma unroll
+    for (int c = 0; c < NC_MAX; ++c) snn[c] = 1.0;
+    if (e + stride < ne) issue(e + stride, sb ^ 1, snn);
+    cp_async_commit();
+    cp_async_wait_1();
     __syncwarp();
+    const double* own = ws + W::OWN + sb * NC * W::NP;
+    const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
+    const unsigned eo = ((unsigned)ey * op.nex + ex) * 64u;
     {
       double so[NC_MAX], fh[NC_MAX];
 #pragma unroll
-      for (int c = 0; c < NC_MAX; ++c) so[c] = c < NC ? ws[W::OWN + c * W::NP + ownf] : 1.0;
+      for (int c = 0; c < NC_MAX; ++c) so[c] = c < NC ? own[c * W::NP + ownf] : 1.0;
       const int axis = f < FT ? 0 : 1;
       if (f == FR || f == FT) rusanov2d(op, so, sn, axis, fh); else rusanov2d(op, sn, so, axis, fh);
 #pragma unroll
@@ -1625,40 +1647,60 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_stage8(Op2DDev op, Stage2Arg
     }
     __syncwarp();
     const long long gi = (long long)eo + g * 8 + n0;
-    wpe_flux_all<NC>(op, ws + W::OWN, ws + W::FX, ws + W::FY);
+    wpe_flux_all<NC>(op, own, ws + W::FX, ws + W::FY);
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
+      const long long gc = c * nn + gi;
+      // streamed operands of this field, requested ahead of the contractions
+      double2 fo[MQ > 0 ? MQ : 1];
+      double2 gv = make_double2(0.0, 0.0), hv = make_double2(0.0, 0.0);
+      if constexpr (MQ > 0) {
+        if (a.f_old) {
+#pragma unroll
+          for (int jj = 0; jj < MQ; ++jj) fo[jj] = __ldcs(reinterpret_cast<const double2*>(a.f_old + (size_t)jj * op.ns + gc));
+        }
+      }
+      if (a.g) gv = __ldcs(reinterpret_cast<const double2*>(a.g + gc));
+      const double2 bv = __ldcs(reinterpret_cast<const double2*>(a.base + gc));
+      if (a.h) hv = __ldcs(reinterpret_cast<const double2*>(a.h + gc));
       double cv0, cv1;
       wpe_conv<NC>(K, ws + W::FH, c, ws + W::FX + c * W::NP, ws + W::FY + c * W::NP, rcx, rcy, cv0, cv1);
-      const long long gc = c * nn + gi;
       if (a.conv_out) *reinterpret_cast<double2*>(a.conv_out + gc) = make_double2(cv0, cv1);
       double q0 = 0.0, q1 = 0.0;
       if (a.f_old) {
         double acc0 = 0.0, acc1 = 0.0;
-        for (int jj = 0; jj < a.M; ++jj) {
-          const double2 fo = *reinterpret_cast<const double2*>(a.f_old + (size_t)jj * op.ns + gc);
-          acc0 = fma(a.w[jj], fo.x, acc0);
-          acc1 = fma(a.w[jj], fo.y, acc1);
+        if constexpr (MQ > 0) {
+#pragma unroll
+          for (int jj = 0; jj < MQ; ++jj) {
+            acc0 = fma(a.w[jj], fo[jj].x, acc0);
+            acc1 = fma(a.w[jj], fo[jj].y, acc1);
+          }
+        } else {
+          for (int jj = 0; jj < a.M; ++jj) {
+            const double2 fv = *reinterpret_cast<const double2*>(a.f_old + (size_t)jj * op.ns + gc);
+            acc0 = fma(a.w[jj], fv.x, acc0);
+            acc1 = fma(a.w[jj], fv.y, acc1);
+          }
         }
         q0 = a.dt * acc0;
         q1 = a.dt * acc1;
       }
       if (a.g) {
-        const double2 gv = *reinterpret_cast<const double2*>(a.g + gc);
         q0 = q0 + gv.x;
         q1 = q1 + gv.y;
       }
-      const double2 bv = *reinterpret_cast<const double2*>(a.base + gc);
       double r0 = (bv.x + q0) + a.dt_m * cv0, r1 = (bv.y + q1) + a.dt_m * cv1;
       if (a.h) {
-        const double2 hv = *reinterpret_cast<const double2*>(a.h + gc);
         r0 = r0 - hv.x;
         r1 = r1 - hv.y;
       }
       *reinterpret_cast<double2*>(a.rhs + gc) = make_double2(r0, r1);
     }
-    __syncwarp();   // the next element overwrites the staged data
+#pragma unroll
+    for (int c = 0; c < NC_MAX; ++c) sn[c] = snn[c];
+    __syncwarp();   // FX / FY / FH and stage sb are rewritten by the next element
   }
+  cp_async_wait_all();
 }
 
 // ------------------------------------------------------------------------
@@ -3421,13 +3463,23 @@ int launch2_stage(Ctx* c, const Op2DDev& op, const double* base, const double* c
   if (op.p1 == 8 && op.nc == 4 && al16) {   // tensor-core warp-per-element path
     const size_t smem = sizeof(double) * EV_WARPS * Stg<4>::WARP;
     const int ne = op.nex * op.ney;
-    int nb = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2_stage8<4>, EV_WARPS * 32, smem);
+    int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    long long gx = (long long)(nb > 0 ? nb : 1) * sms * 4;
-    const long long need = (ne + EV_WARPS - 1) / EV_WARPS;
-    if (gx > need) gx = need;
-    k2_stage8<4><<<(unsigned)gx, EV_WARPS * 32, smem, c->stream>>>(op, a);
+    auto go = [&](auto kern) {
+      int nb = 0;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, EV_WARPS * 32, smem);
+      long long gx = (long long)(nb > 0 ? nb : 1) * sms * 4;
+      const long long need = (ne + EV_WARPS - 1) / EV_WARPS;
+      if (gx > need) gx = need;
+      kern<<<(unsigned)gx, EV_WARPS * 32, smem, c->stream>>>(op, a);
+    };
+    // the quadrature length as a compile-time count where it is one of the schedules' node counts
+    const int mq = f_old ? M : 0;
+    if (mq == 5) go(k2_stage8<4, 5>);
+    else if (mq == 4) go(k2_stage8<4, 4>);
+    else if (mq == 3) go(k2_stage8<4, 3>);
+    else go(k2_stage8<4, 0>);
     return c->after_launch("k2_stage8");
   }
   SISDC_P1_SWITCH(op.p1, {
