@@ -11,6 +11,7 @@ struct sisdc_ctx {
 };
 
 struct sisdc_comm;   // NCCL communicator (part2d.cu)
+constexpr int HALO_MAXVEC = 17;   // node vectors of one packed halo exchange (M + 1 <= 17)
 
 // one element-row partition of a 2-D operator (ghost-row storage)
 struct Part2D {
@@ -43,6 +44,12 @@ struct sisdc_op1d {   // dimension-tagged operator handle (1-D or 2-D)
   sisdc::CgPScal* d_sc = nullptr;
   int* h_done = nullptr;             // pinned [2]
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  // halo / interior overlap of the fused split iteration: the halo and the two ghost-row bands run on
+  // halo_stream while the interior bands run on the operator's stream (fork / join by events)
+  cudaStream_t halo_stream = nullptr;
+  double* d_hsend = nullptr;         // packed NCCL halo: [2 sides][HALO_MAXVEC][nc][row] send / receive buffers
+  double* d_hrecv = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool parted() const { return !parts.empty(); }
   long long n() const { return dim == 1 ? (long long)dev.n * dev.nc : (parted() ? n_total : dev2.n); }
   bool cns() const { return dim == 1 && dev.problem == SISDC_CNS1D; }

@@ -592,6 +592,8 @@ struct Cg2Args {
   double* S2;
   double* W2;
   int mode;
+  int bsel;            // single-pass mode on a partition: 0 every band, 1 interior bands (no ghost row
+                       // touched: runs while the halo is in flight), 2 the first and last band
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -1364,7 +1366,8 @@ struct Ev {                 // per-warp shared region (doubles)
   static constexpr int QX = CFP + 32, QY = QX + NP, DOT = QY + NP, FCON = DOT + 32;
   static constexpr int FX = FCON + 64, FY = FX + NC * NP;     // fluxes of all fields [NC][NP]
   static constexpr int FHM = FY + NC * NP, FHP = FHM + 32 * NC;   // Rusanov fluxes [lane][NC]
-  static constexpr int WARP = FHP + 32 * NC;
+  static constexpr int CPV = FHP + 32 * NC;         // [NC][NP] cached conv(u_{m-1}) (a.conv_prev), staged with the element
+  static constexpr int WARP = CPV + NC * NP;
 };
 constexpr int EV_WARPS = 4;
 
@@ -1468,6 +1471,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
       cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr0, uc + nb[FB] + lane);
       cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr1, uc + nb[FB] + 32 + lane);
       if (need_si || conv_up) cp_async16(ws + W::UPO + c * W::NP + r * RP + cc, up + c * nn + eo + 2 * lane);
+      // the cached conv(u_{m-1}) rides with the staging (read in the field loop it stalled 19% of the samples)
+      if (need_h && a.conv_prev) cp_async16(ws + W::CPV + c * W::NP + r * RP + cc, a.conv_prev + c * nn + eo + 2 * lane);
     }
     double upf[NC_MAX];   // u_{m-1} at this lane's neighbour face node
     const unsigned nbf = (f == FR ? nb[FR] : f == FL ? nb[FL] : f == FT ? nb[FT] : nb[FB]) + fnode;
@@ -1552,7 +1557,7 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
       }
       if (a.h2) *reinterpret_cast<double2*>(a.h2 + go) = make_double2(dtm * (cm0 + ds0), dtm * (cm1 + ds1));
       if (a.conv_prev) {
-        const double2 v = *reinterpret_cast<const double2*>(a.conv_prev + c * nn + gi);
+        const double2 v = *reinterpret_cast<const double2*>(ws + W::CPV + c * W::NP + g * RP + n0);
         *reinterpret_cast<double2*>(a.h1 + go) = make_double2(dtm * (v.x + ds0), dtm * (v.y + ds1));
       }
     }
@@ -2596,7 +2601,9 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
   const int ta = (g & 1) ? sw8(n0 + 1, g) : sw8(n0, g), tb = (g & 1) ? sw8(n0, g) : sw8(n0 + 1, g);
   const int nexT = op.nex / SUB, neyT = op.ney / SUB;   // tiles per row / tile rows (SUB = 2: even sizes only)
   const int nstr = (nexT + SL - 1) / SL, nbands = (neyT + NW - 1) / NW;
-  const long long nunits = (long long)nbands * nstr * NC;
+  // bands of this launch (A.bsel, single-pass mode): all; the interior ones; the two that read ghost rows
+  const int nbsel = A.bsel == 0 ? nbands : A.bsel == 1 ? nbands - 2 : 2;
+  const long long nunits = (long long)nbsel * nstr * NC;
   unsigned oc = 0, hc = 0;   // completed uses of this warp's own stages / of the halo stages (stage = use & 1)
   unsigned ac = 0;           // this warp's arrivals on the column barrier (= steps done)
   int st = 0;                // RT slot of column j (slots advance with j, four of them)
@@ -2625,7 +2632,8 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       const long long tq = un / NC;
       // bands fastest: the blocks in flight work on vertically adjacent bands of one strip column, so the
       // rows bordering a band (rebuilt from their raw r, s, w) are L2 hits, not a second DRAM read
-      const int band = (int)(tq % nbands), sx = (int)(tq / nbands);
+      const int bq = (int)(tq % nbsel), sx = (int)(tq / nbsel);
+      const int band = A.bsel == 0 ? bq : A.bsel == 1 ? bq + 1 : (bq == 0 ? 0 : nbands - 1);
       const int y0 = band * NW, nrows = neyT - y0 < NW ? neyT - y0 : NW;
       const bool valid = warp < nrows;
       const int ey = (valid ? y0 + warp : y0) + op.row0;   // (storage) tile row; a partition's ghost rows: ynb
@@ -3269,6 +3277,33 @@ __global__ void k2p_halo(HaloPArgs H) {
     d[t] = s[t];
 }
 
+// NCCL halo of one partition, packed: the boundary rows of all (vector, field) pairs go through ONE
+// contiguous buffer per side (2 sends + 2 receives per exchange instead of 4 per pair -- 48 NCCL calls
+// per fused CG iteration before, the host cost that starved the GPU on the short coarse iterations).
+// dir 0: buf[side][m][c][row] <- first (side 0) / last (side 1) owned row; dir 1: top ghost row
+// (ney + 1) <- buf[0], bottom ghost row (0) <- buf[1].
+struct HaloPackArgs {
+  int nc, nex, nnod, mcount, ney, dir;
+  long long mstride, nn;
+  double* vec;
+  double* buf;
+};
+__global__ void k2p_halo_pack(HaloPackArgs H) {
+  const long long row = (long long)H.nex * H.nnod;
+  const int y = blockIdx.y, side = y & 1, c = y >> 1, m = blockIdx.z;
+  double* b = H.buf + ((long long)(side * H.mcount + m) * H.nc + c) * row;
+  double* v = H.vec + m * H.mstride + c * H.nn;
+  if (H.dir == 0) {
+    const double* s = v + (side == 0 ? row : (long long)H.ney * row);
+    for (long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; t < row; t += (long long)gridDim.x * blockDim.x * 2)
+      *reinterpret_cast<double2*>(b + t) = *reinterpret_cast<const double2*>(s + t);
+  } else {
+    double* d = v + (side == 0 ? (long long)(H.ney + 1) * row : 0);
+    for (long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; t < row; t += (long long)gridDim.x * blockDim.x * 2)
+      *reinterpret_cast<double2*>(d + t) = *reinterpret_cast<const double2*>(b + t);
+  }
+}
+
 // constant-bank copy of the reference-element matrices for one P1 (idempotent:
 // they depend on P1 only); called at operator creation, outside any capture
 int set_cg2_tables(Ctx* c, int p1, const double* tab) {
@@ -3730,23 +3765,29 @@ int launch2p_phase(Ctx* c, int phase, const Op2DDev& op, CoefDev k, double a, co
   return SISDC_OK;
 }
 
-// one fused iteration pass on a partition (k2_cgf in single-pass mode); par: parity of the (r, s, w) read
+// one fused iteration pass on a partition (k2_cgf in single-pass mode); par: parity of the (r, s, w) read.
+// bsel / slot0 / nblk: the bands of this launch (Cg2Args::bsel), its first block-partial slot and its grid
+// (the interior and the edge launch of one iteration share the partition's G slots: slot0 + nblk <= G)
 int launch2p_fpass(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int G,
-                   const CgPScal* sc, int par) {
+                   const CgPScal* sc, int par, int bsel, int slot0, int nblk) {
   Cg2Args A = cg2p_args(op, k, a, rhs, x, ws, G, sc, -1);
   A.px = par;
   A.maxit = c->maxit;
+  A.bsel = bsel;
+  if (nblk < 0) nblk = G;
+  A.part += 4 * slot0;
+  A.part2 += 4 * slot0;
   cudaError_t e = cudaSuccess;
   if (op.nc == 4) {
     using F = Fz<4>;
     constexpr int smem = (int)(sizeof(double) * F::SIZE);
     cudaFuncSetAttribute(k2_cgf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k2_cgf<4><<<G, F::NW * 32, smem, c->stream>>>(A);
+    k2_cgf<4><<<nblk, F::NW * 32, smem, c->stream>>>(A);
   } else if (op.nc == 1) {
     using F = Fz<1>;
     constexpr int smem = (int)(sizeof(double) * F::SIZE);
     cudaFuncSetAttribute(k2_cgf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k2_cgf<1><<<G, F::NW * 32, smem, c->stream>>>(A);
+    k2_cgf<1><<<nblk, F::NW * 32, smem, c->stream>>>(A);
   } else {
     return c->fail(SISDC_ERR_UNSUPPORTED, "fused 2-D pass: 1 or 4 fields");
   }
@@ -3755,6 +3796,8 @@ int launch2p_fpass(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double*
   if (e != cudaSuccess) return c->cuda(e, "k2_cgf single-pass launch");
   return SISDC_OK;
 }
+// bands of the fused pass on a partition (8 element rows each)
+int cg2p_bands(const Op2DDev& op) { return (op.ney + Fz<4>::NW - 1) / Fz<4>::NW; }
 
 int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out) {
   if (nparts < 1 || nparts > MAXPART) return c->fail(SISDC_ERR_ARG, "partition count");
@@ -3791,6 +3834,17 @@ int launch2p_halo(Ctx* c, int nparts, const Op2DDev* ops, double* const* base, i
   const unsigned gx = (unsigned)((row + 255) / 256 < 64 ? (row + 255) / 256 : 64);
   k2p_halo<<<dim3(gx, 2 * nc * nparts, mcount), 256, 0, c->stream>>>(H);
   return c->after_launch("k2p_halo");
+}
+
+int launch2p_halo_pack(Ctx* c, const Op2DDev& op, double* vec, double* buf, int nc, int mcount, long long mstride,
+                       int dir) {
+  HaloPackArgs H{};
+  H.nc = nc; H.nex = op.nex; H.nnod = op.p1 * op.p1; H.mcount = mcount; H.ney = op.ney; H.dir = dir;
+  H.mstride = mstride; H.nn = op.nn; H.vec = vec; H.buf = buf;
+  const long long row = (long long)H.nex * H.nnod;   // even (nnod = p1^2 rows of a 16-byte aligned field: checked by the caller)
+  const unsigned gx = (unsigned)((row / 2 + 255) / 256 < 64 ? (row / 2 + 255) / 256 : 64);
+  k2p_halo_pack<<<dim3(gx, 2 * nc, mcount), 256, 0, c->stream>>>(H);
+  return c->after_launch("k2p_halo_pack");
 }
 
 // blocks of the split-solve kernels: resident blocks of the matvec x SMs,

@@ -112,6 +112,26 @@ int halo(sisdc_op1d* op, const double* vec_c, int mcount, long long mstride, boo
   const int R = op->comm->nranks, q = op->comm->rank;
   const int prev = (q + R - 1) % R, next = (q + 1) % R;
   const size_t row = (size_t)P.dev.nex * P.dev.p1 * P.dev.p1;
+  // packed exchange (one contiguous buffer per side: 2 sends + 2 receives) when the rows can be moved
+  // with 16-byte copies; per-(vector, field) messages otherwise
+  const bool packed = op->d_hsend && mcount <= HALO_MAXVEC && (row & 1) == 0 && (P.dev.nn & 1) == 0 &&
+                      (mstride & 1) == 0 && (reinterpret_cast<uintptr_t>(vec) & 15) == 0;
+  if (packed) {
+    const size_t cnt = (size_t)mcount * nc * row;   // one side
+    if (int rc = launch2p_halo_pack(c, P.dev, vec, op->d_hsend, nc, mcount, mstride, 0)) return rc;
+    // first owned rows -> prev (its top ghost rows), last owned rows -> next (its bottom ghost rows); the
+    // k-th send to a peer pairs with its k-th receive from us (1 rank: self; 2 ranks: prev == next)
+    ncclResult_t r = api->groupStart();
+    if (r == ncclSuccess) r = api->send(op->d_hsend, cnt, ncclDouble, prev, op->comm->comm, c->stream);
+    if (r == ncclSuccess) r = api->send(op->d_hsend + cnt, cnt, ncclDouble, next, op->comm->comm, c->stream);
+    if (r == ncclSuccess) r = api->recv(op->d_hrecv, cnt, ncclDouble, next, op->comm->comm, c->stream);
+    if (r == ncclSuccess) r = api->recv(op->d_hrecv + cnt, cnt, ncclDouble, prev, op->comm->comm, c->stream);
+    const ncclResult_t r2 = api->groupEnd();
+    if (r != ncclSuccess) return nccl_fail(c, r, "halo send/recv");
+    if (r2 != ncclSuccess) return nccl_fail(c, r2, "halo group");
+    ++c->launches;
+    return launch2p_halo_pack(c, P.dev, vec, op->d_hrecv, nc, mcount, mstride, 1);
+  }
   ncclResult_t r = api->groupStart();
   for (int m = 0; m < mcount && r == ncclSuccess; ++m)
     for (int f = 0; f < nc && r == ncclSuccess; ++f) {
@@ -272,15 +292,69 @@ int halo_ws(sisdc_op1d* op, bool dinv, int par) {
 }
 
 // fused iteration j (P = 7): the (r, s, w) of parity j & 1 get their ghost rows, then ONE pass per
-// partition does update + matvec (k2_cgf single-pass mode) and writes parity (j + 1) & 1
+// partition does update + matvec (k2_cgf single-pass mode) and writes parity (j + 1) & 1.
+// Overlap (partitions of >= 3 bands driven through a communicator; SISDC_PART_OVERLAP, below): only the first and the last band
+// of a partition read ghost rows, so the halo exchange and those two bands run on the operator's second
+// stream while the interior bands run on the main stream; the two launches split the partition's G
+// blocks (and block-partial slots) in proportion to their work and are co-resident.  Fork after the
+// previous iteration's scalar kernel, join before the reduction.
+struct StreamSwap {   // launch on another stream for a scope (Ctx is single-threaded)
+  Ctx* c;
+  cudaStream_t saved;
+  StreamSwap(Ctx* c_, cudaStream_t s) : c(c_), saved(c_->stream) { c->stream = s; }
+  ~StreamSwap() { c->stream = saved; }
+};
+
+// SISDC_PART_OVERLAP: 1 always, 0 never; unset: only with a communicator of more than one rank.  On ONE
+// GPU there is no transfer to hide and the two co-resident launches cost ~8% (cfg4 fine solve 8.07 ->
+// 8.74 ms, in-process partition; 442 -> 494 ms per eager cfg4 step through one NCCL rank), so single-GPU
+// runs keep the single launch unless asked.
+int overlap_mode() {
+  const char* v = getenv("SISDC_PART_OVERLAP");   // read per solve: tests toggle it
+  return !v ? -1 : v[0] == '0' ? 0 : 1;
+}
+
 int iterate_fused(sisdc_op1d* op, int j, const CoefDev& k, double a, const double* rhs, double* x) {
+  Ctx* c = C(op);
   const int par = j & 1;
-  if (int rc = halo_ws(op, false, par)) return rc;
-  for (const Part2D& P : op->parts)
-    if (int rc = launch2p_fpass(C(op), P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc, par))
-      return rc;
+  const int om = overlap_mode();
+  bool split = (om == 1 || (om < 0 && op->comm != nullptr && op->nranks > 1)) && op->halo_stream != nullptr;
+  for (const Part2D& P : op->parts) split = split && cg2p_bands(P.dev) >= 3 && P.G >= 8;
+  if (!split) {
+    if (int rc = halo_ws(op, false, par)) return rc;
+    for (const Part2D& P : op->parts)
+      if (int rc = launch2p_fpass(c, P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc, par))
+        return rc;
+  } else {
+    cudaError_t e = cudaEventRecord(op->ev_fork, c->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(op->halo_stream, op->ev_fork, 0);
+    if (e != cudaSuccess) return c->cuda(e, "halo fork");
+    auto edge_blocks = [](const Part2D& P) {   // the edge launch's share of the G blocks: 2 of nb bands
+      const int nb = cg2p_bands(P.dev);
+      int ge = (5 * P.G + nb) / (2 * nb);   // 1.25 x its share: it starts late by the halo's latency
+      return ge < 1 ? 1 : ge > P.G - 1 ? P.G - 1 : ge;
+    };
+    {
+      StreamSwap sw(c, op->halo_stream);
+      if (int rc = halo_ws(op, false, par)) return rc;
+      for (const Part2D& P : op->parts) {
+        const int ge = edge_blocks(P);
+        if (int rc = launch2p_fpass(c, P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc, par, 2,
+                                    P.G - ge, ge))
+          return rc;
+      }
+    }
+    e = cudaEventRecord(op->ev_join, op->halo_stream);
+    if (e != cudaSuccess) return c->cuda(e, "halo join");
+    for (const Part2D& P : op->parts)
+      if (int rc = launch2p_fpass(c, P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc, par, 1, 0,
+                                  P.G - edge_blocks(P)))
+        return rc;
+    e = cudaStreamWaitEvent(c->stream, op->ev_join, 0);
+    if (e != cudaSuccess) return c->cuda(e, "halo join");
+  }
   if (int rc = reduce_all(op, 1)) return rc;
-  return launch2p_scalar(C(op), 2, op->d_red + 4, op->d_sc);
+  return launch2p_scalar(c, 2, op->d_red + 4, op->d_sc);
 }
 
 // iteration j: u_prev in buffer j & 1 (the setup's u0 in buffer 0), u_new in the other
@@ -358,6 +432,11 @@ void part2_destroy(sisdc_op1d* op) {
   if (op->h_done) cudaFreeHost(op->h_done);
   for (cudaEvent_t& e : op->ev)
     if (e) cudaEventDestroy(e);
+  if (op->ev_fork) cudaEventDestroy(op->ev_fork);
+  if (op->ev_join) cudaEventDestroy(op->ev_join);
+  if (op->halo_stream) cudaStreamDestroy(op->halo_stream);
+  cudaFree(op->d_hsend);
+  cudaFree(op->d_hrecv);
 }
 
 // ------------------------------------------------------------------ ABI
@@ -459,6 +538,14 @@ int sisdc_op2d_create_part(sisdc_ctx* x, const sisdc_op2d_desc* d, int nranks, i
   if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&op->h_done), 2 * sizeof(int), cudaHostAllocDefault);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&op->ev[0], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&op->ev[1], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&op->halo_stream, cudaStreamNonBlocking);
+  if (comm) {   // packed NCCL halo buffers (both sides of up to HALO_MAXVEC node vectors)
+    const size_t hb = 2 * (size_t)HALO_MAXVEC * g.nc * g.nex * nnod * sizeof(double);
+    if (e == cudaSuccess) e = cudaMalloc(&op->d_hsend, hb);
+    if (e == cudaSuccess) e = cudaMalloc(&op->d_hrecv, hb);
+  }
   if (e != cudaSuccess) {
     const int rc = c.cuda(e, "partition workspace");
     sisdc_op1d_destroy(op);

@@ -127,13 +127,16 @@ bool cg2p_fused(const Op2DDev& op);
 size_t cg2p_dinv_off(const Op2DDev& op);
 double* cg2p_RSW(const Op2DDev& op, double* ws, int par);
 int launch2p_fpass(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws, int G,
-                   const CgPScal* sc, int par);
+                   const CgPScal* sc, int par, int bsel = 0, int slot0 = 0, int nblk = -1);
+int cg2p_bands(const Op2DDev& op);
 double* cg2p_U(const Op2DDev& op, double* ws, int which);
 int cg2p_blocks(Ctx* c, const Op2DDev& op, int* G);
 int launch2p_phase(Ctx* c, int phase, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x,
                    double* ws, int G, const CgPScal* sc, int ucur);
 int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out);
 int launch2p_scalar(Ctx* c, int mode, const double* tot, CgPScal* sc);
+int launch2p_halo_pack(Ctx* c, const Op2DDev& op, double* vec, double* buf, int nc, int mcount, long long mstride,
+                       int dir);
 int launch2p_halo(Ctx* c, int nparts, const Op2DDev* ops, double* const* base, int nc, int mcount, long long mstride);
 
 }  // namespace sisdc

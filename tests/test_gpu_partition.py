@@ -186,3 +186,50 @@ def test_partitioned_slab_graph_replays_like_eager(rt, comm1):
         assert rt.cg_log()[0][n1:].tolist() == its_e
         assert bool((g.u == eager).all())
         rt.raise_on_failure()
+
+
+@pytest.mark.parametrize("nex,ney,nparts", [(4, 48, -1), (3, 25, -1), (4, 50, 2)])
+def test_partitioned_solve_halo_overlap(rt, comm1, monkeypatch, nex, ney, nparts):
+    """Partitions of >= 3 bands (24+ element rows) run the fused iteration with the halo overlapped:
+    the exchange and the two ghost-row bands on the operator's second stream, the interior bands on
+    the main stream (part2d.cu iterate_fused).  Same iterations as the single domain, <= 1e-13, for
+    in-process partitions and one NCCL rank (nparts -1; packed send / receive buffers), eager and
+    replayed from a CUDA graph (solves within the captured batch of 32 iterations).  Single-GPU
+    runs overlap only under SISDC_PART_OVERLAP=1 (read per solve): there is no transfer to hide."""
+    import torch
+    monkeypatch.setenv("SISDC_PART_OVERLAP", "1")
+    from paper_2504_18526_b200 import dgsem2d
+    w = small(CFG4, nex, ney)
+    part = dgsem2d.Partition(1, comm1) if nparts < 0 else dgsem2d.Partition(nparts)
+    one, op, u = ops(w, 7, part)
+    us = op.scatter(u)
+    for a in (2e-3, 5e-2):
+        n0 = rt.status()[2]
+        x1 = one.implicit_solve(one.modified_diffusion_matrix(u, a, "si2"), a, u)
+        it1 = rt.cg_log()[0][n0:].tolist()
+        cp = op.modified_diffusion_matrix(us, a, "si2")
+        n0 = rt.status()[2]
+        xp = op.implicit_solve(cp, a, us).clone()
+        assert rt.cg_log()[0][n0:].tolist() == it1, (part, a)
+        ref = x1.cpu().numpy()
+        assert np.abs(glob(op, xp) - ref).max() / np.abs(ref).max() < 1e-13
+        if it1[0] > 30:
+            continue
+        # the same solve captured (fixed-length batch, both streams inside the capture) and replayed
+        out = torch.empty_like(us)
+        rt.synchronize()
+        g = torch.cuda.CUDAGraph()
+        stream = torch.cuda.Stream(device=rt.device)
+        stream.wait_stream(torch.cuda.current_stream(rt.device))
+        op.eager_checks = False          # no status read-back inside a capture (as SlabGraph's sweeps)
+        with torch.cuda.graph(g, stream=stream):
+            rt.bind_stream()
+            op.implicit_solve(cp, a, us, out=out)
+        op.eager_checks = True
+        rt.bind_stream()
+        n0 = rt.status()[2]
+        g.replay()
+        rt.synchronize()
+        assert rt.cg_log()[0][n0:].tolist() == it1
+        assert bool((out == xp).all())
+    rt.raise_on_failure()
