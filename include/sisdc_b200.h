@@ -147,8 +147,8 @@ int  sisdc_op2d_create(sisdc_ctx* ctx, const sisdc_op2d_desc* desc, sisdc_op1d**
 void sisdc_op1d_destroy(sisdc_op1d* op);
 /* Host copies of the element tables: GLL nodes/weights (P+1), D ((P+1)^2). */
 int  sisdc_op1d_tables(const sisdc_op1d* op, double* nodes, double* weights, double* D);
-/* Per-element artificial viscosity nu_art (device, n_elem) or NULL
- * (DGOperator.nu_art, frozen per slab by begin_slab, dgsem.py:563-571). */
+/* Per-element artificial viscosity nu_art (device, n_elem; partitioned 2-D operators: storage rows,
+ * ghost rows included) or NULL (DGOperator.nu_art, frozen per slab by begin_slab, dgsem.py:563-571). */
 int  sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art);
 /* Dirichlet trace data (problem.boundary_state(t), dgsem.py:212-216,282-284):
  * register the outside states g_l(t_j), g_r(t_j) for n times (merged into the
@@ -161,7 +161,9 @@ int  sisdc_op1d_set_boundary(sisdc_op1d* op, int n, const double* times, const d
  * the MLSDC presmoothing hook of the coarse-to-fine solution transfer
  * (mlsdc.py:139-140). */
 int  sisdc_smooth_start(sisdc_op1d* op, int M, const double* u, double* out);
-/* Persson-Peraire modal sensor (dgsem.py:537-559) -> nu_art (device, n_elem). */
+/* Persson-Peraire modal sensor (dgsem.py:537-559) -> nu_art (device, n_elem).
+ * 2-D operators: the tensor-product generalisation (modes with max(k, l) = P, h = max(dx, dy)), one value
+ * per element of the storage ((rows + 2) x nex per partition, ghost rows exchanged here). */
 int  sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, double c_s, double* nu_art);
 
 /* OperatorContext methods (integrators.py:37-60, dgsem.py:205-352). */

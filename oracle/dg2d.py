@@ -168,7 +168,9 @@ class Op2D:
     """Oracle 2-D operator on a periodic nex x ney mesh of [x0,x1] x [y0,y1]."""
 
     def __init__(self, x0, x1, y0, y1, nex, ney, degree, problem, penalty=2.0, rtol=1e-14, maxit=1000,
-                 cg_log=None):
+                 cg_log=None, av=None):
+        self.av = av            # (kappa_s, c_s): Persson-Peraire artificial viscosity, frozen per slab
+        self.nu_art = None      # (ney, nex) once begin_slab has run
         self.nex, self.ney, self.P = int(nex), int(ney), int(degree)
         self.p1 = self.P + 1
         self.dx, self.dy = (x1 - x0) / nex, (y1 - y0) / ney
@@ -313,10 +315,49 @@ class Op2D:
         return np.tile(d.reshape(-1), self.nc)
 
     # rhs / SI coefficient / implicit solve --------------------------------
+    def _av_field(self):
+        """nu_art broadcast to the nodes, or None."""
+        if self.nu_art is None:
+            return None
+        return np.broadcast_to(self.nu_art[:, :, None, None], (self.ney, self.nex, self.p1, self.p1))
+
+    def persson_viscosity(self, u):
+        """Tensor-product generalisation of the reference's modal sensor (``dgsem.py:537-559``):
+        Legendre modes m_kl of field 0, energies m_kl^2 (2/(2k+1)) (2/(2l+1)), sensor = log10 of the
+        share of the modes with max(k, l) = P, the reference's ramp around s0 = -4 log10 P, and
+        eps0 = c_s h lam_max / P with h = max(dx, dy).  On y-invariant data only l = 0 survives and
+        the value is the reference's 1-D one (tests/test_oracle2d.py)."""
+        if self.av is None:
+            return np.zeros((self.ney, self.nex))
+        kap, cs = self.av
+        P = self.P
+        u5 = self.u5(u)
+        V = np.polynomial.legendre.legvander(self.xi, P)
+        Vi = np.linalg.inv(V)
+        modal = np.einsum("kj,li,...ji->...kl", Vi, Vi, u5[0])
+        nk = 2.0 / (2.0 * np.arange(self.p1) + 1.0)
+        en = modal ** 2 * (nk[:, None] * nk[None, :])
+        tot = en.sum(axis=(-1, -2))
+        top = en[..., -1, :].sum(axis=-1) + en[..., :-1, -1].sum(axis=-1)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            sv = np.where(tot > 0.0, np.log10(np.maximum(top, 1e-300) / tot), -np.inf)
+        s0 = -4.0 * np.log10(P)
+        lam = self.prob.max_speed(u5).max(axis=(-1, -2))
+        eps0 = cs * max(self.dx, self.dy) * lam / P
+        with np.errstate(invalid="ignore"):
+            ramp = np.where(sv < s0 - kap, 0.0,
+                            np.where(sv > s0 + kap, 1.0, 0.5 * (1.0 + np.sin(0.5 * np.pi * (sv - s0) / kap))))
+        return eps0 * ramp
+
     def eval_rhs(self, u, t=0.0):
         out = self.apply_convection(u, t)
+        av = self._av_field()
         if getattr(self.prob, "viscous", False):
             out = out + self.apply_viscous(u, t)
+            if av is not None:
+                out = out + self.apply_diffusion(av, u, t)
+        elif av is not None:
+            out = out + self.apply_diffusion(max(self.prob.nu, 0.0) + av, u, t)
         elif self.prob.nu > 0:
             out = out + self.apply_diffusion(self.prob.nu, u, t)
         if not np.all(np.isfinite(out)):
@@ -328,8 +369,12 @@ class Op2D:
     def modified_coeff(self, u_b, dt_m, scheme="si2"):
         lam = self.prob.max_speed(self.u5(u_b))
         c = 0.5 * dt_m * (lam * lam)
+        av = self._av_field()
         if getattr(self.prob, "viscous", False):
-            return c + self.prob.nu_si(self.u5(u_b))
+            c = c + self.prob.nu_si(self.u5(u_b))
+            return c + av if av is not None else c
+        if av is not None:
+            return c + (max(self.prob.nu, 0.0) + av)
         return c + self.prob.nu if self.prob.nu > 0 else c
 
     def implicit_solve(self, C, a, rhs, t=0.0):
@@ -349,7 +394,8 @@ class Op2D:
         return x
 
     def begin_slab(self, u0, t0, dt):
-        pass
+        if self.av is not None:
+            self.nu_art = self.persson_viscosity(u0)
 
 
 class PTransfer2D:

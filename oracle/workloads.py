@@ -27,14 +27,14 @@ def fine_nodes(w):
 
 
 def build_hierarchy_2d(make_problem2d, x0, x1, y0, y1, nex, ney, p_coarse, p_fine, m_coarse, m_fine,
-                       rtol=1e-14, log=None, n_coarse=2):
+                       rtol=1e-14, log=None, n_coarse=2, av=None):
     """Two-level 2-D p-hierarchy (oracle) sharing one CG log in call order."""
     from . import dg2d
     log = [] if log is None else log
 
     def mk(lvl):
         P = p_coarse if lvl == "coarse" else p_fine
-        return dg2d.Op2D(x0, x1, y0, y1, nex, ney, P, make_problem2d(), rtol=rtol, cg_log=log)
+        return dg2d.Op2D(x0, x1, y0, y1, nex, ney, P, make_problem2d(), rtol=rtol, cg_log=log, av=av)
 
     cc, cf = mk("coarse"), mk("fine")
     rc, rf = sweeper.Rule("radau_right", m_coarse), sweeper.Rule("radau_right", m_fine)

@@ -387,6 +387,13 @@ int op2d_create_impl(sisdc_ctx* x, const sisdc_op2d_desc* d, bool alloc_cg, sisd
     tab[TabOff::m(p1) + i] = op->weights[i];
     tab[TabOff::minv(p1) + i] = 1.0 / op->weights[i];
   }
+  {   // inverse Legendre Vandermonde (the modal sensor of the artificial viscosity)
+    std::vector<double> V(p1 * p1), Vi;
+    for (int i = 0; i < p1; ++i)
+      for (int k = 0; k < p1; ++k) { double p, dp; legendre(k, op->nodes[i], p, dp); V[i * p1 + k] = p; }
+    invert(V, p1, Vi);
+    for (int i = 0; i < p1 * p1; ++i) tab[TabOff::Vinv(p1) + i] = Vi[i];
+  }
   Op2DDev& v = op->dev2;
   v.nex = d->nex; v.ney = d->ney; v.p1 = p1; v.nc = d->ncomp;
   v.nys = d->ney; v.row0 = 0; v.e0 = 0;
@@ -455,9 +462,15 @@ int sisdc_op1d_tables(const sisdc_op1d* op, double* nodes, double* weights, doub
 
 int sisdc_op1d_set_nu_art(sisdc_op1d* op, const double* nu_art) {
   if (!op) return SISDC_ERR_ARG;
-  if (op->parted() && nu_art) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "artificial viscosity on a partitioned operator");
   op->dev.nu_art = nu_art;
   op->dev2.nu_art = nu_art;
+  // partitioned 2-D operator: nu_art is stored per STORAGE row ((rows + 2) x nex per partition, the ghost
+  // rows filled by sisdc_persson_viscosity's halo), partitions concatenated
+  long long offe = 0;
+  for (Part2D& P : op->parts) {
+    P.dev.nu_art = nu_art ? nu_art + offe : nullptr;
+    offe += (long long)P.dev.nys * P.dev.nex;
+  }
   return SISDC_OK;
 }
 
@@ -469,7 +482,15 @@ int sisdc_smooth_start(sisdc_op1d* op, int M, const double* u, double* out) {
 
 int sisdc_persson_viscosity(sisdc_op1d* op, const double* u, double kappa_s, double c_s, double* nu_art) {
   if (!op || !u || !nu_art || !(kappa_s > 0)) return SISDC_ERR_ARG;
-  if (op->dim == 2) return C(op)->fail(SISDC_ERR_UNSUPPORTED, "the modal sensor is built for 1-D meshes");
+  if (op->dim == 2) {
+    if (!op->parted()) return launch2_persson(C(op), op->dev2, u, kappa_s, c_s, nu_art);
+    long long offe = 0;
+    for (const Part2D& P : op->parts) {   // owned rows of every local partition, then the ghost rows
+      if (int rc = launch2_persson(C(op), P.dev, u + P.off, kappa_s, c_s, nu_art + offe)) return rc;
+      offe += (long long)P.dev.nys * P.dev.nex;
+    }
+    return part2_halo_elem(op, nu_art);
+  }
   return launch_persson(C(op), op->dev, u, kappa_s, c_s, nu_art);
 }
 

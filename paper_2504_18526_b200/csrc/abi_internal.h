@@ -81,3 +81,5 @@ int part2_eval_nodes(sisdc_op1d* op, int mode, int scheme, int M, int m_first, i
 int part2_stage(sisdc_op1d* op, const double* base, const double* conv_in, double dt_m, const double* f_old, int M,
                 const double* w_row, double dt, const double* g, const double* h, double* rhs, double* conv_out);
 int part2_solve(sisdc_op1d* op, sisdc::CoefDev k, double a, const double* rhs, double* x);
+// ghost rows of a per-element scalar (nys x nex per partition, partitions concatenated): the artificial viscosity
+int part2_halo_elem(sisdc_op1d* op, double* v);

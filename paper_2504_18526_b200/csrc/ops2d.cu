@@ -3412,13 +3412,79 @@ int launch2_conv(Ctx* c, const Op2DDev& op, const double* u, double* out) {
   return c->after_launch("k2_conv");
 }
 int launch2_sip(Ctx* c, const Op2DDev& op, CoefDev k, const double* u, double* out) {
-  if (op.problem == SISDC_NS2D && k.kind == SISDC_COEF_PHYS)   // the physical term is the NS viscous operator
+  if (op.problem == SISDC_NS2D && k.kind == SISDC_COEF_PHYS && op.nu_art == nullptr)   // the physical term is the NS viscous operator
     return launch2_visc(c, op, u, out, 0, 1, 0);
   SISDC_P1_SWITCH(op.p1, {
     set_smem<P1>(k2_sip<P1>);
     k2_sip<P1><<<grid2<P1>(op), Blk<P1>::NT, smem2<P1>(), c->stream>>>(op, k, u, out);
   });
-  return c->after_launch("k2_sip");
+  if (int rc = c->after_launch("k2_sip")) return rc;
+  if (op.problem == SISDC_NS2D && k.kind == SISDC_COEF_PHYS)   // with AV: nu_art Laplacian (above) + viscous operator
+    return launch2_visc(c, op, u, out, 0, 1, 1);
+  return SISDC_OK;
+}
+
+// Persson-Peraire modal sensor on a tensor-product element (the 2-D generalisation of
+// dgsem.py:537-559, oracle/dg2d.py persson_viscosity): Legendre modes m_kl = sum Vinv[k][j] Vinv[l][i]
+// u[j][i] of field 0, energies m_kl^2 (2 / (2k+1)) (2 / (2l+1)), sensor = log10(energy of the modes with
+// max(k, l) = P / total), the reference's ramp around s0 = -4 log10 P, and eps0 = c_s h lam_max / P with
+// h = max(dx, dy) and the element's largest signal speed.  On y-invariant data only the l = 0 modes
+// are non-zero and the sensor is the reference's 1-D value.  One warp per element; fixed-order sums.
+template <int P1>
+__global__ void __launch_bounds__(128) k2_persson(Op2DDev op, const double* __restrict__ u, double kappa, double cs,
+                                                  double* __restrict__ nu_art) {
+  constexpr int NN = P1 * P1, P = P1 - 1;
+  __shared__ double sU[4][NN], sT[4][NN], sV[NN];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < NN; t += blockDim.x) sV[t] = op.tab[TabOff::Vinv(P1) + t];
+  __syncthreads();
+  const int ne = op.nex * op.ney;
+  const int e = blockIdx.x * 4 + warp;
+  if (e >= ne) return;
+  const int oy = e / op.nex, ex = e - oy * op.nex, ey = oy + op.row0;
+  double lam = 0.0;
+  for (int t = lane; t < NN; t += 32) {
+    double s[NC_MAX];
+#pragma unroll
+    for (int c = 0; c < NC_MAX; ++c) s[c] = c < op.nc ? u[nidx(op, c, ey, ex, t / P1, t % P1)] : 1.0;
+    sU[warp][t] = s[0];
+    lam = fmax(lam, lam_max2d(op, s));
+  }
+  for (int o = 16; o > 0; o >>= 1) lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, o));
+  __syncwarp();
+  for (int t = lane; t < NN; t += 32) {   // T[j][l] = sum_i Vinv[l][i] u[j][i]
+    const int j = t / P1, l = t % P1;
+    double a = 0.0;
+    for (int i = 0; i < P1; ++i) a = fma(sV[l * P1 + i], sU[warp][j * P1 + i], a);
+    sT[warp][t] = a;
+  }
+  __syncwarp();
+  for (int t = lane; t < NN; t += 32) {   // m[k][l] = sum_j Vinv[k][j] T[j][l] -> energy
+    const int k = t / P1, l = t % P1;
+    double a = 0.0;
+    for (int j = 0; j < P1; ++j) a = fma(sV[k * P1 + j], sT[warp][j * P1 + l], a);
+    sU[warp][t] = a * a * ((2.0 / (2.0 * k + 1.0)) * (2.0 / (2.0 * l + 1.0)));
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double tot = 0.0, top = 0.0;
+    for (int t = 0; t < NN; ++t) {
+      const double en = sU[warp][t];
+      tot += en;
+      if (t / P1 == P || t % P1 == P) top += en;
+    }
+    const double s = tot > 0.0 ? log10(fmax(top, 1e-300) / tot) : -INFINITY;
+    const double s0 = -4.0 * log10((double)P);
+    const double eps0 = cs * fmax(op.dx, op.dy) * lam / P;
+    const double ramp = s < s0 - kappa ? 0.0 : (s > s0 + kappa ? 1.0 : 0.5 * (1.0 + sin(0.5 * M_PI * (s - s0) / kappa)));
+    nu_art[(long long)ey * op.nex + ex] = eps0 * ramp;
+  }
+}
+
+int launch2_persson(Ctx* c, const Op2DDev& op, const double* u, double kappa, double cs, double* nu_art) {
+  const int ne = op.nex * op.ney;
+  SISDC_P1_SWITCH(op.p1, { k2_persson<P1><<<(ne + 3) / 4, 128, 0, c->stream>>>(op, u, kappa, cs, nu_art); });
+  return c->after_launch("k2_persson");
 }
 // P = 7 viscous operator on the tensor cores (called by launch2_visc, visc2d.cu); returns
 // SISDC_ERR_UNSUPPORTED-free: the caller checks the shape (p1 == 8, four fields, 16-byte alignment)

@@ -169,6 +169,41 @@ inline double* at(double* p, long long o) { return p ? p + o : nullptr; }
 
 }  // namespace
 
+// ghost rows of a per-element scalar field (one value per element: the frozen artificial viscosity).
+// The element "nodes" are 1 x 1, so the exchange runs on copies of the partition descriptors with
+// p1 = 1 (row = nex values, field stride = nys * nex).
+int part2_halo_elem(sisdc_op1d* op, double* v) {
+  Ctx* c = C(op);
+  const int np = (int)op->parts.size();
+  Op2DDev ops[MAXPART];
+  double* base[MAXPART];
+  long long offe = 0;
+  for (int p = 0; p < np; ++p) {
+    ops[p] = op->parts[p].dev;
+    ops[p].p1 = 1;
+    ops[p].nn = (long long)ops[p].nys * ops[p].nex;
+    base[p] = v + offe;
+    offe += ops[p].nn;
+  }
+  if (!op->comm) return launch2p_halo(c, np, ops, base, 1, 1, 0);
+  NcclApi* api = nccl();
+  if (!api) return c->fail(SISDC_ERR_UNSUPPORTED, "NCCL is not available in this process");
+  const int R = op->comm->nranks, q = op->comm->rank;
+  const int prev = (q + R - 1) % R, next = (q + 1) % R;
+  const size_t row = (size_t)ops[0].nex;
+  double* b = base[0];
+  ncclResult_t r = api->groupStart();
+  if (r == ncclSuccess) r = api->send(b + row, row, ncclDouble, prev, op->comm->comm, c->stream);
+  if (r == ncclSuccess) r = api->send(b + (size_t)ops[0].ney * row, row, ncclDouble, next, op->comm->comm, c->stream);
+  if (r == ncclSuccess) r = api->recv(b + (size_t)(ops[0].ney + 1) * row, row, ncclDouble, next, op->comm->comm, c->stream);
+  if (r == ncclSuccess) r = api->recv(b, row, ncclDouble, prev, op->comm->comm, c->stream);
+  const ncclResult_t r2 = api->groupEnd();
+  if (r != ncclSuccess) return nccl_fail(c, r, "nu_art halo send/recv");
+  if (r2 != ncclSuccess) return nccl_fail(c, r2, "nu_art halo group");
+  ++c->launches;
+  return SISDC_OK;
+}
+
 // ------------------------------------------------------ entry points
 int part2_conv(sisdc_op1d* op, const double* u, double* out) {
   if (int rc = halo(op, u, 1, 0, false)) return rc;

@@ -24,7 +24,7 @@ struct Op2DDev {
   double gamma, nu, ax, ay;   // NS2D: nu = dynamic viscosity eta
   double pr, nsi;        // NS2D: Prandtl number, max(4/3, gamma / Pr) (SI coefficient bound)
   const double* tab;     // 1-D element tables (TabOff layout)
-  const double* nu_art;  // per element (ney*nex) or nullptr
+  const double* nu_art;  // per element, storage rows (nys*nex: ghost rows on a partition), or nullptr
 };
 
 constexpr int NC_MAX = 4;
@@ -94,9 +94,9 @@ __device__ __forceinline__ double lam_max2d(const Op2DDev& op, const double* s) 
 // (NS2D: the physical viscous term is the tensor operator of visc2d.cu, not a
 // scalar coefficient, so its scalar physical coefficient is zero)
 __device__ __forceinline__ bool phys2d(const Op2DDev& op, int eg, double& c) {
-  if (op.problem == SISDC_NS2D) {
-    c = 0.0;
-    return false;
+  if (op.problem == SISDC_NS2D) {   // the artificial viscosity (if any) is the only scalar-coefficient part
+    c = op.nu_art ? op.nu_art[eg] : 0.0;
+    return op.nu_art != nullptr;
   }
   if (op.nu_art) {
     c = (op.nu > 0.0 ? op.nu : 0.0) + op.nu_art[eg];
@@ -116,7 +116,8 @@ __device__ __forceinline__ double coef2d(const Op2DDev& op, const CoefDev& k, in
       for (int c = 0; c < NC_MAX; ++c) s[c] = c < op.nc ? k.ptr[nidx(op, c, ey, ex, j, i)] : 1.0;
       const double lam = lam_max2d(op, s);
       const double half = 0.5 * k.value * (lam * lam);
-      if (op.problem == SISDC_NS2D) return half + (op.nu / s[0]) * op.nsi;   // oracle NS2D.nu_si
+      if (op.problem == SISDC_NS2D)   // oracle NS2D.nu_si (+ the frozen artificial viscosity, as dgsem.py:356-396)
+        return half + (op.nu / s[0]) * op.nsi + (op.nu_art ? op.nu_art[eg] : 0.0);
       double ph;
       return phys2d(op, eg, ph) ? half + ph : half;
     }

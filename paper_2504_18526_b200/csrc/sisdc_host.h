@@ -103,6 +103,7 @@ int launch2_sip(Ctx* c, const Op2DDev& op, CoefDev k, const double* u, double* o
 // NS2D physical viscous operator: f[m] (+)= visc(u[m]) for m in [m_first, m_first + m_count)
 int launch2_visc(Ctx* c, const Op2DDev& op, const double* u, double* f, int m_first, int m_count, int accumulate);
 int launch2_visc8(Ctx* c, const Op2DDev& op, const double* u, double* f, int m_first, int m_count, int accumulate);
+int launch2_persson(Ctx* c, const Op2DDev& op, const double* u, double kappa, double cs, double* nu_art);
 int launch2_coef(Ctx* c, const Op2DDev& op, CoefDev k, double* out);
 int launch2_node_eval(Ctx* c, const Op2DDev& op, int mode, int scheme, int M, int m_first, int m_count,
                       const double* u0, const double* u, const double* conv_prev, const double* dts,

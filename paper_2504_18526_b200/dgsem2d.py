@@ -247,11 +247,13 @@ class DGOperator2D:
     is2d = True
 
     def __init__(self, mesh: Mesh2D, problem, penalty_const: float = 2.0, device: int = 0, eager_checks: bool = True,
-                 partition: Partition = None):
+                 partition: Partition = None, av=None):
+        """``av``: ``dgsem.ArtificialViscosityParams(kappa_s, c_s)`` switches on the Persson-Peraire sensor
+        (tensor-product generalisation of ``dgsem.py:537-559``; frozen per slab by ``begin_slab``)."""
         self.mesh = mesh
         self.partition = partition
         self.problem = problem
-        self.av = None
+        self.av = av
         self.ncomp = problem.ncomp
         self.p1 = mesh.degree + 1
         self.ndof = self.ncomp * mesh.n_elem * self.p1 * self.p1
@@ -422,8 +424,33 @@ class DGOperator2D:
             self.rt.raise_on_failure()
         return out
 
+    def _nu_art_buffer(self):
+        """One value per element of the storage (ghost rows included on a partition)."""
+        return self.rt.zeros(self.slab_rows * self.mesh.nex)
+
+    def persson_viscosity(self, u):
+        """Element-wise artificial viscosity of state ``u`` (``dgsem.py:537-559`` on tensor-product
+        Legendre modes): (slab_rows * nex,) device tensor, zeros without ``av``."""
+        out = self._nu_art_buffer()
+        if self.av is None:
+            return out
+        u = self.rt.to_device(u)
+        self.rt.bind_stream()
+        self.rt.check(self.lib.sisdc_persson_viscosity(self.h, u.data_ptr(), float(self.av.kappa_s),
+                                                       float(self.av.c_s), out.data_ptr()), "persson")
+        return out
+
     def begin_slab(self, u0, t0: float, dt: float) -> None:
-        pass
+        """Freeze per-slab data (``dgsem.py:563-571``): the AV field."""
+        if self.av is None:
+            return
+        if self.nu_art is None:
+            self.nu_art = self._nu_art_buffer()
+        u0 = self.rt.to_device(u0)
+        self.rt.bind_stream()
+        self.rt.check(self.lib.sisdc_persson_viscosity(self.h, u0.data_ptr(), float(self.av.kappa_s),
+                                                       float(self.av.c_s), self.nu_art.data_ptr()), "persson")
+        self.rt.check(self.lib.sisdc_op1d_set_nu_art(self.h, self.nu_art.data_ptr()), "set_nu_art")
 
     def boundary_at(self, *times):
         """Periodic 2-D meshes carry no trace data."""

@@ -239,3 +239,81 @@ def test_ns2d_y_invariant_reduces_to_reference_cns(rt, golden):
             d = np.abs(v[c2] - r3[c1][None, :, None, :]).max()
             assert d <= 1e-12 * max(1e-300, np.abs(r3[c1]).max()), (key, c2, d)
         assert np.abs(v[2]).max() <= 1e-12 * np.abs(r3[1]).max()
+
+
+# ------------------------------------------------ artificial viscosity in 2-D (Persson sensor)
+def _front_state(w, X, Y):
+    """The workload's state with an under-resolved oblique front on rho (activates the sensor)."""
+    u = np.array(w.initial_state(X, Y), dtype=np.float64).reshape(4, *X.shape)
+    L = w.length
+    bump = 0.15 * np.tanh((X + 0.4 * Y - 0.55 * L) / (0.004 * L))
+    u[0] += bump
+    u[3] += 0.5 * bump
+    return u.reshape(-1)
+
+
+@pytest.mark.parametrize("base,nex,ney,P", [(CFG4, 5, 4, 7), (CFG3, 6, 3, 3), (CFG4, 4, 5, 5)])
+def test_persson_sensor_and_av_operators_2d(rt, base, nex, ney, P):
+    """2-D Persson-Peraire artificial viscosity (tensor-product generalisation of dgsem.py:537-559;
+    the oracle reduces to the pinned 1-D sensor on y-invariant data, tests/test_oracle2d.py): the
+    sensor, then with the frozen field the right-hand side, the SI coefficient and the implicit solve."""
+    from paper_2504_18526_b200 import dgsem, dgsem2d
+    w = small(base, nex, ney)
+    L = w.length
+    av = dgsem.ArtificialViscosityParams(1.0, 0.7)
+    op = dgsem2d.DGOperator2D(dgsem2d.Mesh2D(0.0, L, 0.0, L, nex, ney, P), w.gpu_problem(), av=av)
+    orc = dg2d.Op2D(0.0, L, 0.0, L, nex, ney, P, workloads.problem2d(w), av=(1.0, 0.7))
+    X, Y = op.mesh.nodes_xy
+    u = _front_state(w, X, Y)
+    nu_o = orc.persson_viscosity(u)
+    assert nu_o.max() > 0 and (nu_o == 0).any()          # the ramp is active on some elements only
+    nu_g = op.persson_viscosity(u).cpu().numpy().reshape(ney, nex)
+    assert np.abs(nu_g - nu_o).max() <= 1e-10 * nu_o.max()
+    op.begin_slab(u, 0.0, 1e-3)
+    orc.begin_slab(u, 0.0, 1e-3)
+    tol = 4e-12 if w.kind == "shear" else 1e-12
+    assert rel(op.eval_rhs(u), orc.eval_rhs(u)) < tol
+    a = 2e-3
+    c = op.modified_diffusion_matrix(u, a, "si2")
+    co = orc.modified_coeff(u, a)
+    assert rel(op.coefficient_field(c), np.asarray(co).reshape(-1)) < 1e-12
+    n0 = rt.status()[2]
+    x = op.implicit_solve(c, a, u)
+    xo = orc.implicit_solve(co, a, u)
+    assert rt.cg_log()[0][n0:].tolist() == [orc.cg_log[-1][0]]
+    assert rel(x, xo) < 1e-13
+    rt.raise_on_failure()
+
+
+def test_mlsdc_step_2d_with_av(rt):
+    """One SI-MLSDC step (P 7/3) with the artificial viscosity frozen per slab on both levels: GPU
+    vs the 2-D restatement, identical CG iteration sequence; and the element-row partitioned
+    operator (nu_art with ghost rows, halo of the per-element field) against the single domain."""
+    from paper_2504_18526_b200 import dgsem, dgsem2d, mlsdc
+    w = small(CFG4, 5, 6)
+    L = w.length
+    av = dgsem.ArtificialViscosityParams(1.0, 0.7)
+
+    def run(partition):
+        mk = lambda P: dgsem2d.DGOperator2D(dgsem2d.Mesh2D(0.0, L, 0.0, L, w.nex, w.ney, P), w.gpu_problem(),
+                                            av=av, partition=partition)
+        h = mlsdc.build_p_hierarchy(mk, [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+        X, Y = h.fine.ctx.mesh.nodes_xy
+        u0 = _front_state(w, X, Y)
+        dt = 0.5 * w.time_step(u0, dgsem.compute_delta(w.p_fine))
+        n0 = rt.status()[2]
+        sol = mlsdc.run_mlsdc(h, h.fine.ctx.scatter(u0), 0.0, dt, w.n_cycles, strategy="fmg")
+        rt.raise_on_failure()
+        assert float(h.fine.ctx.nu_art.max()) > 0
+        return h.fine.ctx.gather(sol.u[-1]).reshape(-1), rt.cg_log()[0][n0:].tolist(), u0, dt
+
+    got, its, u0, dt = run(None)
+    oh, log = workloads.build_hierarchy_2d(lambda: workloads.problem2d(w), 0.0, L, 0.0, L, w.nex, w.ney,
+                                           w.p_coarse, w.p_fine, w.m_coarse, w.m_fine, av=(1.0, 0.7))
+    ref = osw.run_mlsdc(oh, u0, 0.0, dt, w.n_cycles, "fmg").u[-1]
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-11
+    assert its == [i for i, _ in log]
+    for part in (dgsem2d.Partition(2), dgsem2d.Partition(3)):
+        gp, itp, _, _ = run(part)
+        assert itp == its, part
+        assert np.linalg.norm(gp - got) / np.linalg.norm(got) < 1e-11, part

@@ -123,3 +123,32 @@ def test_ns2d_viscous_consistency():
     sw = np.stack([np.ones(X.shape), np.sin(Y), np.zeros(X.shape), np.full(X.shape, 2.5)])
     fv = op.apply_viscous(sw.reshape(-1)).reshape(4, 4, 4, 8, 8)
     assert np.abs(fv[1] + 1e-2 * np.sin(Y)).max() < 1e-6
+
+
+def test_persson_2d_reduces_to_pinned_1d_sensor():
+    """The tensor-product modal sensor on y-invariant data is the 1-D sensor of oracle/dg1d.py
+    (itself pinned to the reference's AV goldens, test_oracle_golden.py): only the l = 0 modes
+    survive, their (2 / (2l+1)) = 2 factor cancels in the energy ratio, h = max(dx, dy) = dx."""
+    from oracle import dg1d
+    ne, P, ney = 24, 6, 3
+    av = (1.0, 0.7)
+    o1 = dg1d.Op1D(0.0, 2.0, ne, P, dg1d.Burgers(1e-3), av=av)
+    x = (o1.xl + o1.dx * np.arange(ne))[:, None] + 0.5 * o1.dx * (o1.xi + 1.0)[None, :]
+    u1 = 0.3 + np.tanh((x - 1.03) / 0.02) + 0.2 * np.tanh((x - 0.41) / 0.01)   # under-resolved fronts: the ramp is active
+    nu1 = o1.persson_viscosity(u1.reshape(-1))
+    assert nu1.max() > 0 and (nu1 == 0).any()
+    o2 = dg2d.Op2D(0.0, 2.0, 0.0, 0.1, ne, ney, P, dg2d.Burgers2D(1e-3), av=av)
+    u2 = np.broadcast_to(u1.reshape(1, 1, ne, 1, P + 1), (1, ney, ne, P + 1, P + 1)).reshape(-1)
+    nu2 = o2.persson_viscosity(u2)
+    assert nu2.shape == (ney, ne)
+    for j in range(ney):
+        assert np.abs(nu2[j] - nu1).max() <= 1e-13 * nu1.max()
+    # frozen per slab, entering the rhs and the SI coefficient as nu + nu_art (dgsem.py:356-396, 563-571)
+    o2.begin_slab(u2, 0.0, 1e-3)
+    o1.begin_slab(u1.reshape(-1), 0.0, 1e-3)
+    r2 = o2.eval_rhs(u2).reshape(1, ney, ne, P + 1, P + 1)
+    r1 = o1.eval_rhs(u1.reshape(-1))
+    assert rel(r2[0, 1, :, 2, :].reshape(-1), r1) < 1e-12
+    c2 = np.asarray(o2.modified_coeff(u2, 2e-3)).reshape(ney, ne, P + 1, P + 1)
+    c1 = np.asarray(o1.modified_coeff(u1.reshape(-1), 2e-3)).reshape(ne, P + 1)
+    assert rel(c2[1, :, 3, :], c1) < 1e-14
