@@ -169,6 +169,10 @@ class DGOperator:
         # source(x, t, u3) (dgsem.py:328-352): a host callable, evaluated on the host
         # at the node coordinates and added to f on the device (no graph capture)
         self.source_fn = getattr(problem, "source", None)
+        # a known forcing src(x, t): device tables keyed by time (no device -> host copy of the state,
+        # one upload per distinct node time; cleared every slab)
+        self.source_tabulated = self.source_fn is not None and not getattr(problem, "source_depends_on_state", True)
+        self._src_tab = {}
         self.nu_art = None            # device tensor (n_elem,) when AV is active
         self._last_dt = None
         self._scratch = None
@@ -302,6 +306,15 @@ class DGOperator:
     def _source_values(self, u, t: float):
         """src(x, t, u3) on the host (dgsem.py:328-335), broadcast over the
         components, as a device vector; None when the source returns None."""
+        if self.source_tabulated:
+            key = float(t)
+            if key not in self._src_tab:
+                if len(self._src_tab) >= 64:   # standalone eval_rhs at many times: keep the cache bounded
+                    self._src_tab.clear()
+                vals = self.source_fn(self.mesh.nodes_x, key, None)
+                self._src_tab[key] = None if vals is None else self.rt.to_device(np.ascontiguousarray(
+                    (np.asarray(vals, dtype=np.float64) + np.zeros((self.ncomp, 1, 1))).reshape(-1)))
+            return self._src_tab[key]
         u3 = self.as_nodes(u).detach().cpu().numpy()
         vals = self.source_fn(self.mesh.nodes_x, float(t), u3)
         if vals is None:
@@ -327,7 +340,7 @@ class DGOperator:
         if self.source_fn is None:
             return self.rt.zeros(self.ndof)
         v = self._source_values(self.rt.to_device(u), t)
-        return self.rt.zeros(self.ndof) if v is None else v
+        return self.rt.zeros(self.ndof) if v is None else v.clone()
 
     def coefficient_field(self, coeff):
         """Materialise a coefficient as an (n_elem, P+1) device field
@@ -373,6 +386,7 @@ class DGOperator:
 
     def begin_slab(self, u0, t0: float, dt: float) -> None:
         """Freeze per-slab data (``dgsem.py:563-571``): the AV field."""
+        self._src_tab.clear()
         if self.av is not None:
             if self.nu_art is None:
                 self.nu_art = self.rt.zeros(self.mesh.n_elem)

@@ -29,18 +29,21 @@ class ConvectionDiffusion:
 
 
 class Burgers:
-    """u_t + (u^2/2)_x = nu u_xx (``problems.py:55-82``); sources are not
-    built on the GPU path."""
+    """u_t + (u^2/2)_x = nu u_xx (``problems.py:55-82``).  ``source`` is the
+    reference's host callable src(x, t, u); ``source_depends_on_state=False``
+    declares a known forcing src(x, t) (manufactured solutions): its node values
+    are then tabulated per time on the device and the state never leaves the GPU."""
 
     ncomp = 1
     is_linear = False
     kind = "burgers"
 
-    def __init__(self, nu: float = 0.0, source=None, boundary=None):
+    def __init__(self, nu: float = 0.0, source=None, boundary=None, source_depends_on_state: bool = True):
         if nu < 0:
             raise ValueError("diffusion coefficient must be nonnegative")
         self.nu = float(nu)
         self.source = source
+        self.source_depends_on_state = bool(source_depends_on_state)
         self.boundary_state = boundary
         self.speed = 0.0
 

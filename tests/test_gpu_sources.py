@@ -40,10 +40,11 @@ def rt():
     return r
 
 
-def gpu_op(P):
+def gpu_op(P, tabulated=False):
     from paper_2504_18526_b200 import dgsem, problems
     return dgsem.DGOperator(dgsem.Mesh1D(-1.0, 1.0, W.n_elem, P, bc="dirichlet"),
-                            problems.Burgers(W.nu, source=W.source, boundary=W.boundary))
+                            problems.Burgers(W.nu, source=W.source, boundary=W.boundary,
+                                             source_depends_on_state=not tabulated))
 
 
 def test_source_steady_state_and_rhs(rt, golden):
@@ -91,3 +92,34 @@ def test_source_sdc_and_mlsdc(rt, golden):
     assert l2rel(u, G["exact_t2"]) < 1e-4   # the manufactured solution itself
     with pytest.raises(ValueError, match="cannot be captured"):
         mlsdc.SlabGraph(h, G["u0"], 0.0, dt, W.n_cycles, "fmg")
+
+
+def test_tabulated_source_keeps_the_state_on_the_device(rt, golden):
+    """A known forcing src(x, t) (``source_depends_on_state=False``) is tabulated per node time on the
+    device: the callable never sees the state (it receives None), and the SI-MLSDC steps reproduce
+    the same reference goldens with the identical CG iteration sequence."""
+    from paper_2504_18526_b200 import mlsdc
+    G = golden["sources"]
+    dt = float(G["dt"])
+    seen = []
+
+    def src(x, t, u=None):
+        seen.append(u)
+        return W.source(x, t, None)
+    from paper_2504_18526_b200 import dgsem, problems
+    mk = lambda P: dgsem.DGOperator(dgsem.Mesh1D(-1.0, 1.0, W.n_elem, P, bc="dirichlet"), problems.Burgers(
+        W.nu, source=src, boundary=W.boundary, source_depends_on_state=False))
+    h = mlsdc.build_p_hierarchy(mk, [W.p_coarse, W.p_fine], [W.m_coarse, W.m_fine])
+    assert h.fine.ctx.source_tabulated
+    u = G["u0"]
+    for step in (1, 2):
+        n0 = rt.status()[2]
+        sol = mlsdc.run_mlsdc(h, u, (step - 1) * dt, dt, W.n_cycles, strategy="fmg")
+        assert rt.cg_log()[0][n0:].tolist() == G[f"mlsdc_pcg_iters{step}"].tolist()
+        assert l2rel(sol.u[-1], G[f"mlsdc_pcg_u{step}"]) < 1e-11
+        u = sol.u[-1].clone()
+    rt.raise_on_failure()
+    assert seen and all(s is None for s in seen)
+    # one table per distinct node time of the slab and level, not one host evaluation per use
+    assert len(seen) <= 2 * (W.m_fine + W.m_coarse + 2)
+    assert rel(gpu_op(W.p_fine, tabulated=True).apply_source(G["u0"], 0.3), G["src_t03"]) < 1e-15
