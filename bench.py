@@ -497,7 +497,7 @@ def measure_part(w, args, torch, rt, rank, world, local, steps, warmup, emulate=
         torch.cuda.synchronize()
     launches = rt.launch_count() - l0
     t_steps = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
-    rt.raise_on_failure()
+    dgsem2d.raise_on_failure_all(rt)   # every rank raises if any rank latched a failure
     its = rt.cg_log()[0][n_log0:]
 
     def tmax(t):

@@ -198,6 +198,38 @@ def bootstrap_id(rank: int, nranks: int, make_id, group=None) -> bytes:
     return obj[0]
 
 
+def agree_on_status(bad: int, fails: int, group=None, device=None):
+    """Failure flags of a multi-rank partitioned run, agreed over the ranks (the NaN flag
+    as an allreduce(min)): the smallest global element index with a non-finite right-hand side (-1:
+    none) and the total number of failed implicit solves.  Every rank then raises the same
+    ``SolverError`` instead of one rank leaving the others inside a collective.  One rank (or no
+    process group): the inputs."""
+    try:
+        import torch
+        import torch.distributed as dist
+    except ImportError:   # pragma: no cover
+        return bad, fails
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return bad, fails
+    big = 2 ** 62
+    t = torch.tensor([bad if bad >= 0 else big, -int(fails)], dtype=torch.int64,
+                     device=device if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)   # min of -fails = -(max fails); the element index: min
+    b, f = int(t[0].item()), -int(t[1].item())
+    return (-1 if b >= big else b), f
+
+
+def raise_on_failure_all(rt, group=None) -> None:
+    """``Runtime.raise_on_failure`` with the flags agreed over the ranks of a partitioned run."""
+    from ._lib import SolverError
+    bad, fails, _ = rt.status()
+    bad, fails = agree_on_status(bad, fails, group, rt.device)
+    if bad >= 0:
+        raise SolverError(f"non-finite right-hand side in element {bad}")
+    if fails > 0:
+        raise SolverError(f"implicit CG solve did not converge within {rt.maxit} iterations (on some rank)")
+
+
 @dataclass(frozen=True)
 class Partition:
     """Element-row partition of a 2-D mesh.

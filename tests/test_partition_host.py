@@ -122,3 +122,36 @@ def test_halo_exchange_gloo(world, ney):
         assert ok_id, rank
         assert top and bot, (rank, top, bot)
         assert tot, rank
+
+
+def _status_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_18526_b200.dgsem2d import agree_on_status
+        clean = agree_on_status(-1, 0)
+        # rank 1 saw a non-finite rhs in (global) element 17 and two failed solves, rank 2 element 5
+        mine = {0: (-1, 0), 1: (17, 2), 2: (5, 1)}[rank]
+        q.put((rank, clean, agree_on_status(*mine)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_failure_flags_agree_over_ranks(world):
+    """SURVEY 8e: the NaN / no-convergence flags are reduced over the ranks (element index: min;
+    failed solves: max), so every rank of a partitioned run raises the same error."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_status_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = (17, 2) if world == 2 else (5, 2)
+    for rank, clean, agreed in res:
+        assert clean == (-1, 0), rank
+        assert agreed == want, (rank, agreed)
