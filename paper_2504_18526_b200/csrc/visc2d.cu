@@ -247,7 +247,8 @@ int launch2_visc(Ctx* c, const Op2DDev& op, const double* u, double* f, int m_fi
   if (op.problem != SISDC_NS2D) return SISDC_OK;
   if (op.nc != 4) return c->fail(SISDC_ERR_ARG, "NS2D needs four fields");
   // P = 7: warp-per-element tensor-core kernel (ops2d.cu); SISDC_VISC_LINE=1 keeps the line formulation (A/B)
-  static const bool line_only = [] { const char* v = getenv("SISDC_VISC_LINE"); return v && v[0] == '1'; }();
+  const char* vl = getenv("SISDC_VISC_LINE");   // read per call: the GPU test compares the two kernels
+  const bool line_only = vl && vl[0] == '1';
   if (op.p1 == 8 && !line_only && ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(f)) & 15) == 0 &&
       (op.ns & 1) == 0)
     return launch2_visc8(c, op, u, f, m_first, m_count, accumulate);

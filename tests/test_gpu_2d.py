@@ -317,3 +317,26 @@ def test_mlsdc_step_2d_with_av(rt):
         gp, itp, _, _ = run(part)
         assert itp == its, part
         assert np.linalg.norm(gp - got) / np.linalg.norm(got) < 1e-11, part
+
+
+@pytest.mark.parametrize("nex,ney", [(5, 4), (1, 3), (9, 1)])
+def test_visc8_equals_line_kernel_bitwise(rt, monkeypatch, nex, ney):
+    """The P = 7 tensor-core viscous kernel (k2_visc8: own-side face fluxes reused from the node
+    pass, two-stage staging pipeline) against the line-formulated k2_visc<8> it replaced
+    (SISDC_VISC_LINE=1): the same operations per node, so bitwise equal -- also on one-element-wide
+    meshes where an element is its own periodic neighbour -- and both within 1e-12 of the oracle."""
+    w = small(CFG4, nex, ney)
+    op, orc, u = pair(w, 7)
+    rng = np.random.default_rng(3)
+    u = u * (1.0 + 1e-2 * rng.standard_normal(u.shape))
+    new = op.apply_viscous(u).cpu().numpy()
+    monkeypatch.setenv("SISDC_VISC_LINE", "1")
+    old = op.apply_viscous(u).cpu().numpy()
+    monkeypatch.delenv("SISDC_VISC_LINE")
+    assert np.array_equal(new, old)
+    assert rel(new, orc.apply_viscous(u)) < 1e-12
+    # accumulate mode (f += visc) through eval_rhs
+    r_new = op.eval_rhs(u).cpu().numpy()
+    monkeypatch.setenv("SISDC_VISC_LINE", "1")
+    r_old = op.eval_rhs(u).cpu().numpy()
+    assert np.array_equal(r_new, r_old)
