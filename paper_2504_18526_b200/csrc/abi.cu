@@ -407,6 +407,7 @@ int op2d_create_impl(sisdc_ctx* x, const sisdc_op2d_desc* d, bool alloc_cg, sisd
   v.pr = d->problem == SISDC_NS2D ? d->prandtl : 1.0;
   v.nsi = d->problem == SISDC_NS2D ? std::max(4.0 / 3.0, d->gamma / d->prandtl) : 0.0;
   v.nu_art = nullptr;
+  v.fused_sub2 = 0;
   cudaError_t e = cudaMalloc(&op->d_tab, tab.size() * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(op->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {

@@ -2636,7 +2636,8 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       const int band = A.bsel == 0 ? bq : A.bsel == 1 ? bq + 1 : (bq == 0 ? 0 : nbands - 1);
       const int y0 = band * NW, nrows = neyT - y0 < NW ? neyT - y0 : NW;
       const bool valid = warp < nrows;
-      const int ey = (valid ? y0 + warp : y0) + op.row0;   // (storage) tile row; a partition's ghost rows: ynb
+      // SUB = 1: the (storage) element row, a partition's ghost rows through ynb; SUB = 2: the tile row (trow maps it)
+      const int ey = (valid ? y0 + warp : y0) + (SUB == 1 ? op.row0 : 0);
       const int x0 = sx * SL, x1 = x0 + SL < nexT ? x0 + SL : nexT;
       // offsets in doubles fit 32 bits (checked by the launcher: n < 2^32)
       const unsigned fo = (unsigned)(c * nn);
@@ -2645,11 +2646,17 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       auto trow = [&](int ty, int d) -> unsigned {
         if constexpr (SUB == 1) return (unsigned)(d == 0 ? ty : ynb(op, ty, d)) * epitch;
         const int t2 = ty + d;
-        return (unsigned)((t2 < 0 ? neyT - 1 : t2 >= neyT ? 0 : t2) * SUB) * epitch;
+        if (op.row0 == 0) return (unsigned)((t2 < 0 ? neyT - 1 : t2 >= neyT ? 0 : t2) * SUB) * epitch;
+        // partition: tile row t2 starts at storage element row row0 + 2 t2.  The tile row above the partition
+        // has only its lower element row in storage (the top ghost row), the one below only its upper one
+        // (the bottom ghost row; t2 = -1 wraps, and only offset + epitch is ever dereferenced): see issue_halo
+        return (unsigned)(op.row0 + t2 * SUB) * epitch;
       };
+      const bool top_out = SUB == 2 && op.row0 != 0 && y0 + nrows == neyT;   // the band's upper neighbour is the ghost row
+      const bool bot_out = SUB == 2 && op.row0 != 0 && y0 == 0;
       const unsigned rowC = trow(ey, 0), rowT = trow(ey, 1), rowB = trow(ey, -1);
-      const unsigned hrow0 = trow(op.row0 + y0 + nrows - 1, 1);   // above the band
-      const unsigned hrow1 = trow(op.row0 + y0, -1);              // below the band
+      const unsigned hrow0 = trow((SUB == 1 ? op.row0 : 0) + y0 + nrows - 1, 1);   // above the band
+      const unsigned hrow1 = trow((SUB == 1 ? op.row0 : 0) + y0, -1);              // below the band
       const unsigned oC = fo + rowC + lglob;
       const unsigned cfb = (f == FT ? rowT : f == FB ? rowB : rowC) + fnode;   // this lane's face coefficient row
       // own stage of step js: r, s, w, dinv of column js+1, cf of column js (js >= x0)
@@ -2687,7 +2694,10 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
           mbar2_expect(mb, NV * 512u);
 #pragma unroll
           for (int rn = 0; rn < SUB; ++rn) {
-            const unsigned eo_ = e1 + rn * epitch;
+            // a partition's ghost tile row holds ONE element row: the missing one is read from the ghost row
+            // too (finite values that the block-diagonal face rows multiply by exact zeros)
+            const int rs = (h == 0 && top_out) ? 0 : (h == 1 && bot_out) ? 1 : rn;
+            const unsigned eo_ = e1 + rs * epitch;
             const uint32_t d = dst + rn * RUN;
             bulk_g2s(d, (MODE == 1 ? A.rhs : Ro) + eo_, RUN, mb);
             if constexpr (MODE == 0) {
@@ -3744,7 +3754,7 @@ bool cg2p_fused(const Op2DDev& op) {
     const char* v = getenv("SISDC_CG_FUSED");
     return !(v && v[0] == '0');
   }();
-  return on && op.p1 == 8;
+  return on && (op.p1 == 8 || (op.p1 == 4 && op.fused_sub2 != 0));
 }
 size_t cg2p_ws_doubles(const Op2DDev& op, int G) { return 7 * (size_t)op.n + 2 * (size_t)op.nn + 8 * (size_t)G; }
 size_t cg2p_part_off(const Op2DDev& op) { return (cg2p_fused(op) ? 7 : 6) * (size_t)op.n + 2 * (size_t)op.nn; }
@@ -3844,7 +3854,19 @@ int launch2p_fpass(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double*
   A.part += 4 * slot0;
   A.part2 += 4 * slot0;
   cudaError_t e = cudaSuccess;
-  if (op.nc == 4) {
+  if (op.p1 == 4 && (op.nc == 4 || op.nc == 1)) {   // P = 3: 2 x 2-element tiles (even nex, even rows: fused_sub2)
+    if (op.nc == 4) {
+      using F = Fz<4, 2>;
+      constexpr int smem = (int)(sizeof(double) * F::SIZE);
+      cudaFuncSetAttribute(k2_cgf<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      k2_cgf<4, 2><<<nblk, F::NW * 32, smem, c->stream>>>(A);
+    } else {
+      using F = Fz<1, 2>;
+      constexpr int smem = (int)(sizeof(double) * F::SIZE);
+      cudaFuncSetAttribute(k2_cgf<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      k2_cgf<1, 2><<<nblk, F::NW * 32, smem, c->stream>>>(A);
+    }
+  } else if (op.nc == 4) {
     using F = Fz<4>;
     constexpr int smem = (int)(sizeof(double) * F::SIZE);
     cudaFuncSetAttribute(k2_cgf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -3862,8 +3884,8 @@ int launch2p_fpass(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double*
   if (e != cudaSuccess) return c->cuda(e, "k2_cgf single-pass launch");
   return SISDC_OK;
 }
-// bands of the fused pass on a partition (8 element rows each)
-int cg2p_bands(const Op2DDev& op) { return (op.ney + Fz<4>::NW - 1) / Fz<4>::NW; }
+// bands of the fused pass on a partition (8 element rows each; P = 3: 8 rows of 2 x 2-element tiles)
+int cg2p_bands(const Op2DDev& op) { return ((op.p1 == 4 ? op.ney / 2 : op.ney) + Fz<4>::NW - 1) / Fz<4>::NW; }
 
 int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out) {
   if (nparts < 1 || nparts > MAXPART) return c->fail(SISDC_ERR_ARG, "partition count");

@@ -530,7 +530,15 @@ int sisdc_op2d_create_part(sisdc_ctx* x, const sisdc_op2d_desc* d, int nranks, i
   if (int rc = op2d_create_impl(x, d, false, &op)) return rc;
   op->comm = comm;
   op->nranks = nranks;
-  const Op2DDev& g = op->dev2;
+  Op2DDev& g = op->dev2;
+  // P = 3 partitions iterate with the fused 2 x 2-tile pass when every rank's block has an even number of
+  // element rows and nex is even (the same decision on every rank: rank_rows is deterministic)
+  g.fused_sub2 = g.p1 == 4 && d->nex % 2 == 0 ? 1 : 0;
+  for (int q = 0; q < nranks && g.fused_sub2; ++q) {
+    int rb = 0, rcnt = 0;
+    rank_rows(d->ney, nranks, q, &rb, &rcnt);
+    if (rcnt % 2 != 0) g.fused_sub2 = 0;
+  }
   const long long nnod = (long long)g.p1 * g.p1;
   long long off = 0, offc = 0;
   for (int l = 0; l < nlocal; ++l) {

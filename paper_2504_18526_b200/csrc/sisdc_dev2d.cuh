@@ -25,6 +25,7 @@ struct Op2DDev {
   double pr, nsi;        // NS2D: Prandtl number, max(4/3, gamma / Pr) (SI coefficient bound)
   const double* tab;     // 1-D element tables (TabOff layout)
   const double* nu_art;  // per element, storage rows (nys*nex: ghost rows on a partition), or nullptr
+  int fused_sub2;        // partition at P = 3 whose split solve iterates with the fused 2 x 2-tile pass (even nex, even rows on every rank)
 };
 
 constexpr int NC_MAX = 4;

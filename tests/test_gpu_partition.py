@@ -100,7 +100,7 @@ def test_partitioned_node_caches_bitwise(rt, comm1):
                 assert np.array_equal(glob(op, b[m]), a[m].cpu().numpy())
 
 
-@pytest.mark.parametrize("nex,ney,P", [(6, 8, 7), (5, 7, 3)])
+@pytest.mark.parametrize("nex,ney,P", [(6, 8, 7), (5, 7, 3), (6, 8, 3), (2, 16, 3), (34, 12, 3)])
 def test_partitioned_implicit_solve(rt, comm1, nex, ney, P):
     w = small(CFG4, nex, ney)
     for part in parts(comm1):
@@ -188,8 +188,8 @@ def test_partitioned_slab_graph_replays_like_eager(rt, comm1):
         rt.raise_on_failure()
 
 
-@pytest.mark.parametrize("nex,ney,nparts", [(4, 48, -1), (3, 25, -1), (4, 50, 2)])
-def test_partitioned_solve_halo_overlap(rt, comm1, monkeypatch, nex, ney, nparts):
+@pytest.mark.parametrize("nex,ney,nparts,P", [(4, 48, -1, 7), (3, 25, -1, 7), (4, 50, 2, 7), (4, 96, -1, 3), (6, 100, 2, 3)])
+def test_partitioned_solve_halo_overlap(rt, comm1, monkeypatch, nex, ney, nparts, P):
     """Partitions of >= 3 bands (24+ element rows) run the fused iteration with the halo overlapped:
     the exchange and the two ghost-row bands on the operator's second stream, the interior bands on
     the main stream (part2d.cu iterate_fused).  Same iterations as the single domain, <= 1e-13, for
@@ -201,7 +201,7 @@ def test_partitioned_solve_halo_overlap(rt, comm1, monkeypatch, nex, ney, nparts
     from paper_2504_18526_b200 import dgsem2d
     w = small(CFG4, nex, ney)
     part = dgsem2d.Partition(1, comm1) if nparts < 0 else dgsem2d.Partition(nparts)
-    one, op, u = ops(w, 7, part)
+    one, op, u = ops(w, P, part)   # P = 3: the fused 2 x 2-tile pass (even rows per partition), bands of 16 rows
     us = op.scatter(u)
     for a in (2e-3, 5e-2):
         n0 = rt.status()[2]
