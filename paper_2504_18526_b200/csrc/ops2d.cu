@@ -2573,9 +2573,11 @@ __global__ void __launch_bounds__(256, 2) k2_cgf(Cg2Args A) {
       thr = A.scal[2]; rho = A.scal[3]; alpha = A.scal[4]; rgam = A.scal[5]; ralpha = A.scal[6];
     }
   } else if constexpr (MODE == 2) {
-    double t2[3];
-    slot_total(slot2, t2);
-    if (t2[1] == 0.0) return;   // b == 0: MODE 0 writes x = 0
+    if (A.sc == nullptr) {   // (a partition's own b may vanish while the solve's does not: no local shortcut)
+      double t2[3];
+      slot_total(slot2, t2);
+      if (t2[1] == 0.0) return;   // b == 0: MODE 0 writes x = 0
+    }
   }
   MmaLane K;
   if constexpr (SUB == 1) mma_lane_init(op, K); else mma_lane_init_sub2(op, K);
@@ -3173,6 +3175,10 @@ __global__ void __launch_bounds__(256) k2p_reduce(RedPArgs R) {
       if (R.mode == 0) {
         v0 += R.pb[p][b * 4];
         v1 += R.pb[p][b * 4 + 1];
+      } else if (R.mode == 2) {   // one slot array holding (r,u), (w,u), (r,r): the fused setup pass (MODE 2)
+        v0 += R.pa[p][b * 4];
+        v1 += R.pa[p][b * 4 + 1];
+        v2 += R.pa[p][b * 4 + 2];
       } else {
         v0 += R.pa[p][b * 4];
         v1 += R.pb[p][b * 4];
@@ -3756,7 +3762,7 @@ bool cg2p_fused(const Op2DDev& op) {
   }();
   return on && (op.p1 == 8 || (op.p1 == 4 && op.fused_sub2 != 0));
 }
-size_t cg2p_ws_doubles(const Op2DDev& op, int G) { return 7 * (size_t)op.n + 2 * (size_t)op.nn + 8 * (size_t)G; }
+size_t cg2p_ws_doubles(const Op2DDev& op, int G) { return 7 * (size_t)op.n + 2 * (size_t)op.nn + 16 * (size_t)G; }   // partA partB | setup slots 2, 3
 size_t cg2p_part_off(const Op2DDev& op) { return (cg2p_fused(op) ? 7 : 6) * (size_t)op.n + 2 * (size_t)op.nn; }
 size_t cg2p_dinv_off(const Op2DDev& op) { return (cg2p_fused(op) ? 7 : 6) * (size_t)op.n; }
 // the two u buffers of the split solve: which 0 -> U, 1 -> U2 (fused: the setup's u0 only, in S1)
@@ -3884,17 +3890,47 @@ int launch2p_fpass(Ctx* c, const Op2DDev& op, CoefDev k, double a, const double*
   if (e != cudaSuccess) return c->cuda(e, "k2_cgf single-pass launch");
   return SISDC_OK;
 }
+// the two setup passes of a fused partition solve as single passes of the fused pipeline (k2_cgf MODE 1:
+// r0 = b - A x0 -> R, partials (b,b), #nonzero -> slot 2; MODE 2: u0 = r0 dinv rebuilt on chip, w0 = A u0 -> W,
+// partials (r,u), (w,u), (r,r) -> slot 3), instead of the split kernels k2p_resid / k2p_u0 / k2p_matvec
+template <int NC, int SUB>
+static cudaError_t fsetup_launch(int mode, const Cg2Args& A, int G, cudaStream_t st) {
+  using F = Fz<NC, SUB>;
+  constexpr int smem = (int)(sizeof(double) * F::SIZE);
+  if (mode == 1) {
+    cudaFuncSetAttribute(k2_cgf<NC, SUB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k2_cgf<NC, SUB, 1><<<G, F::NW * 32, smem, st>>>(A);
+  } else {
+    cudaFuncSetAttribute(k2_cgf<NC, SUB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k2_cgf<NC, SUB, 2><<<G, F::NW * 32, smem, st>>>(A);
+  }
+  return cudaGetLastError();
+}
+int launch2p_fsetup(Ctx* c, int mode, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws,
+                    int G, const CgPScal* sc) {
+  Cg2Args A = cg2p_args(op, k, a, rhs, x, ws, G, sc, -1);
+  A.maxit = c->maxit;
+  cudaError_t e = cudaSuccess;
+  if (op.p1 == 4) e = op.nc == 4 ? fsetup_launch<4, 2>(mode, A, G, c->stream) : fsetup_launch<1, 2>(mode, A, G, c->stream);
+  else e = op.nc == 4 ? fsetup_launch<4, 1>(mode, A, G, c->stream) : fsetup_launch<1, 1>(mode, A, G, c->stream);
+  ++c->launches;
+  if (e != cudaSuccess) return c->cuda(e, "k2_cgf setup-pass launch");
+  return SISDC_OK;
+}
 // bands of the fused pass on a partition (8 element rows each; P = 3: 8 rows of 2 x 2-element tiles)
 int cg2p_bands(const Op2DDev& op) { return ((op.p1 == 4 ? op.ney / 2 : op.ney) + Fz<4>::NW - 1) / Fz<4>::NW; }
 
-int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out) {
+// mode 0: (b,b), #nonzero from partB (fsetup: from the fused setup pass's slot 2); mode 1: the iteration's
+// partA / partB; mode 2: (r,u), (w,u), (r,r) from the fused setup pass's slot 3
+int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out,
+                    int fsetup) {
   if (nparts < 1 || nparts > MAXPART) return c->fail(SISDC_ERR_ARG, "partition count");
   RedPArgs R{};
   R.nparts = nparts; R.G = G; R.mode = mode; R.out = out;
   for (int p = 0; p < nparts; ++p) {
     const double* base = ws[p] + cg2p_part_off(ops[p]);
-    R.pa[p] = base;
-    R.pb[p] = base + 4 * G;
+    R.pa[p] = mode == 2 ? base + 12 * G : base;
+    R.pb[p] = (mode == 0 && fsetup) ? base + 8 * G : base + 4 * G;
   }
   k2p_reduce<<<1, 256, 0, c->stream>>>(R);
   return c->after_launch("k2p_reduce");

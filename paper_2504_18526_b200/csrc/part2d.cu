@@ -261,7 +261,7 @@ int part2_stage(sisdc_op1d* op, const double* base, const double* conv_in, doubl
 
 namespace {
 // sums of the local partitions (fixed order) -> allreduced sums at d_red + 4
-int reduce_all(sisdc_op1d* op, int mode) {
+int reduce_all(sisdc_op1d* op, int mode, int fsetup = 0) {
   Ctx* c = C(op);
   const int np = (int)op->parts.size();
   Op2DDev ops[MAXPART];
@@ -270,8 +270,8 @@ int reduce_all(sisdc_op1d* op, int mode) {
     ops[p] = op->parts[p].dev;
     ws[p] = op->parts[p].ws;
   }
-  if (!op->comm) return launch2p_reduce(c, np, ws, ops, op->parts[0].G, mode, op->d_red + 4);
-  if (int rc = launch2p_reduce(c, np, ws, ops, op->parts[0].G, mode, op->d_red)) return rc;
+  if (!op->comm) return launch2p_reduce(c, np, ws, ops, op->parts[0].G, mode, op->d_red + 4, fsetup);
+  if (int rc = launch2p_reduce(c, np, ws, ops, op->parts[0].G, mode, op->d_red, fsetup)) return rc;
   NcclApi* api = nccl();
   if (!api) return c->fail(SISDC_ERR_UNSUPPORTED, "NCCL is not available in this process");
   const ncclResult_t r = api->allReduce(op->d_red, op->d_red + 4, 3, ncclDouble, ncclSum, op->comm->comm, c->stream);
@@ -309,7 +309,7 @@ int halo_u(sisdc_op1d* op, int which) {
 // ghost rows of CG workspace vectors of every local partition: the (r, s, w) triple of parity par
 // (three consecutive state-sized vectors: one halo call) or, dinv = true, the Jacobi reciprocal (one
 // field).  Partitions differ in size, so bases and strides are per partition (mstride -1).
-int halo_ws(sisdc_op1d* op, bool dinv, int par) {
+int halo_ws(sisdc_op1d* op, bool dinv, int par, int nvec = 3) {
   Ctx* c = C(op);
   const int np = (int)op->parts.size();
   auto vec = [&](const Part2D& P) { return dinv ? P.ws + cg2p_dinv_off(P.dev) : cg2p_RSW(P.dev, P.ws, par); };
@@ -320,10 +320,10 @@ int halo_ws(sisdc_op1d* op, bool dinv, int par) {
       ops[p] = op->parts[p].dev;
       base[p] = vec(op->parts[p]);
     }
-    return launch2p_halo(c, np, ops, base, dinv ? 1 : ops[0].nc, dinv ? 1 : 3, -1);
+    return launch2p_halo(c, np, ops, base, dinv ? 1 : ops[0].nc, dinv ? 1 : nvec, -1);
   }
   const Part2D& P = op->parts[0];   // one local partition: halo() adds P.off / P.offc back
-  return halo(op, vec(P) - (dinv ? P.offc : P.off), dinv ? 1 : 3, P.dev.n, dinv);
+  return halo(op, vec(P) - (dinv ? P.offc : P.off), dinv ? 1 : nvec, P.dev.n, dinv);
 }
 
 // fused iteration j (P = 7): the (r, s, w) of parity j & 1 get their ghost rows, then ONE pass per
@@ -418,14 +418,30 @@ int part2_solve(sisdc_op1d* op, CoefDev k, double a, const double* rhs, double* 
   if (int rc = phase_all(op, P2_DINV, k, a, rhs, x)) return rc;
   if (cg2p_fused(op->parts[0].dev))   // the fused pass rebuilds the neighbour rows' u = r dinv: dinv ghost rows, once
     if (int rc = halo_ws(op, true, 0)) return rc;
-  if (int rc = phase_all(op, P2_RESID, k, a, rhs, x)) return rc;
-  if (int rc = reduce_all(op, 0)) return rc;
-  if (int rc = launch2p_scalar(c, 0, op->d_red + 4, op->d_sc)) return rc;
-  if (int rc = phase_all(op, P2_U0, k, a, rhs, x)) return rc;
-  if (int rc = halo_u(op, 0)) return rc;
-  if (int rc = phase_all(op, P2_MATVEC, k, a, rhs, x)) return rc;
-  if (int rc = reduce_all(op, 1)) return rc;
-  if (int rc = launch2p_scalar(c, 1, op->d_red + 4, op->d_sc)) return rc;
+  // fused levels: the two setup matvecs as single passes of the fused pipeline (k2_cgf MODE 1 / 2; u0 = r0 dinv
+  // is rebuilt on chip, so only r0's ghost rows travel); SISDC_PART_FSETUP=0 keeps the split kernels (A/B)
+  const char* fsv = getenv("SISDC_PART_FSETUP");
+  const bool fsetup = cg2p_fused(op->parts[0].dev) && !(fsv && fsv[0] == '0');
+  if (fsetup) {
+    for (const Part2D& P : op->parts)
+      if (int rc = launch2p_fsetup(c, 1, P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc)) return rc;
+    if (int rc = reduce_all(op, 0, 1)) return rc;
+    if (int rc = launch2p_scalar(c, 0, op->d_red + 4, op->d_sc)) return rc;
+    if (int rc = halo_ws(op, false, 0, 1)) return rc;   // r0
+    for (const Part2D& P : op->parts)
+      if (int rc = launch2p_fsetup(c, 2, P.dev, coef_part(k, P), a, rhs + P.off, x + P.off, P.ws, P.G, op->d_sc)) return rc;
+    if (int rc = reduce_all(op, 2)) return rc;
+    if (int rc = launch2p_scalar(c, 1, op->d_red + 4, op->d_sc)) return rc;
+  } else {
+    if (int rc = phase_all(op, P2_RESID, k, a, rhs, x)) return rc;
+    if (int rc = reduce_all(op, 0)) return rc;
+    if (int rc = launch2p_scalar(c, 0, op->d_red + 4, op->d_sc)) return rc;
+    if (int rc = phase_all(op, P2_U0, k, a, rhs, x)) return rc;
+    if (int rc = halo_u(op, 0)) return rc;
+    if (int rc = phase_all(op, P2_MATVEC, k, a, rhs, x)) return rc;
+    if (int rc = reduce_all(op, 1)) return rc;
+    if (int rc = launch2p_scalar(c, 1, op->d_red + 4, op->d_sc)) return rc;
+  }
   if (capturing) {
     // inside a CUDA-graph capture the host cannot poll: a fixed number of iterations is recorded (kernels
     // after convergence return at once: device-side convergence), and the closing scalar kernel latches a

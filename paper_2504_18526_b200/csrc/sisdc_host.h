@@ -134,7 +134,10 @@ double* cg2p_U(const Op2DDev& op, double* ws, int which);
 int cg2p_blocks(Ctx* c, const Op2DDev& op, int* G);
 int launch2p_phase(Ctx* c, int phase, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x,
                    double* ws, int G, const CgPScal* sc, int ucur);
-int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out);
+int launch2p_reduce(Ctx* c, int nparts, double* const* ws, const Op2DDev* ops, int G, int mode, double* out,
+                    int fsetup = 0);
+int launch2p_fsetup(Ctx* c, int mode, const Op2DDev& op, CoefDev k, double a, const double* rhs, double* x, double* ws,
+                    int G, const CgPScal* sc);
 int launch2p_scalar(Ctx* c, int mode, const double* tot, CgPScal* sc);
 int launch2p_halo_pack(Ctx* c, const Op2DDev& op, double* vec, double* buf, int nc, int mcount, long long mstride,
                        int dir);
