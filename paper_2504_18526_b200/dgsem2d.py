@@ -263,6 +263,7 @@ class NcclComm:
             self.rt.check(self.lib.sisdc_nccl_unique_id(uid), "nccl_unique_id")
             return bytes(uid.raw)
 
+        self.group = group   # the torch.distributed group the ranks also agree failures over
         uid = bootstrap_id(rank, nranks, make_id, group)
         h = C.c_void_p()
         self.rt.check(self.lib.sisdc_comm_create(self.rt.h, uid, nranks, rank, C.byref(h)), "comm_create")

@@ -320,7 +320,7 @@ def integrate_mlsdc(hier: Hierarchy, u0_fine, t0: float, dt: float, n_steps: int
         rt.reset_status()
         for _ in range(n_steps):
             g.step()
-        rt.raise_on_failure()
+        _raise_on_failure(hier)
         return g.u
     u = rt.to_device(u0_fine)
     t = t0
@@ -328,8 +328,21 @@ def integrate_mlsdc(hier: Hierarchy, u0_fine, t0: float, dt: float, n_steps: int
         sol = run_mlsdc(hier, u, t, dt, n_cycles, strategy=strategy, c_fmg=c_fmg)
         u = sol.end_value.clone()
         t += dt
-    rt.raise_on_failure()
+    _raise_on_failure(hier)
     return u
+
+
+def _raise_on_failure(hier) -> None:
+    """Latched device failures -> SolverError; a run partitioned over several ranks agrees on the
+    flags first (dgsem2d.raise_on_failure_all), so every rank raises instead of one rank leaving
+    the others inside a collective."""
+    ctx = hier.fine.ctx
+    comm = getattr(getattr(ctx, "partition", None), "comm", None)
+    if comm is not None and comm.nranks > 1:
+        from .dgsem2d import raise_on_failure_all
+        raise_on_failure_all(ctx.rt, comm.group)
+    else:
+        ctx.rt.raise_on_failure()
 
 
 def build_p_hierarchy(make_op, degrees, node_counts, scheme: str = "si2", nodes: str = "radau_right",
