@@ -11,7 +11,7 @@ from conftest import gpu_available
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
-from paper_2504_18526_b200.configs import CFG4, CFG5  # noqa: E402
+from paper_2504_18526_b200.configs import CFG3, CFG4, CFG5  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -127,3 +127,27 @@ def test_cfg5_full_size_conservation_and_partition(rt):
     got = part.gather(part.eval_rhs(part.scatter(u0))).reshape(-1)
     assert np.array_equal(got, ref)
     rt.raise_on_failure()
+
+
+@pytest.mark.parametrize("w", [CFG3, CFG4], ids=["cfg3", "cfg4"])
+def test_full_size_step_conserves_the_field_integrals(rt, w):
+    """One SI-MLSDC step at the full size of BASELINE configs[2] (Euler vortex, 128^2) and configs[3]
+    (NS shear layer, 256^2): every operator of the sweep is conservative on the periodic mesh
+    (convection, viscous / SI diffusion inside the implicit solve, FAS-corrected transfers), so the
+    integrals of rho, rho u, rho v, rho E are those of the initial state."""
+    import torch
+    from paper_2504_18526_b200 import dgsem, mlsdc
+    h = mlsdc.build_p_hierarchy(lambda P: _op(w, P), [w.p_coarse, w.p_fine], [w.m_coarse, w.m_fine])
+    fine = h.fine.ctx
+    X, Y = fine.mesh.nodes_xy
+    u0 = rt.to_device(w.initial_state(X, Y))
+    dt = w.time_step(u0.cpu().numpy(), dgsem.compute_delta(w.p_fine))
+    m = _mass(fine, torch)
+    i0 = (fine.as_nodes(u0) * m).sum(dim=(1, 2, 3, 4))
+    sol = mlsdc.run_mlsdc(h, u0, 0.0, dt, w.n_cycles, strategy="fmg")
+    rt.raise_on_failure()
+    u1 = sol.u[-1]
+    assert float((u1 - u0).abs().max()) > 0.0
+    i1 = (fine.as_nodes(u1) * m).sum(dim=(1, 2, 3, 4))
+    scale = (fine.as_nodes(u0).abs() * m).sum(dim=(1, 2, 3, 4)).max()
+    assert float((i1 - i0).abs().max() / scale) < 1e-12
