@@ -195,7 +195,8 @@ int  sisdc_stage_solve(sisdc_op1d* op, sisdc_coef k, double a, const double* bas
 /* Node caches f, h1, h2 for nodes m_first..m_first+m_count-1 (sdc.py:77-119):
  * f = eval_rhs(u_m); h1 = dt_m (conv(u_{m-1}) + D[C_m] u_m);
  * h2 = dt_m (conv(u_m) + D[C_m] u_m) with C_m the scheme's coefficient frozen
- * at u_{m-1}.  conv_prev (nullable, only with m_count == 1) reuses conv(u_{m-1}).
+ * at u_{m-1}.  conv_prev (nullable): m_count vectors with the node stride, conv_prev[j] = conv(u_{m_first+j-1})
+ * as the stage kernels left it (one batched launch per sweep instead of one per node).
  * dts = the M substep sizes (host).  h2 may be NULL (euler/si1). */
 int  sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_count,
                        const double* u0, const double* u, const double* conv_prev,

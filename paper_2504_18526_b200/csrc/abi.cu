@@ -644,7 +644,6 @@ int sisdc_node_caches(sisdc_op1d* op, int scheme, int M, int m_first, int m_coun
                       double* f, double* h1, double* h2) {
   if (!op || !u0 || !u || !dts || !f || !h1) return SISDC_ERR_ARG;
   if (scheme < SISDC_EULER || scheme > SISDC_SI2) return C(op)->fail(SISDC_ERR_ARG, "unknown scheme");
-  if (conv_prev && m_count != 1) return C(op)->fail(SISDC_ERR_ARG, "conv_prev needs m_count == 1");
   if (op->parted()) return part2_eval_nodes(op, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);
   if (op->dim == 2)
     return launch2_node_eval(C(op), op->dev2, 1, scheme, M, m_first, m_count, u0, u, conv_prev, dts, f, h1, h2);

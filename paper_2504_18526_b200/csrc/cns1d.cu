@@ -261,7 +261,7 @@ __global__ void kc_coef(Op1DDev op, CoefDev k, double* __restrict__ out) {
 struct CnsCacheArgs {
   const double* u0;
   const double* u;          // (M, 3n)
-  const double* conv_prev;  // nullable (single node)
+  const double* conv_prev;  // nullable: m_count vectors, conv(u_{m-1}) of every evaluated node
   int scheme, m_first, mode;
   W16c dts;
   double* f;
@@ -342,7 +342,7 @@ __global__ void kc_eval(Op1DDev op_in, CnsCacheArgs a) {
   }
   if (a.conv_prev) {
     if (own)
-      for (int c = 0; c < 3; ++c) cp[c] = a.conv_prev[c * op.n + gi];
+      for (int c = 0; c < 3; ++c) cp[c] = a.conv_prev[(size_t)(m - a.m_first) * 3 * op.n + c * op.n + gi];
   } else {
     __syncthreads();
     cns_flux_tile(opp, ft, fpt, T);

@@ -58,7 +58,7 @@ __global__ void k_coef_field(Op1DDev op, CoefDev c, double* __restrict__ out) {
 struct CacheArgs {
   const double* u0;
   const double* u;          // (M, N)
-  const double* conv_prev;  // nullable (single node)
+  const double* conv_prev;  // nullable: m_count vectors, conv(u_{m-1}) of every evaluated node
   int scheme, m_first, mode;
   W16 dts;
   W16 gl, gr, glp, grp;     // Dirichlet outside states at t_m and t_{m-1} per node
@@ -127,7 +127,8 @@ __global__ void k_node_eval(Op1DDev op_in, CacheArgs a) {
   __syncthreads();
   if (!own) return;
   double d = -sip_B_node<DIR>(op, st, ut, ct, qt, el, i, ebase + el) * st[TabOff::minv(p1) + i];
-  double cp = a.conv_prev ? a.conv_prev[gi] : conv_node(opp, st, pt, el, i);
+  // conv_prev: one cached conv(u_{m-1}) vector per evaluated node (node stride N)
+  double cp = a.conv_prev ? a.conv_prev[(size_t)(m - a.m_first) * N + gi] : conv_node(opp, st, pt, el, i);
   a.h1[(size_t)m * N + gi] = dtm * (cp + d);
   if (a.h2) a.h2[(size_t)m * N + gi] = dtm * (cm + d);
 }

@@ -340,7 +340,8 @@ __global__ void __launch_bounds__(256, 3) k2_node_eval(Op2DDev op, Cache2Args a)
   if (a.conv_prev) {
     if (n.valid)
 #pragma unroll
-      for (int c = 0; c < NC_MAX && c < op.nc; ++c) cp[c] = a.conv_prev[nidx(op, c, n.ey, n.ex, n.j, n.i)];
+      for (int c = 0; c < NC_MAX && c < op.nc; ++c)   // one cached vector per evaluated node (node stride op.ns)
+        cp[c] = a.conv_prev[(size_t)(m - a.m_first) * op.ns + nidx(op, c, n.ey, n.ex, n.j, n.i)];
   } else {
     conv_block<P1>(op, sm, up, n, cp);
   }
@@ -1472,7 +1473,8 @@ __global__ void __launch_bounds__(EV_WARPS * 32) k2_eval8(Op2DDev op, Cache2Args
       cp_async8(ws + W::NBR + (FB * NC + c) * 64 + tr1, uc + nb[FB] + 32 + lane);
       if (need_si || conv_up) cp_async16(ws + W::UPO + c * W::NP + r * RP + cc, up + c * nn + eo + 2 * lane);
       // the cached conv(u_{m-1}) rides with the staging (read in the field loop it stalled 19% of the samples)
-      if (need_h && a.conv_prev) cp_async16(ws + W::CPV + c * W::NP + r * RP + cc, a.conv_prev + c * nn + eo + 2 * lane);
+      if (need_h && a.conv_prev)
+        cp_async16(ws + W::CPV + c * W::NP + r * RP + cc, a.conv_prev + (size_t)(m - a.m_first) * op.ns + c * nn + eo + 2 * lane);
     }
     double upf[NC_MAX];   // u_{m-1} at this lane's neighbour face node
     const unsigned nbf = (f == FR ? nb[FR] : f == FL ? nb[FL] : f == FT ? nb[FT] : nb[FB]) + fnode;

@@ -144,10 +144,13 @@ def _stage_solve(ctx, coef: Coef, a, base, conv_in, dt_m, f_old, w_row, dt, g_m,
         out.data_ptr()), "stage_solve")
 
 
-def _substep(ctx, scheme, up, dtm, f_old, w_row, dt, g_m, h1_old, h2_old, out, t_prev=0.0, t_m=0.0):
+def _substep(ctx, scheme, up, dtm, f_old, w_row, dt, g_m, h1_old, h2_old, out, t_prev=0.0, t_m=0.0, conv_out=None):
     """One SI substep into ``out`` (predictor when f_old/h are None):
-    conv(u_{m-1}) at t_{m-1}, the solves and conv(stage) at t_m (sdc.py:225-237)."""
+    conv(u_{m-1}) at t_{m-1}, the solves and conv(stage) at t_m (sdc.py:225-237).
+    ``conv_out``: where conv(u_{m-1}) is left (default: the operator's scratch)."""
     s = ctx.scratch()
+    if conv_out is not None:
+        s = dict(s, conv=conv_out)
     c = _coef(ctx, scheme, up, dtm)
     if scheme in ("euler", "si1"):
         _stage_solve(ctx, c, dtm, up, up, dtm, f_old, w_row, dt, g_m, h1_old, t_prev, t_m, s["rhs"], s["conv"], out)
@@ -158,6 +161,24 @@ def _substep(ctx, scheme, up, dtm, f_old, w_row, dt, g_m, h1_old, h2_old, out, t
     else:
         raise ValueError(f"unknown scheme {scheme!r}")
     return s["conv"]
+
+
+def _batched_caches(ctx, M, dts) -> bool:
+    """Node caches of a whole sweep in ONE launch: the new f / h1 / h2 feed the NEXT sweep only (the
+    stages of this sweep read the old iterate's caches), so they can be evaluated after the last node
+    from the per-node conv(u_{m-1}) vectors the stage kernels leave behind -- the same kernel and the
+    same operands as M single-node launches, bitwise.  1-D levels (launch-latency bound: 2 x (M - 1)
+    launches fewer per sweep); 2-D levels fill the GPU per node and keep one scratch vector."""
+    return (not getattr(ctx, "is2d", False)) and M > 1 and all(d != 0.0 for d in dts) \
+        and getattr(ctx, "source_fn", None) is None
+
+
+def _conv_all(ctx, M):
+    buf = getattr(ctx, "_conv_all", None)
+    if buf is None or buf.shape[0] != M:
+        buf = _rt(ctx).empty(M, ctx.ndof)
+        ctx._conv_all = buf
+    return buf
 
 
 @traced("sisdc.predict")
@@ -171,6 +192,8 @@ def predict(ctx, rule, dt, scheme, u0, t0, out: Optional[NodalSolution] = None) 
     dts = _dts(rule, dt)
     times = _node_times(rule, dt, t0)
     _register_times(ctx, t0, times)
+    batched = _batched_caches(ctx, rule.M, dts)
+    convs = _conv_all(ctx, rule.M) if batched else None
     for m in range(rule.M):
         up = sol.u0 if m == 0 else sol.u[m - 1]
         t_prev = t0 if m == 0 else times[m - 1]
@@ -178,8 +201,12 @@ def predict(ctx, rule, dt, scheme, u0, t0, out: Optional[NodalSolution] = None) 
             _rt(ctx).copy(sol.u[m], up)
             _caches(ctx, scheme, sol, rule.M, m, 1, dts, times=times)
             continue
-        conv = _substep(ctx, scheme, up, dts[m], None, None, 0.0, None, None, None, sol.u[m], t_prev, times[m])
-        _caches(ctx, scheme, sol, rule.M, m, 1, dts, conv, times=times)
+        conv = _substep(ctx, scheme, up, dts[m], None, None, 0.0, None, None, None, sol.u[m], t_prev, times[m],
+                        conv_out=convs[m] if batched else None)
+        if not batched:
+            _caches(ctx, scheme, sol, rule.M, m, 1, dts, conv, times=times)
+    if batched:
+        _caches(ctx, scheme, sol, rule.M, 0, rule.M, dts, convs, times=times)
     return sol
 
 
@@ -216,6 +243,8 @@ def sweep(ctx, rule: CollocationRule, weights: QuadratureWeights, dt: float, sch
     dts = _dts(rule, dt)
     times = _node_times(rule, dt, new.t0)
     _register_times(ctx, new.t0, times)
+    batched = _batched_caches(ctx, rule.M, dts) and new is not sol
+    convs = _conv_all(ctx, rule.M) if batched else None
     for m in range(rule.M):
         up = new.u0 if m == 0 else new.u[m - 1]
         t_prev = new.t0 if m == 0 else times[m - 1]
@@ -225,8 +254,12 @@ def sweep(ctx, rule: CollocationRule, weights: QuadratureWeights, dt: float, sch
             _caches(ctx, scheme, new, rule.M, m, 1, dts, times=times)
             continue
         conv = _substep(ctx, scheme, up, dts[m], sol.f, weights.w_nn[m], dt, gm, sol.h1[m],
-                        None if sol.h2 is None else sol.h2[m], new.u[m], t_prev, times[m])
-        _caches(ctx, scheme, new, rule.M, m, 1, dts, conv, times=times)
+                        None if sol.h2 is None else sol.h2[m], new.u[m], t_prev, times[m],
+                        conv_out=convs[m] if batched else None)
+        if not batched:
+            _caches(ctx, scheme, new, rule.M, m, 1, dts, conv, times=times)
+    if batched:   # one launch: f, h1, h2 of all M nodes from the per-node conv(u_{m-1}) vectors
+        _caches(ctx, scheme, new, rule.M, 0, rule.M, dts, convs, times=times)
     return new
 
 
