@@ -46,6 +46,9 @@ class Level:
         if not self._bufs:
             n = self.ctx.ndof
             self._bufs = [_alloc(self.ctx, self.ctx.rt.zeros(n), self.rule.M, self.scheme, 0.0) for _ in range(2)]
+            # the slab start is the same for every iterate of the level: one shared u0 vector, so a sweep
+            # into the other buffer does not copy it (one launch fewer per sweep)
+            self._bufs[1].u0 = self._bufs[0].u0
         b = self._bufs[0] if self._bufs[0] is not self.sol else self._bufs[1]
         b.t0 = self.t0
         return b

@@ -238,7 +238,8 @@ def sweep(ctx, rule: CollocationRule, weights: QuadratureWeights, dt: float, sch
     rt.bind_stream()
     new = out if out is not None else _alloc(ctx, sol.u0, rule.M, scheme, sol.t0)
     if out is not None:
-        rt.copy(new.u0, sol.u0)
+        if new.u0.data_ptr() != sol.u0.data_ptr():   # a level's buffers share one u0 (mlsdc.Level.next_buffer)
+            rt.copy(new.u0, sol.u0)
         new.t0 = sol.t0
     dts = _dts(rule, dt)
     times = _node_times(rule, dt, new.t0)
@@ -274,7 +275,8 @@ def _sweep_nonincremental(ctx, rule, weights, dt, scheme, sol, g, out=None):
     rt.bind_stream()
     new = out if out is not None else _alloc(ctx, sol.u0, rule.M, scheme, sol.t0)
     if out is not None:
-        rt.copy(new.u0, sol.u0)
+        if new.u0.data_ptr() != sol.u0.data_ptr():   # a level's buffers share one u0 (mlsdc.Level.next_buffer)
+            rt.copy(new.u0, sol.u0)
         new.t0 = sol.t0
     dts = _dts(rule, dt)
     times = _node_times(rule, dt, new.t0)
